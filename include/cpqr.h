@@ -1,0 +1,174 @@
+/*
+ * cpqr.h — C ABI of libcpqr: the per-mode least-squares hot path of QR-based CP-ALS
+ * (arXiv 2112.10855, Alg. 2 "CP-ALS-QR"), its QR-SVD variant
+ * and normal-equations CP-ALS (Alg. 1), on B200 (sm_100a).
+ *
+ * Conventions (DESIGN.md §Data layout, §Readings):
+ *   - all arithmetic is IEEE fp64;
+ *   - the dense tensor X (I_1 x ... x I_N) is column-major, mode 1 fastest (PAPER.md:109,
+ *     Kolda-Bader unfolding, reading 1);
+ *   - factor matrices A_n (I_n x R) are column-major with leading dimension I_n;
+ *   - Khatri-Rao / Kronecker products use A_N (.) ... (.) A_1 (last factor's row fastest,
+ *     PAPER.md:93-95), so V_n rows and Y_(n) columns are in Kolda-Bader order;
+ *   - every thin QR returns diag(R) >= 0 (reading 6); lambda_r = ||Ahat(:,r)||_2 >= 0.
+ *
+ * Errors: every entry point returns a cpqr_status (0 = OK, > 0 = error).  No C++ exception
+ * crosses the ABI.  cpqr_last_error() gives a human-readable message for the last failure on
+ * a context.  A context is not thread-safe; distinct contexts are independent.
+ * Ownership: the context owns all device workspaces, its streams and its NCCL communicator;
+ * every pointer passed in is borrowed for the duration of the call only, except a tensor
+ * given with CPQR_MEM_DEVICE_BORROW (kept until the next cpqr_set_tensor or cpqr_destroy).
+ * Synchronisation: every call is synchronous with respect to the host on return (results
+ * written to host buffers are valid), unless stated otherwise.
+ */
+#ifndef CPQR_H
+#define CPQR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t cpqr_status;
+enum {
+  CPQR_OK = 0,
+  CPQR_EINVAL = 1,     /* bad argument (N, dims, R, variant, NULL pointer, slab range, ...) */
+  CPQR_ENOMEM = 2,     /* device allocation failed */
+  CPQR_ECUDA = 3,      /* CUDA runtime error (message in cpqr_last_error) */
+  CPQR_ENCCL = 4,      /* NCCL error or NCCL unavailable with world > 1 */
+  CPQR_ESTATE = 5,     /* call out of order (no tensor / no factors yet) */
+  CPQR_EDIVERGED = 6   /* non-finite factor produced; state left at the last finite mode */
+};
+
+/* Variant of the per-mode LS solve (substitution or SVD; Alg. 1: normal eqs). */
+typedef enum { CPQR_NE = 0, CPQR_QR = 1, CPQR_SVD = 2 } cpqr_variant;
+
+/* Fit computation: FAST uses the identity ||X-Xh||^2 = ||X||^2 - 2<X,Xh>
+ * + ||Xh||^2 with already-computed quantities; DIRECT forms the residual explicitly (one extra
+ * pass over X, used for noiseless problems, reading 19/28). */
+typedef enum { CPQR_FIT_FAST = 0, CPQR_FIT_DIRECT = 1 } cpqr_fit_mode;
+
+/* Where the tensor passed to cpqr_set_tensor lives. */
+typedef enum {
+  CPQR_MEM_HOST = 0,          /* host memory; copied to the device (pinned is faster) */
+  CPQR_MEM_DEVICE_COPY = 1,   /* device memory; copied into a context-owned buffer */
+  CPQR_MEM_DEVICE_BORROW = 2  /* device memory; used in place, caller keeps it alive */
+} cpqr_mem;
+
+/* Non-fatal condition flags (cpqr_get_flags), OR-ed over all sweeps run so far. */
+enum {
+  CPQR_FLAG_ILLCOND_R0 = 1u,      /* QR variant: min|R0_jj| <= R^(N-1)*eps*max|R0_jj| (reading 17) */
+  CPQR_FLAG_NE_CHOL_FALLBACK = 2u,/* NE: Cholesky met a non-positive pivot; LU used (reading 18) */
+  CPQR_FLAG_SVD_TRUNCATED = 4u    /* SVD variant: at least one sigma_i <= tau*sigma_max dropped */
+};
+
+typedef struct cpqr_options {
+  uint32_t struct_size;   /* = sizeof(cpqr_options); ABI versioning */
+  double svd_tau;         /* SVD truncation: keep sigma_i > svd_tau*sigma_max; < 0 -> R*eps */
+  int32_t fit_mode;       /* cpqr_fit_mode */
+  int32_t device;         /* CUDA device ordinal */
+  void* stream;           /* borrowed cudaStream_t to run on (e.g. torch's), or NULL: own stream */
+  int32_t rank, world;    /* slab data parallelism over the last mode (world = 1: single GPU) */
+  uint8_t nccl_id[128];   /* ncclUniqueId from cpqr_nccl_unique_id() on rank 0, broadcast */
+  int32_t use_graph;      /* 1: capture one sweep as a CUDA graph and replay it */
+  int32_t profile;        /* 1: record CUDA events around each phase (cpqr_get_profile) */
+} cpqr_options;
+
+/* Fills *opt with defaults: svd_tau = -1, FAST fit, device 0, own stream, world 1,
+ * use_graph 1, profile 0. */
+void cpqr_default_options(cpqr_options* opt);
+
+typedef struct cpqr_ctx cpqr_ctx;
+
+/* Create a solver for an N-way tensor of global dims[0..N-1] and CP rank R.
+ * Preconditions: N >= 2; 1 <= R <= 64; dims[k] >= R for all k (tall factors, PAPER.md:33;
+ * reading 27); with world = p > 1, the last mode is split into slabs (cpqr_set_tensor).
+ * Errors: EINVAL, ENOMEM, ECUDA, ENCCL. */
+cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
+                        const cpqr_options* opt, cpqr_ctx** out);
+
+/* Set the local tensor slab X(:, ..., :, slab_begin:slab_end) (0-based, end exclusive, on the
+ * last mode), column-major I_1 x ... x I_{N-1} x (slab_end - slab_begin) = a contiguous block
+ * of the global column-major tensor at element offset slab_begin * prod_{k<N} I_k.
+ * world = 1 requires [0, I_N).  Computes ||X||^2 (all-reduced across ranks).
+ * Errors: EINVAL (slab range / NULL), ENOMEM, ECUDA, ENCCL. */
+cpqr_status cpqr_set_tensor(cpqr_ctx* ctx, const double* x, int64_t slab_begin,
+                            int64_t slab_end, int mem);
+
+/* Set the factors: A[k] is a host pointer to the column-major I_k x R matrix A_k (k = 0..N-1;
+ * A[0] may be NULL for the QR/SVD variants: Alg. 2 line 2 initialises A_2..A_N only).
+ * lambda: host R-vector or NULL (ones).  Must be identical on all ranks.  Recomputes the factor
+ * QR cache (Alg. 2 line 3) or the Gram matrices (Alg. 1 line 3).  Errors: EINVAL. */
+cpqr_status cpqr_set_factors(cpqr_ctx* ctx, const double* const* A, const double* lambda);
+
+/* Initialise the factors with i.i.d. N(0,1) entries from a counter-based generator
+ * (splitmix64 + Box-Muller, seed-determined, identical on every rank), lambda = 1. */
+cpqr_status cpqr_init_factors(cpqr_ctx* ctx, uint64_t seed);
+
+/* Run exactly nsweeps sweeps over modes 1..N (Alg. 2 lines 4-13 / Alg. 1 lines 4-12); no early
+ * stop (convergence is the caller's policy).  If fits != NULL, fits[s] = fit
+ * after sweep s (computed after mode N).  Synchronous.
+ * Errors: ESTATE (no tensor/factors), EDIVERGED, ENCCL, ECUDA. */
+cpqr_status cpqr_sweep(cpqr_ctx* ctx, int nsweeps, double* fits);
+
+/* Current normalised factors (unit 2-norm columns) into host buffers A_out[k] (column-major
+ * I_k x R, NULL entries skipped) and lambda (R, may be NULL).  Identical on all ranks. */
+cpqr_status cpqr_get_factors(cpqr_ctx* ctx, double* const* A_out, double* lambda_out);
+
+cpqr_status cpqr_get_fit(cpqr_ctx* ctx, double* fit);      /* fit after the last sweep */
+cpqr_status cpqr_get_flags(cpqr_ctx* ctx, uint32_t* flags);
+
+/* Per-phase device time (ms) accumulated since the last reset, Table 3.1 taxonomy
+ * (PAPER.md:495-510), only with opt.profile = 1:
+ *   ms[0] Multi-TTM stream-X pass (the dominant kernel)   ms[1] Multi-TTM remaining TTMs
+ *   ms[2] factor QR        ms[3] computing Q0 (QR of V_n)  ms[4] applying Q0
+ *   ms[5] other (solve, normalise, fit)
+ * launches[0..5]: kernel launches per phase; bytes0/flops0: algorithmic HBM bytes and flops of
+ * phase 0.  reset != 0 zeroes the counters after reading. */
+typedef struct cpqr_profile {
+  double ms[6];
+  int64_t launches[6];
+  double bytes0, flops0;
+  int64_t launches_total;
+} cpqr_profile;
+cpqr_status cpqr_get_profile(cpqr_ctx* ctx, cpqr_profile* prof, int reset);
+
+/* Kernel launches issued by one cpqr_sweep(ctx, 1, ...) (claims for bench "gpu_launches"). */
+cpqr_status cpqr_launches_per_sweep(cpqr_ctx* ctx, int64_t* n);
+
+/* Parity hook: for mode n (0-based) compute Alg. 2 lines 6-9 (V_n, Q0/R0, Multi-TTM Y, W_n)
+ * from the current factor QR cache, or from Q_override[k] (host, column-major I_k x R, k != n)
+ * if Q_override != NULL (R_k from the cache still define V_n), WITHOUT changing state.
+ * Outputs (host, any may be NULL):
+ *   Y_out : the Multi-TTM result tensor Y = X x_{k!=n} Q_k^T (dims R..I_n..R, column-major;
+ *           its mode-n unfolding is Y_(n) in Kolda-Bader order).  With world > 1 each rank's
+ *           partial Y is summed across ranks (debug only).
+ *   Q0_out: R^{N-1} x R column-major, rows in Kolda-Bader order;  R0_out: R x R column-major;
+ *   W_out : I_n x R column-major (global rows). */
+cpqr_status cpqr_debug_mode(cpqr_ctx* ctx, int n, const double* const* Q_override,
+                            double* Y_out, double* Q0_out, double* R0_out, double* W_out);
+
+/* Stand-alone kernels exposed for parity tests (host in/out, column-major):
+ * thin Householder QR of an m x R matrix (m >= R): Q (m x R), Rf (R x R), diag(Rf) >= 0. */
+cpqr_status cpqr_debug_qr(cpqr_ctx* ctx, const double* A, int64_t m, double* Q, double* Rf);
+/* One-sided Jacobi SVD pseudo-inverse solve: Ahat = W U S^+ V^T for R0 = U S V^T
+ * (PAPER.md:335-339), W m x R; returns the number of truncated singular values in *ntrunc. */
+cpqr_status cpqr_debug_svd_solve(cpqr_ctx* ctx, const double* R0, const double* W, int64_t m,
+                                 double tau, double* Ahat, int* ntrunc);
+
+cpqr_status cpqr_destroy(cpqr_ctx* ctx);
+const char* cpqr_status_string(cpqr_status s);
+const char* cpqr_last_error(const cpqr_ctx* ctx);
+
+/* NCCL bootstrap: rank 0 calls this, broadcasts the 128 bytes (e.g. over torch.distributed),
+ * every rank passes them in cpqr_options.nccl_id.  Returns ENCCL if NCCL is unavailable. */
+cpqr_status cpqr_nccl_unique_id(uint8_t id[128]);
+
+/* Library version string ("cpqr <semver> sm_100a"). */
+const char* cpqr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPQR_H */

@@ -1,0 +1,357 @@
+"""Plain, slow, obviously-correct fp64 oracle for the CP-ALS-QR hot path.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): never imported by the product path.
+
+Conventions:
+  * tensors are numpy arrays of shape (I_1, ..., I_N) in Fortran (column-major) order,
+    mode 1 fastest -- the bytes of the C-order (I_N, ..., I_1) buffer that synth.py makes;
+  * modes are 0-based in code (paper mode n == code mode n-1);
+  * Kronecker / Khatri-Rao follow PAPER.md:93-95 (second operand's index fastest), so
+    Z_n = A_N (.) ... (.) A_1 has A_1's row index fastest (reading 1, Kolda-Bader);
+  * every thin QR returns diag(R) >= 0 (reading 6);
+  * fp64 throughout.
+
+Pinned by tests/test_oracle_pins.py (closed forms, worked examples, brute force,
+library routines, invariants).  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg
+
+EPS = np.finfo(np.float64).eps
+
+FLAG_ILLCOND_R0 = 1
+FLAG_NE_CHOL_FALLBACK = 2
+FLAG_SVD_TRUNCATED = 4
+
+__all__ = [
+    "EPS", "FLAG_ILLCOND_R0", "FLAG_NE_CHOL_FALLBACK", "FLAG_SVD_TRUNCATED",
+    "as_tensor", "kron", "khatri_rao", "hadamard", "matricize", "tensorize", "ttm",
+    "multi_ttm", "ttm_order", "qr_pos", "kr_of_triangular", "structured_qr", "apply_q0",
+    "solve_qr", "solve_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
+    "fit_direct", "mode_update_qr", "mode_update_ne", "cp_als_qr", "cp_als_ne",
+    "qr_cost", "ttm_cost", "mttkrp",
+]
+
+
+# ----------------------------------------------------------------------------- layout
+def as_tensor(Xc: np.ndarray) -> np.ndarray:
+    """C-order (I_N..I_1) buffer -> Fortran (I_1..I_N) view of the same bytes."""
+    return Xc.T
+
+
+# ------------------------------------------------------------------ matrix products §2.2
+def kron(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """Kronecker product: [A (x) B](K(i-1)+k, M(j-1)+l) = A(i,j) B(k,l)."""
+    I, J = A.shape
+    K, M = B.shape
+    return (A[:, None, :, None] * B[None, :, None, :]).reshape(I * K, J * M)
+
+
+def khatri_rao(mats) -> np.ndarray:
+    """Khatri-Rao product: column k is A(:,k) (x) B(:,k); applied left to right,
+    so the LAST matrix's row index is fastest."""
+    out = mats[0]
+    for B in mats[1:]:
+        I, R = out.shape
+        J, R2 = B.shape
+        assert R == R2
+        out = (out[:, None, :] * B[None, :, :]).reshape(I * J, R)
+    return out
+
+
+def hadamard(A, B):
+    """Elementwise product."""
+    return A * B
+
+
+# ------------------------------------------------------------- tensor operations §2.2
+def matricize(X: np.ndarray, n: int) -> np.ndarray:
+    """Mode-n unfolding X_(n): columns are mode-n fibers, in Kolda-Bader order
+    (reading 1): element (i_1..i_N) -> row i_n, column sum_{k!=n} i_k J_k, J_k = prod_{m<k,m!=n} I_m."""
+    return np.reshape(np.moveaxis(X, n, 0), (X.shape[n], -1), order="F")
+
+
+def tensorize(M: np.ndarray, dims, n: int) -> np.ndarray:
+    """Inverse of matricize (fold back)."""
+    dims = tuple(dims)
+    rest = dims[:n] + dims[n + 1:]
+    T = np.reshape(M, (dims[n],) + rest, order="F")
+    return np.moveaxis(T, 0, n)
+
+
+def ttm(X: np.ndarray, U: np.ndarray, n: int) -> np.ndarray:
+    """n-mode product Y = X x_n U:
+    Y(i_1..j..i_N) = sum_{i_n} X(i_1..i_n..i_N) U(j, i_n), i.e. Y_(n) = U X_(n).
+
+    Written on the 3-index view X3(a, i_n, b) (a over modes < n, fastest; b over modes > n)
+    of the same column-major bytes: Y3(a, j, b) = sum_i U(j, i) X3(a, i, b)."""
+    dims = X.shape
+    A = int(np.prod(dims[:n], dtype=np.int64))
+    B = int(np.prod(dims[n + 1:], dtype=np.int64))
+    X3 = np.reshape(X, (A, dims[n], B), order="F")
+    # X3.T is the C-order (B, I_n, A) view; U @ (I_n, A) for each b.
+    Y3 = np.matmul(U, X3.T).T                       # (A, J, B), Fortran-contiguous
+    return np.reshape(Y3, dims[:n] + (U.shape[0],) + dims[n + 1:], order="F")
+
+
+def ttm_order(dims, skip: int):
+    """Order of the N-1 TTMs: decreasing tensor dimension; ties broken by
+    decreasing mode index (reading 5)."""
+    modes = [k for k in range(len(dims)) if k != skip]
+    return sorted(modes, key=lambda k: (-dims[k], -k))
+
+
+def multi_ttm(X: np.ndarray, Us: dict, order=None) -> np.ndarray:
+    """Multi-TTM Y = X x_{k} U_k over the modes in Us (Eq. (2.2)), as a
+    sequence of single TTMs, in decreasing-dimension order by default."""
+    if order is None:
+        modes = sorted(Us.keys(), key=lambda k: (-X.shape[k], -k))
+    else:
+        modes = list(order)
+    Y = X
+    for k in modes:
+        Y = ttm(Y, Us[k], k)
+    return Y
+
+
+def mttkrp(X: np.ndarray, factors, n: int) -> np.ndarray:
+    """MTTKRP M_n = X_(n) Z_n, Z_n = A_N (.) ... (.) A_{n+1} (.) A_{n-1} (.) ... (.) A_1
+    (Alg. 1 lines 7-8; Eq. (cp_mat))."""
+    N = X.ndim
+    Z = khatri_rao([factors[k] for k in range(N - 1, -1, -1) if k != n])
+    return matricize(X, n) @ Z
+
+
+# --------------------------------------------------------------------------- QR / LS
+def qr_pos(A: np.ndarray):
+    """Compact/thin QR A = QR by LAPACK Householder, then the sign fix
+    diag(R) >= 0 (reading 6; a zero diagonal keeps sign +1)."""
+    Q, R = np.linalg.qr(A, mode="reduced")
+    s = np.where(np.diag(R) < 0, -1.0, 1.0)
+    return Q * s[None, :], R * s[:, None]
+
+
+def kr_of_triangular(Rs, n: int) -> np.ndarray:
+    """V_n = R_N (.) ... (.) R_{n+1} (.) R_{n-1} (.) ... (.) R_1 (Alg. 2 line 6)."""
+    N = len(Rs)
+    return khatri_rao([Rs[k] for k in range(N - 1, -1, -1) if k != n])
+
+
+def structured_qr(Rs, n: int):
+    """Q0, R0 = QR(V_n), dense (Alg. 2 line 7; PAPER.md:314 treats V_n dense)."""
+    return qr_pos(kr_of_triangular(Rs, n))
+
+
+def apply_q0(Y: np.ndarray, n: int, Q0: np.ndarray) -> np.ndarray:
+    """W_n = Y_(n) Q0 (Alg. 2 line 9)."""
+    return matricize(Y, n) @ Q0
+
+
+def solve_qr(R0: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """Solve Ahat R0^T = W by substitution (Alg. 2 line 10; Eq. (ls-qr-q0-step)
+    PAPER.md:331).  (Ahat R0^T)(:, j) = sum_{l >= j} Ahat(:, l) R0(j, l) with R0 upper
+    triangular, so back substitution over columns j = R..1."""
+    R = R0.shape[0]
+    Ahat = np.zeros_like(W)
+    for j in range(R - 1, -1, -1):
+        acc = W[:, j].copy()
+        for l in range(j + 1, R):
+            acc -= Ahat[:, l] * R0[j, l]
+        Ahat[:, j] = acc / R0[j, j]
+    return Ahat
+
+
+def solve_svd(R0: np.ndarray, W: np.ndarray, tau: float = -1.0):
+    """CP-ALS-QR-SVD solve: R0 = U S V^T, Ahat = W U S^+ V^T, truncating
+    sigma_i <= tau * sigma_max (reading 15; tau < 0 -> R*eps).  Returns (Ahat, n_truncated)."""
+    R = R0.shape[0]
+    if tau < 0:
+        tau = R * EPS
+    U, s, Vt = np.linalg.svd(R0)
+    keep = s > tau * s[0]
+    Ahat = ((W @ U[:, keep]) / s[keep][None, :]) @ Vt[keep, :]
+    return Ahat, int(R - keep.sum())
+
+
+def normalize(Ahat: np.ndarray):
+    """Normalize columns (Alg. 2 line 11): lam_r = ||Ahat(:,r)||_2, A = Ahat/lam.
+    A zero column gives lam_r = 0 and column e_1 (reading 10)."""
+    lam = np.sqrt(np.sum(Ahat * Ahat, axis=0))
+    A = np.empty_like(Ahat)
+    for r in range(Ahat.shape[1]):
+        if lam[r] > 0:
+            A[:, r] = Ahat[:, r] / lam[r]
+        else:
+            A[:, r] = 0.0
+            A[0, r] = 1.0
+    return A, lam
+
+
+# ------------------------------------------------------------------------------ fits
+def full_tensor(lam, factors) -> np.ndarray:
+    """X_hat = sum_r lam_r a_r^(1) o ... o a_r^(N) (Eq. (cp)), built from
+    Eq. (cp_mat): X_hat_(1) = Ahat_1 Z_1^T."""
+    dims = tuple(A.shape[0] for A in factors)
+    N = len(factors)
+    Ahat1 = factors[0] * np.asarray(lam)[None, :]
+    if N == 1:
+        return Ahat1.sum(axis=1)
+    Z1 = khatri_rao([factors[k] for k in range(N - 1, 0, -1)])
+    return tensorize(Ahat1 @ Z1.T, dims, 0)
+
+
+def fit_direct(X, lam, factors) -> float:
+    """fit = 1 - ||X - X_hat||_F / ||X||_F with X_hat formed explicitly."""
+    Xh = full_tensor(lam, factors)
+    return 1.0 - np.linalg.norm((X - Xh).ravel()) / np.linalg.norm(X.ravel())
+
+
+def _fit_from_terms(nX2, inner, nXh2):
+    """||X - X_hat||^2 = ||X||^2 - 2<X,X_hat> + ||X_hat||^2; clamp (reading 14)."""
+    res = np.sqrt(max(0.0, nX2 - 2.0 * inner + nXh2))
+    return 1.0 - res / np.sqrt(nX2)
+
+
+def fit_fast_qr(nX2, W_N, Ahat_N, R0, R_N, lam) -> float:
+    """Efficient error for CP-ALS-QR:
+    <X,X_hat> = <W_N, Ahat_N R0^T>,  ||X_hat||^2 = <R0^T R0, diag(lam) R_N^T R_N diag(lam)>."""
+    inner = float(np.sum(W_N * (Ahat_N @ R0.T)))
+    D = np.diag(lam)
+    nXh2 = float(np.sum((R0.T @ R0) * (D @ R_N.T @ R_N @ D)))
+    return _fit_from_terms(nX2, inner, nXh2)
+
+
+def fit_fast_ne(nX2, M_N, Ahat_N, S_N, G_N, lam) -> float:
+    """Efficient error for CP-ALS:
+    <X,X_hat> = <M_N, Ahat_N>,  ||X_hat||^2 = <S_N, diag(lam) G_N diag(lam)>."""
+    inner = float(np.sum(M_N * Ahat_N))
+    D = np.diag(lam)
+    nXh2 = float(np.sum(S_N * (D @ G_N @ D)))
+    return _fit_from_terms(nX2, inner, nXh2)
+
+
+# ----------------------------------------------------------------------- mode updates
+def mode_update_qr(X, Qs, Rs, n, variant="QR", tau=-1.0, order=None):
+    """One CP-ALS-QR(-SVD) mode update, Alg. 2 lines 6-12, in the paper's
+    order.  Qs/Rs: factor QR cache (entry n ignored).  Returns a dict of every intermediate."""
+    N = X.ndim
+    V = kr_of_triangular(Rs, n)                                   # line 6
+    Q0, R0 = qr_pos(V)                                            # line 7
+    Y = multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n},    # line 8
+                  order=order)
+    W = apply_q0(Y, n, Q0)                                        # line 9
+    ntrunc = 0
+    if variant == "QR":                                           # line 10
+        Ahat = solve_qr(R0, W)
+    elif variant == "SVD":
+        Ahat, ntrunc = solve_svd(R0, W, tau)
+    else:
+        raise ValueError(variant)
+    A, lam = normalize(Ahat)                                      # line 11
+    Qn, Rn = qr_pos(A)                                            # line 12
+    d = np.abs(np.diag(R0))
+    # reading 17: numerically rank-deficient R0 when min|R0_jj| <= rows(V_n) * eps * max|R0_jj|
+    # (the numpy.linalg.matrix_rank default tolerance, applied to V_n's R factor)
+    flags = FLAG_ILLCOND_R0 if (variant == "QR" and d.min() <= V.shape[0] * EPS * d.max()) else 0
+    if ntrunc:
+        flags |= FLAG_SVD_TRUNCATED
+    return dict(V=V, Q0=Q0, R0=R0, Y=Y, Yn=matricize(Y, n), W=W, Ahat=Ahat, A=A, lam=lam,
+                Q=Qn, R=Rn, ntrunc=ntrunc, flags=flags)
+
+
+def mode_update_ne(X, factors, grams, n):
+    """One CP-ALS mode update, Alg. 1 lines 6-11: S_n = Hadamard of the other
+    Grams; M_n = X_(n) Z_n (MTTKRP); solve Ahat S_n = M_n by Cholesky, falling back
+    to LU with partial pivoting on a non-positive pivot (reading 18); normalize; G_n = A_n^T A_n."""
+    N = X.ndim
+    S = np.ones_like(grams[0])
+    for k in range(N - 1, -1, -1):                                # line 6
+        if k != n:
+            S = hadamard(S, grams[k])
+    M = mttkrp(X, factors, n)                                     # lines 7-8
+    flags = 0
+    try:                                                          # line 9
+        L = np.linalg.cholesky(S)
+        T = scipy.linalg.solve_triangular(L, M.T, lower=True)
+        Ahat = scipy.linalg.solve_triangular(L.T, T, lower=False).T
+    except np.linalg.LinAlgError:
+        Ahat = scipy.linalg.solve(S, M.T, assume_a="gen").T
+        flags |= FLAG_NE_CHOL_FALLBACK
+    A, lam = normalize(Ahat)                                      # line 10
+    G = A.T @ A                                                   # line 11
+    return dict(S=S, M=M, Ahat=Ahat, A=A, lam=lam, G=G, flags=flags)
+
+
+# ---------------------------------------------------------------------------- drivers
+def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_sweep1=False,
+              order=None):
+    """CP-ALS-QR / CP-ALS-QR-SVD, Alg. 2, exactly `sweeps` sweeps (no early
+    stop; reading 12).  X: Fortran (I_1..I_N) array.  A0: initial factors (A0[0] unused,
+    PAPER.md:350).  fit after mode N of every sweep (reading 13): fast or
+    direct.  Returns dict(lam, factors, fits, flags, debug)."""
+    N = X.ndim
+    nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K")))
+    factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
+    Qs, Rs = [None] * N, [None] * N
+    for k in range(1, N):                                         # line 3
+        Qs[k], Rs[k] = qr_pos(factors[k])
+    lam = np.ones(factors[0].shape[1])
+    fits, flags, debug = [], 0, []
+    for s in range(sweeps):                                       # line 4
+        last = None
+        for n in range(N):                                        # line 5
+            u = mode_update_qr(X, Qs, Rs, n, variant, tau, order)
+            factors[n], lam, Qs[n], Rs[n] = u["A"], u["lam"], u["Q"], u["R"]
+            flags |= u["flags"]
+            if debug_sweep1 and s == 0:
+                debug.append({k: u[k] for k in ("Yn", "Q0", "R0", "W", "Ahat", "A", "lam")})
+            last = u
+        if fit_mode == "fast":
+            fits.append(fit_fast_qr(nX2, last["W"], last["Ahat"], last["R0"], Rs[N - 1], lam))
+        else:
+            fits.append(fit_direct(X, lam, factors))
+    return dict(lam=lam, factors=factors, fits=fits, flags=flags, debug=debug, Qs=Qs, Rs=Rs,
+                nX2=nX2)
+
+
+def cp_als_ne(X, A0, sweeps, fit_mode="fast"):
+    """CP-ALS with normal equations, Alg. 1, exactly `sweeps` sweeps.
+    Fit: PAPER.md:417-425 (fast) or direct."""
+    N = X.ndim
+    nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K")))
+    factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
+    grams = [A.T @ A for A in factors]                            # line 3
+    lam = np.ones(factors[0].shape[1])
+    fits, flags = [], 0
+    for s in range(sweeps):
+        last = None
+        for n in range(N):
+            u = mode_update_ne(X, factors, grams, n)
+            factors[n], lam, grams[n] = u["A"], u["lam"], u["G"]
+            flags |= u["flags"]
+            last = u
+        if fit_mode == "fast":
+            fits.append(fit_fast_ne(nX2, last["M"], last["Ahat"], last["S"], grams[N - 1], lam))
+        else:
+            fits.append(fit_direct(X, lam, factors))
+    return dict(lam=lam, factors=factors, fits=fits, flags=flags, nX2=nX2)
+
+
+# ------------------------------------------------------------------ cost model §3.2
+def qr_cost(N: int, R: int) -> int:
+    """Dense QR of V_n with explicit Q0: 4 R^{N+1} (Eq. (QRcost); leading term)."""
+    return 4 * R ** (N + 1)
+
+
+def ttm_cost(dims, n: int, R: int, order=None) -> int:
+    """Multi-TTM flops (Eq. (TTMcost), general form of reading 4): the j-th
+    TTM over mode k_j costs 2 * (current tensor size) * R."""
+    order = ttm_order(dims, n) if order is None else order
+    cur = list(dims)
+    total = 0
+    for k in order:
+        total += 2 * int(np.prod(cur, dtype=np.int64)) * R
+        cur[k] = R
+    return total
