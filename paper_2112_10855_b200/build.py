@@ -1,0 +1,49 @@
+"""Build libcpqr.so in-tree for sm_100a (nvcc, no JIT cache): `python -m paper_2112_10855_b200.build`."""
+import os
+import subprocess
+import sys
+import sysconfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libcpqr.so")
+SRC = [os.path.join(HERE, "csrc", "cpqr.cu")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "ttm_kernels.cuh", "small_kernels.cuh")] + [
+    os.path.join(ROOT, "include", "cpqr.h")]
+
+
+def nccl_dirs():
+    site = sysconfig.get_paths()["purelib"]
+    base = os.path.join(site, "nvidia", "nccl")
+    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+    if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+        return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+def up_to_date():
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(d) <= t for d in DEPS)
+
+
+def build(force=False, verbose=True):
+    if not force and up_to_date():
+        return LIB
+    inc, lib = nccl_dirs()
+    # link against libnccl.so.2 by soname (the pip package ships no unversioned symlink)
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v" if verbose == "ptxas" else "-O3",
+           "-I", inc, "-I", os.path.join(ROOT, "include"),
+           *SRC, "-o", LIB + ".tmp",
+           "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-cudart", "static"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="ptxas" if "--ptxas" in sys.argv else True)

@@ -1,0 +1,255 @@
+"""Thin ctypes binding of libcpqr (include/cpqr.h).  Argument marshalling only: every step of
+the CP-ALS(-QR) path runs in the library's sm_100a kernels.  There is no CPU fallback: if
+libcpqr.so is missing or fails to load, importing this module raises.
+
+Tensors follow the library convention: X is the column-major I_1 x ... x I_N buffer, i.e. a
+C-contiguous numpy array / torch tensor of shape (I_N, ..., I_1).  Factors are (I_k, R) arrays,
+passed column-major (numpy arrays are converted with np.asfortranarray).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("CPQR_LIB", os.path.join(_HERE, "libcpqr.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libcpqr.so not built ({LIB_PATH}); run `python -m paper_2112_10855_b200.build`")
+_lib = C.CDLL(LIB_PATH)
+
+NE, QR, SVD = 0, 1, 2
+VARIANTS = {"NE": NE, "QR": QR, "SVD": SVD}
+FIT_FAST, FIT_DIRECT = 0, 1
+MEM_HOST, MEM_DEVICE_COPY, MEM_DEVICE_BORROW = 0, 1, 2
+FLAG_ILLCOND_R0, FLAG_NE_CHOL_FALLBACK, FLAG_SVD_TRUNCATED = 1, 2, 4
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE", 6: "EDIVERGED"}
+
+EXPORTS = [
+    "cpqr_default_options", "cpqr_create", "cpqr_set_tensor", "cpqr_set_factors", "cpqr_init_factors",
+    "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile",
+    "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_qr", "cpqr_debug_svd_solve",
+    "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
+]
+
+
+class Options(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("svd_tau", C.c_double), ("fit_mode", C.c_int32),
+                ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
+                ("nccl_id", C.c_uint8 * 128), ("use_graph", C.c_int32), ("profile", C.c_int32)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 6), ("launches", C.c_int64 * 6), ("bytes0", C.c_double),
+                ("flops0", C.c_double), ("launches_total", C.c_int64)]
+
+
+_P = C.c_void_p
+_DP = C.POINTER(C.c_double)
+_sig = {
+    "cpqr_default_options": (None, [C.POINTER(Options)]),
+    "cpqr_create": (C.c_int32, [C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_int, C.POINTER(Options), C.POINTER(_P)]),
+    "cpqr_set_tensor": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.c_int64, C.c_int]),
+    "cpqr_set_factors": (C.c_int32, [_P, C.POINTER(_DP), _DP]),
+    "cpqr_init_factors": (C.c_int32, [_P, C.c_uint64]),
+    "cpqr_sweep": (C.c_int32, [_P, C.c_int, _DP]),
+    "cpqr_get_factors": (C.c_int32, [_P, C.POINTER(_DP), _DP]),
+    "cpqr_get_fit": (C.c_int32, [_P, _DP]),
+    "cpqr_get_flags": (C.c_int32, [_P, C.POINTER(C.c_uint32)]),
+    "cpqr_get_profile": (C.c_int32, [_P, C.POINTER(Profile), C.c_int]),
+    "cpqr_launches_per_sweep": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
+    "cpqr_debug_mode": (C.c_int32, [_P, C.c_int, C.POINTER(_DP), _DP, _DP, _DP, _DP]),
+    "cpqr_debug_qr": (C.c_int32, [_P, _DP, C.c_int64, _DP, _DP]),
+    "cpqr_debug_svd_solve": (C.c_int32, [_P, _DP, _DP, C.c_int64, C.c_double, _DP, C.POINTER(C.c_int)]),
+    "cpqr_destroy": (C.c_int32, [_P]),
+    "cpqr_status_string": (C.c_char_p, [C.c_int32]),
+    "cpqr_last_error": (C.c_char_p, [_P]),
+    "cpqr_nccl_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),
+    "cpqr_version": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class CpqrError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def version() -> str:
+    return _lib.cpqr_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    st = _lib.cpqr_nccl_unique_id(buf)
+    if st:
+        raise CpqrError(st, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+class CPQR:
+    """One CP-ALS(-QR) solver over a (slab of a) dense fp64 tensor on one GPU."""
+
+    def __init__(self, dims, R, variant="QR", svd_tau=-1.0, fit_mode="fast", device=0, stream=None,
+                 rank=0, world=1, nccl_id=None, use_graph=True, profile=False):
+        self.dims = tuple(int(d) for d in dims)
+        self.N, self.R = len(self.dims), int(R)
+        self.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+        opt = Options()
+        _lib.cpqr_default_options(C.byref(opt))
+        opt.svd_tau = float(svd_tau)
+        opt.fit_mode = FIT_DIRECT if fit_mode == "direct" else FIT_FAST
+        opt.device = int(device)
+        opt.stream = C.c_void_p(int(stream)) if stream else None
+        opt.rank, opt.world = int(rank), int(world)
+        if nccl_id is not None:
+            C.memmove(opt.nccl_id, bytes(nccl_id), 128)
+        opt.use_graph = 1 if use_graph else 0
+        opt.profile = 1 if profile else 0
+        self.rank, self.world = int(rank), int(world)
+        per = self.dims[-1] // self.world
+        self.slab = (per * self.rank, per * (self.rank + 1))
+        d = (C.c_int64 * self.N)(*self.dims)
+        h = _P()
+        st = _lib.cpqr_create(self.N, d, self.R, self.variant, C.byref(opt), C.byref(h))
+        if st:
+            raise CpqrError(st, "cpqr_create failed (see stderr)")
+        self._h = h
+        self._x_ref = None
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st):
+        if st:
+            raise CpqrError(st, _lib.cpqr_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.cpqr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------------- API
+    def set_tensor(self, X, copy=False):
+        """X: numpy array (host) or torch tensor (host or CUDA), C-contiguous (I_N_local..I_1)."""
+        b, e = self.slab
+        try:
+            import torch
+            is_torch = isinstance(X, torch.Tensor)
+        except ImportError:  # pragma: no cover
+            is_torch = False
+        if is_torch:
+            assert X.dtype == torch.float64 and X.is_contiguous()
+            if X.is_cuda:
+                mem = MEM_DEVICE_COPY if copy else MEM_DEVICE_BORROW
+            else:
+                mem = MEM_HOST
+            ptr = C.c_void_p(X.data_ptr())
+        else:
+            X = np.ascontiguousarray(X, dtype=np.float64)
+            mem, ptr = MEM_HOST, C.c_void_p(X.ctypes.data)
+        self._check(_lib.cpqr_set_tensor(self._h, ptr, b, e, mem))
+        self._x_ref = X if mem == MEM_DEVICE_BORROW else None
+
+    def set_factors(self, factors, lam=None):
+        arrs = [None if A is None else np.asfortranarray(np.asarray(A, dtype=np.float64)) for A in factors]
+        ptrs = (_DP * self.N)(*[(_dptr(a) if a is not None else _DP()) for a in arrs])
+        lp = _dptr(np.ascontiguousarray(lam, dtype=np.float64)) if lam is not None else _DP()
+        self._check(_lib.cpqr_set_factors(self._h, ptrs, lp))
+
+    def init_factors(self, seed):
+        self._check(_lib.cpqr_init_factors(self._h, int(seed)))
+
+    def sweep(self, nsweeps=1) -> np.ndarray:
+        fits = np.zeros(max(1, nsweeps))
+        self._check(_lib.cpqr_sweep(self._h, int(nsweeps), _dptr(fits)))
+        return fits[:nsweeps]
+
+    def get_factors(self):
+        outs = [np.zeros((d, self.R), order="F") for d in self.dims]
+        lam = np.zeros(self.R)
+        ptrs = (_DP * self.N)(*[_dptr(a) for a in outs])
+        self._check(_lib.cpqr_get_factors(self._h, ptrs, _dptr(lam)))
+        return lam, outs
+
+    @property
+    def fit(self):
+        f = C.c_double()
+        self._check(_lib.cpqr_get_fit(self._h, C.byref(f)))
+        return f.value
+
+    @property
+    def flags(self):
+        f = C.c_uint32()
+        self._check(_lib.cpqr_get_flags(self._h, C.byref(f)))
+        return f.value
+
+    def profile(self, reset=True):
+        p = Profile()
+        self._check(_lib.cpqr_get_profile(self._h, C.byref(p), 1 if reset else 0))
+        return dict(ms=list(p.ms), launches=list(p.launches), bytes0=p.bytes0, flops0=p.flops0,
+                    launches_total=p.launches_total)
+
+    def launches_per_sweep(self):
+        n = C.c_int64()
+        self._check(_lib.cpqr_launches_per_sweep(self._h, C.byref(n)))
+        return n.value
+
+    def debug_mode(self, n, Q_override=None):
+        """Alg. 2 lines 6-9 for mode n without changing state: dict(Y, Q0, R0, W) (host arrays;
+        Y is the column-major Multi-TTM tensor returned as a Fortran array of its dims)."""
+        R, N = self.R, self.N
+        ydims = [R] * N
+        ydims[n] = self.dims[n]
+        Y = np.zeros(ydims, order="F")
+        J = R ** (N - 1)
+        Q0 = np.zeros((J, R), order="F")
+        R0 = np.zeros((R, R), order="F")
+        W = np.zeros((self.dims[n], R), order="F")
+        qp = None
+        keep = []
+        if Q_override is not None:
+            arr = []
+            for k in range(N):
+                if k == n or Q_override[k] is None:
+                    arr.append(_DP())
+                else:
+                    a = np.asfortranarray(Q_override[k], dtype=np.float64)
+                    keep.append(a)
+                    arr.append(_dptr(a))
+            qp = (_DP * N)(*arr)
+        self._check(_lib.cpqr_debug_mode(self._h, int(n), qp, Y.ctypes.data_as(_DP), Q0.ctypes.data_as(_DP),
+                                         R0.ctypes.data_as(_DP), W.ctypes.data_as(_DP)))
+        return dict(Y=Y, Q0=Q0, R0=R0, W=W)
+
+    def debug_qr(self, A):
+        A = np.asfortranarray(A, dtype=np.float64)
+        m = A.shape[0]
+        Q = np.zeros((m, self.R), order="F")
+        Rf = np.zeros((self.R, self.R), order="F")
+        self._check(_lib.cpqr_debug_qr(self._h, _dptr(A), m, Q.ctypes.data_as(_DP), Rf.ctypes.data_as(_DP)))
+        return Q, Rf
+
+    def debug_svd_solve(self, R0, W, tau):
+        R0 = np.asfortranarray(R0, dtype=np.float64)
+        W = np.asfortranarray(W, dtype=np.float64)
+        m = W.shape[0]
+        out = np.zeros((m, self.R), order="F")
+        nt = C.c_int()
+        self._check(_lib.cpqr_debug_svd_solve(self._h, _dptr(R0), _dptr(W), m, float(tau),
+                                              out.ctypes.data_as(_DP), C.byref(nt)))
+        return out, nt.value

@@ -1,0 +1,43 @@
+// Shared device helpers for libcpqr (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CPQR_WARP 32
+
+// FP64 tensor-core MMA, D(8x8) += A(8x4) * B(4x8) (SASS DMMA.8x8x4).  tcgen05 has no f64 kind
+// on sm_100a (SURVEY.md §7 hard part 1), so the warp-level mma.sync is the FP64 tensor path.
+// Fragment ownership, lane = 4*g + t (g = lane>>2, t = lane&3):
+//   a = A[g][t],  b = B[t][g],  d0 = D[g][2t], d1 = D[g][2t+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block reduction (deterministic).  `red` must hold blockDim.x/32 doubles.
+// All threads must call; returns the total on every thread.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+__device__ __forceinline__ double ldg_nc(const double* p) { return __ldg(p); }
+
+// Streaming (evict-first) 16-byte load for the tensor pass.
+__device__ __forceinline__ double2 ldg_stream2(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double ldg_stream1(const double* p) { return __ldcs(p); }

@@ -1,0 +1,1193 @@
+// libcpqr: C-ABI entry points and the host-side sweep driver (streams, CUDA graph, NCCL).
+// The per-mode sequence is Alg. 2 lines 6-12 for CP-ALS-QR / QR-SVD and
+// Alg. 1 lines 6-11 for CP-ALS.  See DESIGN.md for the kernel map.
+#include "../../include/cpqr.h"
+#include "small_kernels.cuh"
+#include "ttm_kernels.cuh"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#define CPQR_API extern "C" __attribute__((visibility("default")))
+
+using namespace cpqr;
+
+namespace {
+
+constexpr int kMaxN = 8;
+constexpr int kMaxR = 32;
+constexpr size_t kQSmemMax = 96 * 1024;  // Q panel budget per CTA (2 CTAs / SM)
+
+struct TtmStep {
+  int kind;  // 0 strided, 1 fiber, 2 slice
+  const double* in;
+  double* out;
+  int64_t A, B, F, L;
+  int I, I1, I2;
+  const double* Q;
+  int64_t ldq;
+  const double* Q2;
+  int64_t ldq2;
+  int gps, nseg;
+};
+
+struct DiagStep {
+  const double* in;
+  double* out;
+  int nd;
+  int64_t dims[kMaxN];
+  int k, rm;
+  const double* Ak;
+  int64_t lda;
+};
+
+struct Plan {
+  std::vector<TtmStep> steps;
+  std::vector<DiagStep> diags;  // NE only
+  const double* Y = nullptr;    // final result (device)
+  int nd = 0;
+  int64_t ydims[kMaxN];
+  int64_t Aa = 1, In = 1, Bb = 1;
+  int m_rowmajor = 1;  // NE: layout of the MTTKRP result
+  size_t max_buf = 0;
+  size_t part = 0;
+};
+
+}  // namespace
+
+struct cpqr_ctx {
+  int N = 0, R = 0, variant = 1;
+  int64_t dims[kMaxN] = {0};
+  int64_t ldims[kMaxN] = {0};
+  int64_t slab_b = 0, slab_e = 0, numel = 0;
+  cpqr_options opt;
+  int sms = 148;
+  cudaStream_t st = nullptr;
+  cudaStream_t user = nullptr;
+  ncclComm_t comm = nullptr;
+  const double* X = nullptr;
+  double* Xown = nullptr;
+  size_t Xown_elems = 0;
+  bool have_tensor = false, have_factors = false;
+  double *dA[kMaxN] = {0}, *dQ[kMaxN] = {0}, *dRk[kMaxN] = {0}, *dG[kMaxN] = {0};
+  double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWloc = nullptr,
+         *dWp = nullptr, *dAhat = nullptr;
+  double* buf[2] = {nullptr, nullptr};
+  size_t buf_elems = 0;
+  double* dPart = nullptr;
+  size_t part_elems = 0;
+  int* dperm = nullptr;
+  double* dKrWork = nullptr;
+  double *dnX2 = nullptr, *dfit = nullptr, *dfits = nullptr, *dred = nullptr;
+  int fits_cap = 0;
+  unsigned* dflags = nullptr;
+  double* hpin = nullptr;  // pinned: [0] fit, [1] flags
+  Plan plans[kMaxN];
+  bool plans_valid = false;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_valid = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evp[16] = {};
+  cpqr_profile prof;
+  int64_t launch_count = 0;
+  int64_t launches_per_sweep = -1;
+  double last_fit = NAN;
+  unsigned flags = 0;
+  std::string err;
+  int kr_smem = 0;
+  size_t wp_elems = 0;
+};
+
+namespace {
+
+cpqr_status fail(cpqr_ctx* c, cpqr_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CK(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(c, CPQR_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                \
+  } while (0)
+#define CKL()                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, CPQR_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                  \
+    c->launch_count++;                                                                        \
+  } while (0)
+#define CN(call)                                                                               \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      return fail(c, CPQR_ENCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+#define TRY(x)                       \
+  do {                               \
+    cpqr_status s_ = (x);            \
+    if (s_ != CPQR_OK) return s_;    \
+  } while (0)
+
+int64_t prod(const int64_t* d, int a, int b) {  // prod d[a..b)
+  int64_t p = 1;
+  for (int i = a; i < b; ++i) p *= d[i];
+  return p;
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+int choose_kc(int I, int ld) {
+  const size_t row = (size_t)ld * sizeof(double);
+  const int full = round_up(I, 16);
+  if ((size_t)full * row <= kQSmemMax) return full;
+  int kc = (int)(kQSmemMax / row) / 16 * 16;
+  return std::max(16, kc);
+}
+
+template <typename K>
+int grid_for(K kernel, int64_t units, size_t smem, int sms) {
+  static bool dummy = false;
+  (void)dummy;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, smem);
+  if (nb < 1) nb = 1;
+  int64_t g = std::min<int64_t>(units, (int64_t)sms * nb);
+  return (int)std::max<int64_t>(1, g);
+}
+
+// ----------------------------------------------------------------------- kernel dispatch
+template <int MT, int NT, bool VEC>
+void run_strided(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  constexpr int LD = 8 * NT + 4;
+  const int KC = choose_kc(s.I, LD);
+  const size_t smem = (size_t)KC * LD * sizeof(double);
+  const int64_t BMc = (int64_t)kWarps * 8 * MT;
+  const int64_t units = ((s.A + BMc - 1) / BMc) * s.B;
+  auto k = k_ttm_strided<MT, NT, VEC>;
+  const int grid = grid_for(k, units, smem, sms);
+  k<<<grid, kThreads, smem, st>>>(s.in, s.A, s.I, s.B, s.Q, s.ldq, R, s.out, KC);
+}
+void launch_strided(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  const bool vec = (s.A % 2 == 0) && (((uintptr_t)s.in & 15) == 0);
+  switch ((R + 7) / 8) {
+    case 1: vec ? run_strided<4, 1, true>(s, R, st, sms) : run_strided<4, 1, false>(s, R, st, sms); break;
+    case 2: vec ? run_strided<4, 2, true>(s, R, st, sms) : run_strided<4, 2, false>(s, R, st, sms); break;
+    case 3: vec ? run_strided<4, 3, true>(s, R, st, sms) : run_strided<4, 3, false>(s, R, st, sms); break;
+    default: vec ? run_strided<4, 4, true>(s, R, st, sms) : run_strided<4, 4, false>(s, R, st, sms); break;
+  }
+}
+
+template <int MT, int NF, bool VEC>
+void run_fiber(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  constexpr int LD = 8 * MT + (VEC ? 2 : 4);
+  const int KC = choose_kc(s.I, LD);
+  const size_t smem = (size_t)KC * LD * sizeof(double);
+  const int64_t BF = (int64_t)kWarps * 8 * NF;
+  const int64_t units = (s.F + BF - 1) / BF;
+  auto k = k_ttm_fiber<MT, NF, VEC>;
+  const int grid = grid_for(k, units, smem, sms);
+  k<<<grid, kThreads, smem, st>>>(s.in, s.I, s.F, s.Q, s.ldq, R, s.out, KC);
+}
+void launch_fiber(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  const bool vec = (s.I % 2 == 0) && (((uintptr_t)s.in & 15) == 0);
+  switch ((R + 7) / 8) {
+    case 1: vec ? run_fiber<1, 4, true>(s, R, st, sms) : run_fiber<1, 4, false>(s, R, st, sms); break;
+    case 2: vec ? run_fiber<2, 2, true>(s, R, st, sms) : run_fiber<2, 2, false>(s, R, st, sms); break;
+    case 3: vec ? run_fiber<3, 2, true>(s, R, st, sms) : run_fiber<3, 2, false>(s, R, st, sms); break;
+    default: vec ? run_fiber<4, 2, true>(s, R, st, sms) : run_fiber<4, 2, false>(s, R, st, sms); break;
+  }
+}
+
+int slice_fw(int R) { return ((R + 7) / 8 == 1) ? 32 : 16; }  // 8 * NF
+
+template <int MT, int NF, bool VEC>
+void run_slice(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  constexpr int LD = 8 * MT + (VEC ? 2 : 4);
+  const int KC = choose_kc(s.I1, LD);
+  const size_t smem = (size_t)KC * LD * sizeof(double);
+  const int64_t wunits = (int64_t)s.nseg * s.L;
+  const int64_t cunits = (wunits + kWarps - 1) / kWarps;
+  auto k = k_mttm_slice<MT, NF, VEC>;
+  const int grid = grid_for(k, cunits, smem, sms);
+  k<<<grid, kThreads, smem, st>>>(s.in, s.I1, s.I2, s.L, s.Q, s.ldq, s.Q2, s.ldq2, R, s.gps, s.out, KC);
+}
+void launch_slice(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  const bool vec = (s.I1 % 2 == 0) && (((uintptr_t)s.in & 15) == 0);
+  switch ((R + 7) / 8) {
+    case 1: vec ? run_slice<1, 4, true>(s, R, st, sms) : run_slice<1, 4, false>(s, R, st, sms); break;
+    case 2: vec ? run_slice<2, 2, true>(s, R, st, sms) : run_slice<2, 2, false>(s, R, st, sms); break;
+    case 3: vec ? run_slice<3, 2, true>(s, R, st, sms) : run_slice<3, 2, false>(s, R, st, sms); break;
+    default: vec ? run_slice<4, 2, true>(s, R, st, sms) : run_slice<4, 2, false>(s, R, st, sms); break;
+  }
+}
+
+// ------------------------------------------------------------------------- plan building
+// Multi-TTM Y = X x_{k != n} Q_k^T (Alg. 2 line 8).  Stream-X pass: modes 1 and 2 together
+// (k_mttm_slice) when n >= 3, else the last mode (k_ttm_strided, the largest contiguous GEMM);
+// the remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
+// (ties by decreasing mode, reading 5).
+struct PlanIn {
+  const double* X;
+  const int64_t* ld;  // local dims
+  int N, R, n;
+  const double* Q[kMaxN];  // per-mode operand (Q_k for QR, A_k for NE); mode N-1 already slab-offset
+  int64_t ldq[kMaxN];
+  bool ne;
+  int sms;
+};
+
+void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
+  p.steps.clear();
+  p.diags.clear();
+  const int N = in.N, R = in.R, n = in.n;
+  int64_t cur[kMaxN];
+  for (int k = 0; k < N; ++k) cur[k] = in.ld[k];
+  const double* src = in.X;
+  int nb = 0;
+  p.max_buf = 0;
+  p.part = 0;
+  std::vector<int> todo;
+  auto emit_ttm = [&](int k) {
+    TtmStep s{};
+    s.in = src;
+    s.out = bufs[nb];
+    s.Q = in.Q[k];
+    s.ldq = in.ldq[k];
+    if (k == 0) {
+      s.kind = 1;
+      s.I = (int)cur[0];
+      s.F = prod(cur, 1, N);
+    } else {
+      s.kind = 0;
+      s.A = prod(cur, 0, k);
+      s.I = (int)cur[k];
+      s.B = prod(cur, k + 1, N);
+    }
+    cur[k] = R;
+    p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
+    p.steps.push_back(s);
+    src = bufs[nb];
+    nb ^= 1;
+  };
+  if (in.ne) {
+    // MTTKRP M_n = X_(n) Z_n: one dense TTM with A_k, then Khatri-Rao-diagonal contractions.
+    int rm;
+    if (n >= 1) { emit_ttm(0); rm = 0; }
+    else { emit_ttm(N - 1); rm = N - 1; }
+    int nd = N;
+    int64_t dd[kMaxN];
+    int orig[kMaxN];
+    for (int k = 0; k < N; ++k) { dd[k] = cur[k]; orig[k] = k; }
+    for (int k = N - 1; k >= 0; --k) {
+      if (k == n || k == (n >= 1 ? 0 : N - 1)) continue;
+      int pos = -1;
+      for (int d = 0; d < nd; ++d) if (orig[d] == k) pos = d;
+      int rpos = -1;
+      for (int d = 0; d < nd; ++d) if (orig[d] == (n >= 1 ? 0 : N - 1)) rpos = d;
+      DiagStep ds{};
+      ds.in = src;
+      ds.out = bufs[nb];
+      ds.nd = nd;
+      for (int d = 0; d < nd; ++d) ds.dims[d] = dd[d];
+      ds.k = pos;
+      ds.rm = rpos;
+      ds.Ak = in.Q[k];
+      ds.lda = in.ldq[k];
+      p.diags.push_back(ds);
+      for (int d = pos; d < nd - 1; ++d) { dd[d] = dd[d + 1]; orig[d] = orig[d + 1]; }
+      --nd;
+      src = bufs[nb];
+      nb ^= 1;
+    }
+    (void)rm;
+    p.Y = src;
+    p.nd = nd;
+    for (int d = 0; d < nd; ++d) p.ydims[d] = dd[d];
+    p.m_rowmajor = (n >= 1) ? 1 : 0;  // (R, I_n) col-major == row-major I_n x R
+    if (N == 2) p.m_rowmajor = (n == 1) ? 1 : 0;
+    return;
+  }
+  if (N >= 3 && n >= 2) {
+    TtmStep s{};
+    s.kind = 2;
+    s.in = src;
+    s.I1 = (int)cur[0];
+    s.I2 = (int)cur[1];
+    s.L = prod(cur, 2, N);
+    s.Q = in.Q[0];
+    s.ldq = in.ldq[0];
+    s.Q2 = in.Q[1];
+    s.ldq2 = in.ldq[1];
+    const int fw = slice_fw(R);
+    const int ngr = (s.I2 + fw - 1) / fw;
+    const int64_t target = (int64_t)in.sms * 2 * kWarps * 4;
+    int gps = 1;
+    if ((int64_t)ngr * s.L > target) gps = (int)std::min<int64_t>(ngr, ((int64_t)ngr * s.L + target - 1) / target);
+    s.gps = gps;
+    s.nseg = (ngr + gps - 1) / gps;
+    if (s.nseg > 1) {
+      s.out = part;
+      p.part = (size_t)s.nseg * s.L * R * R;
+    } else {
+      s.out = bufs[nb];
+    }
+    cur[0] = R;
+    cur[1] = R;
+    p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
+    // when nseg > 1 the reduce kernel writes bufs[nb]
+    TtmStep sr = s;
+    p.steps.push_back(s);
+    if (s.nseg > 1) {
+      sr.kind = 3;  // reduce partials
+      sr.in = part;
+      sr.out = bufs[nb];
+      p.steps.push_back(sr);
+    }
+    src = bufs[nb];
+    nb ^= 1;
+    for (int k = 2; k < N; ++k) if (k != n) todo.push_back(k);
+  } else if (N >= 3) {
+    emit_ttm(N - 1);
+    for (int k = 0; k < N - 1; ++k) if (k != n) todo.push_back(k);
+  } else {
+    todo.push_back(1 - n);
+  }
+  std::sort(todo.begin(), todo.end(), [&](int a, int b) {
+    if (cur[a] != cur[b]) return cur[a] > cur[b];
+    return a > b;
+  });
+  for (int k : todo) emit_ttm(k);
+  p.Y = src;
+  p.nd = N;
+  for (int k = 0; k < N; ++k) p.ydims[k] = cur[k];
+  p.Aa = prod(cur, 0, n);
+  p.In = cur[n];
+  p.Bb = prod(cur, n + 1, N);
+}
+
+cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
+  for (const TtmStep& s : p.steps) {
+    switch (s.kind) {
+      case 0: launch_strided(s, c->R, c->st, c->sms); break;
+      case 1: launch_fiber(s, c->R, c->st, c->sms); break;
+      case 2: launch_slice(s, c->R, c->st, c->sms); break;
+      case 3: {
+        const int64_t n = s.L * c->R * c->R;
+        const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sms * 8);
+        k_reduce_slices<<<grid, 256, 0, c->st>>>(s.in, s.nseg, s.L, c->R * c->R, s.out);
+        break;
+      }
+    }
+    CKL();
+  }
+  for (const DiagStep& d : p.diags) {
+    DiagArgs a{};
+    a.T = d.in;
+    a.nd = d.nd;
+    for (int i = 0; i < d.nd; ++i) a.dims[i] = d.dims[i];
+    a.k = d.k;
+    a.rm = d.rm;
+    a.Ak = d.Ak;
+    a.lda = d.lda;
+    a.out = d.out;
+    int64_t tot = 1;
+    for (int i = 0; i < d.nd; ++i) if (i != d.k) tot *= d.dims[i];
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)c->sms * 16));
+    k_diag_contract<<<grid, 256, 0, c->st>>>(a);
+    CKL();
+  }
+  return CPQR_OK;
+}
+
+cpqr_status build_plans(cpqr_ctx* c) {
+  const bool ne = c->variant == CPQR_NE;
+  size_t mb = 0, mp = 0;
+  for (int n = 0; n < c->N; ++n) {
+    PlanIn in{};
+    in.X = c->X;
+    in.ld = c->ldims;
+    in.N = c->N;
+    in.R = c->R;
+    in.n = n;
+    in.ne = ne;
+    in.sms = c->sms;
+    for (int k = 0; k < c->N; ++k) {
+      const double* base = ne ? c->dA[k] : c->dQ[k];
+      in.Q[k] = (k == c->N - 1) ? base + c->slab_b : base;
+      in.ldq[k] = c->dims[k];
+    }
+    Plan tmp;
+    double* nob[2] = {nullptr, nullptr};
+    plan_mode(in, tmp, nob, nullptr);
+    mb = std::max(mb, tmp.max_buf);
+    mp = std::max(mp, tmp.part);
+  }
+  if (mb > c->buf_elems) {
+    for (int i = 0; i < 2; ++i) { if (c->buf[i]) cudaFree(c->buf[i]); c->buf[i] = nullptr; }
+    for (int i = 0; i < 2; ++i)
+      if (cudaMalloc(&c->buf[i], mb * sizeof(double)) != cudaSuccess)
+        return fail(c, CPQR_ENOMEM, "intermediate buffers (%zu doubles)", mb);
+    c->buf_elems = mb;
+  }
+  if (mp > c->part_elems) {
+    if (c->dPart) cudaFree(c->dPart);
+    c->dPart = nullptr;
+    if (cudaMalloc(&c->dPart, mp * sizeof(double)) != cudaSuccess)
+      return fail(c, CPQR_ENOMEM, "slice partials (%zu doubles)", mp);
+    c->part_elems = mp;
+  }
+  for (int n = 0; n < c->N; ++n) {
+    PlanIn in{};
+    in.X = c->X;
+    in.ld = c->ldims;
+    in.N = c->N;
+    in.R = c->R;
+    in.n = n;
+    in.ne = ne;
+    in.sms = c->sms;
+    for (int k = 0; k < c->N; ++k) {
+      const double* base = ne ? c->dA[k] : c->dQ[k];
+      in.Q[k] = (k == c->N - 1) ? base + c->slab_b : base;
+      in.ldq[k] = c->dims[k];
+    }
+    plan_mode(in, c->plans[n], c->buf, c->dPart);
+  }
+  c->plans_valid = true;
+  return CPQR_OK;
+}
+
+// ----------------------------------------------------------------------------- helpers
+void prof_mark(cpqr_ctx* c, int idx) {
+  if (c->opt.profile) cudaEventRecord(c->evp[idx], c->st);
+}
+
+cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
+  KrQrArgs a{};
+  int m = 0;
+  for (int k = 0; k < c->N; ++k)
+    if (k != n) a.Rk[m++] = c->dRk[k];
+  a.N1 = c->N - 1;
+  a.R = c->R;
+  a.perm = c->dperm;
+  a.Q0 = c->dQ0;
+  a.R0 = c->dR0;
+  a.work_global = c->dKrWork;
+  a.use_smem = c->kr_smem > 0;
+  a.flags = c->variant == CPQR_QR ? c->dflags : c->dflags;
+  k_kr_qr<<<1, 1024, c->kr_smem, c->st>>>(a);
+  CKL();
+  return CPQR_OK;
+}
+
+cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
+  const int64_t J = p.Aa * p.Bb;
+  const int In = (int)p.In;
+  const int iblocks = (In + 7) / 8;
+  int KS = (int)std::max<int64_t>(1, std::min<int64_t>((J + 63) / 64, (2 * c->sms + iblocks - 1) / iblocks));
+  const int jchunk = (int)(((J + KS - 1) / KS + 63) / 64 * 64);
+  KS = (int)((J + jchunk - 1) / jchunk);
+  dim3 grid(iblocks, KS);
+  k_q0_apply<<<grid, 256, 0, c->st>>>(p.Y, p.Aa, In, p.Bb, c->dQ0, c->R, jchunk, c->dWp);
+  CKL();
+  const int64_t nW = (int64_t)In * c->R;
+  k_q0_reduce<<<(int)std::min<int64_t>((nW + 255) / 256, 1024), 256, 0, c->st>>>(c->dWp, KS, nW, Wout);
+  CKL();
+  return CPQR_OK;
+}
+
+// combine the per-rank W (or M) of mode n: sum (n < N-1) or gather rows (n == N-1)
+cpqr_status combine_w(cpqr_ctx* c, int n, double* Wloc, double* Wfull) {
+  const int64_t R = c->R;
+  if (c->opt.world <= 1) {
+    if (Wloc != Wfull)
+      CK(cudaMemcpyAsync(Wfull, Wloc, sizeof(double) * c->dims[n] * R, cudaMemcpyDeviceToDevice, c->st));
+    return CPQR_OK;
+  }
+  if (n < c->N - 1) {
+    CN(ncclAllReduce(Wloc, Wfull, (size_t)(c->dims[n] * R), ncclDouble, ncclSum, c->comm, c->st));
+  } else {
+    CN(ncclAllGather(Wloc, Wfull, (size_t)(c->ldims[n] * R), ncclDouble, c->comm, c->st));
+  }
+  return CPQR_OK;
+}
+
+cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
+  const Plan& p = c->plans[n];
+  const int N = c->N;
+  const bool last = (n == N - 1);
+  const int In = (int)c->dims[n];
+  if (c->variant == CPQR_NE) {
+    prof_mark(c, 0);
+    TRY(run_plan(c, p));
+    prof_mark(c, 2);
+    // M for the tail must be row-major complete; combine per-rank results
+    double* Mloc = const_cast<double*>(p.Y);
+    const double* Mfull = Mloc;
+    if (c->opt.world > 1) {
+      if (!p.m_rowmajor) return fail(c, CPQR_EINVAL, "NE multi-GPU needs row-major M");
+      TRY(combine_w(c, n, Mloc, c->dW));
+      Mfull = c->dW;
+    }
+    TailNeArgs a{};
+    a.M = Mfull;
+    a.m_rowmajor = p.m_rowmajor;
+    for (int k = 0; k < N; ++k) a.G[k] = c->dG[k];
+    a.N = N;
+    a.n = n;
+    a.In = In;
+    a.R = c->R;
+    a.A = c->dA[n];
+    a.Gn = c->dG[n];
+    a.lam = c->dlam;
+    a.flags = c->dflags;
+    a.do_fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
+    a.nX2 = c->dnX2;
+    a.fit = c->dfit;
+    a.Ahat = c->dAhat;
+    k_tail_ne<<<1, 512, 2 * c->R * c->R * sizeof(double), c->st>>>(a);
+    CKL();
+    prof_mark(c, 5);
+    return CPQR_OK;
+  }
+  // Alg. 2 lines 6-7: V_n and its QR (K2)
+  prof_mark(c, 0);
+  TRY(launch_kr_qr(c, n));
+  prof_mark(c, 1);
+  // line 8: Multi-TTM (first step = the stream-X pass)
+  {
+    Plan first;
+    first.steps.assign(p.steps.begin(), p.steps.begin() + 1);
+    TRY(run_plan(c, first));
+    prof_mark(c, 2);
+    Plan rest;
+    rest.steps.assign(p.steps.begin() + 1, p.steps.end());
+    TRY(run_plan(c, rest));
+    prof_mark(c, 3);
+  }
+  // line 9: W_n = Y_(n) Q0 (local rows); combine across ranks
+  double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
+  TRY(launch_q0_apply(c, p, Wloc));
+  TRY(combine_w(c, n, Wloc, c->dW));
+  prof_mark(c, 4);
+  // lines 10-12: solve / SVD, normalise, lambda, factor QR (+ fast fit after mode N)
+  TailArgs a{};
+  a.W = c->dW;
+  a.R0 = c->dR0;
+  a.In = In;
+  a.R = c->R;
+  a.variant = c->variant;
+  a.tau = (c->opt.svd_tau < 0) ? c->R * 2.220446049250313e-16 : c->opt.svd_tau;
+  a.Aw = c->dQ[n];
+  a.A = c->dA[n];
+  a.Rn = c->dRk[n];
+  a.lam = c->dlam;
+  a.flags = c->dflags;
+  a.do_fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
+  a.nX2 = c->dnX2;
+  a.fit = c->dfit;
+  a.Ahat_fit = c->dAhat;
+  const size_t smem = (size_t)(2 * c->R * c->R + 2 * c->R * (c->R + 1)) * sizeof(double);
+  k_tail_qr<<<1, 512, smem, c->st>>>(a);
+  CKL();
+  prof_mark(c, 5);
+  (void)last;
+  return CPQR_OK;
+}
+
+cpqr_status direct_fit(cpqr_ctx* c) {
+  ResidArgs a{};
+  a.X = c->X;
+  a.n = c->numel;
+  a.N = c->N;
+  for (int k = 0; k < c->N; ++k) { a.dims[k] = c->ldims[k]; a.A[k] = c->dA[k]; a.lda[k] = c->dims[k]; }
+  a.off_last = c->slab_b;
+  a.lam = c->dlam;
+  a.R = c->R;
+  a.part = c->dred;
+  const int grid = c->sms * 4;
+  k_resid_partial<<<grid, 256, 0, c->st>>>(a);
+  CKL();
+  k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, c->dred + 4096);
+  CKL();
+  if (c->opt.world > 1) CN(ncclAllReduce(c->dred + 4096, c->dred + 4096, 1, ncclDouble, ncclSum, c->comm, c->st));
+  k_fit_from_resid<<<1, 32, 0, c->st>>>(c->dred + 4096, c->dnX2, c->dfit);
+  CKL();
+  return CPQR_OK;
+}
+
+cpqr_status one_sweep(cpqr_ctx* c) {
+  for (int n = 0; n < c->N; ++n) TRY(mode_update(c, n, n == c->N - 1));
+  if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
+  return CPQR_OK;
+}
+
+void prof_accumulate(cpqr_ctx* c) {
+  // events: 0 start, 1 after K2, 2 after stream pass, 3 after rest TTM, 4 after Q0 apply, 5 end
+  float ms;
+  if (c->variant == CPQR_NE) {
+    if (cudaEventElapsedTime(&ms, c->evp[0], c->evp[2]) == cudaSuccess) c->prof.ms[0] += ms;
+    if (cudaEventElapsedTime(&ms, c->evp[2], c->evp[5]) == cudaSuccess) c->prof.ms[5] += ms;
+    return;
+  }
+  if (cudaEventElapsedTime(&ms, c->evp[0], c->evp[1]) == cudaSuccess) c->prof.ms[3] += ms;
+  if (cudaEventElapsedTime(&ms, c->evp[1], c->evp[2]) == cudaSuccess) c->prof.ms[0] += ms;
+  if (cudaEventElapsedTime(&ms, c->evp[2], c->evp[3]) == cudaSuccess) c->prof.ms[1] += ms;
+  if (cudaEventElapsedTime(&ms, c->evp[3], c->evp[4]) == cudaSuccess) c->prof.ms[4] += ms;
+  if (cudaEventElapsedTime(&ms, c->evp[4], c->evp[5]) == cudaSuccess) c->prof.ms[5] += ms;
+}
+
+cpqr_status ensure_fits(cpqr_ctx* c, int n) {
+  if (n <= c->fits_cap) return CPQR_OK;
+  if (c->dfits) cudaFree(c->dfits);
+  c->dfits = nullptr;
+  if (cudaMalloc(&c->dfits, sizeof(double) * n) != cudaSuccess) return fail(c, CPQR_ENOMEM, "fits");
+  c->fits_cap = n;
+  return CPQR_OK;
+}
+
+// splitmix64 + Box-Muller: counter-based N(0,1) (cpqr_init_factors)
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+double normal_at(uint64_t seed, uint64_t i) {
+  const uint64_t a = splitmix64(seed * 0x2545F4914F6CDD1Dull + 2 * (i / 2));
+  const uint64_t b = splitmix64(seed * 0x2545F4914F6CDD1Dull + 2 * (i / 2) + 1);
+  const double u1 = ((a >> 11) + 1.0) * (1.0 / 9007199254740993.0);
+  const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
+  const double r = std::sqrt(-2.0 * std::log(u1));
+  return (i & 1) ? r * std::sin(2.0 * M_PI * u2) : r * std::cos(2.0 * M_PI * u2);
+}
+
+cpqr_status begin_call(cpqr_ctx* c) {
+  CK(cudaSetDevice(c->opt.device));
+  if (c->user) {
+    CK(cudaEventRecord(c->ev0, c->user));
+    CK(cudaStreamWaitEvent(c->st, c->ev0, 0));
+  }
+  return CPQR_OK;
+}
+cpqr_status end_call(cpqr_ctx* c) {
+  if (c->user) {
+    CK(cudaEventRecord(c->ev1, c->st));
+    CK(cudaStreamWaitEvent(c->user, c->ev1, 0));
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return CPQR_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+CPQR_API void cpqr_default_options(cpqr_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->struct_size = sizeof(cpqr_options);
+  o->svd_tau = -1.0;
+  o->fit_mode = CPQR_FIT_FAST;
+  o->device = 0;
+  o->stream = nullptr;
+  o->rank = 0;
+  o->world = 1;
+  o->use_graph = 1;
+  o->profile = 0;
+}
+
+CPQR_API const char* cpqr_version(void) { return "cpqr 0.1.0 sm_100a fp64"; }
+
+CPQR_API const char* cpqr_status_string(cpqr_status s) {
+  switch (s) {
+    case CPQR_OK: return "ok";
+    case CPQR_EINVAL: return "invalid argument";
+    case CPQR_ENOMEM: return "out of device memory";
+    case CPQR_ECUDA: return "CUDA error";
+    case CPQR_ENCCL: return "NCCL error";
+    case CPQR_ESTATE: return "invalid state (tensor or factors not set)";
+    case CPQR_EDIVERGED: return "non-finite factor (diverged)";
+    default: return "unknown status";
+  }
+}
+
+CPQR_API const char* cpqr_last_error(const cpqr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+CPQR_API cpqr_status cpqr_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return CPQR_EINVAL;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return CPQR_ENCCL;
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return CPQR_OK;
+}
+
+static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R);
+
+CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
+                                 const cpqr_options* opt, cpqr_ctx** out) {
+  if (!out || !dims) return CPQR_EINVAL;
+  *out = nullptr;
+  if (N < 2 || N > kMaxN || R < 1 || R > kMaxR) return CPQR_EINVAL;
+  if (variant < CPQR_NE || variant > CPQR_SVD) return CPQR_EINVAL;
+  for (int k = 0; k < N; ++k)
+    if (dims[k] < R || dims[k] > (1ll << 31) - 1) return CPQR_EINVAL;
+  cpqr_ctx* c = new cpqr_ctx();
+  cpqr_default_options(&c->opt);
+  if (opt) {
+    if (opt->struct_size < sizeof(uint32_t) || opt->struct_size > sizeof(cpqr_options)) { delete c; return CPQR_EINVAL; }
+    std::memcpy(&c->opt, opt, opt->struct_size);
+    c->opt.struct_size = sizeof(cpqr_options);
+  }
+  if (c->opt.world < 1 || c->opt.rank < 0 || c->opt.rank >= c->opt.world) { delete c; return CPQR_EINVAL; }
+  if (c->opt.world > 1 && (dims[N - 1] % c->opt.world) != 0) { delete c; return CPQR_EINVAL; }
+  c->variant = variant;
+  cpqr_status st = create_impl(c, N, dims, R);
+  if (st != CPQR_OK) {
+    fprintf(stderr, "cpqr_create: %s: %s\n", cpqr_status_string(st), c->err.c_str());
+    cpqr_destroy(c);
+    return st;
+  }
+  *out = c;
+  return CPQR_OK;
+}
+
+static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
+  c->N = N;
+  c->R = R;
+  for (int k = 0; k < N; ++k) c->dims[k] = c->ldims[k] = dims[k];
+  const int64_t per = dims[N - 1] / c->opt.world;
+  c->slab_b = per * c->opt.rank;
+  c->slab_e = c->slab_b + per;
+  c->ldims[N - 1] = per;
+  c->numel = prod(c->ldims, 0, N);
+  std::memset(&c->prof, 0, sizeof c->prof);
+  if (cudaSetDevice(c->opt.device) != cudaSuccess) return fail(c, CPQR_ECUDA, "cudaSetDevice(%d)", c->opt.device);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->opt.device);
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  c->user = (cudaStream_t)c->opt.stream;
+  CK(cudaEventCreateWithFlags(&c->ev0, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev1, cudaEventDisableTiming));
+  for (int i = 0; i < 16; ++i) CK(cudaEventCreate(&c->evp[i]));
+  int64_t imax = 0;
+  for (int k = 0; k < N; ++k) {
+    imax = std::max(imax, dims[k]);
+    CK(cudaMalloc(&c->dA[k], sizeof(double) * dims[k] * R));
+    CK(cudaMalloc(&c->dQ[k], sizeof(double) * dims[k] * R));
+    CK(cudaMalloc(&c->dRk[k], sizeof(double) * R * R));
+    CK(cudaMalloc(&c->dG[k], sizeof(double) * R * R));
+    CK(cudaMemset(c->dRk[k], 0, sizeof(double) * R * R));
+    CK(cudaMemset(c->dG[k], 0, sizeof(double) * R * R));
+  }
+  int64_t J = 1;
+  for (int k = 0; k < N - 1; ++k) J *= R;
+  CK(cudaMalloc(&c->dlam, sizeof(double) * R));
+  CK(cudaMalloc(&c->dQ0, sizeof(double) * J * R));
+  CK(cudaMalloc(&c->dR0, sizeof(double) * R * R));
+  CK(cudaMalloc(&c->dW, sizeof(double) * imax * R));
+  CK(cudaMalloc(&c->dWloc, sizeof(double) * imax * R));
+  CK(cudaMalloc(&c->dAhat, sizeof(double) * imax * R));
+  c->wp_elems = (size_t)imax * R * 1024;
+  CK(cudaMalloc(&c->dWp, sizeof(double) * std::min<size_t>(c->wp_elems, (size_t)imax * R * (size_t)std::max<int64_t>(1, (J + 63) / 64))));
+  CK(cudaMalloc(&c->dnX2, sizeof(double) * 4));
+  CK(cudaMalloc(&c->dfit, sizeof(double) * 4));
+  CK(cudaMalloc(&c->dred, sizeof(double) * 8192));
+  CK(cudaMalloc(&c->dflags, sizeof(unsigned) * 4));
+  CK(cudaMemset(c->dflags, 0, sizeof(unsigned) * 4));
+  CK(cudaMallocHost(&c->hpin, sizeof(double) * 64));
+  // staircase row order for K2: sort KB rows of R^{N-1} by (level, index)
+  {
+    std::vector<int> perm(J);
+    std::vector<int> lvl(J);
+    for (int64_t j = 0; j < J; ++j) {
+      int64_t x = j;
+      int l = 0;
+      for (int m = 0; m < N - 1; ++m) { l = std::max<int>(l, (int)(x % R)); x /= R; }
+      lvl[j] = l;
+      perm[j] = (int)j;
+    }
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return lvl[a] < lvl[b]; });
+    CK(cudaMalloc(&c->dperm, sizeof(int) * J));
+    CK(cudaMemcpy(c->dperm, perm.data(), sizeof(int) * J, cudaMemcpyHostToDevice));
+    int64_t packed = 0;
+    for (int cc = 1; cc <= R; ++cc) {
+      int64_t p = 1;
+      for (int m = 0; m < N - 1; ++m) p *= cc;
+      packed += p;
+    }
+    const size_t bytes = packed * sizeof(double);
+    if (bytes <= 200 * 1024) {
+      c->kr_smem = (int)bytes;
+      CK(cudaFuncSetAttribute(k_kr_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, c->kr_smem));
+    } else {
+      c->kr_smem = 0;
+      CK(cudaMalloc(&c->dKrWork, bytes));
+    }
+  }
+  if (c->opt.world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, c->opt.nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&c->comm, c->opt.world, id, c->opt.rank);
+    if (r != ncclSuccess) return fail(c, CPQR_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
+  if (!c) return CPQR_OK;
+  cudaSetDevice(c->opt.device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (int k = 0; k < kMaxN; ++k) {
+    cudaFree(c->dA[k]); cudaFree(c->dQ[k]); cudaFree(c->dRk[k]); cudaFree(c->dG[k]);
+  }
+  double* ps[] = {c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
+                  c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown};
+  for (double* p : ps) if (p) cudaFree(p);
+  if (c->dperm) cudaFree(c->dperm);
+  if (c->dflags) cudaFree(c->dflags);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  for (int i = 0; i < 16; ++i) if (c->evp[i]) cudaEventDestroy(c->evp[i]);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, int64_t e, int mem) {
+  if (!c || !x) return c ? fail(c, CPQR_EINVAL, "null tensor") : CPQR_EINVAL;
+  if (b != c->slab_b || e != c->slab_e)
+    return fail(c, CPQR_EINVAL, "slab [%lld,%lld) != expected [%lld,%lld) for rank %d/%d", (long long)b,
+                (long long)e, (long long)c->slab_b, (long long)c->slab_e, c->opt.rank, c->opt.world);
+  TRY(begin_call(c));
+  const size_t bytes = sizeof(double) * c->numel;
+  if (mem == CPQR_MEM_DEVICE_BORROW) {
+    if (c->Xown) { cudaFree(c->Xown); c->Xown = nullptr; c->Xown_elems = 0; }
+    c->X = x;
+  } else if (mem == CPQR_MEM_HOST || mem == CPQR_MEM_DEVICE_COPY) {
+    if (c->Xown_elems < (size_t)c->numel) {
+      if (c->Xown) cudaFree(c->Xown);
+      c->Xown = nullptr;
+      if (cudaMalloc(&c->Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
+      c->Xown_elems = c->numel;
+    }
+    CK(cudaMemcpyAsync(c->Xown, x, bytes, mem == CPQR_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->st));
+    c->X = c->Xown;
+  } else {
+    return fail(c, CPQR_EINVAL, "bad mem kind %d", mem);
+  }
+  const int grid = c->sms * 4;
+  k_sumsq_partial<<<grid, 256, 0, c->st>>>(c->X, c->numel, c->dred);
+  CKL();
+  k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, c->dnX2);
+  CKL();
+  if (c->opt.world > 1) CN(ncclAllReduce(c->dnX2, c->dnX2, 1, ncclDouble, ncclSum, c->comm, c->st));
+  c->have_tensor = true;
+  c->graph_valid = false;
+  TRY(build_plans(c));
+  return end_call(c);
+}
+
+static cpqr_status upload_factors(cpqr_ctx* c, const double* const* A, const double* lam) {
+  const int R = c->R;
+  for (int k = 0; k < c->N; ++k) {
+    if (!A[k]) {
+      if (c->variant == CPQR_NE && k != 0) return fail(c, CPQR_EINVAL, "NE needs A[%d]", k);
+      if (k != 0) return fail(c, CPQR_EINVAL, "A[%d] is NULL", k);
+      continue;
+    }
+    CK(cudaMemcpyAsync(c->dA[k], A[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
+    if (c->variant == CPQR_NE) {
+      k_gram<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dG[k]);
+      CKL();
+    } else {
+      k_factor_qr<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dQ[k], c->dRk[k]);
+      CKL();
+    }
+  }
+  std::vector<double> l(R, 1.0);
+  if (lam) for (int r = 0; r < R; ++r) l[r] = lam[r];
+  CK(cudaMemcpyAsync(c->dlam, l.data(), sizeof(double) * R, cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->have_factors = true;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_set_factors(cpqr_ctx* c, const double* const* A, const double* lam) {
+  if (!c || !A) return c ? fail(c, CPQR_EINVAL, "null factors") : CPQR_EINVAL;
+  TRY(begin_call(c));
+  TRY(upload_factors(c, A, lam));
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_init_factors(cpqr_ctx* c, uint64_t seed) {
+  if (!c) return CPQR_EINVAL;
+  std::vector<std::vector<double>> h(c->N);
+  std::vector<const double*> p(c->N);
+  uint64_t ctr = 0;
+  for (int k = 0; k < c->N; ++k) {
+    h[k].resize(c->dims[k] * c->R);
+    for (auto& v : h[k]) v = normal_at(seed, ctr++);
+    p[k] = h[k].data();
+  }
+  return cpqr_set_factors(c, p.data(), nullptr);
+}
+
+CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
+  if (!c || nsweeps < 0) return CPQR_EINVAL;
+  if (!c->have_tensor || !c->have_factors) return fail(c, CPQR_ESTATE, "tensor/factors not set");
+  TRY(begin_call(c));
+  TRY(ensure_fits(c, std::max(1, nsweeps)));
+  const bool graph = c->opt.use_graph && !c->opt.profile;
+  for (int s = 0; s < nsweeps; ++s) {
+    if (graph) {
+      if (!c->graph_valid) {
+        const int64_t before = c->launch_count;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        cpqr_status st = one_sweep(c);
+        cudaError_t ce = cudaStreamEndCapture(c->st, &g);
+        if (st != CPQR_OK) { if (ce == cudaSuccess) cudaGraphDestroy(g); return st; }
+        CK(ce);
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+        CK(cudaGraphInstantiate(&c->gexec, g, 0));
+        cudaGraphDestroy(g);
+        c->graph_valid = true;
+        c->launches_per_sweep = c->launch_count - before;
+      }
+      CK(cudaGraphLaunch(c->gexec, c->st));
+      c->launch_count += c->launches_per_sweep;
+    } else {
+      const int64_t before = c->launch_count;
+      for (int n = 0; n < c->N; ++n) {
+        TRY(mode_update(c, n, n == c->N - 1));
+        if (c->opt.profile) {
+          CK(cudaEventSynchronize(c->evp[5]));
+          prof_accumulate(c);
+        }
+      }
+      if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
+      c->launches_per_sweep = c->launch_count - before;
+    }
+    CK(cudaMemcpyAsync(c->dfits + s, c->dfit, sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  }
+  if (nsweeps > 0) {
+    std::vector<double> hf(nsweeps);
+    CK(cudaMemcpyAsync(hf.data(), c->dfits, sizeof(double) * nsweeps, cudaMemcpyDeviceToHost, c->st));
+    unsigned fl = 0;
+    CK(cudaMemcpyAsync(&fl, c->dflags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+    TRY(end_call(c));
+    if (c->variant != CPQR_QR) fl &= ~(unsigned)FLAG_ILLCOND_R0;
+    c->flags |= fl;
+    c->last_fit = hf[nsweeps - 1];
+    if (fits) std::memcpy(fits, hf.data(), sizeof(double) * nsweeps);
+    if (fl & FLAG_NONFINITE) return fail(c, CPQR_EDIVERGED, "non-finite factor");
+    return CPQR_OK;
+  }
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_get_factors(cpqr_ctx* c, double* const* A_out, double* lam) {
+  if (!c) return CPQR_EINVAL;
+  if (!c->have_factors) return fail(c, CPQR_ESTATE, "factors not set");
+  TRY(begin_call(c));
+  if (A_out)
+    for (int k = 0; k < c->N; ++k)
+      if (A_out[k]) CK(cudaMemcpyAsync(A_out[k], c->dA[k], sizeof(double) * c->dims[k] * c->R, cudaMemcpyDeviceToHost, c->st));
+  if (lam) CK(cudaMemcpyAsync(lam, c->dlam, sizeof(double) * c->R, cudaMemcpyDeviceToHost, c->st));
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_get_fit(cpqr_ctx* c, double* fit) {
+  if (!c || !fit) return CPQR_EINVAL;
+  *fit = c->last_fit;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_get_flags(cpqr_ctx* c, uint32_t* f) {
+  if (!c || !f) return CPQR_EINVAL;
+  *f = c->flags & 0xffu;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_get_profile(cpqr_ctx* c, cpqr_profile* p, int reset) {
+  if (!c || !p) return CPQR_EINVAL;
+  *p = c->prof;
+  // algorithmic bytes / flops of the stream-X pass for one sweep:
+  // bytes = N * 8 * numel (X read once per mode); flops = sum over modes of the first TTM (+ the
+  // fused second contraction of k_mttm_slice)
+  double fl = 0.0;
+  for (int n = 0; n < c->N; ++n) {
+    const Plan& pl = c->plans[n];
+    if (pl.steps.empty()) continue;
+    const TtmStep& s = pl.steps[0];
+    const double R = c->R;
+    if (s.kind == 2) fl += 2.0 * c->numel * R + 2.0 * (c->numel / (double)s.I1) * R * R;
+    else fl += 2.0 * c->numel * R;
+  }
+  p->bytes0 = (double)c->N * 8.0 * c->numel;
+  p->flops0 = fl;
+  p->launches_total = c->launch_count;
+  if (reset) std::memset(&c->prof, 0, sizeof c->prof);
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_launches_per_sweep(cpqr_ctx* c, int64_t* n) {
+  if (!c || !n) return CPQR_EINVAL;
+  *n = c->launches_per_sweep;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo, double* Y_out,
+                                     double* Q0_out, double* R0_out, double* W_out) {
+  if (!c) return CPQR_EINVAL;
+  if (n < 0 || n >= c->N) return fail(c, CPQR_EINVAL, "mode %d", n);
+  if (!c->have_tensor || !c->have_factors) return fail(c, CPQR_ESTATE, "tensor/factors not set");
+  if (c->variant == CPQR_NE) return fail(c, CPQR_EINVAL, "debug_mode is for the QR/SVD variants");
+  TRY(begin_call(c));
+  const int R = c->R, N = c->N;
+  std::vector<double*> tmpQ(N, nullptr);
+  PlanIn in{};
+  in.X = c->X;
+  in.ld = c->ldims;
+  in.N = N;
+  in.R = R;
+  in.n = n;
+  in.ne = false;
+  in.sms = c->sms;
+  for (int k = 0; k < N; ++k) {
+    const double* base = c->dQ[k];
+    if (Qo && k != n && Qo[k]) {
+      CK(cudaMalloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
+      CK(cudaMemcpyAsync(tmpQ[k], Qo[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
+      base = tmpQ[k];
+    }
+    in.Q[k] = (k == N - 1) ? base + c->slab_b : base;
+    in.ldq[k] = c->dims[k];
+  }
+  Plan p;
+  plan_mode(in, p, c->buf, c->dPart);
+  cpqr_status st = launch_kr_qr(c, n);
+  if (st == CPQR_OK) st = run_plan(c, p);
+  double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
+  if (st == CPQR_OK) st = launch_q0_apply(c, p, Wloc);
+  if (st == CPQR_OK) st = combine_w(c, n, Wloc, c->dW);
+  const int64_t ylocal = (int64_t)p.Aa * p.In * p.Bb;
+  double* yfull = nullptr;
+  int64_t ytot = ylocal;
+  if (st == CPQR_OK && Y_out) {
+    if (c->opt.world > 1) {
+      ytot = (n == N - 1) ? ylocal * c->opt.world : ylocal;
+      if (cudaMalloc(&yfull, sizeof(double) * ytot) != cudaSuccess) st = fail(c, CPQR_ENOMEM, "debug Y");
+      if (st == CPQR_OK) {
+        ncclResult_t r = (n == N - 1)
+                             ? ncclAllGather(p.Y, yfull, (size_t)ylocal, ncclDouble, c->comm, c->st)
+                             : ncclAllReduce(p.Y, yfull, (size_t)ylocal, ncclDouble, ncclSum, c->comm, c->st);
+        if (r != ncclSuccess) st = fail(c, CPQR_ENCCL, "debug Y collective");
+      }
+    }
+  }
+  if (st == CPQR_OK) {
+    std::vector<double> w((size_t)c->dims[n] * R);
+    cudaMemcpyAsync(w.data(), c->dW, sizeof(double) * w.size(), cudaMemcpyDeviceToHost, c->st);
+    if (Y_out) cudaMemcpyAsync(Y_out, yfull ? yfull : p.Y, sizeof(double) * ytot, cudaMemcpyDeviceToHost, c->st);
+    int64_t J = 1;
+    for (int k = 0; k < N - 1; ++k) J *= R;
+    if (Q0_out) cudaMemcpyAsync(Q0_out, c->dQ0, sizeof(double) * J * R, cudaMemcpyDeviceToHost, c->st);
+    if (R0_out) cudaMemcpyAsync(R0_out, c->dR0, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st);
+    cudaError_t e = cudaStreamSynchronize(c->st);
+    if (e != cudaSuccess) st = fail(c, CPQR_ECUDA, "debug sync: %s", cudaGetErrorString(e));
+    if (W_out && st == CPQR_OK)
+      for (int64_t i = 0; i < c->dims[n]; ++i)
+        for (int r = 0; r < R; ++r) W_out[i + c->dims[n] * r] = w[i * R + r];
+  }
+  cudaStreamSynchronize(c->st);
+  if (yfull) cudaFree(yfull);
+  for (double* q : tmpQ) if (q) cudaFree(q);
+  if (st != CPQR_OK) return st;
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_debug_qr(cpqr_ctx* c, const double* A, int64_t m, double* Q, double* Rf) {
+  if (!c || !A || m < c->R) return CPQR_EINVAL;
+  TRY(begin_call(c));
+  const int R = c->R;
+  double *dA = nullptr, *dQ = nullptr, *dR = nullptr;
+  CK(cudaMalloc(&dA, sizeof(double) * m * R));
+  CK(cudaMalloc(&dQ, sizeof(double) * m * R));
+  CK(cudaMalloc(&dR, sizeof(double) * R * R));
+  CK(cudaMemcpyAsync(dA, A, sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
+  k_factor_qr<<<1, 1024, 0, c->st>>>(dA, (int)m, R, dQ, dR);
+  CKL();
+  if (Q) CK(cudaMemcpyAsync(Q, dQ, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
+  if (Rf) CK(cudaMemcpyAsync(Rf, dR, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  cudaFree(dA); cudaFree(dQ); cudaFree(dR);
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_debug_svd_solve(cpqr_ctx* c, const double* R0, const double* W, int64_t m,
+                                          double tau, double* Ahat, int* ntrunc) {
+  if (!c || !R0 || !W || !Ahat || m < 1) return CPQR_EINVAL;
+  TRY(begin_call(c));
+  const int R = c->R;
+  double *dW, *dR0, *dAw, *dA, *dRn, *dlam, *dAh;
+  unsigned* dfl;
+  CK(cudaMalloc(&dW, sizeof(double) * m * R));
+  CK(cudaMalloc(&dR0, sizeof(double) * R * R));
+  CK(cudaMalloc(&dAw, sizeof(double) * m * R));
+  CK(cudaMalloc(&dA, sizeof(double) * m * R));
+  CK(cudaMalloc(&dAh, sizeof(double) * m * R));
+  CK(cudaMalloc(&dRn, sizeof(double) * R * R));
+  CK(cudaMalloc(&dlam, sizeof(double) * R));
+  CK(cudaMalloc(&dfl, sizeof(unsigned)));
+  CK(cudaMemsetAsync(dfl, 0, sizeof(unsigned), c->st));
+  std::vector<double> wr((size_t)m * R);
+  for (int64_t i = 0; i < m; ++i)
+    for (int r = 0; r < R; ++r) wr[i * R + r] = W[i + m * r];
+  CK(cudaMemcpyAsync(dW, wr.data(), sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(dR0, R0, sizeof(double) * R * R, cudaMemcpyHostToDevice, c->st));
+  TailArgs a{};
+  a.W = dW; a.R0 = dR0; a.In = (int)m; a.R = R; a.variant = CPQR_SVD; a.tau = tau;
+  a.Aw = dAw; a.A = dA; a.Rn = dRn; a.lam = dlam; a.flags = dfl; a.do_fit = 1;
+  a.nX2 = c->dnX2; a.fit = c->dred; a.Ahat_fit = dAh;
+  int* dnt = nullptr;
+  CK(cudaMalloc(&dnt, sizeof(int)));
+  CK(cudaMemsetAsync(dnt, 0, sizeof(int), c->st));
+  a.ntrunc = dnt;
+  const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+  k_tail_qr<<<1, 512, smem, c->st>>>(a);
+  CKL();
+  unsigned fl = 0;
+  CK(cudaMemcpyAsync(Ahat, dAh, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&fl, dfl, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  int nt = 0;
+  CK(cudaMemcpy(&nt, dnt, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(dnt);
+  if (ntrunc) *ntrunc = nt;
+  (void)fl;
+  cudaFree(dW); cudaFree(dR0); cudaFree(dAw); cudaFree(dA); cudaFree(dAh); cudaFree(dRn); cudaFree(dlam); cudaFree(dfl);
+  return end_call(c);
+}

@@ -1,0 +1,767 @@
+// Small per-mode kernels of the CP-ALS-QR hot path (sm_100a, fp64).  Everything here works on
+// O(I_n R + R^N) data; the only pass over the tensor X is in ttm_kernels.cuh (and k_sumsq,
+// once per set_tensor).
+//
+//   K1 k_factor_qr / hh_qr_block  thin Householder QR of I_n x R (Alg. 2 line 3/12)
+//   K2 k_kr_qr      Khatri-Rao of triangular R_k + staircase Householder QR -> Q0, R0
+//                   (Alg. 2 lines 6-7; staircase/no fill-in PAPER.md:458-466)
+//   K4 k_q0_apply   W_n = Y_(n) Q0 (Alg. 2 line 9)
+//   K5 k_tail_qr    solve Ahat R0^T = W (substitution) or Ahat = W U S^+ V^T (one-sided Jacobi SVD
+//                   of R0), normalise, lambda, factor QR, fast fit
+//   K6 k_sumsq      ||X||^2 (fixed-order two-level reduction)
+//   K7 k_diag_contract, k_tail_ne   CP-ALS (Alg. 1) MTTKRP stage 2 and the
+//                   Cholesky/LU solve, normalise, Gram, fast fit
+// All reductions are fixed-order (no floating-point atomics): results are bitwise reproducible.
+#pragma once
+#include "common.cuh"
+
+namespace cpqr {
+
+constexpr double kEps = 2.220446049250313e-16;
+
+enum : unsigned { FLAG_ILLCOND_R0 = 1u, FLAG_NE_CHOL_FALLBACK = 2u, FLAG_SVD_TRUNCATED = 4u,
+                  FLAG_NONFINITE = 0x100u };
+
+// ------------------------------------------------------------------------------ sum of squares
+__global__ void k_sumsq_partial(const double* __restrict__ X, int64_t n, double* __restrict__ part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const int64_t n2 = n / 2;
+  const double2* X2 = reinterpret_cast<const double2*>(X);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = __ldcs(X2 + i);
+    s += v.x * v.x + v.y * v.y;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) s += X[n - 1] * X[n - 1];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_sum_final(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ------------------------------------------------------------------- Householder QR (one CTA)
+// In-place thin QR of the column-major m x R matrix Aw (leading dimension lda).  Reflectors in
+// LAPACK dgeqr2 form: H_j = I - tau_j v v^T, v_j = 1, v_i (i > j) stored below the diagonal,
+// beta_j = -sign(alpha) ||x|| on the diagonal.  Then R (upper triangle, rows sign-fixed so that
+// diag >= 0, reading 6) is written to Rf (R x R column-major) and Aw is overwritten by the
+// explicit Q (dorg2r order, columns sign-fixed to match).  Needs blockDim.x >= 64,
+// smem: tau[R], beta[R], w[R], red[32].  Row range per column: rows j..rows_of(j)-1 where
+// rows_of(j) = m for a dense matrix (staircase version: see k_kr_qr).
+__device__ void hh_qr_block(double* Aw, int64_t lda, int m, int R, double* Rf, double* tau,
+                            double* beta, double* w, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int j = 0; j < R; ++j) {
+    double* colj = Aw + lda * j;
+    double s = 0.0;
+    for (int i = j + 1 + tid; i < m; i += nt) s += colj[i] * colj[i];
+    s = block_sum(s, red);
+    const double alpha = colj[j];
+    const double nrm = sqrt(alpha * alpha + s);
+    double tj, bj, scale;
+    if (s == 0.0) {  // already reduced: H = I (dlarfg), beta = alpha
+      tj = 0.0; bj = alpha; scale = 0.0;
+    } else {
+      bj = (alpha >= 0.0) ? -nrm : nrm;
+      tj = (bj - alpha) / bj;
+      scale = 1.0 / (alpha - bj);
+    }
+    __syncthreads();
+    if (tj != 0.0)
+      for (int i = j + 1 + tid; i < m; i += nt) colj[i] *= scale;
+    if (tid == 0) { tau[j] = tj; beta[j] = bj; colj[j] = bj; }
+    __syncthreads();
+    if (tj != 0.0) {
+      // w_k = A(j,k) + sum_{i>j} v_i A(i,k), k > j: one warp per column, fixed order
+      for (int k = j + 1 + wid; k < R; k += nw) {
+        const double* ck = Aw + lda * k;
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) d += colj[i] * ck[i];
+        d = warp_sum(d);
+        if (lane == 0) w[k] = ck[j] + d;
+      }
+      __syncthreads();
+      const int ncol = R - j - 1;
+      const int64_t tot = (int64_t)ncol * (m - j);
+      for (int64_t e = tid; e < tot; e += nt) {
+        const int k = j + 1 + (int)(e / (m - j));
+        const int i = j + (int)(e % (m - j));
+        const double v = (i == j) ? 1.0 : colj[i];
+        Aw[i + lda * k] -= tj * w[k] * v;
+      }
+      __syncthreads();
+    }
+  }
+  // R factor with sign fix
+  for (int e = tid; e < R * R; e += nt) {
+    const int r = e % R, c = e / R;
+    double v = 0.0;
+    if (r < c) v = Aw[r + lda * c];
+    else if (r == c) v = beta[r];
+    if (beta[r] < 0.0) v = -v;
+    Rf[r + R * c] = v;
+  }
+  __syncthreads();
+  // explicit Q, dorg2r: j = R-1..0
+  for (int j = R - 1; j >= 0; --j) {
+    double* colj = Aw + lda * j;
+    const double tj = tau[j];
+    if (j < R - 1 && tj != 0.0) {
+      for (int k = j + 1 + wid; k < R; k += nw) {
+        const double* ck = Aw + lda * k;
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) d += colj[i] * ck[i];
+        d = warp_sum(d);
+        if (lane == 0) w[k] = ck[j] + d;  // v_j = 1
+      }
+      __syncthreads();
+      const int ncol = R - j - 1;
+      const int64_t tot = (int64_t)ncol * (m - j);
+      for (int64_t e = tid; e < tot; e += nt) {
+        const int k = j + 1 + (int)(e / (m - j));
+        const int i = j + (int)(e % (m - j));
+        const double v = (i == j) ? 1.0 : colj[i];
+        Aw[i + lda * k] -= tj * w[k] * v;
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < m; i += nt) {
+      if (i < j) colj[i] = 0.0;
+      else if (i == j) colj[i] = 1.0 - tj;
+      else colj[i] = -tj * colj[i];
+    }
+    __syncthreads();
+  }
+  // column sign fix of Q to match diag(R) >= 0
+  for (int64_t e = tid; e < (int64_t)m * R; e += nt) {
+    const int c = (int)(e / m);
+    if (beta[c] < 0.0) Aw[(e % m) + lda * c] = -Aw[(e % m) + lda * c];
+  }
+  __syncthreads();
+}
+
+// K1 standalone: Q (m x R, lda m) from A (copied into Q first), Rf (R x R).
+__global__ void __launch_bounds__(1024) k_factor_qr(const double* __restrict__ A, int m, int R, double* __restrict__ Q,
+                            double* __restrict__ Rf) {
+  __shared__ double tau[64], beta[64], w[64], red[32];
+  for (int64_t e = threadIdx.x; e < (int64_t)m * R; e += blockDim.x) Q[e] = A[e];
+  __syncthreads();
+  hh_qr_block(Q, m, m, R, Rf, tau, beta, w, red);
+}
+
+// ------------------------------------------------------------------ K2: structured QR of V_n
+// V_n = R_{k_{N-2}} (.) ... (.) R_{k_0} over the N-1 retained modes k_0 < ... < k_{N-2}; KB row
+// j = sum_m i_m R^m (i_0 fastest).  Row level = max_m i_m; column c is nonzero only on rows of
+// level <= c (the staircase).  Rows are processed in the order `perm` (sorted
+// by level, then KB index): column c occupies sorted rows [0, n_c), n_c = (c+1)^{N-1}, stored
+// packed at offset off_c.  Householder needs no fill-in and Q0 has the same
+// support.  One CTA; `work` is shared memory when the packed matrix fits, else global scratch.
+struct KrQrArgs {
+  const double* Rk[8];  // retained triangular factors, R x R column-major, ascending mode
+  int N1;               // N - 1
+  int R;
+  const int* perm;      // sorted position -> KB row (R^{N1})
+  double* Q0;           // out: dense R^{N1} x R, column-major, KB row order
+  double* R0;           // out: R x R column-major, diag >= 0
+  double* work_global;  // scratch (used when use_smem == 0)
+  int use_smem;
+  unsigned* flags;
+};
+
+__global__ void __launch_bounds__(1024) k_kr_qr(KrQrArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double tau[64], beta[64], w[64], red[32];
+  __shared__ int64_t off[65];
+  __shared__ int ncnt[64];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int R = a.R, N1 = a.N1;
+  if (tid == 0) {
+    int64_t o = 0;
+    for (int c = 0; c < R; ++c) {
+      int64_t p = 1;
+      for (int m = 0; m < N1; ++m) p *= (c + 1);
+      ncnt[c] = (int)p;
+      off[c] = o;
+      o += p;
+    }
+    off[R] = o;
+  }
+  __syncthreads();
+  double* V = a.use_smem ? sm : a.work_global;
+  // 1. form V_n (packed staircase)
+  for (int c = 0; c < R; ++c) {
+    for (int p = tid; p < ncnt[c]; p += nt) {
+      int j = a.perm[p];
+      double v = 1.0;
+      for (int m = 0; m < N1; ++m) {
+        const int im = j % R;
+        j /= R;
+        v *= a.Rk[m][im + R * c];
+      }
+      V[off[c] + p] = v;
+    }
+  }
+  __syncthreads();
+  // 2. Householder on the staircase
+  for (int j = 0; j < R; ++j) {
+    double* colj = V + off[j];
+    const int mj = ncnt[j];
+    double s = 0.0;
+    for (int i = j + 1 + tid; i < mj; i += nt) s += colj[i] * colj[i];
+    s = block_sum(s, red);
+    const double alpha = colj[j];
+    const double nrm = sqrt(alpha * alpha + s);
+    double tj, bj, scale;
+    if (s == 0.0) { tj = 0.0; bj = alpha; scale = 0.0; }
+    else { bj = (alpha >= 0.0) ? -nrm : nrm; tj = (bj - alpha) / bj; scale = 1.0 / (alpha - bj); }
+    __syncthreads();
+    if (tj != 0.0)
+      for (int i = j + 1 + tid; i < mj; i += nt) colj[i] *= scale;
+    if (tid == 0) { tau[j] = tj; beta[j] = bj; colj[j] = bj; }
+    __syncthreads();
+    if (tj != 0.0) {
+      for (int k = j + 1 + wid; k < R; k += nw) {
+        const double* ck = V + off[k];
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < mj; i += 32) d += colj[i] * ck[i];
+        d = warp_sum(d);
+        if (lane == 0) w[k] = ck[j] + d;
+      }
+      __syncthreads();
+      for (int k = j + 1; k < R; ++k) {
+        double* ck = V + off[k];
+        const double wk = tj * w[k];
+        for (int i = j + tid; i < mj; i += nt) ck[i] -= wk * ((i == j) ? 1.0 : colj[i]);
+      }
+      __syncthreads();
+    }
+  }
+  // 3. R0 (sign fixed)
+  for (int e = tid; e < R * R; e += nt) {
+    const int r = e % R, c = e / R;
+    double v = 0.0;
+    if (r < c) v = V[off[c] + r];
+    else if (r == c) v = beta[r];
+    if (beta[r] < 0.0) v = -v;
+    a.R0[r + R * c] = v;
+  }
+  if (tid == 0) {
+    double mx = 0.0, mn = 1e308;
+    for (int c = 0; c < R; ++c) { mx = fmax(mx, fabs(beta[c])); mn = fmin(mn, fabs(beta[c])); }
+    int64_t J = 1;
+    for (int m = 0; m < N1; ++m) J *= R;
+    if (mn <= (double)J * kEps * mx) atomicOr(a.flags, FLAG_ILLCOND_R0);
+  }
+  __syncthreads();
+  // 4. explicit Q0 in place (dorg2r on the staircase)
+  for (int j = R - 1; j >= 0; --j) {
+    double* colj = V + off[j];
+    const int mj = ncnt[j];
+    const double tj = tau[j];
+    if (j < R - 1 && tj != 0.0) {
+      for (int k = j + 1 + wid; k < R; k += nw) {
+        const double* ck = V + off[k];
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < mj; i += 32) d += colj[i] * ck[i];
+        d = warp_sum(d);
+        if (lane == 0) w[k] = ck[j] + d;
+      }
+      __syncthreads();
+      for (int k = j + 1; k < R; ++k) {
+        double* ck = V + off[k];
+        const double wk = tj * w[k];
+        for (int i = j + tid; i < mj; i += nt) ck[i] -= wk * ((i == j) ? 1.0 : colj[i]);
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < mj; i += nt) {
+      if (i < j) colj[i] = 0.0;
+      else if (i == j) colj[i] = 1.0 - tj;
+      else colj[i] = -tj * colj[i];
+    }
+    __syncthreads();
+  }
+  // 5. scatter to dense KB order with the column sign fix
+  int64_t J = 1;
+  for (int m = 0; m < N1; ++m) J *= R;
+  for (int64_t e = tid; e < J * R; e += nt) a.Q0[e] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < R; ++c) {
+    const double sg = (beta[c] < 0.0) ? -1.0 : 1.0;
+    for (int p = tid; p < ncnt[c]; p += nt) a.Q0[a.perm[p] + J * c] = sg * V[off[c] + p];
+  }
+}
+
+// ------------------------------------------------------------------------- K4: Q0 apply
+// Y column-major viewed as (Aa, In, Bb); Y_(n) column j = a + Aa b (Kolda-Bader).  Partial
+// W_part[ks](i, c) = sum_{j in chunk ks} Y_(n)(i, j) Q0(j, c), row-major (In x R); grid
+// (ceil(In/8), KS).  k_q0_reduce sums the KS partials in order.
+__global__ void __launch_bounds__(256)
+k_q0_apply(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb,
+           const double* __restrict__ Q0, int R, int jchunk, double* __restrict__ Wp) {
+  __shared__ double Ys[8][65];
+  __shared__ double Qs[64][65];
+  const int64_t J = Aa * Bb;
+  const int i0 = blockIdx.x * 8;
+  const int64_t jb = (int64_t)blockIdx.y * jchunk, je = min(J, jb + jchunk);
+  const int tid = threadIdx.x;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t j0 = jb; j0 < je; j0 += 64) {
+    for (int e = tid; e < 8 * 64; e += 256) {
+      const int ii = e / 64, jj = e % 64;
+      const int64_t j = j0 + jj;
+      const int i = i0 + ii;
+      double v = 0.0;
+      if (i < In && j < je) {
+        const int64_t b = j / Aa, aa = j - b * Aa;
+        v = Y[aa + Aa * i + Aa * (int64_t)In * b];
+      }
+      Ys[ii][jj] = v;
+    }
+    for (int e = tid; e < 64 * R; e += 256) {
+      const int jj = e % 64, c = e / 64;
+      const int64_t j = j0 + jj;
+      Qs[jj][c] = (j < je) ? Q0[j + J * c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int o = tid + 256 * q;
+      if (o < 8 * R) {
+        const int ii = o / R, c = o % R;
+        double s = acc[q];
+#pragma unroll 8
+        for (int jj = 0; jj < 64; ++jj) s = fma(Ys[ii][jj], Qs[jj][c], s);
+        acc[q] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int o = tid + 256 * q;
+    if (o < 8 * R) {
+      const int ii = o / R, c = o % R;
+      const int i = i0 + ii;
+      if (i < In) Wp[((int64_t)blockIdx.y * In + i) * R + c] = acc[q];
+    }
+  }
+}
+__global__ void k_q0_reduce(const double* __restrict__ Wp, int KS, int64_t n, double* __restrict__ W) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < KS; ++k) s += Wp[k * n + e];
+    W[e] = s;
+  }
+}
+
+// ------------------------------------------------------------- one-sided Jacobi SVD of R0
+// B = R0 V with orthogonal columns (cyclic round-robin pairs, one warp per pair); returns
+// M = U S^+ V^T = sum_{kept j} b_j v_j^T / sigma_j^2 in Ms (R x R, column-major) and the number
+// of truncated sigma_j (sigma_j <= tau * sigma_max, reading 15).  Bs, Vs: smem R x (R+1) col-major.
+__device__ int jacobi_pinv(const double* R0, int R, double tau, double* Bs, double* Vs, double* Ms,
+                           int* sflag) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int n = (R & 1) ? R + 1 : R;  // padded even count (dummy zero column)
+  for (int e = tid; e < R * n; e += blockDim.x) {
+    const int r = e % R, c = e / R;
+    Bs[e] = (c < R) ? R0[r + R * c] : 0.0;
+    Vs[e] = (c < R && r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) *sflag = 0;
+    __syncthreads();
+    for (int s = 0; s < n - 1; ++s) {
+      for (int k = wid; k < n / 2; k += nw) {
+        int p, q;
+        if (k == 0) { p = 0; q = 1 + s; }
+        else { p = 1 + (s + k) % (n - 1); q = 1 + (s - k + n - 1) % (n - 1); }
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        if (q >= R) continue;  // dummy column
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < R; r += 32) {
+          const double bp = Bs[r + R * p], bq = Bs[r + R * q];
+          al += bp * bp; be += bq * bq; ga += bp * bq;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (fabs(ga) > kEps * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+          for (int r = lane; r < R; r += 32) {
+            const double bp = Bs[r + R * p], bq = Bs[r + R * q];
+            Bs[r + R * p] = cs * bp - sn * bq;
+            Bs[r + R * q] = sn * bp + cs * bq;
+            const double vp = Vs[r + R * p], vq = Vs[r + R * q];
+            Vs[r + R * p] = cs * vp - sn * vq;
+            Vs[r + R * q] = sn * vp + cs * vq;
+          }
+          if (lane == 0) *sflag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int rot = *sflag;
+    __syncthreads();
+    if (!rot) break;
+  }
+  // sigma_j = ||b_j||; M = sum_kept b_j v_j^T / sigma_j^2
+  __shared__ double sig[64];
+  for (int c = wid; c < R; c += nw) {
+    double s = 0.0;
+    for (int r = lane; r < R; r += 32) s += Bs[r + R * c] * Bs[r + R * c];
+    s = warp_sum(s);
+    if (lane == 0) sig[c] = sqrt(s);
+  }
+  __syncthreads();
+  double smax = 0.0;
+  for (int c = 0; c < R; ++c) smax = fmax(smax, sig[c]);
+  int ntr = 0;
+  for (int c = 0; c < R; ++c) ntr += (sig[c] > tau * smax) ? 0 : 1;
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int r = e % R, c = e / R;  // M(r, c) = sum_j B(r, j) V(c, j) / sig_j^2
+    double s = 0.0;
+    for (int j = 0; j < R; ++j)
+      if (sig[j] > tau * smax) s += Bs[r + R * j] * Vs[c + R * j] / (sig[j] * sig[j]);
+    Ms[r + R * c] = s;
+  }
+  __syncthreads();
+  return ntr;
+}
+
+// ------------------------------------------------------------------ K5: per-mode tail (QR/SVD)
+struct TailArgs {
+  const double* W;   // In x R row-major (complete, all rows)
+  const double* R0;  // R x R column-major
+  int In, R;
+  int variant;       // 1 QR, 2 SVD
+  double tau;
+  double* Aw;        // scratch In x R column-major (becomes Q_n)
+  double* A;         // out: normalised factor, column-major
+  double* Rn;        // out: R_n (R x R)
+  double* lam;       // out: lambda
+  unsigned* flags;
+  int do_fit;
+  const double* nX2;
+  double* fit;       // out (when do_fit)
+  double* Ahat_fit;  // scratch In x R column-major for the fit (unnormalised Ahat)
+  int* ntrunc;       // optional out: number of truncated singular values
+};
+
+__global__ void __launch_bounds__(512) k_tail_qr(TailArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double tau[64], beta[64], w[64], red[32], lam[64];
+  __shared__ int sflag;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int R = a.R, In = a.In;
+  double* R0s = sm;               // R x R
+  double* Ms = sm + R * R;        // R x R (SVD pinv) or unused
+  double* Bs = Ms + R * R;        // R x (R+1)
+  double* Vs = Bs + R * (R + 1);  // R x (R+1)
+  for (int e = tid; e < R * R; e += nt) R0s[e] = a.R0[e];
+  __syncthreads();
+  // 1. solve: rows are independent
+  if (a.variant == 2) {
+    const int ntr = jacobi_pinv(R0s, R, a.tau, Bs, Vs, Ms, &sflag);
+    if (tid == 0 && ntr > 0) atomicOr(a.flags, FLAG_SVD_TRUNCATED);
+    if (tid == 0 && a.ntrunc) *a.ntrunc = ntr;
+    for (int i = tid; i < In; i += nt) {
+      const double* wr = a.W + (int64_t)i * R;
+      for (int c = 0; c < R; ++c) {
+        double s = 0.0;
+        for (int r = 0; r < R; ++r) s = fma(wr[r], Ms[r + R * c], s);
+        a.Aw[i + (int64_t)In * c] = s;
+      }
+    }
+  } else {
+    for (int i = tid; i < In; i += nt) {
+      const double* wr = a.W + (int64_t)i * R;
+      double x[64];
+      for (int j = R - 1; j >= 0; --j) {  // Ahat(i,j) = (W(i,j) - sum_{l>j} Ahat(i,l) R0(j,l)) / R0(j,j)
+        double acc = wr[j];
+        for (int l = j + 1; l < R; ++l) acc -= x[l] * R0s[j + R * l];
+        x[j] = acc / R0s[j + R * j];
+      }
+      for (int j = 0; j < R; ++j) a.Aw[i + (int64_t)In * j] = x[j];
+    }
+  }
+  __syncthreads();
+  // 2. lambda = column 2-norms (one warp per column, fixed order); non-finite check
+  for (int c = wid; c < R; c += nw) {
+    const double* col = a.Aw + (int64_t)In * c;
+    double s = 0.0;
+    for (int i = lane; i < In; i += 32) s += col[i] * col[i];
+    s = warp_sum(s);
+    if (lane == 0) lam[c] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int c = 0; c < R; ++c)
+      if (!isfinite(lam[c])) atomicOr(a.flags, FLAG_NONFINITE);
+  }
+  // keep Ahat for the fit, normalise (zero column -> e_1, reading 10)
+  for (int64_t e = tid; e < (int64_t)In * R; e += nt) {
+    const int c = (int)(e / In), i = (int)(e % In);
+    const double v = a.Aw[e];
+    if (a.do_fit) a.Ahat_fit[e] = v;
+    const double nv = (lam[c] > 0.0) ? v / lam[c] : (i == 0 ? 1.0 : 0.0);
+    a.Aw[e] = nv;
+    a.A[e] = nv;
+  }
+  if (tid < R) a.lam[tid] = lam[tid];
+  __syncthreads();
+  // 3. factor QR (Alg. 2 line 12) in place: Aw -> Q_n, R_n
+  hh_qr_block(a.Aw, In, In, R, a.Rn, tau, beta, w, red);
+  // 4. fast fit after mode N
+  if (a.do_fit) {
+    // inner = <W, Ahat R0^T> = sum_i sum_c W(i,c) sum_l Ahat(i,l) R0(c,l)
+    double s = 0.0;
+    for (int i = tid; i < In; i += nt) {
+      const double* wr = a.W + (int64_t)i * R;
+      for (int c = 0; c < R; ++c) {
+        double t = 0.0;
+        for (int l = c; l < R; ++l) t = fma(a.Ahat_fit[i + (int64_t)In * l], R0s[c + R * l], t);
+        s = fma(wr[c], t, s);
+      }
+    }
+    const double inner = block_sum(s, red);
+    // ||Xh||^2 = <R0^T R0, diag(lam) R_n^T R_n diag(lam)>
+    double q = 0.0;
+    for (int e = tid; e < R * R; e += nt) {
+      const int x = e % R, y = e / R;
+      double g0 = 0.0, g1 = 0.0;
+      for (int k = 0; k < R; ++k) {
+        g0 = fma(R0s[k + R * x], R0s[k + R * y], g0);
+        g1 = fma(a.Rn[k + R * x], a.Rn[k + R * y], g1);
+      }
+      q = fma(g0, lam[x] * lam[y] * g1, q);
+    }
+    const double nxh2 = block_sum(q, red);
+    if (tid == 0) {
+      const double nx2 = *a.nX2;
+      const double res2 = fmax(0.0, nx2 - 2.0 * inner + nxh2);
+      *a.fit = 1.0 - sqrt(res2) / sqrt(nx2);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------- K7: CP-ALS (NE)
+// out(idx) = sum_i T(... i@k ...) A_k(i, r) with r the index of mode rm (size R) of T:
+// the Khatri-Rao-diagonal contraction that finishes an MTTKRP after its first (dense) TTM.
+struct DiagArgs {
+  const double* T;
+  int nd;
+  int64_t dims[8];
+  int k, rm;
+  const double* Ak;
+  int64_t lda;
+  double* out;  // dims without mode k, column-major
+};
+__global__ void k_diag_contract(DiagArgs a) {
+  int64_t tot = 1;
+  for (int d = 0; d < a.nd; ++d) if (d != a.k) tot *= a.dims[d];
+  int64_t stride_k = 1;
+  for (int d = 0; d < a.k; ++d) stride_k *= a.dims[d];
+  const int64_t Ik = a.dims[a.k];
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < tot; o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = o, base = 0, st = 1;
+    int r = 0;
+    for (int d = 0; d < a.nd; ++d) {
+      if (d == a.k) { st *= a.dims[d]; continue; }
+      const int64_t id = rem % a.dims[d];
+      rem /= a.dims[d];
+      base += id * st;
+      if (d == a.rm) r = (int)id;
+      st *= a.dims[d];
+    }
+    double s = 0.0;
+    for (int64_t i = 0; i < Ik; ++i) s = fma(a.T[base + i * stride_k], a.Ak[i + a.lda * r], s);
+    a.out[o] = s;
+  }
+}
+
+// NE tail: S = Hadamard of the other Grams; Ahat S = M by Cholesky (LU with partial pivoting on a
+// non-positive pivot, reading 18); normalise; G_n = A_n^T A_n; fast fit.
+struct TailNeArgs {
+  const double* M;        // In x R, layout given by m_rowmajor
+  int m_rowmajor;
+  const double* G[8];     // Grams (R x R), index k; G[n] ignored
+  int N, n, In, R;
+  double* A;              // out: normalised factor (column-major)
+  double* Gn;             // out: new Gram of mode n
+  double* lam;
+  unsigned* flags;
+  int do_fit;
+  const double* nX2;
+  double* fit;
+  double* Ahat;           // scratch In x R column-major
+};
+__global__ void __launch_bounds__(512) k_tail_ne(TailNeArgs a) {
+  extern __shared__ double smne[];
+  double* S = smne;                 // R x R
+  double* L = smne + a.R * a.R;     // R x R
+  __shared__ double red[32], lam[64];
+  __shared__ int piv[64];
+  __shared__ int use_lu;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int R = a.R, In = a.In;
+  for (int e = tid; e < R * R; e += nt) {
+    double v = 1.0;
+    for (int k = a.N - 1; k >= 0; --k)
+      if (k != a.n) v *= a.G[k][e];
+    S[e] = v;
+    L[e] = v;
+  }
+  if (tid == 0) use_lu = 0;
+  __syncthreads();
+  // Cholesky S = L L^T (lower, column-major in L), by warp 0
+  if (wid == 0) {
+    for (int j = 0; j < R; ++j) {
+      double d = L[j + R * j];
+      for (int k = 0; k < j; ++k) d -= L[j + R * k] * L[j + R * k];
+      if (!(d > 0.0)) { if (lane == 0) use_lu = 1; break; }
+      d = sqrt(d);
+      for (int i = j + 1 + lane; i < R; i += 32) {
+        double v = L[i + R * j];
+        for (int k = 0; k < j; ++k) v -= L[i + R * k] * L[j + R * k];
+        L[i + R * j] = v / d;
+      }
+      __syncwarp();
+      if (lane == 0) L[j + R * j] = d;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (use_lu) {
+    if (tid == 0) {
+      atomicOr(a.flags, FLAG_NE_CHOL_FALLBACK);
+      for (int e = 0; e < R * R; ++e) L[e] = S[e];
+      for (int j = 0; j < R; ++j) {  // LU with partial pivoting, L and U packed in L
+        int p = j;
+        for (int i = j + 1; i < R; ++i) if (fabs(L[i + R * j]) > fabs(L[p + R * j])) p = i;
+        piv[j] = p;
+        if (p != j) for (int c = 0; c < R; ++c) { double t = L[j + R * c]; L[j + R * c] = L[p + R * c]; L[p + R * c] = t; }
+        for (int i = j + 1; i < R; ++i) {
+          L[i + R * j] /= L[j + R * j];
+          for (int c = j + 1; c < R; ++c) L[i + R * c] -= L[i + R * j] * L[j + R * c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // rows: solve S x = m (S symmetric, so Ahat(i,:) S = M(i,:) <=> S Ahat(i,:)^T = M(i,:)^T)
+  for (int i = tid; i < In; i += nt) {
+    double x[64];
+    for (int c = 0; c < R; ++c) x[c] = a.m_rowmajor ? a.M[(int64_t)i * R + c] : a.M[i + (int64_t)In * c];
+    if (!use_lu) {
+      for (int j = 0; j < R; ++j) { double v = x[j]; for (int k = 0; k < j; ++k) v -= L[j + R * k] * x[k]; x[j] = v / L[j + R * j]; }
+      for (int j = R - 1; j >= 0; --j) { double v = x[j]; for (int k = j + 1; k < R; ++k) v -= L[k + R * j] * x[k]; x[j] = v / L[j + R * j]; }
+    } else {
+      for (int j = 0; j < R; ++j) { const int p = piv[j]; if (p != j) { double t = x[j]; x[j] = x[p]; x[p] = t; } }
+      for (int j = 0; j < R; ++j) { double v = x[j]; for (int k = 0; k < j; ++k) v -= L[j + R * k] * x[k]; x[j] = v; }
+      for (int j = R - 1; j >= 0; --j) { double v = x[j]; for (int k = j + 1; k < R; ++k) v -= L[j + R * k] * x[k]; x[j] = v / L[j + R * j]; }
+    }
+    for (int c = 0; c < R; ++c) a.Ahat[i + (int64_t)In * c] = x[c];
+  }
+  __syncthreads();
+  for (int c = wid; c < R; c += nw) {
+    const double* col = a.Ahat + (int64_t)In * c;
+    double s = 0.0;
+    for (int i = lane; i < In; i += 32) s += col[i] * col[i];
+    s = warp_sum(s);
+    if (lane == 0) lam[c] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < R; ++c) if (!isfinite(lam[c])) atomicOr(a.flags, FLAG_NONFINITE);
+  for (int64_t e = tid; e < (int64_t)In * R; e += nt) {
+    const int c = (int)(e / In), i = (int)(e % In);
+    a.A[e] = (lam[c] > 0.0) ? a.Ahat[e] / lam[c] : (i == 0 ? 1.0 : 0.0);
+  }
+  if (tid < R) a.lam[tid] = lam[tid];
+  __syncthreads();
+  // G_n = A_n^T A_n (warp per entry, fixed order)
+  for (int e = wid; e < R * R; e += nw) {
+    const int x = e % R, y = e / R;
+    const double* cx = a.A + (int64_t)In * x;
+    const double* cy = a.A + (int64_t)In * y;
+    double s = 0.0;
+    for (int i = lane; i < In; i += 32) s += cx[i] * cy[i];
+    s = warp_sum(s);
+    if (lane == 0) a.Gn[e] = s;
+  }
+  __syncthreads();
+  if (a.do_fit) {
+    double s = 0.0;  // <M_N, Ahat_N>
+    for (int64_t e = tid; e < (int64_t)In * R; e += nt) {
+      const int c = (int)(e / In), i = (int)(e % In);
+      const double m = a.m_rowmajor ? a.M[(int64_t)i * R + c] : a.M[e];
+      s = fma(m, a.Ahat[e], s);
+    }
+    const double inner = block_sum(s, red);
+    double q = 0.0;  // <S_N, diag(lam) G_N diag(lam)>
+    for (int e = tid; e < R * R; e += nt) q += S[e] * lam[e % R] * lam[e / R] * a.Gn[e];
+    const double nxh2 = block_sum(q, red);
+    if (tid == 0) {
+      const double nx2 = *a.nX2;
+      *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner + nxh2)) / sqrt(nx2);
+    }
+  }
+}
+
+// Gram G = A^T A (warp per entry) for set_factors in the NE variant.
+__global__ void __launch_bounds__(1024) k_gram(const double* __restrict__ A, int In, int R, double* __restrict__ G) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = wid; e < R * R; e += nw) {
+    const int x = e % R, y = e / R;
+    double s = 0.0;
+    for (int i = lane; i < In; i += 32) s += A[i + (int64_t)In * x] * A[i + (int64_t)In * y];
+    s = warp_sum(s);
+    if (lane == 0) G[e] = s;
+  }
+}
+
+// Direct residual ||X - Xh||^2: Xh(i) = sum_r lam_r prod_k A_k(i_k, r), over the
+// local slab (last-mode offset `off`).  Deterministic block partials.
+struct ResidArgs {
+  const double* X;
+  int64_t n;           // local numel
+  int N;
+  int64_t dims[8];     // local dims
+  int64_t off_last;    // global offset of the slab on the last mode
+  const double* A[8];  // global factors (column-major, lda = global I_k)
+  int64_t lda[8];
+  const double* lam;
+  int R;
+  double* part;
+};
+__global__ void k_resid_partial(ResidArgs a) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx[8];
+    int64_t rem = e;
+    for (int k = 0; k < a.N; ++k) { idx[k] = rem % a.dims[k]; rem /= a.dims[k]; }
+    idx[a.N - 1] += a.off_last;
+    double xh = 0.0;
+    for (int r = 0; r < a.R; ++r) {
+      double p = a.lam[r];
+      for (int k = 0; k < a.N; ++k) p *= a.A[k][idx[k] + a.lda[k] * r];
+      xh += p;
+    }
+    const double d = a.X[e] - xh;
+    s = fma(d, d, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = s;
+}
+__global__ void k_fit_from_resid(const double* res2, const double* nX2, double* fit) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *fit = 1.0 - sqrt(fmax(0.0, *res2)) / sqrt(*nX2);
+}
+
+}  // namespace cpqr

@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star / SURVEY.md §8(c)): Y relative Frobenius <= 1e-11; factors and lambda
+after one sweep <= 1e-9; fit within 1e-8.  Small shapes span several tiles and ragged tails
+(odd sizes disable the 16-byte load path, exercising the scalar kernels too)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2112_10855_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def cp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2112_10855_b200 import cpqr
+    return cpqr
+
+
+SHAPES = [
+    ((30, 40, 50), 5),        # C1 shape
+    ((37, 29, 43), 7),        # odd sizes: scalar (non-VEC) kernels, ragged tiles
+    ((64, 48, 40), 16),       # R = 16
+    ((70, 66, 34), 32),       # R = 32 (4 M/N tiles), ragged fibres
+    ((12, 10, 9, 11), 6),     # N = 4
+    ((6, 7, 5, 6, 8), 3),     # N = 5
+    ((60, 40), 5),            # N = 2
+]
+
+
+@pytest.mark.parametrize("dims,R", SHAPES)
+def test_debug_mode_Y_Q0_W(cp, dims, R):
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=101 + len(dims) + R)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    N = len(dims)
+    Qs, Rs = [None] * N, [None] * N
+    for k in range(N):
+        Qs[k], Rs[k] = O.qr_pos(init[k])
+    for n in range(N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+        Q0o, R0o = O.structured_qr(Rs, n)
+        assert rel(out["R0"], R0o) <= 1e-11
+        assert rel(out["Q0"], Q0o) <= 1e-11
+        Wo = O.apply_q0(Yo, n, Q0o)
+        assert rel(out["W"], Wo) <= 1e-11
+    s.close()
+
+
+@pytest.mark.parametrize("m,R", [(50, 5), (1000, 32), (37, 7), (128, 16)])
+def test_factor_qr(cp, m, R):
+    A = np.random.default_rng(m + R).standard_normal((m, R))
+    s = cp.CPQR((m, m), R, "QR")
+    Q, Rf = s.debug_qr(A)
+    Qo, Ro = O.qr_pos(A)
+    assert rel(Rf, Ro) <= 1e-13 and rel(Q, Qo) <= 1e-12
+    assert np.all(np.diag(Rf) >= 0)
+    s.close()
+
+
+def test_svd_solve_truncation_and_agreement(cp):
+    rng = np.random.default_rng(5)
+    R = 8
+    R0 = np.triu(rng.standard_normal((R, R))) + 4 * np.eye(R)
+    W = rng.standard_normal((40, R))
+    s = cp.CPQR((40, 40), R, "SVD")
+    out, nt = s.debug_svd_solve(R0, W, 0.0)
+    ref, _ = O.solve_svd(R0, W, 0.0)
+    assert nt == 0 and rel(out, ref) <= 1e-12
+    R0[5, 5] = 1e-17 * abs(R0).max()
+    R0[5, 6:] = 0.0
+    out, nt = s.debug_svd_solve(R0, W, 1e-12)
+    ref, ntr = O.solve_svd(R0, W, 1e-12)
+    assert nt == ntr == 1 and rel(out, ref) <= 1e-10
+    s.close()
+
+
+@pytest.mark.parametrize("dims,R,variant", [
+    ((30, 40, 50), 5, "QR"), ((37, 29, 43), 7, "SVD"), ((30, 40, 50), 5, "NE"),
+    ((12, 10, 9, 11), 6, "QR"), ((6, 7, 5, 6, 8), 3, "SVD"), ((70, 66, 34), 32, "QR"), ((60, 40), 5, "QR"),
+    ((21, 19, 17), 4, "NE"),
+])
+def test_sweeps_match_oracle(cp, dims, R, variant):
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=7 + R, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    fits = s.sweep(1)
+    lam, A = s.get_factors()
+    ref = O.cp_als_ne(X, init, 1) if variant == "NE" else O.cp_als_qr(X, init, 1, variant=variant)
+    for k in range(len(dims)):
+        assert rel(A[k], ref["factors"][k]) <= 1e-9, (k, rel(A[k], ref["factors"][k]))
+    assert rel(lam, ref["lam"]) <= 1e-9
+    assert abs(fits[0] - ref["fits"][0]) <= 1e-8
+    more = s.sweep(4)
+    ref5 = O.cp_als_ne(X, init, 5) if variant == "NE" else O.cp_als_qr(X, init, 5, variant=variant)
+    assert np.max(np.abs(more - np.array(ref5["fits"][1:]))) <= 1e-8
+    s.close()
+
+
+def test_graph_and_eager_paths_agree_bitwise(cp):
+    dims, R = (30, 40, 50), 5
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=3)
+    outs = []
+    for g in (True, False):
+        s = cp.CPQR(dims, R, "QR", use_graph=g)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        f = s.sweep(3)
+        outs.append((f, s.get_factors()))
+        s.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    for a, b in zip(outs[0][1][1], outs[1][1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_direct_fit_and_torch_borrow(cp):
+    import torch
+    dims, R = (30, 40, 50), 5
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=8, eta=0.0)
+    s = cp.CPQR(dims, R, "QR", fit_mode="direct")
+    Xt = torch.from_numpy(Xc).cuda()
+    s.set_tensor(Xt)  # borrowed device pointer
+    s.set_factors(truth)
+    f = s.sweep(1)
+    assert 1.0 - f[0] <= 1e-13
+    s.close()
+
+
+def test_errors_are_reported(cp):
+    with pytest.raises(cp.CpqrError):
+        cp.CPQR((4, 4, 4), 8, "QR")          # wide factors (reading 27)
+    s = cp.CPQR((10, 10, 10), 2, "QR")
+    with pytest.raises(cp.CpqrError) as e:
+        s.sweep(1)                           # no tensor yet
+    assert e.value.status == 5
+    s.close()
