@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark: CP-ALS-QR sweeps/s and Multi-TTM HBM GB/s (fp64) on 1..8 B200 (BASELINE.json metric).
+
+A "step" is one CP-ALS-QR sweep (Alg. 2 lines 5-13): all N mode updates over
+the whole (slab of the) tensor, i.e. every row of SURVEY.md §8(a).  Default workload: C5
+(1000^3, R = 32, QR variant, 8 GB fp64), sharded in 1000/p slabs on mode 3; --config selects
+another BASELINE config.  Inputs are the seeded synthetic tensors of synth.py (DESIGN.md
+§Inputs); X (8 GB) is far larger than the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--variant QR]
+  python bench.py --impl reference ...     # the CPU oracle (oracle/) on the host cores
+
+Multi-GPU: launched by torch.distributed.run, one process per GPU; the NCCL id is broadcast
+over a gloo group; timing = CUDA events on the stream the library runs on, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2112_10855_b200 import synth  # noqa: E402
+
+P64_DMMA_TFLOPS = 37.08        # measured, profiles/ubench_r01.log (mma.sync m8n8k4 f64, 148 SMs)
+HBM_READ_GBS = 7243.3          # measured read-only stream, profiles/ubench_r01.log
+
+
+def peaks():
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(m["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def load_input(conf, rank, world):
+    """Full X on the host (cached .npy, memory-mapped) and this rank's contiguous slab."""
+    cdir = synth._cache_dir()
+    if world > 1:
+        import torch.distributed as dist
+        if rank == 0:
+            synth.make_problem(conf.cfg)  # generate + cache once
+        dist.barrier()
+    conf, Xc, truth, init = synth.make_problem(conf.cfg)
+    per = conf.dims[-1] // world
+    slab = Xc[rank * per:(rank + 1) * per]
+    return conf, Xc, slab, truth, init, cdir
+
+
+def cpu_baseline(conf, Xc, init, variant, sweeps=2):
+    """The oracle as it stands, on this host's cores, on a bounded sample (`sweeps` full sweeps)."""
+    import oracle as O
+    X = O.as_tensor(Xc)
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    if variant == "NE":
+        O.cp_als_ne(X, init, sweeps)
+    else:
+        O.cp_als_qr(X, init, sweeps, variant=variant, tau=conf.svd_tau)
+    dt = time.perf_counter() - t0
+    return {"value": sweeps / dt, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+            "sample": f"{sweeps} full CP-ALS-{variant} sweeps of {conf.name} from the shared init, "
+                      f"numpy/OpenBLAS fp64, wall clock"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    conf = synth.CONFIGS[args.config]
+    variant = args.variant or conf.variants[0]
+    conf, Xc, truth, init = synth.make_problem(conf.cfg)
+    import oracle as O
+    X = O.as_tensor(Xc)
+    cores = len(os.sched_getaffinity(0))
+    run = (lambda A0, s: O.cp_als_ne(X, A0, s)) if variant == "NE" else \
+        (lambda A0, s: O.cp_als_qr(X, A0, s, variant=variant, tau=conf.svd_tau))
+    state = run(init, max(1, args.warmup))   # warm-up sweeps (untimed)
+    A0 = state["factors"]
+    t0 = time.perf_counter()
+    run(A0, args.steps)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": "CP-ALS-QR sweeps/s (fp64)", "value": v, "unit": "sweeps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synth.py recipe, seeded)",
+            "config": {"workload": conf.name, "variant": variant, "dims": list(conf.dims), "R": conf.R,
+                       "sweeps_per_step": 1, "parallelism": "host cores"},
+            "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} full sweeps of {conf.name} after {args.warmup} warm-up"},
+            "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("--impl", default="cpqr", choices=["cpqr", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    from paper_2112_10855_b200 import cpqr
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        obj = [cpqr.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    conf = synth.CONFIGS[args.config]
+    variant = args.variant or conf.variants[0]
+    conf, Xc, slab, truth, init, _ = load_input(conf, rank, world)
+
+    stream = torch.cuda.current_stream()
+    s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
+                  rank=rank, world=world, nccl_id=nccl_id)
+    Xd = torch.from_numpy(np.ascontiguousarray(slab)).to(f"cuda:{local}")
+    s.set_tensor(Xd)                         # device-resident input (borrowed)
+    s.set_factors(init)
+    s.sweep(args.warmup)                     # warm-up (also captures the CUDA graph)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = s.profile(reset=False)["launches_total"]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        s.sweep(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = s.profile(reset=False)["launches_total"] - launches0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sweeps_s = args.steps / (ms / 1e3)
+
+    # phase profile (separate short run; events around each phase on the library stream)
+    sp = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
+                   rank=rank, world=world, nccl_id=nccl_id, profile=True, use_graph=False) if world == 1 else None
+    prof = None
+    if sp is not None:
+        sp.set_tensor(Xd)
+        sp.set_factors(init)
+        sp.sweep(1)
+        sp.profile(reset=True)
+        nprof = 2
+        sp.sweep(nprof)
+        prof = sp.profile(reset=True)
+        prof["sweeps"] = nprof
+        sp.close()
+
+    # end-to-end through the public API with HOST buffers: H2D of X (pinned), set_factors,
+    # the config's sweep count, D2H of factors + fits -- per step = one solve
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(np.ascontiguousarray(slab)).pin_memory()
+        se = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
+                       rank=rank, world=world, nccl_id=nccl_id)
+        se.set_tensor(Xh)
+        se.set_factors(init)
+        se.sweep(1)
+        barrier()
+        torch.cuda.synchronize()
+        nrep = 2
+        t0 = time.perf_counter()
+        f1 = f2 = None
+        for _ in range(nrep):
+            se.set_tensor(Xh)
+            se.set_factors(init)
+            fits = se.sweep(conf.sweeps)
+            lam, A = se.get_factors()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        barrier()
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([dt], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = Xh.numel() * 8 + sum(int(np.prod(a.shape)) * 8 for a in init)
+        d2h = sum(int(np.prod(a.shape)) * 8 for a in A) + conf.R * 8 + conf.sweeps * 8
+        e2e = {"value": nrep * conf.sweeps / dt, "unit": "sweeps/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "step": f"one solve through the C-ABI from host buffers: H2D X slab (pinned) + set_factors + "
+                       f"{conf.sweeps} sweeps + D2H factors/fits; wall clock, max over ranks"}
+        se.close()
+    s.close()
+
+    if rank != 0:
+        return 0
+    hbm_peak, hbm_src = peaks()
+    numel_local = int(np.prod(conf.dims)) // world
+    mt_bytes_sweep = conf.N * 8.0 * numel_local           # X read once per mode
+    line = {
+        "metric": "CP-ALS-QR sweeps/s & Multi-TTM HBM GB/s (fp64)",
+        "value": sweeps_s * 1.0, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (synth.py seeded recipe of BASELINE.json config; no dataset)",
+        "config": {"workload": conf.name, "variant": variant, "dims": list(conf.dims), "R": conf.R,
+                   "global_batch": 1, "parallelism": f"slab-dp{world} on mode {conf.N}",
+                   "l2": "inputs larger than L2 (X = %.2f GB/GPU vs 126 MB L2)" % (8.0 * numel_local / 1e9)},
+        "gpu_launches": int(launches),
+    }
+    if prof:
+        nsw = prof["sweeps"]
+        n_launch0 = conf.N * nsw
+        t0_avg_ms = prof["ms"][0] / n_launch0
+        bytes_launch = prof["bytes0"] / conf.N
+        flops_launch = prof["flops0"] / conf.N
+        gbs = bytes_launch / (t0_avg_ms / 1e3) / 1e9
+        tfl = flops_launch / (t0_avg_ms / 1e3) / 1e12
+        t_hbm, t_fp = bytes_launch / (hbm_peak * 1e9), flops_launch / (P64_DMMA_TFLOPS * 1e12)
+        if t_fp > t_hbm:
+            roof = {"bound": "tensor", "achieved": tfl, "peak": P64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                    "frac": tfl / P64_DMMA_TFLOPS, "peak_source": "measured FP64 DMMA (profiles/ubench_r01.log)"}
+        else:
+            roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                    "peak_source": hbm_src}
+        roof["kernel"] = "Multi-TTM stream-X pass (k_ttm_strided / k_mttm_slice), avg over %d launches" % n_launch0
+        roof["traffic"] = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            roof["traffic"] = json.load(open(tfile)).get(conf.name)
+        roof["hbm_gbs"] = gbs
+        roof["hbm_frac"] = gbs / hbm_peak
+        roof["fp64_tflops"] = tfl
+        roof["roofline_frac"] = max(t_hbm, t_fp) / (t0_avg_ms / 1e3)
+        line["roofline"] = roof
+        line["multi_ttm_gbs"] = mt_bytes_sweep / ((prof["ms"][0] + prof["ms"][1]) / nsw / 1e3) / 1e9
+        line["phase_ms_per_sweep"] = {k: v / nsw for k, v in zip(
+            ["stream_pass", "rest_ttm", "factor_qr", "q0_compute", "q0_apply", "other"], prof["ms"])}
+    line["clocks"] = clk.summary()
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(conf, Xc, init, variant)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
