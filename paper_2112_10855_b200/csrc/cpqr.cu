@@ -3,8 +3,10 @@
 // Alg. 1 lines 6-11 for CP-ALS.  See DESIGN.md for the kernel map.
 #include "../../include/cpqr.h"
 #include "small_kernels.cuh"
+#include "tma_kernels.cuh"
 #include "ttm_kernels.cuh"
 
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -26,7 +28,12 @@ constexpr int kMaxR = 32;
 constexpr size_t kQSmemMax = 96 * 1024;  // Q panel budget per CTA (2 CTAs / SM)
 
 struct TtmStep {
-  int kind;  // 0 strided, 1 fiber, 2 slice
+  int kind;  // 0 strided, 1 fiber, 2 slice, 3 slice-reduce, 4 strided TMA, 5 fiber TMA, 6 slice TMA, 7 slice fix-up
+  alignas(64) CUtensorMap mx;
+  alignas(64) CUtensorMap mq;
+  int S = 0, nslots = 1, nfb = 1;
+  int64_t G = 1;
+  double* P = nullptr;
   const double* in;
   double* out;
   int64_t A, B, F, L;
@@ -77,6 +84,9 @@ struct cpqr_ctx {
   size_t Xown_elems = 0;
   bool have_tensor = false, have_factors = false;
   double *dA[kMaxN] = {0}, *dQ[kMaxN] = {0}, *dRk[kMaxN] = {0}, *dG[kMaxN] = {0};
+  double *dQt[kMaxN] = {0}, *dAt[kMaxN] = {0};  // transposed, zero-padded (I_k x RQ) TMA panels
+  int RQ = 16;
+  bool use_tma = true;
   double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWloc = nullptr,
          *dWp = nullptr, *dAhat = nullptr;
   double* buf[2] = {nullptr, nullptr};
@@ -249,16 +259,64 @@ struct PlanIn {
   const double* X;
   const int64_t* ld;  // local dims
   int N, R, n;
-  const double* Q[kMaxN];  // per-mode operand (Q_k for QR, A_k for NE); mode N-1 already slab-offset
+  const double* Q[kMaxN];   // per-mode operand (Q_k for QR, A_k for NE); mode N-1 already slab-offset
   int64_t ldq[kMaxN];
+  const double* Qt[kMaxN];  // transposed padded panels (TMA), slab-offset for mode N-1
+  int RQ;
   bool ne;
+  bool tma;
   int sms;
 };
 
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// fp64 tiled map, SWIZZLE_128B (inner box = 16 doubles = 128 B), zero OOB fill.
+bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+               const uint32_t* box) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if (((uintptr_t)base & 15) != 0) return false;
+  for (int i = 0; i < rank - 1; ++i)
+    if (strides_bytes[i] % 16 != 0 || strides_bytes[i] >= (1ull << 40)) return false;
+  for (int i = 0; i < rank; ++i)
+    if (dims[i] == 0 || dims[i] >= (1ull << 31)) return false;
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void*>(base),
+                   (const cuuint64_t*)dims, (const cuuint64_t*)strides_bytes, (const cuuint32_t*)box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+constexpr size_t kSmemOptin = 227 * 1024;
+
+int stages_for(size_t stage, size_t extra) {
+  const size_t avail = kSmemOptin - 1024 - 2048 - extra;
+  return (int)std::min<size_t>(8, avail / stage);
+}
+
+// Multi-TTM Y = X x_{k != n} Q_k^T (Alg. 2 line 8).  Stream-X pass: modes 1 and 2 together
+// (fused slice kernel) when n >= 3, else the last mode (strided kernel, the largest contiguous
+// GEMM); the remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
+// (ties by decreasing mode, reading 5).  TMA kernels whenever the layout allows
+// (even leading dimension, 16-B aligned base), else the register-staged kernels.
 void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   p.steps.clear();
   p.diags.clear();
   const int N = in.N, R = in.R, n = in.n;
+  const int NT = (R + 7) / 8, NQB = (NT + 1) / 2;
   int64_t cur[kMaxN];
   for (int k = 0; k < N; ++k) cur[k] = in.ld[k];
   const double* src = in.X;
@@ -266,6 +324,12 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   p.max_buf = 0;
   p.part = 0;
   std::vector<int> todo;
+  auto qmap = [&](TtmStep& s, int k, int64_t I) {
+    const uint64_t d[2] = {(uint64_t)in.RQ, (uint64_t)I};
+    const uint64_t st[1] = {(uint64_t)in.RQ * 8};
+    const uint32_t box[2] = {16, 16};
+    return in.Qt[k] && make_tmap(&s.mq, in.Qt[k], 2, d, st, box);
+  };
   auto emit_ttm = [&](int k) {
     TtmStep s{};
     s.in = src;
@@ -276,11 +340,29 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       s.kind = 1;
       s.I = (int)cur[0];
       s.F = prod(cur, 1, N);
+      if (in.tma && s.I % 2 == 0 && s.F < (1ll << 31) && bufs[0]) {
+        const uint64_t d[2] = {(uint64_t)s.I, (uint64_t)s.F};
+        const uint64_t st[1] = {(uint64_t)s.I * 8};
+        const uint32_t box[2] = {16, 128};
+        if (make_tmap(&s.mx, src, 2, d, st, box) && qmap(s, k, s.I)) {
+          s.kind = 5;
+          s.S = stages_for(128 * 128 + NQB * kBoxBytes, 0);
+        }
+      }
     } else {
       s.kind = 0;
       s.A = prod(cur, 0, k);
       s.I = (int)cur[k];
       s.B = prod(cur, k + 1, N);
+      if (in.tma && s.A % 2 == 0 && s.A < (1ll << 31) && s.B < (1ll << 31) && bufs[0]) {
+        const uint64_t d[3] = {(uint64_t)s.A, (uint64_t)s.I, (uint64_t)s.B};
+        const uint64_t st[2] = {(uint64_t)s.A * 8, (uint64_t)s.A * s.I * 8};
+        const uint32_t box[3] = {16, 16, 1};
+        if (make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, k, s.I)) {
+          s.kind = 4;
+          s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0);
+        }
+      }
     }
     cur[k] = R;
     p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
@@ -290,19 +372,19 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   };
   if (in.ne) {
     // MTTKRP M_n = X_(n) Z_n: one dense TTM with A_k, then Khatri-Rao-diagonal contractions.
-    int rm;
-    if (n >= 1) { emit_ttm(0); rm = 0; }
-    else { emit_ttm(N - 1); rm = N - 1; }
+    const int rmode = (n >= 1) ? 0 : N - 1;
+    emit_ttm(rmode);
     int nd = N;
     int64_t dd[kMaxN];
     int orig[kMaxN];
     for (int k = 0; k < N; ++k) { dd[k] = cur[k]; orig[k] = k; }
     for (int k = N - 1; k >= 0; --k) {
-      if (k == n || k == (n >= 1 ? 0 : N - 1)) continue;
-      int pos = -1;
-      for (int d = 0; d < nd; ++d) if (orig[d] == k) pos = d;
-      int rpos = -1;
-      for (int d = 0; d < nd; ++d) if (orig[d] == (n >= 1 ? 0 : N - 1)) rpos = d;
+      if (k == n || k == rmode) continue;
+      int pos = -1, rpos = -1;
+      for (int d = 0; d < nd; ++d) {
+        if (orig[d] == k) pos = d;
+        if (orig[d] == rmode) rpos = d;
+      }
       DiagStep ds{};
       ds.in = src;
       ds.out = bufs[nb];
@@ -318,12 +400,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       src = bufs[nb];
       nb ^= 1;
     }
-    (void)rm;
     p.Y = src;
     p.nd = nd;
     for (int d = 0; d < nd; ++d) p.ydims[d] = dd[d];
-    p.m_rowmajor = (n >= 1) ? 1 : 0;  // (R, I_n) col-major == row-major I_n x R
-    if (N == 2) p.m_rowmajor = (n == 1) ? 1 : 0;
+    p.m_rowmajor = (n >= 1) ? 1 : 0;  // (R, I_n) column-major == row-major I_n x R
     return;
   }
   if (N >= 3 && n >= 2) {
@@ -337,31 +417,62 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     s.ldq = in.ldq[0];
     s.Q2 = in.Q[1];
     s.ldq2 = in.ldq[1];
-    const int fw = slice_fw(R);
-    const int ngr = (s.I2 + fw - 1) / fw;
-    const int64_t target = (int64_t)in.sms * 2 * kWarps * 4;
-    int gps = 1;
-    if ((int64_t)ngr * s.L > target) gps = (int)std::min<int64_t>(ngr, ((int64_t)ngr * s.L + target - 1) / target);
-    s.gps = gps;
-    s.nseg = (ngr + gps - 1) / gps;
-    if (s.nseg > 1) {
-      s.out = part;
-      p.part = (size_t)s.nseg * s.L * R * R;
-    } else {
+    bool tma = false;
+    if (in.tma && s.I1 % 2 == 0 && s.L < (1ll << 31) && bufs[0]) {
+      const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
+      const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
+      const uint32_t box[3] = {16, 128, 1};
+      tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
+    }
+    if (tma) {
+      s.kind = 6;
+      const int MT = NT;
+      s.S = stages_for(128 * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
+      s.nfb = (s.I2 + 127) / 128;
+      const int64_t U = s.L * s.nfb;
+      s.G = std::min<int64_t>(U, in.sms);
+      int ns = 1;
+      for (int64_t l = 0; l < s.L; ++l) {
+        const int64_t c0 = ((l * s.nfb + 1) * s.G - 1) / U, c1 = ((l * s.nfb + s.nfb) * s.G - 1) / U;
+        ns = std::max<int>(ns, (int)(c1 - c0 + 1));
+      }
+      s.nslots = ns;
       s.out = bufs[nb];
+      s.P = part;
+      p.part = (ns > 1) ? (size_t)s.L * ns * R * R : 0;
+      (void)MT;
+      p.steps.push_back(s);
+      if (ns > 1) {
+        TtmStep f = s;
+        f.kind = 7;
+        p.steps.push_back(f);
+      }
+    } else {
+      const int fw = slice_fw(R);
+      const int ngr = (s.I2 + fw - 1) / fw;
+      const int64_t target = (int64_t)in.sms * 2 * kWarps * 4;
+      int gps = 1;
+      if ((int64_t)ngr * s.L > target) gps = (int)std::min<int64_t>(ngr, ((int64_t)ngr * s.L + target - 1) / target);
+      s.gps = gps;
+      s.nseg = (ngr + gps - 1) / gps;
+      if (s.nseg > 1) {
+        s.out = part;
+        p.part = (size_t)s.nseg * s.L * R * R;
+      } else {
+        s.out = bufs[nb];
+      }
+      TtmStep sr = s;
+      p.steps.push_back(s);
+      if (s.nseg > 1) {
+        sr.kind = 3;  // reduce partials
+        sr.in = part;
+        sr.out = bufs[nb];
+        p.steps.push_back(sr);
+      }
     }
     cur[0] = R;
     cur[1] = R;
     p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
-    // when nseg > 1 the reduce kernel writes bufs[nb]
-    TtmStep sr = s;
-    p.steps.push_back(s);
-    if (s.nseg > 1) {
-      sr.kind = 3;  // reduce partials
-      sr.in = part;
-      sr.out = bufs[nb];
-      p.steps.push_back(sr);
-    }
     src = bufs[nb];
     nb ^= 1;
     for (int k = 2; k < N; ++k) if (k != n) todo.push_back(k);
@@ -384,6 +495,51 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   p.Bb = prod(cur, n + 1, N);
 }
 
+template <typename K>
+void set_smem(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
+  const int NT = (R + 7) / 8, NQB = (NT + 1) / 2;
+  if (s.kind == 4) {
+    const size_t smem = 3072 + (size_t)s.S * (16 * kBoxBytes + NQB * kBoxBytes);
+    const int64_t units = ((s.A + 255) / 256) * s.B;
+    const int grid = (int)std::min<int64_t>(units, sms);
+#define STR(NTV)                                                                                     \
+  {                                                                                                  \
+    set_smem(k_strided_tma<NTV>, smem);                                                              \
+    k_strided_tma<NTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S);   \
+  }
+    switch (NT) { case 1: STR(1) break; case 2: STR(2) break; case 3: STR(3) break; default: STR(4) break; }
+#undef STR
+  } else if (s.kind == 5) {
+    const size_t smem = 3072 + (size_t)s.S * (128 * 128 + NQB * kBoxBytes);
+    const int64_t units = (s.F + 127) / 128;
+    const int grid = (int)std::min<int64_t>(units, sms);
+#define FIB(MTV)                                                                                   \
+  {                                                                                                \
+    set_smem(k_fiber_tma<MTV>, smem);                                                              \
+    k_fiber_tma<MTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I, s.F, R, s.out, s.S);        \
+  }
+    switch (NT) { case 1: FIB(1) break; case 2: FIB(2) break; case 3: FIB(3) break; default: FIB(4) break; }
+#undef FIB
+  } else if (s.kind == 6) {
+    const size_t smem = 3072 + (size_t)s.S * (128 * 128 + NQB * kBoxBytes) + (size_t)kCW * R * R * 8;
+#define SLC(MTV)                                                                                          \
+  {                                                                                                       \
+    set_smem(k_slice_tma<MTV>, smem);                                                                     \
+    k_slice_tma<MTV><<<(int)s.G, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, s.out, \
+                                                          s.P, s.nslots, s.S);                            \
+  }
+    switch (NT) { case 1: SLC(1) break; case 2: SLC(2) break; case 3: SLC(3) break; default: SLC(4) break; }
+#undef SLC
+  } else if (s.kind == 7) {
+    const int grid = (int)std::min<int64_t>(s.L, (int64_t)sms * 4);
+    k_slice_fixup<<<grid, 256, 0, st>>>(s.P, s.nslots, s.L, s.nfb, s.G, R * R, s.out);
+  }
+}
+
 cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
   for (const TtmStep& s : p.steps) {
     switch (s.kind) {
@@ -396,6 +552,7 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
         k_reduce_slices<<<grid, 256, 0, c->st>>>(s.in, s.nseg, s.L, c->R * c->R, s.out);
         break;
       }
+      default: launch_tma(s, c->R, c->st, c->sms); break;
     }
     CKL();
   }
@@ -418,28 +575,47 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
   return CPQR_OK;
 }
 
-cpqr_status build_plans(cpqr_ctx* c) {
+void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = nullptr,
+                  const double* const* Qtover = nullptr) {
   const bool ne = c->variant == CPQR_NE;
+  in.X = c->X;
+  in.ld = c->ldims;
+  in.N = c->N;
+  in.R = c->R;
+  in.n = n;
+  in.ne = ne;
+  in.tma = c->use_tma;
+  in.sms = c->sms;
+  in.RQ = c->RQ;
+  for (int k = 0; k < c->N; ++k) {
+    const double* base = ne ? c->dA[k] : c->dQ[k];
+    const double* bt = ne ? c->dAt[k] : c->dQt[k];
+    if (Qover && Qover[k]) base = Qover[k];
+    if (Qtover && Qtover[k]) bt = Qtover[k];
+    const bool last = (k == c->N - 1);
+    in.Q[k] = last ? base + c->slab_b : base;
+    in.Qt[k] = last ? bt + c->slab_b * c->RQ : bt;
+    in.ldq[k] = c->dims[k];
+  }
+}
+
+cpqr_status build_plans(cpqr_ctx* c) {
   size_t mb = 0, mp = 0;
   for (int n = 0; n < c->N; ++n) {
     PlanIn in{};
-    in.X = c->X;
-    in.ld = c->ldims;
-    in.N = c->N;
-    in.R = c->R;
-    in.n = n;
-    in.ne = ne;
-    in.sms = c->sms;
-    for (int k = 0; k < c->N; ++k) {
-      const double* base = ne ? c->dA[k] : c->dQ[k];
-      in.Q[k] = (k == c->N - 1) ? base + c->slab_b : base;
-      in.ldq[k] = c->dims[k];
-    }
+    fill_plan_in(c, in, n);
+    in.tma = false;  // sizing pass (no maps)
     Plan tmp;
     double* nob[2] = {nullptr, nullptr};
     plan_mode(in, tmp, nob, nullptr);
     mb = std::max(mb, tmp.max_buf);
     mp = std::max(mp, tmp.part);
+    // TMA slice partials: L * nslots * R^2 with nslots <= ceil(nfb*G/U)+1 <= 2 + nfb
+    if (c->N >= 3 && n >= 2) {
+      const int64_t L = prod(c->ldims, 2, c->N);
+      const int nfb = (int)((c->ldims[1] + 127) / 128);
+      mp = std::max(mp, (size_t)L * (size_t)(nfb + 2) * c->R * c->R);
+    }
   }
   if (mb > c->buf_elems) {
     for (int i = 0; i < 2; ++i) { if (c->buf[i]) cudaFree(c->buf[i]); c->buf[i] = nullptr; }
@@ -457,18 +633,7 @@ cpqr_status build_plans(cpqr_ctx* c) {
   }
   for (int n = 0; n < c->N; ++n) {
     PlanIn in{};
-    in.X = c->X;
-    in.ld = c->ldims;
-    in.N = c->N;
-    in.R = c->R;
-    in.n = n;
-    in.ne = ne;
-    in.sms = c->sms;
-    for (int k = 0; k < c->N; ++k) {
-      const double* base = ne ? c->dA[k] : c->dQ[k];
-      in.Q[k] = (k == c->N - 1) ? base + c->slab_b : base;
-      in.ldq[k] = c->dims[k];
-    }
+    fill_plan_in(c, in, n);
     plan_mode(in, c->plans[n], c->buf, c->dPart);
   }
   c->plans_valid = true;
@@ -565,6 +730,8 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     a.Ahat = c->dAhat;
     k_tail_ne<<<1, 512, 2 * c->R * c->R * sizeof(double), c->st>>>(a);
     CKL();
+    k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[n], c->dims[n], In, c->R, c->RQ, c->dAt[n]);
+    CKL();
     prof_mark(c, 5);
     return CPQR_OK;
   }
@@ -607,6 +774,8 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   a.Ahat_fit = c->dAhat;
   const size_t smem = (size_t)(2 * c->R * c->R + 2 * c->R * (c->R + 1)) * sizeof(double);
   k_tail_qr<<<1, 512, smem, c->st>>>(a);
+  CKL();
+  k_transpose_pad<<<64, 256, 0, c->st>>>(c->dQ[n], c->dims[n], In, c->R, c->RQ, c->dQt[n]);
   CKL();
   prof_mark(c, 5);
   (void)last;
@@ -773,6 +942,8 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
 static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->N = N;
   c->R = R;
+  c->RQ = 16 * ((R + 15) / 16);
+  c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
   for (int k = 0; k < N; ++k) c->dims[k] = c->ldims[k] = dims[k];
   const int64_t per = dims[N - 1] / c->opt.world;
   c->slab_b = per * c->opt.rank;
@@ -794,6 +965,8 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     CK(cudaMalloc(&c->dQ[k], sizeof(double) * dims[k] * R));
     CK(cudaMalloc(&c->dRk[k], sizeof(double) * R * R));
     CK(cudaMalloc(&c->dG[k], sizeof(double) * R * R));
+    CK(cudaMalloc(&c->dQt[k], sizeof(double) * dims[k] * c->RQ));
+    CK(cudaMalloc(&c->dAt[k], sizeof(double) * dims[k] * c->RQ));
     CK(cudaMemset(c->dRk[k], 0, sizeof(double) * R * R));
     CK(cudaMemset(c->dG[k], 0, sizeof(double) * R * R));
   }
@@ -859,6 +1032,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   for (int k = 0; k < kMaxN; ++k) {
     cudaFree(c->dA[k]); cudaFree(c->dQ[k]); cudaFree(c->dRk[k]); cudaFree(c->dG[k]);
+    cudaFree(c->dQt[k]); cudaFree(c->dAt[k]);
   }
   double* ps[] = {c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown};
@@ -920,8 +1094,12 @@ static cpqr_status upload_factors(cpqr_ctx* c, const double* const* A, const dou
     if (c->variant == CPQR_NE) {
       k_gram<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dG[k]);
       CKL();
+      k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[k], c->dims[k], (int)c->dims[k], R, c->RQ, c->dAt[k]);
+      CKL();
     } else {
       k_factor_qr<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dQ[k], c->dRk[k]);
+      CKL();
+      k_transpose_pad<<<64, 256, 0, c->st>>>(c->dQ[k], c->dims[k], (int)c->dims[k], R, c->RQ, c->dQt[k]);
       CKL();
     }
   }
@@ -1067,25 +1245,18 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   if (c->variant == CPQR_NE) return fail(c, CPQR_EINVAL, "debug_mode is for the QR/SVD variants");
   TRY(begin_call(c));
   const int R = c->R, N = c->N;
-  std::vector<double*> tmpQ(N, nullptr);
-  PlanIn in{};
-  in.X = c->X;
-  in.ld = c->ldims;
-  in.N = N;
-  in.R = R;
-  in.n = n;
-  in.ne = false;
-  in.sms = c->sms;
+  std::vector<double*> tmpQ(N, nullptr), tmpQt(N, nullptr);
   for (int k = 0; k < N; ++k) {
-    const double* base = c->dQ[k];
     if (Qo && k != n && Qo[k]) {
       CK(cudaMalloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
+      CK(cudaMalloc(&tmpQt[k], sizeof(double) * c->dims[k] * c->RQ));
       CK(cudaMemcpyAsync(tmpQ[k], Qo[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
-      base = tmpQ[k];
+      k_transpose_pad<<<64, 256, 0, c->st>>>(tmpQ[k], c->dims[k], (int)c->dims[k], R, c->RQ, tmpQt[k]);
+      CKL();
     }
-    in.Q[k] = (k == N - 1) ? base + c->slab_b : base;
-    in.ldq[k] = c->dims[k];
   }
+  PlanIn in{};
+  fill_plan_in(c, in, n, tmpQ.data(), tmpQt.data());
   Plan p;
   plan_mode(in, p, c->buf, c->dPart);
   cpqr_status st = launch_kr_qr(c, n);
@@ -1125,6 +1296,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   cudaStreamSynchronize(c->st);
   if (yfull) cudaFree(yfull);
   for (double* q : tmpQ) if (q) cudaFree(q);
+  for (double* q : tmpQt) if (q) cudaFree(q);
   if (st != CPQR_OK) return st;
   return end_call(c);
 }

@@ -1,0 +1,456 @@
+// TMA-pipelined Multi-TTM stream-X kernels (sm_100a): the Blackwell mainloop for the dominant
+// step of CP-ALS-QR (Alg. 2 line 8; cost Eq. (TTMcost)).
+//
+// One producer warp (warp kCW) issues cp.async.bulk.tensor loads of each stage -- an X tile plus
+// the matching rows of the (transposed, zero-padded) Q panel -- into a ring of kStages shared-
+// memory buffers, signalling `full[s]` via mbarrier complete_tx.  kCW consumer warps run FP64
+// tensor-core MMAs (DMMA m8n8k4) straight from the swizzled tiles and release each stage on
+// `empty[s]`.  X is read from HBM exactly once; Q rows come from L2 alongside each X tile, so no
+// panel has to fit in shared memory whole (C5's Q_k is 256 KB).  Out-of-range rows/fibres are
+// zero-filled by TMA, which handles every ragged edge.
+//
+// Swizzle: every box has 128-byte rows (16 doubles) and SWIZZLE_128B: the 16-byte chunk c of
+// row r lives at chunk c ^ (r & 7).  MMA k-steps use the permuted k sets {2t} / {2t+1} (see
+// ttm_kernels.cuh), which makes every fragment load below bank-conflict free.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace cpqr {
+
+constexpr int kCW = 8;                 // consumer warps
+constexpr int kTmaThreads = (kCW + 1) * 32;
+constexpr int kBK = 16;                // K (contraction index) per stage
+constexpr int kBoxBytes = 16 * 128;    // {16 doubles x 16 rows} box = 2 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {  // named barrier over the consumer warps only
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kCW * 32) : "memory");
+}
+// byte offset of (row, 16-byte chunk) inside a 128B-swizzled box whose base is 1024-B aligned
+__device__ __forceinline__ uint32_t swz(int row, int chunk) { return row * 128 + (((chunk ^ row) & 7) << 4); }
+
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+struct TmaSmem {
+  uint32_t base;  // 1024-aligned shared address of stage 0
+  uint64_t* full;
+  uint64_t* empty;
+};
+
+// Carve the dynamic shared memory: [barriers (2 KB)] [stage 0] ... [stage S-1] [extra]
+__device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& full, uint64_t*& empty) {
+  uintptr_t p = reinterpret_cast<uintptr_t>(raw);
+  p = (p + 1023) & ~uintptr_t(1023);
+  full = reinterpret_cast<uint64_t*>(p);
+  empty = full + S;
+  return reinterpret_cast<uint8_t*>(p + 2048);
+}
+
+// ======================================================================= strided (mode k > 1)
+// T(a, r, b) = sum_i X(a, i, b) Q(i, r).  Unit = 256 consecutive a (8 warps x 32 rows) of one b;
+// X map 3D {A, I, B}, box {16, 16, 1} (16 boxes per stage); Q map 2D {RQ, I} over the transposed
+// padded panel Qt[i*RQ + r], box {16, 16} (NT/2 boxes).  Consumer warp w owns rows 32w..32w+31:
+// M-tiles mt = 2p + s hold rows 16(2w+p) + 2g + s (one 16-byte load feeds two tiles).
+template <int NT>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
+              int I, int64_t B, int R, double* __restrict__ T, int S) {
+  extern __shared__ uint8_t smraw[];
+  constexpr int NQB = (NT + 1) / 2;
+  constexpr uint32_t XBYTES = 16 * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
+  uint64_t *full, *empty;
+  uint8_t* st0 = tma_carve(smraw, S, full, empty);
+  const uint32_t sbase = smem_u32(st0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t nA = (A + 255) / 256;
+  const int64_t units = nA * B;
+  const int KS = (I + kBK - 1) / kBK;
+  if (warp == kCW) {  // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      prefetch_tmap(&tmQ);
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int b = (int)(u / nA);
+        const int a0 = (int)((u - (int64_t)b * nA) * 256);
+        for (int ks = 0; ks < KS; ++ks, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_expect_tx(&full[s], STAGE);
+          uint8_t* dst = st0 + (size_t)s * STAGE;
+#pragma unroll 4
+          for (int q = 0; q < 16; ++q) tma_load_3d(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s]);
+#pragma unroll
+          for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  // --------------------------------------------------------------------------------- consumers
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t it = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t b = u / nA;
+    const int64_t a0 = (u - b * nA) * 256;
+    double acc[4][NT][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    for (int ks = 0; ks < KS; ++ks, ++it) {
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const uint32_t xs = sbase + s * STAGE, qs = xs + XBYTES;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int sk = 0; sk < 2; ++sk) {
+          const int k = 8 * h + 2 * t + sk;  // row (k index) inside the stage
+          double2 xa[2];
+#pragma unroll
+          for (int p = 0; p < 2; ++p) xa[p] = lds128(xs + (2 * warp + p) * kBoxBytes + swz(k, g));
+          double qb[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+            qb[n] = lds64(qs + (n >> 1) * kBoxBytes + swz(k, 4 * (n & 1) + (g >> 1)) + 8 * (g & 1));
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            dmma(acc[0][n][0], acc[0][n][1], xa[0].x, qb[n]);
+            dmma(acc[1][n][0], acc[1][n][1], xa[0].y, qb[n]);
+            dmma(acc[2][n][0], acc[2][n][1], xa[1].x, qb[n]);
+            dmma(acc[3][n][0], acc[3][n][1], xa[1].y, qb[n]);
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    double* __restrict__ Tb = T + A * (int64_t)R * b;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int64_t row = a0 + 32 * warp + 16 * (m >> 1) + 2 * g + (m & 1);
+      if (row >= A) continue;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int r0 = 8 * n + 2 * t;
+        if (r0 < R) Tb[row + A * r0] = acc[m][n][0];
+        if (r0 + 1 < R) Tb[row + A * (r0 + 1)] = acc[m][n][1];
+      }
+    }
+  }
+}
+
+// ======================================================== fibre kernels (mode 1 / fused slice)
+// X map 3D {I1, F2, L} (F2 = fibres per slice), box {16, 128, 1}: a stage is 16 i x 128 fibres,
+// rows = fibres.  Q1 (A operand) map 2D over Qt1 {RQ, I1}, box {16, 16}.  Consumer warp w owns
+// fibres 16w..16w+15 of the block; N-tile n (0/1), lane g -> fibre 16w + 8n + fmap(g) with
+// fmap(g) = (g>>1) + 4(g&1) (makes the 16-byte X loads conflict free under the swizzle).
+__device__ __forceinline__ int fmap(int g) { return (g >> 1) + 4 * (g & 1); }
+
+// One stage of the first contraction: acc[m][n] += Q1^T(r1, i) X(i, fibre) over the 16 i.
+template <int MT>
+__device__ __forceinline__ void fiber_stage(uint32_t xs, uint32_t qs, int warp, int g, int t,
+                                            double (&acc)[MT][2][2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 xb[2];
+#pragma unroll
+    for (int n = 0; n < 2; ++n) xb[n] = lds128(xs + swz(16 * warp + 8 * n + fmap(g), 4 * h + t));
+#pragma unroll
+    for (int sk = 0; sk < 2; ++sk) {
+      const int k = 8 * h + 2 * t + sk;
+      double qa[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+        qa[m] = lds64(qs + (m >> 1) * kBoxBytes + swz(k, 4 * (m & 1) + (g >> 1)) + 8 * (g & 1));
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) dmma(acc[m][n][0], acc[m][n][1], qa[m], sk ? xb[n].y : xb[n].x);
+    }
+  }
+}
+
+// T(r, f) = sum_i Q(i, r) X(i, f), f < F (= F2 * L fibres, 2D map with L = 1).  Unit = 128 fibres.
+template <int MT>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int I,
+            int64_t F, int R, double* __restrict__ T, int S) {
+  extern __shared__ uint8_t smraw[];
+  constexpr int NQB = (MT + 1) / 2;
+  constexpr uint32_t XBYTES = 128 * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
+  uint64_t *full, *empty;
+  uint8_t* st0 = tma_carve(smraw, S, full, empty);
+  const uint32_t sbase = smem_u32(st0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t units = (F + 127) / 128;
+  const int KS = (I + kBK - 1) / kBK;
+  if (warp == kCW) {
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      prefetch_tmap(&tmQ);
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
+        for (int ks = 0; ks < KS; ++ks, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_expect_tx(&full[s], STAGE);
+          uint8_t* dst = st0 + (size_t)s * STAGE;
+          tma_load_2d(dst, &tmX, ks * kBK, (int)(u * 128), &full[s]);
+#pragma unroll
+          for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
+        }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t it = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    double acc[MT][2][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    for (int ks = 0; ks < KS; ++ks, ++it) {
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const uint32_t xs = sbase + s * STAGE;
+      fiber_stage<MT>(xs, xs + XBYTES, warp, g, t, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    const int64_t f0 = u * 128 + 16 * warp;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int r = 8 * m + g;
+      if (r >= R) continue;
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int64_t f = f0 + 8 * n + fmap(2 * t + j);
+          if (f < F) T[r + (int64_t)R * f] = acc[m][n][j];
+        }
+    }
+  }
+}
+
+// Fused two-mode slice kernel (modes 1 and 2 of X(I1, I2, L) in one pass, n >= 3):
+//   Y(r1, r2, l) = sum_{i2} [sum_{i1} Q1(i1, r1) X(i1, i2, l)] Q2(i2, r2).
+// Units u = l * nfb + fb (fibre blocks of 128 within slice l), contiguous balanced ranges per CTA
+// (u0 = c U / G).  After a unit's K loop each warp chains its first-contraction fragments into the
+// second contraction (acc[m][n][j] is the A fragment of k-step (n, j), whose k index t maps to
+// fibre fmap(2t+j)), accumulating Y in registers over the run of units of the same slice.  At a
+// slice change the 8 warps' Y are summed in a fixed order through shared memory and written to
+// Yout[l] when the run covers the whole slice, else to the partial slot P[l][c - cta_of(l nfb)]
+// (fixed-order fix-up by k_slice_fixup).  Deterministic, no atomics.
+template <int MT>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int I1, int I2,
+            int64_t L, const double* __restrict__ Q2, int64_t ldq2, int R, double* __restrict__ Yout,
+            double* __restrict__ P, int nslots, int S) {
+  extern __shared__ uint8_t smraw[];
+  constexpr int NQB = (MT + 1) / 2;
+  constexpr uint32_t XBYTES = 128 * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
+  uint64_t *full, *empty;
+  uint8_t* st0 = tma_carve(smraw, S, full, empty);
+  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // kCW x R x R
+  const uint32_t sbase = smem_u32(st0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int nfb = (I2 + 127) / 128;
+  const int64_t U = L * nfb;
+  const int64_t G = gridDim.x;
+  const int64_t u0 = (int64_t)blockIdx.x * U / G, u1 = ((int64_t)blockIdx.x + 1) * U / G;
+  const int KS = (I1 + kBK - 1) / kBK;
+  if (warp == kCW) {
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      prefetch_tmap(&tmQ);
+      uint32_t it = 0;
+      for (int64_t u = u0; u < u1; ++u) {
+        const int l = (int)(u / nfb), fb = (int)(u - (int64_t)l * nfb);
+        for (int ks = 0; ks < KS; ++ks, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_expect_tx(&full[s], STAGE);
+          uint8_t* dst = st0 + (size_t)s * STAGE;
+          tma_load_3d(dst, &tmX, ks * kBK, fb * 128, l, &full[s]);
+#pragma unroll
+          for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int RR = R * R;
+  double yacc[MT][MT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < MT; ++n) yacc[m][n][0] = yacc[m][n][1] = 0.0;
+  uint32_t it = 0;
+  int64_t run_start = u0;
+  for (int64_t u = u0; u < u1; ++u) {
+    const int64_t l = u / nfb;
+    const int fb = (int)(u - l * nfb);
+    double acc[MT][2][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    for (int ks = 0; ks < KS; ++ks, ++it) {
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const uint32_t xs = sbase + s * STAGE;
+      fiber_stage<MT>(xs, xs + XBYTES, warp, g, t, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // second contraction over this warp's 16 fibres (i2)
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i2 = fb * 128 + 16 * warp + 8 * n + fmap(2 * t + j);
+        double qb[MT];
+#pragma unroll
+        for (int m2 = 0; m2 < MT; ++m2) {
+          const int r2 = 8 * m2 + g;
+          qb[m2] = (i2 < I2 && r2 < R) ? __ldg(Q2 + i2 + ldq2 * r2) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int m2 = 0; m2 < MT; ++m2) dmma(yacc[m][m2][0], yacc[m][m2][1], acc[m][n][j], qb[m2]);
+      }
+    const bool flush = (u + 1 == u1) || ((u + 1) / nfb != l);
+    if (flush) {
+      // fixed-order reduction of the kCW warps' partial Y through shared memory
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int m2 = 0; m2 < MT; ++m2)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int r1 = 8 * m + g, r2 = 8 * m2 + 2 * t + j;
+            if (r1 < R && r2 < R) red[warp * RR + r1 + R * r2] = yacc[m][m2][j];
+            yacc[m][m2][j] = 0.0;
+          }
+      consumers_sync();
+      const bool whole = (run_start == l * nfb) && (u == l * nfb + nfb - 1);
+      double* dst;
+      if (whole) {
+        dst = Yout + l * RR;
+      } else {
+        const int64_t first_cta = ((l * nfb + 1) * G - 1) / U;  // owner of unit l*nfb
+        dst = P + (l * nslots + (blockIdx.x - first_cta)) * RR;
+      }
+      for (int e = threadIdx.x; e < RR; e += kCW * 32) {
+        double v = 0.0;
+        for (int w = 0; w < kCW; ++w) v += red[w * RR + e];
+        dst[e] = v;
+      }
+      consumers_sync();
+      run_start = u + 1;
+    }
+  }
+}
+
+// Sum the partial slots of the slices split across CTA ranges (fixed order).
+__global__ void k_slice_fixup(const double* __restrict__ P, int nslots, int64_t L, int nfb, int64_t G, int RR,
+                              double* __restrict__ Y) {
+  const int64_t U = L * nfb;
+  for (int64_t l = blockIdx.x; l < L; l += gridDim.x) {
+    const int64_t c0 = ((l * nfb + 1) * G - 1) / U;
+    const int64_t c1 = ((l * nfb + nfb) * G - 1) / U;
+    if (c0 == c1) continue;
+    for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+      double v = 0.0;
+      for (int64_t c = 0; c <= c1 - c0; ++c) v += P[(l * nslots + c) * RR + e];
+      Y[l * RR + e] = v;
+    }
+  }
+}
+
+// Qt[i * RQ + r] = Q[i + ldq * r] (r < R), 0 for R <= r < RQ: the TMA-friendly panel copy.
+__global__ void k_transpose_pad(const double* __restrict__ Q, int64_t ldq, int I, int R, int RQ,
+                                double* __restrict__ Qt) {
+  const int64_t n = (int64_t)I * RQ;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / RQ), r = (int)(e - (int64_t)i * RQ);
+    Qt[e] = (r < R) ? Q[i + ldq * r] : 0.0;
+  }
+}
+
+}  // namespace cpqr

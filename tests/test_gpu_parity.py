@@ -148,3 +148,17 @@ def test_errors_are_reported(cp):
         s.sweep(1)                           # no tensor yet
     assert e.value.status == 5
     s.close()
+
+
+@pytest.mark.parametrize("dims,R", [((30, 40, 50), 5), ((64, 48, 40), 16), ((12, 10, 9, 11), 6)])
+def test_register_staged_fallback_kernels(cp, dims, R, monkeypatch):
+    """The non-TMA (register-staged) kernels used for odd/unaligned layouts, forced on even shapes."""
+    monkeypatch.setenv("CPQR_NO_TMA", "1")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=55)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f = s.sweep(2)
+    ref = O.cp_als_qr(O.as_tensor(Xc), init, 2)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
