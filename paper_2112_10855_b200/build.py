@@ -34,13 +34,17 @@ def build(force=False, verbose=True):
     inc, lib = nccl_dirs()
     # link against libnccl.so.2 by soname (the pip package ships no unversioned symlink)
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v" if verbose == "ptxas" else "-O3",
+           "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v" if verbose == "ptxas" else "-O3", *(["-DCPQR_DEBUG_FIT"] if os.environ.get("CPQR_DEBUG_FIT") else []),
            "-I", inc, "-I", os.path.join(ROOT, "include"),
            *SRC, "-o", LIB + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-cudart", "static"]
     if verbose:
         print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+    if os.path.exists(LIB + ".tmp"):
+        os.remove(LIB + ".tmp")
+    r = subprocess.run(cmd)
+    if r.returncode != 0 or not os.path.exists(LIB + ".tmp"):
+        raise RuntimeError(f"nvcc failed (rc={r.returncode}); libcpqr.so NOT rebuilt")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -2,6 +2,7 @@
 // The per-mode sequence is Alg. 2 lines 6-12 for CP-ALS-QR / QR-SVD and
 // Alg. 1 lines 6-11 for CP-ALS.  See DESIGN.md for the kernel map.
 #include "../../include/cpqr.h"
+#include "qr_kernels.cuh"
 #include "small_kernels.cuh"
 #include "tma_kernels.cuh"
 #include "ttm_kernels.cuh"
@@ -87,6 +88,11 @@ struct cpqr_ctx {
   double *dQt[kMaxN] = {0}, *dAt[kMaxN] = {0};  // transposed, zero-padded (I_k x RQ) TMA panels
   int RQ = 16;
   bool use_tma = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t evf = nullptr, evj = nullptr;
+  double *dRstack = nullptr, *dV = nullptr, *dtauv = nullptr, *dQtop = nullptr, *dinner = nullptr;
+  double* dMpinv = nullptr;
+  int nparts = 0;
   double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWloc = nullptr,
          *dWp = nullptr, *dAhat = nullptr;
   double* buf[2] = {nullptr, nullptr};
@@ -645,6 +651,75 @@ void prof_mark(cpqr_ctx* c, int idx) {
   if (c->opt.profile) cudaEventRecord(c->evp[idx], c->st);
 }
 
+int rb_for(int R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 32); }
+
+// Ahat = W R0^{-T} (substitution) or W (R0^T)^+ (SVD) into c->dAhat, per-CTA partials in c->dred.
+cpqr_status launch_solve(cpqr_ctx* c, const double* W, int In, bool fit, int* ntrunc) {
+  const int R = c->R, RB = rb_for(R);
+  const double* Rm = c->dR0;
+  if (c->variant == CPQR_SVD) {
+    const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
+    const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+    k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, ntrunc);
+    CKL();
+    Rm = c->dMpinv;
+  }
+  const int BT = (RB > 16) ? 64 : 128;
+  const int grid = (In + BT - 1) / BT;
+  c->nparts = grid;
+  switch (RB) {
+    case 8: k_solve_rows<8><<<grid, 128, 0, c->st>>>(W, Rm, c->dR0, In, R, c->variant, c->dAhat, c->dred, fit); break;
+    case 16: k_solve_rows<16><<<grid, 128, 0, c->st>>>(W, Rm, c->dR0, In, R, c->variant, c->dAhat, c->dred, fit); break;
+    default: k_solve_rows<32><<<grid, 64, 0, c->st>>>(W, Rm, c->dR0, In, R, c->variant, c->dAhat, c->dred, fit); break;
+  }
+  CKL();
+  return CPQR_OK;
+}
+
+cpqr_status launch_normalize(cpqr_ctx* c, int In, double* A) {
+  k_normalize<<<1, 1024, 0, c->st>>>(c->dAhat, c->dred, c->nparts, rb_for(c->R), In, c->R, A, c->dlam, c->dinner,
+                                     c->dflags);
+  CKL();
+  return CPQR_OK;
+}
+
+// thin QR (TSQR) of the m x R column-major A -> Q (column-major), Qt (padded row-major), Rn.
+cpqr_status launch_factor_qr(cpqr_ctx* c, const double* A, int m, double* Q, double* Qt, double* Rn,
+                             bool do_fit) {
+  const int R = c->R;
+  int nleaf = std::max(1, std::min(8, (m + 127) / 128));
+  int mb = (m + nleaf - 1) / nleaf;
+  while (nleaf > 1 && m - (nleaf - 1) * mb < R) { --nleaf; mb = (m + nleaf - 1) / nleaf; }
+  const size_t leaf_smem = (size_t)mb * R * 8, qf_smem = 2 * leaf_smem, root_smem = (size_t)std::max(nleaf, 2) * R * R * 8;
+  if (qf_smem > 200 * 1024) {  // very tall factors: single-CTA global-memory Householder
+    if (do_fit) return fail(c, CPQR_EINVAL, "factor too tall for the TSQR path with fast fit");
+    k_factor_qr<<<1, 1024, 0, c->st>>>(A, m, R, Q, Rn);
+    CKL();
+    k_transpose_pad<<<64, 256, 0, c->st>>>(Q, m, m, R, c->RQ, Qt);
+    CKL();
+    return CPQR_OK;
+  }
+  TsqrArgs a{};
+  a.A = A; a.m = m; a.R = R; a.nleaf = nleaf; a.mb = mb;
+  a.Rstack = c->dRstack; a.V = c->dV; a.tauv = c->dtauv; a.Qtop = c->dQtop;
+  a.Q = Q; a.Qt = Qt; a.RQ = c->RQ; a.Rn = Rn;
+  a.do_fit = do_fit ? 1 : 0; a.R0 = c->dR0; a.lam = c->dlam; a.inner = c->dinner; a.nX2 = c->dnX2; a.fit = c->dfit;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tsqr_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_root, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_qform, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    attr = true;
+  }
+  k_tsqr_leaf<<<nleaf, 512, leaf_smem, c->st>>>(a);
+  CKL();
+  k_tsqr_root<<<1, 512, root_smem, c->st>>>(a);
+  CKL();
+  k_tsqr_qform<<<nleaf, 512, qf_smem, c->st>>>(a);
+  CKL();
+  return CPQR_OK;
+}
+
 cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   KrQrArgs a{};
   int m = 0;
@@ -658,7 +733,7 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   a.work_global = c->dKrWork;
   a.use_smem = c->kr_smem > 0;
   a.flags = c->variant == CPQR_QR ? c->dflags : c->dflags;
-  k_kr_qr<<<1, 1024, c->kr_smem, c->st>>>(a);
+  k_kr_qr2<<<1, 1024, c->kr_smem, c->side ? c->side : c->st>>>(a);
   CKL();
   return CPQR_OK;
 }
@@ -735,9 +810,22 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     prof_mark(c, 5);
     return CPQR_OK;
   }
-  // Alg. 2 lines 6-7: V_n and its QR (K2)
+  // Alg. 2 lines 6-7: V_n and its QR (K2), on the side stream: it depends only on the R_k and
+  // overlaps the Multi-TTM (joined before the Q0 apply).  With profiling on it runs in line.
+  const bool fork = !c->opt.profile;
   prof_mark(c, 0);
-  TRY(launch_kr_qr(c, n));
+  if (fork) {
+    CK(cudaEventRecord(c->evf, c->st));
+    CK(cudaStreamWaitEvent(c->side, c->evf, 0));
+  }
+  {
+    cudaStream_t keep = c->side;
+    if (!fork) c->side = nullptr;
+    cpqr_status st = launch_kr_qr(c, n);
+    c->side = keep;
+    TRY(st);
+  }
+  if (fork) CK(cudaEventRecord(c->evj, c->side));
   prof_mark(c, 1);
   // line 8: Multi-TTM (first step = the stream-X pass)
   {
@@ -750,33 +838,18 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     TRY(run_plan(c, rest));
     prof_mark(c, 3);
   }
+  if (fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
   // line 9: W_n = Y_(n) Q0 (local rows); combine across ranks
   double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
   TRY(launch_q0_apply(c, p, Wloc));
   TRY(combine_w(c, n, Wloc, c->dW));
   prof_mark(c, 4);
-  // lines 10-12: solve / SVD, normalise, lambda, factor QR (+ fast fit after mode N)
-  TailArgs a{};
-  a.W = c->dW;
-  a.R0 = c->dR0;
-  a.In = In;
-  a.R = c->R;
-  a.variant = c->variant;
-  a.tau = (c->opt.svd_tau < 0) ? c->R * 2.220446049250313e-16 : c->opt.svd_tau;
-  a.Aw = c->dQ[n];
-  a.A = c->dA[n];
-  a.Rn = c->dRk[n];
-  a.lam = c->dlam;
-  a.flags = c->dflags;
-  a.do_fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
-  a.nX2 = c->dnX2;
-  a.fit = c->dfit;
-  a.Ahat_fit = c->dAhat;
-  const size_t smem = (size_t)(2 * c->R * c->R + 2 * c->R * (c->R + 1)) * sizeof(double);
-  k_tail_qr<<<1, 512, smem, c->st>>>(a);
-  CKL();
-  k_transpose_pad<<<64, 256, 0, c->st>>>(c->dQ[n], c->dims[n], In, c->R, c->RQ, c->dQt[n]);
-  CKL();
+  // lines 10-11: solve / SVD, lambda, normalise (+ <W, Ahat R0^T> for the fit)
+  const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
+  TRY(launch_solve(c, c->dW, In, fit, nullptr));
+  TRY(launch_normalize(c, In, c->dA[n]));
+  // line 12: factor QR of the updated factor (TSQR) -> Q_n, its TMA panel, R_n (+ fast fit)
+  TRY(launch_factor_qr(c, c->dA[n], In, c->dQ[n], c->dQt[n], c->dRk[n], fit));
   prof_mark(c, 5);
   (void)last;
   return CPQR_OK;
@@ -955,6 +1028,9 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->opt.device);
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->user = (cudaStream_t)c->opt.stream;
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->evf, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->evj, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev0, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev1, cudaEventDisableTiming));
   for (int i = 0; i < 16; ++i) CK(cudaEventCreate(&c->evp[i]));
@@ -978,6 +1054,12 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(cudaMalloc(&c->dW, sizeof(double) * imax * R));
   CK(cudaMalloc(&c->dWloc, sizeof(double) * imax * R));
   CK(cudaMalloc(&c->dAhat, sizeof(double) * imax * R));
+  CK(cudaMalloc(&c->dRstack, sizeof(double) * 8 * R * R));
+  CK(cudaMalloc(&c->dQtop, sizeof(double) * 8 * R * R));
+  CK(cudaMalloc(&c->dV, sizeof(double) * (imax + 8) * R));
+  CK(cudaMalloc(&c->dtauv, sizeof(double) * 8 * R));
+  CK(cudaMalloc(&c->dinner, sizeof(double) * 4));
+  CK(cudaMalloc(&c->dMpinv, sizeof(double) * R * R));
   c->wp_elems = (size_t)imax * R * 1024;
   CK(cudaMalloc(&c->dWp, sizeof(double) * std::min<size_t>(c->wp_elems, (size_t)imax * R * (size_t)std::max<int64_t>(1, (J + 63) / 64))));
   CK(cudaMalloc(&c->dnX2, sizeof(double) * 4));
@@ -1009,7 +1091,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     const size_t bytes = packed * sizeof(double);
     if (bytes <= 200 * 1024) {
       c->kr_smem = (int)bytes;
-      CK(cudaFuncSetAttribute(k_kr_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, c->kr_smem));
+      CK(cudaFuncSetAttribute(k_kr_qr2, cudaFuncAttributeMaxDynamicSharedMemorySize, c->kr_smem));
     } else {
       c->kr_smem = 0;
       CK(cudaMalloc(&c->dKrWork, bytes));
@@ -1034,7 +1116,10 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
     cudaFree(c->dA[k]); cudaFree(c->dQ[k]); cudaFree(c->dRk[k]); cudaFree(c->dG[k]);
     cudaFree(c->dQt[k]); cudaFree(c->dAt[k]);
   }
-  double* ps[] = {c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->evf) cudaEventDestroy(c->evf);
+  if (c->evj) cudaEventDestroy(c->evj);
+  double* ps[] = {c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown};
   for (double* p : ps) if (p) cudaFree(p);
   if (c->dperm) cudaFree(c->dperm);
@@ -1097,10 +1182,7 @@ static cpqr_status upload_factors(cpqr_ctx* c, const double* const* A, const dou
       k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[k], c->dims[k], (int)c->dims[k], R, c->RQ, c->dAt[k]);
       CKL();
     } else {
-      k_factor_qr<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dQ[k], c->dRk[k]);
-      CKL();
-      k_transpose_pad<<<64, 256, 0, c->st>>>(c->dQ[k], c->dims[k], (int)c->dims[k], R, c->RQ, c->dQt[k]);
-      CKL();
+      TRY(launch_factor_qr(c, c->dA[k], (int)c->dims[k], c->dQ[k], c->dQt[k], c->dRk[k], false));
     }
   }
   std::vector<double> l(R, 1.0);
@@ -1259,8 +1341,14 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   fill_plan_in(c, in, n, tmpQ.data(), tmpQt.data());
   Plan p;
   plan_mode(in, p, c->buf, c->dPart);
+  CK(cudaEventRecord(c->evf, c->st));
+  CK(cudaStreamWaitEvent(c->side, c->evf, 0));
   cpqr_status st = launch_kr_qr(c, n);
   if (st == CPQR_OK) st = run_plan(c, p);
+  if (st == CPQR_OK) {
+    CK(cudaEventRecord(c->evj, c->side));
+    CK(cudaStreamWaitEvent(c->st, c->evj, 0));
+  }
   double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
   if (st == CPQR_OK) st = launch_q0_apply(c, p, Wloc);
   if (st == CPQR_OK) st = combine_w(c, n, Wloc, c->dW);
@@ -1310,8 +1398,11 @@ CPQR_API cpqr_status cpqr_debug_qr(cpqr_ctx* c, const double* A, int64_t m, doub
   CK(cudaMalloc(&dQ, sizeof(double) * m * R));
   CK(cudaMalloc(&dR, sizeof(double) * R * R));
   CK(cudaMemcpyAsync(dA, A, sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
-  k_factor_qr<<<1, 1024, 0, c->st>>>(dA, (int)m, R, dQ, dR);
-  CKL();
+  double* dQt = nullptr;
+  CK(cudaMalloc(&dQt, sizeof(double) * m * c->RQ));
+  TRY(launch_factor_qr(c, dA, (int)m, dQ, dQt, dR, false));
+  CK(cudaStreamSynchronize(c->st));
+  cudaFree(dQt);
   if (Q) CK(cudaMemcpyAsync(Q, dQ, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
   if (Rf) CK(cudaMemcpyAsync(Rf, dR, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -1340,17 +1431,21 @@ CPQR_API cpqr_status cpqr_debug_svd_solve(cpqr_ctx* c, const double* R0, const d
     for (int r = 0; r < R; ++r) wr[i * R + r] = W[i + m * r];
   CK(cudaMemcpyAsync(dW, wr.data(), sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(dR0, R0, sizeof(double) * R * R, cudaMemcpyHostToDevice, c->st));
-  TailArgs a{};
-  a.W = dW; a.R0 = dR0; a.In = (int)m; a.R = R; a.variant = CPQR_SVD; a.tau = tau;
-  a.Aw = dAw; a.A = dA; a.Rn = dRn; a.lam = dlam; a.flags = dfl; a.do_fit = 1;
-  a.nX2 = c->dnX2; a.fit = c->dred; a.Ahat_fit = dAh;
   int* dnt = nullptr;
   CK(cudaMalloc(&dnt, sizeof(int)));
   CK(cudaMemsetAsync(dnt, 0, sizeof(int), c->st));
-  a.ntrunc = dnt;
-  const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
-  k_tail_qr<<<1, 512, smem, c->st>>>(a);
-  CKL();
+  CK(cudaMemcpyAsync(c->dR0, dR0, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->st));
+  {
+    const double keep = c->opt.svd_tau;
+    const int kv = c->variant;
+    c->opt.svd_tau = tau;
+    c->variant = CPQR_SVD;
+    cpqr_status st = launch_solve(c, dW, (int)m, false, dnt);
+    c->opt.svd_tau = keep;
+    c->variant = kv;
+    TRY(st);
+  }
+  dAh = c->dAhat;
   unsigned fl = 0;
   CK(cudaMemcpyAsync(Ahat, dAh, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(&fl, dfl, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
@@ -1360,6 +1455,6 @@ CPQR_API cpqr_status cpqr_debug_svd_solve(cpqr_ctx* c, const double* R0, const d
   cudaFree(dnt);
   if (ntrunc) *ntrunc = nt;
   (void)fl;
-  cudaFree(dW); cudaFree(dR0); cudaFree(dAw); cudaFree(dA); cudaFree(dAh); cudaFree(dRn); cudaFree(dlam); cudaFree(dfl);
+  cudaFree(dW); cudaFree(dR0); cudaFree(dAw); cudaFree(dA); cudaFree(dRn); cudaFree(dlam); cudaFree(dfl);
   return end_call(c);
 }

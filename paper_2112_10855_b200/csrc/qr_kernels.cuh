@@ -1,0 +1,555 @@
+// Householder QR kernels of the per-mode tail (sm_100a, fp64), shared-memory resident.
+//
+//   hh_factor / hh_formq   in-place Householder QR (LAPACK dgeqr2 / dorg2r conventions) of a
+//                          matrix whose column k is the contiguous run col(k)[0 .. nrow[k]) -- a
+//                          dense panel (nrow = m) or the packed staircase of V_n (nrow[k] =
+//                          (k+1)^{N-1}: no fill-in, Q0 has V_n's support).
+//                          Two block barriers per column: after the reflector-dot phase, warp 0
+//                          applies H_j to column j+1 and immediately builds reflector j+1 while
+//                          the other warps update the remaining columns.
+//   k_tsqr_leaf/root/qform thin QR of the I_n x R factor (Alg. 2 line 12) as a
+//                          one-level TSQR: leaf blocks in parallel CTAs, QR of the stacked R_b
+//                          in one CTA (diag(R) >= 0, reading 6), explicit Q = diag(Q_b) Q_top
+//                          written both column-major (Q_n) and as the transposed padded panel the
+//                          TMA kernels stream.
+//   k_solve_norm           Alg. 2 lines 10-11: Ahat R0^T = W (row-parallel back substitution) or
+//                          Ahat = W U S^+ V^T (one-sided Jacobi SVD of R0), lambda, normalise,
+//                          and <W, Ahat R0^T> for the fast fit.
+#pragma once
+#include <cstdio>
+#include "small_kernels.cuh"
+
+namespace cpqr {
+
+struct HHCols {        // packed staircase: column k at base + off[k], nrow[k] rows
+  double* base;
+  const int64_t* off;  // column offsets (shared memory)
+  const int* nrow;     // rows per column (shared memory)
+  __device__ __forceinline__ double* col(int k) const { return base + off[k]; }
+  __device__ __forceinline__ int rows(int k) const { return nrow[k]; }
+};
+struct DenseCols {     // dense panel: column k at base + k*ld, m rows
+  double* base;
+  int ld, m;
+  __device__ __forceinline__ double* col(int k) const { return base + (int64_t)k * ld; }
+  __device__ __forceinline__ int rows(int) const { return m; }
+};
+
+// warp 0 only: Householder vector for column j (dlarfg): beta = -sign(x0) ||x||, tau = (beta - x0)/beta,
+// v = x / (x0 - beta) below the diagonal, col(j)[j] = beta.
+template <class Cols>
+__device__ __forceinline__ void hh_make_reflector(const Cols& M, int j, double* tau, double* beta) {
+  const int lane = threadIdx.x & 31;
+  double* cj = M.col(j);
+  const int mj = M.rows(j);
+  double s = 0.0;
+  for (int i = j + 1 + lane; i < mj; i += 32) s += cj[i] * cj[i];
+  s = warp_sum(s);
+  const double x0 = cj[j];
+  double tj, bj, scale;
+  if (s == 0.0) { tj = 0.0; bj = x0; scale = 0.0; }
+  else {
+    const double nrm = sqrt(x0 * x0 + s);
+    bj = (x0 >= 0.0) ? -nrm : nrm;
+    tj = (bj - x0) / bj;
+    scale = 1.0 / (x0 - bj);
+  }
+  if (tj != 0.0)
+    for (int i = j + 1 + lane; i < mj; i += 32) cj[i] *= scale;
+  __syncwarp();
+  if (lane == 0) { cj[j] = bj; tau[j] = tj; beta[j] = bj; }
+  __syncwarp();
+}
+
+// Factorisation.  On exit: col(k)[r] (r < k) = R(r, k) (unsigned), beta[k] = R(k, k), reflector
+// j stored below the diagonal of column j, tau[j].  All threads of the block must call.
+template <class Cols>
+__device__ void hh_factor(const Cols& M, int R, double* tau, double* beta, double* w) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  if (wid == 0) hh_make_reflector(M, 0, tau, beta);
+  __syncthreads();
+  for (int j = 0; j < R; ++j) {
+    const double tj = tau[j];
+    const double* vj = M.col(j);
+    const int mj = M.rows(j);
+    if (tj != 0.0) {  // w_k = A(j,k) + sum_{i>j} v_i A(i,k): one warp per column, 4 partial sums
+      for (int k = j + 1 + wid; k < R; k += nw) {
+        const double* ck = M.col(k);
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+        int i = j + 1 + lane;
+        for (; i + 96 < mj; i += 128) {
+          d0 = fma(vj[i], ck[i], d0);
+          d1 = fma(vj[i + 32], ck[i + 32], d1);
+          d2 = fma(vj[i + 64], ck[i + 64], d2);
+          d3 = fma(vj[i + 96], ck[i + 96], d3);
+        }
+        for (; i < mj; i += 32) d0 = fma(vj[i], ck[i], d0);
+        const double d = warp_sum((d0 + d1) + (d2 + d3));
+        if (lane == 0) w[k] = ck[j] + d;
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      if (j + 1 < R) {
+        double* ck = M.col(j + 1);
+        if (tj != 0.0) {
+          const double wk = tj * w[j + 1];
+          for (int i = j + lane; i < mj; i += 32) ck[i] -= wk * ((i == j) ? 1.0 : vj[i]);
+        }
+        __syncwarp();
+        hh_make_reflector(M, j + 1, tau, beta);
+      }
+    } else if (tj != 0.0 && j + 2 < R) {
+      for (int i = j + tid - 32; i < mj; i += nt - 32) {
+        const double vi = (i == j) ? tj : tj * vj[i];
+#pragma unroll 8
+        for (int k = j + 2; k < R; ++k) M.col(k)[i] -= w[k] * vi;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Explicit Q in place (dorg2r), after hh_factor (R must have been saved first).  Columns are NOT
+// sign-fixed here.
+template <class Cols>
+__device__ void hh_formq(const Cols& M, int R, const double* tau, double* w) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int j = R - 1; j >= 0; --j) {
+    double* cj = M.col(j);
+    const int mj = M.rows(j);
+    const double tj = tau[j];
+    if (j < R - 1 && tj != 0.0) {
+      for (int k = j + 1 + wid; k < R; k += nw) {
+        const double* ck = M.col(k);
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+        int i = j + 1 + lane;
+        for (; i + 96 < mj; i += 128) {
+          d0 = fma(cj[i], ck[i], d0);
+          d1 = fma(cj[i + 32], ck[i + 32], d1);
+          d2 = fma(cj[i + 64], ck[i + 64], d2);
+          d3 = fma(cj[i + 96], ck[i + 96], d3);
+        }
+        for (; i < mj; i += 32) d0 = fma(cj[i], ck[i], d0);
+        const double d = warp_sum((d0 + d1) + (d2 + d3));
+        if (lane == 0) w[k] = ck[j] + d;  // v_j = 1; row j of column k is 0 (zeroed earlier)
+      }
+      __syncthreads();
+      for (int i = j + tid; i < mj; i += nt) {
+        const double vi = (i == j) ? tj : tj * cj[i];
+#pragma unroll 8
+        for (int k = j + 1; k < R; ++k) M.col(k)[i] -= w[k] * vi;
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < mj; i += nt) cj[i] = (i < j) ? 0.0 : ((i == j) ? 1.0 - tj : -tj * cj[i]);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------ TSQR (K1)
+struct TsqrArgs {
+  const double* A;  // m x R column-major (lda = m)
+  int m, R, nleaf, mb;  // leaf b: rows [b*mb, min(m, (b+1)*mb))
+  double* Rstack;   // (nleaf*R) x R column-major
+  double* V;        // leaf reflectors: mb x R per leaf, column-major, leaf stride mb*R
+  double* tauv;     // nleaf * R
+  double* Qtop;     // (nleaf*R) x R column-major
+  double* Q;        // out: m x R column-major
+  double* Qt;       // out: m x RQ row-major, zero padded
+  int RQ;
+  double* Rn;       // out: R x R column-major, diag >= 0
+  // fast fit after mode N: ||Xh||^2 = <R0^T R0, diag(lam) Rn^T Rn diag(lam)>
+  int do_fit;
+  const double* R0;
+  const double* lam;
+  const double* inner;  // <W, Ahat R0^T>
+  const double* nX2;
+  double* fit;
+};
+
+__global__ void __launch_bounds__(512) k_tsqr_leaf(TsqrArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double tau[64], beta[64], w[64];
+  const int b = blockIdx.x, R = a.R;
+  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
+  for (int c = 0; c < R; ++c)
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) sm[i + rows * c] = a.A[r0 + i + (int64_t)a.m * c];
+  __syncthreads();
+  DenseCols M{sm, rows, rows};
+  hh_factor(M, R, tau, beta, w);
+  const int ldr = a.nleaf * R;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int r = e % R, c = e / R;
+    a.Rstack[b * R + r + (int64_t)ldr * c] = (r < c) ? sm[r + rows * c] : ((r == c) ? beta[r] : 0.0);
+  }
+  for (int c = 0; c < R; ++c)
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) a.V[(int64_t)b * a.mb * R + i + rows * c] = sm[i + rows * c];
+  if (threadIdx.x < R) a.tauv[b * R + threadIdx.x] = tau[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(512) k_tsqr_root(TsqrArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double tau[64], beta[64], w[64], red[32];
+  const int R = a.R, rows = a.nleaf * R;
+  for (int e = threadIdx.x; e < rows * R; e += blockDim.x) sm[e] = a.Rstack[e];
+  __syncthreads();
+  DenseCols M{sm, rows, rows};
+  hh_factor(M, R, tau, beta, w);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int r = e % R, c = e / R;
+    double v = (r < c) ? sm[r + rows * c] : ((r == c) ? beta[r] : 0.0);
+    if (beta[r] < 0.0) v = -v;
+    a.Rn[r + R * c] = v;
+  }
+  __syncthreads();
+  hh_formq(M, R, tau, w);
+  for (int e = threadIdx.x; e < rows * R; e += blockDim.x) {
+    const int c = e / rows;
+    a.Qtop[e] = (beta[c] < 0.0) ? -sm[e] : sm[e];
+  }
+  if (a.do_fit) {
+    __syncthreads();
+    double* r0s = sm;            // reuse: R0 and Rn (sign-fixed) in shared memory
+    double* rns = sm + R * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      r0s[e] = a.R0[e];
+      const int r = e % R, c = e / R;
+      rns[e] = a.Rn[e];
+      (void)r; (void)c;
+    }
+    __syncthreads();
+    double q = 0.0;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int x = e % R, y = e / R;
+      double g0 = 0.0, g1 = 0.0;
+      for (int k = 0; k <= min(x, y); ++k) {
+        g0 = fma(r0s[k + R * x], r0s[k + R * y], g0);
+        g1 = fma(rns[k + R * x], rns[k + R * y], g1);
+      }
+      q = fma(g0, a.lam[x] * a.lam[y] * g1, q);
+    }
+    const double nxh2 = block_sum(q, red);
+    if (threadIdx.x == 0) {
+      const double nx2 = *a.nX2;
+      *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * (*a.inner) + nxh2)) / sqrt(nx2);
+#ifdef CPQR_DEBUG_FIT
+      printf("fit: nx2 %.17g inner %.17g nxh2 %.17g\n", nx2, *a.inner, nxh2);
+#endif
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) k_tsqr_qform(TsqrArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double w[64], tv[64];
+  const int b = blockIdx.x, R = a.R, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5,
+            nw = nt >> 5;
+  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
+  double* Mq = sm;                // rows x R : [Qtop_b; 0]
+  double* Vb = sm + rows * R;     // rows x R : leaf reflectors
+  const int ldt = a.nleaf * R;
+  for (int c = 0; c < R; ++c)
+    for (int i = tid; i < rows; i += nt) {
+      Mq[i + rows * c] = (i < R) ? a.Qtop[b * R + i + (int64_t)ldt * c] : 0.0;
+      Vb[i + rows * c] = a.V[(int64_t)b * a.mb * R + i + rows * c];
+    }
+  if (tid < R) tv[tid] = a.tauv[b * R + tid];
+  __syncthreads();
+  for (int j = R - 1; j >= 0; --j) {
+    const double tj = tv[j];
+    if (tj == 0.0) continue;
+    const double* vj = Vb + (int64_t)rows * j;
+    for (int k = wid; k < R; k += nw) {
+      const double* ck = Mq + (int64_t)rows * k;
+      double d0 = 0.0, d1 = 0.0;
+      int i = j + 1 + lane;
+      for (; i + 32 < rows; i += 64) { d0 = fma(vj[i], ck[i], d0); d1 = fma(vj[i + 32], ck[i + 32], d1); }
+      for (; i < rows; i += 32) d0 = fma(vj[i], ck[i], d0);
+      const double d = warp_sum(d0 + d1);
+      if (lane == 0) w[k] = ck[j] + d;
+    }
+    __syncthreads();
+    for (int i = j + tid; i < rows; i += nt) {
+      const double vi = (i == j) ? tj : tj * vj[i];
+#pragma unroll 8
+      for (int k = 0; k < R; ++k) Mq[i + rows * k] -= w[k] * vi;
+    }
+    __syncthreads();
+  }
+  for (int c = 0; c < R; ++c)
+    for (int i = tid; i < rows; i += nt) a.Q[r0 + i + (int64_t)a.m * c] = Mq[i + rows * c];
+  for (int i = tid / a.RQ; i < rows; i += nt / a.RQ) {  // blockDim is a multiple of RQ (16/32)
+    const int c = tid % a.RQ;
+    a.Qt[(int64_t)(r0 + i) * a.RQ + c] = (c < R) ? Mq[i + rows * c] : 0.0;
+  }
+}
+
+// ----------------------------------------------------------------------- solve + normalise
+struct SolveArgs {
+  const double* W;   // In x R row-major
+  const double* R0;  // R x R column-major
+  int In, R, variant;
+  double tau;
+  double* A;         // out: normalised factor, column-major
+  double* Ahat;      // out: unnormalised solution, column-major
+  double* lam;
+  unsigned* flags;
+  int do_fit;
+  double* inner;     // out: <W, Ahat R0^T>
+  int* ntrunc;
+};
+
+__global__ void __launch_bounds__(512) k_solve_norm(SolveArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double red[32], lam[64];
+  __shared__ int sflag;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int R = a.R, In = a.In;
+  double* R0s = sm;
+  double* Ms = R0s + R * R;
+  double* Bs = Ms + R * R;
+  double* Vs = Bs + R * (R + 1);
+  for (int e = tid; e < R * R; e += nt) R0s[e] = a.R0[e];
+  __syncthreads();
+  if (a.variant == 2) {
+    const int ntr = jacobi_pinv(R0s, R, a.tau, Bs, Vs, Ms, &sflag);
+    if (tid == 0 && ntr > 0) atomicOr(a.flags, FLAG_SVD_TRUNCATED);
+    if (tid == 0 && a.ntrunc) *a.ntrunc = ntr;
+    for (int64_t e = tid; e < (int64_t)In * R; e += nt) {  // e = c * In + i (coalesced store)
+      const int c = (int)(e / In), i = (int)(e - (int64_t)c * In);
+      const double* wr = a.W + (int64_t)i * R;
+      double s = 0.0;
+      for (int r = 0; r < R; ++r) s = fma(wr[r], Ms[r + R * c], s);
+      a.Ahat[e] = s;
+    }
+  } else {
+    for (int i = tid; i < In; i += nt) {  // Ahat(i,j) = (W(i,j) - sum_{l>j} Ahat(i,l) R0(j,l)) / R0(j,j)
+      const double* wr = a.W + (int64_t)i * R;
+      double x[32];
+#pragma unroll 1
+      for (int j = R - 1; j >= 0; --j) {
+        double acc = wr[j];
+#pragma unroll 1
+        for (int l = j + 1; l < R; ++l) acc -= x[l] * R0s[j + R * l];
+        x[j] = acc / R0s[j + R * j];
+      }
+#pragma unroll 1
+      for (int j = 0; j < R; ++j) a.Ahat[i + (int64_t)In * j] = x[j];
+    }
+  }
+  __syncthreads();
+  for (int c = wid; c < R; c += nw) {
+    const double* col = a.Ahat + (int64_t)In * c;
+    double s = 0.0;
+    for (int i = lane; i < In; i += 32) s += col[i] * col[i];
+    s = warp_sum(s);
+    if (lane == 0) lam[c] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < R; ++c) if (!isfinite(lam[c])) atomicOr(a.flags, FLAG_NONFINITE);
+  for (int64_t e = tid; e < (int64_t)In * R; e += nt) {
+    const int c = (int)(e / In), i = (int)(e - (int64_t)c * In);
+    a.A[e] = (lam[c] > 0.0) ? a.Ahat[e] / lam[c] : (i == 0 ? 1.0 : 0.0);
+  }
+  if (tid < R) a.lam[tid] = lam[tid];
+  if (a.do_fit) {  // <W, Ahat R0^T> = sum_i sum_c W(i,c) sum_{l>=c} Ahat(i,l) R0(c,l)
+    double s = 0.0;
+    for (int i = tid; i < In; i += nt) {
+      const double* wr = a.W + (int64_t)i * R;
+      for (int c = 0; c < R; ++c) {
+        double t = 0.0;
+        for (int l = c; l < R; ++l) t = fma(a.Ahat[i + (int64_t)In * l], R0s[c + R * l], t);
+        s = fma(wr[c], t, s);
+      }
+    }
+    s = block_sum(s, red);
+    if (tid == 0) *a.inner = s;
+  }
+}
+
+// ------------------------------------------------------------- K2 with the 2-barrier primitive
+__global__ void __launch_bounds__(1024) k_kr_qr2(KrQrArgs a) {
+  extern __shared__ double smk[];
+  __shared__ double tau[64], beta[64], w[64];
+  __shared__ int64_t off[65];
+  __shared__ int ncnt[64];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int R = a.R, N1 = a.N1;
+  if (tid == 0) {
+    int64_t o = 0;
+    for (int c = 0; c < R; ++c) {
+      int64_t p = 1;
+      for (int m = 0; m < N1; ++m) p *= (c + 1);
+      ncnt[c] = (int)p;
+      off[c] = o;
+      o += p;
+    }
+    off[R] = o;
+  }
+  __syncthreads();
+  double* V = a.use_smem ? smk : a.work_global;
+  for (int c = 0; c < R; ++c)  // V_n entries in packed staircase order
+    for (int p = tid; p < ncnt[c]; p += nt) {
+      int j = a.perm[p];
+      double v = 1.0;
+      for (int m = 0; m < N1; ++m) {
+        const int im = j % R;
+        j /= R;
+        v *= a.Rk[m][im + R * c];
+      }
+      V[off[c] + p] = v;
+    }
+  __syncthreads();
+  HHCols M{V, off, ncnt};
+  hh_factor(M, R, tau, beta, w);
+  for (int e = tid; e < R * R; e += nt) {
+    const int r = e % R, c = e / R;
+    double v = (r < c) ? V[off[c] + r] : ((r == c) ? beta[r] : 0.0);
+    if (beta[r] < 0.0) v = -v;
+    a.R0[r + R * c] = v;
+  }
+  if (tid == 0) {
+    double mx = 0.0, mn = 1e308;
+    for (int c = 0; c < R; ++c) { mx = fmax(mx, fabs(beta[c])); mn = fmin(mn, fabs(beta[c])); }
+    int64_t J = 1;
+    for (int m = 0; m < N1; ++m) J *= R;
+    if (mn <= (double)J * kEps * mx) atomicOr(a.flags, FLAG_ILLCOND_R0);
+  }
+  __syncthreads();
+  hh_formq(M, R, tau, w);
+  int64_t J = 1;
+  for (int m = 0; m < N1; ++m) J *= R;
+  for (int64_t e = tid; e < J * R; e += nt) a.Q0[e] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < R; ++c) {
+    const double sg = (beta[c] < 0.0) ? -1.0 : 1.0;
+    for (int p = tid; p < ncnt[c]; p += nt) a.Q0[a.perm[p] + J * c] = sg * V[off[c] + p];
+  }
+}
+
+
+// ------------------------------------------------------------- multi-CTA solve (Alg. 2 l. 10-11)
+// k_svd_pinv: M = U S^+ V^T of R0 (one CTA, one-sided Jacobi) for the QR-SVD variant.
+__global__ void __launch_bounds__(512) k_svd_pinv(const double* __restrict__ R0, int R, double tau,
+                                                  double* __restrict__ Mout, unsigned* flags, int* ntrunc) {
+  extern __shared__ double sm[];
+  __shared__ int sflag;
+  double* R0s = sm;
+  double* Ms = R0s + R * R;
+  double* Bs = Ms + R * R;
+  double* Vs = Bs + R * (R + 1);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) R0s[e] = R0[e];
+  __syncthreads();
+  const int ntr = jacobi_pinv(R0s, R, tau, Bs, Vs, Ms, &sflag);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Mout[e] = Ms[e];
+  if (threadIdx.x == 0) {
+    if (ntr > 0) atomicOr(flags, FLAG_SVD_TRUNCATED);
+    if (ntrunc) *ntrunc = ntr;
+  }
+}
+
+// k_solve_rows<RB>: one thread per row i: Ahat(i,:) from W(i,:) by back substitution with R0
+// (variant 1) or x = W(i,:) M (variant 2), registers only (R <= RB).  Per-CTA partial column
+// sums of squares and the per-CTA partial of <W, Ahat R0^T> go to part[cta][0..R] (fixed order).
+template <int RB, int BT = (RB > 16 ? 64 : 128)>
+__global__ void __launch_bounds__(BT) k_solve_rows(const double* __restrict__ W, const double* __restrict__ Rm,
+                                                    const double* __restrict__ R0, int In, int R, int variant,
+                                                    double* __restrict__ Ahat, double* __restrict__ part,
+                                                    int do_fit) {
+  __shared__ double Ms[RB * RB];
+  __shared__ double R0s[RB * RB];
+  __shared__ double Xs[BT * (RB + 1)];
+  __shared__ double red[BT / 32][RB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    const int r = e % RB, c = e / RB;
+    Ms[e] = (r < R && c < R) ? Rm[r + R * c] : 0.0;
+    R0s[e] = (r < R && c < R) ? R0[r + R * c] : 0.0;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + tid;
+  double* x = Xs + tid * (RB + 1);
+  double w[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) w[r] = (i < In && r < R) ? W[(int64_t)i * R + r] : 0.0;
+  if (variant == 2) {
+#pragma unroll 4
+    for (int c = 0; c < RB; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) s = fma(w[r], Ms[r + RB * c], s);
+      x[c] = s;
+    }
+  } else {
+#pragma unroll
+    for (int j = RB - 1; j >= 0; --j) {  // x_j = (w_j - sum_{l>j} x_l R0(j,l)) / R0(j,j)
+      double acc = w[j];
+#pragma unroll
+      for (int l = j + 1; l < RB; ++l) acc = fma(-x[l], Ms[j + RB * l], acc);
+      x[j] = (j < R) ? acc / Ms[j + RB * j] : 0.0;
+    }
+  }
+  double inner = 0.0;
+  if (do_fit) {  // <W, Ahat R0^T>: sum_c w_c sum_{l>=c} x_l R0(c,l)
+#pragma unroll 4
+    for (int c = 0; c < RB; ++c) {
+      double t = 0.0;
+#pragma unroll
+      for (int l = 0; l < RB; ++l)
+        if (l >= c) t = fma(x[l], R0s[c + RB * l], t);
+      inner = fma(w[c], t, inner);
+    }
+  }
+  if (i >= In) inner = 0.0;
+  __syncthreads();
+  // coalesced store of the block's rows (column-major Ahat) and per-column sums of squares
+  const int i0 = blockIdx.x * blockDim.x;
+  for (int c = 0; c < R; ++c) {
+    const int ii = i0 + tid;
+    const double v = (ii < In) ? Xs[tid * (RB + 1) + c] : 0.0;
+    if (ii < In) Ahat[ii + (int64_t)In * c] = v;
+    const double q = warp_sum(v * v);
+    if (lane == 0) red[wid][c] = q;
+  }
+  {
+    const double q = warp_sum(inner);
+    if (lane == 0) red[wid][RB] = q;
+  }
+  __syncthreads();
+  for (int c = tid; c <= RB; c += blockDim.x) {
+    double v = 0.0;
+    if (c < R || c == RB)
+      for (int q = 0; q < BT / 32; ++q) v += red[q][c];
+    part[(int64_t)blockIdx.x * (RB + 1) + c] = v;
+  }
+}
+
+// lambda, non-finite check, normalisation, <W, Ahat R0^T> (fixed-order over CTA partials).
+__global__ void __launch_bounds__(1024) k_normalize(const double* __restrict__ Ahat, const double* __restrict__ part,
+                                                    int nparts, int RB, int In, int R, double* __restrict__ A,
+                                                    double* __restrict__ lam_out, double* __restrict__ inner,
+                                                    unsigned* flags) {
+  __shared__ double lam[64];
+  if (threadIdx.x <= R) {
+    const int c = (threadIdx.x == R) ? RB : threadIdx.x;
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * (RB + 1) + c];
+    if (threadIdx.x < R) {
+      lam[c] = sqrt(s);
+      lam_out[c] = lam[c];
+      if (!isfinite(lam[c])) atomicOr(flags, FLAG_NONFINITE);
+    } else {
+      *inner = s;
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < R; ++c) {
+    const double l = lam[c];
+    for (int i = threadIdx.x; i < In; i += blockDim.x)
+      A[i + (int64_t)In * c] = (l > 0.0) ? Ahat[i + (int64_t)In * c] / l : (i == 0 ? 1.0 : 0.0);
+  }
+}
+
+}  // namespace cpqr
