@@ -430,7 +430,23 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       const uint32_t box[3] = {16, 128, 1};
       tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
     }
-    if (tma) {
+    const bool small = tma && s.I2 <= 64 && s.I2 % 8 == 0 && NT <= 2;
+    if (small) {
+      const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
+      const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
+      const uint32_t box[3] = {16, (uint32_t)s.I2, 8};
+      if (make_tmap(&s.mx, src, 3, d, st, box)) {
+        s.kind = 8;
+        s.S = stages_for((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes, 0);
+        s.out = bufs[nb];
+        p.steps.push_back(s);
+      } else {
+        tma = false;
+      }
+    }
+    if (small && s.kind == 8) {
+      // done
+    } else if (tma) {
       s.kind = 6;
       const int MT = NT;
       s.S = stages_for(128 * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
@@ -540,6 +556,17 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
   }
     switch (NT) { case 1: SLC(1) break; case 2: SLC(2) break; case 3: SLC(3) break; default: SLC(4) break; }
 #undef SLC
+  } else if (s.kind == 8) {
+    const size_t smem = 3072 + (size_t)s.S * ((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes);
+    const int64_t units = (s.L + 7) / 8;
+    const int grid = (int)std::min<int64_t>(units, sms);
+#define SSM(MTV)                                                                                             \
+  {                                                                                                          \
+    set_smem(k_slice_small_tma<MTV>, smem);                                                                  \
+    k_slice_small_tma<MTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, s.out, s.S); \
+  }
+    switch (NT) { case 1: SSM(1) break; case 2: SSM(2) break; case 3: SSM(3) break; default: SSM(4) break; }
+#undef SSM
   } else if (s.kind == 7) {
     const int grid = (int)std::min<int64_t>(s.L, (int64_t)sms * 4);
     k_slice_fixup<<<grid, 256, 0, st>>>(s.P, s.nslots, s.L, s.nfb, s.G, R * R, s.out);

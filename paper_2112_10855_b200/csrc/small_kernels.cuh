@@ -389,7 +389,7 @@ __device__ int jacobi_pinv(const double* R0, int R, double tau, double* Bs, doub
           al += bp * bp; be += bq * bq; ga += bp * bq;
         }
         al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (fabs(ga) > kEps * sqrt(al * be) && ga != 0.0) {
+        if (fabs(ga) > (double)R * kEps * sqrt(al * be) && ga != 0.0) {
           const double zeta = (be - al) / (2.0 * ga);
           const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;

@@ -427,6 +427,126 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   }
 }
 
+
+// Small-slice variant (I2 <= 64, I2 % 8 == 0): a stage is the 3D box {16 i1, I2 fibres, 8 slices};
+// consumer warp w owns slice 8u + w entirely (nf2 = I2/8 N-tiles), chains the second contraction
+// itself and writes Y(:, :, l) directly -- no cross-warp reduction, no partial slots.
+template <int MT>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int I1,
+                  int I2, int64_t L, const double* __restrict__ Q2, int64_t ldq2, int R,
+                  double* __restrict__ Yout, int S) {
+  extern __shared__ uint8_t smraw[];
+  constexpr int NQB = (MT + 1) / 2;
+  const uint32_t XBYTES = (uint32_t)I2 * 8 * 128, STAGE = XBYTES + NQB * kBoxBytes;
+  uint64_t *full, *empty;
+  uint8_t* st0 = tma_carve(smraw, S, full, empty);
+  const uint32_t sbase = smem_u32(st0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int nf2 = I2 / 8;
+  const int64_t units = (L + 7) / 8;
+  const int KS = (I1 + kBK - 1) / kBK;
+  if (warp == kCW) {
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      prefetch_tmap(&tmQ);
+      uint32_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
+        for (int ks = 0; ks < KS; ++ks, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_expect_tx(&full[s], STAGE);
+          uint8_t* dst = st0 + (size_t)s * STAGE;
+          tma_load_3d(dst, &tmX, ks * kBK, 0, (int)(u * 8), &full[s]);
+#pragma unroll
+          for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
+        }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t it = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    double acc[MT][8][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int n = 0; n < 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    const int rowbase = warp * I2;
+    for (int ks = 0; ks < KS; ++ks, ++it) {
+      const int s = it % S;
+      mbar_wait(&full[s], (it / S) & 1);
+      const uint32_t xs = sbase + s * STAGE, qs = xs + XBYTES;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 xb[8];
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+          if (n < nf2) xb[n] = lds128(xs + swz(rowbase + 8 * n + fmap(g), 4 * h + t));
+#pragma unroll
+        for (int sk = 0; sk < 2; ++sk) {
+          const int k = 8 * h + 2 * t + sk;
+          double qa[MT];
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+            qa[m] = lds64(qs + (m >> 1) * kBoxBytes + swz(k, 4 * (m & 1) + (g >> 1)) + 8 * (g & 1));
+#pragma unroll
+          for (int n = 0; n < 8; ++n)
+            if (n < nf2)
+#pragma unroll
+              for (int m = 0; m < MT; ++m) dmma(acc[m][n][0], acc[m][n][1], qa[m], sk ? xb[n].y : xb[n].x);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    const int64_t l = u * 8 + warp;
+    double yacc[MT][MT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int n = 0; n < MT; ++n) yacc[m][n][0] = yacc[m][n][1] = 0.0;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      if (n >= nf2) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i2 = 8 * n + fmap(2 * t + j);
+        double qb[MT];
+#pragma unroll
+        for (int m2 = 0; m2 < MT; ++m2) {
+          const int r2 = 8 * m2 + g;
+          qb[m2] = (r2 < R) ? __ldg(Q2 + i2 + ldq2 * r2) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int m2 = 0; m2 < MT; ++m2) dmma(yacc[m][m2][0], yacc[m][m2][1], acc[m][n][j], qb[m2]);
+      }
+    }
+    if (l < L) {
+      double* o = Yout + l * R * R;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int r1 = 8 * m + g;
+        if (r1 >= R) continue;
+#pragma unroll
+        for (int m2 = 0; m2 < MT; ++m2)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int r2 = 8 * m2 + 2 * t + j;
+            if (r2 < R) o[r1 + R * r2] = yacc[m][m2][j];
+          }
+      }
+    }
+  }
+}
+
 // Sum the partial slots of the slices split across CTA ranges (fixed order).
 __global__ void k_slice_fixup(const double* __restrict__ P, int nslots, int64_t L, int nfb, int64_t G, int RR,
                               double* __restrict__ Y) {

@@ -162,3 +162,24 @@ def test_register_staged_fallback_kernels(cp, dims, R, monkeypatch):
     ref = O.cp_als_qr(O.as_tensor(Xc), init, 2)
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
     s.close()
+
+
+@pytest.mark.parametrize("dims,R,variant", [((16, 48, 20, 9), 8, "SVD"), ((32, 64, 20), 16, "QR"),
+                                            ((24, 40, 12, 10), 5, "QR")])
+def test_small_slice_kernel(cp, dims, R, variant):
+    """I2 <= 64, I2 % 8 == 0: the whole-slice-per-warp TMA kernel (modes n >= 3)."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=91, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    N = len(dims)
+    Qs = [O.qr_pos(a)[0] for a in init]
+    for n in range(2, N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11
+    f = s.sweep(2)
+    ref = O.cp_als_qr(X, init, 2, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
