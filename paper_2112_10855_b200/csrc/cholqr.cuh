@@ -1,0 +1,1022 @@
+// CholeskyQR2 for the I_n x R factor panels (Alg. 2 line 12), with a device-side
+// switch to the Householder TSQR (rowqr.cuh) when the panel is too ill-conditioned.
+//
+//   pass 1:  G1 = A^T A (per-block partials, fixed-order sum), G1 = L1 L1^T, Q1 = A L1^{-T}
+//   pass 2:  G2 = Q1^T Q1,  G2 = L2 L2^T,  Q = Q1 L2^{-T},  R = L2^T L1^T
+// Both passes yield the unique thin QR with diag(R) > 0 (reading 6); after pass 2 ||Q^T Q - I|| =
+// O(eps) when kappa(A) < ~1e7.  k_cq_chol1 estimates kappa(A) ~ max(L1_jj)/min(L1_jj) and sets
+// FLAG_USE_HOUSEHOLDER when it exceeds kCqKappaMax or a pivot is not positive; every CholeskyQR
+// kernel after it then returns immediately and the Householder kernels (which otherwise return at
+// once) produce Q, R -- all launches stay in the CUDA graph.
+//
+// In solve mode the first kernel also forms Ahat(i,:) (substitution with R0 or W M for the SVD
+// variant) and factors Ahat itself: lambda_c^2 = G1(c,c), A_n = Ahat diag(1/lambda)
+// and R_n = R_hat diag(1/lambda) (the Q factor is unchanged by the positive column scaling).
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace cpqr {
+
+constexpr double kCqKappaMax = 1.0e5;
+constexpr unsigned FLAG_USE_HOUSEHOLDER = 0x200u;
+
+struct CqArgs {
+  const double* A;   // solve = 0: m x R column-major input
+  int m, R, nb, mb;  // row blocks of mb rows
+  int solve;
+  const double* W;   // m x R row-major
+  const double* Rm;  // R0 (variant 1) or M (variant 2)
+  const double* R0;
+  int variant;
+  double* Ahat;      // out (solve): unnormalised solution, column-major
+  double* Q1;        // scratch: m x R column-major
+  double* Gp;        // scratch: nb x R x R Gram partials
+  double* innerp;    // scratch: nb partial <W, Ahat R0^T>
+  double* R1;        // scratch: R x R upper (L1^T)
+  double* R2;        // scratch: R x R upper (L2^T)
+  double* Q;         // out: m x R column-major
+  double* Qt;        // out: m x RQ row-major, zero padded
+  int RQ;
+  double* Rn;        // out: R x R
+  double* Aout;      // out (solve): A_n
+  double* lam;       // out (solve)
+  unsigned* flags;
+  int do_fit;
+  const double* nX2;
+  double* fit;
+};
+
+// Upper triangle of the block Gram from a shared-memory panel P (rows x R, leading dim ld).
+__device__ __forceinline__ void cq_block_gram(const double* P, int ld, int rows, int R, double* out) {
+  const int npairs = R * (R + 1) / 2;
+  for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
+    int p = 0, rem = e;  // (p, q) with p <= q, row-major over the upper triangle
+    while (rem >= R - p) { rem -= R - p; ++p; }
+    const int q = p + rem;
+    const double* cp = P + (int64_t)ld * p;
+    const double* cq = P + (int64_t)ld * q;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = 0;
+    for (; i + 3 < rows; i += 4) {
+      s0 = fma(cp[i], cq[i], s0);
+      s1 = fma(cp[i + 1], cq[i + 1], s1);
+      s2 = fma(cp[i + 2], cq[i + 2], s2);
+      s3 = fma(cp[i + 3], cq[i + 3], s3);
+    }
+    for (; i < rows; ++i) s0 = fma(cp[i], cq[i], s0);
+    const double s = (s0 + s1) + (s2 + s3);
+    out[p + R * q] = s;
+    out[q + R * p] = s;
+  }
+}
+
+// pass-1 Gram (and, in solve mode, the solve of Ahat).  blockDim = 32 * ceil(mb/32) <= 256.
+template <int RB>
+__global__ void __launch_bounds__(256) k_cq_gram1(CqArgs a) {
+  extern __shared__ double P[];  // rows x R, ld = rows | 1
+  __shared__ double Ms[RB * RB], R0s[RB * RB], redi[8];
+  const int b = blockIdx.x, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (b == 0 && tid == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);  // per-mode decision
+  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0, ld = rows | 1;
+  if (!a.solve) {
+    for (int c = 0; c < R; ++c)
+      for (int i = tid; i < rows; i += blockDim.x) P[i + ld * c] = a.A[r0 + i + (int64_t)a.m * c];
+  } else {
+    for (int e = tid; e < RB * RB; e += blockDim.x) {
+      const int r = e % RB, c = e / RB;
+      Ms[e] = (r < R && c < R) ? a.Rm[r + R * c] : 0.0;
+      R0s[e] = (r < R && c < R) ? a.R0[r + R * c] : 0.0;
+    }
+    __syncthreads();
+    double inner = 0.0;
+    if (tid < rows) {
+      const int i = r0 + tid;
+      double wv[RB], x[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) wv[k] = (k < R) ? a.W[(int64_t)i * R + k] : 0.0;
+      if (a.variant == 2) {  // x = w M, M = U S^+ V^T
+#pragma unroll
+        for (int c = 0; c < RB; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int r = 0; r < RB; ++r) s = fma(wv[r], Ms[r + RB * c], s);
+          x[c] = s;
+        }
+      } else {  // Ahat R0^T = W by back substitution
+#pragma unroll
+        for (int j = RB - 1; j >= 0; --j) {
+          double acc = wv[j];
+#pragma unroll
+          for (int l = j + 1; l < RB; ++l) acc = fma(-x[l], Ms[j + RB * l], acc);
+          x[j] = (j < R) ? acc / Ms[j + RB * j] : 0.0;
+        }
+      }
+      if (a.do_fit) {  // <W, Ahat R0^T>
+#pragma unroll
+        for (int c = 0; c < RB; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int l = c; l < RB; ++l) t = fma(x[l], R0s[c + RB * l], t);
+          inner = fma(wv[c], t, inner);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (k < R) {
+          P[tid + ld * k] = x[k];
+          a.Ahat[i + (int64_t)a.m * k] = x[k];
+        }
+    }
+    inner = warp_sum(inner);
+    if (lane == 0) redi[wid] = inner;
+  }
+  __syncthreads();
+  if (a.solve && tid == 0) {
+    double v = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) v += redi[q];
+    a.innerp[b] = v;
+  }
+  cq_block_gram(P, ld, rows, R, a.Gp + (int64_t)b * R * R);
+}
+
+// Sum the block Grams (fixed order) and Cholesky-factor them: returns R1 = L^T (upper) in
+// shared memory Ls (R x R column-major); pass 1 also decides the Householder fallback.
+__device__ void cq_chol(const CqArgs& a, double* Gs, double* Ls, bool pass1, bool* ok_out) {
+  const int R = a.R, tid = threadIdx.x, lane = tid & 31;
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < a.nb; ++b) s += a.Gp[(int64_t)b * R * R + e];
+    Gs[e] = s;
+  }
+  __syncthreads();
+  if (tid < 32) {  // warp 0: left-looking Cholesky, lane i owns row i of L (R <= 32)
+    bool ok = true;
+    double dmax = 0.0, dmin = 1e308;
+    for (int j = 0; j < R; ++j) {
+      // L(i, j) for i >= j: G(i,j) - sum_{k<j} L(i,k) L(j,k)
+      double s = (lane < R) ? Gs[lane + R * j] : 0.0;
+      for (int k = 0; k < j; ++k) {
+        const double ljk = Ls[k + R * j];  // R1(k, j) = L(j, k)
+        const double lik = (lane < R) ? Ls[k + R * lane] : 0.0;
+        s = fma(-lik, ljk, s);
+      }
+      const double djj = __shfl_sync(0xffffffffu, s, j);
+      if (!(djj > 0.0)) ok = false;
+      const double ljj = sqrt(fmax(djj, 0.0));
+      dmax = fmax(dmax, ljj);
+      dmin = fmin(dmin, ljj);
+      if (lane == j) Ls[j + R * j] = ljj;
+      else if (lane > j && lane < R) Ls[j + R * lane] = (ljj > 0.0) ? s / ljj : 0.0;  // R1(j, lane)
+      __syncwarp();
+    }
+    if (lane == 0) *ok_out = ok && (dmin > 0.0) && (dmax / dmin < (pass1 ? kCqKappaMax : 1.0e3));
+  }
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int r = e % R, c = e / R;
+    if (r > c) Ls[e] = 0.0;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_cq_chol1(CqArgs a) {
+  __shared__ double Gs[32 * 32], Ls[32 * 32];
+  __shared__ bool ok;
+  cq_chol(a, Gs, Ls, true, &ok);
+  if (!ok) {
+    if (threadIdx.x == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    return;
+  }
+  for (int e = threadIdx.x; e < a.R * a.R; e += blockDim.x) a.R1[e] = Ls[e];
+}
+
+// Row-wise triangular solve y R1 = x for this block's rows (x = A or Ahat rows for pass 1, Q1 for
+// pass 2).  pass 1: write Q1 and its block Gram.  pass 2: write Q, Qt (and A_n in solve mode).
+template <int RB>
+__global__ void __launch_bounds__(256) k_cq_apply(CqArgs a, int pass) {
+  extern __shared__ double P[];
+  __shared__ double Rs[RB * RB];
+  __shared__ unsigned fl;
+  if (threadIdx.x == 0) fl = *a.flags;
+  __syncthreads();
+  if (fl & FLAG_USE_HOUSEHOLDER) return;
+  const int b = blockIdx.x, R = a.R, tid = threadIdx.x;
+  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0, ld = rows | 1;
+  const double* Rf = (pass == 1) ? a.R1 : a.R2;
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    const int r = e % RB, c = e / RB;
+    Rs[e] = (r < R && c < R) ? Rf[r + R * c] : 0.0;
+  }
+  __syncthreads();
+  const double* src = (pass == 1) ? (a.solve ? a.Ahat : a.A) : a.Q1;
+  if (tid < rows) {
+    const int i = r0 + tid;
+    double x[RB], y[RB];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) x[k] = (k < R) ? src[i + (int64_t)a.m * k] : 0.0;
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {  // y_j = (x_j - sum_{l<j} y_l R1(l,j)) / R1(j,j)
+      double acc = x[j];
+#pragma unroll
+      for (int l = 0; l < j; ++l) acc = fma(-y[l], Rs[l + RB * j], acc);
+      y[j] = (j < R) ? acc / Rs[j + RB * j] : 0.0;
+    }
+    if (pass == 1) {
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (k < R) { a.Q1[i + (int64_t)a.m * k] = y[k]; P[tid + ld * k] = y[k]; }
+    } else {
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (k < R) a.Q[i + (int64_t)a.m * k] = y[k];
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (k < a.RQ) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? y[k] : 0.0;
+      for (int k = RB; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = 0.0;
+      if (a.solve) {  // A_n = Ahat / lambda (zero column -> e_1, reading 10)
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+          if (k >= R) continue;
+          const double l = a.lam[k];
+          const int64_t e = i + (int64_t)a.m * k;
+          a.Aout[e] = (l > 0.0) ? a.Ahat[e] / l : (i == 0 ? 1.0 : 0.0);
+        }
+      }
+    }
+  }
+  if (pass == 1) {
+    __syncthreads();
+    cq_block_gram(P, ld, rows, R, a.Gp + (int64_t)b * R * R);
+  }
+}
+
+// pass-2 Cholesky, R = L2^T L1^T, lambda / R_n scaling and the fast fit.
+__global__ void __launch_bounds__(256) k_cq_chol2(CqArgs a, const double* G1diag_src) {
+  __shared__ double Gs[32 * 32], Ls[32 * 32], R1s[32 * 32], lam[32], red[8];
+  __shared__ bool ok;
+  __shared__ unsigned fl;
+  if (threadIdx.x == 0) fl = *a.flags;
+  __syncthreads();
+  if (fl & FLAG_USE_HOUSEHOLDER) return;
+  const int R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < R * R; e += blockDim.x) R1s[e] = a.R1[e];
+  cq_chol(a, Gs, Ls, false, &ok);  // Ls = R2 = L2^T
+  // safety: after pass 1 the Gram of Q1 must be I to O(kappa^2 eps); otherwise fall back
+  __shared__ double emax[8];
+  {
+    double e = 0.0;
+    for (int q = tid; q < R * R; q += blockDim.x) e = fmax(e, fabs(Gs[q] - ((q % R) == (q / R) ? 1.0 : 0.0)));
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) emax[wid] = e;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double e = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) e = fmax(e, emax[w]);
+    if (!ok || !(e < 1.0e-4)) { atomicOr(a.flags, FLAG_USE_HOUSEHOLDER); fl = FLAG_USE_HOUSEHOLDER; }
+  }
+  __syncthreads();
+  if (fl & FLAG_USE_HOUSEHOLDER) return;
+  if (a.solve && tid < R) {  // lambda_c = ||Ahat(:,c)||_2 = sqrt(G1(c,c)) = ||R1(:,c)||_2
+    double s = 0.0;
+    for (int k = 0; k <= tid; ++k) s = fma(R1s[k + R * tid], R1s[k + R * tid], s);
+    lam[tid] = sqrt(s);
+    a.lam[tid] = lam[tid];
+    if (!isfinite(lam[tid])) atomicOr(a.flags, FLAG_NONFINITE);
+  }
+  __syncthreads();
+  for (int e = tid; e < R * R; e += blockDim.x) a.R2[e] = Ls[e];
+  for (int e = tid; e < R * R; e += blockDim.x) {  // R = R2 R1 (upper x upper), then / lambda
+    const int r = e % R, c = e / R;
+    double s = 0.0;
+    for (int k = r; k <= c; ++k) s = fma(Ls[r + R * k], R1s[k + R * c], s);
+    if (a.solve && lam[c] > 0.0) s /= lam[c];
+    a.Rn[e] = (r <= c) ? s : 0.0;
+    Gs[e] = (r <= c) ? s : 0.0;
+  }
+  (void)G1diag_src;
+  __syncthreads();
+  if (a.do_fit) {  // ||Xh||^2 = <R0^T R0, diag(lam) R_n^T R_n diag(lam)>; <W, Ahat R0^T> from partials
+    for (int e = tid; e < R * R; e += blockDim.x) Ls[e] = a.R0[e];
+    __syncthreads();
+    double q = 0.0;
+    for (int e = tid; e < R * R; e += blockDim.x) {
+      const int x = e % R, y = e / R;
+      double g0 = 0.0, g1 = 0.0;
+      for (int k = 0; k <= min(x, y); ++k) {
+        g0 = fma(Ls[k + R * x], Ls[k + R * y], g0);
+        g1 = fma(Gs[k + R * x], Gs[k + R * y], g1);
+      }
+      q = fma(g0, lam[x] * lam[y] * g1, q);
+    }
+    q = warp_sum(q);
+    if (lane == 0) red[wid] = q;
+    __syncthreads();
+    if (tid == 0) {
+      double nxh2 = 0.0, inner = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) nxh2 += red[w];
+      for (int b = 0; b < a.nb; ++b) inner += a.innerp[b];
+      const double nx2 = *a.nX2;
+      *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner + nxh2)) / sqrt(nx2);
+    }
+  }
+}
+
+
+// ================================================================ single-launch cluster variant
+// Cluster of nb <= 8 CTAs (one per row block of <= 256 rows, one thread per row, rows kept in
+// registers).  Block Grams on the FP64 tensor cores from a shared-memory panel, summed in a fixed
+// order over the cluster through distributed shared memory by EVERY CTA (so each CTA factors the
+// same G redundantly and no broadcast is needed), Cholesky by one warp with the rows in
+// registers, triangular solves in registers.  4 cluster barriers for the whole factor QR.
+
+// G (RB x RB, symmetric, ld RB) = P^T P for the shared panel P (rows4 x RB, leading dim ld,
+// zero-padded rows/columns), DMMA 8x8x4 tiles of the upper triangle, one warp per tile.
+template <int RB>
+__device__ __forceinline__ void cq_gram_dmma(const double* P, int ld, int rows4, double* G) {
+  constexpr int T = RB / 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  int tile = 0;
+  for (int pi = 0; pi < T; ++pi)
+    for (int qi = pi; qi < T; ++qi, ++tile) {
+      if (tile % nw != wid) continue;
+      double d0 = 0.0, d1 = 0.0;
+      const double* cp = P + (int64_t)ld * (8 * pi + g);
+      const double* cq = P + (int64_t)ld * (8 * qi + g);
+      for (int k0 = 0; k0 < rows4; k0 += 4) dmma(d0, d1, cp[k0 + t], cq[k0 + t]);
+      const int r = 8 * pi + g, c0 = 8 * qi + 2 * t;
+      G[r + RB * c0] = d0;
+      G[r + RB * (c0 + 1)] = d1;
+      G[c0 + RB * r] = d0;
+      G[(c0 + 1) + RB * r] = d1;
+    }
+}
+
+// Right-looking Cholesky G = L L^T by warp 0 (lane i = row i, R <= RB <= 32), rows in registers.
+// Writes Rt = L^T (upper, RB x RB, ld RB) and invd[j] = 1 / L_jj.  Returns ok (pivots > 0) and
+// the ratio max L_jj / min L_jj through *ratio.
+template <int RB>
+__device__ __noinline__ bool cq_chol_warp(const double* G, int R, double* Rt, double* invd, double* ratio) {
+  const int lane = threadIdx.x & 31;
+  double gr[RB];
+#pragma unroll
+  for (int k = 0; k < RB; ++k) gr[k] = (lane < R && k < R) ? G[lane + RB * k] : 0.0;
+  bool ok = true;
+  double dmax = 0.0, dmin = 1e308;
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    if (j >= R) break;
+    const double piv = __shfl_sync(0xffffffffu, gr[j], j);
+    if (!(piv > 0.0)) ok = false;
+    const double ljj = sqrt(fmax(piv, 0.0));
+    const double inv = (ljj > 0.0) ? 1.0 / ljj : 0.0;
+    dmax = fmax(dmax, ljj);
+    dmin = fmin(dmin, ljj);
+    const double lij = (lane == j) ? ljj : ((lane > j && lane < R) ? gr[j] * inv : 0.0);
+    gr[j] = lij;  // lane i now keeps L(i, j) in gr[j]
+#pragma unroll
+    for (int k = j + 1; k < RB; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, lij, k);
+      if (lane > j) gr[k] = fma(-lij, lkj, gr[k]);
+    }
+    if (lane == 0) invd[j] = inv;
+  }
+  if (lane < RB)
+#pragma unroll
+    for (int j = 0; j < RB; ++j) Rt[j + RB * lane] = (j <= lane && j < R && lane < R) ? gr[j] : 0.0;  // R(j, lane) = L(lane, j)
+  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;
+  return ok;
+}
+
+// Ui = Ru^{-1} (Ru upper triangular RB x RB in shared memory, inverse diagonal in invd) by warp 0:
+// lane c back-substitutes column c in registers (fully unrolled, no divisions).
+template <int RB>
+__device__ __noinline__ void cq_tri_inv_warp(const double* Ru, const double* invd, int R, double* Ui) {
+  const int c = threadIdx.x & 31;
+  double u[RB];
+#pragma unroll
+  for (int r = RB - 1; r >= 0; --r) {
+    double acc = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = r + 1; l < RB; ++l) acc = fma(-Ru[r + RB * l], u[l], acc);
+    u[r] = (r <= c && r < R && c < R) ? acc * invd[r] : 0.0;
+  }
+  if (c < RB)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) Ui[r + RB * c] = u[r];
+}
+
+template <int RB>
+__global__ void __launch_bounds__(256) k_cq_fused(CqArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  // dynamic shared memory: [7 x RB*RB matrices][panel ld x RB], ld = roundup(rows, 16) + 4
+  extern __shared__ double smq[];
+  double* G1b = smq;
+  double* G2b = G1b + RB * RB;
+  double* Gs = G2b + RB * RB;
+  double* R1s = Gs + RB * RB;
+  double* R2s = R1s + RB * RB;
+  double* Ms = R2s + RB * RB;
+  double* R0s = Ms + RB * RB;
+  double* P = R0s + RB * RB;
+  __shared__ double inv1[RB], inv2[RB], lam[RB], redi[8], innerb;
+  __shared__ int okf;
+  const int nb = a.nb, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int b = (int)cluster.block_rank();
+  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
+  const int rows4 = (rows + 3) & ~3, ld = (((int)blockDim.x + 15) & ~15) + 4;  // >= every thread's row
+  const int i = r0 + tid;
+  const bool own = tid < rows;
+  if (tid == 0 && b == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);
+  // ---- 1. rows of the panel: A, or Ahat solved from W (PAPER.md:358 / 339)
+  double x[RB];
+  double inner = 0.0;
+  if (!a.solve) {
+#pragma unroll
+    for (int k = 0; k < RB; ++k) x[k] = (own && k < R) ? a.A[i + (int64_t)a.m * k] : 0.0;
+  } else {
+    for (int e = tid; e < RB * RB; e += blockDim.x) {
+      const int r = e % RB, c = e / RB;
+      Ms[e] = (r < R && c < R) ? a.Rm[r + R * c] : 0.0;
+      R0s[e] = (r < R && c < R) ? a.R0[r + R * c] : 0.0;
+    }
+    __syncthreads();
+    double wv[RB];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) wv[k] = (own && k < R) ? a.W[(int64_t)i * R + k] : 0.0;
+    if (a.variant == 2) {
+#pragma unroll
+      for (int c = 0; c < RB; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) s = fma(wv[r], Ms[r + RB * c], s);
+        x[c] = s;
+      }
+    } else {
+#pragma unroll
+      for (int j = RB - 1; j >= 0; --j) {
+        double acc = wv[j];
+#pragma unroll
+        for (int l = j + 1; l < RB; ++l) acc = fma(-x[l], Ms[j + RB * l], acc);
+        x[j] = (j < R) ? acc / Ms[j + RB * j] : 0.0;
+      }
+    }
+    if (a.do_fit) {
+#pragma unroll
+      for (int c = 0; c < RB; ++c) {
+        double tt = 0.0;
+#pragma unroll
+        for (int l = c; l < RB; ++l) tt = fma(x[l], R0s[c + RB * l], tt);
+        inner = fma(wv[c], tt, inner);
+      }
+    }
+    if (own)
+#pragma unroll
+      for (int k = 0; k < RB; ++k)
+        if (k < R) a.Ahat[i + (int64_t)a.m * k] = x[k];
+  }
+  inner = warp_sum(inner);
+  if (lane == 0) redi[wid] = inner;
+  for (int e = tid; e < ld * RB; e += blockDim.x) P[e] = 0.0;
+  __syncthreads();
+  if (own)
+#pragma unroll
+    for (int k = 0; k < RB; ++k) P[tid + ld * k] = x[k];
+  if (tid == 0) {
+    double v = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) v += redi[q];
+    innerb = v;
+  }
+  __syncthreads();
+  // ---- 2. block Gram, cluster sum (every CTA, same order), Cholesky -> R1
+  cq_gram_dmma<RB>(P, ld, rows4, G1b);
+  cluster.sync();
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G1b, c)[e];
+    Gs[e] = s;
+  }
+  double inner_all = 0.0;
+  for (int c = 0; c < nb; ++c) inner_all += *cluster.map_shared_rank(&innerb, c);
+  __syncthreads();
+  if (wid == 0) {
+    double ratio;
+    const bool ok = cq_chol_warp<RB>(Gs, R, R1s, inv1, &ratio);
+    if (lane == 0) okf = ok && ratio < kCqKappaMax;
+  }
+  if (a.solve && tid < R) lam[tid] = sqrt(Gs[tid + RB * tid]);  // lambda_c = ||Ahat(:,c)||_2
+  __syncthreads();
+  if (!okf) {
+    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    cluster.sync();  // peers may still read this CTA's shared memory
+    return;
+  }
+  // ---- 3. Q1 rows: y R1 = x (forward substitution), Gram of Q1, Cholesky -> R2
+  double y[RB];
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    double acc = x[j];
+#pragma unroll
+    for (int l = 0; l < j; ++l) acc = fma(-y[l], R1s[l + RB * j], acc);
+    y[j] = (j < R) ? acc * inv1[j] : 0.0;
+  }
+  __syncthreads();
+  if (own)
+#pragma unroll
+    for (int k = 0; k < RB; ++k) P[tid + ld * k] = y[k];
+  __syncthreads();
+  cq_gram_dmma<RB>(P, ld, rows4, G2b);
+  cluster.sync();
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G2b, c)[e];
+    Gs[e] = s;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    double ratio;
+    const bool ok = cq_chol_warp<RB>(Gs, R, R2s, inv2, &ratio);
+    double e = 0.0;  // ||G2 - I||_max must be O(kappa^2 eps)
+    for (int q = lane; q < R * R; q += 32) {
+      const int r = q % R, c = q / R;
+      e = fmax(e, fabs(Gs[r + RB * c] - (r == c ? 1.0 : 0.0)));
+    }
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) okf = ok && (e < 1.0e-4);
+  }
+  __syncthreads();
+  if (!okf) {
+    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    cluster.sync();
+    return;
+  }
+  // ---- 4. Q = Q1 R2^{-1}; A_n = Ahat / lambda; R_n = R2 R1 diag(1/lambda); fit
+  double q[RB];
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    double acc = y[j];
+#pragma unroll
+    for (int l = 0; l < j; ++l) acc = fma(-q[l], R2s[l + RB * j], acc);
+    q[j] = (j < R) ? acc * inv2[j] : 0.0;
+  }
+  if (own) {
+#pragma unroll
+    for (int k = 0; k < RB; ++k)
+      if (k < R) a.Q[i + (int64_t)a.m * k] = q[k];
+    for (int k = 0; k < a.RQ; ++k) {
+      double v = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < RB; ++kk) v = (kk == k && kk < R) ? q[kk] : v;
+      a.Qt[(int64_t)i * a.RQ + k] = v;
+    }
+    if (a.solve)
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        if (k >= R) continue;
+        const double l = lam[k];
+        a.Aout[i + (int64_t)a.m * k] = (l > 0.0) ? x[k] / l : (i == 0 ? 1.0 : 0.0);
+      }
+  }
+  if (b == 0) {
+    for (int e = tid; e < RB * RB; e += blockDim.x) {
+      const int r = e % RB, c = e / RB;
+      double s = 0.0;
+      for (int k = r; k <= c; ++k) s = fma(R2s[r + RB * k], R1s[k + RB * c], s);
+      if (a.solve && c < R && lam[c] > 0.0) s /= lam[c];
+      s = (r <= c && r < R && c < R) ? s : 0.0;
+      Gs[e] = s;  // R_n
+      if (r < R && c < R) a.Rn[r + R * c] = s;
+    }
+    if (a.solve && tid < R) {
+      a.lam[tid] = lam[tid];
+      if (!isfinite(lam[tid])) atomicOr(a.flags, FLAG_NONFINITE);
+    }
+    if (a.do_fit) {
+      __syncthreads();
+      double qq = 0.0;
+      for (int e = tid; e < R * R; e += blockDim.x) {
+        const int xx = e % R, yy = e / R;
+        double g0 = 0.0, g1 = 0.0;
+        for (int k = 0; k <= min(xx, yy); ++k) {
+          g0 = fma(R0s[k + RB * xx], R0s[k + RB * yy], g0);
+          g1 = fma(Gs[k + RB * xx], Gs[k + RB * yy], g1);
+        }
+        qq = fma(g0, lam[xx] * lam[yy] * g1, qq);
+      }
+      qq = warp_sum(qq);
+      if (lane == 0) redi[wid] = qq;
+      __syncthreads();
+      if (tid == 0) {
+        double nxh2 = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) nxh2 += redi[w];
+        const double nx2 = *a.nX2;
+        *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner_all + nxh2)) / sqrt(nx2);
+      }
+    }
+  }
+  cluster.sync();  // no CTA leaves while peers may read its shared memory
+}
+
+
+// ----------------------------------------------------------------- compact (I-cache friendly) variant
+// Same algorithm as k_cq_fused, but every per-row quantity lives in a shared-memory panel row
+// (owner thread tid, stride 1 across threads -> conflict free) and all loops are rolled: the
+// fully unrolled register version compiles to >600 KB of SASS and thrashes the 32 KB instruction
+// cache.  Q1 = A R1^{-1} and Q = Q1 R2^{-1} use the explicit upper-triangular inverses (column-
+// parallel back substitution by R threads), turning the per-row solves into independent dot
+// products; the paper's own solve Ahat R0^T = W keeps row-wise substitution.
+
+// Cholesky of Gs (RB x RB) in place by warp 0: lower part becomes L; writes Ru = L^T (upper,
+// R x R in RB x RB), returns ok and max/min pivot ratio.
+__device__ bool cq_chol_smem(double* Gs, int R, int RB, double* Ru, double* ratio) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  double dmax = 0.0, dmin = 1e308;
+  #pragma unroll 1
+  for (int j = 0; j < R; ++j) {
+    const double piv = Gs[j + RB * j];
+    if (!(piv > 0.0)) ok = false;
+    const double ljj = sqrt(fmax(piv, 0.0));
+    const double inv = (ljj > 0.0) ? 1.0 / ljj : 0.0;
+    dmax = fmax(dmax, ljj);
+    dmin = fmin(dmin, ljj);
+    const int i = lane;
+    double lij = 0.0;
+    if (i > j && i < R) { lij = Gs[i + RB * j] * inv; Gs[i + RB * j] = lij; }
+    __syncwarp();
+    if (i > j && i < R)
+      #pragma unroll 1
+      for (int k = j + 1; k <= i; ++k) Gs[i + RB * k] = fma(-lij, Gs[k + RB * j], Gs[i + RB * k]);
+    __syncwarp();
+    if (lane == 0) Gs[j + RB * j] = ljj;
+    __syncwarp();
+  }
+  #pragma unroll 1
+  for (int e = lane; e < RB * RB; e += 32) {
+    const int r = e % RB, c = e / RB;  // Ru(r, c) = L(c, r)
+    Ru[e] = (r <= c && c < R) ? Gs[c + RB * r] : 0.0;
+  }
+  __syncwarp();
+  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;
+  return ok;
+}
+
+// Ui = Ru^{-1} (upper triangular), column c by thread c (back substitution Ru Ui(:,c) = e_c).
+__device__ void cq_tri_inv(const double* Ru, int R, int RB, double* Ui) {
+  const int c = threadIdx.x;
+  if (c < RB)
+    #pragma unroll 1
+    for (int r = RB - 1; r >= 0; --r) {
+      double v = 0.0;
+      if (c < R && r <= c) {
+        double acc = (r == c) ? 1.0 : 0.0;
+        #pragma unroll 1
+        for (int l = r + 1; l <= c; ++l) acc = fma(-Ru[r + RB * l], Ui[l + RB * c], acc);
+        v = acc / Ru[r + RB * r];
+      }
+      Ui[r + RB * c] = v;
+    }
+}
+
+// Row-panel product Y[tid, :] = X[tid, :] U for the owned row (U upper triangular RB x RB).
+__device__ __forceinline__ void cq_row_times_upper(const double* X, double* Y, int ld, int tid, int R, int RB,
+                                                   const double* U) {
+  double xr[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) xr[l] = (l < R) ? X[tid + ld * l] : 0.0;
+#pragma unroll 1
+  for (int cc = 0; cc < R; ++cc) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int l = 0; l < 32; l += 4) {
+      if (l < RB) {
+        s0 = fma(xr[l], U[l + RB * cc], s0);
+        s1 = fma(xr[l + 1], U[l + 1 + RB * cc], s1);
+        s2 = fma(xr[l + 2], U[l + 2 + RB * cc], s2);
+        s3 = fma(xr[l + 3], U[l + 3 + RB * cc], s3);
+      }
+    }
+    Y[tid + ld * cc] = (s0 + s1) + (s2 + s3);
+  }
+  return;
+  #pragma unroll 1
+  for (int cc = 0; cc < R; ++cc) {
+    double s0 = 0.0, s1 = 0.0;
+    int l = 0;
+    #pragma unroll 1
+    for (; l + 1 <= cc; l += 2) {
+      s0 = fma(X[tid + ld * l], U[l + RB * cc], s0);
+      s1 = fma(X[tid + ld * (l + 1)], U[(l + 1) + RB * cc], s1);
+    }
+    if (l <= cc) s0 = fma(X[tid + ld * l], U[l + RB * cc], s0);
+    Y[tid + ld * cc] = s0 + s1;
+  }
+}
+
+
+// Block-parallel outer-product Cholesky of Gs (RB x RB, R x R used) with tight loops: the tail
+// kernels run once per mode right after the stream pass has flushed L2 and the instruction caches,
+// so their cost is dominated by cold instruction fetches (~600 cycles per 128 B of SASS); this
+// routine is ~2 KB of code.  One barrier per column.  On exit Ru = L^T (upper), invd = 1/L_jj.
+__device__ __noinline__ bool cq_chol_par(double* Gs, int R, int RB, double* Ru, double* invd, double* ratio) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  bool ok = true;
+  double dmax = 0.0, dmin = 1e308;
+  __syncthreads();
+#pragma unroll 1
+  for (int j = 0; j < R; ++j) {
+    const double d = Gs[j + RB * j];
+    if (!(d > 0.0)) ok = false;
+    const double ljj = sqrt(fmax(d, 0.0));
+    dmax = fmax(dmax, ljj);
+    dmin = fmin(dmin, ljj);
+    const double id = (d > 0.0) ? 1.0 / d : 0.0;
+    const int T = R - j - 1;
+#pragma unroll 1
+    for (int e = tid; e < T * T; e += nt) {  // trailing update with the unscaled column j
+      const int i = j + 1 + e / T, k = j + 1 + e % T;
+      if (k <= i) Gs[i + RB * k] = fma(-Gs[i + RB * j] * id, Gs[k + RB * j], Gs[i + RB * k]);
+    }
+    if (tid == 0) invd[j] = (ljj > 0.0) ? 1.0 / ljj : 0.0;
+    __syncthreads();
+  }
+#pragma unroll 1
+  for (int e = tid; e < RB * RB; e += nt) {  // Ru(r, c) = L(c, r) = G(c, r) / L_rr, Ru(r, r) = L_rr
+    const int r = e % RB, c = e / RB;
+    double v = 0.0;
+    if (r < R && c < R && r <= c) v = (r == c) ? sqrt(fmax(Gs[r + RB * r], 0.0)) : Gs[c + RB * r] * invd[r];
+    Ru[e] = v;
+  }
+  __syncthreads();
+  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;
+  return ok;
+}
+
+// Owned-row forward substitution y U = x (U upper, inverse diagonal invd) in place on the panel row.
+__device__ __forceinline__ void cq_row_fwd_subst(double* Prow, int ld, int R, int RB, const double* U,
+                                                 const double* invd) {
+#pragma unroll 1
+  for (int j = 0; j < R; ++j) {
+    double a0 = Prow[ld * j], a1 = 0.0;
+    int l = 0;
+#pragma unroll 1
+    for (; l + 1 < j; l += 2) {
+      a0 = fma(-Prow[ld * l], U[l + RB * j], a0);
+      a1 = fma(-Prow[ld * (l + 1)], U[(l + 1) + RB * j], a1);
+    }
+    if (l < j) a0 = fma(-Prow[ld * l], U[l + RB * j], a0);
+    Prow[ld * j] = (a0 + a1) * invd[j];
+  }
+}
+
+#ifdef CPQR_DEBUG_TIMING
+#define CQ_T(k) do { if (threadIdx.x == 0) tstamp[k] = clock64(); } while (0)
+#define CQ_DUMP() do { if (threadIdx.x == 0 && cluster.block_rank() == 0) printf("cq phases: %lld %lld %lld %lld %lld %lld %lld %lld | lam+sync %lld chol %lld sync %lld inv %lld\n", tstamp[1]-tstamp[0], tstamp[2]-tstamp[1], tstamp[3]-tstamp[2], tstamp[4]-tstamp[3], tstamp[5]-tstamp[4], tstamp[6]-tstamp[5], tstamp[7]-tstamp[6], tstamp[8]-tstamp[7], tstamp[9]-tstamp[3], tstamp[10]-tstamp[9], tstamp[11]-tstamp[10], tstamp[12]-tstamp[11]); } while (0)
+#else
+#define CQ_T(k) do {} while (0)
+#define CQ_DUMP() do {} while (0)
+#endif
+template <int RB>
+__global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
+#ifdef CPQR_DEBUG_TIMING
+  __shared__ long long tstamp[16];
+#endif
+  CQ_T(0);
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double smq[];
+  double* G1b = smq;
+  double* G2b = G1b + RB * RB;
+  double* Gs = G2b + RB * RB;
+  double* R1s = Gs + RB * RB;
+  double* R2s = R1s + RB * RB;
+  double* Ui = R2s + RB * RB;
+  double* Ms = Ui + RB * RB;
+  double* R0s = Ms + RB * RB;
+  __shared__ double lam[RB], redi[8], innerb, inv1[RB], inv2[RB];
+  __shared__ int okf;
+  const int nb = a.nb, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int b = (int)cluster.block_rank();
+  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
+  const int rows4 = (rows + 3) & ~3, ld = (((int)blockDim.x + 15) & ~15) + 4;  // >= every thread's row
+  double* X = R0s + RB * RB;   // panel of Ahat (or A) rows
+  double* Y = X + ld * RB;     // panel of W / Q1 / Q rows
+  const int i = r0 + tid;
+  const bool own = tid < rows;
+  if (tid == 0 && b == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);
+  #pragma unroll 1
+  for (int e = tid; e < 2 * ld * RB; e += blockDim.x) X[e] = 0.0;
+  #pragma unroll 1
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    const int r = e % RB, c = e / RB;
+    Ms[e] = (a.solve && r < R && c < R) ? a.Rm[r + R * c] : 0.0;
+    R0s[e] = (a.solve && r < R && c < R) ? a.R0[r + R * c] : 0.0;
+  }
+  __syncthreads();
+  // ---- 1. panel rows
+  double inner = 0.0;
+  if (own) {
+    if (!a.solve) {
+#pragma unroll 1
+      for (int k = 0; k < R; ++k) X[tid + ld * k] = a.A[i + (int64_t)a.m * k];
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < R; ++k) Y[tid + ld * k] = a.W[(int64_t)i * R + k];  // W row (panel Y)
+      if (a.variant == 2) {  // x = w M, M = U S^+ V^T
+#pragma unroll 1
+        for (int cc = 0; cc < R; ++cc) {
+          double s0 = 0.0, s1 = 0.0;
+          int r = 0;
+#pragma unroll 1
+          for (; r + 1 < R; r += 2) {
+            s0 = fma(Y[tid + ld * r], Ms[r + RB * cc], s0);
+            s1 = fma(Y[tid + ld * (r + 1)], Ms[r + 1 + RB * cc], s1);
+          }
+          if (r < R) s0 = fma(Y[tid + ld * r], Ms[r + RB * cc], s0);
+          X[tid + ld * cc] = s0 + s1;
+        }
+      } else {  // Ahat R0^T = W by back substitution over columns j = R..1
+#pragma unroll 1
+        for (int j = R - 1; j >= 0; --j) {
+          double acc = Y[tid + ld * j], acc1 = 0.0;
+          int l = j + 1;
+#pragma unroll 1
+          for (; l + 1 < R; l += 2) {
+            acc = fma(-X[tid + ld * l], Ms[j + RB * l], acc);
+            acc1 = fma(-X[tid + ld * (l + 1)], Ms[j + RB * (l + 1)], acc1);
+          }
+          if (l < R) acc = fma(-X[tid + ld * l], Ms[j + RB * l], acc);
+          X[tid + ld * j] = (acc + acc1) / Ms[j + RB * j];
+        }
+      }
+      if (a.do_fit)  // <W, Ahat R0^T>: sum_c w_c sum_{l>=c} x_l R0(c,l)
+#pragma unroll 1
+        for (int cc = 0; cc < R; ++cc) {
+          double tt = 0.0;
+#pragma unroll 1
+          for (int l = cc; l < R; ++l) tt = fma(X[tid + ld * l], R0s[cc + RB * l], tt);
+          inner = fma(Y[tid + ld * cc], tt, inner);
+        }
+#pragma unroll 1
+      for (int k = 0; k < R; ++k) a.Ahat[i + (int64_t)a.m * k] = X[tid + ld * k];
+    }
+  }
+  inner = warp_sum(inner);
+  if (lane == 0) redi[wid] = inner;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    #pragma unroll 1
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) v += redi[q];
+    innerb = v;
+  }
+  CQ_T(1);
+  // ---- 2. Gram of the panel, cluster sum, Cholesky -> R1, R1^{-1}
+  cq_gram_dmma<RB>(X, ld, rows4, G1b);
+  CQ_T(2);
+  cluster.sync();
+  #pragma unroll 1
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    double s = 0.0;
+    #pragma unroll 1
+    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G1b, c)[e];
+    Gs[e] = s;
+  }
+  double inner_all = 0.0;
+  #pragma unroll 1
+  for (int c = 0; c < nb; ++c) inner_all += *cluster.map_shared_rank(&innerb, c);
+  __syncthreads();
+  CQ_T(3);
+  if (a.solve && tid < R) lam[tid] = sqrt(Gs[tid + RB * tid]);  // lambda_c = ||Ahat(:,c)||_2
+  __syncthreads();
+  CQ_T(9);
+  {
+    double ratio;
+    const bool ok = cq_chol_par(Gs, R, RB, R1s, inv1, &ratio);
+    if (tid == 0) okf = ok && ratio < kCqKappaMax;
+  }
+  CQ_T(10);
+  __syncthreads();
+  CQ_T(11);
+  if (!okf) {
+    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    cluster.sync();
+    return;
+  }
+
+  CQ_T(12);
+  __syncthreads();
+  CQ_T(4);
+  // ---- 3. Q1 = X R1^{-1}, Gram, Cholesky -> R2, R2^{-1}
+  if (own) {
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) Y[tid + ld * k] = X[tid + ld * k];
+    cq_row_fwd_subst(Y + tid, ld, R, RB, R1s, inv1);
+  } else for (int k = 0; k < RB; ++k) Y[tid + ld * k] = 0.0;
+  __syncthreads();
+  CQ_T(5);
+  cq_gram_dmma<RB>(Y, ld, rows4, G2b);
+  cluster.sync();
+  #pragma unroll 1
+  for (int e = tid; e < RB * RB; e += blockDim.x) {
+    double s = 0.0;
+    #pragma unroll 1
+    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G2b, c)[e];
+    Gs[e] = s;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    double e = 0.0;  // ||G2 - I||_max must be O(kappa^2 eps)
+    #pragma unroll 1
+    for (int q = lane; q < R * R; q += 32) {
+      const int r = q % R, c = q / R;
+      e = fmax(e, fabs(Gs[r + RB * c] - (r == c ? 1.0 : 0.0)));
+    }
+    #pragma unroll 1
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+    if (lane == 0) okf = (e < 1.0e-4);
+  }
+  {
+    double ratio;
+    const bool ok = cq_chol_par(Gs, R, RB, R2s, inv2, &ratio);
+    if (tid == 0) okf = okf && ok;
+  }
+  __syncthreads();
+  if (!okf) {
+    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    cluster.sync();
+    return;
+  }
+
+  __syncthreads();
+  CQ_T(6);
+  // ---- 4. Q = Q1 R2^{-1} (into X, Ahat is kept in global), outputs
+  if (own) {
+#pragma unroll 1
+    for (int k = 0; k < R; ++k) X[tid + ld * k] = Y[tid + ld * k];
+    cq_row_fwd_subst(X + tid, ld, R, RB, R2s, inv2);
+    #pragma unroll 1
+    for (int k = 0; k < R; ++k) a.Q[i + (int64_t)a.m * k] = X[tid + ld * k];
+    #pragma unroll 1
+    for (int k = 0; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? X[tid + ld * k] : 0.0;
+    if (a.solve)
+      #pragma unroll 1
+      for (int k = 0; k < R; ++k) {
+        const double l = lam[k];
+        const int64_t e = i + (int64_t)a.m * k;
+        a.Aout[e] = (l > 0.0) ? a.Ahat[e] / l : (i == 0 ? 1.0 : 0.0);
+      }
+  }
+  CQ_T(7);
+  if (b == 0) {
+    #pragma unroll 1
+    for (int e = tid; e < RB * RB; e += blockDim.x) {  // R_n = R2 R1 diag(1/lambda)
+      const int r = e % RB, c = e / RB;
+      double s = 0.0;
+      if (r <= c && c < R)
+        #pragma unroll 1
+        for (int k = r; k <= c; ++k) s = fma(R2s[r + RB * k], R1s[k + RB * c], s);
+      if (a.solve && c < R && lam[c] > 0.0) s /= lam[c];
+      Gs[e] = s;
+      if (r < R && c < R) a.Rn[r + R * c] = s;
+    }
+    if (a.solve && tid < R) {
+      a.lam[tid] = lam[tid];
+      if (!isfinite(lam[tid])) atomicOr(a.flags, FLAG_NONFINITE);
+    }
+    if (a.do_fit) {  // ||Xh||^2 = <R0^T R0, diag(lam) R_n^T R_n diag(lam)>
+      __syncthreads();
+      double qq = 0.0;
+      #pragma unroll 1
+      for (int e = tid; e < R * R; e += blockDim.x) {
+        const int xx = e % R, yy = e / R;
+        double g0 = 0.0, g1 = 0.0;
+        #pragma unroll 1
+        for (int k = 0; k <= min(xx, yy); ++k) {
+          g0 = fma(R0s[k + RB * xx], R0s[k + RB * yy], g0);
+          g1 = fma(Gs[k + RB * xx], Gs[k + RB * yy], g1);
+        }
+        qq = fma(g0, lam[xx] * lam[yy] * g1, qq);
+      }
+      qq = warp_sum(qq);
+      if (lane == 0) redi[wid] = qq;
+      __syncthreads();
+      if (tid == 0) {
+        double nxh2 = 0.0;
+        #pragma unroll 1
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) nxh2 += redi[w];
+        const double nx2 = *a.nX2;
+        *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner_all + nxh2)) / sqrt(nx2);
+      }
+    }
+  }
+  CQ_T(8);
+  cluster.sync();  // no CTA leaves while peers may read its shared memory
+  CQ_DUMP();
+}
+
+}  // namespace cpqr

@@ -3,6 +3,8 @@
 // Alg. 1 lines 6-11 for CP-ALS.  See DESIGN.md for the kernel map.
 #include "../../include/cpqr.h"
 #include "qr_kernels.cuh"
+#include "rowqr.cuh"
+#include "cholqr.cuh"
 #include "small_kernels.cuh"
 #include "tma_kernels.cuh"
 #include "ttm_kernels.cuh"
@@ -92,7 +94,10 @@ struct cpqr_ctx {
   cudaEvent_t evf = nullptr, evj = nullptr;
   double *dRstack = nullptr, *dV = nullptr, *dtauv = nullptr, *dQtop = nullptr, *dinner = nullptr;
   double* dMpinv = nullptr;
+  double *dQ1 = nullptr, *dGp = nullptr, *dinnerp = nullptr, *dR1 = nullptr, *dR2 = nullptr;
+  int factor_qr_mode = 0;  // 0 auto (CholeskyQR2, Householder fallback), 1 Householder only
   int nparts = 0;
+  int stream_sms = 148;  // CTAs of the stream-X kernels (one SM left to the concurrent V_n QR)
   double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWloc = nullptr,
          *dWp = nullptr, *dAhat = nullptr;
   double* buf[2] = {nullptr, nullptr};
@@ -576,16 +581,16 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
 cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
   for (const TtmStep& s : p.steps) {
     switch (s.kind) {
-      case 0: launch_strided(s, c->R, c->st, c->sms); break;
-      case 1: launch_fiber(s, c->R, c->st, c->sms); break;
-      case 2: launch_slice(s, c->R, c->st, c->sms); break;
+      case 0: launch_strided(s, c->R, c->st, c->stream_sms); break;
+      case 1: launch_fiber(s, c->R, c->st, c->stream_sms); break;
+      case 2: launch_slice(s, c->R, c->st, c->stream_sms); break;
       case 3: {
         const int64_t n = s.L * c->R * c->R;
         const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sms * 8);
         k_reduce_slices<<<grid, 256, 0, c->st>>>(s.in, s.nseg, s.L, c->R * c->R, s.out);
         break;
       }
-      default: launch_tma(s, c->R, c->st, c->sms); break;
+      default: launch_tma(s, c->R, c->st, c->stream_sms); break;
     }
     CKL();
   }
@@ -618,7 +623,7 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
   in.n = n;
   in.ne = ne;
   in.tma = c->use_tma;
-  in.sms = c->sms;
+  in.sms = c->stream_sms;
   in.RQ = c->RQ;
   for (int k = 0; k < c->N; ++k) {
     const double* base = ne ? c->dA[k] : c->dQ[k];
@@ -710,41 +715,232 @@ cpqr_status launch_normalize(cpqr_ctx* c, int In, double* A) {
   return CPQR_OK;
 }
 
-// thin QR (TSQR) of the m x R column-major A -> Q (column-major), Qt (padded row-major), Rn.
-cpqr_status launch_factor_qr(cpqr_ctx* c, const double* A, int m, double* Q, double* Qt, double* Rn,
-                             bool do_fit) {
-  const int R = c->R;
+// TSQR launcher.  solve = false: thin QR of the m x R column-major A -> Q, Qt, Rn.
+// solve = true: the fused per-mode tail -- Ahat from W (and R0 / M), lambda, A_n = Ahat/lambda into
+// Aout, and the QR of A_n (Q, Qt, Rn), plus the fast fit when do_fit.
+cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const double* W, double* Q,
+                        double* Qt, double* Rn, double* Aout, bool do_fit) {
+  const int R = c->R, RB = rb_for(R);
   int nleaf = std::max(1, std::min(8, (m + 127) / 128));
   int mb = (m + nleaf - 1) / nleaf;
   while (nleaf > 1 && m - (nleaf - 1) * mb < R) { --nleaf; mb = (m + nleaf - 1) / nleaf; }
-  const size_t leaf_smem = (size_t)mb * R * 8, qf_smem = 2 * leaf_smem, root_smem = (size_t)std::max(nleaf, 2) * R * R * 8;
-  if (qf_smem > 200 * 1024) {  // very tall factors: single-CTA global-memory Householder
-    if (do_fit) return fail(c, CPQR_EINVAL, "factor too tall for the TSQR path with fast fit");
+  const size_t leaf_smem = (size_t)mb * R * 8, qf_smem = 2 * leaf_smem,
+               root_smem = (size_t)std::max(nleaf, 2) * R * R * 8;
+  if (qf_smem > 200 * 1024) {  // very tall factors: unfused kernels, global-memory Householder
+    if (do_fit) return fail(c, CPQR_EINVAL, "factor too tall for the fused tail with fast fit");
+    if (solve) {
+      TRY(launch_solve(c, W, m, false, nullptr));
+      TRY(launch_normalize(c, m, Aout));
+      A = Aout;
+    }
     k_factor_qr<<<1, 1024, 0, c->st>>>(A, m, R, Q, Rn);
     CKL();
     k_transpose_pad<<<64, 256, 0, c->st>>>(Q, m, m, R, c->RQ, Qt);
     CKL();
     return CPQR_OK;
   }
+  // fast path: CholeskyQR2 (cholqr.cuh); the Householder kernels below then run gated
+  bool gated = false;
+  const int nbq = (m + 255) / 256;
+  if (c->factor_qr_mode == 0 && nbq <= 8 && !getenv("CPQR_CQ_MULTI")) {  // single cluster launch
+    CqArgs q{};
+    const int mbq = (m + nbq - 1) / nbq;
+    q.A = A; q.m = m; q.R = R; q.nb = nbq; q.mb = mbq; q.solve = solve ? 1 : 0; q.W = W;
+    q.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0; q.R0 = c->dR0; q.variant = c->variant;
+    q.Ahat = c->dAhat; q.Q1 = c->dQ1; q.Gp = c->dGp; q.innerp = c->dinnerp; q.R1 = c->dR1; q.R2 = c->dR2;
+    q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
+    q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
+    if (solve && c->variant == CPQR_SVD) {
+      const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
+      const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+      k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
+      CKL();
+    }
+    const int tb = 32 * ((mbq + 31) / 32);
+    const int ld = ((tb + 15) & ~15) + 4;
+    const bool compact = !getenv("CPQR_CQ_UNROLLED");
+    const size_t smem = compact ? (size_t)(8 * RB * RB + 2 * ld * RB) * sizeof(double)
+                                : (size_t)(7 * RB * RB + ld * RB) * sizeof(double);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nbq);
+    cfg.blockDim = dim3(tb);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nbq;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    switch (RB) {
+      case 8:
+        if (compact) {
+          cudaFuncSetAttribute(k_cq_compact<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          e = cudaLaunchKernelEx(&cfg, k_cq_compact<8>, q);
+        } else {
+          cudaFuncSetAttribute(k_cq_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          e = cudaLaunchKernelEx(&cfg, k_cq_fused<8>, q);
+        }
+        break;
+      case 16:
+        if (compact) {
+          cudaFuncSetAttribute(k_cq_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          e = cudaLaunchKernelEx(&cfg, k_cq_compact<16>, q);
+        } else {
+          cudaFuncSetAttribute(k_cq_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          e = cudaLaunchKernelEx(&cfg, k_cq_fused<16>, q);
+        }
+        break;
+      default:
+        if (compact) {
+          cudaFuncSetAttribute(k_cq_compact<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          e = cudaLaunchKernelEx(&cfg, k_cq_compact<32>, q);
+        } else {
+          cudaFuncSetAttribute(k_cq_fused<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          e = cudaLaunchKernelEx(&cfg, k_cq_fused<32>, q);
+        }
+        break;
+    }
+    if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_cq_fused launch: %s", cudaGetErrorString(e));
+    CKL();
+    gated = true;
+  } else if (c->factor_qr_mode == 0) {
+    CqArgs q{};
+    const int nb = (m + 255) / 256, mbq = (m + nb - 1) / nb;
+    q.A = A; q.m = m; q.R = R; q.nb = nb; q.mb = mbq; q.solve = solve ? 1 : 0; q.W = W;
+    q.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0; q.R0 = c->dR0; q.variant = c->variant;
+    q.Ahat = c->dAhat; q.Q1 = c->dQ1; q.Gp = c->dGp; q.innerp = c->dinnerp; q.R1 = c->dR1; q.R2 = c->dR2;
+    q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
+    q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
+    if (solve && c->variant == CPQR_SVD) {
+      const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
+      const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+      k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
+      CKL();
+    }
+    const int tb = 32 * ((mbq + 31) / 32);
+    const size_t psm = (size_t)(mbq | 1) * R * 8;
+    static bool cq_attr = false;
+    if (!cq_attr) {
+      cudaFuncSetAttribute(k_cq_gram1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_cq_gram1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_cq_gram1<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_cq_apply<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_cq_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(k_cq_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cq_attr = true;
+    }
+    switch (RB) {
+      case 8:
+        k_cq_gram1<8><<<nb, tb, psm, c->st>>>(q); CKL();
+        k_cq_chol1<<<1, 256, 0, c->st>>>(q); CKL();
+        k_cq_apply<8><<<nb, tb, psm, c->st>>>(q, 1); CKL();
+        k_cq_chol2<<<1, 256, 0, c->st>>>(q, nullptr); CKL();
+        k_cq_apply<8><<<nb, tb, psm, c->st>>>(q, 2); CKL();
+        break;
+      case 16:
+        k_cq_gram1<16><<<nb, tb, psm, c->st>>>(q); CKL();
+        k_cq_chol1<<<1, 256, 0, c->st>>>(q); CKL();
+        k_cq_apply<16><<<nb, tb, psm, c->st>>>(q, 1); CKL();
+        k_cq_chol2<<<1, 256, 0, c->st>>>(q, nullptr); CKL();
+        k_cq_apply<16><<<nb, tb, psm, c->st>>>(q, 2); CKL();
+        break;
+      default:
+        k_cq_gram1<32><<<nb, tb, psm, c->st>>>(q); CKL();
+        k_cq_chol1<<<1, 256, 0, c->st>>>(q); CKL();
+        k_cq_apply<32><<<nb, tb, psm, c->st>>>(q, 1); CKL();
+        k_cq_chol2<<<1, 256, 0, c->st>>>(q, nullptr); CKL();
+        k_cq_apply<32><<<nb, tb, psm, c->st>>>(q, 2); CKL();
+        break;
+    }
+    gated = true;
+  }
+  // register-resident Householder TSQR (one thread per row) whenever leaves and root fit in 256 rows
+  {
+    int nl = std::max(1, (m + 255) / 256);
+    int mbr = (m + nl - 1) / nl;
+    while (nl > 1 && m - (nl - 1) * mbr < R) { --nl; mbr = (m + nl - 1) / nl; }
+    if (nl <= 8 && mbr <= 256 && nl * R <= 256 && !getenv("CPQR_SMEM_QR")) {
+      RqArgs q{};
+      q.A = A; q.m = m; q.R = R; q.nleaf = nl; q.mb = mbr;
+      q.Rstack = c->dRstack; q.V = c->dV; q.tauv = c->dtauv; q.Qtop = c->dQtop;
+      q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn;
+      q.solve = solve ? 1 : 0; q.W = W; q.R0 = c->dR0;
+      q.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0;
+      q.variant = c->variant;
+      q.Ahat = c->dAhat; q.part = c->dred; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
+      q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
+      q.gated = gated ? 1 : 0;
+      if (solve && c->variant == CPQR_SVD && !gated) {
+        const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
+        const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+        k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
+        CKL();
+      }
+      const int tl = 32 * ((mbr + 31) / 32), tr = 32 * ((nl * R + 31) / 32);
+      switch (RB) {
+        case 8:
+          k_rq_leaf<8><<<nl, tl, 0, c->st>>>(q); CKL();
+          k_rq_root<8><<<1, tr, 0, c->st>>>(q); CKL();
+          k_rq_qform<8><<<nl, tl, 0, c->st>>>(q); CKL();
+          break;
+        case 16:
+          k_rq_leaf<16><<<nl, tl, 0, c->st>>>(q); CKL();
+          k_rq_root<16><<<1, tr, 0, c->st>>>(q); CKL();
+          k_rq_qform<16><<<nl, tl, 0, c->st>>>(q); CKL();
+          break;
+        default:
+          k_rq_leaf<32><<<nl, tl, 0, c->st>>>(q); CKL();
+          k_rq_root<32><<<1, tr, 0, c->st>>>(q); CKL();
+          k_rq_qform<32><<<nl, tl, 0, c->st>>>(q); CKL();
+          break;
+      }
+      return CPQR_OK;
+    }
+  }
   TsqrArgs a{};
   a.A = A; a.m = m; a.R = R; a.nleaf = nleaf; a.mb = mb;
   a.Rstack = c->dRstack; a.V = c->dV; a.tauv = c->dtauv; a.Qtop = c->dQtop;
   a.Q = Q; a.Qt = Qt; a.RQ = c->RQ; a.Rn = Rn;
-  a.do_fit = do_fit ? 1 : 0; a.R0 = c->dR0; a.lam = c->dlam; a.inner = c->dinner; a.nX2 = c->dnX2; a.fit = c->dfit;
+  a.solve = solve ? 1 : 0;
+  a.W = W;
+  a.R0 = c->dR0;
+  a.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0;
+  a.variant = c->variant;
+  a.Ahat = c->dAhat; a.part = c->dred; a.Aout = Aout; a.lam = c->dlam; a.flags = c->dflags;
+  a.do_fit = do_fit ? 1 : 0; a.nX2 = c->dnX2; a.fit = c->dfit;
+  if (solve && c->variant == CPQR_SVD) {
+    const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
+    const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+    k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
+    CKL();
+  }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_tsqr_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_leaf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_leaf<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tsqr_leaf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tsqr_root, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tsqr_qform, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     attr = true;
   }
-  k_tsqr_leaf<<<nleaf, 512, leaf_smem, c->st>>>(a);
+  switch (RB) {
+    case 8: k_tsqr_leaf<8><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
+    case 16: k_tsqr_leaf<16><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
+    default: k_tsqr_leaf<32><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
+  }
   CKL();
   k_tsqr_root<<<1, 512, root_smem, c->st>>>(a);
   CKL();
   k_tsqr_qform<<<nleaf, 512, qf_smem, c->st>>>(a);
   CKL();
   return CPQR_OK;
+}
+
+cpqr_status launch_factor_qr(cpqr_ctx* c, const double* A, int m, double* Q, double* Qt, double* Rn, bool do_fit) {
+  return launch_tsqr(c, m, A, false, nullptr, Q, Qt, Rn, nullptr, do_fit);
 }
 
 cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
@@ -871,12 +1067,9 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   TRY(launch_q0_apply(c, p, Wloc));
   TRY(combine_w(c, n, Wloc, c->dW));
   prof_mark(c, 4);
-  // lines 10-11: solve / SVD, lambda, normalise (+ <W, Ahat R0^T> for the fit)
+  // lines 10-12: solve (substitution / SVD), lambda, normalise, factor QR (+ fast fit after mode N)
   const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
-  TRY(launch_solve(c, c->dW, In, fit, nullptr));
-  TRY(launch_normalize(c, In, c->dA[n]));
-  // line 12: factor QR of the updated factor (TSQR) -> Q_n, its TMA panel, R_n (+ fast fit)
-  TRY(launch_factor_qr(c, c->dA[n], In, c->dQ[n], c->dQt[n], c->dRk[n], fit));
+  TRY(launch_tsqr(c, In, nullptr, true, c->dW, c->dQ[n], c->dQt[n], c->dRk[n], c->dA[n], fit));
   prof_mark(c, 5);
   (void)last;
   return CPQR_OK;
@@ -1053,6 +1246,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   std::memset(&c->prof, 0, sizeof c->prof);
   if (cudaSetDevice(c->opt.device) != cudaSuccess) return fail(c, CPQR_ECUDA, "cudaSetDevice(%d)", c->opt.device);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->opt.device);
+  c->stream_sms = (c->variant == CPQR_NE || getenv("CPQR_ALL_SMS")) ? c->sms : std::max(1, c->sms - 1);
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->user = (cudaStream_t)c->opt.stream;
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -1087,6 +1281,15 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(cudaMalloc(&c->dtauv, sizeof(double) * 8 * R));
   CK(cudaMalloc(&c->dinner, sizeof(double) * 4));
   CK(cudaMalloc(&c->dMpinv, sizeof(double) * R * R));
+  CK(cudaMalloc(&c->dQ1, sizeof(double) * imax * R));
+  CK(cudaMalloc(&c->dGp, sizeof(double) * ((imax + 255) / 256 + 1) * R * R));
+  CK(cudaMalloc(&c->dinnerp, sizeof(double) * ((imax + 255) / 256 + 1)));
+  CK(cudaMalloc(&c->dR1, sizeof(double) * R * R));
+  CK(cudaMalloc(&c->dR2, sizeof(double) * R * R));
+  {
+    const char* f = getenv("CPQR_FACTOR_QR");
+    c->factor_qr_mode = (f && std::string(f) == "householder") ? 1 : 0;
+  }
   c->wp_elems = (size_t)imax * R * 1024;
   CK(cudaMalloc(&c->dWp, sizeof(double) * std::min<size_t>(c->wp_elems, (size_t)imax * R * (size_t)std::max<int64_t>(1, (J + 63) / 64))));
   CK(cudaMalloc(&c->dnX2, sizeof(double) * 4));
@@ -1146,7 +1349,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->evf) cudaEventDestroy(c->evf);
   if (c->evj) cudaEventDestroy(c->evj);
-  double* ps[] = {c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
+  double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown};
   for (double* p : ps) if (p) cudaFree(p);
   if (c->dperm) cudaFree(c->dperm);

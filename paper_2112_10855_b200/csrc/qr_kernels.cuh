@@ -62,17 +62,47 @@ __device__ __forceinline__ void hh_make_reflector(const Cols& M, int j, double* 
 }
 
 // Factorisation.  On exit: col(k)[r] (r < k) = R(r, k) (unsigned), beta[k] = R(k, k), reflector
-// j stored below the diagonal of column j, tau[j].  All threads of the block must call.
+// j (v_j = 1 implicit) stored below the diagonal of column j, tau[j].  All threads must call;
+// `w` needs R doubles, `np` 64 doubles of shared memory.
+// Per column two block barriers and no serial section: (A) one warp per trailing column forms
+// w_k = col(k)[j] + scale_j sum_{i>j} col(j)[i] col(k)[i] (the reflector is scaled lazily);
+// (B) each thread owns rows: writes v_i = scale_j col(j)[i], applies H_j to all trailing columns
+// and accumulates its share of ||col(j+1)[j+2..]||^2; (C) every thread rebuilds beta/tau/scale of
+// column j+1 from the per-warp partials (identical arithmetic everywhere, fixed summation order).
 template <class Cols>
-__device__ void hh_factor(const Cols& M, int R, double* tau, double* beta, double* w) {
+__device__ __forceinline__ void hh_reflector_from(const Cols& M, int j, const double* np, int nw, double& tj,
+                                                  double& bj, double& sc) {
+  double s = 0.0;
+  for (int q = 0; q < nw; ++q) s += np[q];
+  const double x0 = M.col(j)[j];
+  if (s == 0.0) { tj = 0.0; bj = x0; sc = 0.0; }
+  else {
+    const double nrm = sqrt(x0 * x0 + s);
+    bj = (x0 >= 0.0) ? -nrm : nrm;
+    tj = (bj - x0) / bj;
+    sc = 1.0 / (x0 - bj);
+  }
+}
+
+template <class Cols>
+__device__ void hh_factor(const Cols& M, int R, double* tau, double* beta, double* w, double* np) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  if (wid == 0) hh_make_reflector(M, 0, tau, beta);
+  {  // column 0 norm partials
+    const double* c0 = M.col(0);
+    double q = 0.0;
+    for (int i = 1 + tid; i < M.rows(0); i += nt) q = fma(c0[i], c0[i], q);
+    q = warp_sum(q);
+    if (lane == 0) np[32 + wid] = q;
+  }
   __syncthreads();
+  double tj, bj, sc;
+  hh_reflector_from(M, 0, np + 32, nw, tj, bj, sc);
   for (int j = 0; j < R; ++j) {
-    const double tj = tau[j];
-    const double* vj = M.col(j);
+    double* vj = M.col(j);
     const int mj = M.rows(j);
-    if (tj != 0.0) {  // w_k = A(j,k) + sum_{i>j} v_i A(i,k): one warp per column, 4 partial sums
+    if (tid == 0) { tau[j] = tj; beta[j] = bj; }
+    // (A) dots with the (still unscaled) reflector
+    if (tj != 0.0) {
       for (int k = j + 1 + wid; k < R; k += nw) {
         const double* ck = M.col(k);
         double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
@@ -85,33 +115,40 @@ __device__ void hh_factor(const Cols& M, int R, double* tau, double* beta, doubl
         }
         for (; i < mj; i += 32) d0 = fma(vj[i], ck[i], d0);
         const double d = warp_sum((d0 + d1) + (d2 + d3));
-        if (lane == 0) w[k] = ck[j] + d;
+        if (lane == 0) w[k] = tj * (ck[j] + sc * d);  // tau_j * (v^T col k)
       }
     }
     __syncthreads();
-    if (wid == 0) {
-      if (j + 1 < R) {
-        double* ck = M.col(j + 1);
-        if (tj != 0.0) {
-          const double wk = tj * w[j + 1];
-          for (int i = j + lane; i < mj; i += 32) ck[i] -= wk * ((i == j) ? 1.0 : vj[i]);
-        }
-        __syncwarp();
-        hh_make_reflector(M, j + 1, tau, beta);
+    // (B) scale v, apply H_j, partial norm of column j+1 (rows > j+1)
+    const int mnext = (j + 1 < R) ? M.rows(j + 1) : 0;
+    double q = 0.0;
+    const int iend = max(mj, mnext);
+    for (int i = j + tid; i < iend; i += nt) {
+      double vi = 0.0;
+      if (i < mj) {
+        if (i == j) { vi = 1.0; vj[j] = bj; }
+        else { vi = sc * vj[i]; vj[i] = vi; }
       }
-    } else if (tj != 0.0 && j + 2 < R) {
-      for (int i = j + tid - 32; i < mj; i += nt - 32) {
-        const double vi = (i == j) ? tj : tj * vj[i];
+      if (tj != 0.0 && i < mj) {
 #pragma unroll 8
-        for (int k = j + 2; k < R; ++k) M.col(k)[i] -= w[k] * vi;
+        for (int k = j + 1; k < R; ++k) M.col(k)[i] -= w[k] * vi;
+      }
+      if (j + 1 < R && i > j + 1 && i < mnext) {
+        const double x = M.col(j + 1)[i];
+        q = fma(x, x, q);
       }
     }
+    q = warp_sum(q);
+    double* npj = np + 32 * (j & 1);  // double-buffered: (C) of step j reads what (B) of step j+1 must not overwrite
+    if (lane == 0) npj[wid] = q;
     __syncthreads();
+    // (C) reflector of column j+1, redundantly in every thread
+    if (j + 1 < R) hh_reflector_from(M, j + 1, npj, nw, tj, bj, sc);
   }
 }
 
 // Explicit Q in place (dorg2r), after hh_factor (R must have been saved first).  Columns are NOT
-// sign-fixed here.
+// sign-fixed here.  Two barriers per column: dots, then the row-owned update + finalisation.
 template <class Cols>
 __device__ void hh_formq(const Cols& M, int R, const double* tau, double* w) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -132,24 +169,31 @@ __device__ void hh_formq(const Cols& M, int R, const double* tau, double* w) {
         }
         for (; i < mj; i += 32) d0 = fma(cj[i], ck[i], d0);
         const double d = warp_sum((d0 + d1) + (d2 + d3));
-        if (lane == 0) w[k] = ck[j] + d;  // v_j = 1; row j of column k is 0 (zeroed earlier)
+        if (lane == 0) w[k] = tj * (ck[j] + d);  // v_j = 1; row j of column k is 0 (zeroed earlier)
       }
-      __syncthreads();
-      for (int i = j + tid; i < mj; i += nt) {
-        const double vi = (i == j) ? tj : tj * cj[i];
+    }
+    __syncthreads();
+    for (int i = tid; i < mj; i += nt) {
+      if (i >= j && j < R - 1 && tj != 0.0) {
+        const double vi = (i == j) ? 1.0 : cj[i];
 #pragma unroll 8
         for (int k = j + 1; k < R; ++k) M.col(k)[i] -= w[k] * vi;
       }
-      __syncthreads();
+      cj[i] = (i < j) ? 0.0 : ((i == j) ? 1.0 - tj : -tj * cj[i]);
     }
-    for (int i = tid; i < mj; i += nt) cj[i] = (i < j) ? 0.0 : ((i == j) ? 1.0 - tj : -tj * cj[i]);
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------------------ TSQR (K1)
+// Fused per-mode tail in three launches (leaf / root / qform).  With solve = 1 the leaf first
+// solves its rows of Ahat (Alg. 2 line 10: substitution with R0, or W M with M = (R0^T)^+ for the
+// SVD variant) straight into the shared-memory panel, and the TSQR factors Ahat itself: since
+// Ahat = A diag(lambda), QR(A) has the same Q and R_n = R_hat diag(1/lambda) (positive scaling keeps
+// diag(R) >= 0), so the leaf needs no grid-wide column norms.  The root turns the per-leaf partial
+// sums of squares into lambda; qform writes Q_n, its TMA panel and A_n = Ahat / lambda.
 struct TsqrArgs {
-  const double* A;  // m x R column-major (lda = m)
+  const double* A;  // solve = 0: m x R column-major input
   int m, R, nleaf, mb;  // leaf b: rows [b*mb, min(m, (b+1)*mb))
   double* Rstack;   // (nleaf*R) x R column-major
   double* V;        // leaf reflectors: mb x R per leaf, column-major, leaf stride mb*R
@@ -159,47 +203,137 @@ struct TsqrArgs {
   double* Qt;       // out: m x RQ row-major, zero padded
   int RQ;
   double* Rn;       // out: R x R column-major, diag >= 0
+  // solve mode
+  int solve;
+  const double* W;    // m x R row-major
+  const double* Rm;   // R0 (variant 1) or M (variant 2)
+  const double* R0;   // R0 (fit)
+  int variant;
+  double* Ahat;       // out: m x R column-major (unnormalised)
+  double* part;       // nleaf x (R+1): column sums of squares, <W, Ahat R0^T>
+  double* Aout;       // out: normalised factor (qform)
+  double* lam;        // out: lambda (root)
+  unsigned* flags;
   // fast fit after mode N: ||Xh||^2 = <R0^T R0, diag(lam) Rn^T Rn diag(lam)>
   int do_fit;
-  const double* R0;
-  const double* lam;
-  const double* inner;  // <W, Ahat R0^T>
   const double* nX2;
   double* fit;
 };
 
-__global__ void __launch_bounds__(512) k_tsqr_leaf(TsqrArgs a) {
+template <int RB>
+__global__ void __launch_bounds__(256) k_tsqr_leaf(TsqrArgs a) {
   extern __shared__ double sm[];
-  __shared__ double tau[64], beta[64], w[64];
-  const int b = blockIdx.x, R = a.R;
+  __shared__ double tau[64], beta[64], w[64], red[8][RB + 1], np[64];
+  __shared__ double Ms[RB * RB], R0s[RB * RB];
+  const int b = blockIdx.x, R = a.R, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
-  for (int c = 0; c < R; ++c)
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) sm[i + rows * c] = a.A[r0 + i + (int64_t)a.m * c];
-  __syncthreads();
+  if (!a.solve) {
+    for (int c = 0; c < R; ++c)
+      for (int i = tid; i < rows; i += nt) sm[i + rows * c] = a.A[r0 + i + (int64_t)a.m * c];
+    __syncthreads();
+  } else {
+    for (int e = tid; e < RB * RB; e += nt) {
+      const int r = e % RB, c = e / RB;
+      Ms[e] = (r < R && c < R) ? a.Rm[r + R * c] : 0.0;
+      R0s[e] = (r < R && c < R) ? a.R0[r + R * c] : 0.0;
+    }
+    __syncthreads();
+    double inner = 0.0;
+    for (int ii = tid; ii < rows; ii += nt) {
+      const int i = r0 + ii;
+      double wv[RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) wv[r] = (r < R) ? a.W[(int64_t)i * R + r] : 0.0;
+      double* x = sm + ii;  // x[l] at x[rows * l]
+      if (a.variant == 2) {
+#pragma unroll 4
+        for (int c = 0; c < RB; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int r = 0; r < RB; ++r) s = fma(wv[r], Ms[r + RB * c], s);
+          if (c < R) x[rows * c] = s;
+        }
+      } else {
+        double xr[RB];
+#pragma unroll
+        for (int j = RB - 1; j >= 0; --j) {  // xr_j = (w_j - sum_{l>j} xr_l R0(j,l)) / R0(j,j)
+          double acc = wv[j];
+#pragma unroll
+          for (int l = j + 1; l < RB; ++l) acc = fma(-xr[l], Ms[j + RB * l], acc);
+          xr[j] = (j < R) ? acc / Ms[j + RB * j] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < RB; ++c)
+          if (c < R) x[rows * c] = xr[c];
+      }
+      if (a.do_fit) {  // <W, Ahat R0^T> row contribution: sum_c w_c sum_{l>=c} x_l R0(c,l)
+#pragma unroll 4
+        for (int c = 0; c < RB; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int l = 0; l < RB; ++l)
+            if (l >= c && l < R) t = fma(x[rows * l], R0s[c + RB * l], t);
+          inner = fma(wv[c], t, inner);
+        }
+      }
+    }
+    __syncthreads();
+    // Ahat rows out, per-leaf column sums of squares and fit partial (fixed order)
+    for (int c = 0; c < R; ++c)
+      for (int ii = tid; ii < rows; ii += nt) a.Ahat[r0 + ii + (int64_t)a.m * c] = sm[ii + rows * c];
+    for (int c = wid; c < R; c += nt / 32) {
+      double q = 0.0;
+      for (int ii = lane; ii < rows; ii += 32) q = fma(sm[ii + rows * c], sm[ii + rows * c], q);
+      q = warp_sum(q);
+      if (lane == 0) a.part[b * (R + 1) + c] = q;
+    }
+    inner = warp_sum(inner);
+    if (lane == 0) red[wid][0] = inner;
+    __syncthreads();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int q = 0; q < nt / 32; ++q) v += red[q][0];
+      a.part[b * (R + 1) + R] = v;
+    }
+  }
   DenseCols M{sm, rows, rows};
-  hh_factor(M, R, tau, beta, w);
+  hh_factor(M, R, tau, beta, w, np);
   const int ldr = a.nleaf * R;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+  for (int e = tid; e < R * R; e += nt) {
     const int r = e % R, c = e / R;
     a.Rstack[b * R + r + (int64_t)ldr * c] = (r < c) ? sm[r + rows * c] : ((r == c) ? beta[r] : 0.0);
   }
   for (int c = 0; c < R; ++c)
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) a.V[(int64_t)b * a.mb * R + i + rows * c] = sm[i + rows * c];
-  if (threadIdx.x < R) a.tauv[b * R + threadIdx.x] = tau[threadIdx.x];
+    for (int i = tid; i < rows; i += nt) a.V[(int64_t)b * a.mb * R + i + rows * c] = sm[i + rows * c];
+  if (tid < R) a.tauv[b * R + tid] = tau[tid];
 }
 
 __global__ void __launch_bounds__(512) k_tsqr_root(TsqrArgs a) {
   extern __shared__ double sm[];
-  __shared__ double tau[64], beta[64], w[64], red[32];
+  __shared__ double tau[64], beta[64], w[64], red[32], lam[64], np[64];
   const int R = a.R, rows = a.nleaf * R;
+  if (a.solve && threadIdx.x <= R) {  // lambda and <W, Ahat R0^T> from the leaf partials
+    double s = 0.0;
+    for (int b = 0; b < a.nleaf; ++b) s += a.part[b * (R + 1) + threadIdx.x];
+    if (threadIdx.x < R) {
+      lam[threadIdx.x] = sqrt(s);
+      a.lam[threadIdx.x] = lam[threadIdx.x];
+      if (!isfinite(lam[threadIdx.x])) atomicOr(a.flags, FLAG_NONFINITE);
+    } else {
+      red[0] = s;  // inner
+    }
+  }
   for (int e = threadIdx.x; e < rows * R; e += blockDim.x) sm[e] = a.Rstack[e];
   __syncthreads();
+  const double inner = a.solve ? red[0] : 0.0;
+  __syncthreads();
   DenseCols M{sm, rows, rows};
-  hh_factor(M, R, tau, beta, w);
+  hh_factor(M, R, tau, beta, w, np);
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int r = e % R, c = e / R;
     double v = (r < c) ? sm[r + rows * c] : ((r == c) ? beta[r] : 0.0);
     if (beta[r] < 0.0) v = -v;
+    if (a.solve && lam[c] > 0.0) v /= lam[c];  // R_n = R_hat diag(1/lambda)
     a.Rn[r + R * c] = v;
   }
   __syncthreads();
@@ -210,14 +344,9 @@ __global__ void __launch_bounds__(512) k_tsqr_root(TsqrArgs a) {
   }
   if (a.do_fit) {
     __syncthreads();
-    double* r0s = sm;            // reuse: R0 and Rn (sign-fixed) in shared memory
+    double* r0s = sm;  // R0 and R_n in shared memory (capacity >= 2 R^2 guaranteed by the host)
     double* rns = sm + R * R;
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      r0s[e] = a.R0[e];
-      const int r = e % R, c = e / R;
-      rns[e] = a.Rn[e];
-      (void)r; (void)c;
-    }
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) { r0s[e] = a.R0[e]; rns[e] = a.Rn[e]; }
     __syncthreads();
     double q = 0.0;
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -227,14 +356,14 @@ __global__ void __launch_bounds__(512) k_tsqr_root(TsqrArgs a) {
         g0 = fma(r0s[k + R * x], r0s[k + R * y], g0);
         g1 = fma(rns[k + R * x], rns[k + R * y], g1);
       }
-      q = fma(g0, a.lam[x] * a.lam[y] * g1, q);
+      q = fma(g0, lam[x] * lam[y] * g1, q);
     }
-    const double nxh2 = block_sum(q, red);
+    const double nxh2 = block_sum(q, red + 1);
     if (threadIdx.x == 0) {
       const double nx2 = *a.nX2;
-      *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * (*a.inner) + nxh2)) / sqrt(nx2);
+      *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner + nxh2)) / sqrt(nx2);
 #ifdef CPQR_DEBUG_FIT
-      printf("fit: nx2 %.17g inner %.17g nxh2 %.17g\n", nx2, *a.inner, nxh2);
+      printf("fit: nx2 %.17g inner %.17g nxh2 %.17g\n", nx2, inner, nxh2);
 #endif
     }
   }
@@ -255,6 +384,15 @@ __global__ void __launch_bounds__(512) k_tsqr_qform(TsqrArgs a) {
       Vb[i + rows * c] = a.V[(int64_t)b * a.mb * R + i + rows * c];
     }
   if (tid < R) tv[tid] = a.tauv[b * R + tid];
+  if (a.solve) {  // A_n = Ahat / lambda (zero column -> e_1, reading 10)
+    for (int c = 0; c < R; ++c) {
+      const double l = a.lam[c];
+      for (int i = tid; i < rows; i += nt) {
+        const int64_t e = r0 + i + (int64_t)a.m * c;
+        a.Aout[e] = (l > 0.0) ? a.Ahat[e] / l : ((r0 + i) == 0 ? 1.0 : 0.0);
+      }
+    }
+  }
   __syncthreads();
   for (int j = R - 1; j >= 0; --j) {
     const double tj = tv[j];
@@ -372,7 +510,7 @@ __global__ void __launch_bounds__(512) k_solve_norm(SolveArgs a) {
 // ------------------------------------------------------------- K2 with the 2-barrier primitive
 __global__ void __launch_bounds__(1024) k_kr_qr2(KrQrArgs a) {
   extern __shared__ double smk[];
-  __shared__ double tau[64], beta[64], w[64];
+  __shared__ double tau[64], beta[64], w[64], np[64];
   __shared__ int64_t off[65];
   __shared__ int ncnt[64];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -403,7 +541,7 @@ __global__ void __launch_bounds__(1024) k_kr_qr2(KrQrArgs a) {
     }
   __syncthreads();
   HHCols M{V, off, ncnt};
-  hh_factor(M, R, tau, beta, w);
+  hh_factor(M, R, tau, beta, w, np);
   for (int e = tid; e < R * R; e += nt) {
     const int r = e % R, c = e / R;
     double v = (r < c) ? V[off[c] + r] : ((r == c) ? beta[r] : 0.0);

@@ -66,6 +66,30 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 evict-first policy for the single-use tensor stream: X passes through L2 without evicting
+// the small reused working set (Q panels, W, factors) and, above all, the code of the per-mode
+// tail kernels, whose cold instruction fetches from DRAM otherwise dominate their run time.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_ef(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_ef(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                               uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -129,6 +153,7 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     if (lane == 0) {
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
+      const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = (int)(u / nA);
@@ -139,7 +164,7 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
 #pragma unroll 4
-          for (int q = 0; q < 16; ++q) tma_load_3d(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s]);
+          for (int q = 0; q < 16; ++q) tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
 #pragma unroll
           for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }
@@ -254,6 +279,7 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     if (lane == 0) {
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
+      const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
         for (int ks = 0; ks < KS; ++ks, ++it) {
@@ -261,7 +287,7 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
-          tma_load_2d(dst, &tmX, ks * kBK, (int)(u * 128), &full[s]);
+          tma_load_2d_ef(dst, &tmX, ks * kBK, (int)(u * 128), &full[s], pol);
 #pragma unroll
           for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }
@@ -336,6 +362,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     if (lane == 0) {
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
+      const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
       for (int64_t u = u0; u < u1; ++u) {
         const int l = (int)(u / nfb), fb = (int)(u - (int64_t)l * nfb);
@@ -344,7 +371,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
-          tma_load_3d(dst, &tmX, ks * kBK, fb * 128, l, &full[s]);
+          tma_load_3d_ef(dst, &tmX, ks * kBK, fb * 128, l, &full[s], pol);
 #pragma unroll
           for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }
@@ -455,6 +482,7 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (lane == 0) {
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
+      const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
         for (int ks = 0; ks < KS; ++ks, ++it) {
@@ -462,7 +490,7 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
-          tma_load_3d(dst, &tmX, ks * kBK, 0, (int)(u * 8), &full[s]);
+          tma_load_3d_ef(dst, &tmX, ks * kBK, 0, (int)(u * 8), &full[s], pol);
 #pragma unroll
           for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }

@@ -183,3 +183,53 @@ def test_small_slice_kernel(cp, dims, R, variant):
     ref = O.cp_als_qr(X, init, 2, variant=variant)
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
     s.close()
+
+
+@pytest.mark.parametrize("dims,R,variant", [((30, 40, 50), 5, "QR"), ((70, 66, 34), 32, "QR"),
+                                            ((12, 10, 9, 11), 6, "SVD")])
+def test_householder_factor_qr_path(cp, dims, R, variant, monkeypatch):
+    """Force the Householder TSQR factor QR (the CholeskyQR2 fallback) for whole sweeps."""
+    monkeypatch.setenv("CPQR_FACTOR_QR", "householder")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=17, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f = s.sweep(2)
+    lam, A = s.get_factors()
+    ref = O.cp_als_qr(X, init, 2, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    for k in range(len(dims)):
+        assert rel(A[k], ref["factors"][k]) <= 1e-9
+    s.close()
+
+
+def test_factor_qr_fallback_on_ill_conditioned_panel(cp):
+    """kappa(A) ~ 1e10: CholeskyQR2 must hand over to Householder; Q orthonormal, QR = A."""
+    rng = np.random.default_rng(3)
+    m, R = 300, 8
+    U, _ = np.linalg.qr(rng.standard_normal((m, R)))
+    Vt, _ = np.linalg.qr(rng.standard_normal((R, R)))
+    A = U @ np.diag(np.logspace(0, -10, R)) @ Vt
+    s = cp.CPQR((m, m), R, "QR")
+    Q, Rf = s.debug_qr(A)
+    assert np.linalg.norm(Q.T @ Q - np.eye(R)) <= 1e-13
+    assert rel(Q @ Rf, A) <= 1e-14 and np.all(np.diag(Rf) >= 0)
+    Qo, Ro = O.qr_pos(A)
+    assert rel(Rf, Ro) <= 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("dims,R", [((30, 40, 50), 5), ((70, 66, 34), 32)])
+def test_multi_kernel_cholqr_path(cp, dims, R, monkeypatch):
+    """The 5-launch CholeskyQR2 path (used for factors taller than 8 x 256 rows), forced."""
+    monkeypatch.setenv("CPQR_CQ_MULTI", "1")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=23, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f = s.sweep(2)
+    ref = O.cp_als_qr(X, init, 2)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
