@@ -302,11 +302,14 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
     for s in range(sweeps):                                       # line 4
         last = None
         for n in range(N):                                        # line 5
+            qs_in = [None if (k == n or Qs[k] is None) else Qs[k].copy() for k in range(N)] if (debug_sweep1 and s == 0) else None
             u = mode_update_qr(X, Qs, Rs, n, variant, tau, order)
             factors[n], lam, Qs[n], Rs[n] = u["A"], u["lam"], u["Q"], u["R"]
             flags |= u["flags"]
             if debug_sweep1 and s == 0:
-                debug.append({k: u[k] for k in ("Yn", "Q0", "R0", "W", "Ahat", "A", "lam")})
+                d = {k: u[k] for k in ("Yn", "Q0", "R0", "W", "Ahat", "A", "lam")}
+                d["Qs_in"] = qs_in  # the Q_k this mode's Multi-TTM used (debug snapshot)
+                debug.append(d)
             last = u
         if fit_mode == "fast":
             fits.append(fit_fast_qr(nX2, last["W"], last["Ahat"], last["R0"], Rs[N - 1], lam))

@@ -1,0 +1,76 @@
+"""Full-size parity at the BASELINE.json configs (C1..C5), in the launch configuration bench.py
+times (CUDA-graph sweeps, default options, tensor resident on the device).
+
+Tolerances (north_star):
+  * Y_(n), relative Frobenius, every mode of sweep 1 (with the Q_k the oracle used): <= 1e-11
+  * factors and lambda after one sweep from the shared init: <= 1e-9 (all five configs)
+  * fit after the config's sweep count: within 1e-8 (C4: DIRECT fit, reading 28)
+The oracle computes every output here in full (no sampling needed at these sizes); the C5 tensor
+(8 GB) is generated once on the host and shared by both sides.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2112_10855_b200 import synth
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def rel(a, b):
+    return np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def cp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2112_10855_b200 import cpqr
+    return cpqr
+
+
+CASES = [(1, "QR"), (2, "QR"), (2, "NE"), (3, "QR"), (3, "SVD"), (4, "SVD"), (5, "QR")]
+
+
+@pytest.mark.parametrize("cfg,variant", CASES)
+def test_fullsize_parity(cp, cfg, variant):
+    import torch
+    conf, Xc, truth, init = synth.make_problem(cfg)
+    X = O.as_tensor(Xc)
+    fit_mode = "direct" if cfg == 4 else "fast"
+    s = cp.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, fit_mode=fit_mode)
+    Xd = torch.from_numpy(np.ascontiguousarray(Xc)).cuda()
+    s.set_tensor(Xd)
+    s.set_factors(init)
+    N = conf.N
+    if variant == "NE":
+        ref1 = O.cp_als_ne(X, init, 1)
+    else:
+        ref1 = O.cp_als_qr(X, init, 1, variant=variant, tau=conf.svd_tau, debug_sweep1=True)
+        # Y of every mode of sweep 1, from the Q_k the oracle used at that mode
+        for n in range(N):
+            d = ref1["debug"][n]
+            out = s.debug_mode(n, Q_override=d["Qs_in"])
+            Yo = O.multi_ttm(X, {k: d["Qs_in"][k].T for k in range(N) if k != n})
+            e = rel(out["Y"], Yo)
+            assert e <= 1e-11, (cfg, n, e)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (cfg, k, rel(A[k], ref1["factors"][k]))
+    assert rel(lam, ref1["lam"]) <= 1e-9
+    rest = s.sweep(conf.sweeps - 1) if conf.sweeps > 1 else np.array([])
+    fits = np.concatenate([f1, rest])
+    if variant == "NE":
+        ref = O.cp_als_ne(X, init, conf.sweeps)
+    else:
+        ref = O.cp_als_qr(X, init, conf.sweeps, variant=variant, tau=conf.svd_tau)
+    last = ref["fits"][-1]
+    if fit_mode == "direct":  # noiseless C4: the final fit is compared in DIRECT form (reading 28)
+        last = O.fit_direct(X, ref["lam"], ref["factors"])
+    assert abs(fits[-1] - last) <= 1e-8, (cfg, fits[-1], last)
+    assert np.max(np.abs(fits - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+    del Xd
+    torch.cuda.empty_cache()
