@@ -8,8 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcpqr.so")
 SRC = [os.path.join(HERE, "csrc", "cpqr.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "ttm_kernels.cuh", "small_kernels.cuh")] + [
-    os.path.join(ROOT, "include", "cpqr.h")]
+DEPS = SRC + sorted(os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
+                    if f.endswith(".cuh")) + [os.path.join(ROOT, "include", "cpqr.h")]
 
 
 def nccl_dirs():

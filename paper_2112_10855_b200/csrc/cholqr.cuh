@@ -702,19 +702,6 @@ __device__ __forceinline__ void cq_row_times_upper(const double* X, double* Y, i
     }
     Y[tid + ld * cc] = (s0 + s1) + (s2 + s3);
   }
-  return;
-  #pragma unroll 1
-  for (int cc = 0; cc < R; ++cc) {
-    double s0 = 0.0, s1 = 0.0;
-    int l = 0;
-    #pragma unroll 1
-    for (; l + 1 <= cc; l += 2) {
-      s0 = fma(X[tid + ld * l], U[l + RB * cc], s0);
-      s1 = fma(X[tid + ld * (l + 1)], U[(l + 1) + RB * cc], s1);
-    }
-    if (l <= cc) s0 = fma(X[tid + ld * l], U[l + RB * cc], s0);
-    Y[tid + ld * cc] = s0 + s1;
-  }
 }
 
 
@@ -773,6 +760,181 @@ __device__ __forceinline__ void cq_row_fwd_subst(double* Prow, int ld, int R, in
   }
 }
 
+// ---- blocked row kernels for k_cq_compact -------------------------------------------------
+// Each thread owns one panel row in shared memory (stride ld).  A dependent LDS costs ~70 cycles
+// on sm_100a, so the row is processed in 8-column chunks held in registers: one shared-memory
+// round trip per 8x8 block instead of one per element.  Columns >= R are zero in the panel and
+// in the (zero-padded) triangular factors, and invd[j] = 0 there, so they stay zero.
+
+// In-place triangular solve on the row.  FWD: y U = x (U upper, invd = 1/U_jj), columns
+// ascending.  BACK: sum_{l >= c} T(c, l) x_l = w_c (T upper, invd = 1/T_cc), i.e. x T^T = w,
+// columns descending (the back substitution of Alg. 2 line 10).
+template <int RB, bool BACK>
+__device__ __noinline__ void cq_row_trsv(double* row, int ld, const double* T, const double* invd) {
+  constexpr int NB = RB / 8;
+#pragma unroll 1
+  for (int s = 0; s < NB; ++s) {
+    const int jb = BACK ? NB - 1 - s : s;
+    const int j0 = 8 * jb;
+    double y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = row[ld * (j0 + q)];
+    if (BACK) {
+#pragma unroll
+      for (int q = 7; q >= 0; --q) {
+#pragma unroll
+        for (int p = q + 1; p < 8; ++p) y[q] = fma(-y[p], T[(j0 + q) + RB * (j0 + p)], y[q]);
+        y[q] *= invd[j0 + q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+#pragma unroll
+        for (int p = 0; p < q; ++p) y[q] = fma(-y[p], T[(j0 + p) + RB * (j0 + q)], y[q]);
+        y[q] *= invd[j0 + q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) row[ld * (j0 + q)] = y[q];
+#pragma unroll 1
+    for (int t = s + 1; t < NB; ++t) {  // eliminate the solved chunk from the unsolved ones
+      const int i0 = 8 * (BACK ? NB - 1 - t : t);
+      double a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = row[ld * (i0 + q)];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+          a[q] = fma(-y[p], BACK ? T[(i0 + q) + RB * (j0 + p)] : T[(j0 + p) + RB * (i0 + q)], a[q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) row[ld * (i0 + q)] = a[q];
+    }
+  }
+}
+
+// out_row = in_row M (M dense RB x RB col-major): the SVD-variant solve x = w U S^+ V^T
+template <int RB>
+__device__ __noinline__ void cq_row_gemv(const double* in, double* out, int ld, const double* M) {
+  constexpr int NB = RB / 8;
+#pragma unroll 1
+  for (int ob = 0; ob < NB; ++ob) {
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = 0.0;
+#pragma unroll 1
+    for (int sb = 0; sb < NB; ++sb) {
+      double w[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) w[p] = in[ld * (8 * sb + p)];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) a[q] = fma(w[p], M[(8 * sb + p) + RB * (8 * ob + q)], a[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) out[ld * (8 * ob + q)] = a[q];
+  }
+}
+
+// <w, T x> for the row pair (T upper): the per-row term of <W, Ahat R0^T>
+template <int RB>
+__device__ __noinline__ double cq_row_wTx(const double* w, const double* x, int ld, const double* T) {
+  constexpr int NB = RB / 8;
+  double inner = 0.0;
+#pragma unroll 1
+  for (int cb = 0; cb < NB; ++cb) {
+    double t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = 0.0;
+#pragma unroll 1
+    for (int lb = cb; lb < NB; ++lb) {
+      double xv[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) xv[p] = x[ld * (8 * lb + p)];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) t[q] = fma(T[(8 * cb + q) + RB * (8 * lb + p)], xv[p], t[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) inner = fma(w[ld * (8 * cb + q)], t[q], inner);
+  }
+  return inner;
+}
+
+// Right-looking Cholesky of Gs (R x R used, RB ld) with a 2-D thread map: lane = row i, warp kk
+// updates columns k = kk (mod nwarps) -- no integer division, all loads of a column step issued
+// together, one barrier per column.  The update expression and order equal cq_chol_par's.
+// On exit Ru = L^T (upper, zero padded), invd[j] = 1/L_jj (0 for j >= R).
+template <int RB>
+__device__ __noinline__ bool cq_chol_2d(double* Gs, int R, double* Ru, double* invd, double* ratio) {
+  const int tid = threadIdx.x, i = tid & 31, kk = tid >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  // critical path per column: LDS of the pivot, its reciprocal (__drcp_rn == 1.0 / d, correctly
+  // rounded), one FMA per owned entry, barrier; square roots are taken after the loop
+#pragma unroll 1
+  for (int j = 0; j < R; ++j) {
+    const double d = Gs[j + RB * j];
+    if (i > j && i < R) {
+      const double id = (d > 0.0) ? __drcp_rn(d) : 0.0;
+      const double gij = -Gs[i + RB * j] * id;
+      if (nw == 8) {
+#pragma unroll
+        for (int q = 0; q < RB / 8; ++q) {
+          const int k = kk + 8 * q;
+          if (k > j && k <= i) Gs[i + RB * k] = fma(gij, Gs[k + RB * j], Gs[i + RB * k]);
+        }
+      } else {
+#pragma unroll 1
+        for (int k = kk; k < RB; k += nw)
+          if (k > j && k <= i) Gs[i + RB * k] = fma(gij, Gs[k + RB * j], Gs[i + RB * k]);
+      }
+    }
+    __syncthreads();
+  }
+  // pivots d_j = Gs(j, j) are final; L_jj = sqrt(d_j); warp 0 also forms ok / max L_jj / min L_jj
+  bool ok = true;
+  double dmax = 0.0, dmin = 1e308;
+  if (tid < 32) {
+    const double d = (tid < R) ? Gs[tid + RB * tid] : 1.0;
+    const double l = sqrt(fmax(d, 0.0));
+    if (tid < RB) invd[tid] = (tid < R && l > 0.0) ? 1.0 / l : 0.0;
+    ok = __all_sync(0xffffffffu, d > 0.0);
+    dmax = (tid < R) ? l : 0.0;
+    dmin = (tid < R) ? l : 1e308;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int e = tid; e < RB * RB; e += blockDim.x) {  // Ru(r, c) = L(c, r) = G(c, r) / L_rr, Ru(r, r) = L_rr
+    const int r = e % RB, c = e / RB;
+    double v = 0.0;
+    if (r < R && c < R && r <= c) v = (r == c) ? sqrt(fmax(Gs[r + RB * r], 0.0)) : Gs[c + RB * r] * invd[r];
+    Ru[e] = v;
+  }
+  __syncthreads();
+  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;  // valid on thread 0 (the caller reads it there)
+  return ok;
+}
+
+// sum_{c < nb} (value at p in cluster CTA c), c in increasing order (bitwise the rolled loop);
+// the nb <= 8 remote loads are issued together instead of one DSMEM round trip per rank
+__device__ __forceinline__ double cluster_sum_ordered(cooperative_groups::cluster_group& cl, double* p, int nb) {
+  double v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = (c < nb) ? *cl.map_shared_rank(p, c) : 0.0;
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < nb) s += v[c];
+  return s;
+}
+
 #ifdef CPQR_DEBUG_TIMING
 #define CQ_T(k) do { if (threadIdx.x == 0) tstamp[k] = clock64(); } while (0)
 #define CQ_DUMP() do { if (threadIdx.x == 0 && cluster.block_rank() == 0) printf("cq phases: %lld %lld %lld %lld %lld %lld %lld %lld | lam+sync %lld chol %lld sync %lld inv %lld\n", tstamp[1]-tstamp[0], tstamp[2]-tstamp[1], tstamp[3]-tstamp[2], tstamp[4]-tstamp[3], tstamp[5]-tstamp[4], tstamp[6]-tstamp[5], tstamp[7]-tstamp[6], tstamp[8]-tstamp[7], tstamp[9]-tstamp[3], tstamp[10]-tstamp[9], tstamp[11]-tstamp[10], tstamp[12]-tstamp[11]); } while (0)
@@ -794,76 +956,60 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   double* Gs = G2b + RB * RB;
   double* R1s = Gs + RB * RB;
   double* R2s = R1s + RB * RB;
-  double* Ui = R2s + RB * RB;
+  double* Ui = R2s + RB * RB;  // (unused scratch; keeps the host smem size formula)
   double* Ms = Ui + RB * RB;
   double* R0s = Ms + RB * RB;
-  __shared__ double lam[RB], redi[8], innerb, inv1[RB], inv2[RB];
+  __shared__ double lam[RB], redi[8], innerb, inv1[RB], inv2[RB], invm[RB];
   __shared__ int okf;
+  (void)Ui;
   const int nb = a.nb, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int b = (int)cluster.block_rank();
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
   const int rows4 = (rows + 3) & ~3, ld = (((int)blockDim.x + 15) & ~15) + 4;  // >= every thread's row
   double* X = R0s + RB * RB;   // panel of Ahat (or A) rows
-  double* Y = X + ld * RB;     // panel of W / Q1 / Q rows
+  double* Y = X + ld * RB;     // panel of W / Q1 rows
   const int i = r0 + tid;
   const bool own = tid < rows;
   if (tid == 0 && b == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);
   #pragma unroll 1
   for (int e = tid; e < 2 * ld * RB; e += blockDim.x) X[e] = 0.0;
   #pragma unroll 1
-  for (int e = tid; e < RB * RB; e += blockDim.x) {
-    const int r = e % RB, c = e / RB;
-    Ms[e] = (a.solve && r < R && c < R) ? a.Rm[r + R * c] : 0.0;
-    R0s[e] = (a.solve && r < R && c < R) ? a.R0[r + R * c] : 0.0;
-  }
+  for (int e = tid; e < 2 * RB * RB; e += blockDim.x) Ms[e] = 0.0;  // Ms, R0s
   __syncthreads();
-  // ---- 1. panel rows
-  double inner = 0.0;
-  if (own) {
-    if (!a.solve) {
-#pragma unroll 1
-      for (int k = 0; k < R; ++k) X[tid + ld * k] = a.A[i + (int64_t)a.m * k];
-    } else {
-#pragma unroll 1
-      for (int k = 0; k < R; ++k) Y[tid + ld * k] = a.W[(int64_t)i * R + k];  // W row (panel Y)
-      if (a.variant == 2) {  // x = w M, M = U S^+ V^T
-#pragma unroll 1
-        for (int cc = 0; cc < R; ++cc) {
-          double s0 = 0.0, s1 = 0.0;
-          int r = 0;
-#pragma unroll 1
-          for (; r + 1 < R; r += 2) {
-            s0 = fma(Y[tid + ld * r], Ms[r + RB * cc], s0);
-            s1 = fma(Y[tid + ld * (r + 1)], Ms[r + 1 + RB * cc], s1);
-          }
-          if (r < R) s0 = fma(Y[tid + ld * r], Ms[r + RB * cc], s0);
-          X[tid + ld * cc] = s0 + s1;
-        }
-      } else {  // Ahat R0^T = W by back substitution over columns j = R..1
-#pragma unroll 1
-        for (int j = R - 1; j >= 0; --j) {
-          double acc = Y[tid + ld * j], acc1 = 0.0;
-          int l = j + 1;
-#pragma unroll 1
-          for (; l + 1 < R; l += 2) {
-            acc = fma(-X[tid + ld * l], Ms[j + RB * l], acc);
-            acc1 = fma(-X[tid + ld * (l + 1)], Ms[j + RB * (l + 1)], acc1);
-          }
-          if (l < R) acc = fma(-X[tid + ld * l], Ms[j + RB * l], acc);
-          X[tid + ld * j] = (acc + acc1) / Ms[j + RB * j];
-        }
-      }
-      if (a.do_fit)  // <W, Ahat R0^T>: sum_c w_c sum_{l>=c} x_l R0(c,l)
-#pragma unroll 1
-        for (int cc = 0; cc < R; ++cc) {
-          double tt = 0.0;
-#pragma unroll 1
-          for (int l = cc; l < R; ++l) tt = fma(X[tid + ld * l], R0s[cc + RB * l], tt);
-          inner = fma(Y[tid + ld * cc], tt, inner);
-        }
-#pragma unroll 1
-      for (int k = 0; k < R; ++k) a.Ahat[i + (int64_t)a.m * k] = X[tid + ld * k];
+  // all global inputs in flight at once (cp.async), one wait
+  if (a.solve) {
+    #pragma unroll 1
+    for (int e = tid; e < R * R; e += blockDim.x) {
+      const int r = e % R, c = e / R;
+      if (a.variant == 2 || r <= c) cp_async8(&Ms[r + RB * c], a.Rm + e);  // R0 upper / M dense
+      if (r <= c) cp_async8(&R0s[r + RB * c], a.R0 + e);
     }
+  }
+  if (own) {
+    #pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+      if (a.solve) cp_async8(&Y[tid + ld * k], a.W + (int64_t)i * R + k);  // W row (panel Y)
+      else cp_async8(&X[tid + ld * k], a.A + i + (int64_t)a.m * k);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (a.solve && a.variant != 2 && tid < RB) invm[tid] = (tid < R) ? 1.0 / Ms[tid + RB * tid] : 0.0;
+  __syncthreads();
+  // ---- 1. solve for the panel rows (Alg. 2 line 10)
+  double inner = 0.0;
+  if (a.solve) {
+    if (a.variant == 2) {
+      cq_row_gemv<RB>(Y + tid, X + tid, ld, Ms);  // x = w M, M = U S^+ V^T
+    } else {
+      #pragma unroll 1
+      for (int k = 0; k < RB; ++k) X[tid + ld * k] = Y[tid + ld * k];
+      cq_row_trsv<RB, true>(X + tid, ld, Ms, invm);  // Ahat R0^T = W
+    }
+    if (a.do_fit) inner = cq_row_wTx<RB>(Y + tid, X + tid, ld, R0s);  // <W, Ahat R0^T>
+    if (own)
+      #pragma unroll 1
+      for (int k = 0; k < R; ++k) a.Ahat[i + (int64_t)a.m * k] = X[tid + ld * k];
   }
   inner = warp_sum(inner);
   if (lane == 0) redi[wid] = inner;
@@ -880,23 +1026,23 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   CQ_T(2);
   cluster.sync();
   #pragma unroll 1
-  for (int e = tid; e < RB * RB; e += blockDim.x) {
-    double s = 0.0;
-    #pragma unroll 1
-    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G1b, c)[e];
-    Gs[e] = s;
-  }
-  double inner_all = 0.0;
-  #pragma unroll 1
-  for (int c = 0; c < nb; ++c) inner_all += *cluster.map_shared_rank(&innerb, c);
+  for (int e = tid; e < RB * RB; e += blockDim.x) Gs[e] = cluster_sum_ordered(cluster, G1b + e, nb);
+  const double inner_all = cluster_sum_ordered(cluster, &innerb, nb);
   __syncthreads();
   CQ_T(3);
   if (a.solve && tid < R) lam[tid] = sqrt(Gs[tid + RB * tid]);  // lambda_c = ||Ahat(:,c)||_2
   __syncthreads();
+  if (a.solve && own) {  // A_n = Ahat diag(1/lambda) straight from the panel
+    #pragma unroll 1
+    for (int k = 0; k < R; ++k) {
+      const double l = lam[k];
+      a.Aout[i + (int64_t)a.m * k] = (l > 0.0) ? X[tid + ld * k] / l : (i == 0 ? 1.0 : 0.0);
+    }
+  }
   CQ_T(9);
   {
     double ratio;
-    const bool ok = cq_chol_par(Gs, R, RB, R1s, inv1, &ratio);
+    const bool ok = cq_chol_2d<RB>(Gs, R, R1s, inv1, &ratio);
     if (tid == 0) okf = ok && ratio < kCqKappaMax;
   }
   CQ_T(10);
@@ -907,27 +1053,18 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
     cluster.sync();
     return;
   }
-
   CQ_T(12);
-  __syncthreads();
   CQ_T(4);
   // ---- 3. Q1 = X R1^{-1}, Gram, Cholesky -> R2, R2^{-1}
-  if (own) {
-#pragma unroll 1
-    for (int k = 0; k < R; ++k) Y[tid + ld * k] = X[tid + ld * k];
-    cq_row_fwd_subst(Y + tid, ld, R, RB, R1s, inv1);
-  } else for (int k = 0; k < RB; ++k) Y[tid + ld * k] = 0.0;
+  #pragma unroll 1
+  for (int k = 0; k < RB; ++k) Y[tid + ld * k] = X[tid + ld * k];
+  cq_row_trsv<RB, false>(Y + tid, ld, R1s, inv1);
   __syncthreads();
   CQ_T(5);
   cq_gram_dmma<RB>(Y, ld, rows4, G2b);
   cluster.sync();
   #pragma unroll 1
-  for (int e = tid; e < RB * RB; e += blockDim.x) {
-    double s = 0.0;
-    #pragma unroll 1
-    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G2b, c)[e];
-    Gs[e] = s;
-  }
+  for (int e = tid; e < RB * RB; e += blockDim.x) Gs[e] = cluster_sum_ordered(cluster, G2b + e, nb);
   __syncthreads();
   if (wid == 0) {
     double e = 0.0;  // ||G2 - I||_max must be O(kappa^2 eps)
@@ -942,7 +1079,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   }
   {
     double ratio;
-    const bool ok = cq_chol_par(Gs, R, RB, R2s, inv2, &ratio);
+    const bool ok = cq_chol_2d<RB>(Gs, R, R2s, inv2, &ratio);
     if (tid == 0) okf = okf && ok;
   }
   __syncthreads();
@@ -951,25 +1088,14 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
     cluster.sync();
     return;
   }
-
-  __syncthreads();
   CQ_T(6);
-  // ---- 4. Q = Q1 R2^{-1} (into X, Ahat is kept in global), outputs
+  // ---- 4. Q = Q1 R2^{-1} (in the Y panel), outputs
+  cq_row_trsv<RB, false>(Y + tid, ld, R2s, inv2);
   if (own) {
-#pragma unroll 1
-    for (int k = 0; k < R; ++k) X[tid + ld * k] = Y[tid + ld * k];
-    cq_row_fwd_subst(X + tid, ld, R, RB, R2s, inv2);
     #pragma unroll 1
-    for (int k = 0; k < R; ++k) a.Q[i + (int64_t)a.m * k] = X[tid + ld * k];
+    for (int k = 0; k < R; ++k) a.Q[i + (int64_t)a.m * k] = Y[tid + ld * k];
     #pragma unroll 1
-    for (int k = 0; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? X[tid + ld * k] : 0.0;
-    if (a.solve)
-      #pragma unroll 1
-      for (int k = 0; k < R; ++k) {
-        const double l = lam[k];
-        const int64_t e = i + (int64_t)a.m * k;
-        a.Aout[e] = (l > 0.0) ? a.Ahat[e] / l : (i == 0 ? 1.0 : 0.0);
-      }
+    for (int k = 0; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? Y[tid + ld * k] : 0.0;
   }
   CQ_T(7);
   if (b == 0) {
@@ -978,7 +1104,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
       const int r = e % RB, c = e / RB;
       double s = 0.0;
       if (r <= c && c < R)
-        #pragma unroll 1
+        #pragma unroll 4
         for (int k = r; k <= c; ++k) s = fma(R2s[r + RB * k], R1s[k + RB * c], s);
       if (a.solve && c < R && lam[c] > 0.0) s /= lam[c];
       Gs[e] = s;
@@ -995,7 +1121,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
       for (int e = tid; e < R * R; e += blockDim.x) {
         const int xx = e % R, yy = e / R;
         double g0 = 0.0, g1 = 0.0;
-        #pragma unroll 1
+        #pragma unroll 4
         for (int k = 0; k <= min(xx, yy); ++k) {
           g0 = fma(R0s[k + RB * xx], R0s[k + RB * yy], g0);
           g1 = fma(Gs[k + RB * xx], Gs[k + RB * yy], g1);

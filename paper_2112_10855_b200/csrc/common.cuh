@@ -36,6 +36,15 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 __device__ __forceinline__ double ldg_nc(const double* p) { return __ldg(p); }
 
+// Asynchronous 8-byte global -> shared copy (LDGSTS): a rolled loop of these does not wait on
+// each load, so the run-once tail kernels issue all their inputs at once and wait a single time.
+__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // Streaming (evict-first) 16-byte load for the tensor pass.
 __device__ __forceinline__ double2 ldg_stream2(const double* p) {
   return __ldcs(reinterpret_cast<const double2*>(p));

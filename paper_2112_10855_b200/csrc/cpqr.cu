@@ -28,7 +28,8 @@ namespace {
 
 constexpr int kMaxN = 8;
 constexpr int kMaxR = 32;
-constexpr size_t kQSmemMax = 96 * 1024;  // Q panel budget per CTA (2 CTAs / SM)
+constexpr size_t kQSmemMax = 96 * 1024;
+constexpr int64_t kQ0MaxSlices = 64;      // k-step slices of k_q0_apply_tc (partials buffer)  // Q panel budget per CTA (2 CTAs / SM)
 
 struct TtmStep {
   int kind;  // 0 strided, 1 fiber, 2 slice, 3 slice-reduce, 4 strided TMA, 5 fiber TMA, 6 slice TMA, 7 slice fix-up
@@ -100,6 +101,7 @@ struct cpqr_ctx {
   int stream_sms = 148;  // CTAs of the stream-X kernels (one SM left to the concurrent V_n QR)
   double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWloc = nullptr,
          *dWp = nullptr, *dAhat = nullptr;
+  unsigned* dq0cnt = nullptr;  // per-row-block arrival counters of k_q0_apply_tc (self re-arming)
   double* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
   double* dPart = nullptr;
@@ -323,6 +325,9 @@ int stages_for(size_t stage, size_t extra) {
 // GEMM); the remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
 // (ties by decreasing mode, reading 5).  TMA kernels whenever the layout allows
 // (even leading dimension, 16-B aligned base), else the register-staged kernels.
+// N-tiles of 8 fibres per consumer warp in the fused slice kernel (box height kCW * 8 * NF)
+static int slice_nf(int I2) { return I2 >= 256 ? 4 : 2; }
+
 void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   p.steps.clear();
   p.diags.clear();
@@ -432,7 +437,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     if (in.tma && s.I1 % 2 == 0 && s.L < (1ll << 31) && bufs[0]) {
       const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
       const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
-      const uint32_t box[3] = {16, 128, 1};
+      const uint32_t box[3] = {16, (uint32_t)(kCW * 8 * slice_nf(s.I2)), 1};
       tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
     }
     const bool small = tma && s.I2 <= 64 && s.I2 % 8 == 0 && NT <= 2;
@@ -454,8 +459,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     } else if (tma) {
       s.kind = 6;
       const int MT = NT;
-      s.S = stages_for(128 * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
-      s.nfb = (s.I2 + 127) / 128;
+      s.gps = slice_nf(s.I2);
+      const int BN = kCW * 8 * s.gps;
+      s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
+      s.nfb = (s.I2 + BN - 1) / BN;
       const int64_t U = s.L * s.nfb;
       s.G = std::min<int64_t>(U, in.sms);
       int ns = 1;
@@ -552,14 +559,19 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
     switch (NT) { case 1: FIB(1) break; case 2: FIB(2) break; case 3: FIB(3) break; default: FIB(4) break; }
 #undef FIB
   } else if (s.kind == 6) {
-    const size_t smem = 3072 + (size_t)s.S * (128 * 128 + NQB * kBoxBytes) + (size_t)kCW * R * R * 8;
-#define SLC(MTV)                                                                                          \
-  {                                                                                                       \
-    set_smem(k_slice_tma<MTV>, smem);                                                                     \
-    k_slice_tma<MTV><<<(int)s.G, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, s.out, \
-                                                          s.P, s.nslots, s.S);                            \
+    const int BN = kCW * 8 * s.gps;
+    const size_t smem = 3072 + (size_t)s.S * ((size_t)BN * 128 + NQB * kBoxBytes) + (size_t)kCW * R * R * 8;
+#define SLC(MTV, NFV)                                                                                      \
+  {                                                                                                        \
+    set_smem(k_slice_tma<MTV, NFV>, smem);                                                                 \
+    k_slice_tma<MTV, NFV><<<(int)s.G, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, \
+                                                               s.out, s.P, s.nslots, s.S);                 \
   }
-    switch (NT) { case 1: SLC(1) break; case 2: SLC(2) break; case 3: SLC(3) break; default: SLC(4) break; }
+    if (s.gps == 4) {
+      switch (NT) { case 1: SLC(1, 4) break; case 2: SLC(2, 4) break; case 3: SLC(3, 4) break; default: SLC(4, 4) break; }
+    } else {
+      switch (NT) { case 1: SLC(1, 2) break; case 2: SLC(2, 2) break; case 3: SLC(3, 2) break; default: SLC(4, 2) break; }
+    }
 #undef SLC
   } else if (s.kind == 8) {
     const size_t smem = 3072 + (size_t)s.S * ((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes);
@@ -773,7 +785,13 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
+#ifdef CPQR_DEBUG_TIMING
+    const int reps = getenv("CPQR_CQ_TWICE") ? 2 : 1;  // warm-vs-cold instruction-fetch experiment
+#else
+    const int reps = 1;
+#endif
+    for (int rep = 0; rep < reps && e == cudaSuccess; ++rep)
     switch (RB) {
       case 8:
         if (compact) {
@@ -962,17 +980,19 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
 }
 
 cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
-  const int64_t J = p.Aa * p.Bb;
+  const int64_t J = p.Aa * p.Bb, KT = (J + 3) / 4;
   const int In = (int)p.In;
   const int iblocks = (In + 7) / 8;
-  int KS = (int)std::max<int64_t>(1, std::min<int64_t>((J + 63) / 64, (2 * c->sms + iblocks - 1) / iblocks));
-  const int jchunk = (int)(((J + KS - 1) / KS + 63) / 64 * 64);
-  KS = (int)((J + jchunk - 1) / jchunk);
-  dim3 grid(iblocks, KS);
-  k_q0_apply<<<grid, 256, 0, c->st>>>(p.Y, p.Aa, In, p.Bb, c->dQ0, c->R, jchunk, c->dWp);
-  CKL();
-  const int64_t nW = (int64_t)In * c->R;
-  k_q0_reduce<<<(int)std::min<int64_t>((nW + 255) / 256, 1024), 256, 0, c->st>>>(c->dWp, KS, nW, Wout);
+  // slices of Q0's k-steps so that ~2 CTAs per SM run, each with >= 1 k-step per warp
+  int64_t KS = std::max<int64_t>(1, std::min<int64_t>((2 * c->sms + iblocks - 1) / iblocks, (KT + 7) / 8));
+  KS = std::min<int64_t>(KS, kQ0MaxSlices);
+  const int kpc = (int)((KT + KS - 1) / KS);
+  KS = (KT + kpc - 1) / kpc;
+  dim3 grid(iblocks, (unsigned)KS);
+  const int NT = (c->R + 7) / 8;
+#define Q0A(NTV) k_q0_apply_tc<NTV><<<grid, 256, 0, c->st>>>(p.Y, p.Aa, In, p.Bb, c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout)
+  switch (NT) { case 1: Q0A(1); break; case 2: Q0A(2); break; case 3: Q0A(3); break; default: Q0A(4); break; }
+#undef Q0A
   CKL();
   return CPQR_OK;
 }
@@ -1290,8 +1310,10 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     const char* f = getenv("CPQR_FACTOR_QR");
     c->factor_qr_mode = (f && std::string(f) == "householder") ? 1 : 0;
   }
-  c->wp_elems = (size_t)imax * R * 1024;
-  CK(cudaMalloc(&c->dWp, sizeof(double) * std::min<size_t>(c->wp_elems, (size_t)imax * R * (size_t)std::max<int64_t>(1, (J + 63) / 64))));
+  c->wp_elems = (size_t)imax * R * kQ0MaxSlices;
+  CK(cudaMalloc(&c->dWp, sizeof(double) * c->wp_elems));
+  CK(cudaMalloc(&c->dq0cnt, sizeof(unsigned) * ((imax + 7) / 8 + 1)));
+  CK(cudaMemset(c->dq0cnt, 0, sizeof(unsigned) * ((imax + 7) / 8 + 1)));
   CK(cudaMalloc(&c->dnX2, sizeof(double) * 4));
   CK(cudaMalloc(&c->dfit, sizeof(double) * 4));
   CK(cudaMalloc(&c->dred, sizeof(double) * 8192));
@@ -1354,6 +1376,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   for (double* p : ps) if (p) cudaFree(p);
   if (c->dperm) cudaFree(c->dperm);
   if (c->dflags) cudaFree(c->dflags);
+  if (c->dq0cnt) cudaFree(c->dq0cnt);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);

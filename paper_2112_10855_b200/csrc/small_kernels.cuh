@@ -297,66 +297,73 @@ __global__ void __launch_bounds__(1024) k_kr_qr(KrQrArgs a) {
 }
 
 // ------------------------------------------------------------------------- K4: Q0 apply
-// Y column-major viewed as (Aa, In, Bb); Y_(n) column j = a + Aa b (Kolda-Bader).  Partial
-// W_part[ks](i, c) = sum_{j in chunk ks} Y_(n)(i, j) Q0(j, c), row-major (In x R); grid
-// (ceil(In/8), KS).  k_q0_reduce sums the KS partials in order.
+// W_n = Y_(n) Q0 (Alg. 2 line 9) on the FP64 tensor path (DMMA m8n8k4).
+// Y column-major viewed as (Aa, In, Bb); Y_(n) column j = a + Aa b (Kolda-Bader); W row-major.
+// CTA (ib, ks) multiplies rows [8 ib, 8 ib + 8) of Y_(n) by k-steps [ks kpc, (ks+1) kpc) of
+// Q0 (4 columns j per k-step); its 8 warps interleave those k-steps.  Warp partials are summed in
+// warp order; with KS > 1 slices, the last CTA of a row block to finish (threadfence + counter)
+// sums the slice partials in slice order.  One launch, bitwise reproducible.
+template <int NT>
 __global__ void __launch_bounds__(256)
-k_q0_apply(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb,
-           const double* __restrict__ Q0, int R, int jchunk, double* __restrict__ Wp) {
-  __shared__ double Ys[8][65];
-  __shared__ double Qs[64][65];
-  const int64_t J = Aa * Bb;
-  const int i0 = blockIdx.x * 8;
-  const int64_t jb = (int64_t)blockIdx.y * jchunk, je = min(J, jb + jchunk);
-  const int tid = threadIdx.x;
-  double acc[2] = {0.0, 0.0};
-  for (int64_t j0 = jb; j0 < je; j0 += 64) {
-    for (int e = tid; e < 8 * 64; e += 256) {
-      const int ii = e / 64, jj = e % 64;
-      const int64_t j = j0 + jj;
-      const int i = i0 + ii;
-      double v = 0.0;
-      if (i < In && j < je) {
-        const int64_t b = j / Aa, aa = j - b * Aa;
-        v = Y[aa + Aa * i + Aa * (int64_t)In * b];
-      }
-      Ys[ii][jj] = v;
-    }
-    for (int e = tid; e < 64 * R; e += 256) {
-      const int jj = e % 64, c = e / 64;
-      const int64_t j = j0 + jj;
-      Qs[jj][c] = (j < je) ? Q0[j + J * c] : 0.0;
-    }
-    __syncthreads();
+k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, const double* __restrict__ Q0, int R,
+              int kpc, int KS, double* __restrict__ Wp, unsigned* __restrict__ counters, double* __restrict__ W) {
+  __shared__ double red[8][64 * NT];
+  __shared__ int last;
+  const int64_t J = Aa * Bb, KT = (J + 3) / 4;
+  const int ib = blockIdx.x, ks = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int i = ib * 8 + g;
+  double acc[NT][2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int o = tid + 256 * q;
-      if (o < 8 * R) {
-        const int ii = o / R, c = o % R;
-        double s = acc[q];
-#pragma unroll 8
-        for (int jj = 0; jj < 64; ++jj) s = fma(Ys[ii][jj], Qs[jj][c], s);
-        acc[q] = s;
-      }
+  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+  const int64_t kb = (int64_t)ks * kpc, ke = min(KT, kb + kpc);
+#pragma unroll 4
+  for (int64_t kk = kb + warp; kk < ke; kk += 8) {
+    const int64_t j = 4 * kk + t;
+    double av = 0.0;
+    if (i < In && j < J) {
+      const int64_t bq = j / Aa, aa = j - bq * Aa;
+      av = __ldg(Y + aa + Aa * (i + (int64_t)In * bq));
     }
-    __syncthreads();
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int c = 8 * n + g;
+      const double bv = (j < J && c < R) ? __ldg(Q0 + j + J * c) : 0.0;
+      dmma(acc[n][0], acc[n][1], av, bv);
+    }
   }
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int o = tid + 256 * q;
-    if (o < 8 * R) {
-      const int ii = o / R, c = o % R;
-      const int i = i0 + ii;
-      if (i < In) Wp[((int64_t)blockIdx.y * In + i) * R + c] = acc[q];
-    }
+  for (int n = 0; n < NT; ++n) {
+    red[warp][g * 8 * NT + 8 * n + 2 * t] = acc[n][0];
+    red[warp][g * 8 * NT + 8 * n + 2 * t + 1] = acc[n][1];
   }
-}
-__global__ void k_q0_reduce(const double* __restrict__ Wp, int KS, int64_t n, double* __restrict__ W) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * NT; e += blockDim.x) {
+    const int r = e / (8 * NT), c = e % (8 * NT), ii = ib * 8 + r;
     double s = 0.0;
-    for (int k = 0; k < KS; ++k) s += Wp[k * n + e];
-    W[e] = s;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][e];
+    if (ii < In && c < R) {
+      if (KS == 1) W[(int64_t)ii * R + c] = s;
+      else Wp[((int64_t)ks * In + ii) * R + c] = s;
+    }
   }
+  if (KS == 1) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&counters[ib], 1u) == (unsigned)(KS - 1));
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < 8 * R; e += blockDim.x) {
+    const int ii = ib * 8 + e / R, c = e % R;
+    if (ii < In) {
+      double s = 0.0;
+      for (int k = 0; k < KS; ++k) s += __ldcg(Wp + ((int64_t)k * In + ii) * R + c);
+      W[(int64_t)ii * R + c] = s;
+    }
+  }
+  if (threadIdx.x == 0) counters[ib] = 0u;  // re-armed for the next launch (graph replay)
 }
 
 // ------------------------------------------------------------- one-sided Jacobi SVD of R0

@@ -232,15 +232,16 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
 // fmap(g) = (g>>1) + 4(g&1) (makes the 16-byte X loads conflict free under the swizzle).
 __device__ __forceinline__ int fmap(int g) { return (g >> 1) + 4 * (g & 1); }
 
-// One stage of the first contraction: acc[m][n] += Q1^T(r1, i) X(i, fibre) over the 16 i.
-template <int MT>
+// One stage of the first contraction: acc[m][n] += Q1^T(r1, i) X(i, fibre) over the 16 i, for the
+// warp's NF N-tiles of 8 fibres (fibre rows FW*warp + 8n + fmap(g) of the stage box).
+template <int MT, int NF = 2>
 __device__ __forceinline__ void fiber_stage(uint32_t xs, uint32_t qs, int warp, int g, int t,
-                                            double (&acc)[MT][2][2]) {
+                                            double (&acc)[MT][NF][2]) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    double2 xb[2];
+    double2 xb[NF];
 #pragma unroll
-    for (int n = 0; n < 2; ++n) xb[n] = lds128(xs + swz(16 * warp + 8 * n + fmap(g), 4 * h + t));
+    for (int n = 0; n < NF; ++n) xb[n] = lds128(xs + swz(8 * NF * warp + 8 * n + fmap(g), 4 * h + t));
 #pragma unroll
     for (int sk = 0; sk < 2; ++sk) {
       const int k = 8 * h + 2 * t + sk;
@@ -251,7 +252,7 @@ __device__ __forceinline__ void fiber_stage(uint32_t xs, uint32_t qs, int warp, 
 #pragma unroll
       for (int m = 0; m < MT; ++m)
 #pragma unroll
-        for (int n = 0; n < 2; ++n) dmma(acc[m][n][0], acc[m][n][1], qa[m], sk ? xb[n].y : xb[n].x);
+        for (int n = 0; n < NF; ++n) dmma(acc[m][n][0], acc[m][n][1], qa[m], sk ? xb[n].y : xb[n].x);
     }
   }
 }
@@ -306,7 +307,7 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
       const int s = it % S;
       mbar_wait(&full[s], (it / S) & 1);
       const uint32_t xs = sbase + s * STAGE;
-      fiber_stage<MT>(xs, xs + XBYTES, warp, g, t, acc);
+      fiber_stage<MT, 2>(xs, xs + XBYTES, warp, g, t, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -335,25 +336,28 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 // slice change the 8 warps' Y are summed in a fixed order through shared memory and written to
 // Yout[l] when the run covers the whole slice, else to the partial slot P[l][c - cta_of(l nfb)]
 // (fixed-order fix-up by k_slice_fixup).  Deterministic, no atomics.
-template <int MT>
+template <int MT, int NF>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int I1, int I2,
             int64_t L, const double* __restrict__ Q2, int64_t ldq2, int R, double* __restrict__ Yout,
             double* __restrict__ P, int nslots, int S) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (MT + 1) / 2;
-  constexpr uint32_t XBYTES = 128 * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
+  constexpr int BN = kCW * 8 * NF;  // fibres per unit (box height)
+  constexpr uint32_t XBYTES = BN * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
   uint8_t* st0 = tma_carve(smraw, S, full, empty);
-  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // kCW x R x R
+  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // kCW x R x R: per-warp Y
   const uint32_t sbase = smem_u32(st0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int RR = R * R;
+  for (int e = threadIdx.x; e < kCW * RR; e += blockDim.x) red[e] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
     fence_barrier_init();
   }
   __syncthreads();
-  const int nfb = (I2 + 127) / 128;
+  const int nfb = (I2 + BN - 1) / BN;
   const int64_t U = L * nfb;
   const int64_t G = gridDim.x;
   const int64_t u0 = (int64_t)blockIdx.x * U / G, u1 = ((int64_t)blockIdx.x + 1) * U / G;
@@ -371,7 +375,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
-          tma_load_3d_ef(dst, &tmX, ks * kBK, fb * 128, l, &full[s], pol);
+          tma_load_3d_ef(dst, &tmX, ks * kBK, fb * BN, l, &full[s], pol);
 #pragma unroll
           for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }
@@ -380,60 +384,99 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     return;
   }
   const int g = lane >> 2, t = lane & 3;
-  const int RR = R * R;
-  double yacc[MT][MT][2];
+  double* yw = red + warp * RR;  // this warp's running Y (r1 + R r2)
+  // NF == 2 (few stages per unit): Y stays in registers between flushes; NF == 4: in smem (yw),
+  // which frees the registers the 4 N-tiles of the first contraction need
+  constexpr bool YREG = NF <= 2;
+  double yreg[YREG ? MT : 1][YREG ? MT : 1][2];
 #pragma unroll
-  for (int m = 0; m < MT; ++m)
+  for (int m = 0; m < (YREG ? MT : 1); ++m)
 #pragma unroll
-    for (int n = 0; n < MT; ++n) yacc[m][n][0] = yacc[m][n][1] = 0.0;
+    for (int m2 = 0; m2 < (YREG ? MT : 1); ++m2) yreg[m][m2][0] = yreg[m][m2][1] = 0.0;
   uint32_t it = 0;
   int64_t run_start = u0;
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t l = u / nfb;
     const int fb = (int)(u - l * nfb);
-    double acc[MT][2][2];
+    double acc[MT][NF][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+      for (int n = 0; n < NF; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
     for (int ks = 0; ks < KS; ++ks, ++it) {
       const int s = it % S;
       mbar_wait(&full[s], (it / S) & 1);
       const uint32_t xs = sbase + s * STAGE;
-      fiber_stage<MT>(xs, xs + XBYTES, warp, g, t, acc);
+      fiber_stage<MT, NF>(xs, xs + XBYTES, warp, g, t, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // second contraction over this warp's 16 fibres (i2)
+    if constexpr (YREG) {
 #pragma unroll
-    for (int n = 0; n < 2; ++n)
+      for (int n = 0; n < NF; ++n)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int i2 = fb * 128 + 16 * warp + 8 * n + fmap(2 * t + j);
-        double qb[MT];
+        for (int j = 0; j < 2; ++j) {
+          const int i2 = fb * BN + 8 * NF * warp + 8 * n + fmap(2 * t + j);
+          double qb[MT];
 #pragma unroll
-        for (int m2 = 0; m2 < MT; ++m2) {
-          const int r2 = 8 * m2 + g;
-          qb[m2] = (i2 < I2 && r2 < R) ? __ldg(Q2 + i2 + ldq2 * r2) : 0.0;
+          for (int m2 = 0; m2 < MT; ++m2) {
+            const int r2 = 8 * m2 + g;
+            qb[m2] = (i2 < I2 && r2 < R) ? __ldg(Q2 + i2 + ldq2 * r2) : 0.0;
+          }
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int m2 = 0; m2 < MT; ++m2) dmma(yreg[m][m2][0], yreg[m][m2][1], acc[m][n][j], qb[m2]);
         }
+    } else {
+      // second contraction over this warp's 8 NF fibres (i2), accumulated into the warp's Y in smem;
+      // one 8-row block of Y (r1 in [8m, 8m+8)) live at a time keeps the register peak low
+  #pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int r1 = 8 * m + g;
+        double yacc[MT][2];
+  #pragma unroll
+        for (int m2 = 0; m2 < MT; ++m2)
+  #pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int r2 = 8 * m2 + 2 * t + j;
+            yacc[m2][j] = (r1 < R && r2 < R) ? yw[r1 + R * r2] : 0.0;
+          }
+  #pragma unroll
+        for (int n = 0; n < NF; ++n)
+  #pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i2 = fb * BN + 8 * NF * warp + 8 * n + fmap(2 * t + j);
+  #pragma unroll
+            for (int m2 = 0; m2 < MT; ++m2) {
+              const int r2 = 8 * m2 + g;
+              const double qb = (i2 < I2 && r2 < R) ? __ldg(Q2 + i2 + ldq2 * r2) : 0.0;
+              dmma(yacc[m2][0], yacc[m2][1], acc[m][n][j], qb);
+            }
+          }
+  #pragma unroll
+        for (int m2 = 0; m2 < MT; ++m2)
+  #pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int r2 = 8 * m2 + 2 * t + j;
+            if (r1 < R && r2 < R) yw[r1 + R * r2] = yacc[m2][j];
+          }
+      }
+    }
+    const bool flush = (u + 1 == u1) || ((u + 1) / nfb != l);
+    if (flush) {  // fixed-order reduction of the kCW warps' partial Y
+      if constexpr (YREG) {
 #pragma unroll
         for (int m = 0; m < MT; ++m)
 #pragma unroll
-          for (int m2 = 0; m2 < MT; ++m2) dmma(yacc[m][m2][0], yacc[m][m2][1], acc[m][n][j], qb[m2]);
+          for (int m2 = 0; m2 < MT; ++m2)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int r1 = 8 * m + g, r2 = 8 * m2 + 2 * t + j;
+              if (r1 < R && r2 < R) yw[r1 + R * r2] = yreg[m][m2][j];
+              yreg[m][m2][j] = 0.0;
+            }
       }
-    const bool flush = (u + 1 == u1) || ((u + 1) / nfb != l);
-    if (flush) {
-      // fixed-order reduction of the kCW warps' partial Y through shared memory
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int m2 = 0; m2 < MT; ++m2)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int r1 = 8 * m + g, r2 = 8 * m2 + 2 * t + j;
-            if (r1 < R && r2 < R) red[warp * RR + r1 + R * r2] = yacc[m][m2][j];
-            yacc[m][m2][j] = 0.0;
-          }
       consumers_sync();
       const bool whole = (run_start == l * nfb) && (u == l * nfb + nfb - 1);
       double* dst;
@@ -449,11 +492,12 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         dst[e] = v;
       }
       consumers_sync();
+      for (int e = threadIdx.x; e < kCW * RR; e += kCW * 32) red[e] = 0.0;
+      consumers_sync();
       run_start = u + 1;
     }
   }
 }
-
 
 // Small-slice variant (I2 <= 64, I2 % 8 == 0): a stage is the 3D box {16 i1, I2 fibres, 8 slices};
 // consumer warp w owns slice 8u + w entirely (nf2 = I2/8 N-tiles), chains the second contraction
