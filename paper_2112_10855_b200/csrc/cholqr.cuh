@@ -343,10 +343,18 @@ __device__ __forceinline__ void cq_gram_dmma(const double* P, int ld, int rows4,
   for (int pi = 0; pi < T; ++pi)
     for (int qi = pi; qi < T; ++qi, ++tile) {
       if (tile % nw != wid) continue;
-      double d0 = 0.0, d1 = 0.0;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;  // two independent DMMA chains
       const double* cp = P + (int64_t)ld * (8 * pi + g);
       const double* cq = P + (int64_t)ld * (8 * qi + g);
-      for (int k0 = 0; k0 < rows4; k0 += 4) dmma(d0, d1, cp[k0 + t], cq[k0 + t]);
+      int k0 = 0;
+#pragma unroll 2
+      for (; k0 + 8 <= rows4; k0 += 8) {
+        dmma(d0, d1, cp[k0 + t], cq[k0 + t]);
+        dmma(e0, e1, cp[k0 + 4 + t], cq[k0 + 4 + t]);
+      }
+      if (k0 < rows4) dmma(d0, d1, cp[k0 + t], cq[k0 + t]);
+      d0 += e0;
+      d1 += e1;
       const int r = 8 * pi + g, c0 = 8 * qi + 2 * t;
       G[r + RB * c0] = d0;
       G[r + RB * (c0 + 1)] = d1;
@@ -873,25 +881,45 @@ __device__ __noinline__ bool cq_chol_2d(double* Gs, int R, double* Ru, double* i
   __syncthreads();
   // critical path per column: LDS of the pivot, its reciprocal (__drcp_rn == 1.0 / d, correctly
   // rounded), one FMA per owned entry, barrier; square roots are taken after the loop
+  if (nw == 8) {
 #pragma unroll 1
-  for (int j = 0; j < R; ++j) {
-    const double d = Gs[j + RB * j];
-    if (i > j && i < R) {
-      const double id = (d > 0.0) ? __drcp_rn(d) : 0.0;
-      const double gij = -Gs[i + RB * j] * id;
-      if (nw == 8) {
+    for (int j = 0; j < R; ++j) {
+      // every load of the column step first (one shared-memory round trip), then the reciprocal
+      const bool act = i > j && i < R;
+      const double d = Gs[j + RB * j];
+      double gi = 0.0, gk[RB / 8], gik[RB / 8];
+#pragma unroll
+      for (int q = 0; q < RB / 8; ++q) {
+        const int k = kk + 8 * q;
+        const bool on = act && k > j && k <= i;
+        gk[q] = on ? Gs[k + RB * j] : 0.0;
+        gik[q] = on ? Gs[i + RB * k] : 0.0;
+      }
+      if (act) gi = Gs[i + RB * j];
+      if (act) {
+        const double id = (d > 0.0) ? __drcp_rn(d) : 0.0;
+        const double gij = -gi * id;
 #pragma unroll
         for (int q = 0; q < RB / 8; ++q) {
           const int k = kk + 8 * q;
-          if (k > j && k <= i) Gs[i + RB * k] = fma(gij, Gs[k + RB * j], Gs[i + RB * k]);
+          if (k > j && k <= i) Gs[i + RB * k] = fma(gij, gk[q], gik[q]);
         }
-      } else {
+      }
+      __syncthreads();
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < R; ++j) {
+      const double d = Gs[j + RB * j];
+      if (i > j && i < R) {
+        const double id = (d > 0.0) ? __drcp_rn(d) : 0.0;
+        const double gij = -Gs[i + RB * j] * id;
 #pragma unroll 1
         for (int k = kk; k < RB; k += nw)
           if (k > j && k <= i) Gs[i + RB * k] = fma(gij, Gs[k + RB * j], Gs[i + RB * k]);
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   // pivots d_j = Gs(j, j) are final; L_jj = sqrt(d_j); warp 0 also forms ok / max L_jj / min L_jj
   bool ok = true;
@@ -937,7 +965,7 @@ __device__ __forceinline__ double cluster_sum_ordered(cooperative_groups::cluste
 
 #ifdef CPQR_DEBUG_TIMING
 #define CQ_T(k) do { if (threadIdx.x == 0) tstamp[k] = clock64(); } while (0)
-#define CQ_DUMP() do { if (threadIdx.x == 0 && cluster.block_rank() == 0) printf("cq phases: %lld %lld %lld %lld %lld %lld %lld %lld | lam+sync %lld chol %lld sync %lld inv %lld\n", tstamp[1]-tstamp[0], tstamp[2]-tstamp[1], tstamp[3]-tstamp[2], tstamp[4]-tstamp[3], tstamp[5]-tstamp[4], tstamp[6]-tstamp[5], tstamp[7]-tstamp[6], tstamp[8]-tstamp[7], tstamp[9]-tstamp[3], tstamp[10]-tstamp[9], tstamp[11]-tstamp[10], tstamp[12]-tstamp[11]); } while (0)
+#define CQ_DUMP() do { if (threadIdx.x == 0 && cluster.block_rank() == 0) printf("cq phases: %lld %lld %lld %lld %lld %lld %lld %lld | lam+sync %lld chol %lld sync %lld inv %lld | zero %lld load %lld solve %lld\n", tstamp[1]-tstamp[0], tstamp[2]-tstamp[1], tstamp[3]-tstamp[2], tstamp[4]-tstamp[3], tstamp[5]-tstamp[4], tstamp[6]-tstamp[5], tstamp[7]-tstamp[6], tstamp[8]-tstamp[7], tstamp[9]-tstamp[3], tstamp[10]-tstamp[9], tstamp[11]-tstamp[10], tstamp[12]-tstamp[11], tstamp[13]-tstamp[0], tstamp[14]-tstamp[13], tstamp[15]-tstamp[14]); } while (0)
 #else
 #define CQ_T(k) do {} while (0)
 #define CQ_DUMP() do {} while (0)
@@ -959,7 +987,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   double* Ui = R2s + RB * RB;  // (unused scratch; keeps the host smem size formula)
   double* Ms = Ui + RB * RB;
   double* R0s = Ms + RB * RB;
-  __shared__ double lam[RB], redi[8], innerb, inv1[RB], inv2[RB], invm[RB];
+  __shared__ double lam[RB], invlam[RB], redi[8], innerb, inv1[RB], inv2[RB], invm[RB];
   __shared__ int okf;
   (void)Ui;
   const int nb = a.nb, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -976,6 +1004,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   #pragma unroll 1
   for (int e = tid; e < 2 * RB * RB; e += blockDim.x) Ms[e] = 0.0;  // Ms, R0s
   __syncthreads();
+  CQ_T(13);
   // all global inputs in flight at once (cp.async), one wait
   if (a.solve) {
     #pragma unroll 1
@@ -985,15 +1014,16 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
       if (r <= c) cp_async8(&R0s[r + RB * c], a.R0 + e);
     }
   }
-  if (own) {
-    #pragma unroll 1
-    for (int k = 0; k < R; ++k) {
-      if (a.solve) cp_async8(&Y[tid + ld * k], a.W + (int64_t)i * R + k);  // W row (panel Y)
-      else cp_async8(&X[tid + ld * k], a.A + i + (int64_t)a.m * k);
-    }
+  if (a.solve) {  // the CTA's W rows are one contiguous row-major block: coalesced copy
+    #pragma unroll 4
+    for (int e = tid; e < rows * R; e += blockDim.x) cp_async8(&Y[(e / R) + ld * (e % R)], a.W + (int64_t)r0 * R + e);
+  } else if (own) {
+    #pragma unroll 4
+    for (int k = 0; k < R; ++k) cp_async8(&X[tid + ld * k], a.A + i + (int64_t)a.m * k);
   }
   cp_async_wait_all();
   __syncthreads();
+  CQ_T(14);
   if (a.solve && a.variant != 2 && tid < RB) invm[tid] = (tid < R) ? 1.0 / Ms[tid + RB * tid] : 0.0;
   __syncthreads();
   // ---- 1. solve for the panel rows (Alg. 2 line 10)
@@ -1002,13 +1032,14 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
     if (a.variant == 2) {
       cq_row_gemv<RB>(Y + tid, X + tid, ld, Ms);  // x = w M, M = U S^+ V^T
     } else {
-      #pragma unroll 1
+      #pragma unroll 8
       for (int k = 0; k < RB; ++k) X[tid + ld * k] = Y[tid + ld * k];
       cq_row_trsv<RB, true>(X + tid, ld, Ms, invm);  // Ahat R0^T = W
     }
+    CQ_T(15);
     if (a.do_fit) inner = cq_row_wTx<RB>(Y + tid, X + tid, ld, R0s);  // <W, Ahat R0^T>
     if (own)
-      #pragma unroll 1
+      #pragma unroll 8
       for (int k = 0; k < R; ++k) a.Ahat[i + (int64_t)a.m * k] = X[tid + ld * k];
   }
   inner = warp_sum(inner);
@@ -1030,14 +1061,16 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   const double inner_all = cluster_sum_ordered(cluster, &innerb, nb);
   __syncthreads();
   CQ_T(3);
-  if (a.solve && tid < R) lam[tid] = sqrt(Gs[tid + RB * tid]);  // lambda_c = ||Ahat(:,c)||_2
+  if (a.solve && tid < R) {
+    const double l = sqrt(Gs[tid + RB * tid]);  // lambda_c = ||Ahat(:,c)||_2
+    lam[tid] = l;
+    invlam[tid] = (l > 0.0) ? 1.0 / l : 0.0;
+  }
   __syncthreads();
   if (a.solve && own) {  // A_n = Ahat diag(1/lambda) straight from the panel
-    #pragma unroll 1
-    for (int k = 0; k < R; ++k) {
-      const double l = lam[k];
-      a.Aout[i + (int64_t)a.m * k] = (l > 0.0) ? X[tid + ld * k] / l : (i == 0 ? 1.0 : 0.0);
-    }
+    #pragma unroll 8
+    for (int k = 0; k < R; ++k)
+      a.Aout[i + (int64_t)a.m * k] = (lam[k] > 0.0) ? X[tid + ld * k] * invlam[k] : (i == 0 ? 1.0 : 0.0);
   }
   CQ_T(9);
   {
@@ -1056,7 +1089,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   CQ_T(12);
   CQ_T(4);
   // ---- 3. Q1 = X R1^{-1}, Gram, Cholesky -> R2, R2^{-1}
-  #pragma unroll 1
+  #pragma unroll 8
   for (int k = 0; k < RB; ++k) Y[tid + ld * k] = X[tid + ld * k];
   cq_row_trsv<RB, false>(Y + tid, ld, R1s, inv1);
   __syncthreads();
@@ -1065,17 +1098,15 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   cluster.sync();
   #pragma unroll 1
   for (int e = tid; e < RB * RB; e += blockDim.x) Gs[e] = cluster_sum_ordered(cluster, G2b + e, nb);
-  __syncthreads();
-  if (wid == 0) {
-    double e = 0.0;  // ||G2 - I||_max must be O(kappa^2 eps)
-    #pragma unroll 1
-    for (int q = lane; q < R * R; q += 32) {
-      const int r = q % R, c = q / R;
-      e = fmax(e, fabs(Gs[r + RB * c] - (r == c ? 1.0 : 0.0)));
+  {
+    bool bad = false;  // ||G2 - I||_max must be O(kappa^2 eps)
+    #pragma unroll 4
+    for (int q = tid; q < RB * RB; q += blockDim.x) {
+      const int r = q % RB, c = q / RB;
+      if (r < R && c < R) bad |= !(fabs(Gs[q] - (r == c ? 1.0 : 0.0)) < 1.0e-4);
     }
-    #pragma unroll 1
-    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
-    if (lane == 0) okf = (e < 1.0e-4);
+    bad = __syncthreads_or(bad);
+    if (tid == 0) okf = !bad;
   }
   {
     double ratio;
@@ -1092,10 +1123,17 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   // ---- 4. Q = Q1 R2^{-1} (in the Y panel), outputs
   cq_row_trsv<RB, false>(Y + tid, ld, R2s, inv2);
   if (own) {
-    #pragma unroll 1
+    #pragma unroll 8
     for (int k = 0; k < R; ++k) a.Q[i + (int64_t)a.m * k] = Y[tid + ld * k];
-    #pragma unroll 1
-    for (int k = 0; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? Y[tid + ld * k] : 0.0;
+  }
+  __syncthreads();
+  {  // Qt rows of this CTA: one contiguous row-major block, written coalesced
+    const int RQ = a.RQ;
+    #pragma unroll 4
+    for (int e = tid; e < rows * RQ; e += blockDim.x) {
+      const int row = e / RQ, k = e - row * RQ;
+      a.Qt[(int64_t)r0 * RQ + e] = (k < R) ? Y[row + ld * k] : 0.0;
+    }
   }
   CQ_T(7);
   if (b == 0) {

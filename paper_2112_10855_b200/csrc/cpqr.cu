@@ -91,6 +91,7 @@ struct cpqr_ctx {
   double *dQt[kMaxN] = {0}, *dAt[kMaxN] = {0};  // transposed, zero-padded (I_k x RQ) TMA panels
   int RQ = 16;
   bool use_tma = true;
+  bool fuse_slice = true;  // see plan_mode
   cudaStream_t side = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   double *dRstack = nullptr, *dV = nullptr, *dtauv = nullptr, *dQtop = nullptr, *dinner = nullptr;
@@ -278,6 +279,7 @@ struct PlanIn {
   int RQ;
   bool ne;
   bool tma;
+  bool fuse;  // fused two-mode slice kernel allowed for n >= 3
   int sms;
 };
 
@@ -321,8 +323,10 @@ int stages_for(size_t stage, size_t extra) {
 }
 
 // Multi-TTM Y = X x_{k != n} Q_k^T (Alg. 2 line 8).  Stream-X pass: modes 1 and 2 together
-// (fused slice kernel) when n >= 3, else the last mode (strided kernel, the largest contiguous
-// GEMM); the remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
+// (fused slice kernel) when n >= 3 and the pass is HBM-bound (R < 24: R/4 flop per byte is below
+// the FP64-DMMA : HBM balance of ~5.7); when it is FP64-bound (R >= 24) mode 2 alone (strided
+// kernel over the middle mode, no second contraction on the critical DMMA loop); for n < 3 the
+// last mode (strided kernel, the largest contiguous GEMM).  The remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
 // (ties by decreasing mode, reading 5).  TMA kernels whenever the layout allows
 // (even leading dimension, 16-B aligned base), else the register-staged kernels.
 // N-tiles of 8 fibres per consumer warp in the fused slice kernel (box height kCW * 8 * NF)
@@ -422,7 +426,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     p.m_rowmajor = (n >= 1) ? 1 : 0;  // (R, I_n) column-major == row-major I_n x R
     return;
   }
-  if (N >= 3 && n >= 2) {
+  if (N >= 3 && n >= 2 && !in.fuse) {
+    emit_ttm(1);  // stream pass over the middle mode (strided kernel), then the rest
+    for (int k = 0; k < N; ++k) if (k != n && k != 1) todo.push_back(k);
+  } else if (N >= 3 && n >= 2) {
     TtmStep s{};
     s.kind = 2;
     s.in = src;
@@ -635,6 +642,7 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
   in.n = n;
   in.ne = ne;
   in.tma = c->use_tma;
+  in.fuse = c->fuse_slice;
   in.sms = c->stream_sms;
   in.RQ = c->RQ;
   for (int k = 0; k < c->N; ++k) {
@@ -1257,6 +1265,10 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->R = R;
   c->RQ = 16 * ((R + 15) / 16);
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
+  {
+    const char* f = getenv("CPQR_SLICE");  // "1" / "0" force the fused slice kernel on / off
+    c->fuse_slice = f ? (f[0] == '1') : (R < 24);
+  }
   for (int k = 0; k < N; ++k) c->dims[k] = c->ldims[k] = dims[k];
   const int64_t per = dims[N - 1] / c->opt.world;
   c->slab_b = per * c->opt.rank;

@@ -233,3 +233,27 @@ def test_multi_kernel_cholqr_path(cp, dims, R, monkeypatch):
     ref = O.cp_als_qr(X, init, 2)
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
     s.close()
+
+
+@pytest.mark.parametrize("dims,R,fuse", [((34, 300, 40), 32, "1"), ((70, 66, 34), 32, "1"),
+                                         ((64, 48, 40), 16, "0"), ((26, 270, 24, 25), 24, "1"),
+                                         ((26, 270, 24, 25), 24, "0")])
+def test_fused_slice_on_and_off(cp, dims, R, fuse, monkeypatch):
+    """Modes n >= 3 with the fused two-mode slice kernel forced on (NF = 4 for I2 >= 256, ragged
+    last fibre block, per-warp Y in shared memory) or off (strided pass over the middle mode)."""
+    monkeypatch.setenv("CPQR_SLICE", fuse)
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=73, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    N = len(dims)
+    Qs = [O.qr_pos(a)[0] for a in init]
+    for n in range(2, N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+    f = s.sweep(2)
+    ref = O.cp_als_qr(X, init, 2)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
