@@ -237,10 +237,12 @@ def test_multi_kernel_cholqr_path(cp, dims, R, monkeypatch):
 
 @pytest.mark.parametrize("dims,R,fuse", [((34, 300, 40), 32, "1"), ((70, 66, 34), 32, "1"),
                                          ((64, 48, 40), 16, "0"), ((26, 270, 24, 25), 24, "1"),
-                                         ((26, 270, 24, 25), 24, "0")])
+                                         ((26, 270, 24, 25), 24, "0"), ((300, 40, 100), 32, "0")])
 def test_fused_slice_on_and_off(cp, dims, R, fuse, monkeypatch):
     """Modes n >= 3 with the fused two-mode slice kernel forced on (NF = 4 for I2 >= 256, ragged
-    last fibre block, per-warp Y in shared memory) or off (strided pass over the middle mode)."""
+    last fibre block, per-warp Y in shared memory) or off (strided pass over the middle mode).
+    (300, 40, 100): 200 strided units > the grid, so the stream-K last wave (pieces of 1-2 k-steps
+    summed by the last arrival) runs."""
     monkeypatch.setenv("CPQR_SLICE", fuse)
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=73, eta=0.05)
     X = O.as_tensor(Xc)
