@@ -7,8 +7,13 @@ the whole (slab of the) tensor, i.e. every row of SURVEY.md §8(a).  Default wor
 another BASELINE config.  Inputs are the seeded synthetic tensors of synth.py (DESIGN.md
 §Inputs); X (8 GB) is far larger than the 126 MB L2, so no flush is needed between steps.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--variant QR]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--variant QR] [--tree]
   python bench.py --impl reference ...     # the CPU oracle (oracle/) on the host cores
+
+The headline `value` times the paper's schedule (one Multi-TTM pass over X per mode, Alg. 2
+line 8).  The same line carries "dimension_tree": the dimension-tree Multi-TTM (PAPER.md:472-478,
+SURVEY.md §8(f) NEXT-1; two passes over X per sweep, identical mode updates up to rounding) timed
+the same way on the same resident tensor.  --tree swaps the two.
 
 Multi-GPU: launched by torch.distributed.run, one process per GPU; the NCCL id is broadcast
 over a gloo group; timing = CUDA events on the stream the library runs on, max over ranks.
@@ -162,6 +167,7 @@ def main():
     ap.add_argument("--impl", default="cpqr", choices=["cpqr", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tree", action="store_true", help="headline = dimension-tree Multi-TTM")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -182,40 +188,55 @@ def main():
     conf, Xc, slab, truth, init, _ = load_input(conf, rank, world)
 
     stream = torch.cuda.current_stream()
-    s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                  rank=rank, world=world, nccl_id=nccl_id)
+    tree_ok = variant != "NE" and conf.N >= 3
+    tree = bool(args.tree and tree_ok)
     Xd = torch.from_numpy(np.ascontiguousarray(slab)).to(f"cuda:{local}")
-    s.set_tensor(Xd)                         # device-resident input (borrowed)
-    s.set_factors(init)
-    s.sweep(args.warmup)                     # warm-up (also captures the CUDA graph)
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
 
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = s.profile(reset=False)["launches_total"]
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        s.sweep(args.steps)
-        e1.record(stream)
+    def timed_arm(use_tree, sample_clocks):
+        """W warm-up sweeps (CUDA-graph capture), then exactly K sweeps between CUDA events on
+        the library's stream, barrier + synchronize on both sides, max over ranks."""
+        s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
+                      rank=rank, world=world, nccl_id=nccl_id, tree=use_tree)
+        s.set_tensor(Xd)                     # device-resident input (borrowed)
+        s.set_factors(init)
+        s.sweep(args.warmup)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = s.profile(reset=False)["launches_total"]
+        barrier()
         torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    launches = s.profile(reset=False)["launches_total"] - launches0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            s.sweep(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        launches = s.profile(reset=False)["launches_total"] - launches0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        s.close()
+        return ms, launches, (clk.summary() if sample_clocks else None)
+
+    ms, launches, clocks = timed_arm(tree, True)
     sweeps_s = args.steps / (ms / 1e3)
+    other = None
+    if tree_ok:
+        ms2, l2, _ = timed_arm(not tree, False)
+        other = {"value": args.steps / (ms2 / 1e3), "unit": "sweeps/s", "ms_per_step": ms2 / args.steps,
+                 "gpu_launches": int(l2)}
 
     # phase profile (separate short run; events around each phase on the library stream)
     sp = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                   rank=rank, world=world, nccl_id=nccl_id, profile=True, use_graph=False) if world == 1 else None
+                   rank=rank, world=world, nccl_id=nccl_id, profile=True, use_graph=False,
+                   tree=tree) if world == 1 else None
     prof = None
     if sp is not None:
         sp.set_tensor(Xd)
@@ -234,7 +255,7 @@ def main():
     if not args.no_e2e:
         Xh = torch.from_numpy(np.ascontiguousarray(slab)).pin_memory()
         se = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                       rank=rank, world=world, nccl_id=nccl_id)
+                       rank=rank, world=world, nccl_id=nccl_id, tree=tree)
         se.set_tensor(Xh)
         se.set_factors(init)
         se.sweep(1)
@@ -263,13 +284,12 @@ def main():
                "step": f"one solve through the C-ABI from host buffers: H2D X slab (pinned) + set_factors + "
                        f"{conf.sweeps} sweeps + D2H factors/fits; wall clock, max over ranks"}
         se.close()
-    s.close()
-
     if rank != 0:
         return 0
     hbm_peak, hbm_src = peaks()
     numel_local = int(np.prod(conf.dims)) // world
-    mt_bytes_sweep = conf.N * 8.0 * numel_local           # X read once per mode
+    # X read once per mode; twice per sweep with the dimension tree
+    mt_bytes_sweep = (2 if tree else conf.N) * 8.0 * numel_local
     line = {
         "metric": "CP-ALS-QR sweeps/s & Multi-TTM HBM GB/s (fp64)",
         "value": sweeps_s * 1.0, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
@@ -278,15 +298,17 @@ def main():
         "data": "synthetic (synth.py seeded recipe of BASELINE.json config; no dataset)",
         "config": {"workload": conf.name, "variant": variant, "dims": list(conf.dims), "R": conf.R,
                    "global_batch": 1, "parallelism": f"slab-dp{world} on mode {conf.N}",
+                   "multittm": "dimension tree (2 passes over X per sweep)" if tree else
+                               "per mode (one pass over X per mode, Alg. 2 line 8)",
                    "l2": "inputs larger than L2 (X = %.2f GB/GPU vs 126 MB L2)" % (8.0 * numel_local / 1e9)},
         "gpu_launches": int(launches),
     }
     if prof:
         nsw = prof["sweeps"]
-        n_launch0 = conf.N * nsw
+        n_launch0 = (2 if tree else conf.N) * nsw
         t0_avg_ms = prof["ms"][0] / n_launch0
-        bytes_launch = prof["bytes0"] / conf.N
-        flops_launch = prof["flops0"] / conf.N
+        bytes_launch = prof["bytes0"] / (2 if tree else conf.N)
+        flops_launch = prof["flops0"] / (2 if tree else conf.N)
         gbs = bytes_launch / (t0_avg_ms / 1e3) / 1e9
         tfl = flops_launch / (t0_avg_ms / 1e3) / 1e12
         t_hbm, t_fp = bytes_launch / (hbm_peak * 1e9), flops_launch / (P64_DMMA_TFLOPS * 1e12)
@@ -296,7 +318,8 @@ def main():
         else:
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                     "peak_source": hbm_src}
-        roof["kernel"] = "Multi-TTM stream-X pass (k_ttm_strided / k_mttm_slice), avg over %d launches" % n_launch0
+        roof["kernel"] = ("Multi-TTM stream-X pass (k_strided_tma / k_slice_tma / k_slice_small_tma), "
+                          "avg over %d passes" % n_launch0)
         roof["traffic"] = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tfile):
@@ -309,7 +332,11 @@ def main():
         line["multi_ttm_gbs"] = mt_bytes_sweep / ((prof["ms"][0] + prof["ms"][1]) / nsw / 1e3) / 1e9
         line["phase_ms_per_sweep"] = {k: v / nsw for k, v in zip(
             ["stream_pass", "rest_ttm", "factor_qr", "q0_compute", "q0_apply", "other"], prof["ms"])}
-    line["clocks"] = clk.summary()
+    line["clocks"] = clocks
+    if other:
+        line["per_mode" if tree else "dimension_tree"] = dict(other, note=(
+            "the other Multi-TTM schedule, same config/inputs/timing; dimension tree = PAPER.md:472-478, "
+            "SURVEY.md 8(f) NEXT-1, mode updates identical up to rounding (tests/test_gpu_parity.py)"))
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu:

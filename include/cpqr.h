@@ -73,10 +73,15 @@ typedef struct cpqr_options {
   uint8_t nccl_id[128];   /* ncclUniqueId from cpqr_nccl_unique_id() on rank 0, broadcast */
   int32_t use_graph;      /* 1: capture one sweep as a CUDA graph and replay it */
   int32_t profile;        /* 1: record CUDA events around each phase (cpqr_get_profile) */
+  int32_t mttm_tree;      /* QR/SVD, N >= 3: 1 = dimension-tree Multi-TTM: modes
+                             [0, h) share T_L = X x_{k>=h} Q_k^T and modes [h, N) share
+                             T_R = X x_{k<h} Q_k^T, h = ceil(N/2), so a sweep streams X twice
+                             instead of N times; Y_(n) equals the per-mode Multi-TTM up to
+                             rounding.  0 (default) = one pass over X per mode (Alg. 2 line 8). */
 } cpqr_options;
 
 /* Fills *opt with defaults: svd_tau = -1, FAST fit, device 0, own stream, world 1,
- * use_graph 1, profile 0. */
+ * use_graph 1, profile 0, mttm_tree 0. */
 void cpqr_default_options(cpqr_options* opt);
 
 typedef struct cpqr_ctx cpqr_ctx;

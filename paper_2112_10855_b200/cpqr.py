@@ -38,7 +38,8 @@ EXPORTS = [
 class Options(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("svd_tau", C.c_double), ("fit_mode", C.c_int32),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
-                ("nccl_id", C.c_uint8 * 128), ("use_graph", C.c_int32), ("profile", C.c_int32)]
+                ("nccl_id", C.c_uint8 * 128), ("use_graph", C.c_int32), ("profile", C.c_int32),
+                ("mttm_tree", C.c_int32)]
 
 
 class Profile(C.Structure):
@@ -101,7 +102,7 @@ class CPQR:
     """One CP-ALS(-QR) solver over a (slab of a) dense fp64 tensor on one GPU."""
 
     def __init__(self, dims, R, variant="QR", svd_tau=-1.0, fit_mode="fast", device=0, stream=None,
-                 rank=0, world=1, nccl_id=None, use_graph=True, profile=False):
+                 rank=0, world=1, nccl_id=None, use_graph=True, profile=False, tree=False):
         self.dims = tuple(int(d) for d in dims)
         self.N, self.R = len(self.dims), int(R)
         self.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
@@ -116,6 +117,7 @@ class CPQR:
             C.memmove(opt.nccl_id, bytes(nccl_id), 128)
         opt.use_graph = 1 if use_graph else 0
         opt.profile = 1 if profile else 0
+        opt.mttm_tree = 1 if tree else 0  # dimension-tree Multi-TTM (QR/SVD, N >= 3)
         self.rank, self.world = int(rank), int(world)
         per = self.dims[-1] // self.world
         self.slab = (per * self.rank, per * (self.rank + 1))

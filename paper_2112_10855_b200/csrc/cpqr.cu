@@ -69,6 +69,7 @@ struct Plan {
   int m_rowmajor = 1;  // NE: layout of the MTTKRP result
   size_t max_buf = 0;
   size_t part = 0;
+  size_t tree_elems = 0;  // dimension tree: size of the half intermediate this plan writes
 };
 
 }  // namespace
@@ -92,6 +93,10 @@ struct cpqr_ctx {
   int RQ = 16;
   bool use_tma = true;
   bool fuse_slice = true;  // see plan_mode
+  bool tree = false;       // dimension-tree Multi-TTM (opt.mttm_tree, QR/SVD, N >= 3)
+  int tree_h = 0;
+  double* dTree = nullptr;
+  size_t tree_alloc = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   double *dRstack = nullptr, *dV = nullptr, *dtauv = nullptr, *dQtop = nullptr, *dinner = nullptr;
@@ -281,6 +286,10 @@ struct PlanIn {
   bool tma;
   bool fuse;  // fused two-mode slice kernel allowed for n >= 3
   int sms;
+  bool tree = false;        // dimension-tree Multi-TTM (QR/SVD variants)
+  int h = 0;                // tree split: halves [0, h) and [h, N)
+  bool tree_fresh = false;  // this mode computes its half's intermediate from X
+  double* tbuf = nullptr;   // the tree buffer
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -350,10 +359,15 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     const uint32_t box[2] = {16, 16};
     return in.Qt[k] && make_tmap(&s.mq, in.Qt[k], 2, d, st, box);
   };
+  double* out_override = nullptr;  // tree plans: the last step of a half pass writes the tree buffer
+  auto advance = [&](double* out) {  // the next step reads `out`
+    src = out;
+    if (!out_override) nb ^= 1;
+  };
   auto emit_ttm = [&](int k) {
     TtmStep s{};
     s.in = src;
-    s.out = bufs[nb];
+    s.out = out_override ? out_override : bufs[nb];
     s.Q = in.Q[k];
     s.ldq = in.ldq[k];
     if (k == 0) {
@@ -387,8 +401,95 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     cur[k] = R;
     p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
     p.steps.push_back(s);
-    src = bufs[nb];
-    nb ^= 1;
+    advance(s.out);
+  };
+  // fused contraction of modes 0 and 1 of src (fused slice kernels, Alg. 2 line 8)
+  auto emit_slice = [&]() {
+      TtmStep s{};
+      s.kind = 2;
+      s.in = src;
+      s.I1 = (int)cur[0];
+      s.I2 = (int)cur[1];
+      s.L = prod(cur, 2, N);
+      s.Q = in.Q[0];
+      s.ldq = in.ldq[0];
+      s.Q2 = in.Q[1];
+      s.ldq2 = in.ldq[1];
+      bool tma = false;
+      if (in.tma && s.I1 % 2 == 0 && s.L < (1ll << 31) && bufs[0]) {
+        const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
+        const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
+        const uint32_t box[3] = {16, (uint32_t)(kCW * 8 * slice_nf(s.I2)), 1};
+        tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
+      }
+      const bool small = tma && s.I2 <= 64 && s.I2 % 8 == 0 && NT <= 2;
+      if (small) {
+        const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
+        const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
+        const uint32_t box[3] = {16, (uint32_t)s.I2, 8};
+        if (make_tmap(&s.mx, src, 3, d, st, box)) {
+          s.kind = 8;
+          s.S = stages_for((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes, 0);
+          s.out = out_override ? out_override : bufs[nb];
+          p.steps.push_back(s);
+        } else {
+          tma = false;
+        }
+      }
+      if (small && s.kind == 8) {
+        // done
+      } else if (tma) {
+        s.kind = 6;
+        const int MT = NT;
+        s.gps = slice_nf(s.I2);
+        const int BN = kCW * 8 * s.gps;
+        s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
+        s.nfb = (s.I2 + BN - 1) / BN;
+        const int64_t U = s.L * s.nfb;
+        s.G = std::min<int64_t>(U, in.sms);
+        int ns = 1;
+        for (int64_t l = 0; l < s.L; ++l) {
+          const int64_t c0 = ((l * s.nfb + 1) * s.G - 1) / U, c1 = ((l * s.nfb + s.nfb) * s.G - 1) / U;
+          ns = std::max<int>(ns, (int)(c1 - c0 + 1));
+        }
+        s.nslots = ns;
+        s.out = out_override ? out_override : bufs[nb];
+        s.P = part;
+        if (ns > 1) p.part = std::max(p.part, (size_t)s.L * ns * R * R);
+        (void)MT;
+        p.steps.push_back(s);
+        if (ns > 1) {
+          TtmStep f = s;
+          f.kind = 7;
+          p.steps.push_back(f);
+        }
+      } else {
+        const int fw = slice_fw(R);
+        const int ngr = (s.I2 + fw - 1) / fw;
+        const int64_t target = (int64_t)in.sms * 2 * kWarps * 4;
+        int gps = 1;
+        if ((int64_t)ngr * s.L > target) gps = (int)std::min<int64_t>(ngr, ((int64_t)ngr * s.L + target - 1) / target);
+        s.gps = gps;
+        s.nseg = (ngr + gps - 1) / gps;
+        if (s.nseg > 1) {
+          s.out = part;
+          p.part = std::max(p.part, (size_t)s.nseg * s.L * R * R);
+        } else {
+          s.out = out_override ? out_override : bufs[nb];
+        }
+        TtmStep sr = s;
+        p.steps.push_back(s);
+        if (s.nseg > 1) {
+          sr.kind = 3;  // reduce partials
+          sr.in = part;
+          sr.out = out_override ? out_override : bufs[nb];
+          p.steps.push_back(sr);
+        }
+      }
+      cur[0] = R;
+      cur[1] = R;
+      p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
+      advance(out_override ? out_override : bufs[nb]);
   };
   if (in.ne) {
     // MTTKRP M_n = X_(n) Z_n: one dense TTM with A_k, then Khatri-Rao-diagonal contractions.
@@ -426,96 +527,49 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     p.m_rowmajor = (n >= 1) ? 1 : 0;  // (R, I_n) column-major == row-major I_n x R
     return;
   }
-  if (N >= 3 && n >= 2 && !in.fuse) {
+  if (in.tree && N >= 3) {
+    // Dimension tree: modes [0, h) share T_L = X x_{k >= h} Q_k^T, modes
+    // [h, N) share T_R = X x_{k < h} Q_k^T.  The first mode of each half streams X once into the
+    // tree buffer; the others start from it.  Same Y_(n) as the per-mode Multi-TTM up to rounding.
+    const int h = in.h;
+    const bool left = n < h;
+    const int o0 = left ? h : 0, o1 = left ? N : h;  // the other half [o0, o1)
+    if (in.tree_fresh) {
+      std::vector<int> ord;
+      if (left) {
+        for (int k = N - 1; k >= h; --k) ord.push_back(k);  // last mode first: strided, B = 1
+        for (size_t q = 0; q < ord.size(); ++q) {
+          if (q + 1 == ord.size()) out_override = in.tbuf;
+          emit_ttm(ord[q]);
+        }
+      } else if (h >= 2 && in.fuse) {
+        if (h == 2) out_override = in.tbuf;
+        emit_slice();
+        for (int k = 2; k < h; ++k) {
+          if (k == h - 1) out_override = in.tbuf;
+          emit_ttm(k);
+        }
+      } else {
+        if (h >= 2) ord.push_back(1);  // middle mode (strided), then mode 0 (fibres), then the rest
+        ord.push_back(0);
+        for (int k = 2; k < h; ++k) ord.push_back(k);
+        for (size_t q = 0; q < ord.size(); ++q) {
+          if (q + 1 == ord.size()) out_override = in.tbuf;
+          emit_ttm(ord[q]);
+        }
+      }
+      out_override = nullptr;
+      p.tree_elems = (size_t)prod(cur, 0, N);
+    } else {
+      src = in.tbuf;
+      for (int k = o0; k < o1; ++k) cur[k] = R;
+    }
+    for (int k = left ? 0 : h; k < (left ? h : N); ++k) if (k != n) todo.push_back(k);
+  } else if (N >= 3 && n >= 2 && !in.fuse) {
     emit_ttm(1);  // stream pass over the middle mode (strided kernel), then the rest
     for (int k = 0; k < N; ++k) if (k != n && k != 1) todo.push_back(k);
   } else if (N >= 3 && n >= 2) {
-    TtmStep s{};
-    s.kind = 2;
-    s.in = src;
-    s.I1 = (int)cur[0];
-    s.I2 = (int)cur[1];
-    s.L = prod(cur, 2, N);
-    s.Q = in.Q[0];
-    s.ldq = in.ldq[0];
-    s.Q2 = in.Q[1];
-    s.ldq2 = in.ldq[1];
-    bool tma = false;
-    if (in.tma && s.I1 % 2 == 0 && s.L < (1ll << 31) && bufs[0]) {
-      const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
-      const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
-      const uint32_t box[3] = {16, (uint32_t)(kCW * 8 * slice_nf(s.I2)), 1};
-      tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
-    }
-    const bool small = tma && s.I2 <= 64 && s.I2 % 8 == 0 && NT <= 2;
-    if (small) {
-      const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
-      const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
-      const uint32_t box[3] = {16, (uint32_t)s.I2, 8};
-      if (make_tmap(&s.mx, src, 3, d, st, box)) {
-        s.kind = 8;
-        s.S = stages_for((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes, 0);
-        s.out = bufs[nb];
-        p.steps.push_back(s);
-      } else {
-        tma = false;
-      }
-    }
-    if (small && s.kind == 8) {
-      // done
-    } else if (tma) {
-      s.kind = 6;
-      const int MT = NT;
-      s.gps = slice_nf(s.I2);
-      const int BN = kCW * 8 * s.gps;
-      s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
-      s.nfb = (s.I2 + BN - 1) / BN;
-      const int64_t U = s.L * s.nfb;
-      s.G = std::min<int64_t>(U, in.sms);
-      int ns = 1;
-      for (int64_t l = 0; l < s.L; ++l) {
-        const int64_t c0 = ((l * s.nfb + 1) * s.G - 1) / U, c1 = ((l * s.nfb + s.nfb) * s.G - 1) / U;
-        ns = std::max<int>(ns, (int)(c1 - c0 + 1));
-      }
-      s.nslots = ns;
-      s.out = bufs[nb];
-      s.P = part;
-      p.part = (ns > 1) ? (size_t)s.L * ns * R * R : 0;
-      (void)MT;
-      p.steps.push_back(s);
-      if (ns > 1) {
-        TtmStep f = s;
-        f.kind = 7;
-        p.steps.push_back(f);
-      }
-    } else {
-      const int fw = slice_fw(R);
-      const int ngr = (s.I2 + fw - 1) / fw;
-      const int64_t target = (int64_t)in.sms * 2 * kWarps * 4;
-      int gps = 1;
-      if ((int64_t)ngr * s.L > target) gps = (int)std::min<int64_t>(ngr, ((int64_t)ngr * s.L + target - 1) / target);
-      s.gps = gps;
-      s.nseg = (ngr + gps - 1) / gps;
-      if (s.nseg > 1) {
-        s.out = part;
-        p.part = (size_t)s.nseg * s.L * R * R;
-      } else {
-        s.out = bufs[nb];
-      }
-      TtmStep sr = s;
-      p.steps.push_back(s);
-      if (s.nseg > 1) {
-        sr.kind = 3;  // reduce partials
-        sr.in = part;
-        sr.out = bufs[nb];
-        p.steps.push_back(sr);
-      }
-    }
-    cur[0] = R;
-    cur[1] = R;
-    p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
-    src = bufs[nb];
-    nb ^= 1;
+    emit_slice();
     for (int k = 2; k < N; ++k) if (k != n) todo.push_back(k);
   } else if (N >= 3) {
     emit_ttm(N - 1);
@@ -644,6 +698,10 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
   in.tma = c->use_tma;
   in.fuse = c->fuse_slice;
   in.sms = c->stream_sms;
+  in.tree = c->tree && !ne;
+  in.h = c->tree_h;
+  in.tree_fresh = (n == 0 || n == c->tree_h);
+  in.tbuf = c->dTree;
   in.RQ = c->RQ;
   for (int k = 0; k < c->N; ++k) {
     const double* base = ne ? c->dA[k] : c->dQ[k];
@@ -658,7 +716,7 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
 }
 
 cpqr_status build_plans(cpqr_ctx* c) {
-  size_t mb = 0, mp = 0;
+  size_t mb = 0, mp = 0, mt = 0;
   for (int n = 0; n < c->N; ++n) {
     PlanIn in{};
     fill_plan_in(c, in, n);
@@ -668,6 +726,7 @@ cpqr_status build_plans(cpqr_ctx* c) {
     plan_mode(in, tmp, nob, nullptr);
     mb = std::max(mb, tmp.max_buf);
     mp = std::max(mp, tmp.part);
+    mt = std::max(mt, tmp.tree_elems);
     // TMA slice partials: L * nslots * R^2 with nslots <= ceil(nfb*G/U)+1 <= 2 + nfb
     if (c->N >= 3 && n >= 2) {
       const int64_t L = prod(c->ldims, 2, c->N);
@@ -681,6 +740,13 @@ cpqr_status build_plans(cpqr_ctx* c) {
       if (cudaMalloc(&c->buf[i], mb * sizeof(double)) != cudaSuccess)
         return fail(c, CPQR_ENOMEM, "intermediate buffers (%zu doubles)", mb);
     c->buf_elems = mb;
+  }
+  if (mt > c->tree_alloc) {
+    if (c->dTree) cudaFree(c->dTree);
+    c->dTree = nullptr;
+    if (cudaMalloc(&c->dTree, mt * sizeof(double)) != cudaSuccess)
+      return fail(c, CPQR_ENOMEM, "dimension-tree buffer (%zu doubles)", mt);
+    c->tree_alloc = mt;
   }
   if (mp > c->part_elems) {
     if (c->dPart) cudaFree(c->dPart);
@@ -1078,14 +1144,16 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   }
   if (fork) CK(cudaEventRecord(c->evj, c->side));
   prof_mark(c, 1);
-  // line 8: Multi-TTM (first step = the stream-X pass)
+  // line 8: Multi-TTM (first step = the stream-X pass; with the dimension tree only the first mode
+  // of each half has one)
   {
+    const size_t nx = (!p.steps.empty() && p.steps[0].in == c->X) ? 1 : 0;
     Plan first;
-    first.steps.assign(p.steps.begin(), p.steps.begin() + 1);
+    first.steps.assign(p.steps.begin(), p.steps.begin() + nx);
     TRY(run_plan(c, first));
     prof_mark(c, 2);
     Plan rest;
-    rest.steps.assign(p.steps.begin() + 1, p.steps.end());
+    rest.steps.assign(p.steps.begin() + nx, p.steps.end());
     TRY(run_plan(c, rest));
     prof_mark(c, 3);
   }
@@ -1202,6 +1270,7 @@ CPQR_API void cpqr_default_options(cpqr_options* o) {
   o->world = 1;
   o->use_graph = 1;
   o->profile = 0;
+  o->mttm_tree = 0;
 }
 
 CPQR_API const char* cpqr_version(void) { return "cpqr 0.1.0 sm_100a fp64"; }
@@ -1265,6 +1334,8 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->R = R;
   c->RQ = 16 * ((R + 15) / 16);
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
+  c->tree = c->opt.mttm_tree != 0 && N >= 3 && c->variant != CPQR_NE;
+  c->tree_h = (N + 1) / 2;
   {
     const char* f = getenv("CPQR_SLICE");  // "1" / "0" force the fused slice kernel on / off
     c->fuse_slice = f ? (f[0] == '1') : (R < 24);
@@ -1389,6 +1460,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->dperm) cudaFree(c->dperm);
   if (c->dflags) cudaFree(c->dflags);
   if (c->dq0cnt) cudaFree(c->dq0cnt);
+  if (c->dTree) cudaFree(c->dTree);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1559,19 +1631,21 @@ CPQR_API cpqr_status cpqr_get_flags(cpqr_ctx* c, uint32_t* f) {
 CPQR_API cpqr_status cpqr_get_profile(cpqr_ctx* c, cpqr_profile* p, int reset) {
   if (!c || !p) return CPQR_EINVAL;
   *p = c->prof;
-  // algorithmic bytes / flops of the stream-X pass for one sweep:
-  // bytes = N * 8 * numel (X read once per mode); flops = sum over modes of the first TTM (+ the
-  // fused second contraction of k_mttm_slice)
+  // algorithmic bytes / flops of the stream-X passes of one sweep:
+  // bytes = passes * 8 * numel (X read once per pass: N passes, or 2 with the dimension tree);
+  // flops = the first TTM of each pass (+ the fused second contraction of the slice kernels)
   double fl = 0.0;
+  int passes = 0;
   for (int n = 0; n < c->N; ++n) {
     const Plan& pl = c->plans[n];
-    if (pl.steps.empty()) continue;
+    if (pl.steps.empty() || pl.steps[0].in != c->X) continue;  // passes over X only
     const TtmStep& s = pl.steps[0];
     const double R = c->R;
-    if (s.kind == 2) fl += 2.0 * c->numel * R + 2.0 * (c->numel / (double)s.I1) * R * R;
+    ++passes;
+    if (s.kind == 2 || s.kind == 6 || s.kind == 8) fl += 2.0 * c->numel * R + 2.0 * (c->numel / (double)s.I1) * R * R;
     else fl += 2.0 * c->numel * R;
   }
-  p->bytes0 = (double)c->N * 8.0 * c->numel;
+  p->bytes0 = (double)passes * 8.0 * c->numel;
   p->flops0 = fl;
   p->launches_total = c->launch_count;
   if (reset) std::memset(&c->prof, 0, sizeof c->prof);
@@ -1604,6 +1678,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   }
   PlanIn in{};
   fill_plan_in(c, in, n, tmpQ.data(), tmpQt.data());
+  in.tree_fresh = true;  // the tree buffer holds no valid half intermediate outside a sweep
   Plan p;
   plan_mode(in, p, c->buf, c->dPart);
   CK(cudaEventRecord(c->evf, c->st));

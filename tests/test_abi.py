@@ -51,3 +51,23 @@ def test_sass_is_sm100a_and_uses_dmma(lib):
     out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, check=True).stdout
     assert "sm_100a" in out
     assert "DMMA.8x8x4" in out  # FP64 tensor-core path of the Multi-TTM
+
+
+def test_options_struct_layout_matches_binding(tmp_path):
+    """The ctypes mirror of cpqr_options (and cpqr_profile) has the C header's size and offsets."""
+    import ctypes as C
+    from paper_2112_10855_b200 import cpqr
+    fields = [f[0] for f in cpqr.Options._fields_]
+    src = tmp_path / "lay.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "cpqr.h"\nint main(void){\n'
+                   + f'printf("%zu\\n", sizeof(cpqr_options));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(cpqr_options, {f}));\n' for f in fields)
+                   + 'printf("%zu\\n", sizeof(cpqr_profile));\nreturn 0;}\n')
+    exe = tmp_path / "lay"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    r = subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    vals = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert vals[0] == C.sizeof(cpqr.Options)
+    assert vals[1:1 + len(fields)] == [getattr(cpqr.Options, f).offset for f in fields]
+    assert vals[-1] == C.sizeof(cpqr.Profile)

@@ -30,16 +30,19 @@ def cp():
     return cpqr
 
 
-CASES = [(1, "QR"), (2, "QR"), (2, "NE"), (3, "QR"), (3, "SVD"), (4, "SVD"), (5, "QR")]
+CASES = [(1, "QR", False), (2, "QR", False), (2, "NE", False), (3, "QR", False), (3, "SVD", False),
+         (4, "SVD", False), (5, "QR", False),
+         # dimension-tree Multi-TTM (opt.mttm_tree): same mode updates
+         (3, "QR", True), (4, "SVD", True), (5, "QR", True)]
 
 
-@pytest.mark.parametrize("cfg,variant", CASES)
-def test_fullsize_parity(cp, cfg, variant):
+@pytest.mark.parametrize("cfg,variant,tree", CASES)
+def test_fullsize_parity(cp, cfg, variant, tree):
     import torch
     conf, Xc, truth, init = synth.make_problem(cfg)
     X = O.as_tensor(Xc)
     fit_mode = "direct" if cfg == 4 else "fast"
-    s = cp.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, fit_mode=fit_mode)
+    s = cp.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, fit_mode=fit_mode, tree=tree)
     Xd = torch.from_numpy(np.ascontiguousarray(Xc)).cuda()
     s.set_tensor(Xd)
     s.set_factors(init)

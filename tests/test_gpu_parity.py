@@ -259,3 +259,52 @@ def test_fused_slice_on_and_off(cp, dims, R, fuse, monkeypatch):
     ref = O.cp_als_qr(X, init, 2)
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
     s.close()
+
+
+@pytest.mark.parametrize("dims,R,variant,fuse", [((30, 40, 50), 5, "QR", None), ((70, 66, 34), 32, "QR", "0"),
+                                                 ((64, 48, 40), 16, "QR", "1"), ((12, 10, 9, 11), 6, "SVD", None),
+                                                 ((6, 7, 5, 6, 8), 3, "QR", None), ((300, 40, 100), 32, "QR", "0")])
+def test_dimension_tree_multittm(cp, dims, R, variant, fuse, monkeypatch):
+    """opt.mttm_tree: two passes over X per sweep, halves [0, h) / [h, N).
+    Same mode updates as Alg. 2 up to rounding: factors after one sweep <= 1e-9 and fits within
+    1e-8 of the oracle's per-mode CP-ALS-QR; Y of every mode (fresh tree plan) <= 1e-11."""
+    if fuse is not None:
+        monkeypatch.setenv("CPQR_SLICE", fuse)
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=29, eta=0.05)
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    s = cp.CPQR(dims, R, variant, tree=True)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    Qs = [O.qr_pos(a)[0] for a in init]
+    for n in range(N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_qr(X, init, 1, variant=variant)
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(3)])
+    ref = O.cp_als_qr(X, init, 4, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+
+
+def test_dimension_tree_graph_replay_matches_eager(cp):
+    """The tree buffer carries state between the modes of a sweep: CUDA-graph replay and eager
+    launches must agree bitwise."""
+    dims, R = (40, 36, 30, 28), 8
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=5, eta=0.05)
+    out = []
+    for g in (True, False):
+        s = cp.CPQR(dims, R, "QR", tree=True, use_graph=g)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        f = s.sweep(3)
+        lam, A = s.get_factors()
+        out.append((f, lam, A))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert all(np.array_equal(a, b) for a, b in zip(out[0][2], out[1][2]))
