@@ -93,6 +93,7 @@ struct cpqr_ctx {
   int RQ = 16;
   bool use_tma = true;
   bool fuse_slice = true;  // see plan_mode
+  bool pinv_ready = false; // M = pinv(R0) already launched for this mode (side stream, after K2)
   bool tree = false;       // dimension-tree Multi-TTM (opt.mttm_tree, QR/SVD, N >= 3)
   int tree_h = 0;
   double* dTree = nullptr;
@@ -772,14 +773,21 @@ void prof_mark(cpqr_ctx* c, int idx) {
 int rb_for(int R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 32); }
 
 // Ahat = W R0^{-T} (substitution) or W (R0^T)^+ (SVD) into c->dAhat, per-CTA partials in c->dred.
+// M = U S^+ V^T of R0 (QR-SVD): one-sided Jacobi, depends on R0 only
+cpqr_status launch_pinv(cpqr_ctx* c, cudaStream_t st, int* ntrunc) {
+  const int R = c->R;
+  const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
+  const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
+  k_svd_pinv<<<1, 512, smem, st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, ntrunc);
+  CKL();
+  return CPQR_OK;
+}
+
 cpqr_status launch_solve(cpqr_ctx* c, const double* W, int In, bool fit, int* ntrunc) {
   const int R = c->R, RB = rb_for(R);
   const double* Rm = c->dR0;
   if (c->variant == CPQR_SVD) {
-    const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
-    const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
-    k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, ntrunc);
-    CKL();
+    if (!c->pinv_ready || ntrunc) TRY(launch_pinv(c, c->st, ntrunc));
     Rm = c->dMpinv;
   }
   const int BT = (RB > 16) ? 64 : 128;
@@ -837,10 +845,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
     q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
     if (solve && c->variant == CPQR_SVD) {
-      const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
-      const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
-      k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
-      CKL();
+      if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
     }
     const int tb = 32 * ((mbq + 31) / 32);
     const int ld = ((tb + 15) & ~15) + 4;
@@ -907,10 +912,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
     q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
     if (solve && c->variant == CPQR_SVD) {
-      const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
-      const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
-      k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
-      CKL();
+      if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
     }
     const int tb = 32 * ((mbq + 31) / 32);
     const size_t psm = (size_t)(mbq | 1) * R * 8;
@@ -966,10 +968,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
       q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
       q.gated = gated ? 1 : 0;
       if (solve && c->variant == CPQR_SVD && !gated) {
-        const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
-        const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
-        k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
-        CKL();
+        if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
       }
       const int tl = 32 * ((mbr + 31) / 32), tr = 32 * ((nl * R + 31) / 32);
       switch (RB) {
@@ -1004,10 +1003,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
   a.Ahat = c->dAhat; a.part = c->dred; a.Aout = Aout; a.lam = c->dlam; a.flags = c->dflags;
   a.do_fit = do_fit ? 1 : 0; a.nX2 = c->dnX2; a.fit = c->dfit;
   if (solve && c->variant == CPQR_SVD) {
-    const double tau = (c->opt.svd_tau < 0) ? R * 2.220446049250313e-16 : c->opt.svd_tau;
-    const size_t smem = (size_t)(2 * R * R + 2 * R * (R + 1)) * sizeof(double);
-    k_svd_pinv<<<1, 512, smem, c->st>>>(c->dR0, R, tau, c->dMpinv, c->dflags, nullptr);
-    CKL();
+    if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
   }
   static bool attr = false;
   if (!attr) {
@@ -1139,6 +1135,10 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     cudaStream_t keep = c->side;
     if (!fork) c->side = nullptr;
     cpqr_status st = launch_kr_qr(c, n);
+    if (st == CPQR_OK && c->variant == CPQR_SVD) {  // SVD of R0 right behind its QR, off the critical path
+      st = launch_pinv(c, c->side ? c->side : c->st, nullptr);
+      c->pinv_ready = (st == CPQR_OK);
+    }
     c->side = keep;
     TRY(st);
   }
@@ -1165,7 +1165,9 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   prof_mark(c, 4);
   // lines 10-12: solve (substitution / SVD), lambda, normalise, factor QR (+ fast fit after mode N)
   const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
-  TRY(launch_tsqr(c, In, nullptr, true, c->dW, c->dQ[n], c->dQt[n], c->dRk[n], c->dA[n], fit));
+  const cpqr_status tst = launch_tsqr(c, In, nullptr, true, c->dW, c->dQ[n], c->dQt[n], c->dRk[n], c->dA[n], fit);
+  c->pinv_ready = false;
+  TRY(tst);
   prof_mark(c, 5);
   (void)last;
   return CPQR_OK;
