@@ -28,14 +28,15 @@ namespace {
 
 constexpr int kMaxN = 8;
 constexpr int kMaxR = 32;
-constexpr size_t kQSmemMax = 96 * 1024;
-constexpr int64_t kQ0MaxSlices = 64;      // k-step slices of k_q0_apply_tc (partials buffer)  // Q panel budget per CTA (2 CTAs / SM)
+constexpr size_t kQSmemMax = 96 * 1024;   // Q panel budget per CTA (2 CTAs / SM)
+constexpr int64_t kQ0MaxSlices = 64;      // k-step slices of k_q0_apply_tc (partials buffer)
 
 struct TtmStep {
   int kind;  // 0 strided, 1 fiber, 2 slice, 3 slice-reduce, 4 strided TMA, 5 fiber TMA, 6 slice TMA, 7 slice fix-up
   alignas(64) CUtensorMap mx;
   alignas(64) CUtensorMap mq;
   int S = 0, nslots = 1, nfb = 1;
+  int big = 0;  // strided TMA: stage loaded as one 4-D box (A % 16 == 0)
   int64_t G = 1;
   double* P = nullptr;
   const double* in;
@@ -286,6 +287,7 @@ struct PlanIn {
   bool ne;
   bool tma;
   bool fuse;  // fused two-mode slice kernel allowed for n >= 3
+  bool big_box = true;  // strided kernel: one 4-D TMA box per stage when A % 16 == 0
   int sms;
   bool tree = false;        // dimension-tree Multi-TTM (QR/SVD variants)
   int h = 0;                // tree split: halves [0, h) and [h, N)
@@ -317,7 +319,7 @@ bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
     if (strides_bytes[i] % 16 != 0 || strides_bytes[i] >= (1ull << 40)) return false;
   for (int i = 0; i < rank; ++i)
     if (dims[i] == 0 || dims[i] >= (1ull << 31)) return false;
-  cuuint32_t es[3] = {1, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void*>(base),
                    (const cuuint64_t*)dims, (const cuuint64_t*)strides_bytes, (const cuuint32_t*)box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -396,6 +398,18 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         if (make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, k, s.I)) {
           s.kind = 4;
           s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0);
+          // A % 16 == 0: view a = 16 a_hi + a_lo and load a stage as ONE 32 KB box
+          // {a_lo 16, i 16, a_hi 16} (strides 8 B, A*8, 128 B) -- same shared-memory layout
+          if (s.A % 16 == 0 && in.big_box) {
+            CUtensorMap m4;
+            const uint64_t d4[4] = {16, (uint64_t)s.I, (uint64_t)(s.A / 16), (uint64_t)s.B};
+            const uint64_t st4[3] = {(uint64_t)s.A * 8, 128, (uint64_t)s.A * s.I * 8};
+            const uint32_t box4[4] = {16, 16, 16, 1};
+            if (make_tmap(&m4, src, 4, d4, st4, box4)) {
+              s.mx = m4;
+              s.big = 1;
+            }
+          }
         }
       }
     }
@@ -605,7 +619,7 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
 #define STR(NTV)                                                                                     \
   {                                                                                                  \
     set_smem(k_strided_tma<NTV>, smem);                                                              \
-    k_strided_tma<NTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S);   \
+    k_strided_tma<NTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S, s.big); \
   }
     switch (NT) { case 1: STR(1) break; case 2: STR(2) break; case 3: STR(3) break; default: STR(4) break; }
 #undef STR
@@ -698,6 +712,7 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
   in.ne = ne;
   in.tma = c->use_tma;
   in.fuse = c->fuse_slice;
+  in.big_box = !(getenv("CPQR_BIG_BOX") && atoi(getenv("CPQR_BIG_BOX")) == 0);
   in.sms = c->stream_sms;
   in.tree = c->tree && !ne;
   in.h = c->tree_h;
