@@ -176,13 +176,19 @@ def main():
     rank, local, world = dist_env()
     torch.cuda.set_device(local)
     from paper_2112_10855_b200 import cpqr
-    nccl_id = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
+
+    def new_nccl_id():
+        """A fresh ncclUniqueId for every context (one NCCL communicator each), broadcast from
+        rank 0 over the gloo group; all ranks create contexts in the same order."""
+        if world == 1:
+            return None
+        import torch.distributed as dist
         obj = [cpqr.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
     conf = synth.CONFIGS[args.config]
     variant = args.variant or conf.variants[0]
     conf, Xc, slab, truth, init, _ = load_input(conf, rank, world)
@@ -201,7 +207,7 @@ def main():
         """W warm-up sweeps (CUDA-graph capture), then exactly K sweeps between CUDA events on
         the library's stream, barrier + synchronize on both sides, max over ranks."""
         s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                      rank=rank, world=world, nccl_id=nccl_id, tree=use_tree)
+                      rank=rank, world=world, nccl_id=new_nccl_id(), tree=use_tree)
         s.set_tensor(Xd)                     # device-resident input (borrowed)
         s.set_factors(init)
         s.sweep(args.warmup)
@@ -235,7 +241,7 @@ def main():
 
     # phase profile (separate short run; events around each phase on the library stream)
     sp = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                   rank=rank, world=world, nccl_id=nccl_id, profile=True, use_graph=False,
+                   rank=rank, world=world, nccl_id=None, profile=True, use_graph=False,
                    tree=tree) if world == 1 else None
     prof = None
     if sp is not None:
@@ -255,7 +261,7 @@ def main():
     if not args.no_e2e:
         Xh = torch.from_numpy(np.ascontiguousarray(slab)).pin_memory()
         se = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                       rank=rank, world=world, nccl_id=nccl_id, tree=tree)
+                       rank=rank, world=world, nccl_id=new_nccl_id(), tree=tree)
         se.set_tensor(Xh)
         se.set_factors(init)
         se.sweep(1)

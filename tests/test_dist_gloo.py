@@ -90,3 +90,63 @@ def test_slab_bounds_match_library_convention():
         spans = [(q * per, (q + 1) * per) for q in range(world)]
         assert spans[0][0] == 0 and spans[-1][1] == IN
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _tree_worker(rank, world, port, dims, R, results):
+    """Dimension-tree Multi-TTM over slabs: T_L = X_slab x_{k>=h} Q_k^T (Q_N's slab rows) is a
+    rank-partial of the left-half intermediate, so W_n (n < h) all-reduces as in the per-mode
+    schedule; T_R = X_slab x_{k<h} Q_k^T keeps the slab's i_N, so modes h..N-2 all-reduce and mode
+    N all-gathers rows.  Checked against the full-tensor per-mode W of every mode."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2112_10855_b200 import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        conf, Xc, truth, init = synth.small_problem(dims, R, seed=43, eta=0.05)
+        N = len(dims)
+        h = (N + 1) // 2
+        per = dims[-1] // world
+        b, e = rank * per, (rank + 1) * per
+        Xfull = O.as_tensor(Xc)
+        Xslab = O.as_tensor(np.ascontiguousarray(Xc[b:e]))
+        Qs = [O.qr_pos(a)[0] for a in init]
+        Rs = [O.qr_pos(a)[1] for a in init]
+
+        def slabQ(k):
+            return Qs[k][b:e] if k == N - 1 else Qs[k]
+        TL = O.multi_ttm(Xslab, {k: slabQ(k).T for k in range(h, N)})
+        TR = O.multi_ttm(Xslab, {k: Qs[k].T for k in range(h)})
+        ok = True
+        for n in range(N):
+            Q0, R0 = O.structured_qr(Rs, n)
+            if n < h:
+                Yp = O.multi_ttm(TL, {k: Qs[k].T for k in range(h) if k != n})
+            else:
+                Yp = O.multi_ttm(TR, {k: slabQ(k).T for k in range(h, N) if k != n})
+            Wp = O.apply_q0(Yp, n, Q0)
+            if n < N - 1:
+                t = torch.from_numpy(np.ascontiguousarray(Wp))
+                dist.all_reduce(t)
+                W = t.numpy()
+            else:
+                parts = [torch.zeros(per, R, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(Wp)))
+                W = torch.cat(parts).numpy()
+            Wref = O.apply_q0(O.multi_ttm(Xfull, {k: Qs[k].T for k in range(N) if k != n}), n, Q0)
+            ok = ok and np.linalg.norm(W - Wref) <= 1e-13 * np.linalg.norm(Wref)
+        results[rank] = bool(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims,R", [((12, 10, 8), 4), ((6, 5, 7, 8), 3), ((5, 4, 6, 3, 4), 2)])
+def test_dimension_tree_slab_decomposition_world2(dims, R):
+    world = 2
+    port = 30500 + (sum(dims) * 11 + R) % 1000
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_tree_worker, args=(world, port, dims, R, results), nprocs=world, join=True)
+    assert results.get(0) and results.get(1), dict(results)
