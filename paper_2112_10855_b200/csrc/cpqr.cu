@@ -694,7 +694,7 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
     a.out = d.out;
     int64_t tot = 1;
     for (int i = 0; i < d.nd; ++i) if (i != d.k) tot *= d.dims[i];
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)c->sms * 16));
+    const int grid = (int)std::max<int64_t>(1, (tot + 31) / 32);
     k_diag_contract<<<grid, 256, 0, c->st>>>(a);
     CKL();
   }
@@ -1131,7 +1131,16 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     a.nX2 = c->dnX2;
     a.fit = c->dfit;
     a.Ahat = c->dAhat;
-    k_tail_ne<<<1, 512, 2 * c->R * c->R * sizeof(double), c->st>>>(a);
+    {
+      a.force_lu = getenv("CPQR_NE_FORCE_LU") ? 1 : 0;
+      const int RB = rb_for(c->R);
+      const size_t smem = (size_t)(3 * RB * RB + kNeLd * RB) * sizeof(double);
+      switch (RB) {
+        case 8: set_smem(k_tail_ne<8>, smem); k_tail_ne<8><<<1, kNeThreads, smem, c->st>>>(a); break;
+        case 16: set_smem(k_tail_ne<16>, smem); k_tail_ne<16><<<1, kNeThreads, smem, c->st>>>(a); break;
+        default: set_smem(k_tail_ne<32>, smem); k_tail_ne<32><<<1, kNeThreads, smem, c->st>>>(a); break;
+      }
+    }
     CKL();
     k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[n], c->dims[n], In, c->R, c->RQ, c->dAt[n]);
     CKL();

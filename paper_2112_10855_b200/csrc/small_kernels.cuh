@@ -14,6 +14,7 @@
 // All reductions are fixed-order (no floating-point atomics): results are bitwise reproducible.
 #pragma once
 #include "common.cuh"
+#include "rowsolve.cuh"
 
 namespace cpqr {
 
@@ -569,13 +570,21 @@ struct DiagArgs {
   int64_t lda;
   double* out;  // dims without mode k, column-major
 };
-__global__ void k_diag_contract(DiagArgs a) {
+// out(o) = sum_i T(.., i at dim k, ..) A_k(i, r(o)): 32 consecutive outputs per CTA on the lanes
+// (coalesced along the fastest remaining dimension), the i range split over the 8 warps and the
+// warp partials summed in warp order (fixed order, deterministic).  A CTA per 32 outputs keeps
+// enough warps in flight when there are few outputs (C2: 4000 outputs, I_k = 400).
+__global__ void __launch_bounds__(256) k_diag_contract(DiagArgs a) {
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int64_t tot = 1;
   for (int d = 0; d < a.nd; ++d) if (d != a.k) tot *= a.dims[d];
   int64_t stride_k = 1;
   for (int d = 0; d < a.k; ++d) stride_k *= a.dims[d];
   const int64_t Ik = a.dims[a.k];
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < tot; o += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t o = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (o < tot) {
     int64_t rem = o, base = 0, st = 1;
     int r = 0;
     for (int d = 0; d < a.nd; ++d) {
@@ -586,9 +595,26 @@ __global__ void k_diag_contract(DiagArgs a) {
       if (d == a.rm) r = (int)id;
       st *= a.dims[d];
     }
-    double s = 0.0;
-    for (int64_t i = 0; i < Ik; ++i) s = fma(a.T[base + i * stride_k], a.Ak[i + a.lda * r], s);
-    a.out[o] = s;
+    const int64_t chunk = (Ik + 7) / 8, i0 = w * chunk, i1 = min(Ik, i0 + chunk);
+    const double* Tp = a.T + base;
+    const double* Ap = a.Ak + a.lda * r;
+    double s1 = 0.0;
+    int64_t i = i0;
+#pragma unroll 2
+    for (; i + 1 < i1; i += 2) {
+      s = fma(Tp[i * stride_k], __ldg(Ap + i), s);
+      s1 = fma(Tp[(i + 1) * stride_k], __ldg(Ap + i + 1), s1);
+    }
+    if (i < i1) s = fma(Tp[i * stride_k], __ldg(Ap + i), s);
+    s += s1;
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && o < tot) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += part[q][lane];
+    a.out[o] = v;
   }
 }
 
@@ -607,39 +633,52 @@ struct TailNeArgs {
   const double* nX2;
   double* fit;
   double* Ahat;           // scratch In x R column-major
+  int force_lu;           // testing: take the LU path even when S is positive definite
 };
-__global__ void __launch_bounds__(512) k_tail_ne(TailNeArgs a) {
+// One CTA of kNeThreads threads; RB = 8/16/32 >= R.  Rows of M are solved kNeThreads at a time on
+// a shared-memory row panel with the blocked register solves of cholqr.cuh:
+// x S = m, S = L L^T  <=>  y U = m (forward, U = L^T) then x U^T = y (backward).
+constexpr int kNeThreads = 256;
+constexpr int kNeLd = kNeThreads + 4;
+template <int RB>
+__global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
   extern __shared__ double smne[];
-  double* S = smne;                 // R x R
-  double* L = smne + a.R * a.R;     // R x R
-  __shared__ double red[32], lam[64];
-  __shared__ int piv[64];
+  double* S = smne;            // RB x RB, zero padded
+  double* L = S + RB * RB;     // Cholesky factor (lower) or packed LU, ld RB
+  double* U = L + RB * RB;     // L^T, zero padded
+  double* P = U + RB * RB;     // row panel, ld kNeLd
+  __shared__ double red[32], lam[RB], invd[RB];
+  __shared__ int piv[RB];
   __shared__ int use_lu;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   const int R = a.R, In = a.In;
-  for (int e = tid; e < R * R; e += nt) {
-    double v = 1.0;
-    for (int k = a.N - 1; k >= 0; --k)
-      if (k != a.n) v *= a.G[k][e];
+  for (int e = tid; e < RB * RB; e += nt) {
+    const int r = e % RB, c = e / RB;
+    double v = 0.0;
+    if (r < R && c < R) {
+      v = 1.0;
+      for (int k = a.N - 1; k >= 0; --k)
+        if (k != a.n) v *= a.G[k][r + R * c];
+    }
     S[e] = v;
     L[e] = v;
   }
-  if (tid == 0) use_lu = 0;
+  if (tid == 0) use_lu = a.force_lu;
   __syncthreads();
   // Cholesky S = L L^T (lower, column-major in L), by warp 0
-  if (wid == 0) {
+  if (wid == 0 && !use_lu) {
     for (int j = 0; j < R; ++j) {
-      double d = L[j + R * j];
-      for (int k = 0; k < j; ++k) d -= L[j + R * k] * L[j + R * k];
+      double d = L[j + RB * j];
+      for (int k = 0; k < j; ++k) d -= L[j + RB * k] * L[j + RB * k];
       if (!(d > 0.0)) { if (lane == 0) use_lu = 1; break; }
       d = sqrt(d);
       for (int i = j + 1 + lane; i < R; i += 32) {
-        double v = L[i + R * j];
-        for (int k = 0; k < j; ++k) v -= L[i + R * k] * L[j + R * k];
-        L[i + R * j] = v / d;
+        double v = L[i + RB * j];
+        for (int k = 0; k < j; ++k) v -= L[i + RB * k] * L[j + RB * k];
+        L[i + RB * j] = v / d;
       }
       __syncwarp();
-      if (lane == 0) L[j + R * j] = d;
+      if (lane == 0) L[j + RB * j] = d;
       __syncwarp();
     }
   }
@@ -647,33 +686,56 @@ __global__ void __launch_bounds__(512) k_tail_ne(TailNeArgs a) {
   if (use_lu) {
     if (tid == 0) {
       atomicOr(a.flags, FLAG_NE_CHOL_FALLBACK);
-      for (int e = 0; e < R * R; ++e) L[e] = S[e];
+      for (int e = 0; e < RB * RB; ++e) L[e] = S[e];
       for (int j = 0; j < R; ++j) {  // LU with partial pivoting, L and U packed in L
         int p = j;
-        for (int i = j + 1; i < R; ++i) if (fabs(L[i + R * j]) > fabs(L[p + R * j])) p = i;
+        for (int i = j + 1; i < R; ++i) if (fabs(L[i + RB * j]) > fabs(L[p + RB * j])) p = i;
         piv[j] = p;
-        if (p != j) for (int c = 0; c < R; ++c) { double t = L[j + R * c]; L[j + R * c] = L[p + R * c]; L[p + R * c] = t; }
+        if (p != j) for (int c = 0; c < R; ++c) { double t = L[j + RB * c]; L[j + RB * c] = L[p + RB * c]; L[p + RB * c] = t; }
         for (int i = j + 1; i < R; ++i) {
-          L[i + R * j] /= L[j + R * j];
-          for (int c = j + 1; c < R; ++c) L[i + R * c] -= L[i + R * j] * L[j + R * c];
+          L[i + RB * j] /= L[j + RB * j];
+          for (int c = j + 1; c < R; ++c) L[i + RB * c] -= L[i + RB * j] * L[j + RB * c];
         }
       }
     }
-    __syncthreads();
-  }
-  // rows: solve S x = m (S symmetric, so Ahat(i,:) S = M(i,:) <=> S Ahat(i,:)^T = M(i,:)^T)
-  for (int i = tid; i < In; i += nt) {
-    double x[64];
-    for (int c = 0; c < R; ++c) x[c] = a.m_rowmajor ? a.M[(int64_t)i * R + c] : a.M[i + (int64_t)In * c];
-    if (!use_lu) {
-      for (int j = 0; j < R; ++j) { double v = x[j]; for (int k = 0; k < j; ++k) v -= L[j + R * k] * x[k]; x[j] = v / L[j + R * j]; }
-      for (int j = R - 1; j >= 0; --j) { double v = x[j]; for (int k = j + 1; k < R; ++k) v -= L[k + R * j] * x[k]; x[j] = v / L[j + R * j]; }
-    } else {
-      for (int j = 0; j < R; ++j) { const int p = piv[j]; if (p != j) { double t = x[j]; x[j] = x[p]; x[p] = t; } }
-      for (int j = 0; j < R; ++j) { double v = x[j]; for (int k = 0; k < j; ++k) v -= L[j + R * k] * x[k]; x[j] = v; }
-      for (int j = R - 1; j >= 0; --j) { double v = x[j]; for (int k = j + 1; k < R; ++k) v -= L[j + R * k] * x[k]; x[j] = v / L[j + R * j]; }
+  } else {
+    for (int e = tid; e < RB * RB; e += nt) {  // U = L^T (upper), invd = 1 / L_jj
+      const int r = e % RB, c = e / RB;
+      U[e] = (r <= c && c < R) ? L[c + RB * r] : 0.0;
     }
-    for (int c = 0; c < R; ++c) a.Ahat[i + (int64_t)In * c] = x[c];
+    if (tid < RB) invd[tid] = (tid < R) ? 1.0 / L[tid + RB * tid] : 0.0;
+  }
+  __syncthreads();
+  // rows: Ahat(i,:) S = M(i,:)  (S symmetric)
+  double* row = P + tid;
+  for (int i0 = 0; i0 < In; i0 += nt) {
+    const int i = i0 + tid;
+    const bool own = i < In;
+#pragma unroll 4
+    for (int c = 0; c < RB; ++c)
+      row[kNeLd * c] = (own && c < R) ? (a.m_rowmajor ? a.M[(int64_t)i * R + c] : a.M[i + (int64_t)In * c]) : 0.0;
+    if (!use_lu) {
+      cq_row_trsv<RB, false>(row, kNeLd, U, invd);  // y U = m
+      cq_row_trsv<RB, true>(row, kNeLd, U, invd);   // x U^T = y
+    } else {
+      for (int j = 0; j < R; ++j) {
+        const int p = piv[j];
+        if (p != j) { const double t = row[kNeLd * j]; row[kNeLd * j] = row[kNeLd * p]; row[kNeLd * p] = t; }
+      }
+      for (int j = 0; j < R; ++j) {
+        double v = row[kNeLd * j];
+        for (int k = 0; k < j; ++k) v -= L[j + RB * k] * row[kNeLd * k];
+        row[kNeLd * j] = v;
+      }
+      for (int j = R - 1; j >= 0; --j) {
+        double v = row[kNeLd * j];
+        for (int k = j + 1; k < R; ++k) v -= L[j + RB * k] * row[kNeLd * k];
+        row[kNeLd * j] = v / L[j + RB * j];
+      }
+    }
+    if (own)
+#pragma unroll 4
+      for (int c = 0; c < R; ++c) a.Ahat[i + (int64_t)In * c] = row[kNeLd * c];
   }
   __syncthreads();
   for (int c = wid; c < R; c += nw) {
@@ -712,7 +774,7 @@ __global__ void __launch_bounds__(512) k_tail_ne(TailNeArgs a) {
     }
     const double inner = block_sum(s, red);
     double q = 0.0;  // <S_N, diag(lam) G_N diag(lam)>
-    for (int e = tid; e < R * R; e += nt) q += S[e] * lam[e % R] * lam[e / R] * a.Gn[e];
+    for (int e = tid; e < R * R; e += nt) q += S[(e % R) + RB * (e / R)] * lam[e % R] * lam[e / R] * a.Gn[e];
     const double nxh2 = block_sum(q, red);
     if (tid == 0) {
       const double nx2 = *a.nX2;

@@ -308,3 +308,29 @@ def test_dimension_tree_graph_replay_matches_eager(cp):
         s.close()
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert all(np.array_equal(a, b) for a, b in zip(out[0][2], out[1][2]))
+
+
+@pytest.mark.parametrize("dims,R,force_lu", [((40, 36, 30), 10, False), ((44, 41, 38), 20, False),
+                                              ((12, 10, 9, 11), 6, False), ((40, 36, 30), 10, True)])
+def test_ne_variant_tail(cp, dims, R, force_lu, monkeypatch):
+    """Normal-equations CP-ALS (Alg. 1) at RB = 16 / 32 and N = 4 (blocked row solves
+    y L^T = m, x L = y on the row panel), and the LU-with-partial-pivoting path (reading 18) forced
+    on a positive-definite S: fits within 1e-8, factors after one sweep <= 1e-9 of the oracle."""
+    if force_lu:
+        monkeypatch.setenv("CPQR_NE_FORCE_LU", "1")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=61, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "NE")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_ne(X, init, 1)
+    for k in range(len(dims)):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(3)])
+    ref = O.cp_als_ne(X, init, 4)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    if force_lu:
+        assert s.flags & 2  # NE_CHOL_FALLBACK reported
+    s.close()
