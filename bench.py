@@ -241,8 +241,7 @@ def main():
 
     # phase profile (separate short run; events around each phase on the library stream)
     sp = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                   rank=rank, world=world, nccl_id=None, profile=True, use_graph=False,
-                   tree=tree) if world == 1 else None
+                   rank=rank, world=world, nccl_id=new_nccl_id(), profile=True, use_graph=False, tree=tree)
     prof = None
     if sp is not None:
         sp.set_tensor(Xd)

@@ -364,273 +364,6 @@ __device__ __forceinline__ void cq_gram_dmma(const double* P, int ld, int rows4,
     }
 }
 
-// Right-looking Cholesky G = L L^T by warp 0 (lane i = row i, R <= RB <= 32), rows in registers.
-// Writes Rt = L^T (upper, RB x RB, ld RB) and invd[j] = 1 / L_jj.  Returns ok (pivots > 0) and
-// the ratio max L_jj / min L_jj through *ratio.
-template <int RB>
-__device__ __noinline__ bool cq_chol_warp(const double* G, int R, double* Rt, double* invd, double* ratio) {
-  const int lane = threadIdx.x & 31;
-  double gr[RB];
-#pragma unroll
-  for (int k = 0; k < RB; ++k) gr[k] = (lane < R && k < R) ? G[lane + RB * k] : 0.0;
-  bool ok = true;
-  double dmax = 0.0, dmin = 1e308;
-#pragma unroll
-  for (int j = 0; j < RB; ++j) {
-    if (j >= R) break;
-    const double piv = __shfl_sync(0xffffffffu, gr[j], j);
-    if (!(piv > 0.0)) ok = false;
-    const double ljj = sqrt(fmax(piv, 0.0));
-    const double inv = (ljj > 0.0) ? 1.0 / ljj : 0.0;
-    dmax = fmax(dmax, ljj);
-    dmin = fmin(dmin, ljj);
-    const double lij = (lane == j) ? ljj : ((lane > j && lane < R) ? gr[j] * inv : 0.0);
-    gr[j] = lij;  // lane i now keeps L(i, j) in gr[j]
-#pragma unroll
-    for (int k = j + 1; k < RB; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, lij, k);
-      if (lane > j) gr[k] = fma(-lij, lkj, gr[k]);
-    }
-    if (lane == 0) invd[j] = inv;
-  }
-  if (lane < RB)
-#pragma unroll
-    for (int j = 0; j < RB; ++j) Rt[j + RB * lane] = (j <= lane && j < R && lane < R) ? gr[j] : 0.0;  // R(j, lane) = L(lane, j)
-  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;
-  return ok;
-}
-
-// Ui = Ru^{-1} (Ru upper triangular RB x RB in shared memory, inverse diagonal in invd) by warp 0:
-// lane c back-substitutes column c in registers (fully unrolled, no divisions).
-template <int RB>
-__device__ __noinline__ void cq_tri_inv_warp(const double* Ru, const double* invd, int R, double* Ui) {
-  const int c = threadIdx.x & 31;
-  double u[RB];
-#pragma unroll
-  for (int r = RB - 1; r >= 0; --r) {
-    double acc = (r == c) ? 1.0 : 0.0;
-#pragma unroll
-    for (int l = r + 1; l < RB; ++l) acc = fma(-Ru[r + RB * l], u[l], acc);
-    u[r] = (r <= c && r < R && c < R) ? acc * invd[r] : 0.0;
-  }
-  if (c < RB)
-#pragma unroll
-    for (int r = 0; r < RB; ++r) Ui[r + RB * c] = u[r];
-}
-
-template <int RB>
-__global__ void __launch_bounds__(256) k_cq_fused(CqArgs a) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  // dynamic shared memory: [7 x RB*RB matrices][panel ld x RB], ld = roundup(rows, 16) + 4
-  extern __shared__ double smq[];
-  double* G1b = smq;
-  double* G2b = G1b + RB * RB;
-  double* Gs = G2b + RB * RB;
-  double* R1s = Gs + RB * RB;
-  double* R2s = R1s + RB * RB;
-  double* Ms = R2s + RB * RB;
-  double* R0s = Ms + RB * RB;
-  double* P = R0s + RB * RB;
-  __shared__ double inv1[RB], inv2[RB], lam[RB], redi[8], innerb;
-  __shared__ int okf;
-  const int nb = a.nb, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int b = (int)cluster.block_rank();
-  const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
-  const int rows4 = (rows + 3) & ~3, ld = (((int)blockDim.x + 15) & ~15) + 4;  // >= every thread's row
-  const int i = r0 + tid;
-  const bool own = tid < rows;
-  if (tid == 0 && b == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);
-  // ---- 1. rows of the panel: A, or Ahat solved from W (PAPER.md:358 / 339)
-  double x[RB];
-  double inner = 0.0;
-  if (!a.solve) {
-#pragma unroll
-    for (int k = 0; k < RB; ++k) x[k] = (own && k < R) ? a.A[i + (int64_t)a.m * k] : 0.0;
-  } else {
-    for (int e = tid; e < RB * RB; e += blockDim.x) {
-      const int r = e % RB, c = e / RB;
-      Ms[e] = (r < R && c < R) ? a.Rm[r + R * c] : 0.0;
-      R0s[e] = (r < R && c < R) ? a.R0[r + R * c] : 0.0;
-    }
-    __syncthreads();
-    double wv[RB];
-#pragma unroll
-    for (int k = 0; k < RB; ++k) wv[k] = (own && k < R) ? a.W[(int64_t)i * R + k] : 0.0;
-    if (a.variant == 2) {
-#pragma unroll
-      for (int c = 0; c < RB; ++c) {
-        double s = 0.0;
-#pragma unroll
-        for (int r = 0; r < RB; ++r) s = fma(wv[r], Ms[r + RB * c], s);
-        x[c] = s;
-      }
-    } else {
-#pragma unroll
-      for (int j = RB - 1; j >= 0; --j) {
-        double acc = wv[j];
-#pragma unroll
-        for (int l = j + 1; l < RB; ++l) acc = fma(-x[l], Ms[j + RB * l], acc);
-        x[j] = (j < R) ? acc / Ms[j + RB * j] : 0.0;
-      }
-    }
-    if (a.do_fit) {
-#pragma unroll
-      for (int c = 0; c < RB; ++c) {
-        double tt = 0.0;
-#pragma unroll
-        for (int l = c; l < RB; ++l) tt = fma(x[l], R0s[c + RB * l], tt);
-        inner = fma(wv[c], tt, inner);
-      }
-    }
-    if (own)
-#pragma unroll
-      for (int k = 0; k < RB; ++k)
-        if (k < R) a.Ahat[i + (int64_t)a.m * k] = x[k];
-  }
-  inner = warp_sum(inner);
-  if (lane == 0) redi[wid] = inner;
-  for (int e = tid; e < ld * RB; e += blockDim.x) P[e] = 0.0;
-  __syncthreads();
-  if (own)
-#pragma unroll
-    for (int k = 0; k < RB; ++k) P[tid + ld * k] = x[k];
-  if (tid == 0) {
-    double v = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) v += redi[q];
-    innerb = v;
-  }
-  __syncthreads();
-  // ---- 2. block Gram, cluster sum (every CTA, same order), Cholesky -> R1
-  cq_gram_dmma<RB>(P, ld, rows4, G1b);
-  cluster.sync();
-  for (int e = tid; e < RB * RB; e += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G1b, c)[e];
-    Gs[e] = s;
-  }
-  double inner_all = 0.0;
-  for (int c = 0; c < nb; ++c) inner_all += *cluster.map_shared_rank(&innerb, c);
-  __syncthreads();
-  if (wid == 0) {
-    double ratio;
-    const bool ok = cq_chol_warp<RB>(Gs, R, R1s, inv1, &ratio);
-    if (lane == 0) okf = ok && ratio < kCqKappaMax;
-  }
-  if (a.solve && tid < R) lam[tid] = sqrt(Gs[tid + RB * tid]);  // lambda_c = ||Ahat(:,c)||_2
-  __syncthreads();
-  if (!okf) {
-    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
-    cluster.sync();  // peers may still read this CTA's shared memory
-    return;
-  }
-  // ---- 3. Q1 rows: y R1 = x (forward substitution), Gram of Q1, Cholesky -> R2
-  double y[RB];
-#pragma unroll
-  for (int j = 0; j < RB; ++j) {
-    double acc = x[j];
-#pragma unroll
-    for (int l = 0; l < j; ++l) acc = fma(-y[l], R1s[l + RB * j], acc);
-    y[j] = (j < R) ? acc * inv1[j] : 0.0;
-  }
-  __syncthreads();
-  if (own)
-#pragma unroll
-    for (int k = 0; k < RB; ++k) P[tid + ld * k] = y[k];
-  __syncthreads();
-  cq_gram_dmma<RB>(P, ld, rows4, G2b);
-  cluster.sync();
-  for (int e = tid; e < RB * RB; e += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nb; ++c) s += cluster.map_shared_rank(G2b, c)[e];
-    Gs[e] = s;
-  }
-  __syncthreads();
-  if (wid == 0) {
-    double ratio;
-    const bool ok = cq_chol_warp<RB>(Gs, R, R2s, inv2, &ratio);
-    double e = 0.0;  // ||G2 - I||_max must be O(kappa^2 eps)
-    for (int q = lane; q < R * R; q += 32) {
-      const int r = q % R, c = q / R;
-      e = fmax(e, fabs(Gs[r + RB * c] - (r == c ? 1.0 : 0.0)));
-    }
-    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
-    if (lane == 0) okf = ok && (e < 1.0e-4);
-  }
-  __syncthreads();
-  if (!okf) {
-    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
-    cluster.sync();
-    return;
-  }
-  // ---- 4. Q = Q1 R2^{-1}; A_n = Ahat / lambda; R_n = R2 R1 diag(1/lambda); fit
-  double q[RB];
-#pragma unroll
-  for (int j = 0; j < RB; ++j) {
-    double acc = y[j];
-#pragma unroll
-    for (int l = 0; l < j; ++l) acc = fma(-q[l], R2s[l + RB * j], acc);
-    q[j] = (j < R) ? acc * inv2[j] : 0.0;
-  }
-  if (own) {
-#pragma unroll
-    for (int k = 0; k < RB; ++k)
-      if (k < R) a.Q[i + (int64_t)a.m * k] = q[k];
-    for (int k = 0; k < a.RQ; ++k) {
-      double v = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < RB; ++kk) v = (kk == k && kk < R) ? q[kk] : v;
-      a.Qt[(int64_t)i * a.RQ + k] = v;
-    }
-    if (a.solve)
-#pragma unroll
-      for (int k = 0; k < RB; ++k) {
-        if (k >= R) continue;
-        const double l = lam[k];
-        a.Aout[i + (int64_t)a.m * k] = (l > 0.0) ? x[k] / l : (i == 0 ? 1.0 : 0.0);
-      }
-  }
-  if (b == 0) {
-    for (int e = tid; e < RB * RB; e += blockDim.x) {
-      const int r = e % RB, c = e / RB;
-      double s = 0.0;
-      for (int k = r; k <= c; ++k) s = fma(R2s[r + RB * k], R1s[k + RB * c], s);
-      if (a.solve && c < R && lam[c] > 0.0) s /= lam[c];
-      s = (r <= c && r < R && c < R) ? s : 0.0;
-      Gs[e] = s;  // R_n
-      if (r < R && c < R) a.Rn[r + R * c] = s;
-    }
-    if (a.solve && tid < R) {
-      a.lam[tid] = lam[tid];
-      if (!isfinite(lam[tid])) atomicOr(a.flags, FLAG_NONFINITE);
-    }
-    if (a.do_fit) {
-      __syncthreads();
-      double qq = 0.0;
-      for (int e = tid; e < R * R; e += blockDim.x) {
-        const int xx = e % R, yy = e / R;
-        double g0 = 0.0, g1 = 0.0;
-        for (int k = 0; k <= min(xx, yy); ++k) {
-          g0 = fma(R0s[k + RB * xx], R0s[k + RB * yy], g0);
-          g1 = fma(Gs[k + RB * xx], Gs[k + RB * yy], g1);
-        }
-        qq = fma(g0, lam[xx] * lam[yy] * g1, qq);
-      }
-      qq = warp_sum(qq);
-      if (lane == 0) redi[wid] = qq;
-      __syncthreads();
-      if (tid == 0) {
-        double nxh2 = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) nxh2 += redi[w];
-        const double nx2 = *a.nX2;
-        *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner_all + nxh2)) / sqrt(nx2);
-      }
-    }
-  }
-  cluster.sync();  // no CTA leaves while peers may read its shared memory
-}
-
-
 // ----------------------------------------------------------------- compact (I-cache friendly) variant
 // Same algorithm as k_cq_fused, but every per-row quantity lives in a shared-memory panel row
 // (owner thread tid, stride 1 across threads -> conflict free) and all loops are rolled: the
@@ -638,136 +371,6 @@ __global__ void __launch_bounds__(256) k_cq_fused(CqArgs a) {
 // cache.  Q1 = A R1^{-1} and Q = Q1 R2^{-1} use the explicit upper-triangular inverses (column-
 // parallel back substitution by R threads), turning the per-row solves into independent dot
 // products; the paper's own solve Ahat R0^T = W keeps row-wise substitution.
-
-// Cholesky of Gs (RB x RB) in place by warp 0: lower part becomes L; writes Ru = L^T (upper,
-// R x R in RB x RB), returns ok and max/min pivot ratio.
-__device__ bool cq_chol_smem(double* Gs, int R, int RB, double* Ru, double* ratio) {
-  const int lane = threadIdx.x & 31;
-  bool ok = true;
-  double dmax = 0.0, dmin = 1e308;
-  #pragma unroll 1
-  for (int j = 0; j < R; ++j) {
-    const double piv = Gs[j + RB * j];
-    if (!(piv > 0.0)) ok = false;
-    const double ljj = sqrt(fmax(piv, 0.0));
-    const double inv = (ljj > 0.0) ? 1.0 / ljj : 0.0;
-    dmax = fmax(dmax, ljj);
-    dmin = fmin(dmin, ljj);
-    const int i = lane;
-    double lij = 0.0;
-    if (i > j && i < R) { lij = Gs[i + RB * j] * inv; Gs[i + RB * j] = lij; }
-    __syncwarp();
-    if (i > j && i < R)
-      #pragma unroll 1
-      for (int k = j + 1; k <= i; ++k) Gs[i + RB * k] = fma(-lij, Gs[k + RB * j], Gs[i + RB * k]);
-    __syncwarp();
-    if (lane == 0) Gs[j + RB * j] = ljj;
-    __syncwarp();
-  }
-  #pragma unroll 1
-  for (int e = lane; e < RB * RB; e += 32) {
-    const int r = e % RB, c = e / RB;  // Ru(r, c) = L(c, r)
-    Ru[e] = (r <= c && c < R) ? Gs[c + RB * r] : 0.0;
-  }
-  __syncwarp();
-  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;
-  return ok;
-}
-
-// Ui = Ru^{-1} (upper triangular), column c by thread c (back substitution Ru Ui(:,c) = e_c).
-__device__ void cq_tri_inv(const double* Ru, int R, int RB, double* Ui) {
-  const int c = threadIdx.x;
-  if (c < RB)
-    #pragma unroll 1
-    for (int r = RB - 1; r >= 0; --r) {
-      double v = 0.0;
-      if (c < R && r <= c) {
-        double acc = (r == c) ? 1.0 : 0.0;
-        #pragma unroll 1
-        for (int l = r + 1; l <= c; ++l) acc = fma(-Ru[r + RB * l], Ui[l + RB * c], acc);
-        v = acc / Ru[r + RB * r];
-      }
-      Ui[r + RB * c] = v;
-    }
-}
-
-// Row-panel product Y[tid, :] = X[tid, :] U for the owned row (U upper triangular RB x RB).
-__device__ __forceinline__ void cq_row_times_upper(const double* X, double* Y, int ld, int tid, int R, int RB,
-                                                   const double* U) {
-  double xr[32];
-#pragma unroll
-  for (int l = 0; l < 32; ++l) xr[l] = (l < R) ? X[tid + ld * l] : 0.0;
-#pragma unroll 1
-  for (int cc = 0; cc < R; ++cc) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int l = 0; l < 32; l += 4) {
-      if (l < RB) {
-        s0 = fma(xr[l], U[l + RB * cc], s0);
-        s1 = fma(xr[l + 1], U[l + 1 + RB * cc], s1);
-        s2 = fma(xr[l + 2], U[l + 2 + RB * cc], s2);
-        s3 = fma(xr[l + 3], U[l + 3 + RB * cc], s3);
-      }
-    }
-    Y[tid + ld * cc] = (s0 + s1) + (s2 + s3);
-  }
-}
-
-
-// Block-parallel outer-product Cholesky of Gs (RB x RB, R x R used) with tight loops: the tail
-// kernels run once per mode right after the stream pass has flushed L2 and the instruction caches,
-// so their cost is dominated by cold instruction fetches (~600 cycles per 128 B of SASS); this
-// routine is ~2 KB of code.  One barrier per column.  On exit Ru = L^T (upper), invd = 1/L_jj.
-__device__ __noinline__ bool cq_chol_par(double* Gs, int R, int RB, double* Ru, double* invd, double* ratio) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  bool ok = true;
-  double dmax = 0.0, dmin = 1e308;
-  __syncthreads();
-#pragma unroll 1
-  for (int j = 0; j < R; ++j) {
-    const double d = Gs[j + RB * j];
-    if (!(d > 0.0)) ok = false;
-    const double ljj = sqrt(fmax(d, 0.0));
-    dmax = fmax(dmax, ljj);
-    dmin = fmin(dmin, ljj);
-    const double id = (d > 0.0) ? 1.0 / d : 0.0;
-    const int T = R - j - 1;
-#pragma unroll 1
-    for (int e = tid; e < T * T; e += nt) {  // trailing update with the unscaled column j
-      const int i = j + 1 + e / T, k = j + 1 + e % T;
-      if (k <= i) Gs[i + RB * k] = fma(-Gs[i + RB * j] * id, Gs[k + RB * j], Gs[i + RB * k]);
-    }
-    if (tid == 0) invd[j] = (ljj > 0.0) ? 1.0 / ljj : 0.0;
-    __syncthreads();
-  }
-#pragma unroll 1
-  for (int e = tid; e < RB * RB; e += nt) {  // Ru(r, c) = L(c, r) = G(c, r) / L_rr, Ru(r, r) = L_rr
-    const int r = e % RB, c = e / RB;
-    double v = 0.0;
-    if (r < R && c < R && r <= c) v = (r == c) ? sqrt(fmax(Gs[r + RB * r], 0.0)) : Gs[c + RB * r] * invd[r];
-    Ru[e] = v;
-  }
-  __syncthreads();
-  *ratio = (dmin > 0.0) ? dmax / dmin : 1e308;
-  return ok;
-}
-
-// Owned-row forward substitution y U = x (U upper, inverse diagonal invd) in place on the panel row.
-__device__ __forceinline__ void cq_row_fwd_subst(double* Prow, int ld, int R, int RB, const double* U,
-                                                 const double* invd) {
-#pragma unroll 1
-  for (int j = 0; j < R; ++j) {
-    double a0 = Prow[ld * j], a1 = 0.0;
-    int l = 0;
-#pragma unroll 1
-    for (; l + 1 < j; l += 2) {
-      a0 = fma(-Prow[ld * l], U[l + RB * j], a0);
-      a1 = fma(-Prow[ld * (l + 1)], U[(l + 1) + RB * j], a1);
-    }
-    if (l < j) a0 = fma(-Prow[ld * l], U[l + RB * j], a0);
-    Prow[ld * j] = (a0 + a1) * invd[j];
-  }
-}
 
 // Right-looking Cholesky of Gs (R x R used, RB ld) with a 2-D thread map: lane = row i, warp kk
 // updates columns k = kk (mod nwarps) -- no integer division, all loads of a column step issued

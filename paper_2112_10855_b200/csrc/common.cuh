@@ -34,8 +34,6 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-__device__ __forceinline__ double ldg_nc(const double* p) { return __ldg(p); }
-
 // Asynchronous 8-byte global -> shared copy (LDGSTS): a rolled loop of these does not wait on
 // each load, so the run-once tail kernels issue all their inputs at once and wait a single time.
 __device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {

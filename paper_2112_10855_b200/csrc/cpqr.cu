@@ -36,7 +36,6 @@ struct TtmStep {
   alignas(64) CUtensorMap mx;
   alignas(64) CUtensorMap mq;
   int S = 0, nslots = 1, nfb = 1;
-  int big = 0;  // strided TMA: stage loaded as one 4-D box (A % 16 == 0)
   int64_t G = 1;
   double* P = nullptr;
   const double* in;
@@ -287,13 +286,25 @@ struct PlanIn {
   bool ne;
   bool tma;
   bool fuse;  // fused two-mode slice kernel allowed for n >= 3
-  bool big_box = true;  // strided kernel: one 4-D TMA box per stage when A % 16 == 0
   int sms;
   bool tree = false;        // dimension-tree Multi-TTM (QR/SVD variants)
   int h = 0;                // tree split: halves [0, h) and [h, N)
   bool tree_fresh = false;  // this mode computes its half's intermediate from X
   double* tbuf = nullptr;   // the tree buffer
 };
+
+// cudaMalloc; with CPQR_POISON=1 (debugging) the block is filled with 0xFF bytes (NaN as fp64), so
+// a kernel reading device memory before it was written shows up as NaN in the parity tests.
+template <typename T>
+cudaError_t dmalloc(T** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  static const bool poison = getenv("CPQR_POISON") != nullptr;
+  if (e == cudaSuccess && poison) {
+    e = cudaMemset(*p, 0xff, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  return e;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -398,18 +409,6 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         if (make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, k, s.I)) {
           s.kind = 4;
           s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0);
-          // A % 16 == 0: view a = 16 a_hi + a_lo and load a stage as ONE 32 KB box
-          // {a_lo 16, i 16, a_hi 16} (strides 8 B, A*8, 128 B) -- same shared-memory layout
-          if (s.A % 16 == 0 && in.big_box) {
-            CUtensorMap m4;
-            const uint64_t d4[4] = {16, (uint64_t)s.I, (uint64_t)(s.A / 16), (uint64_t)s.B};
-            const uint64_t st4[3] = {(uint64_t)s.A * 8, 128, (uint64_t)s.A * s.I * 8};
-            const uint32_t box4[4] = {16, 16, 16, 1};
-            if (make_tmap(&m4, src, 4, d4, st4, box4)) {
-              s.mx = m4;
-              s.big = 1;
-            }
-          }
         }
       }
     }
@@ -619,7 +618,7 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
 #define STR(NTV)                                                                                     \
   {                                                                                                  \
     set_smem(k_strided_tma<NTV>, smem);                                                              \
-    k_strided_tma<NTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S, s.big); \
+    k_strided_tma<NTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S); \
   }
     switch (NT) { case 1: STR(1) break; case 2: STR(2) break; case 3: STR(3) break; default: STR(4) break; }
 #undef STR
@@ -712,7 +711,6 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
   in.ne = ne;
   in.tma = c->use_tma;
   in.fuse = c->fuse_slice;
-  in.big_box = !(getenv("CPQR_BIG_BOX") && atoi(getenv("CPQR_BIG_BOX")) == 0);
   in.sms = c->stream_sms;
   in.tree = c->tree && !ne;
   in.h = c->tree_h;
@@ -753,21 +751,21 @@ cpqr_status build_plans(cpqr_ctx* c) {
   if (mb > c->buf_elems) {
     for (int i = 0; i < 2; ++i) { if (c->buf[i]) cudaFree(c->buf[i]); c->buf[i] = nullptr; }
     for (int i = 0; i < 2; ++i)
-      if (cudaMalloc(&c->buf[i], mb * sizeof(double)) != cudaSuccess)
+      if (dmalloc(&c->buf[i], mb * sizeof(double)) != cudaSuccess)
         return fail(c, CPQR_ENOMEM, "intermediate buffers (%zu doubles)", mb);
     c->buf_elems = mb;
   }
   if (mt > c->tree_alloc) {
     if (c->dTree) cudaFree(c->dTree);
     c->dTree = nullptr;
-    if (cudaMalloc(&c->dTree, mt * sizeof(double)) != cudaSuccess)
+    if (dmalloc(&c->dTree, mt * sizeof(double)) != cudaSuccess)
       return fail(c, CPQR_ENOMEM, "dimension-tree buffer (%zu doubles)", mt);
     c->tree_alloc = mt;
   }
   if (mp > c->part_elems) {
     if (c->dPart) cudaFree(c->dPart);
     c->dPart = nullptr;
-    if (cudaMalloc(&c->dPart, mp * sizeof(double)) != cudaSuccess)
+    if (dmalloc(&c->dPart, mp * sizeof(double)) != cudaSuccess)
       return fail(c, CPQR_ENOMEM, "slice partials (%zu doubles)", mp);
     c->part_elems = mp;
   }
@@ -864,9 +862,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     }
     const int tb = 32 * ((mbq + 31) / 32);
     const int ld = ((tb + 15) & ~15) + 4;
-    const bool compact = !getenv("CPQR_CQ_UNROLLED");
-    const size_t smem = compact ? (size_t)(8 * RB * RB + 2 * ld * RB) * sizeof(double)
-                                : (size_t)(7 * RB * RB + ld * RB) * sizeof(double);
+    const size_t smem = (size_t)(8 * RB * RB + 2 * ld * RB) * sizeof(double);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nbq);
     cfg.blockDim = dim3(tb);
@@ -885,37 +881,16 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
 #else
     const int reps = 1;
 #endif
-    for (int rep = 0; rep < reps && e == cudaSuccess; ++rep)
-    switch (RB) {
-      case 8:
-        if (compact) {
-          cudaFuncSetAttribute(k_cq_compact<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          e = cudaLaunchKernelEx(&cfg, k_cq_compact<8>, q);
-        } else {
-          cudaFuncSetAttribute(k_cq_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          e = cudaLaunchKernelEx(&cfg, k_cq_fused<8>, q);
-        }
-        break;
-      case 16:
-        if (compact) {
-          cudaFuncSetAttribute(k_cq_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          e = cudaLaunchKernelEx(&cfg, k_cq_compact<16>, q);
-        } else {
-          cudaFuncSetAttribute(k_cq_fused<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          e = cudaLaunchKernelEx(&cfg, k_cq_fused<16>, q);
-        }
-        break;
-      default:
-        if (compact) {
-          cudaFuncSetAttribute(k_cq_compact<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          e = cudaLaunchKernelEx(&cfg, k_cq_compact<32>, q);
-        } else {
-          cudaFuncSetAttribute(k_cq_fused<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          e = cudaLaunchKernelEx(&cfg, k_cq_fused<32>, q);
-        }
-        break;
+#define CQL(RBV)                                                                                    \
+  {                                                                                                 \
+    cudaFuncSetAttribute(k_cq_compact<RBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    e = cudaLaunchKernelEx(&cfg, k_cq_compact<RBV>, q);                                             \
+  }
+    for (int rep = 0; rep < reps && e == cudaSuccess; ++rep) {
+      switch (RB) { case 8: CQL(8) break; case 16: CQL(16) break; default: CQL(32) break; }
     }
-    if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_cq_fused launch: %s", cudaGetErrorString(e));
+#undef CQL
+    if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_cq_compact launch: %s", cudaGetErrorString(e));
     CKL();
     gated = true;
   } else if (c->factor_qr_mode == 0) {
@@ -1149,7 +1124,8 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   }
   // Alg. 2 lines 6-7: V_n and its QR (K2), on the side stream: it depends only on the R_k and
   // overlaps the Multi-TTM (joined before the Q0 apply).  With profiling on it runs in line.
-  const bool fork = !c->opt.profile;
+  static const bool no_fork = getenv("CPQR_NO_FORK") != nullptr;  // debugging: V_n QR inline
+  const bool fork = !c->opt.profile && !no_fork;
   prof_mark(c, 0);
   if (fork) {
     CK(cudaEventRecord(c->evf, c->st));
@@ -1159,7 +1135,8 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     cudaStream_t keep = c->side;
     if (!fork) c->side = nullptr;
     cpqr_status st = launch_kr_qr(c, n);
-    if (st == CPQR_OK && c->variant == CPQR_SVD) {  // SVD of R0 right behind its QR, off the critical path
+    static const bool pinv_main = getenv("CPQR_PINV_MAIN") != nullptr;  // debugging: old placement
+    if (st == CPQR_OK && c->variant == CPQR_SVD && !pinv_main) {  // SVD of R0 right behind its QR, off the critical path
       st = launch_pinv(c, c->side ? c->side : c->st, nullptr);
       c->pinv_ready = (st == CPQR_OK);
     }
@@ -1243,7 +1220,7 @@ cpqr_status ensure_fits(cpqr_ctx* c, int n) {
   if (n <= c->fits_cap) return CPQR_OK;
   if (c->dfits) cudaFree(c->dfits);
   c->dfits = nullptr;
-  if (cudaMalloc(&c->dfits, sizeof(double) * n) != cudaSuccess) return fail(c, CPQR_ENOMEM, "fits");
+  if (dmalloc(&c->dfits, sizeof(double) * n) != cudaSuccess) return fail(c, CPQR_ENOMEM, "fits");
   c->fits_cap = n;
   return CPQR_OK;
 }
@@ -1387,46 +1364,46 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   int64_t imax = 0;
   for (int k = 0; k < N; ++k) {
     imax = std::max(imax, dims[k]);
-    CK(cudaMalloc(&c->dA[k], sizeof(double) * dims[k] * R));
-    CK(cudaMalloc(&c->dQ[k], sizeof(double) * dims[k] * R));
-    CK(cudaMalloc(&c->dRk[k], sizeof(double) * R * R));
-    CK(cudaMalloc(&c->dG[k], sizeof(double) * R * R));
-    CK(cudaMalloc(&c->dQt[k], sizeof(double) * dims[k] * c->RQ));
-    CK(cudaMalloc(&c->dAt[k], sizeof(double) * dims[k] * c->RQ));
+    CK(dmalloc(&c->dA[k], sizeof(double) * dims[k] * R));
+    CK(dmalloc(&c->dQ[k], sizeof(double) * dims[k] * R));
+    CK(dmalloc(&c->dRk[k], sizeof(double) * R * R));
+    CK(dmalloc(&c->dG[k], sizeof(double) * R * R));
+    CK(dmalloc(&c->dQt[k], sizeof(double) * dims[k] * c->RQ));
+    CK(dmalloc(&c->dAt[k], sizeof(double) * dims[k] * c->RQ));
     CK(cudaMemset(c->dRk[k], 0, sizeof(double) * R * R));
     CK(cudaMemset(c->dG[k], 0, sizeof(double) * R * R));
   }
   int64_t J = 1;
   for (int k = 0; k < N - 1; ++k) J *= R;
-  CK(cudaMalloc(&c->dlam, sizeof(double) * R));
-  CK(cudaMalloc(&c->dQ0, sizeof(double) * J * R));
-  CK(cudaMalloc(&c->dR0, sizeof(double) * R * R));
-  CK(cudaMalloc(&c->dW, sizeof(double) * imax * R));
-  CK(cudaMalloc(&c->dWloc, sizeof(double) * imax * R));
-  CK(cudaMalloc(&c->dAhat, sizeof(double) * imax * R));
-  CK(cudaMalloc(&c->dRstack, sizeof(double) * 8 * R * R));
-  CK(cudaMalloc(&c->dQtop, sizeof(double) * 8 * R * R));
-  CK(cudaMalloc(&c->dV, sizeof(double) * (imax + 8) * R));
-  CK(cudaMalloc(&c->dtauv, sizeof(double) * 8 * R));
-  CK(cudaMalloc(&c->dinner, sizeof(double) * 4));
-  CK(cudaMalloc(&c->dMpinv, sizeof(double) * R * R));
-  CK(cudaMalloc(&c->dQ1, sizeof(double) * imax * R));
-  CK(cudaMalloc(&c->dGp, sizeof(double) * ((imax + 255) / 256 + 1) * R * R));
-  CK(cudaMalloc(&c->dinnerp, sizeof(double) * ((imax + 255) / 256 + 1)));
-  CK(cudaMalloc(&c->dR1, sizeof(double) * R * R));
-  CK(cudaMalloc(&c->dR2, sizeof(double) * R * R));
+  CK(dmalloc(&c->dlam, sizeof(double) * R));
+  CK(dmalloc(&c->dQ0, sizeof(double) * J * R));
+  CK(dmalloc(&c->dR0, sizeof(double) * R * R));
+  CK(dmalloc(&c->dW, sizeof(double) * imax * R));
+  CK(dmalloc(&c->dWloc, sizeof(double) * imax * R));
+  CK(dmalloc(&c->dAhat, sizeof(double) * imax * R));
+  CK(dmalloc(&c->dRstack, sizeof(double) * 8 * R * R));
+  CK(dmalloc(&c->dQtop, sizeof(double) * 8 * R * R));
+  CK(dmalloc(&c->dV, sizeof(double) * (imax + 8) * R));
+  CK(dmalloc(&c->dtauv, sizeof(double) * 8 * R));
+  CK(dmalloc(&c->dinner, sizeof(double) * 4));
+  CK(dmalloc(&c->dMpinv, sizeof(double) * R * R));
+  CK(dmalloc(&c->dQ1, sizeof(double) * imax * R));
+  CK(dmalloc(&c->dGp, sizeof(double) * ((imax + 255) / 256 + 1) * R * R));
+  CK(dmalloc(&c->dinnerp, sizeof(double) * ((imax + 255) / 256 + 1)));
+  CK(dmalloc(&c->dR1, sizeof(double) * R * R));
+  CK(dmalloc(&c->dR2, sizeof(double) * R * R));
   {
     const char* f = getenv("CPQR_FACTOR_QR");
     c->factor_qr_mode = (f && std::string(f) == "householder") ? 1 : 0;
   }
   c->wp_elems = (size_t)imax * R * kQ0MaxSlices;
-  CK(cudaMalloc(&c->dWp, sizeof(double) * c->wp_elems));
-  CK(cudaMalloc(&c->dq0cnt, sizeof(unsigned) * ((imax + 7) / 8 + 1)));
+  CK(dmalloc(&c->dWp, sizeof(double) * c->wp_elems));
+  CK(dmalloc(&c->dq0cnt, sizeof(unsigned) * ((imax + 7) / 8 + 1)));
   CK(cudaMemset(c->dq0cnt, 0, sizeof(unsigned) * ((imax + 7) / 8 + 1)));
-  CK(cudaMalloc(&c->dnX2, sizeof(double) * 4));
-  CK(cudaMalloc(&c->dfit, sizeof(double) * 4));
-  CK(cudaMalloc(&c->dred, sizeof(double) * 8192));
-  CK(cudaMalloc(&c->dflags, sizeof(unsigned) * 4));
+  CK(dmalloc(&c->dnX2, sizeof(double) * 4));
+  CK(dmalloc(&c->dfit, sizeof(double) * 4));
+  CK(dmalloc(&c->dred, sizeof(double) * 8192));
+  CK(dmalloc(&c->dflags, sizeof(unsigned) * 4));
   CK(cudaMemset(c->dflags, 0, sizeof(unsigned) * 4));
   CK(cudaMallocHost(&c->hpin, sizeof(double) * 64));
   // staircase row order for K2: sort KB rows of R^{N-1} by (level, index)
@@ -1441,7 +1418,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       perm[j] = (int)j;
     }
     std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return lvl[a] < lvl[b]; });
-    CK(cudaMalloc(&c->dperm, sizeof(int) * J));
+    CK(dmalloc(&c->dperm, sizeof(int) * J));
     CK(cudaMemcpy(c->dperm, perm.data(), sizeof(int) * J, cudaMemcpyHostToDevice));
     int64_t packed = 0;
     for (int cc = 1; cc <= R; ++cc) {
@@ -1455,7 +1432,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       CK(cudaFuncSetAttribute(k_kr_qr2, cudaFuncAttributeMaxDynamicSharedMemorySize, c->kr_smem));
     } else {
       c->kr_smem = 0;
-      CK(cudaMalloc(&c->dKrWork, bytes));
+      CK(dmalloc(&c->dKrWork, bytes));
     }
   }
   if (c->opt.world > 1) {
@@ -1510,7 +1487,7 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
     if (c->Xown_elems < (size_t)c->numel) {
       if (c->Xown) cudaFree(c->Xown);
       c->Xown = nullptr;
-      if (cudaMalloc(&c->Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
+      if (dmalloc(&c->Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
       c->Xown_elems = c->numel;
     }
     CK(cudaMemcpyAsync(c->Xown, x, bytes, mem == CPQR_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->st));
@@ -1603,8 +1580,10 @@ CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
       c->launch_count += c->launches_per_sweep;
     } else {
       const int64_t before = c->launch_count;
+      static const bool sync_modes = getenv("CPQR_SYNC_MODES") != nullptr;  // debugging
       for (int n = 0; n < c->N; ++n) {
         TRY(mode_update(c, n, n == c->N - 1));
+        if (sync_modes) CK(cudaDeviceSynchronize());
         if (c->opt.profile) {
           CK(cudaEventSynchronize(c->evp[5]));
           prof_accumulate(c);
@@ -1695,8 +1674,8 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   std::vector<double*> tmpQ(N, nullptr), tmpQt(N, nullptr);
   for (int k = 0; k < N; ++k) {
     if (Qo && k != n && Qo[k]) {
-      CK(cudaMalloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
-      CK(cudaMalloc(&tmpQt[k], sizeof(double) * c->dims[k] * c->RQ));
+      CK(dmalloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
+      CK(dmalloc(&tmpQt[k], sizeof(double) * c->dims[k] * c->RQ));
       CK(cudaMemcpyAsync(tmpQ[k], Qo[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
       k_transpose_pad<<<64, 256, 0, c->st>>>(tmpQ[k], c->dims[k], (int)c->dims[k], R, c->RQ, tmpQt[k]);
       CKL();
@@ -1724,7 +1703,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   if (st == CPQR_OK && Y_out) {
     if (c->opt.world > 1) {
       ytot = (n == N - 1) ? ylocal * c->opt.world : ylocal;
-      if (cudaMalloc(&yfull, sizeof(double) * ytot) != cudaSuccess) st = fail(c, CPQR_ENOMEM, "debug Y");
+      if (dmalloc(&yfull, sizeof(double) * ytot) != cudaSuccess) st = fail(c, CPQR_ENOMEM, "debug Y");
       if (st == CPQR_OK) {
         ncclResult_t r = (n == N - 1)
                              ? ncclAllGather(p.Y, yfull, (size_t)ylocal, ncclDouble, c->comm, c->st)
@@ -1760,12 +1739,12 @@ CPQR_API cpqr_status cpqr_debug_qr(cpqr_ctx* c, const double* A, int64_t m, doub
   TRY(begin_call(c));
   const int R = c->R;
   double *dA = nullptr, *dQ = nullptr, *dR = nullptr;
-  CK(cudaMalloc(&dA, sizeof(double) * m * R));
-  CK(cudaMalloc(&dQ, sizeof(double) * m * R));
-  CK(cudaMalloc(&dR, sizeof(double) * R * R));
+  CK(dmalloc(&dA, sizeof(double) * m * R));
+  CK(dmalloc(&dQ, sizeof(double) * m * R));
+  CK(dmalloc(&dR, sizeof(double) * R * R));
   CK(cudaMemcpyAsync(dA, A, sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
   double* dQt = nullptr;
-  CK(cudaMalloc(&dQt, sizeof(double) * m * c->RQ));
+  CK(dmalloc(&dQt, sizeof(double) * m * c->RQ));
   TRY(launch_factor_qr(c, dA, (int)m, dQ, dQt, dR, false));
   CK(cudaStreamSynchronize(c->st));
   cudaFree(dQt);
@@ -1783,14 +1762,14 @@ CPQR_API cpqr_status cpqr_debug_svd_solve(cpqr_ctx* c, const double* R0, const d
   const int R = c->R;
   double *dW, *dR0, *dAw, *dA, *dRn, *dlam, *dAh;
   unsigned* dfl;
-  CK(cudaMalloc(&dW, sizeof(double) * m * R));
-  CK(cudaMalloc(&dR0, sizeof(double) * R * R));
-  CK(cudaMalloc(&dAw, sizeof(double) * m * R));
-  CK(cudaMalloc(&dA, sizeof(double) * m * R));
-  CK(cudaMalloc(&dAh, sizeof(double) * m * R));
-  CK(cudaMalloc(&dRn, sizeof(double) * R * R));
-  CK(cudaMalloc(&dlam, sizeof(double) * R));
-  CK(cudaMalloc(&dfl, sizeof(unsigned)));
+  CK(dmalloc(&dW, sizeof(double) * m * R));
+  CK(dmalloc(&dR0, sizeof(double) * R * R));
+  CK(dmalloc(&dAw, sizeof(double) * m * R));
+  CK(dmalloc(&dA, sizeof(double) * m * R));
+  CK(dmalloc(&dAh, sizeof(double) * m * R));
+  CK(dmalloc(&dRn, sizeof(double) * R * R));
+  CK(dmalloc(&dlam, sizeof(double) * R));
+  CK(dmalloc(&dfl, sizeof(unsigned)));
   CK(cudaMemsetAsync(dfl, 0, sizeof(unsigned), c->st));
   std::vector<double> wr((size_t)m * R);
   for (int64_t i = 0; i < m; ++i)
@@ -1798,7 +1777,7 @@ CPQR_API cpqr_status cpqr_debug_svd_solve(cpqr_ctx* c, const double* R0, const d
   CK(cudaMemcpyAsync(dW, wr.data(), sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(dR0, R0, sizeof(double) * R * R, cudaMemcpyHostToDevice, c->st));
   int* dnt = nullptr;
-  CK(cudaMalloc(&dnt, sizeof(int)));
+  CK(dmalloc(&dnt, sizeof(int)));
   CK(cudaMemsetAsync(dnt, 0, sizeof(int), c->st));
   CK(cudaMemcpyAsync(c->dR0, dR0, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->st));
   {

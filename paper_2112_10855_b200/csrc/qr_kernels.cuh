@@ -35,32 +35,6 @@ struct DenseCols {     // dense panel: column k at base + k*ld, m rows
   __device__ __forceinline__ int rows(int) const { return m; }
 };
 
-// warp 0 only: Householder vector for column j (dlarfg): beta = -sign(x0) ||x||, tau = (beta - x0)/beta,
-// v = x / (x0 - beta) below the diagonal, col(j)[j] = beta.
-template <class Cols>
-__device__ __forceinline__ void hh_make_reflector(const Cols& M, int j, double* tau, double* beta) {
-  const int lane = threadIdx.x & 31;
-  double* cj = M.col(j);
-  const int mj = M.rows(j);
-  double s = 0.0;
-  for (int i = j + 1 + lane; i < mj; i += 32) s += cj[i] * cj[i];
-  s = warp_sum(s);
-  const double x0 = cj[j];
-  double tj, bj, scale;
-  if (s == 0.0) { tj = 0.0; bj = x0; scale = 0.0; }
-  else {
-    const double nrm = sqrt(x0 * x0 + s);
-    bj = (x0 >= 0.0) ? -nrm : nrm;
-    tj = (bj - x0) / bj;
-    scale = 1.0 / (x0 - bj);
-  }
-  if (tj != 0.0)
-    for (int i = j + 1 + lane; i < mj; i += 32) cj[i] *= scale;
-  __syncwarp();
-  if (lane == 0) { cj[j] = bj; tau[j] = tj; beta[j] = bj; }
-  __syncwarp();
-}
-
 // Factorisation.  On exit: col(k)[r] (r < k) = R(r, k) (unsigned), beta[k] = R(k, k), reflector
 // j (v_j = 1 implicit) stored below the diagonal of column j, tau[j].  All threads must call;
 // `w` needs R doubles, `np` 64 doubles of shared memory.
@@ -420,90 +394,6 @@ __global__ void __launch_bounds__(512) k_tsqr_qform(TsqrArgs a) {
   for (int i = tid / a.RQ; i < rows; i += nt / a.RQ) {  // blockDim is a multiple of RQ (16/32)
     const int c = tid % a.RQ;
     a.Qt[(int64_t)(r0 + i) * a.RQ + c] = (c < R) ? Mq[i + rows * c] : 0.0;
-  }
-}
-
-// ----------------------------------------------------------------------- solve + normalise
-struct SolveArgs {
-  const double* W;   // In x R row-major
-  const double* R0;  // R x R column-major
-  int In, R, variant;
-  double tau;
-  double* A;         // out: normalised factor, column-major
-  double* Ahat;      // out: unnormalised solution, column-major
-  double* lam;
-  unsigned* flags;
-  int do_fit;
-  double* inner;     // out: <W, Ahat R0^T>
-  int* ntrunc;
-};
-
-__global__ void __launch_bounds__(512) k_solve_norm(SolveArgs a) {
-  extern __shared__ double sm[];
-  __shared__ double red[32], lam[64];
-  __shared__ int sflag;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const int R = a.R, In = a.In;
-  double* R0s = sm;
-  double* Ms = R0s + R * R;
-  double* Bs = Ms + R * R;
-  double* Vs = Bs + R * (R + 1);
-  for (int e = tid; e < R * R; e += nt) R0s[e] = a.R0[e];
-  __syncthreads();
-  if (a.variant == 2) {
-    const int ntr = jacobi_pinv(R0s, R, a.tau, Bs, Vs, Ms, &sflag);
-    if (tid == 0 && ntr > 0) atomicOr(a.flags, FLAG_SVD_TRUNCATED);
-    if (tid == 0 && a.ntrunc) *a.ntrunc = ntr;
-    for (int64_t e = tid; e < (int64_t)In * R; e += nt) {  // e = c * In + i (coalesced store)
-      const int c = (int)(e / In), i = (int)(e - (int64_t)c * In);
-      const double* wr = a.W + (int64_t)i * R;
-      double s = 0.0;
-      for (int r = 0; r < R; ++r) s = fma(wr[r], Ms[r + R * c], s);
-      a.Ahat[e] = s;
-    }
-  } else {
-    for (int i = tid; i < In; i += nt) {  // Ahat(i,j) = (W(i,j) - sum_{l>j} Ahat(i,l) R0(j,l)) / R0(j,j)
-      const double* wr = a.W + (int64_t)i * R;
-      double x[32];
-#pragma unroll 1
-      for (int j = R - 1; j >= 0; --j) {
-        double acc = wr[j];
-#pragma unroll 1
-        for (int l = j + 1; l < R; ++l) acc -= x[l] * R0s[j + R * l];
-        x[j] = acc / R0s[j + R * j];
-      }
-#pragma unroll 1
-      for (int j = 0; j < R; ++j) a.Ahat[i + (int64_t)In * j] = x[j];
-    }
-  }
-  __syncthreads();
-  for (int c = wid; c < R; c += nw) {
-    const double* col = a.Ahat + (int64_t)In * c;
-    double s = 0.0;
-    for (int i = lane; i < In; i += 32) s += col[i] * col[i];
-    s = warp_sum(s);
-    if (lane == 0) lam[c] = sqrt(s);
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int c = 0; c < R; ++c) if (!isfinite(lam[c])) atomicOr(a.flags, FLAG_NONFINITE);
-  for (int64_t e = tid; e < (int64_t)In * R; e += nt) {
-    const int c = (int)(e / In), i = (int)(e - (int64_t)c * In);
-    a.A[e] = (lam[c] > 0.0) ? a.Ahat[e] / lam[c] : (i == 0 ? 1.0 : 0.0);
-  }
-  if (tid < R) a.lam[tid] = lam[tid];
-  if (a.do_fit) {  // <W, Ahat R0^T> = sum_i sum_c W(i,c) sum_{l>=c} Ahat(i,l) R0(c,l)
-    double s = 0.0;
-    for (int i = tid; i < In; i += nt) {
-      const double* wr = a.W + (int64_t)i * R;
-      for (int c = 0; c < R; ++c) {
-        double t = 0.0;
-        for (int l = c; l < R; ++l) t = fma(a.Ahat[i + (int64_t)In * l], R0s[c + R * l], t);
-        s = fma(wr[c], t, s);
-      }
-    }
-    s = block_sum(s, red);
-    if (tid == 0) *a.inner = s;
   }
 }
 

@@ -1,16 +1,16 @@
 // Small per-mode kernels of the CP-ALS-QR hot path (sm_100a, fp64).  Everything here works on
-// O(I_n R + R^N) data; the only pass over the tensor X is in ttm_kernels.cuh (and k_sumsq,
-// once per set_tensor).
+// O(I_n R + R^N) data; the passes over the tensor X are in tma_kernels.cuh / ttm_kernels.cuh
+// (and k_sumsq, once per set_tensor).
 //
-//   K1 k_factor_qr / hh_qr_block  thin Householder QR of I_n x R (Alg. 2 line 3/12)
-//   K2 k_kr_qr      Khatri-Rao of triangular R_k + staircase Householder QR -> Q0, R0
-//                   (Alg. 2 lines 6-7; staircase/no fill-in PAPER.md:458-466)
-//   K4 k_q0_apply   W_n = Y_(n) Q0 (Alg. 2 line 9)
-//   K5 k_tail_qr    solve Ahat R0^T = W (substitution) or Ahat = W U S^+ V^T (one-sided Jacobi SVD
-//                   of R0), normalise, lambda, factor QR, fast fit
-//   K6 k_sumsq      ||X||^2 (fixed-order two-level reduction)
-//   K7 k_diag_contract, k_tail_ne   CP-ALS (Alg. 1) MTTKRP stage 2 and the
+//   k_factor_qr / hh_qr_block  thin Householder QR of I_n x R for very tall factors (Alg. 2 line
+//                   3/12); the usual factor QR is cholqr.cuh
+//   k_q0_apply_tc   W_n = Y_(n) Q0 on DMMA (Alg. 2 line 9)
+//   jacobi_pinv     one-sided Jacobi SVD of R0 -> M = U S^+ V^T
+//   k_sumsq         ||X||^2 (fixed-order two-level reduction)
+//   k_diag_contract, k_tail_ne   CP-ALS (Alg. 1) MTTKRP stage 2 and the
 //                   Cholesky/LU solve, normalise, Gram, fast fit
+//   k_resid_partial direct fit ||X - [[lambda; A]]||
+// The V_n QR (k_kr_qr2) is in qr_kernels.cuh.
 // All reductions are fixed-order (no floating-point atomics): results are bitwise reproducible.
 #pragma once
 #include "common.cuh"
@@ -173,130 +173,6 @@ struct KrQrArgs {
   unsigned* flags;
 };
 
-__global__ void __launch_bounds__(1024) k_kr_qr(KrQrArgs a) {
-  extern __shared__ double sm[];
-  __shared__ double tau[64], beta[64], w[64], red[32];
-  __shared__ int64_t off[65];
-  __shared__ int ncnt[64];
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const int R = a.R, N1 = a.N1;
-  if (tid == 0) {
-    int64_t o = 0;
-    for (int c = 0; c < R; ++c) {
-      int64_t p = 1;
-      for (int m = 0; m < N1; ++m) p *= (c + 1);
-      ncnt[c] = (int)p;
-      off[c] = o;
-      o += p;
-    }
-    off[R] = o;
-  }
-  __syncthreads();
-  double* V = a.use_smem ? sm : a.work_global;
-  // 1. form V_n (packed staircase)
-  for (int c = 0; c < R; ++c) {
-    for (int p = tid; p < ncnt[c]; p += nt) {
-      int j = a.perm[p];
-      double v = 1.0;
-      for (int m = 0; m < N1; ++m) {
-        const int im = j % R;
-        j /= R;
-        v *= a.Rk[m][im + R * c];
-      }
-      V[off[c] + p] = v;
-    }
-  }
-  __syncthreads();
-  // 2. Householder on the staircase
-  for (int j = 0; j < R; ++j) {
-    double* colj = V + off[j];
-    const int mj = ncnt[j];
-    double s = 0.0;
-    for (int i = j + 1 + tid; i < mj; i += nt) s += colj[i] * colj[i];
-    s = block_sum(s, red);
-    const double alpha = colj[j];
-    const double nrm = sqrt(alpha * alpha + s);
-    double tj, bj, scale;
-    if (s == 0.0) { tj = 0.0; bj = alpha; scale = 0.0; }
-    else { bj = (alpha >= 0.0) ? -nrm : nrm; tj = (bj - alpha) / bj; scale = 1.0 / (alpha - bj); }
-    __syncthreads();
-    if (tj != 0.0)
-      for (int i = j + 1 + tid; i < mj; i += nt) colj[i] *= scale;
-    if (tid == 0) { tau[j] = tj; beta[j] = bj; colj[j] = bj; }
-    __syncthreads();
-    if (tj != 0.0) {
-      for (int k = j + 1 + wid; k < R; k += nw) {
-        const double* ck = V + off[k];
-        double d = 0.0;
-        for (int i = j + 1 + lane; i < mj; i += 32) d += colj[i] * ck[i];
-        d = warp_sum(d);
-        if (lane == 0) w[k] = ck[j] + d;
-      }
-      __syncthreads();
-      for (int k = j + 1; k < R; ++k) {
-        double* ck = V + off[k];
-        const double wk = tj * w[k];
-        for (int i = j + tid; i < mj; i += nt) ck[i] -= wk * ((i == j) ? 1.0 : colj[i]);
-      }
-      __syncthreads();
-    }
-  }
-  // 3. R0 (sign fixed)
-  for (int e = tid; e < R * R; e += nt) {
-    const int r = e % R, c = e / R;
-    double v = 0.0;
-    if (r < c) v = V[off[c] + r];
-    else if (r == c) v = beta[r];
-    if (beta[r] < 0.0) v = -v;
-    a.R0[r + R * c] = v;
-  }
-  if (tid == 0) {
-    double mx = 0.0, mn = 1e308;
-    for (int c = 0; c < R; ++c) { mx = fmax(mx, fabs(beta[c])); mn = fmin(mn, fabs(beta[c])); }
-    int64_t J = 1;
-    for (int m = 0; m < N1; ++m) J *= R;
-    if (mn <= (double)J * kEps * mx) atomicOr(a.flags, FLAG_ILLCOND_R0);
-  }
-  __syncthreads();
-  // 4. explicit Q0 in place (dorg2r on the staircase)
-  for (int j = R - 1; j >= 0; --j) {
-    double* colj = V + off[j];
-    const int mj = ncnt[j];
-    const double tj = tau[j];
-    if (j < R - 1 && tj != 0.0) {
-      for (int k = j + 1 + wid; k < R; k += nw) {
-        const double* ck = V + off[k];
-        double d = 0.0;
-        for (int i = j + 1 + lane; i < mj; i += 32) d += colj[i] * ck[i];
-        d = warp_sum(d);
-        if (lane == 0) w[k] = ck[j] + d;
-      }
-      __syncthreads();
-      for (int k = j + 1; k < R; ++k) {
-        double* ck = V + off[k];
-        const double wk = tj * w[k];
-        for (int i = j + tid; i < mj; i += nt) ck[i] -= wk * ((i == j) ? 1.0 : colj[i]);
-      }
-      __syncthreads();
-    }
-    for (int i = tid; i < mj; i += nt) {
-      if (i < j) colj[i] = 0.0;
-      else if (i == j) colj[i] = 1.0 - tj;
-      else colj[i] = -tj * colj[i];
-    }
-    __syncthreads();
-  }
-  // 5. scatter to dense KB order with the column sign fix
-  int64_t J = 1;
-  for (int m = 0; m < N1; ++m) J *= R;
-  for (int64_t e = tid; e < J * R; e += nt) a.Q0[e] = 0.0;
-  __syncthreads();
-  for (int c = 0; c < R; ++c) {
-    const double sg = (beta[c] < 0.0) ? -1.0 : 1.0;
-    for (int p = tid; p < ncnt[c]; p += nt) a.Q0[a.perm[p] + J * c] = sg * V[off[c] + p];
-  }
-}
-
 // ------------------------------------------------------------------------- K4: Q0 apply
 // W_n = Y_(n) Q0 (Alg. 2 line 9) on the FP64 tensor path (DMMA m8n8k4).
 // Y column-major viewed as (Aa, In, Bb); Y_(n) column j = a + Aa b (Kolda-Bader); W row-major.
@@ -440,122 +316,6 @@ __device__ int jacobi_pinv(const double* R0, int R, double tau, double* Bs, doub
   }
   __syncthreads();
   return ntr;
-}
-
-// ------------------------------------------------------------------ K5: per-mode tail (QR/SVD)
-struct TailArgs {
-  const double* W;   // In x R row-major (complete, all rows)
-  const double* R0;  // R x R column-major
-  int In, R;
-  int variant;       // 1 QR, 2 SVD
-  double tau;
-  double* Aw;        // scratch In x R column-major (becomes Q_n)
-  double* A;         // out: normalised factor, column-major
-  double* Rn;        // out: R_n (R x R)
-  double* lam;       // out: lambda
-  unsigned* flags;
-  int do_fit;
-  const double* nX2;
-  double* fit;       // out (when do_fit)
-  double* Ahat_fit;  // scratch In x R column-major for the fit (unnormalised Ahat)
-  int* ntrunc;       // optional out: number of truncated singular values
-};
-
-__global__ void __launch_bounds__(512) k_tail_qr(TailArgs a) {
-  extern __shared__ double sm[];
-  __shared__ double tau[64], beta[64], w[64], red[32], lam[64];
-  __shared__ int sflag;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const int R = a.R, In = a.In;
-  double* R0s = sm;               // R x R
-  double* Ms = sm + R * R;        // R x R (SVD pinv) or unused
-  double* Bs = Ms + R * R;        // R x (R+1)
-  double* Vs = Bs + R * (R + 1);  // R x (R+1)
-  for (int e = tid; e < R * R; e += nt) R0s[e] = a.R0[e];
-  __syncthreads();
-  // 1. solve: rows are independent
-  if (a.variant == 2) {
-    const int ntr = jacobi_pinv(R0s, R, a.tau, Bs, Vs, Ms, &sflag);
-    if (tid == 0 && ntr > 0) atomicOr(a.flags, FLAG_SVD_TRUNCATED);
-    if (tid == 0 && a.ntrunc) *a.ntrunc = ntr;
-    for (int i = tid; i < In; i += nt) {
-      const double* wr = a.W + (int64_t)i * R;
-      for (int c = 0; c < R; ++c) {
-        double s = 0.0;
-        for (int r = 0; r < R; ++r) s = fma(wr[r], Ms[r + R * c], s);
-        a.Aw[i + (int64_t)In * c] = s;
-      }
-    }
-  } else {
-    for (int i = tid; i < In; i += nt) {
-      const double* wr = a.W + (int64_t)i * R;
-      double x[64];
-      for (int j = R - 1; j >= 0; --j) {  // Ahat(i,j) = (W(i,j) - sum_{l>j} Ahat(i,l) R0(j,l)) / R0(j,j)
-        double acc = wr[j];
-        for (int l = j + 1; l < R; ++l) acc -= x[l] * R0s[j + R * l];
-        x[j] = acc / R0s[j + R * j];
-      }
-      for (int j = 0; j < R; ++j) a.Aw[i + (int64_t)In * j] = x[j];
-    }
-  }
-  __syncthreads();
-  // 2. lambda = column 2-norms (one warp per column, fixed order); non-finite check
-  for (int c = wid; c < R; c += nw) {
-    const double* col = a.Aw + (int64_t)In * c;
-    double s = 0.0;
-    for (int i = lane; i < In; i += 32) s += col[i] * col[i];
-    s = warp_sum(s);
-    if (lane == 0) lam[c] = sqrt(s);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int c = 0; c < R; ++c)
-      if (!isfinite(lam[c])) atomicOr(a.flags, FLAG_NONFINITE);
-  }
-  // keep Ahat for the fit, normalise (zero column -> e_1, reading 10)
-  for (int64_t e = tid; e < (int64_t)In * R; e += nt) {
-    const int c = (int)(e / In), i = (int)(e % In);
-    const double v = a.Aw[e];
-    if (a.do_fit) a.Ahat_fit[e] = v;
-    const double nv = (lam[c] > 0.0) ? v / lam[c] : (i == 0 ? 1.0 : 0.0);
-    a.Aw[e] = nv;
-    a.A[e] = nv;
-  }
-  if (tid < R) a.lam[tid] = lam[tid];
-  __syncthreads();
-  // 3. factor QR (Alg. 2 line 12) in place: Aw -> Q_n, R_n
-  hh_qr_block(a.Aw, In, In, R, a.Rn, tau, beta, w, red);
-  // 4. fast fit after mode N
-  if (a.do_fit) {
-    // inner = <W, Ahat R0^T> = sum_i sum_c W(i,c) sum_l Ahat(i,l) R0(c,l)
-    double s = 0.0;
-    for (int i = tid; i < In; i += nt) {
-      const double* wr = a.W + (int64_t)i * R;
-      for (int c = 0; c < R; ++c) {
-        double t = 0.0;
-        for (int l = c; l < R; ++l) t = fma(a.Ahat_fit[i + (int64_t)In * l], R0s[c + R * l], t);
-        s = fma(wr[c], t, s);
-      }
-    }
-    const double inner = block_sum(s, red);
-    // ||Xh||^2 = <R0^T R0, diag(lam) R_n^T R_n diag(lam)>
-    double q = 0.0;
-    for (int e = tid; e < R * R; e += nt) {
-      const int x = e % R, y = e / R;
-      double g0 = 0.0, g1 = 0.0;
-      for (int k = 0; k < R; ++k) {
-        g0 = fma(R0s[k + R * x], R0s[k + R * y], g0);
-        g1 = fma(a.Rn[k + R * x], a.Rn[k + R * y], g1);
-      }
-      q = fma(g0, lam[x] * lam[y] * g1, q);
-    }
-    const double nxh2 = block_sum(q, red);
-    if (tid == 0) {
-      const double nx2 = *a.nX2;
-      const double res2 = fmax(0.0, nx2 - 2.0 * inner + nxh2);
-      *a.fit = 1.0 - sqrt(res2) / sqrt(nx2);
-    }
-  }
 }
 
 // --------------------------------------------------------------------------- K7: CP-ALS (NE)

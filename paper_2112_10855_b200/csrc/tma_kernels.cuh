@@ -58,14 +58,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
 // L2 evict-first policy for the single-use tensor stream: X passes through L2 without evicting
 // the small reused working set (Q panels, W, factors) and, above all, the code of the per-mode
 // tail kernels, whose cold instruction fetches from DRAM otherwise dominate their run time.
@@ -88,14 +80,6 @@ __device__ __forceinline__ void tma_load_3d_ef(void* dst, const CUtensorMap* map
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_4d_ef(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                               uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -141,7 +125,7 @@ __device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& fu
 template <int NT>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
-              int I, int64_t B, int R, double* __restrict__ T, int S, int big) {
+              int I, int64_t B, int R, double* __restrict__ T, int S) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (NT + 1) / 2;
   constexpr uint32_t XBYTES = 16 * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
@@ -171,12 +155,8 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
-          if (big) {  // one 32 KB box {16 a, 16 i, 16 a-groups}: same smem layout as the 16 boxes
-            tma_load_4d_ef(dst, &tmX, 0, ks * kBK, a0 / 16, b, &full[s], pol);
-          } else {
 #pragma unroll 4
-            for (int q = 0; q < 16; ++q) tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
-          }
+          for (int q = 0; q < 16; ++q) tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
 #pragma unroll
           for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }

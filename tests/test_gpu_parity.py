@@ -334,3 +334,25 @@ def test_ne_variant_tail(cp, dims, R, force_lu, monkeypatch):
     if force_lu:
         assert s.flags & 2  # NE_CHOL_FALLBACK reported
     s.close()
+
+
+def test_run_to_run_determinism(cp):
+    """Every reduction is fixed-order, so repeated runs are bitwise identical.  N = 5 with a
+    48-row strided step (many TMA boxes partly out of bounds) and back-to-back graph replays vs one
+    sweep per call: a race or a TMA misuse shows up as a second distinct result."""
+    dims, R = (48, 20, 12, 10, 8), 8
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=97, eta=0.05)
+    s = cp.CPQR(dims, R, "SVD")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    ref = s.debug_mode(0)["Y"]
+    for _ in range(150):
+        assert np.array_equal(s.debug_mode(0)["Y"], ref)
+    fa = s.sweep(12)
+    s.close()
+    s = cp.CPQR(dims, R, "SVD")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    fb = np.concatenate([s.sweep(1) for _ in range(12)])
+    s.close()
+    assert np.array_equal(fa, fb)
