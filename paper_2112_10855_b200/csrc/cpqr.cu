@@ -615,12 +615,22 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
     const size_t smem = 3072 + (size_t)s.S * (16 * kBoxBytes + NQB * kBoxBytes);
     const int64_t units = ((s.A + 255) / 256) * s.B;
     const int grid = (int)std::min<int64_t>(units, sms);
-#define STR(NTV)                                                                                     \
-  {                                                                                                  \
-    set_smem(k_strided_tma<NTV>, smem);                                                              \
-    k_strided_tma<NTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S); \
+#define STR(NTV, NPV)                                                                                  \
+  {                                                                                                     \
+    set_smem(k_strided_tma<NTV, NPV>, smem);                                                            \
+    k_strided_tma<NTV, NPV><<<grid, (kCW + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S); \
   }
-    switch (NT) { case 1: STR(1) break; case 2: STR(2) break; case 3: STR(3) break; default: STR(4) break; }
+    // producer warps issuing the 16 X boxes of a stage in parallel: a single issuing thread bounds
+    // the HBM-bound passes (C2 +16 %); 4 for the FP64-bound R >= 24 passes (+1.5 % on C5, -1.5 % C4)
+    static const int np_env = getenv("CPQR_NPROD") ? atoi(getenv("CPQR_NPROD")) : 0;
+    const int np = np_env ? np_env : (R >= 24 ? 4 : 2);
+    if (np == 4) {
+      switch (NT) { case 1: STR(1, 4) break; case 2: STR(2, 4) break; case 3: STR(3, 4) break; default: STR(4, 4) break; }
+    } else if (np == 2) {
+      switch (NT) { case 1: STR(1, 2) break; case 2: STR(2, 2) break; case 3: STR(3, 2) break; default: STR(4, 2) break; }
+    } else {
+      switch (NT) { case 1: STR(1, 1) break; case 2: STR(2, 1) break; case 3: STR(3, 1) break; default: STR(4, 1) break; }
+    }
 #undef STR
   } else if (s.kind == 5) {
     const size_t smem = 3072 + (size_t)s.S * (128 * 128 + NQB * kBoxBytes);

@@ -142,8 +142,8 @@ __device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& fu
 // X map 3D {A, I, B}, box {16, 16, 1} (16 boxes per stage); Q map 2D {RQ, I} over the transposed
 // padded panel Qt[i*RQ + r], box {16, 16} (NT/2 boxes).  Consumer warp w owns rows 32w..32w+31:
 // M-tiles mt = 2p + s hold rows 16(2w+p) + 2g + s (one 16-byte load feeds two tiles).
-template <int NT>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int NT, int NP = 1>
+__global__ void __launch_bounds__((kCW + NP) * 32, 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
               int I, int64_t B, int R, double* __restrict__ T, int S) {
   extern __shared__ uint8_t smraw[];
@@ -161,10 +161,14 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   const int64_t nA = (A + 255) / 256;
   const int64_t units = nA * B;
   const int KS = (I + kBK - 1) / kBK;
-  if (warp == kCW) {  // ---------------------------------------------------------- producer
+  if (warp >= kCW) {  // ---------------------------------------------------------- producer(s)
+    // NP producer warps split the 16 X boxes of a stage (the per-box TMA issue cost bounds the
+    // HBM-bound passes); producer 0 also loads Q and does the arrive.expect_tx for the whole stage
+    // (bytes of the other producers may land first: the tx count just dips below zero meanwhile)
+    const int pw = warp - kCW;
     if (lane == 0) {
       prefetch_tmap(&tmX);
-      prefetch_tmap(&tmQ);
+      if (pw == 0) prefetch_tmap(&tmQ);
       const uint64_t pol = policy_evict_first();
       uint32_t it = 0;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
@@ -173,12 +177,14 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
         for (int ks = 0; ks < KS; ++ks, ++it) {
           const int s = it % S;
           mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          mbar_expect_tx(&full[s], STAGE);
+          if (pw == 0) mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
 #pragma unroll 4
-          for (int q = 0; q < 16; ++q) tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
+          for (int q = pw * (16 / NP); q < (pw + 1) * (16 / NP); ++q)
+            tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
+          if (pw == 0)
 #pragma unroll
-          for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
+            for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }
       }
     }
