@@ -356,3 +356,26 @@ def test_run_to_run_determinism(cp):
     fb = np.concatenate([s.sweep(1) for _ in range(12)])
     s.close()
     assert np.array_equal(fa, fb)
+
+
+def test_householder_fallback_inside_captured_graph(cp):
+    """Factors with congruence 1 - 1e-10 (kappa(A_n) > 1e5): CholeskyQR2 fails its guard and the
+    device-flag-gated Householder TSQR kernels take over, inside the captured CUDA graph and in
+    eager launches alike.  Both must agree bitwise and follow the oracle.  (A conditional graph
+    node for this branch measured slower than the three early-exiting kernels: C2 -4 %.)"""
+    dims, R = (40, 36, 30), 4
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=83, eta=1e-6, kind="congruence", c=1.0 - 1e-10)
+    Xt = O.as_tensor(Xc)
+    res = []
+    for g in (True, False):
+        s = cp.CPQR(dims, R, "QR", use_graph=g)
+        s.set_tensor(Xc)
+        s.set_factors(truth)  # start at the (ill-conditioned) planted factors
+        f = s.sweep(3)
+        lam, A = s.get_factors()
+        res.append((f, lam, A))
+        s.close()
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][2], res[1][2]))
+    ref = O.cp_als_qr(Xt, truth, 3)
+    assert np.max(np.abs(res[0][0] - np.array(ref["fits"]))) <= 1e-8
