@@ -87,7 +87,7 @@ void cpqr_default_options(cpqr_options* opt);
 typedef struct cpqr_ctx cpqr_ctx;
 
 /* Create a solver for an N-way tensor of global dims[0..N-1] and CP rank R.
- * Preconditions: N >= 2; 1 <= R <= 64; dims[k] >= R for all k (tall factors, PAPER.md:33;
+ * Preconditions: 2 <= N <= 8; 1 <= R <= 32; dims[k] >= R for all k (tall factors, PAPER.md:33;
  * reading 27); with world = p > 1, the last mode is split into slabs (cpqr_set_tensor).
  * Errors: EINVAL, ENOMEM, ECUDA, ENCCL. */
 cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,

@@ -1145,8 +1145,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     cudaStream_t keep = c->side;
     if (!fork) c->side = nullptr;
     cpqr_status st = launch_kr_qr(c, n);
-    static const bool pinv_main = getenv("CPQR_PINV_MAIN") != nullptr;  // debugging: old placement
-    if (st == CPQR_OK && c->variant == CPQR_SVD && !pinv_main) {  // SVD of R0 right behind its QR, off the critical path
+    if (st == CPQR_OK && c->variant == CPQR_SVD) {  // SVD of R0 right behind its QR, off the critical path
       st = launch_pinv(c, c->side ? c->side : c->st, nullptr);
       c->pinv_ready = (st == CPQR_OK);
     }

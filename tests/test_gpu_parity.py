@@ -379,3 +379,53 @@ def test_householder_fallback_inside_captured_graph(cp):
     assert all(np.array_equal(a, b) for a, b in zip(res[0][2], res[1][2]))
     ref = O.cp_als_qr(Xt, truth, 3)
     assert np.max(np.abs(res[0][0] - np.array(ref["fits"]))) <= 1e-8
+
+
+@pytest.mark.parametrize("dims,R,variant", [((30, 40, 50), 1, "QR"), ((12, 10, 9, 11), 1, "QR"),
+                                            ((8, 8, 8), 8, "QR"), ((5, 5, 5, 5), 5, "SVD"),
+                                            ((3,) * 8, 2, "QR"), ((40, 3), 3, "QR")])
+def test_edge_shapes(cp, dims, R, variant):
+    """Degenerate and extreme shapes: rank one, square factors (I_k = R), the maximum order N = 8,
+    N = 2 with a square factor (exact fit 1).  Fits within 1e-8 and factors <= 1e-9 of the oracle."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=5, eta=0.01)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_qr(X, init, 1, variant=variant)
+    for k in range(len(dims)):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(2)])
+    ref = O.cp_als_qr(X, init, 3, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+
+
+def test_zero_tensor(cp):
+    """X = 0 (degenerate: every W is 0).  QR: the factors collapse to e_1 columns, R0 is singular
+    and the oracle's back substitution produces NaN; the library reports EDIVERGED with the
+    ILLCOND_R0 flag.  SVD: everything is truncated, lambda = 0, and the fit is 0/0 = NaN in both."""
+    import warnings
+    dims, R = (6, 5, 4), 2
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=5)
+    Z = np.zeros_like(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Z)
+    s.set_factors(init)
+    with pytest.raises(cp.CpqrError) as ei:
+        s.sweep(2)
+    assert "EDIVERGED" in str(ei.value) and s.flags & 1
+    s.close()
+    s = cp.CPQR(dims, R, "SVD")
+    s.set_tensor(Z)
+    s.set_factors(init)
+    f = s.sweep(2)
+    lam, A = s.get_factors()
+    assert np.all(np.isnan(f)) and np.all(lam == 0.0) and s.flags & 4
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        ref = O.cp_als_qr(O.as_tensor(Z), init, 2, variant="SVD")
+    assert np.all(ref["lam"] == 0.0) and np.all(np.isnan(ref["fits"]))
+    s.close()
