@@ -23,6 +23,7 @@ namespace cpqr {
 
 constexpr double kCqKappaMax = 1.0e5;
 constexpr unsigned FLAG_USE_HOUSEHOLDER = 0x200u;
+constexpr unsigned FLAG_VN_HOUSEHOLDER = 0x400u;  // the CholeskyQR2 V_n QR handed over to K2
 
 struct CqArgs {
   const double* A;   // solve = 0: m x R column-major input
@@ -48,7 +49,9 @@ struct CqArgs {
   int do_fit;
   const double* nX2;
   double* fit;
+  unsigned hh_bit;  // flag bit of the Householder-fallback decision (0: FLAG_USE_HOUSEHOLDER)
 };
+__device__ __forceinline__ unsigned cq_hh_bit(const CqArgs& a) { return a.hh_bit ? a.hh_bit : FLAG_USE_HOUSEHOLDER; }
 
 // Upper triangle of the block Gram from a shared-memory panel P (rows x R, leading dim ld).
 __device__ __forceinline__ void cq_block_gram(const double* P, int ld, int rows, int R, double* out) {
@@ -80,7 +83,7 @@ __global__ void __launch_bounds__(256) k_cq_gram1(CqArgs a) {
   extern __shared__ double P[];  // rows x R, ld = rows | 1
   __shared__ double Ms[RB * RB], R0s[RB * RB], redi[8];
   const int b = blockIdx.x, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (b == 0 && tid == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);  // per-mode decision
+  if (b == 0 && tid == 0) atomicAnd(a.flags, ~cq_hh_bit(a));  // per-mode decision
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0, ld = rows | 1;
   if (!a.solve) {
     for (int c = 0; c < R; ++c)
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(256) k_cq_chol1(CqArgs a) {
   __shared__ bool ok;
   cq_chol(a, Gs, Ls, true, &ok);
   if (!ok) {
-    if (threadIdx.x == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    if (threadIdx.x == 0) atomicOr(a.flags, cq_hh_bit(a));
     return;
   }
   for (int e = threadIdx.x; e < a.R * a.R; e += blockDim.x) a.R1[e] = Ls[e];
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(256) k_cq_apply(CqArgs a, int pass) {
   __shared__ unsigned fl;
   if (threadIdx.x == 0) fl = *a.flags;
   __syncthreads();
-  if (fl & FLAG_USE_HOUSEHOLDER) return;
+  if (fl & cq_hh_bit(a)) return;
   const int b = blockIdx.x, R = a.R, tid = threadIdx.x;
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0, ld = rows | 1;
   const double* Rf = (pass == 1) ? a.R1 : a.R2;
@@ -232,10 +235,12 @@ __global__ void __launch_bounds__(256) k_cq_apply(CqArgs a, int pass) {
 #pragma unroll
       for (int k = 0; k < RB; ++k)
         if (k < R) a.Q[i + (int64_t)a.m * k] = y[k];
+      if (a.Qt) {
 #pragma unroll
-      for (int k = 0; k < RB; ++k)
-        if (k < a.RQ) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? y[k] : 0.0;
-      for (int k = RB; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = 0.0;
+        for (int k = 0; k < RB; ++k)
+          if (k < a.RQ) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? y[k] : 0.0;
+        for (int k = RB; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = 0.0;
+      }
       if (a.solve) {  // A_n = Ahat / lambda (zero column -> e_1, reading 10)
 #pragma unroll
         for (int k = 0; k < RB; ++k) {
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(256) k_cq_chol2(CqArgs a, const double* G1diag
   __shared__ unsigned fl;
   if (threadIdx.x == 0) fl = *a.flags;
   __syncthreads();
-  if (fl & FLAG_USE_HOUSEHOLDER) return;
+  if (fl & cq_hh_bit(a)) return;
   const int R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int e = tid; e < R * R; e += blockDim.x) R1s[e] = a.R1[e];
   cq_chol(a, Gs, Ls, false, &ok);  // Ls = R2 = L2^T
@@ -276,10 +281,10 @@ __global__ void __launch_bounds__(256) k_cq_chol2(CqArgs a, const double* G1diag
   if (tid == 0) {
     double e = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) e = fmax(e, emax[w]);
-    if (!ok || !(e < 1.0e-4)) { atomicOr(a.flags, FLAG_USE_HOUSEHOLDER); fl = FLAG_USE_HOUSEHOLDER; }
+    if (!ok || !(e < 1.0e-4)) { atomicOr(a.flags, cq_hh_bit(a)); fl = cq_hh_bit(a); }
   }
   __syncthreads();
-  if (fl & FLAG_USE_HOUSEHOLDER) return;
+  if (fl & cq_hh_bit(a)) return;
   if (a.solve && tid < R) {  // lambda_c = ||Ahat(:,c)||_2 = sqrt(G1(c,c)) = ||R1(:,c)||_2
     double s = 0.0;
     for (int k = 0; k <= tid; ++k) s = fma(R1s[k + R * tid], R1s[k + R * tid], s);

@@ -94,6 +94,9 @@ struct cpqr_ctx {
   bool use_tma = true;
   bool fuse_slice = true;  // see plan_mode
   bool pinv_ready = false; // M = pinv(R0) already launched for this mode (side stream, after K2)
+  bool vn_cq = false;      // V_n QR by multi-CTA CholeskyQR2 (high rank), k_kr_qr2 as fallback
+  int64_t vnJ = 0;         // R^{N-1}
+  double *dVn = nullptr, *dVq1 = nullptr, *dVgp = nullptr, *dVr1 = nullptr, *dVr2 = nullptr;
   bool tree = false;       // dimension-tree Multi-TTM (opt.mttm_tree, QR/SVD, N >= 3)
   int tree_h = 0;
   double* dTree = nullptr;
@@ -835,6 +838,18 @@ cpqr_status launch_normalize(cpqr_ctx* c, int In, double* A) {
 // TSQR launcher.  solve = false: thin QR of the m x R column-major A -> Q, Qt, Rn.
 // solve = true: the fused per-mode tail -- Ahat from W (and R0 / M), lambda, A_n = Ahat/lambda into
 // Aout, and the QR of A_n (Q, Qt, Rn), plus the fast fit when do_fit.
+void cq_multi_attrs() {  // dynamic shared memory of the multi-kernel CholeskyQR2 (once)
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_cq_gram1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_cq_gram1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_cq_gram1<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_cq_apply<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_cq_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_cq_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  done = true;
+}
+
 cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const double* W, double* Q,
                         double* Qt, double* Rn, double* Aout, bool do_fit) {
   const int R = c->R, RB = rb_for(R);
@@ -916,16 +931,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     }
     const int tb = 32 * ((mbq + 31) / 32);
     const size_t psm = (size_t)(mbq | 1) * R * 8;
-    static bool cq_attr = false;
-    if (!cq_attr) {
-      cudaFuncSetAttribute(k_cq_gram1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_cq_gram1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_cq_gram1<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_cq_apply<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_cq_apply<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cudaFuncSetAttribute(k_cq_apply<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      cq_attr = true;
-    }
+    cq_multi_attrs();
     switch (RB) {
       case 8:
         k_cq_gram1<8><<<nb, tb, psm, c->st>>>(q); CKL();
@@ -1031,6 +1037,29 @@ cpqr_status launch_factor_qr(cpqr_ctx* c, const double* A, int m, double* Q, dou
   return launch_tsqr(c, m, A, false, nullptr, Q, Qt, Rn, nullptr, do_fit);
 }
 
+// Multi-kernel CholeskyQR2 of the m x R column-major q.A (row blocks of 256 rows) on stream st.
+cpqr_status launch_cq_multi(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
+  const int RB = rb_for(c->R);
+  const int tb = 32 * ((q.mb + 31) / 32);
+  const size_t psm = (size_t)(q.mb | 1) * c->R * 8;
+  cq_multi_attrs();
+#define CQM(RBV)                                                   \
+  {                                                                \
+    k_cq_gram1<RBV><<<q.nb, tb, psm, st>>>(q); CKL();              \
+    k_cq_chol1<<<1, 256, 0, st>>>(q); CKL();                       \
+    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 1); CKL();           \
+    k_cq_chol2<<<1, 256, 0, st>>>(q, nullptr); CKL();              \
+    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 2); CKL();           \
+  }
+  switch (RB) { case 8: CQM(8) break; case 16: CQM(16) break; default: CQM(32) break; }
+#undef CQM
+  return CPQR_OK;
+}
+
+// Alg. 2 lines 6-7: V_n and its QR -> Q0, R0.  Default: k_kr_qr2, one CTA, Householder on the
+// packed staircase.  High rank (R^{N-1} R large): V_n is
+// formed densely and factored by the multi-CTA CholeskyQR2 under the same kappa guard as the
+// factor QR; k_kr_qr2 then runs only if the guard rejected V_n (device flag FLAG_VN_HOUSEHOLDER).
 cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   KrQrArgs a{};
   int m = 0;
@@ -1043,8 +1072,22 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   a.R0 = c->dR0;
   a.work_global = c->dKrWork;
   a.use_smem = c->kr_smem > 0;
-  a.flags = c->variant == CPQR_QR ? c->dflags : c->dflags;
-  k_kr_qr2<<<1, 1024, c->kr_smem, c->side ? c->side : c->st>>>(a);
+  a.flags = c->dflags;
+  cudaStream_t st = c->side ? c->side : c->st;
+  if (c->vn_cq) {
+    const int64_t J = c->vnJ;
+    const int grid = (int)std::min<int64_t>((J * c->R + 255) / 256, (int64_t)c->sms * 8);
+    k_form_v<<<grid, 256, 0, st>>>(a, J, c->dVn);
+    CKL();
+    CqArgs q{};
+    q.A = c->dVn; q.m = (int)J; q.R = c->R; q.nb = (int)((J + 255) / 256); q.mb = (int)((J + q.nb - 1) / q.nb);
+    q.solve = 0; q.Q1 = c->dVq1; q.Gp = c->dVgp; q.innerp = c->dinnerp; q.R1 = c->dVr1; q.R2 = c->dVr2;
+    q.Q = c->dQ0; q.Qt = nullptr; q.RQ = c->RQ; q.Rn = c->dR0; q.flags = c->dflags; q.do_fit = 0;
+    q.nX2 = c->dnX2; q.fit = c->dfit; q.hh_bit = FLAG_VN_HOUSEHOLDER;
+    TRY(launch_cq_multi(c, q, st));
+    a.gate_bit = FLAG_VN_HOUSEHOLDER;
+  }
+  k_kr_qr2<<<1, 1024, c->kr_smem, st>>>(a);
   CKL();
   return CPQR_OK;
 }
@@ -1444,6 +1487,18 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       CK(dmalloc(&c->dKrWork, bytes));
     }
   }
+  {  // high rank: V_n QR by the multi-CTA CholeskyQR2 (see launch_kr_qr)
+    const char* v = getenv("CPQR_VN_QR");  // "cq" / "householder" force the choice
+    c->vn_cq = v ? std::string(v) == "cq" : (J * R >= 200000);
+    c->vnJ = J;
+    if (c->vn_cq) {
+      CK(dmalloc(&c->dVn, sizeof(double) * J * R));
+      CK(dmalloc(&c->dVq1, sizeof(double) * J * R));
+      CK(dmalloc(&c->dVgp, sizeof(double) * ((J + 255) / 256 + 1) * R * R));
+      CK(dmalloc(&c->dVr1, sizeof(double) * R * R));
+      CK(dmalloc(&c->dVr2, sizeof(double) * R * R));
+    }
+  }
   if (c->opt.world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, c->opt.nccl_id, sizeof id);
@@ -1467,7 +1522,8 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->evf) cudaEventDestroy(c->evf);
   if (c->evj) cudaEventDestroy(c->evj);
   double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
-                  c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown};
+                  c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown,
+                  c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2};
   for (double* p : ps) if (p) cudaFree(p);
   if (c->dperm) cudaFree(c->dperm);
   if (c->dflags) cudaFree(c->dflags);

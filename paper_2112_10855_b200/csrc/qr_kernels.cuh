@@ -397,14 +397,38 @@ __global__ void __launch_bounds__(512) k_tsqr_qform(TsqrArgs a) {
   }
 }
 
+// V_n = R_{k_{N-1}} (.) ... (.) R_{k_1} (Khatri-Rao of the retained triangular factors, Alg. 2
+// line 6) formed densely: V(j, c) = prod_m R_{k_m}(j_m, c), j = sum_m j_m R^m (the
+// Kolda-Bader row order of K2's Q0).  Used by the multi-CTA CholeskyQR2 V_n QR (high rank).
+__global__ void k_form_v(KrQrArgs a, int64_t J, double* __restrict__ V) {
+  const int R = a.R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < J * R; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / J);
+    int64_t j = e - (int64_t)c * J;
+    double v = 1.0;
+    for (int m = 0; m < a.N1; ++m) {
+      const int im = (int)(j % R);
+      j /= R;
+      v *= (im <= c) ? a.Rk[m][im + R * c] : 0.0;
+    }
+    V[e] = v;
+  }
+}
+
 // ------------------------------------------------------------- K2 with the 2-barrier primitive
 __global__ void __launch_bounds__(1024) k_kr_qr2(KrQrArgs a) {
   extern __shared__ double smk[];
   __shared__ double tau[64], beta[64], w[64], np[64];
   __shared__ int64_t off[65];
   __shared__ int ncnt[64];
+  __shared__ unsigned gate;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int R = a.R, N1 = a.N1;
+  if (a.gate_bit) {  // fallback of the CholeskyQR2 V_n QR: run only if that was rejected
+    if (tid == 0) gate = *a.flags & a.gate_bit;
+    __syncthreads();
+    if (!gate) return;
+  }
   if (tid == 0) {
     int64_t o = 0;
     for (int c = 0; c < R; ++c) {

@@ -171,6 +171,7 @@ struct KrQrArgs {
   double* work_global;  // scratch (used when use_smem == 0)
   int use_smem;
   unsigned* flags;
+  unsigned gate_bit;    // != 0: run only if this flag bit is set (fallback of the CholeskyQR2 V_n QR)
 };
 
 // ------------------------------------------------------------------------- K4: Q0 apply

@@ -429,3 +429,52 @@ def test_zero_tensor(cp):
         ref = O.cp_als_qr(O.as_tensor(Z), init, 2, variant="SVD")
     assert np.all(ref["lam"] == 0.0) and np.all(np.isnan(ref["fits"]))
     s.close()
+
+
+@pytest.mark.parametrize("dims,R,variant,kind,c", [((30, 40, 50), 5, "QR", "normal", 0.0),
+                                                   ((12, 10, 9, 11), 6, "QR", "normal", 0.0),
+                                                   ((9, 8, 7, 8, 9), 4, "SVD", "normal", 0.0),
+                                                   ((40, 36, 30), 4, "QR", "congruence", 1.0 - 1e-10)])
+def test_vn_qr_by_cholesky_qr2(cp, dims, R, variant, kind, c, monkeypatch):
+    """High-rank V_n QR path, forced on small shapes: V_n formed densely and
+    factored by the multi-CTA CholeskyQR2 under the kappa guard; with congruence 1 - 1e-10 the
+    guard rejects V_n and the staircase Householder K2 runs instead (device flag).  Q0 orthonormal,
+    V_n = Q0 R0 with diag(R0) > 0 (the unique thin QR), sweeps follow the oracle."""
+    monkeypatch.setenv("CPQR_VN_QR", "cq")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=67, eta=0.05, kind=kind, c=c)
+    X = O.as_tensor(Xc)
+    start = truth if kind == "congruence" else init
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(start)
+    Rs = [O.qr_pos(a)[1] for a in start]
+    for n in range(len(dims)):
+        d = s.debug_mode(n)
+        Q0o, R0o = O.structured_qr(Rs, n)
+        assert np.linalg.norm(d["Q0"].T @ d["Q0"] - np.eye(R)) <= 1e-12
+        assert rel(d["R0"], R0o) <= 1e-9, (n, rel(d["R0"], R0o))
+        assert rel(d["Q0"], Q0o) <= 1e-9, (n, rel(d["Q0"], Q0o))
+    f = s.sweep(3)
+    ref = O.cp_als_qr(X, start, 3, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+
+
+def test_high_rank_sweeps(cp):
+    """A high-rank problem (R^{N-1} R = 1.05e6 >= the 2e5 threshold, so the CholeskyQR2 V_n QR runs
+    by default): 40^4, R = 32.  Factors after one sweep <= 1e-9, fits within 1e-8 of the oracle."""
+    dims, R = (40, 40, 40, 40), 32
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=71, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_qr(X, init, 1)
+    for k in range(4):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(2)])
+    ref = O.cp_als_qr(X, init, 3)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
