@@ -1489,7 +1489,9 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   }
   {  // high rank: V_n QR by the multi-CTA CholeskyQR2 (see launch_kr_qr)
     const char* v = getenv("CPQR_VN_QR");  // "cq" / "householder" force the choice
-    c->vn_cq = v ? std::string(v) == "cq" : (J * R >= 200000);
+    // by default above R^{N-1} R = 2e5 (the one-CTA K2 dominates the sweep), and from 5e4 with the
+    // dimension tree, whose modes without an X pass cannot hide K2 (C3 tree +7.5 %)
+    c->vn_cq = v ? std::string(v) == "cq" : (J * R >= 200000 || (c->tree && J * R >= 50000));
     c->vnJ = J;
     if (c->vn_cq) {
       CK(dmalloc(&c->dVn, sizeof(double) * J * R));
