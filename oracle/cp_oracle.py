@@ -31,7 +31,8 @@ __all__ = [
     "multi_ttm", "ttm_order", "qr_pos", "kr_of_triangular", "structured_qr", "apply_q0",
     "solve_qr", "solve_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
     "fit_direct", "mode_update_qr", "mode_update_ne", "cp_als_qr", "cp_als_ne",
-    "qr_cost", "ttm_cost", "mttkrp",
+    "qr_cost", "ttm_cost", "mttkrp", "ktensor_norm2", "w_ktensor", "mttkrp_ktensor",
+    "sine_of_sums_ktensor",
 ]
 
 
@@ -233,15 +234,20 @@ def fit_fast_ne(nX2, M_N, Ahat_N, S_N, G_N, lam) -> float:
 
 
 # ----------------------------------------------------------------------- mode updates
-def mode_update_qr(X, Qs, Rs, n, variant="QR", tau=-1.0, order=None):
+def mode_update_qr(X, Qs, Rs, n, variant="QR", tau=-1.0, order=None, kt=None):
     """One CP-ALS-QR(-SVD) mode update, Alg. 2 lines 6-12, in the paper's
-    order.  Qs/Rs: factor QR cache (entry n ignored).  Returns a dict of every intermediate."""
-    N = X.ndim
+    order.  Qs/Rs: factor QR cache (entry n ignored).  kt = (lam_x, B): Kruskal input, X unused
+    (lines 8-9 by w_ktensor).  Returns a dict of every intermediate."""
+    N = X.ndim if kt is None else len(kt[1])
     V = kr_of_triangular(Rs, n)                                   # line 6  (PAPER.md:354)
     Q0, R0 = qr_pos(V)                                            # line 7  (PAPER.md:355)
-    Y = multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n},    # line 8  (PAPER.md:356)
-                  order=order)
-    W = apply_q0(Y, n, Q0)                                        # line 9  (PAPER.md:357)
+    if kt is None:
+        Y = multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n},  # line 8  (PAPER.md:356)
+                      order=order)
+        W = apply_q0(Y, n, Q0)                                    # line 9  (PAPER.md:357)
+    else:
+        Y = None
+        W = w_ktensor(kt[0], kt[1], Qs, n, Q0)                    # lines 8-9 (PAPER.md:452-456)
     ntrunc = 0
     if variant == "QR":                                           # line 10 (PAPER.md:358)
         Ahat = solve_qr(R0, W)
@@ -257,20 +263,21 @@ def mode_update_qr(X, Qs, Rs, n, variant="QR", tau=-1.0, order=None):
     flags = FLAG_ILLCOND_R0 if (variant == "QR" and d.min() <= V.shape[0] * EPS * d.max()) else 0
     if ntrunc:
         flags |= FLAG_SVD_TRUNCATED
-    return dict(V=V, Q0=Q0, R0=R0, Y=Y, Yn=matricize(Y, n), W=W, Ahat=Ahat, A=A, lam=lam,
-                Q=Qn, R=Rn, ntrunc=ntrunc, flags=flags)
+    return dict(V=V, Q0=Q0, R0=R0, Y=Y, Yn=None if Y is None else matricize(Y, n), W=W, Ahat=Ahat,
+                A=A, lam=lam, Q=Qn, R=Rn, ntrunc=ntrunc, flags=flags)
 
 
-def mode_update_ne(X, factors, grams, n):
+def mode_update_ne(X, factors, grams, n, kt=None):
     """One CP-ALS mode update, Alg. 1 lines 6-11: S_n = Hadamard of the other
     Grams; M_n = X_(n) Z_n (MTTKRP); solve Ahat S_n = M_n by Cholesky, falling back
-    to LU with partial pivoting on a non-positive pivot (reading 18); normalize; G_n = A_n^T A_n."""
-    N = X.ndim
+    to LU with partial pivoting on a non-positive pivot (reading 18); normalize; G_n = A_n^T A_n.
+    kt = (lam_x, B): Kruskal input (MTTKRP by mttkrp_ktensor)."""
+    N = len(factors)
     S = np.ones_like(grams[0])
     for k in range(N - 1, -1, -1):                                # line 6
         if k != n:
             S = hadamard(S, grams[k])
-    M = mttkrp(X, factors, n)                                     # lines 7-8
+    M = mttkrp(X, factors, n) if kt is None else mttkrp_ktensor(kt[0], kt[1], factors, n)  # lines 7-8
     flags = 0
     try:                                                          # line 9
         L = np.linalg.cholesky(S)
@@ -284,15 +291,61 @@ def mode_update_ne(X, factors, grams, n):
     return dict(S=S, M=M, Ahat=Ahat, A=A, lam=lam, G=G, flags=flags)
 
 
+# ------------------------------------------------------------ Kruskal-tensor input (§3.3.2)
+def ktensor_norm2(lam_x, B) -> float:
+    """||X||^2 of a Kruskal tensor X = [[lam_x; B_1..B_N]]: lam_x^T (B_1^T B_1 * ... * B_N^T B_N)
+    lam_x (Hadamard product of the factor Grams; PAPER.md:127-131 with Eq. (cp_mat))."""
+    G = np.ones((len(lam_x), len(lam_x)))
+    for Bk in B:
+        G = hadamard(G, Bk.T @ Bk)
+    lam_x = np.asarray(lam_x, dtype=np.float64)
+    return float(lam_x @ G @ lam_x)
+
+
+def w_ktensor(lam_x, B, Qs, n: int, Q0) -> np.ndarray:
+    """W_n = Y_(n) Q0 for a Kruskal input without forming X or Y: Y is the
+    Kruskal tensor [[lam_x; Q_1^T B_1, .., B_n, .., Q_N^T B_N]], so
+    Y_(n) = B_n diag(lam_x) (C_N (.) .. (.) C_{n+1} (.) C_{n-1} (.) .. (.) C_1)^T with C_k = Q_k^T B_k
+    (the Khatri-Rao order of the Kolda-Bader unfolding, Eq. (cp_mat)), and
+    W_n = B_n diag(lam_x) [ (.)_k C_k )^T Q0 ]."""
+    N = len(B)
+    Z = khatri_rao([Qs[k].T @ B[k] for k in range(N - 1, -1, -1) if k != n])
+    return (B[n] * np.asarray(lam_x)[None, :]) @ (Z.T @ Q0)
+
+
+def mttkrp_ktensor(lam_x, B, factors, n: int) -> np.ndarray:
+    """M_n = X_(n) Z_n for a Kruskal input (PAPER.md:446-450): B_n diag(lam_x) (*)_{k != n}
+    (B_k^T A_k), the Hadamard product of the small cross-Gram matrices."""
+    N = len(B)
+    H = np.ones((len(lam_x), factors[0].shape[1]))
+    for k in range(N - 1, -1, -1):
+        if k != n:
+            H = hadamard(H, B[k].T @ factors[k])
+    return (B[n] * np.asarray(lam_x)[None, :]) @ H
+
+
+def sine_of_sums_ktensor(N: int, n: int):
+    """The N-variable sine of sums sin(x_1 + .. + x_N) on the grid x_j = 2 pi i / n, i < n
+    (PAPER.md:597), as its exact rank-2^{N-1} Kruskal representation: expanding
+    with sin(a+b) = sin a cos b + cos a sin b, every term is a product over the modes of sin or cos
+    with an odd number k of sines and sign (-1)^((k-1)/2)."""
+    x = 2.0 * np.pi * np.arange(n) / n
+    terms = [t for t in range(1 << N) if bin(t).count("1") % 2 == 1]
+    lam = np.array([(-1.0) ** ((bin(t).count("1") - 1) // 2) for t in terms])
+    B = [np.stack([np.sin(x) if (t >> j) & 1 else np.cos(x) for t in terms], axis=1) for j in range(N)]
+    return lam, B
+
+
 # ---------------------------------------------------------------------------- drivers
 def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_sweep1=False,
-              order=None):
+              order=None, kt=None):
     """CP-ALS-QR / CP-ALS-QR-SVD, Alg. 2, exactly `sweeps` sweeps (no early
     stop; reading 12).  X: Fortran (I_1..I_N) array.  A0: initial factors (A0[0] unused,
     PAPER.md:350).  fit after mode N of every sweep (reading 13): fast or
-    direct.  Returns dict(lam, factors, fits, flags, debug)."""
-    N = X.ndim
-    nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K")))
+    direct.  kt = (lam_x, B): Kruskal input instead of X (X = None; fast fit only,
+    PAPER.md:440-456).  Returns dict(lam, factors, fits, flags, debug)."""
+    N = X.ndim if kt is None else len(kt[1])
+    nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K"))) if kt is None else ktensor_norm2(*kt)
     factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
     Qs, Rs = [None] * N, [None] * N
     for k in range(1, N):                                         # line 3 (PAPER.md:351)
@@ -303,7 +356,7 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
         last = None
         for n in range(N):                                        # line 5
             qs_in = [None if (k == n or Qs[k] is None) else Qs[k].copy() for k in range(N)] if (debug_sweep1 and s == 0) else None
-            u = mode_update_qr(X, Qs, Rs, n, variant, tau, order)
+            u = mode_update_qr(X, Qs, Rs, n, variant, tau, order, kt)
             factors[n], lam, Qs[n], Rs[n] = u["A"], u["lam"], u["Q"], u["R"]
             flags |= u["flags"]
             if debug_sweep1 and s == 0:
@@ -319,11 +372,11 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
                 nX2=nX2)
 
 
-def cp_als_ne(X, A0, sweeps, fit_mode="fast"):
+def cp_als_ne(X, A0, sweeps, fit_mode="fast", kt=None):
     """CP-ALS with normal equations, Alg. 1, exactly `sweeps` sweeps.
-    Fit: PAPER.md:417-425 (fast) or direct."""
-    N = X.ndim
-    nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K")))
+    Fit: PAPER.md:417-425 (fast) or direct.  kt = (lam_x, B): Kruskal input instead of X."""
+    N = X.ndim if kt is None else len(kt[1])
+    nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K"))) if kt is None else ktensor_norm2(*kt)
     factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
     grams = [A.T @ A for A in factors]                            # line 3 (PAPER.md:248)
     lam = np.ones(factors[0].shape[1])
@@ -331,7 +384,7 @@ def cp_als_ne(X, A0, sweeps, fit_mode="fast"):
     for s in range(sweeps):
         last = None
         for n in range(N):
-            u = mode_update_ne(X, factors, grams, n)
+            u = mode_update_ne(X, factors, grams, n, kt)
             factors[n], lam, grams[n] = u["A"], u["lam"], u["G"]
             flags |= u["flags"]
             last = u

@@ -388,3 +388,57 @@ def test_survey_dryrun_anchor_c1():
     out = O.cp_als_qr(X, init, g["sweeps"])
     assert abs(out["fits"][0] - g["fit_sweep1"]) <= 2e-10
     assert abs(out["fits"][-1] - g["fit_last"]) <= 2e-10
+
+
+# ------------------------------------------------------------ Kruskal input
+@pytest.mark.parametrize("N,n", [(3, 9), (4, 8), (5, 6)])
+def test_sine_of_sums_ktensor_closed_form(N, n):
+    """The rank-2^{N-1} representation reproduces sin(x_1 + .. + x_N) on the grid
+    x = 2 pi i / n pointwise."""
+    lam, B = O.sine_of_sums_ktensor(N, n)
+    assert len(lam) == 2 ** (N - 1) and all(b.shape == (n, 2 ** (N - 1)) for b in B)
+    X = O.full_tensor(lam, B)
+    x = 2 * np.pi * np.arange(n) / n
+    grid = np.meshgrid(*([x] * N), indexing="ij")
+    assert np.max(np.abs(X - np.sin(sum(grid)))) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,S,R", [((7, 6, 5), 3, 2), ((5, 4, 6, 3), 4, 3)])
+def test_ktensor_formulas_match_the_formed_tensor(dims, S, R):
+    """||X||^2, W_n = Y_(n) Q0 and M_n = X_(n) Z_n computed from the factors
+    equal the dense definitions on the formed tensor [[lam; B]]."""
+    rng = np.random.default_rng(13)
+    lam = rng.standard_normal(S)
+    B = [rng.standard_normal((d, S)) for d in dims]
+    X = O.full_tensor(lam, B)
+    assert abs(O.ktensor_norm2(lam, B) - float(np.sum(X * X))) <= 1e-12 * float(np.sum(X * X))
+    A = [rng.standard_normal((d, R)) for d in dims]
+    Qs = [O.qr_pos(a)[0] for a in A]
+    Rs = [O.qr_pos(a)[1] for a in A]
+    for n in range(len(dims)):
+        Q0, R0 = O.structured_qr(Rs, n)
+        Wd = O.apply_q0(O.multi_ttm(X, {k: Qs[k].T for k in range(len(dims)) if k != n}), n, Q0)
+        Wk = O.w_ktensor(lam, B, Qs, n, Q0)
+        assert np.linalg.norm(Wk - Wd) <= 1e-12 * np.linalg.norm(Wd)
+        Md = O.mttkrp(X, A, n)
+        Mk = O.mttkrp_ktensor(lam, B, A, n)
+        assert np.linalg.norm(Mk - Md) <= 1e-12 * np.linalg.norm(Md)
+
+
+@pytest.mark.parametrize("variant", ["QR", "SVD", "NE"])
+def test_ktensor_drivers_match_dense_drivers(variant):
+    """CP-ALS(-QR) on a Kruskal input (X never formed) follows the dense-input algorithm on the
+    formed tensor: same fits and factors up to rounding."""
+    lam, B = O.sine_of_sums_ktensor(4, 10)
+    X = O.full_tensor(lam, B)
+    rng = np.random.default_rng(3)
+    A0 = [rng.standard_normal((10, 4)) for _ in range(4)]
+    if variant == "NE":
+        a = O.cp_als_ne(None, A0, 3, kt=(lam, B))
+        b = O.cp_als_ne(X, A0, 3)
+    else:
+        a = O.cp_als_qr(None, A0, 3, variant=variant, kt=(lam, B))
+        b = O.cp_als_qr(X, A0, 3, variant=variant)
+    assert np.max(np.abs(np.array(a["fits"]) - np.array(b["fits"]))) <= 1e-11
+    for fa, fb in zip(a["factors"], b["factors"]):
+        assert np.linalg.norm(fa - fb) <= 1e-9 * np.linalg.norm(fb)
