@@ -101,6 +101,15 @@ cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
 cpqr_status cpqr_set_tensor(cpqr_ctx* ctx, const double* x, int64_t slab_begin,
                             int64_t slab_end, int mem);
 
+/* Kruskal-tensor input: X = [[lambda; B_1..B_N]] of rank S is never formed.
+ * B[k] is a host pointer to the column-major I_k x S matrix B_k, lambda a host S-vector (NULL:
+ * ones).  Each mode then computes W_n = B_n diag(lambda) [((.)_{k != n} Q_k^T B_k)^T Q0]
+ * (QR / SVD) or the MTTKRP B_n diag(lambda) (*)_{k != n} B_k^T A_k (NE) in O(R^N S + I_n R S),
+ * and ||X||^2 = lambda^T ((*)_k B_k^T B_k) lambda.  Replaces a dense tensor set before (and
+ * cpqr_set_tensor replaces this).  The arrays are copied before return.  Single GPU (world = 1),
+ * FAST fit only; cpqr_debug_mode is unavailable.  Errors: EINVAL, ENOMEM, ECUDA. */
+cpqr_status cpqr_set_ktensor(cpqr_ctx* ctx, int S, const double* lambda, const double* const* B);
+
 /* Set the factors: A[k] is a host pointer to the column-major I_k x R matrix A_k (k = 0..N-1;
  * A[0] may be NULL for the QR/SVD variants: Alg. 2 line 2 initialises A_2..A_N only).
  * lambda: host R-vector or NULL (ones).  Must be identical on all ranks.  Recomputes the factor

@@ -29,7 +29,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE"
 
 EXPORTS = [
     "cpqr_default_options", "cpqr_create", "cpqr_set_tensor", "cpqr_set_factors", "cpqr_init_factors",
-    "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile",
+    "cpqr_set_ktensor", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile",
     "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_qr", "cpqr_debug_svd_solve",
     "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
 ]
@@ -53,6 +53,7 @@ _sig = {
     "cpqr_default_options": (None, [C.POINTER(Options)]),
     "cpqr_create": (C.c_int32, [C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_int, C.POINTER(Options), C.POINTER(_P)]),
     "cpqr_set_tensor": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.c_int64, C.c_int]),
+    "cpqr_set_ktensor": (C.c_int32, [_P, C.c_int, _DP, C.POINTER(_DP)]),
     "cpqr_set_factors": (C.c_int32, [_P, C.POINTER(_DP), _DP]),
     "cpqr_init_factors": (C.c_int32, [_P, C.c_uint64]),
     "cpqr_sweep": (C.c_int32, [_P, C.c_int, _DP]),
@@ -166,6 +167,14 @@ class CPQR:
             mem, ptr = MEM_HOST, C.c_void_p(X.ctypes.data)
         self._check(_lib.cpqr_set_tensor(self._h, ptr, b, e, mem))
         self._x_ref = X if mem == MEM_DEVICE_BORROW else None
+
+    def set_ktensor(self, lam, B):
+        """Kruskal-tensor input X = [[lam; B_1..B_N]]: B[k] is I_k x S."""
+        arrs = [np.asfortranarray(np.asarray(b, dtype=np.float64)) for b in B]
+        S = arrs[0].shape[1]
+        ptrs = (_DP * self.N)(*[_dptr(a) for a in arrs])
+        lam = None if lam is None else np.ascontiguousarray(lam, dtype=np.float64)
+        self._check(_lib.cpqr_set_ktensor(self._h, int(S), _dptr(lam) if lam is not None else _DP(), ptrs))
 
     def set_factors(self, factors, lam=None):
         arrs = [None if A is None else np.asfortranarray(np.asarray(A, dtype=np.float64)) for A in factors]

@@ -8,6 +8,7 @@
 #include "small_kernels.cuh"
 #include "tma_kernels.cuh"
 #include "ttm_kernels.cuh"
+#include "ktensor_kernels.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -94,6 +95,13 @@ struct cpqr_ctx {
   bool use_tma = true;
   bool fuse_slice = true;  // see plan_mode
   bool pinv_ready = false; // M = pinv(R0) already launched for this mode (side stream, after K2)
+  bool kt = false;         // Kruskal-tensor input (cpqr_set_ktensor): X never formed
+  int ktS = 0;
+  double* dKtLam = nullptr;
+  double* dKtB[kMaxN] = {nullptr};
+  double* dKtC = nullptr;  // cross products C_k (N blocks of up to max(R,S)^2)
+  double* dKtM = nullptr;  // S x R
+  size_t ktC_elems = 0;
   bool vn_cq = false;      // V_n QR by multi-CTA CholeskyQR2 (high rank), k_kr_qr2 as fallback
   int64_t vnJ = 0;         // R^{N-1}
   double *dVn = nullptr, *dVq1 = nullptr, *dVgp = nullptr, *dVr1 = nullptr, *dVr2 = nullptr;
@@ -1126,6 +1134,25 @@ cpqr_status combine_w(cpqr_ctx* c, int n, double* Wloc, double* Wfull) {
   return CPQR_OK;
 }
 
+// out_k = P_k^T B_k for the listed modes (k_kt_cross)
+cpqr_status kt_cross(cpqr_ctx* c, const int* modes, int K, const double* const* P, int np,
+                            const double* const* B, int nb, double* out) {
+  KtCrossArgs a{};
+  for (int i = 0; i < K; ++i) {
+    a.P[i] = P[modes[i]];
+    a.B[i] = B[modes[i]];
+    a.I[i] = c->dims[modes[i]];
+  }
+  a.K = K;
+  a.np = np;
+  a.nb = nb;
+  a.out = out;
+  const int64_t warps = (int64_t)K * np * nb;
+  k_kt_cross<<<(int)((warps * 32 + 255) / 256), 256, 0, c->st>>>(a);
+  CKL();
+  return CPQR_OK;
+}
+
 cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   const Plan& p = c->plans[n];
   const int N = c->N;
@@ -1133,10 +1160,26 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   const int In = (int)c->dims[n];
   if (c->variant == CPQR_NE) {
     prof_mark(c, 0);
-    TRY(run_plan(c, p));
+    double* Mloc;
+    int m_rowmajor = p.m_rowmajor;
+    if (c->kt) {  // Kruskal input: M_n = B_n diag(lam_x) (*)_{k != n} B_k^T A_k
+      int modes[kMaxN], K = 0;
+      for (int k = 0; k < N; ++k) if (k != n) modes[K++] = k;
+      const double* Ac[kMaxN];
+      const double* Bc[kMaxN];
+      for (int k = 0; k < N; ++k) { Ac[k] = c->dA[k]; Bc[k] = c->dKtB[k]; }
+      TRY(kt_cross(c, modes, K, Bc, c->ktS, Ac, c->R, c->dKtC));
+      const int grid = (int)std::min<int64_t>(((int64_t)In * c->R + 255) / 256, (int64_t)c->sms * 8);
+      k_kt_mttkrp<<<grid, 256, 0, c->st>>>(c->dKtB[n], In, c->ktS, c->dKtLam, c->dKtC, K, c->R, c->dW);
+      CKL();
+      Mloc = c->dW;
+      m_rowmajor = 1;
+    } else {
+      TRY(run_plan(c, p));
+      Mloc = const_cast<double*>(p.Y);
+    }
     prof_mark(c, 2);
     // M for the tail must be row-major complete; combine per-rank results
-    double* Mloc = const_cast<double*>(p.Y);
     const double* Mfull = Mloc;
     if (c->opt.world > 1) {
       if (!p.m_rowmajor) return fail(c, CPQR_EINVAL, "NE multi-GPU needs row-major M");
@@ -1145,7 +1188,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     }
     TailNeArgs a{};
     a.M = Mfull;
-    a.m_rowmajor = p.m_rowmajor;
+    a.m_rowmajor = m_rowmajor;
     for (int k = 0; k < N; ++k) a.G[k] = c->dG[k];
     a.N = N;
     a.n = n;
@@ -1198,8 +1241,17 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   if (fork) CK(cudaEventRecord(c->evj, c->side));
   prof_mark(c, 1);
   // line 8: Multi-TTM (first step = the stream-X pass; with the dimension tree only the first mode
-  // of each half has one)
-  {
+  // of each half has one).  Kruskal input: C_k = Q_k^T B_k, then W_n below
+  if (c->kt) {
+    int modes[kMaxN], K = 0;
+    for (int k = 0; k < N; ++k) if (k != n) modes[K++] = k;
+    const double* Qc[kMaxN];
+    const double* Bc[kMaxN];
+    for (int k = 0; k < N; ++k) { Qc[k] = c->dQ[k]; Bc[k] = c->dKtB[k]; }
+    TRY(kt_cross(c, modes, K, Qc, c->R, Bc, c->ktS, c->dKtC));
+    prof_mark(c, 2);
+    prof_mark(c, 3);
+  } else {
     const size_t nx = (!p.steps.empty() && p.steps[0].in == c->X) ? 1 : 0;
     Plan first;
     first.steps.assign(p.steps.begin(), p.steps.begin() + nx);
@@ -1212,9 +1264,23 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   }
   if (fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
   // line 9: W_n = Y_(n) Q0 (local rows); combine across ranks
-  double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
-  TRY(launch_q0_apply(c, p, Wloc));
-  TRY(combine_w(c, n, Wloc, c->dW));
+  if (c->kt) {  // W_n = B_n diag(lam_x) [((.)_k C_k)^T Q0]
+    int64_t J = 1;
+    for (int k = 0; k < N - 1; ++k) J *= c->R;
+    switch (rb_for(c->R)) {
+      case 8: k_kt_m<8><<<c->ktS, 256, 0, c->st>>>(c->dKtC, N - 1, c->R, c->ktS, J, c->dQ0, c->dKtM); break;
+      case 16: k_kt_m<16><<<c->ktS, 256, 0, c->st>>>(c->dKtC, N - 1, c->R, c->ktS, J, c->dQ0, c->dKtM); break;
+      default: k_kt_m<32><<<c->ktS, 256, 0, c->st>>>(c->dKtC, N - 1, c->R, c->ktS, J, c->dQ0, c->dKtM); break;
+    }
+    CKL();
+    const int grid = (int)std::min<int64_t>(((int64_t)In * c->R + 255) / 256, (int64_t)c->sms * 8);
+    k_kt_w<<<grid, 256, 0, c->st>>>(c->dKtB[n], In, c->ktS, c->dKtLam, c->dKtM, c->R, c->dW);
+    CKL();
+  } else {
+    double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
+    TRY(launch_q0_apply(c, p, Wloc));
+    TRY(combine_w(c, n, Wloc, c->dW));
+  }
   prof_mark(c, 4);
   // lines 10-12: solve (substitution / SVD), lambda, normalise, factor QR (+ fast fit after mode N)
   const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
@@ -1530,6 +1596,10 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->dperm) cudaFree(c->dperm);
   if (c->dflags) cudaFree(c->dflags);
   if (c->dq0cnt) cudaFree(c->dq0cnt);
+  for (int k = 0; k < kMaxN; ++k) if (c->dKtB[k]) cudaFree(c->dKtB[k]);
+  if (c->dKtLam) cudaFree(c->dKtLam);
+  if (c->dKtM) cudaFree(c->dKtM);
+  if (c->dKtC) cudaFree(c->dKtC);
   if (c->dTree) cudaFree(c->dTree);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1569,8 +1639,49 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
   CKL();
   if (c->opt.world > 1) CN(ncclAllReduce(c->dnX2, c->dnX2, 1, ncclDouble, ncclSum, c->comm, c->st));
   c->have_tensor = true;
+  c->kt = false;
   c->graph_valid = false;
   TRY(build_plans(c));
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_set_ktensor(cpqr_ctx* c, int S, const double* lam, const double* const* B) {
+  if (!c || !B || S < 1) return c ? fail(c, CPQR_EINVAL, "Kruskal input: S >= 1 and B required") : CPQR_EINVAL;
+  if (c->opt.world > 1) return fail(c, CPQR_EINVAL, "Kruskal input is single-GPU (the factors are replicated)");
+  if (c->opt.fit_mode != CPQR_FIT_FAST) return fail(c, CPQR_EINVAL, "Kruskal input supports the FAST fit only");
+  for (int k = 0; k < c->N; ++k)
+    if (!B[k]) return fail(c, CPQR_EINVAL, "B[%d] is NULL", k);
+  TRY(begin_call(c));
+  const int N = c->N, R = c->R;
+  if (S != c->ktS) {
+    for (int k = 0; k < N; ++k) { if (c->dKtB[k]) cudaFree(c->dKtB[k]); c->dKtB[k] = nullptr; }
+    if (c->dKtLam) cudaFree(c->dKtLam);
+    if (c->dKtM) cudaFree(c->dKtM);
+    if (c->dKtC) cudaFree(c->dKtC);
+    c->dKtLam = c->dKtM = c->dKtC = nullptr;
+    for (int k = 0; k < N; ++k) CK(dmalloc(&c->dKtB[k], sizeof(double) * c->dims[k] * S));
+    CK(dmalloc(&c->dKtLam, sizeof(double) * S));
+    CK(dmalloc(&c->dKtM, sizeof(double) * S * R));
+    const int mx = std::max(R, S);
+    c->ktC_elems = (size_t)N * mx * mx;
+    CK(dmalloc(&c->dKtC, sizeof(double) * c->ktC_elems));
+    c->ktS = S;
+  }
+  for (int k = 0; k < N; ++k)
+    CK(cudaMemcpyAsync(c->dKtB[k], B[k], sizeof(double) * c->dims[k] * S, cudaMemcpyHostToDevice, c->st));
+  std::vector<double> ones(S, 1.0);
+  CK(cudaMemcpyAsync(c->dKtLam, lam ? lam : ones.data(), sizeof(double) * S, cudaMemcpyHostToDevice, c->st));
+  int modes[kMaxN];
+  for (int k = 0; k < N; ++k) modes[k] = k;
+  const double* Bc[kMaxN];
+  for (int k = 0; k < N; ++k) Bc[k] = c->dKtB[k];
+  TRY(kt_cross(c, modes, N, Bc, S, Bc, S, c->dKtC));  // G_k = B_k^T B_k
+  k_kt_norm2<<<1, 256, 0, c->st>>>(c->dKtC, N, S, c->dKtLam, c->dnX2);
+  CKL();
+  CK(cudaStreamSynchronize(c->st));  // the host arrays may go away after return
+  c->have_tensor = true;
+  c->kt = true;
+  c->graph_valid = false;
   return end_call(c);
 }
 
@@ -1736,6 +1847,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   if (n < 0 || n >= c->N) return fail(c, CPQR_EINVAL, "mode %d", n);
   if (!c->have_tensor || !c->have_factors) return fail(c, CPQR_ESTATE, "tensor/factors not set");
   if (c->variant == CPQR_NE) return fail(c, CPQR_EINVAL, "debug_mode is for the QR/SVD variants");
+  if (c->kt) return fail(c, CPQR_EINVAL, "debug_mode needs a dense tensor (Kruskal input forms no Y)");
   TRY(begin_call(c));
   const int R = c->R, N = c->N;
   std::vector<double*> tmpQ(N, nullptr), tmpQt(N, nullptr);

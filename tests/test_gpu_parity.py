@@ -478,3 +478,58 @@ def test_high_rank_sweeps(cp):
     ref = O.cp_als_qr(X, init, 3)
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
     s.close()
+
+
+@pytest.mark.parametrize("N,n,R,variant", [(4, 16, 4, "QR"), (4, 16, 4, "SVD"), (4, 16, 4, "NE"),
+                                           (5, 8, 5, "QR"), (3, 40, 3, "QR")])
+def test_kruskal_input(cp, N, n, R, variant):
+    """Kruskal-tensor input: the sine-of-sums tensor
+    (rank 2^{N-1}) or a random rank-5 Kruskal tensor (N = 3), never formed on the
+    GPU.  Factors after one sweep <= 1e-9 and fits within 1e-8 of the oracle's Kruskal drivers,
+    which are pinned to the dense algorithm on the formed tensor; also equal to the GPU's own
+    dense path on the formed tensor."""
+    if N == 3:
+        rng = np.random.default_rng(41)
+        lam_x, B = rng.standard_normal(5), [rng.standard_normal((n, 5)) for _ in range(N)]
+    else:
+        lam_x, B = O.sine_of_sums_ktensor(N, n)
+    rng = np.random.default_rng(9)
+    A0 = [rng.standard_normal((n, R)) for _ in range(N)]
+    dims = (n,) * N
+    s = cp.CPQR(dims, R, variant)
+    s.set_ktensor(lam_x, B)
+    s.set_factors(A0)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    if variant == "NE":
+        ref1, ref = O.cp_als_ne(None, A0, 1, kt=(lam_x, B)), O.cp_als_ne(None, A0, 4, kt=(lam_x, B))
+    else:
+        ref1 = O.cp_als_qr(None, A0, 1, variant=variant, kt=(lam_x, B))
+        ref = O.cp_als_qr(None, A0, 4, variant=variant, kt=(lam_x, B))
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(3)])
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+    # the GPU's dense path on the formed tensor follows the same trajectory
+    Xf = O.full_tensor(lam_x, B)
+    sd = cp.CPQR(dims, R, variant)
+    sd.set_tensor(np.ascontiguousarray(np.transpose(Xf)))
+    sd.set_factors(A0)
+    fd = sd.sweep(4)
+    sd.close()
+    assert np.max(np.abs(fd - f)) <= 1e-9
+
+
+def test_kruskal_input_errors(cp):
+    lam_x, B = O.sine_of_sums_ktensor(4, 8)
+    s = cp.CPQR((8,) * 4, 3, "QR")
+    s.set_ktensor(lam_x, B)
+    s.set_factors([np.eye(8)[:, :3]] * 4)
+    with pytest.raises(cp.CpqrError):
+        s.debug_mode(0)
+    s.close()
+    s = cp.CPQR((8,) * 4, 3, "QR", fit_mode="direct")
+    with pytest.raises(cp.CpqrError):
+        s.set_ktensor(lam_x, B)
+    s.close()
