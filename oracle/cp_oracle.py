@@ -32,7 +32,7 @@ __all__ = [
     "solve_qr", "solve_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
     "fit_direct", "mode_update_qr", "mode_update_ne", "cp_als_qr", "cp_als_ne",
     "qr_cost", "ttm_cost", "mttkrp", "ktensor_norm2", "w_ktensor", "mttkrp_ktensor",
-    "sine_of_sums_ktensor",
+    "sine_of_sums_ktensor", "score",
 ]
 
 
@@ -334,6 +334,35 @@ def sine_of_sums_ktensor(N: int, n: int):
     lam = np.array([(-1.0) ** ((bin(t).count("1") - 1) // 2) for t in terms])
     B = [np.stack([np.sin(x) if (t >> j) & 1 else np.cos(x) for t in terms], axis=1) for j in range(N)]
     return lam, B
+
+
+# ------------------------------------------------------------------- score (§4.2)
+def score(lam_a, A, lam_b, B) -> float:
+    """Similarity of two rank-R Kruskal tensors up to scaling and permutation, in [0, 1]
+    (the score of the cited Tomasi-Bro comparison; reading 30): columns
+    normalised (norms folded into the weights); for a permutation p of the components
+    score_p = (1/R) sum_r (1 - |l_r - m_p(r)| / max(l_r, m_p(r))) prod_k |a_r^(k) . b_p(r)^(k)|,
+    and the score is the maximum over all permutations (exhaustive; R <= 8)."""
+    import itertools
+    N = len(A)
+    R = A[0].shape[1]
+    la = np.abs(np.asarray(lam_a, dtype=np.float64)).copy()
+    lb = np.abs(np.asarray(lam_b, dtype=np.float64)).copy()
+    An, Bn = [], []
+    for k in range(N):
+        na = np.linalg.norm(A[k], axis=0)
+        nb = np.linalg.norm(B[k], axis=0)
+        la *= na
+        lb *= nb
+        An.append(A[k] / np.where(na > 0, na, 1.0))
+        Bn.append(B[k] / np.where(nb > 0, nb, 1.0))
+    cong = np.ones((R, R))
+    for k in range(N):
+        cong *= np.abs(An[k].T @ Bn[k])                  # cong[r, q] = prod_k |a_r . b_q|
+    den = np.maximum(la[:, None], lb[None, :])
+    pen = 1.0 - np.abs(la[:, None] - lb[None, :]) / np.where(den > 0, den, 1.0)
+    S = pen * cong
+    return float(max(np.mean(S[np.arange(R), list(p)]) for p in itertools.permutations(range(R))))
 
 
 # ---------------------------------------------------------------------------- drivers

@@ -442,3 +442,23 @@ def test_ktensor_drivers_match_dense_drivers(variant):
     assert np.max(np.abs(np.array(a["fits"]) - np.array(b["fits"]))) <= 1e-11
     for fa, fb in zip(a["factors"], b["factors"]):
         assert np.linalg.norm(fa - fb) <= 1e-9 * np.linalg.norm(fb)
+
+
+# ------------------------------------------------------------------- score
+def test_score_limits_and_invariances():
+    """1 for equal Kruskal tensors, invariant to component permutation, column scaling (folded
+    into the weights) and sign flips; 0 when the components are orthogonal in one mode; the
+    weight penalty alone for equal directions with weights 1 vs 2."""
+    rng = np.random.default_rng(5)
+    R = 4
+    A = [rng.standard_normal((d, R)) for d in (6, 7, 8)]
+    lam = rng.uniform(1, 2, R)
+    assert abs(O.score(lam, A, lam, A) - 1.0) <= 1e-14
+    p = [2, 0, 3, 1]
+    d = np.array([2.0, -1.0, 0.5, -3.0])       # per-component scale (and sign) in every mode
+    B = [a[:, p] * d for a in A]
+    assert abs(O.score(lam, A, lam[p] / np.abs(d) ** 3, B) - 1.0) <= 1e-12
+    E = [np.eye(8)[:6, :R], np.eye(8)[:7, :R], np.eye(8)[:, :R]]
+    Fo = [np.vstack([np.zeros((4, R)), np.ones((2, R))]), E[1], E[2]]  # mode-1 columns orthogonal to E's
+    assert O.score(np.ones(R), E, np.ones(R), Fo) <= 1e-14
+    assert abs(O.score(np.ones(R), E, 2.0 * np.ones(R), E) - 0.5) <= 1e-14
