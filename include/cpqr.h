@@ -60,7 +60,10 @@ typedef enum {
 enum {
   CPQR_FLAG_ILLCOND_R0 = 1u,      /* QR variant: min|R0_jj| <= R^(N-1)*eps*max|R0_jj| (reading 17) */
   CPQR_FLAG_NE_CHOL_FALLBACK = 2u,/* NE: Cholesky met a non-positive pivot; LU used (reading 18) */
-  CPQR_FLAG_SVD_TRUNCATED = 4u    /* SVD variant: at least one sigma_i <= tau*sigma_max dropped */
+  CPQR_FLAG_SVD_TRUNCATED = 4u,   /* SVD variant: at least one sigma_i <= tau*sigma_max dropped */
+  CPQR_FLAG_NE_ILLCOND = 8u       /* NE: kappa(S_n) estimate (max/min Cholesky pivot)^2 > 1e8: the
+                                     normal equations lose > 8 digits; a robust driver switches to
+                                     QR / QR-SVD */
 };
 
 typedef struct cpqr_options {

@@ -24,7 +24,7 @@ NE, QR, SVD = 0, 1, 2
 VARIANTS = {"NE": NE, "QR": QR, "SVD": SVD}
 FIT_FAST, FIT_DIRECT = 0, 1
 MEM_HOST, MEM_DEVICE_COPY, MEM_DEVICE_BORROW = 0, 1, 2
-FLAG_ILLCOND_R0, FLAG_NE_CHOL_FALLBACK, FLAG_SVD_TRUNCATED = 1, 2, 4
+FLAG_ILLCOND_R0, FLAG_NE_CHOL_FALLBACK, FLAG_SVD_TRUNCATED, FLAG_NE_ILLCOND = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE", 6: "EDIVERGED"}
 
 EXPORTS = [

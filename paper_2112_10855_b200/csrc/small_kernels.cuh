@@ -21,7 +21,10 @@ namespace cpqr {
 constexpr double kEps = 2.220446049250313e-16;
 
 enum : unsigned { FLAG_ILLCOND_R0 = 1u, FLAG_NE_CHOL_FALLBACK = 2u, FLAG_SVD_TRUNCATED = 4u,
-                  FLAG_NONFINITE = 0x100u };
+                  FLAG_NE_ILLCOND = 8u, FLAG_NONFINITE = 0x100u };
+// NE: kappa(S_n) estimated as (max L_jj / min L_jj)^2 from the Cholesky factor; above this the
+// normal equations lose more than ~8 of 16 digits (switch to QR when detected)
+constexpr double kNeKappaMax = 1.0e8;
 
 // ------------------------------------------------------------------------------ sum of squares
 __global__ void k_sumsq_partial(const double* __restrict__ X, int64_t n, double* __restrict__ part) {
@@ -441,6 +444,11 @@ __global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
       __syncwarp();
       if (lane == 0) L[j + RB * j] = d;
       __syncwarp();
+    }
+    if (!use_lu && lane == 0) {  // ill-conditioning estimate (robust-policy hook)
+      double dmax = 0.0, dmin = 1e308;
+      for (int j = 0; j < R; ++j) { dmax = fmax(dmax, L[j + RB * j]); dmin = fmin(dmin, L[j + RB * j]); }
+      if (!(dmin > 0.0) || (dmax / dmin) * (dmax / dmin) > kNeKappaMax) atomicOr(a.flags, FLAG_NE_ILLCOND);
     }
   }
   __syncthreads();
