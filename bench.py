@@ -92,6 +92,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "source": "NVML, 5 ms"}
 
 
+METRIC = "CP-ALS-QR sweeps/s & Multi-TTM HBM GB/s (fp64)"
+
+
+def bench_config(conf, variant, world, tree):
+    """The `config` object of both arms (identical keys and values)."""
+    numel_local = int(np.prod(conf.dims)) // world
+    return {"workload": conf.name, "variant": variant, "dims": list(conf.dims), "R": conf.R,
+            "global_batch": 1, "parallelism": f"slab-dp{world} on mode {conf.N}",
+            "multittm": "dimension tree (2 passes over X per sweep)" if tree else
+                        "per mode (one pass over X per mode, Alg. 2 line 8)",
+            "l2": ("inputs larger than L2 (X = %.2f GB/GPU vs 126 MB L2), no flush needed" % (8.0 * numel_local / 1e9))
+                  if 8.0 * numel_local > 126e6 else
+                  ("X = %.2f MB/GPU fits in L2: a launch-latency-bound config, timed warm" % (8.0 * numel_local / 1e6))}
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
@@ -144,12 +159,11 @@ def run_reference(args):
     run(A0, args.steps)
     dt = time.perf_counter() - t0
     v = args.steps / dt
-    line = {"impl": "reference", "metric": "CP-ALS-QR sweeps/s (fp64)", "value": v, "unit": "sweeps/s",
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "sweeps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (synth.py recipe, seeded)",
-            "config": {"workload": conf.name, "variant": variant, "dims": list(conf.dims), "R": conf.R,
-                       "sweeps_per_step": 1, "parallelism": "host cores"},
+            "data": "synthetic (synth.py seeded recipe of BASELINE.json config; no dataset)",
+            "config": bench_config(conf, variant, world, bool(args.tree and variant != "NE" and conf.N >= 3)),
             "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} full sweeps of {conf.name} after {args.warmup} warm-up"},
             "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -296,16 +310,12 @@ def main():
     # X read once per mode; twice per sweep with the dimension tree
     mt_bytes_sweep = (2 if tree else conf.N) * 8.0 * numel_local
     line = {
-        "metric": "CP-ALS-QR sweeps/s & Multi-TTM HBM GB/s (fp64)",
+        "metric": METRIC,
         "value": sweeps_s * 1.0, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (synth.py seeded recipe of BASELINE.json config; no dataset)",
-        "config": {"workload": conf.name, "variant": variant, "dims": list(conf.dims), "R": conf.R,
-                   "global_batch": 1, "parallelism": f"slab-dp{world} on mode {conf.N}",
-                   "multittm": "dimension tree (2 passes over X per sweep)" if tree else
-                               "per mode (one pass over X per mode, Alg. 2 line 8)",
-                   "l2": "inputs larger than L2 (X = %.2f GB/GPU vs 126 MB L2)" % (8.0 * numel_local / 1e9)},
+        "config": bench_config(conf, variant, world, tree),
         "gpu_launches": int(launches),
     }
     if prof:
