@@ -104,6 +104,19 @@ cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
 cpqr_status cpqr_set_tensor(cpqr_ctx* ctx, const double* x, int64_t slab_begin,
                             int64_t slab_end, int mem);
 
+/* Batched CP-ALS-QR of P independent small 3-way problems, one CTA per problem (SURVEY.md 8(f)
+ * NEXT-4; the collinear-factor study's regime).  Stateless: all pointers are
+ * DEVICE pointers, launched on `stream` (NULL: default stream), asynchronous.
+ *   dims[3] = I_1, I_2, I_3 (R <= I_k <= 64), 1 <= R <= 8, I_1 I_2 R <= 16384, I_2 I_3 R <= 16384.
+ *   X: P consecutive column-major I_1 x I_2 x I_3 tensors.  A0 / A: P blocks of the three factors
+ *   (I_1 x R, I_2 x R, I_3 x R column-major, consecutive); A0[mode 1] is unused (Alg. 2 line 2).
+ *   Each CTA runs QR-variant sweeps until the fit changes by less than tol or
+ *   max_iters sweeps; fits: P x max_iters (NaN after the last sweep), iters: P, lam: P x R.
+ * Errors: EINVAL (shapes / NULL), ECUDA (launch). */
+cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const double* X, const double* A0,
+                            int max_iters, double tol, double* A, double* lam, double* fits,
+                            int* iters, void* stream);
+
 /* Kruskal-tensor input: X = [[lambda; B_1..B_N]] of rank S is never formed.
  * B[k] is a host pointer to the column-major I_k x S matrix B_k, lambda a host S-vector (NULL:
  * ones).  Each mode then computes W_n = B_n diag(lambda) [((.)_{k != n} Q_k^T B_k)^T Q0]

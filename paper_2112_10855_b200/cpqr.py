@@ -29,7 +29,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE"
 
 EXPORTS = [
     "cpqr_default_options", "cpqr_create", "cpqr_set_tensor", "cpqr_set_factors", "cpqr_init_factors",
-    "cpqr_set_ktensor", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile",
+    "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile",
     "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_qr", "cpqr_debug_svd_solve",
     "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
 ]
@@ -54,6 +54,8 @@ _sig = {
     "cpqr_create": (C.c_int32, [C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_int, C.POINTER(Options), C.POINTER(_P)]),
     "cpqr_set_tensor": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.c_int64, C.c_int]),
     "cpqr_set_ktensor": (C.c_int32, [_P, C.c_int, _DP, C.POINTER(_DP)]),
+    "cpqr_batched_qr": (C.c_int32, [C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                    C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cpqr_set_factors": (C.c_int32, [_P, C.POINTER(_DP), _DP]),
     "cpqr_init_factors": (C.c_int32, [_P, C.c_uint64]),
     "cpqr_sweep": (C.c_int32, [_P, C.c_int, _DP]),
@@ -97,6 +99,33 @@ def nccl_unique_id() -> bytes:
 
 def _dptr(a: np.ndarray):
     return a.ctypes.data_as(_DP)
+
+
+def batched_qr(X, A0, R, max_iters=500, tol=1e-15, stream=None):
+    """Batched CP-ALS-QR, one CTA per problem (cpqr_batched_qr).  X: CUDA float64 tensor
+    (P, I_3, I_2, I_1) C-contiguous (= P column-major tensors); A0: list of three CUDA float64
+    tensors (P, R, I_k) C-contiguous (= column-major I_k x R per problem).  Returns (A, lam, fits,
+    iters) as CUDA tensors: A a list of (P, R, I_k), lam (P, R), fits (P, max_iters), iters (P,)."""
+    import torch
+    P, I3, I2, I1 = X.shape
+    dims = (C.c_int64 * 3)(I1, I2, I3)
+    dev = X.device
+    A0cat = torch.cat([a.reshape(P, -1) for a in A0], dim=1).contiguous()
+    Aout = torch.empty_like(A0cat)
+    lam = torch.empty((P, R), dtype=torch.float64, device=dev)
+    fits = torch.empty((P, max_iters), dtype=torch.float64, device=dev)
+    iters = torch.empty((P,), dtype=torch.int32, device=dev)
+    st = _lib.cpqr_batched_qr(P, dims, int(R), C.c_void_p(X.data_ptr()), C.c_void_p(A0cat.data_ptr()),
+                              int(max_iters), float(tol), C.c_void_p(Aout.data_ptr()), C.c_void_p(lam.data_ptr()),
+                              C.c_void_p(fits.data_ptr()), C.c_void_p(iters.data_ptr()),
+                              C.c_void_p(int(stream)) if stream else None)
+    if st:
+        raise CpqrError(st, "cpqr_batched_qr failed")
+    out, o = [], 0
+    for I in (I1, I2, I3):
+        out.append(Aout[:, o:o + I * R].reshape(P, R, I))
+        o += I * R
+    return out, lam, fits, iters
 
 
 class CPQR:

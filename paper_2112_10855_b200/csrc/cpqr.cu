@@ -9,6 +9,7 @@
 #include "tma_kernels.cuh"
 #include "ttm_kernels.cuh"
 #include "ktensor_kernels.cuh"
+#include "batched_kernels.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -1643,6 +1644,26 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
   c->graph_valid = false;
   TRY(build_plans(c));
   return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const double* X, const double* A0,
+                                     int max_iters, double tol, double* A, double* lam, double* fits,
+                                     int* iters, void* stream) {
+  if (P < 0 || !dims || !X || !A0 || !A || !lam || !fits || !iters || max_iters < 1) return CPQR_EINVAL;
+  if (R < 1 || R > kBatMaxR) return CPQR_EINVAL;
+  for (int k = 0; k < 3; ++k)
+    if (dims[k] < R || dims[k] > kBatMaxI) return CPQR_EINVAL;
+  if (dims[0] * dims[1] * R > kBatTBuf || dims[1] * dims[2] * R > kBatTBuf || R * R > kBatMaxI) return CPQR_EINVAL;
+  if (P == 0) return CPQR_OK;
+  BatchedArgs a{};
+  a.X = X; a.A0 = A0; a.R = R; a.max_iters = max_iters; a.tol = tol;
+  for (int k = 0; k < 3; ++k) a.I[k] = (int)dims[k];
+  a.A = A; a.lam = lam; a.fits = fits; a.iters = iters;
+  const size_t smem = (size_t)(kBatTBuf + 64 * 64 + 3 * 64 * 8 + 3 * 64 + 64 * 8 + 64 + 2 * 64 * 8) * sizeof(double);
+  if (cudaFuncSetAttribute(k_batched_cpqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return CPQR_ECUDA;
+  k_batched_cpqr<<<P, 256, smem, (cudaStream_t)stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? CPQR_OK : CPQR_ECUDA;
 }
 
 CPQR_API cpqr_status cpqr_set_ktensor(cpqr_ctx* c, int S, const double* lam, const double* const* B) {

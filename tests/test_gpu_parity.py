@@ -533,3 +533,54 @@ def test_kruskal_input_errors(cp):
     with pytest.raises(cp.CpqrError):
         s.set_ktensor(lam_x, B)
     s.close()
+
+
+def _batched_inputs(dims, R, seeds, **kw):
+    import torch
+    Xs, A0s, truths = [], [], []
+    for sd in seeds:
+        conf, Xc, truth, init = synth.small_problem(dims, R, seed=sd, **kw)
+        Xs.append(Xc)
+        A0s.append(init)
+        truths.append(truth)
+    X = torch.from_numpy(np.stack(Xs)).cuda()
+    A0 = [torch.from_numpy(np.stack([np.ascontiguousarray(a[k].T) for a in A0s])).cuda() for k in range(3)]
+    return Xs, A0s, X, A0
+
+
+@pytest.mark.parametrize("dims,R,kw", [((20, 18, 16), 3, dict(eta=0.05)),
+                                       ((12, 14, 10), 5, dict(eta=1e-3, kind="congruence", c=0.99))])
+def test_batched_one_cta_per_problem(cp, dims, R, kw):
+    """cpqr_batched_qr: each CTA runs a whole CP-ALS-QR solve.  With tol = 0
+    it runs exactly max_iters sweeps: factors and lambda after 1 sweep <= 1e-9, fits within 1e-8
+    of the oracle for every sweep, for every problem of the batch."""
+    seeds = [101, 102, 103, 104, 105, 106]
+    Xs, A0s, X, A0 = _batched_inputs(dims, R, seeds, **kw)
+    for sweeps in (1, 6):
+        A, lam, fits, iters = cp.batched_qr(X, A0, R, max_iters=sweeps, tol=0.0)
+        A = [a.cpu().numpy() for a in A]
+        lam, fits, iters = lam.cpu().numpy(), fits.cpu().numpy(), iters.cpu().numpy()
+        assert np.all(iters == sweeps)
+        for p in range(len(seeds)):
+            ref = O.cp_als_qr(O.as_tensor(Xs[p]), A0s[p], sweeps)
+            assert np.max(np.abs(fits[p] - np.array(ref["fits"]))) <= 1e-8, (p, fits[p], ref["fits"])
+            if sweeps == 1:
+                for k in range(3):
+                    assert rel(A[k][p].T, ref["factors"][k]) <= 1e-9, (p, k)
+                assert rel(lam[p], ref["lam"]) <= 1e-9
+
+
+def test_batched_stopping_rule_and_paper_shape(cp):
+    """tol > 0: a problem stops at the first sweep whose fit change is below tol (NaN afterwards);
+    the paper's 50^3 rank-5 shape runs and matches the oracle's fits."""
+    Xs, A0s, X, A0 = _batched_inputs((50, 50, 50), 5, [201, 202], eta=1e-4)
+    A, lam, fits, iters = cp.batched_qr(X, A0, 5, max_iters=40, tol=1e-9)
+    fits, iters = fits.cpu().numpy(), iters.cpu().numpy()
+    for p in range(2):
+        k = int(iters[p])
+        f = fits[p, :k]
+        assert np.all(np.isnan(fits[p, k:]))
+        if k < 40:
+            assert abs(f[-1] - f[-2]) < 1e-9 and np.all(np.abs(np.diff(f[:-1])) >= 1e-9)
+        ref = O.cp_als_qr(O.as_tensor(Xs[p]), A0s[p], k)
+        assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
