@@ -103,7 +103,8 @@ struct cpqr_ctx {
   double* dKtC = nullptr;  // cross products C_k (N blocks of up to max(R,S)^2)
   double* dKtM = nullptr;  // S x R
   size_t ktC_elems = 0;
-  bool vn_cq = false;      // V_n QR by multi-CTA CholeskyQR2 (high rank), k_kr_qr2 as fallback
+  bool vn_cq = false;      // CholeskyQR2 V_n buffers allocated (some mode may use that path)
+  bool vn_cq_always = false, vn_cq_tree = false, vn_mode_cq = false;  // per-mode choice (launch_kr_qr)
   int64_t vnJ = 0;         // R^{N-1}
   double *dVn = nullptr, *dVq1 = nullptr, *dVgp = nullptr, *dVr1 = nullptr, *dVr2 = nullptr;
   bool tree = false;       // dimension-tree Multi-TTM (opt.mttm_tree, QR/SVD, N >= 3)
@@ -1083,7 +1084,7 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   a.use_smem = c->kr_smem > 0;
   a.flags = c->dflags;
   cudaStream_t st = c->side ? c->side : c->st;
-  if (c->vn_cq) {
+  if (c->vn_mode_cq) {
     const int64_t J = c->vnJ;
     const int grid = (int)std::min<int64_t>((J * c->R + 255) / 256, (int64_t)c->sms * 8);
     k_form_v<<<grid, 256, 0, st>>>(a, J, c->dVn);
@@ -1222,7 +1223,11 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   // Alg. 2 lines 6-7: V_n and its QR (K2), on the side stream: it depends only on the R_k and
   // overlaps the Multi-TTM (joined before the Q0 apply).  With profiling on it runs in line.
   static const bool no_fork = getenv("CPQR_NO_FORK") != nullptr;  // debugging: V_n QR inline
-  const bool fork = !c->opt.profile && !no_fork;
+  // dimension-tree modes without an X pass have no long kernel to hide K2 behind, and a side-stream
+  // multi-CTA QR would find no free SMs: there the CholeskyQR2 V_n QR runs inline (vn_inline)
+  const bool tree_nofresh = c->tree && !(n == 0 || n == c->tree_h) && c->variant != CPQR_NE && !c->kt;
+  c->vn_mode_cq = c->vn_cq_always || (c->vn_cq_tree && tree_nofresh);
+  const bool fork = !c->opt.profile && !no_fork && !(c->vn_mode_cq && tree_nofresh);
   prof_mark(c, 0);
   if (fork) {
     CK(cudaEventRecord(c->evf, c->st));
@@ -1556,9 +1561,14 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   }
   {  // high rank: V_n QR by the multi-CTA CholeskyQR2 (see launch_kr_qr)
     const char* v = getenv("CPQR_VN_QR");  // "cq" / "householder" force the choice
-    // by default above R^{N-1} R = 2e5 (the one-CTA K2 dominates the sweep), and from 5e4 with the
-    // dimension tree, whose modes without an X pass cannot hide K2 (C3 tree +7.5 %)
-    c->vn_cq = v ? std::string(v) == "cq" : (J * R >= 200000 || (c->tree && J * R >= 50000));
+    // every mode above R^{N-1} R = 2e5 (the one-CTA K2 dominates the sweep); from 5e4, inline, in the
+    // dimension tree's modes without an X pass, which cannot hide K2 (see mode_update)
+    c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000);
+    {  // tree modes without an X pass run the V_n QR inline (CholeskyQR2); CPQR_VN_TREE=0/1 overrides
+      const char* t = getenv("CPQR_VN_TREE");
+      c->vn_cq_tree = !v && c->tree && (t ? atoi(t) == 1 : J * R >= 50000);
+    }
+    c->vn_cq = c->vn_cq_always || c->vn_cq_tree;
     c->vnJ = J;
     if (c->vn_cq) {
       CK(dmalloc(&c->dVn, sizeof(double) * J * R));
@@ -1888,6 +1898,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   plan_mode(in, p, c->buf, c->dPart);
   CK(cudaEventRecord(c->evf, c->st));
   CK(cudaStreamWaitEvent(c->side, c->evf, 0));
+  c->vn_mode_cq = c->vn_cq_always;
   cpqr_status st = launch_kr_qr(c, n);
   if (st == CPQR_OK) st = run_plan(c, p);
   if (st == CPQR_OK) {

@@ -310,6 +310,35 @@ def test_dimension_tree_graph_replay_matches_eager(cp):
     assert all(np.array_equal(a, b) for a, b in zip(out[0][2], out[1][2]))
 
 
+@pytest.mark.parametrize("dims,R,variant", [((40, 36, 30, 28), 8, "QR"), ((30, 28, 26, 24, 22), 5, "SVD"),
+                                             ((40, 36, 30), 10, "QR")])
+def test_dimension_tree_inline_vn_qr(cp, dims, R, variant, monkeypatch):
+    """CPQR_VN_TREE=1: the tree's modes without an X pass run the V_n QR inline by the multi-CTA
+    CholeskyQR2 (no side-stream fork), the fresh modes by the side-stream Householder K2.  The
+    mode updates are Alg. 2's: factors after one sweep <= 1e-9, fits within 1e-8 of the oracle,
+    graph replay bitwise equal to eager launches."""
+    monkeypatch.setenv("CPQR_VN_TREE", "1")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=31, eta=0.05)
+    X = O.as_tensor(Xc)
+    out = []
+    for g in (True, False):
+        s = cp.CPQR(dims, R, variant, tree=True, use_graph=g)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        f1 = s.sweep(1)
+        lam, A = s.get_factors()
+        f = np.concatenate([f1, s.sweep(3)])
+        out.append((f, lam, A))
+        s.close()
+    ref1 = O.cp_als_qr(X, init, 1, variant=variant)
+    for k in range(len(dims)):
+        assert rel(out[0][2][k], ref1["factors"][k]) <= 1e-9, (k, rel(out[0][2][k], ref1["factors"][k]))
+    ref = O.cp_als_qr(X, init, 4, variant=variant)
+    assert np.max(np.abs(out[0][0] - np.array(ref["fits"]))) <= 1e-8
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert all(np.array_equal(a, b) for a, b in zip(out[0][2], out[1][2]))
+
+
 @pytest.mark.parametrize("dims,R,force_lu", [((40, 36, 30), 10, False), ((44, 41, 38), 20, False),
                                               ((12, 10, 9, 11), 6, False), ((40, 36, 30), 10, True)])
 def test_ne_variant_tail(cp, dims, R, force_lu, monkeypatch):
