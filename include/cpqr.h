@@ -19,7 +19,10 @@
  * every pointer passed in is borrowed for the duration of the call only, except a tensor
  * given with CPQR_MEM_DEVICE_BORROW (kept until the next cpqr_set_tensor or cpqr_destroy).
  * Synchronisation: every call is synchronous with respect to the host on return (results
- * written to host buffers are valid), unless stated otherwise.
+ * written to host buffers are valid), unless stated otherwise.  Device inputs must be complete
+ * when a call is made: the context runs on its own non-blocking stream (or opt.stream) and does
+ * not order itself after work the caller queued on other streams (the Python binding
+ * synchronises torch's current stream before passing a CUDA tensor).
  */
 #ifndef CPQR_H
 #define CPQR_H

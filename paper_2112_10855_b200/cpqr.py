@@ -115,6 +115,8 @@ def batched_qr(X, A0, R, max_iters=500, tol=1e-15, stream=None):
     lam = torch.empty((P, R), dtype=torch.float64, device=dev)
     fits = torch.empty((P, max_iters), dtype=torch.float64, device=dev)
     iters = torch.empty((P,), dtype=torch.int32, device=dev)
+    if stream is None:  # run in order with the torch work that produced X / A0 and reads the outputs
+        stream = torch.cuda.current_stream(dev).cuda_stream
     st = _lib.cpqr_batched_qr(P, dims, int(R), C.c_void_p(X.data_ptr()), C.c_void_p(A0cat.data_ptr()),
                               int(max_iters), float(tol), C.c_void_p(Aout.data_ptr()), C.c_void_p(lam.data_ptr()),
                               C.c_void_p(fits.data_ptr()), C.c_void_p(iters.data_ptr()),
@@ -188,6 +190,8 @@ class CPQR:
             assert X.dtype == torch.float64 and X.is_contiguous()
             if X.is_cuda:
                 mem = MEM_DEVICE_COPY if copy else MEM_DEVICE_BORROW
+                # the context reads X on its own stream: finish the torch work that produced X first
+                torch.cuda.current_stream(X.device).synchronize()
             else:
                 mem = MEM_HOST
             ptr = C.c_void_p(X.data_ptr())

@@ -353,9 +353,17 @@ bool make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
 
 constexpr size_t kSmemOptin = 227 * 1024;
 
-int stages_for(size_t stage, size_t extra) {
+// Ring depth: as many stages as fit, capped.  Deeper is not better for the HBM-bound passes: a
+// compute-free replica of the strided ring (tools/ubench/tma_bench.cu) streams C3's X at 7.2 TB/s
+// with 3-4 stages of 32 KB per SM but 6.4 TB/s with 6 (more requests in flight than the memory
+// system serves well), and the interleaved sweeps of tools/ab_stages.sh set the defaults:
+// strided 4 (3 when a unit has <= 3 k-steps), small slice 3, the rest 8 (C3 +2.5 %, C4 +9 %).
+// Env: CPQR_STAGES caps every ring, then CPQR_ST_<KIND> the one kernel kind.
+int stages_for(size_t stage, size_t extra, const char* kind_env, int cap = 8) {
   const size_t avail = kSmemOptin - 1024 - 2048 - extra;
-  return (int)std::min<size_t>(8, avail / stage);
+  if (const char* v = getenv("CPQR_STAGES")) cap = std::max(2, atoi(v));
+  if (const char* v = getenv(kind_env)) cap = std::max(2, atoi(v));
+  return (int)std::min<size_t>(cap, avail / stage);
 }
 
 // Multi-TTM Y = X x_{k != n} Q_k^T (Alg. 2 line 8).  Stream-X pass: modes 1 and 2 together
@@ -407,7 +415,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         const uint32_t box[2] = {16, 128};
         if (make_tmap(&s.mx, src, 2, d, st, box) && qmap(s, k, s.I)) {
           s.kind = 5;
-          s.S = stages_for(128 * 128 + NQB * kBoxBytes, 0);
+          s.S = stages_for(128 * 128 + NQB * kBoxBytes, 0, "CPQR_ST_FIBER");
         }
       }
     } else {
@@ -421,7 +429,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         const uint32_t box[3] = {16, 16, 1};
         if (make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, k, s.I)) {
           s.kind = 4;
-          s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0);
+          s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0, "CPQR_ST_STRIDED", (s.I + kBK - 1) / kBK <= 3 ? 3 : 4);
         }
       }
     }
@@ -456,7 +464,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         const uint32_t box[3] = {16, (uint32_t)s.I2, 8};
         if (make_tmap(&s.mx, src, 3, d, st, box)) {
           s.kind = 8;
-          s.S = stages_for((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes, 0);
+          s.S = stages_for((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes, 0, "CPQR_ST_SMALL", 3);
           s.out = out_override ? out_override : bufs[nb];
           p.steps.push_back(s);
         } else {
@@ -470,7 +478,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         const int MT = NT;
         s.gps = slice_nf(s.I2);
         const int BN = kCW * 8 * s.gps;
-        s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8);
+        s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8, "CPQR_ST_SLICE");
         s.nfb = (s.I2 + BN - 1) / BN;
         const int64_t U = s.L * s.nfb;
         s.G = std::min<int64_t>(U, in.sms);
