@@ -122,6 +122,16 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
   return v;
 }
 
+// Position in an S-stage ring: slot s and the parity of its current phase, advanced without the
+// integer division (`it % S`, `it / S` with a runtime S) that cost ~20 instructions per stage.
+struct RingPos {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int S) {
+    if (++s == S) { s = 0; ph ^= 1u; }
+  }
+};
+
 struct TmaSmem {
   uint32_t base;  // 1024-aligned shared address of stage 0
   uint64_t* full;
@@ -170,13 +180,13 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
       prefetch_tmap(&tmX);
       if (pw == 0) prefetch_tmap(&tmQ);
       const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
+      RingPos rp;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = (int)(u / nA);
         const int a0 = (int)((u - (int64_t)b * nA) * 256);
-        for (int ks = 0; ks < KS; ++ks, ++it) {
-          const int s = it % S;
-          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+          const int s = rp.s;
+          mbar_wait(&empty[s], rp.ph ^ 1);
           if (pw == 0) mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
 #pragma unroll 4
@@ -192,7 +202,7 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   }
   // --------------------------------------------------------------------------------- consumers
   const int g = lane >> 2, t = lane & 3;
-  uint32_t it = 0;
+  RingPos rp;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t b = u / nA;
     const int64_t a0 = (u - b * nA) * 256;
@@ -201,9 +211,9 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     for (int m = 0; m < 4; ++m)
 #pragma unroll
       for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-    for (int ks = 0; ks < KS; ++ks, ++it) {
-      const int s = it % S;
-      mbar_wait(&full[s], (it / S) & 1);
+    for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+      const int s = rp.s;
+      mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE, qs = xs + XBYTES;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
@@ -299,11 +309,11 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
       const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
+      RingPos rp;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
-        for (int ks = 0; ks < KS; ++ks, ++it) {
-          const int s = it % S;
-          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+          const int s = rp.s;
+          mbar_wait(&empty[s], rp.ph ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
           tma_load_2d_ef(dst, &tmX, ks * kBK, (int)(u * 128), &full[s], pol);
@@ -314,16 +324,16 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     return;
   }
   const int g = lane >> 2, t = lane & 3;
-  uint32_t it = 0;
+  RingPos rp;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     double acc[MT][2][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-    for (int ks = 0; ks < KS; ++ks, ++it) {
-      const int s = it % S;
-      mbar_wait(&full[s], (it / S) & 1);
+    for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+      const int s = rp.s;
+      mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE;
       fiber_stage<MT, 2>(xs, xs + XBYTES, warp, g, t, acc);
       __syncwarp();
@@ -385,12 +395,12 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
       const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
+      RingPos rp;
       for (int64_t u = u0; u < u1; ++u) {
         const int l = (int)(u / nfb), fb = (int)(u - (int64_t)l * nfb);
-        for (int ks = 0; ks < KS; ++ks, ++it) {
-          const int s = it % S;
-          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+          const int s = rp.s;
+          mbar_wait(&empty[s], rp.ph ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
           tma_load_3d_ef(dst, &tmX, ks * kBK, fb * BN, l, &full[s], pol);
@@ -411,7 +421,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   for (int m = 0; m < (YREG ? MT : 1); ++m)
 #pragma unroll
     for (int m2 = 0; m2 < (YREG ? MT : 1); ++m2) yreg[m][m2][0] = yreg[m][m2][1] = 0.0;
-  uint32_t it = 0;
+  RingPos rp;
   int64_t run_start = u0;
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t l = u / nfb;
@@ -421,9 +431,9 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     for (int m = 0; m < MT; ++m)
 #pragma unroll
       for (int n = 0; n < NF; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-    for (int ks = 0; ks < KS; ++ks, ++it) {
-      const int s = it % S;
-      mbar_wait(&full[s], (it / S) & 1);
+    for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+      const int s = rp.s;
+      mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE;
       fiber_stage<MT, NF>(xs, xs + XBYTES, warp, g, t, acc);
       __syncwarp();
@@ -545,11 +555,11 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
       const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
+      RingPos rp;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
-        for (int ks = 0; ks < KS; ++ks, ++it) {
-          const int s = it % S;
-          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+          const int s = rp.s;
+          mbar_wait(&empty[s], rp.ph ^ 1);
           mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
           tma_load_3d_ef(dst, &tmX, ks * kBK, 0, (int)(u * 8), &full[s], pol);
@@ -560,7 +570,7 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     return;
   }
   const int g = lane >> 2, t = lane & 3;
-  uint32_t it = 0;
+  RingPos rp;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     double acc[MT][8][2];
 #pragma unroll
@@ -568,9 +578,9 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 #pragma unroll
       for (int n = 0; n < 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
     const int rowbase = warp * I2;
-    for (int ks = 0; ks < KS; ++ks, ++it) {
-      const int s = it % S;
-      mbar_wait(&full[s], (it / S) & 1);
+    for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+      const int s = rp.s;
+      mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE, qs = xs + XBYTES;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
