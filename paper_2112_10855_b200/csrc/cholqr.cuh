@@ -387,11 +387,11 @@ __device__ __noinline__ bool cq_chol_2d(double* Gs, int R, double* Ru, double* i
   __syncthreads();
   // critical path per column: LDS of the pivot, its reciprocal (__drcp_rn == 1.0 / d, correctly
   // rounded), one FMA per owned entry, barrier; square roots are taken after the loop
-  if (nw == 8) {
+  if (nw >= 8) {  // warps 0..7 map the columns (k = kk mod 8); any further warps only join the barriers
 #pragma unroll 1
     for (int j = 0; j < R; ++j) {
       // every load of the column step first (one shared-memory round trip), then the reciprocal
-      const bool act = i > j && i < R;
+      const bool act = i > j && i < R && kk < 8;
       const double d = Gs[j + RB * j];
       double gi = 0.0, gk[RB / 8], gik[RB / 8];
 #pragma unroll
@@ -477,7 +477,7 @@ __device__ __forceinline__ double cluster_sum_ordered(cooperative_groups::cluste
 #define CQ_DUMP() do {} while (0)
 #endif
 template <int RB>
-__global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
+__global__ void __launch_bounds__(512) k_cq_compact(CqArgs a) {
 #ifdef CPQR_DEBUG_TIMING
   __shared__ long long tstamp[16];
 #endif
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   double* Ui = R2s + RB * RB;  // (unused scratch; keeps the host smem size formula)
   double* Ms = Ui + RB * RB;
   double* R0s = Ms + RB * RB;
-  __shared__ double lam[RB], invlam[RB], redi[8], innerb, inv1[RB], inv2[RB], invm[RB];
+  __shared__ double lam[RB], invlam[RB], redi[32], innerb, inv1[RB], inv2[RB], invm[RB];
   __shared__ int okf;
   (void)Ui;
   const int nb = a.nb, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   double* Y = X + ld * RB;     // panel of W / Q1 rows
   const int i = r0 + tid;
   const bool own = tid < rows;
-  if (tid == 0 && b == 0) atomicAnd(a.flags, ~FLAG_USE_HOUSEHOLDER);
+  if (tid == 0 && b == 0) atomicAnd(a.flags, ~cq_hh_bit(a));
   #pragma unroll 1
   for (int e = tid; e < 2 * ld * RB; e += blockDim.x) X[e] = 0.0;
   #pragma unroll 1
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   __syncthreads();
   CQ_T(11);
   if (!okf) {
-    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    if (tid == 0 && b == 0) atomicOr(a.flags, cq_hh_bit(a));
     cluster.sync();
     return;
   }
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
   }
   __syncthreads();
   if (!okf) {
-    if (tid == 0 && b == 0) atomicOr(a.flags, FLAG_USE_HOUSEHOLDER);
+    if (tid == 0 && b == 0) atomicOr(a.flags, cq_hh_bit(a));
     cluster.sync();
     return;
   }
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(256) k_cq_compact(CqArgs a) {
     for (int k = 0; k < R; ++k) a.Q[i + (int64_t)a.m * k] = Y[tid + ld * k];
   }
   __syncthreads();
-  {  // Qt rows of this CTA: one contiguous row-major block, written coalesced
+  if (a.Qt) {  // Qt rows of this CTA: one contiguous row-major block, written coalesced
     const int RQ = a.RQ;
     #pragma unroll 4
     for (int e = tid; e < rows * RQ; e += blockDim.x) {

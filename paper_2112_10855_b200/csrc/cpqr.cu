@@ -868,6 +868,42 @@ void cq_multi_attrs() {  // dynamic shared memory of the multi-kernel CholeskyQR
   done = true;
 }
 
+// one cluster launch of k_cq_compact: nb CTAs (<= 8) of tb threads, one panel row per thread
+cpqr_status launch_cq_compact(cpqr_ctx* c, const CqArgs& q, int RB, int tb, cudaStream_t st) {
+  const int ld = ((tb + 15) & ~15) + 4;
+  const size_t smem = (size_t)(8 * RB * RB + 2 * ld * RB) * sizeof(double);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(q.nb);
+  cfg.blockDim = dim3(tb);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = q.nb;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaSuccess;
+#ifdef CPQR_DEBUG_TIMING
+  const int reps = getenv("CPQR_CQ_TWICE") ? 2 : 1;  // warm-vs-cold instruction-fetch experiment
+#else
+  const int reps = 1;
+#endif
+#define CQL(RBV)                                                                                    \
+  {                                                                                                 \
+    cudaFuncSetAttribute(k_cq_compact<RBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    e = cudaLaunchKernelEx(&cfg, k_cq_compact<RBV>, q);                                             \
+  }
+  for (int rep = 0; rep < reps && e == cudaSuccess; ++rep) {
+    switch (RB) { case 8: CQL(8) break; case 16: CQL(16) break; default: CQL(32) break; }
+  }
+#undef CQL
+  if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_cq_compact launch: %s", cudaGetErrorString(e));
+  CKL();
+  return CPQR_OK;
+}
+
 cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const double* W, double* Q,
                         double* Qt, double* Rn, double* Aout, bool do_fit) {
   const int R = c->R, RB = rb_for(R);
@@ -903,38 +939,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     if (solve && c->variant == CPQR_SVD) {
       if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
     }
-    const int tb = 32 * ((mbq + 31) / 32);
-    const int ld = ((tb + 15) & ~15) + 4;
-    const size_t smem = (size_t)(8 * RB * RB + 2 * ld * RB) * sizeof(double);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(nbq);
-    cfg.blockDim = dim3(tb);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c->st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = nbq;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaSuccess;
-#ifdef CPQR_DEBUG_TIMING
-    const int reps = getenv("CPQR_CQ_TWICE") ? 2 : 1;  // warm-vs-cold instruction-fetch experiment
-#else
-    const int reps = 1;
-#endif
-#define CQL(RBV)                                                                                    \
-  {                                                                                                 \
-    cudaFuncSetAttribute(k_cq_compact<RBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    e = cudaLaunchKernelEx(&cfg, k_cq_compact<RBV>, q);                                             \
-  }
-    for (int rep = 0; rep < reps && e == cudaSuccess; ++rep) {
-      switch (RB) { case 8: CQL(8) break; case 16: CQL(16) break; default: CQL(32) break; }
-    }
-#undef CQL
-    if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_cq_compact launch: %s", cudaGetErrorString(e));
-    CKL();
+    TRY(launch_cq_compact(c, q, RB, 32 * ((mbq + 31) / 32), c->st));
     gated = true;
   } else if (c->factor_qr_mode == 0) {
     CqArgs q{};
@@ -1102,7 +1107,16 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
     q.solve = 0; q.Q1 = c->dVq1; q.Gp = c->dVgp; q.innerp = c->dinnerp; q.R1 = c->dVr1; q.R2 = c->dVr2;
     q.Q = c->dQ0; q.Qt = nullptr; q.RQ = c->RQ; q.Rn = c->dR0; q.flags = c->dflags; q.do_fit = 0;
     q.nX2 = c->dnX2; q.fit = c->dfit; q.hh_bit = FLAG_VN_HOUSEHOLDER;
-    TRY(launch_cq_multi(c, q, st));
+    // one cluster launch when the rows fit 8 CTAs of <= 512 (R <= 16) or 256 (R <= 32) threads
+    const int rb = c->R <= 8 ? 8 : c->R <= 16 ? 16 : 32, tmax = rb <= 16 ? 512 : 256;  // (see create)
+    const bool no_compact = getenv("CPQR_VN_COMPACT") && atoi(getenv("CPQR_VN_COMPACT")) == 0;
+    if (J <= 8 * tmax && !no_compact) {
+      q.nb = (int)std::min<int64_t>(8, (J + 255) / 256);
+      q.mb = (int)((J + q.nb - 1) / q.nb);
+      TRY(launch_cq_compact(c, q, rb, 32 * ((q.mb + 31) / 32), st));
+    } else {
+      TRY(launch_cq_multi(c, q, st));
+    }
     a.gate_bit = FLAG_VN_HOUSEHOLDER;
   }
   k_kr_qr2<<<1, 1024, c->kr_smem, st>>>(a);
@@ -1574,7 +1588,11 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000);
     {  // tree modes without an X pass run the V_n QR inline (CholeskyQR2); CPQR_VN_TREE=0/1 overrides
       const char* t = getenv("CPQR_VN_TREE");
-      c->vn_cq_tree = !v && c->tree && (t ? atoi(t) == 1 : J * R >= 50000);
+      // the one-launch cluster CholeskyQR2 (k_cq_compact) takes V_n up to 8 CTAs x 512 rows (R <= 16)
+      // or x 256 rows (R <= 32): inline it is cheaper than the exposed K2 in every measured config
+      // (C2-C5 tree +2..14 %); larger V_n take the multi-kernel CholeskyQR2 from R^{N-1} R = 5e4
+      const bool compact_ok = J <= 8 * (R <= 16 ? 512 : 256);
+      c->vn_cq_tree = !v && c->tree && (t ? atoi(t) == 1 : (compact_ok || J * R >= 50000));
     }
     c->vn_cq = c->vn_cq_always || c->vn_cq_tree;
     c->vnJ = J;

@@ -460,16 +460,21 @@ def test_zero_tensor(cp):
     s.close()
 
 
+@pytest.mark.parametrize("compact", [True, False])
 @pytest.mark.parametrize("dims,R,variant,kind,c", [((30, 40, 50), 5, "QR", "normal", 0.0),
                                                    ((12, 10, 9, 11), 6, "QR", "normal", 0.0),
                                                    ((9, 8, 7, 8, 9), 4, "SVD", "normal", 0.0),
-                                                   ((40, 36, 30), 4, "QR", "congruence", 1.0 - 1e-10)])
-def test_vn_qr_by_cholesky_qr2(cp, dims, R, variant, kind, c, monkeypatch):
+                                                   ((40, 36, 30), 4, "QR", "congruence", 1.0 - 1e-10),
+                                                   ((12, 11, 9, 10, 13), 8, "QR", "normal", 0.0),
+                                                   ((24, 20, 18, 22), 16, "QR", "normal", 0.0)])
+def test_vn_qr_by_cholesky_qr2(cp, dims, R, variant, kind, c, compact, monkeypatch):
     """High-rank V_n QR path, forced on small shapes: V_n formed densely and
-    factored by the multi-CTA CholeskyQR2 under the kappa guard; with congruence 1 - 1e-10 the
+    factored under the kappa guard by the one-launch cluster CholeskyQR2 (k_cq_compact, up to 8 CTAs
+    x 512 rows: the J = 4096 cases fill it) or the multi-kernel CholeskyQR2 (compact=False); with congruence 1 - 1e-10 the
     guard rejects V_n and the staircase Householder K2 runs instead (device flag).  Q0 orthonormal,
     V_n = Q0 R0 with diag(R0) > 0 (the unique thin QR), sweeps follow the oracle."""
     monkeypatch.setenv("CPQR_VN_QR", "cq")
+    monkeypatch.setenv("CPQR_VN_COMPACT", "1" if compact else "0")
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=67, eta=0.05, kind=kind, c=c)
     X = O.as_tensor(Xc)
     start = truth if kind == "congruence" else init

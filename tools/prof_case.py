@@ -18,13 +18,15 @@ ap.add_argument("--sweeps", type=int, default=1)
 ap.add_argument("--warm", type=int, default=1)
 ap.add_argument("--graph", type=int, default=0)
 ap.add_argument("--profile", type=int, default=1)
+ap.add_argument("--tree", type=int, default=0)
 a = ap.parse_args()
 conf = synth.CONFIGS[a.config]
 variant = a.variant or conf.variants[0]
 torch.manual_seed(0)
 X = torch.randn(int(np.prod(conf.dims)), dtype=torch.float64, device="cuda")
 init = synth.init_factors(conf)
-s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, use_graph=bool(a.graph), profile=bool(a.profile))
+s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, use_graph=bool(a.graph), profile=bool(a.profile),
+               tree=bool(a.tree))
 s.set_tensor(X)
 s.set_factors(init)
 s.sweep(a.warm)
