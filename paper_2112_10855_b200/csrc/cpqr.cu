@@ -633,13 +633,25 @@ void set_smem(K kernel, size_t smem) {
 void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
   const int NT = (R + 7) / 8, NQB = (NT + 1) / 2;
   if (s.kind == 4) {
-    const size_t smem = 3072 + (size_t)s.S * (16 * kBoxBytes + NQB * kBoxBytes);
-    const int64_t units = ((s.A + 255) / 256) * s.B;
-    const int grid = (int)std::min<int64_t>(units, sms);
+    // CW consumer warps per CTA over 32 CW-row units.  CW = 4 runs two CTAs per SM, each with its
+    // own ring, so one computes while the other waits for data: measured C2 +1..5 %, C4 tree +3 %,
+    // but C3 -0.8 % and C5 -1.1 % (interleaved A/B), hence only for R <= 12.  Env CPQR_STR_CW=4/8.
+    static const int cw_env = getenv("CPQR_STR_CW") ? atoi(getenv("CPQR_STR_CW")) : 0;
+    const int cw = cw_env == 4 ? 4 : cw_env == 8 ? 8 : (R <= 12 ? 4 : 8);
+    const size_t stage = (size_t)(2 * cw + NQB) * kBoxBytes;
+    const int S = cw == 4 ? std::min<int>(s.S, (int)((110 * 1024 - 3072) / stage)) : s.S;
+    const size_t smem = 3072 + (size_t)S * stage;
+    const int64_t units = ((s.A + 32 * cw - 1) / (32 * cw)) * s.B;
+    const int grid = (int)std::min<int64_t>(units, (int64_t)sms * (cw == 4 ? 2 : 1));
 #define STR(NTV, NPV)                                                                                  \
   {                                                                                                     \
-    set_smem(k_strided_tma<NTV, NPV>, smem);                                                            \
-    k_strided_tma<NTV, NPV><<<grid, (kCW + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, s.S); \
+    if (cw == 4) {                                                                                      \
+      set_smem(k_strided_tma<NTV, NPV, 4>, smem);                                                       \
+      k_strided_tma<NTV, NPV, 4><<<grid, (4 + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S); \
+    } else {                                                                                            \
+      set_smem(k_strided_tma<NTV, NPV>, smem);                                                          \
+      k_strided_tma<NTV, NPV><<<grid, (kCW + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S); \
+    }                                                                                                   \
   }
     // producer warps issuing the 16 X boxes of a stage in parallel: a single issuing thread bounds
     // the HBM-bound passes (C2 +16 %); 4 for the FP64-bound R >= 24 passes (+1.5 % on C5, -1.5 % C4)

@@ -152,30 +152,30 @@ __device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& fu
 // X map 3D {A, I, B}, box {16, 16, 1} (16 boxes per stage); Q map 2D {RQ, I} over the transposed
 // padded panel Qt[i*RQ + r], box {16, 16} (NT/2 boxes).  Consumer warp w owns rows 32w..32w+31:
 // M-tiles mt = 2p + s hold rows 16(2w+p) + 2g + s (one 16-byte load feeds two tiles).
-template <int NT, int NP = 1>
-__global__ void __launch_bounds__((kCW + NP) * 32, 1)
+template <int NT, int NP = 1, int CW = kCW>
+__global__ void __launch_bounds__((CW + NP) * 32, CW == 4 ? 2 : 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
               int I, int64_t B, int R, double* __restrict__ T, int S) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (NT + 1) / 2;
-  constexpr uint32_t XBYTES = 16 * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
+  constexpr uint32_t XBYTES = 2 * CW * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
   uint8_t* st0 = tma_carve(smraw, S, full, empty);
   const uint32_t sbase = smem_u32(st0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CW); }
     fence_barrier_init();
   }
   __syncthreads();
-  const int64_t nA = (A + 255) / 256;
+  const int64_t nA = (A + 32 * CW - 1) / (32 * CW);
   const int64_t units = nA * B;
   const int KS = (I + kBK - 1) / kBK;
-  if (warp >= kCW) {  // ---------------------------------------------------------- producer(s)
+  if (warp >= CW) {  // ---------------------------------------------------------- producer(s)
     // NP producer warps split the 16 X boxes of a stage (the per-box TMA issue cost bounds the
     // HBM-bound passes); producer 0 also loads Q and does the arrive.expect_tx for the whole stage
     // (bytes of the other producers may land first: the tx count just dips below zero meanwhile)
-    const int pw = warp - kCW;
+    const int pw = warp - CW;
     if (lane == 0) {
       prefetch_tmap(&tmX);
       if (pw == 0) prefetch_tmap(&tmQ);
@@ -183,14 +183,14 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
       RingPos rp;
       for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         const int b = (int)(u / nA);
-        const int a0 = (int)((u - (int64_t)b * nA) * 256);
+        const int a0 = (int)((u - (int64_t)b * nA) * 32 * CW);
         for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
           const int s = rp.s;
           mbar_wait(&empty[s], rp.ph ^ 1);
           if (pw == 0) mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
 #pragma unroll 4
-          for (int q = pw * (16 / NP); q < (pw + 1) * (16 / NP); ++q)
+          for (int q = pw * (2 * CW / NP); q < (pw + 1) * (2 * CW / NP); ++q)
             tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
           if (pw == 0)
 #pragma unroll
@@ -205,7 +205,7 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   RingPos rp;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t b = u / nA;
-    const int64_t a0 = (u - b * nA) * 256;
+    const int64_t a0 = (u - b * nA) * 32 * CW;
     double acc[4][NT][2];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
