@@ -277,10 +277,13 @@ __device__ int jacobi_pinv(const double* R0, int R, double tau, double* Bs, doub
           al += bp * bp; be += bq * bq; ga += bp * bq;
         }
         al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (fabs(ga) > (double)R * kEps * sqrt(al * be) && ga != 0.0) {
+        // |ga| > R eps sqrt(al be), compared squared, and cs = rsqrt(1 + t^2): one square root and
+        // one division fewer on the round's dependent chain (the rounds are latency-bound)
+        const double thr = (double)R * kEps;
+        if (ga * ga > thr * thr * (al * be) && ga != 0.0) {
           const double zeta = (be - al) / (2.0 * ga);
           const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+          const double cs = rsqrt(1.0 + tt * tt), sn = cs * tt;
           for (int r = lane; r < R; r += 32) {
             const double bp = Bs[r + R * p], bq = Bs[r + R * q];
             Bs[r + R * p] = cs * bp - sn * bq;
