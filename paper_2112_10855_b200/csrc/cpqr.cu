@@ -1262,6 +1262,9 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   const bool tree_nofresh = c->tree && !(n == 0 || n == c->tree_h) && c->variant != CPQR_NE && !c->kt;
   c->vn_mode_cq = c->vn_cq_always || (c->vn_cq_tree && tree_nofresh);
   const bool fork = !c->opt.profile && !no_fork && !(c->vn_mode_cq && tree_nofresh);
+  // there the V_n QR runs inline, but the one-CTA SVD of R0 (QR-SVD) still forks to the side
+  // stream (the stream grids leave it an SM) and is joined only before the solve
+  const bool pinv_fork = !fork && c->variant == CPQR_SVD && !c->opt.profile && !no_fork;
   prof_mark(c, 0);
   if (fork) {
     CK(cudaEventRecord(c->evf, c->st));
@@ -1271,6 +1274,11 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     cudaStream_t keep = c->side;
     if (!fork) c->side = nullptr;
     cpqr_status st = launch_kr_qr(c, n);
+    if (st == CPQR_OK && pinv_fork) {
+      CK(cudaEventRecord(c->evf, c->st));
+      CK(cudaStreamWaitEvent(keep, c->evf, 0));
+      c->side = keep;
+    }
     if (st == CPQR_OK && c->variant == CPQR_SVD) {  // SVD of R0 right behind its QR, off the critical path
       st = launch_pinv(c, c->side ? c->side : c->st, nullptr);
       c->pinv_ready = (st == CPQR_OK);
@@ -1278,7 +1286,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     c->side = keep;
     TRY(st);
   }
-  if (fork) CK(cudaEventRecord(c->evj, c->side));
+  if (fork || pinv_fork) CK(cudaEventRecord(c->evj, c->side));
   prof_mark(c, 1);
   // line 8: Multi-TTM (first step = the stream-X pass; with the dimension tree only the first mode
   // of each half has one).  Kruskal input: C_k = Q_k^T B_k, then W_n below
@@ -1322,6 +1330,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     TRY(combine_w(c, n, Wloc, c->dW));
   }
   prof_mark(c, 4);
+  if (pinv_fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
   // lines 10-12: solve (substitution / SVD), lambda, normalise, factor QR (+ fast fit after mode N)
   const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
   const cpqr_status tst = launch_tsqr(c, In, nullptr, true, c->dW, c->dQ[n], c->dQt[n], c->dRk[n], c->dA[n], fit);
