@@ -166,6 +166,11 @@ typedef struct cpqr_profile {
   int64_t launches_total;
 } cpqr_profile;
 cpqr_status cpqr_get_profile(cpqr_ctx* ctx, cpqr_profile* prof, int reset);
+/* cpqr_get_timings: the six per-phase milliseconds of cpqr_get_profile (ms[0..5]
+ * as above: the paper's five-way split, with the Multi-TTM's stream-X pass
+ * separated from its remaining TTMs), accumulated since the last reset; zeros unless
+ * opt.profile = 1.  ms: caller buffer of 6 doubles.  Errors: EINVAL (NULL ctx or ms). */
+cpqr_status cpqr_get_timings(cpqr_ctx* ctx, double* ms);
 
 /* Kernel launches issued by one cpqr_sweep(ctx, 1, ...) (claims for bench "gpu_launches"). */
 cpqr_status cpqr_launches_per_sweep(cpqr_ctx* ctx, int64_t* n);

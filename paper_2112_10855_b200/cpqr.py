@@ -29,7 +29,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE"
 
 EXPORTS = [
     "cpqr_default_options", "cpqr_create", "cpqr_set_tensor", "cpqr_set_factors", "cpqr_init_factors",
-    "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile",
+    "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile", "cpqr_get_timings",
     "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_qr", "cpqr_debug_svd_solve",
     "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
 ]
@@ -63,6 +63,7 @@ _sig = {
     "cpqr_get_fit": (C.c_int32, [_P, _DP]),
     "cpqr_get_flags": (C.c_int32, [_P, C.POINTER(C.c_uint32)]),
     "cpqr_get_profile": (C.c_int32, [_P, C.POINTER(Profile), C.c_int]),
+    "cpqr_get_timings": (C.c_int32, [_P, C.POINTER(C.c_double)]),
     "cpqr_launches_per_sweep": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
     "cpqr_debug_mode": (C.c_int32, [_P, C.c_int, C.POINTER(_DP), _DP, _DP, _DP, _DP]),
     "cpqr_debug_qr": (C.c_int32, [_P, _DP, C.c_int64, _DP, _DP]),
@@ -247,6 +248,13 @@ class CPQR:
         self._check(_lib.cpqr_get_profile(self._h, C.byref(p), 1 if reset else 0))
         return dict(ms=list(p.ms), launches=list(p.launches), bytes0=p.bytes0, flops0=p.flops0,
                     launches_total=p.launches_total)
+
+    def timings(self):
+        """cpqr_get_timings: per-phase ms since the last profile reset (needs profile=True):
+        stream-X pass, remaining TTMs, factor QR, Q0 compute, Q0 apply, other."""
+        ms = (C.c_double * 6)()
+        self._check(_lib.cpqr_get_timings(self._h, ms))
+        return list(ms)
 
     def launches_per_sweep(self):
         n = C.c_int64()

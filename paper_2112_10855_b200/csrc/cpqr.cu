@@ -1913,6 +1913,12 @@ CPQR_API cpqr_status cpqr_get_profile(cpqr_ctx* c, cpqr_profile* p, int reset) {
   return CPQR_OK;
 }
 
+CPQR_API cpqr_status cpqr_get_timings(cpqr_ctx* c, double* ms) {
+  if (!c || !ms) return CPQR_EINVAL;
+  for (int i = 0; i < 6; ++i) ms[i] = c->prof.ms[i];
+  return CPQR_OK;
+}
+
 CPQR_API cpqr_status cpqr_launches_per_sweep(cpqr_ctx* c, int64_t* n) {
   if (!c || !n) return CPQR_EINVAL;
   *n = c->launches_per_sweep;

@@ -618,3 +618,27 @@ def test_batched_stopping_rule_and_paper_shape(cp):
             assert abs(f[-1] - f[-2]) < 1e-9 and np.all(np.abs(np.diff(f[:-1])) >= 1e-9)
         ref = O.cp_als_qr(O.as_tensor(Xs[p]), A0s[p], k)
         assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+
+
+def test_profile_and_timings(cp):
+    """opt.profile = 1 (the paper's per-phase time breakdown): eager sweeps with
+    events around each phase.  cpqr_get_timings returns the same six per-phase ms as
+    cpqr_get_profile; the stream-X pass is timed, the algorithmic bytes equal N passes over X, and
+    the fits equal those of the graph path bitwise (profiling changes launch order only)."""
+    dims, R = (40, 36, 30), 6
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=13, eta=0.05)
+    fits = []
+    for prof in (True, False):
+        s = cp.CPQR(dims, R, "QR", profile=prof, use_graph=not prof)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        fits.append(s.sweep(3))
+        if prof:
+            t = s.timings()
+            p = s.profile(reset=True)
+            assert len(t) == 6 and t == p["ms"]
+            assert t[0] > 0.0 and all(v >= 0.0 for v in t)
+            assert p["bytes0"] == len(dims) * 8.0 * np.prod(dims)
+            assert s.timings() == [0.0] * 6  # reset by profile(reset=True)
+        s.close()
+    assert np.array_equal(fits[0], fits[1])
