@@ -370,7 +370,7 @@ __device__ __forceinline__ void cq_gram_dmma(const double* P, int ld, int rows4,
 }
 
 // ----------------------------------------------------------------- compact (I-cache friendly) variant
-// Same algorithm as k_cq_fused, but every per-row quantity lives in a shared-memory panel row
+// CholeskyQR2 in one cluster launch; every per-row quantity lives in a shared-memory panel row
 // (owner thread tid, stride 1 across threads -> conflict free) and all loops are rolled: the
 // fully unrolled register version compiles to >600 KB of SASS and thrashes the 32 KB instruction
 // cache.  Q1 = A R1^{-1} and Q = Q1 R2^{-1} use the explicit upper-triangular inverses (column-

@@ -12,9 +12,13 @@
 //                          in one CTA (diag(R) >= 0, reading 6), explicit Q = diag(Q_b) Q_top
 //                          written both column-major (Q_n) and as the transposed padded panel the
 //                          TMA kernels stream.
-//   k_solve_norm           Alg. 2 lines 10-11: Ahat R0^T = W (row-parallel back substitution) or
-//                          Ahat = W U S^+ V^T (one-sided Jacobi SVD of R0), lambda, normalise,
-//                          and <W, Ahat R0^T> for the fast fit.
+//   k_form_v / k_kr_qr2    V_n (Khatri-Rao of the R_k, Alg. 2 line 6) formed densely for the
+//                          CholeskyQR2 path, and the one-CTA staircase Householder QR of V_n
+//                          (K2, line 7), gated by FLAG_VN_HOUSEHOLDER behind the CholeskyQR2 path.
+//   k_svd_pinv             M = U S^+ V^T of R0 by one-sided Jacobi (QR-SVD).
+//   k_solve_rows / k_normalize  Alg. 2 lines 10-11 for factors too tall for the fused tail:
+//                          Ahat R0^T = W (row-parallel back substitution) or Ahat = W M, lambda,
+//                          normalise, and <W, Ahat R0^T> for the fast fit.
 #pragma once
 #include <cstdio>
 #include "small_kernels.cuh"

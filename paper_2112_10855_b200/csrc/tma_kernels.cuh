@@ -1,9 +1,9 @@
 // TMA-pipelined Multi-TTM stream-X kernels (sm_100a): the Blackwell mainloop for the dominant
 // step of CP-ALS-QR (Alg. 2 line 8; cost Eq. (TTMcost)).
 //
-// One producer warp (warp kCW) issues cp.async.bulk.tensor loads of each stage -- an X tile plus
-// the matching rows of the (transposed, zero-padded) Q panel -- into a ring of kStages shared-
-// memory buffers, signalling `full[s]` via mbarrier complete_tx.  kCW consumer warps run FP64
+// Producer warp(s) after the consumer warps issue cp.async.bulk.tensor loads of each stage -- an X
+// tile plus the matching rows of the (transposed, zero-padded) Q panel -- into an S-stage ring of
+// shared-memory buffers, signalling `full[s]` via mbarrier complete_tx.  The consumer warps run FP64
 // tensor-core MMAs (DMMA m8n8k4) straight from the swizzled tiles and release each stage on
 // `empty[s]`.  X is read from HBM exactly once; Q rows come from L2 alongside each X tile, so no
 // panel has to fit in shared memory whole (C5's Q_k is 256 KB).  Out-of-range rows/fibres are
@@ -148,10 +148,11 @@ __device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& fu
 }
 
 // ======================================================================= strided (mode k > 1)
-// T(a, r, b) = sum_i X(a, i, b) Q(i, r).  Unit = 256 consecutive a (8 warps x 32 rows) of one b;
-// X map 3D {A, I, B}, box {16, 16, 1} (16 boxes per stage); Q map 2D {RQ, I} over the transposed
-// padded panel Qt[i*RQ + r], box {16, 16} (NT/2 boxes).  Consumer warp w owns rows 32w..32w+31:
-// M-tiles mt = 2p + s hold rows 16(2w+p) + 2g + s (one 16-byte load feeds two tiles).
+// T(a, r, b) = sum_i X(a, i, b) Q(i, r).  Unit = 32 CW consecutive a (CW consumer warps x 32 rows)
+// of one b; X map 3D {A, I, B}, box {16, 16, 1} (2 CW boxes per stage, split over NP producer
+// warps); Q map 2D {RQ, I} over the transposed padded panel Qt[i*RQ + r], box {16, 16} (NT/2
+// boxes).  Consumer warp w owns rows 32w..32w+31: M-tiles mt = 2p + s hold rows 16(2w+p) + 2g + s
+// (one 16-byte load feeds two tiles).  CW = 4 runs two CTAs per SM (see launch_tma).
 template <int NT, int NP = 1, int CW = kCW>
 __global__ void __launch_bounds__((CW + NP) * 32, CW == 4 ? 2 : 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
