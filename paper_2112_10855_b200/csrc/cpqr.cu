@@ -951,7 +951,9 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     if (solve && c->variant == CPQR_SVD) {
       if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
     }
-    TRY(launch_cq_compact(c, q, RB, 32 * ((mbq + 31) / 32), c->st));
+    // >= 8 warps even for short factors: the 2-D Cholesky maps its columns to 8 warps (the rolled
+    // fallback for fewer warps cost ~680 vs ~440 cycles per column); spare threads own no row
+    TRY(launch_cq_compact(c, q, RB, std::max(256, 32 * ((mbq + 31) / 32)), c->st));
     gated = true;
   } else if (c->factor_qr_mode == 0) {
     CqArgs q{};
