@@ -1014,6 +1014,29 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
         if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
       }
       const int tl = 32 * ((mbr + 31) / 32), tr = 32 * ((nl * R + 31) / 32);
+      static const bool rq_split = getenv("CPQR_RQ_SPLIT") && atoi(getenv("CPQR_RQ_SPLIT")) == 1;
+      if (!rq_split) {  // one cluster launch of the three phases (k_rq_fused)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(nl);
+        cfg.blockDim = dim3(std::max(tl, tr));
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = c->st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = nl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e;
+        switch (RB) {
+          case 8: e = cudaLaunchKernelEx(&cfg, k_rq_fused<8>, q); break;
+          case 16: e = cudaLaunchKernelEx(&cfg, k_rq_fused<16>, q); break;
+          default: e = cudaLaunchKernelEx(&cfg, k_rq_fused<32>, q); break;
+        }
+        if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_rq_fused launch: %s", cudaGetErrorString(e));
+        CKL();
+      } else {
       switch (RB) {
         case 8:
           k_rq_leaf<8><<<nl, tl, 0, c->st>>>(q); CKL();
@@ -1030,6 +1053,7 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
           k_rq_root<32><<<1, tr, 0, c->st>>>(q); CKL();
           k_rq_qform<32><<<nl, tl, 0, c->st>>>(q); CKL();
           break;
+      }
       }
       return CPQR_OK;
     }

@@ -12,6 +12,8 @@
 // LAPACK dgeqr2 / dorg2r conventions (beta = -sign(x0) ||.||, tau = (beta - x0)/beta); diag(R) >= 0
 // is applied by the callers (reading 6).  All reductions have a fixed order (deterministic).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace cpqr {
@@ -221,12 +223,13 @@ __device__ __forceinline__ bool rq_skip(const RqArgs& a) {
   return (fl & 0x200u) == 0;
 }
 
+// The three TSQR phases as device bodies: launched as three kernels (k_rq_leaf/root/qform) or as
+// one cluster kernel (k_rq_fused) with cluster barriers between the phases.
 template <int RB>
-__global__ void __launch_bounds__(256) k_rq_leaf(RqArgs a) {
-  if (rq_skip(a)) return;
+__device__ __forceinline__ void rq_leaf_body(const RqArgs& a, const int b) {
   __shared__ double tau[RB], beta[RB], rowbuf[2 * RB], red[8 * RB], fin[2 * RB], Ms[RB * RB], R0s[RB * RB];
   __shared__ double redi[8];
-  const int b = blockIdx.x, R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int R = a.R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
   const int row = (tid < rows) ? tid : -1;
   const int i = r0 + tid;
@@ -304,8 +307,7 @@ __global__ void __launch_bounds__(256) k_rq_leaf(RqArgs a) {
 }
 
 template <int RB>
-__global__ void __launch_bounds__(256) k_rq_root(RqArgs a) {
-  if (rq_skip(a)) return;
+__device__ __forceinline__ void rq_root_body(const RqArgs& a) {
   __shared__ double tau[RB], beta[RB], rowbuf[2 * RB], red[8 * RB], fin[2 * RB], lam[RB], r0s[RB * RB], rns[RB * RB];
   __shared__ double redq[8], inner_s;
   const int R = a.R, rows = a.nleaf * R, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -371,10 +373,9 @@ __global__ void __launch_bounds__(256) k_rq_root(RqArgs a) {
 }
 
 template <int RB>
-__global__ void __launch_bounds__(256) k_rq_qform(RqArgs a) {
-  if (rq_skip(a)) return;
+__device__ __forceinline__ void rq_qform_body(const RqArgs& a, const int b) {
   __shared__ double tau[RB], rowbuf[2 * RB], red[8 * RB], fin[2 * RB];
-  const int b = blockIdx.x, R = a.R, tid = threadIdx.x;
+  const int R = a.R, tid = threadIdx.x;
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0;
   const int row = (tid < rows) ? tid : -1;
   const int i = r0 + tid;
@@ -403,6 +404,41 @@ __global__ void __launch_bounds__(256) k_rq_qform(RqArgs a) {
       if (k < R) a.Q[i + (int64_t)a.m * k] = m[k];
     for (int k = 0; k < a.RQ; ++k) a.Qt[(int64_t)i * a.RQ + k] = (k < R) ? m[k] : 0.0;
   }
+}
+
+template <int RB>
+__global__ void __launch_bounds__(256) k_rq_leaf(RqArgs a) {
+  if (rq_skip(a)) return;
+  rq_leaf_body<RB>(a, blockIdx.x);
+}
+template <int RB>
+__global__ void __launch_bounds__(256) k_rq_root(RqArgs a) {
+  if (rq_skip(a)) return;
+  rq_root_body<RB>(a);
+}
+template <int RB>
+__global__ void __launch_bounds__(256) k_rq_qform(RqArgs a) {
+  if (rq_skip(a)) return;
+  rq_qform_body<RB>(a, blockIdx.x);
+}
+
+// All three phases in one launch: a cluster of nleaf (<= 8) CTAs.  The cluster barrier orders the
+// leaves' global writes (Rstack, V, tau, partials) before the root reads them, and the root's
+// (Q_top, lambda) before the Q formation.  Gated like the three kernels: every CTA reads the same
+// flag word, so either all of them return at once or none does (no barrier is left waiting).
+// Behind the CholeskyQR2 path this turns three gated launches per mode into one (2-3 % of a
+// dimension-tree sweep on C2-C4).
+template <int RB>
+__global__ void __launch_bounds__(256) k_rq_fused(RqArgs a) {
+  if (rq_skip(a)) return;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int b = (int)cl.block_rank();
+  rq_leaf_body<RB>(a, b);
+  cl.sync();
+  if (b == 0) rq_root_body<RB>(a);
+  cl.sync();
+  rq_qform_body<RB>(a, b);
 }
 
 }  // namespace cpqr
