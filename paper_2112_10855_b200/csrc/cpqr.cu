@@ -49,6 +49,7 @@ struct TtmStep {
   const double* Q2;
   int64_t ldq2;
   int gps, nseg;
+  int cw = 8;  // slice TMA: consumer warps per CTA (4: two CTAs per SM)
 };
 
 struct DiagStep {
@@ -477,11 +478,21 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         s.kind = 6;
         const int MT = NT;
         s.gps = slice_nf(s.I2);
-        const int BN = kCW * 8 * s.gps;
-        s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8, "CPQR_ST_SLICE");
+        // 128-fibre boxes: CW = 4 consumer warps of NF = 4 fibre tiles, two CTAs per SM, so one CTA's
+        // DMMAs overlap the other's waits and each warp does twice the work per stage (C3 per-mode
+        // 524 -> 565 sweeps/s, tree 895 -> 947; CPQR_SLICE_CW=8 restores 8 warps of NF = 2)
+        static const int scw_env = getenv("CPQR_SLICE_CW") ? atoi(getenv("CPQR_SLICE_CW")) : 0;
+        if (scw_env != 8 && s.gps == 2) { s.cw = 4; s.gps = 4; }
+        const int BN = s.cw * 8 * s.gps;
+        if (s.cw == 4) {
+          const size_t stage = (size_t)BN * 128 + NQB * kBoxBytes, extra = (size_t)4 * R * R * 8;
+          s.S = std::min<int>(stages_for(stage, extra, "CPQR_ST_SLICE", 4), (int)((110 * 1024 - 3072 - extra) / stage));
+        } else {
+          s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8, "CPQR_ST_SLICE");
+        }
         s.nfb = (s.I2 + BN - 1) / BN;
         const int64_t U = s.L * s.nfb;
-        s.G = std::min<int64_t>(U, in.sms);
+        s.G = std::min<int64_t>(U, (int64_t)in.sms * (s.cw == 4 ? 2 : 1));
         int ns = 1;
         for (int64_t l = 0; l < s.L; ++l) {
           const int64_t c0 = ((l * s.nfb + 1) * s.G - 1) / U, c1 = ((l * s.nfb + s.nfb) * s.G - 1) / U;
@@ -677,20 +688,29 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
     switch (NT) { case 1: FIB(1) break; case 2: FIB(2) break; case 3: FIB(3) break; default: FIB(4) break; }
 #undef FIB
   } else if (s.kind == 6) {
-    const int BN = kCW * 8 * s.gps;
-    const size_t smem = 3072 + (size_t)s.S * ((size_t)BN * 128 + NQB * kBoxBytes) + (size_t)kCW * R * R * 8;
+    const int BN = s.cw * 8 * s.gps;
+    const size_t smem = 3072 + (size_t)s.S * ((size_t)BN * 128 + NQB * kBoxBytes) + (size_t)s.cw * R * R * 8;
 #define SLC(MTV, NFV)                                                                                      \
   {                                                                                                        \
     set_smem(k_slice_tma<MTV, NFV>, smem);                                                                 \
     k_slice_tma<MTV, NFV><<<(int)s.G, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, \
                                                                s.out, s.P, s.nslots, s.S);                 \
   }
-    if (s.gps == 4) {
+#define SLC4(MTV)                                                                                          \
+  {                                                                                                        \
+    set_smem(k_slice_tma<MTV, 4, 4>, smem);                                                                \
+    k_slice_tma<MTV, 4, 4><<<(int)s.G, 5 * 32, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R,    \
+                                                          s.out, s.P, s.nslots, s.S);                      \
+  }
+    if (s.cw == 4) {
+      switch (NT) { case 1: SLC4(1) break; case 2: SLC4(2) break; case 3: SLC4(3) break; default: SLC4(4) break; }
+    } else if (s.gps == 4) {
       switch (NT) { case 1: SLC(1, 4) break; case 2: SLC(2, 4) break; case 3: SLC(3, 4) break; default: SLC(4, 4) break; }
     } else {
       switch (NT) { case 1: SLC(1, 2) break; case 2: SLC(2, 2) break; case 3: SLC(3, 2) break; default: SLC(4, 2) break; }
     }
 #undef SLC
+#undef SLC4
   } else if (s.kind == 8) {
     const size_t smem = 3072 + (size_t)s.S * ((size_t)s.I2 * 8 * 128 + NQB * kBoxBytes);
     const int64_t units = (s.L + 7) / 8;

@@ -105,6 +105,10 @@ __device__ __forceinline__ void tma_load_3d_ef(void* dst, const CUtensorMap* map
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+template <int NTH>
+__device__ __forceinline__ void consumers_sync_n() {  // named barrier over NTH consumer threads
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory");
+}
 __device__ __forceinline__ void consumers_sync() {  // named barrier over the consumer warps only
   asm volatile("bar.sync 1, %0;\n" ::"n"(kCW * 32) : "memory");
 }
@@ -365,24 +369,24 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 // slice change the 8 warps' Y are summed in a fixed order through shared memory and written to
 // Yout[l] when the run covers the whole slice, else to the partial slot P[l][c - cta_of(l nfb)]
 // (fixed-order fix-up by k_slice_fixup).  Deterministic, no atomics.
-template <int MT, int NF>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int MT, int NF, int CW = kCW>
+__global__ void __launch_bounds__((CW + 1) * 32, CW == 4 ? 2 : 1)
 k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int I1, int I2,
             int64_t L, const double* __restrict__ Q2, int64_t ldq2, int R, double* __restrict__ Yout,
             double* __restrict__ P, int nslots, int S) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (MT + 1) / 2;
-  constexpr int BN = kCW * 8 * NF;  // fibres per unit (box height)
+  constexpr int BN = CW * 8 * NF;  // fibres per unit (box height)
   constexpr uint32_t XBYTES = BN * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
   uint8_t* st0 = tma_carve(smraw, S, full, empty);
-  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // kCW x R x R: per-warp Y
+  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // CW x R x R: per-warp Y
   const uint32_t sbase = smem_u32(st0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int RR = R * R;
-  for (int e = threadIdx.x; e < kCW * RR; e += blockDim.x) red[e] = 0.0;
+  for (int e = threadIdx.x; e < CW * RR; e += blockDim.x) red[e] = 0.0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CW); }
     fence_barrier_init();
   }
   __syncthreads();
@@ -391,7 +395,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   const int64_t G = gridDim.x;
   const int64_t u0 = (int64_t)blockIdx.x * U / G, u1 = ((int64_t)blockIdx.x + 1) * U / G;
   const int KS = (I1 + kBK - 1) / kBK;
-  if (warp == kCW) {
+  if (warp == CW) {
     if (lane == 0) {
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
@@ -493,7 +497,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
       }
     }
     const bool flush = (u + 1 == u1) || ((u + 1) / nfb != l);
-    if (flush) {  // fixed-order reduction of the kCW warps' partial Y
+    if (flush) {  // fixed-order reduction of the CW warps' partial Y
       if constexpr (YREG) {
 #pragma unroll
         for (int m = 0; m < MT; ++m)
@@ -506,7 +510,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
               yreg[m][m2][j] = 0.0;
             }
       }
-      consumers_sync();
+      consumers_sync_n<CW * 32>();
       const bool whole = (run_start == l * nfb) && (u == l * nfb + nfb - 1);
       double* dst;
       if (whole) {
@@ -515,14 +519,14 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         const int64_t first_cta = ((l * nfb + 1) * G - 1) / U;  // owner of unit l*nfb
         dst = P + (l * nslots + (blockIdx.x - first_cta)) * RR;
       }
-      for (int e = threadIdx.x; e < RR; e += kCW * 32) {
+      for (int e = threadIdx.x; e < RR; e += CW * 32) {
         double v = 0.0;
-        for (int w = 0; w < kCW; ++w) v += red[w * RR + e];
+        for (int w = 0; w < CW; ++w) v += red[w * RR + e];
         dst[e] = v;
       }
-      consumers_sync();
-      for (int e = threadIdx.x; e < kCW * RR; e += kCW * 32) red[e] = 0.0;
-      consumers_sync();
+      consumers_sync_n<CW * 32>();
+      for (int e = threadIdx.x; e < CW * RR; e += CW * 32) red[e] = 0.0;
+      consumers_sync_n<CW * 32>();
       run_start = u + 1;
     }
   }
