@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 for cfg in "2 k_strided_tma 0" "3 k_strided_tma 0" "3 k_slice_tma 0" "4 k_strided_tma 0" "4 k_slice_small_tma 0"; do
   set -- $cfg
   timeout 300 python tools/prof_case.py --config $1 --sweeps 1 --graph 0 --profile 0 > /dev/null 2>&1 && timeout 600 \
-    ncu --set full --import-source on --clock-control none -k regex:"$2" -s $3 -c 1 \
+    ncu -f --set full --import-source on --clock-control none -k regex:"$2" -s $3 -c 1 \
         -o /tmp/hbm_c$1_$2 python tools/prof_case.py --config $1 --sweeps 1 --graph 0 --profile 0 > gpurun_out/ncu_hbm_c$1_$2.log 2>&1
   ncu -i /tmp/hbm_c$1_$2.ncu-rep --page raw --csv > gpurun_out/hbm_c$1_$2.csv 2>/dev/null
 done

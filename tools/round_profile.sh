@@ -12,7 +12,9 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5_$R.csv \
       python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
 timeout 300 python tools/prof_case.py --config 5 --sweeps 1 --graph 0 --profile 0 > /dev/null 2>&1 && timeout 900 \
-  ncu --set full --import-source on --clock-control none -k regex:"k_strided_tma|k_fiber_tma" -s 4 -c 4 \
-      -o gpurun_out/c5_stream_$R python tools/prof_case.py --config 5 --sweeps 1 --graph 0 --profile 0 \
+  ncu -f --set full --import-source on --clock-control none -k regex:"k_strided_tma|k_fiber_tma" -s 4 -c 4 \
+      -o /tmp/c5_stream_$R python tools/prof_case.py --config 5 --sweeps 1 --graph 0 --profile 0 \
       > gpurun_out/ncu_full.log 2>&1
+ncu -i /tmp/c5_stream_$R.ncu-rep --page raw --csv > gpurun_out/c5_stream_$R.csv 2>/dev/null
+bash tools/prof_hbm.sh
 ls -la gpurun_out
