@@ -455,7 +455,14 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       if (in.tma && s.I1 % 2 == 0 && s.L < (1ll << 31) && bufs[0]) {
         const uint64_t d[3] = {(uint64_t)s.I1, (uint64_t)s.I2, (uint64_t)s.L};
         const uint64_t st[2] = {(uint64_t)s.I1 * 8, (uint64_t)s.I1 * s.I2 * 8};
-        const uint32_t box[3] = {16, (uint32_t)(kCW * 8 * slice_nf(s.I2)), 1};
+        // slice TMA decomposition: 128-fibre boxes run CW = 4 warps of NF = 4 fibre tiles, two CTAs
+        // per SM (C3 per-mode 524 -> 565 sweeps/s, tree 895 -> 947; CPQR_SLICE_CW=8 restores 8 warps
+        // of NF = 2); wider slices keep 256-fibre boxes of 8 warps x NF = 4 unless CPQR_SLICE_WIDE4=1
+        static const int scw_env = getenv("CPQR_SLICE_CW") ? atoi(getenv("CPQR_SLICE_CW")) : 0;
+        static const bool wide4 = getenv("CPQR_SLICE_WIDE4") && atoi(getenv("CPQR_SLICE_WIDE4")) == 1;
+        s.gps = slice_nf(s.I2);
+        if (scw_env != 8 && (s.gps == 2 || wide4)) { s.cw = 4; s.gps = 4; }
+        const uint32_t box[3] = {16, (uint32_t)(s.cw * 8 * s.gps), 1};
         tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
       }
       const bool small = tma && s.I2 <= 64 && s.I2 % 8 == 0 && NT <= 2;
@@ -477,12 +484,6 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       } else if (tma) {
         s.kind = 6;
         const int MT = NT;
-        s.gps = slice_nf(s.I2);
-        // 128-fibre boxes: CW = 4 consumer warps of NF = 4 fibre tiles, two CTAs per SM, so one CTA's
-        // DMMAs overlap the other's waits and each warp does twice the work per stage (C3 per-mode
-        // 524 -> 565 sweeps/s, tree 895 -> 947; CPQR_SLICE_CW=8 restores 8 warps of NF = 2)
-        static const int scw_env = getenv("CPQR_SLICE_CW") ? atoi(getenv("CPQR_SLICE_CW")) : 0;
-        if (scw_env != 8 && s.gps == 2) { s.cw = 4; s.gps = 4; }
         const int BN = s.cw * 8 * s.gps;
         if (s.cw == 4) {
           const size_t stage = (size_t)BN * 128 + NQB * kBoxBytes, extra = (size_t)4 * R * R * 8;
@@ -677,13 +678,24 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
     }
 #undef STR
   } else if (s.kind == 5) {
-    const size_t smem = 3072 + (size_t)s.S * (128 * 128 + NQB * kBoxBytes);
+    // 8 warps of 2 fibre tiles; CPQR_FIB_CW=4 runs 4 warps of 4 tiles, two CTAs per SM (parity-
+    // tested, but measured slower: C2 NE 2698 -> 2660 sweeps/s, neutral on C2 / C5 intermediates)
+    static const int fcw_env = getenv("CPQR_FIB_CW") ? atoi(getenv("CPQR_FIB_CW")) : 0;
+    const int cw = fcw_env == 4 ? 4 : 8;
+    const size_t stage = 128 * 128 + NQB * kBoxBytes;
+    const int S = cw == 4 ? std::min<int>(s.S, (int)((110 * 1024 - 3072) / stage)) : s.S;
+    const size_t smem = 3072 + (size_t)S * stage;
     const int64_t units = (s.F + 127) / 128;
-    const int grid = (int)std::min<int64_t>(units, sms);
+    const int grid = (int)std::min<int64_t>(units, (int64_t)sms * (cw == 4 ? 2 : 1));
 #define FIB(MTV)                                                                                   \
   {                                                                                                \
-    set_smem(k_fiber_tma<MTV>, smem);                                                              \
-    k_fiber_tma<MTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I, s.F, R, s.out, s.S);        \
+    if (cw == 4) {                                                                                 \
+      set_smem(k_fiber_tma<MTV, 4>, smem);                                                         \
+      k_fiber_tma<MTV, 4><<<grid, 5 * 32, smem, st>>>(s.mx, s.mq, s.I, s.F, R, s.out, S);          \
+    } else {                                                                                       \
+      set_smem(k_fiber_tma<MTV>, smem);                                                            \
+      k_fiber_tma<MTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I, s.F, R, s.out, S);        \
+    }                                                                                              \
   }
     switch (NT) { case 1: FIB(1) break; case 2: FIB(2) break; case 3: FIB(3) break; default: FIB(4) break; }
 #undef FIB

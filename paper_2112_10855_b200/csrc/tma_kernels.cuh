@@ -291,25 +291,26 @@ __device__ __forceinline__ void fiber_stage(uint32_t xs, uint32_t qs, int warp, 
 }
 
 // T(r, f) = sum_i Q(i, r) X(i, f), f < F (= F2 * L fibres, 2D map with L = 1).  Unit = 128 fibres.
-template <int MT>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int MT, int CW = kCW>
+__global__ void __launch_bounds__((CW + 1) * 32, CW == 4 ? 2 : 1)
 k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int I,
             int64_t F, int R, double* __restrict__ T, int S) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (MT + 1) / 2;
+  constexpr int NF = 16 / CW;  // fibre tiles of 8 per warp: CW warps x 8 NF = 128 fibres per unit
   constexpr uint32_t XBYTES = 128 * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
   uint8_t* st0 = tma_carve(smraw, S, full, empty);
   const uint32_t sbase = smem_u32(st0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kCW); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CW); }
     fence_barrier_init();
   }
   __syncthreads();
   const int64_t units = (F + 127) / 128;
   const int KS = (I + kBK - 1) / kBK;
-  if (warp == kCW) {
+  if (warp == CW) {
     if (lane == 0) {
       prefetch_tmap(&tmX);
       prefetch_tmap(&tmQ);
@@ -331,26 +332,26 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   const int g = lane >> 2, t = lane & 3;
   RingPos rp;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    double acc[MT][2][2];
+    double acc[MT][NF][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m)
 #pragma unroll
-      for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+      for (int n = 0; n < NF; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
     for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
       const int s = rp.s;
       mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE;
-      fiber_stage<MT, 2>(xs, xs + XBYTES, warp, g, t, acc);
+      fiber_stage<MT, NF>(xs, xs + XBYTES, warp, g, t, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    const int64_t f0 = u * 128 + 16 * warp;
+    const int64_t f0 = u * 128 + 8 * NF * warp;
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
       const int r = 8 * m + g;
       if (r >= R) continue;
 #pragma unroll
-      for (int n = 0; n < 2; ++n)
+      for (int n = 0; n < NF; ++n)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int64_t f = f0 + 8 * n + fmap(2 * t + j);
