@@ -642,3 +642,29 @@ def test_profile_and_timings(cp):
             assert s.timings() == [0.0] * 6  # reset by profile(reset=True)
         s.close()
     assert np.array_equal(fits[0], fits[1])
+
+
+@pytest.mark.parametrize("dims,R", [((24, 200, 6, 5), 4), ((40, 130, 7, 6), 6), ((18, 300, 5, 4), 3)])
+def test_slice_kernel_split_slices(cp, dims, R):
+    """Fused slice pass (modes 1 and 2 in one TMA pass, k_slice_tma) where a slice spans several
+    128- or 256-fibre units (I_2 = 130, 200, 300) and I_1 is ragged against the 16-row k-stage:
+    every slice's Y is summed from per-CTA partial slots by the fix-up kernel.  Y of the modes that
+    take the slice pass (n >= 2) <= 1e-11 against the oracle's Multi-TTM, and one sweep's factors
+    <= 1e-9."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=53, eta=0.05)
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    Qs = [O.qr_pos(a)[0] for a in init]
+    for n in range(2, N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+    s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_qr(X, init, 1)
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    s.close()
