@@ -419,7 +419,7 @@ struct TailNeArgs {
 // One CTA of kNeThreads threads; RB = 8/16/32 >= R.  Rows of M are solved kNeThreads at a time on
 // a shared-memory row panel with the blocked register solves of cholqr.cuh:
 // x S = m, S = L L^T  <=>  y U = m (forward, U = L^T) then x U^T = y (backward).
-constexpr int kNeThreads = 256;
+constexpr int kNeThreads = 512;
 constexpr int kNeLd = kNeThreads + 4;
 template <int RB>
 __global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
