@@ -15,8 +15,11 @@ line 8).  The same line carries "dimension_tree": the dimension-tree Multi-TTM (
 SURVEY.md §8(f) NEXT-1; two passes over X per sweep, identical mode updates up to rounding) timed
 the same way on the same resident tensor.  --tree swaps the two.
 
-Multi-GPU: launched by torch.distributed.run, one process per GPU; the NCCL id is broadcast
-over a gloo group; timing = CUDA events on the stream the library runs on, max over ranks.
+Multi-GPU: one process per GPU under torch.distributed.run (`--gpus N` without WORLD_SIZE in
+the environment re-launches itself that way); the NCCL id is broadcast over a gloo group; timing =
+CUDA events on the stream the library runs on, max over ranks.  The same slab path on one GPU
+(virtual ranks, parity tests and per-rank projections): tests/test_gpu_slabs.py,
+tools/slab_projection.py.
 """
 from __future__ import annotations
 
@@ -125,20 +128,31 @@ def load_input(conf, rank, world):
     return conf, Xc, slab, truth, init, cdir
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(conf, Xc, init, variant, sweeps=2):
-    """The oracle as it stands, on this host's cores, on a bounded sample (`sweeps` full sweeps)."""
+    """The oracle as it stands, on this host's cores, on a bounded sample: one untimed warm-up
+    sweep (PAPER.md:520 excludes the first iteration), then `sweeps` timed full sweeps."""
     import oracle as O
     X = O.as_tensor(Xc)
     cores = len(os.sched_getaffinity(0))
+    run = (lambda A0, k: O.cp_als_ne(X, A0, k)) if variant == "NE" else \
+        (lambda A0, k: O.cp_als_qr(X, A0, k, variant=variant, tau=conf.svd_tau))
+    A1 = run(init, 1)["factors"]
     t0 = time.perf_counter()
-    if variant == "NE":
-        O.cp_als_ne(X, init, sweeps)
-    else:
-        O.cp_als_qr(X, init, sweeps, variant=variant, tau=conf.svd_tau)
+    run(A1, sweeps)
     dt = time.perf_counter() - t0
-    return {"value": sweeps / dt, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
-            "sample": f"{sweeps} full CP-ALS-{variant} sweeps of {conf.name} from the shared init, "
-                      f"numpy/OpenBLAS fp64, wall clock"}
+    return {"value": sweeps / dt, "unit": "sweeps/s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
+            "sample": f"{sweeps} full CP-ALS-{variant} sweeps of {conf.name} after 1 untimed sweep from the "
+                      f"shared init, numpy/OpenBLAS fp64, wall clock"}
 
 
 def run_reference(args):
@@ -164,11 +178,31 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (synth.py seeded recipe of BASELINE.json config; no dataset)",
             "config": bench_config(conf, variant, world, bool(args.tree and variant != "NE" and conf.N >= 3)),
-            "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "sweeps/s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                              "sample": f"{args.steps} full sweeps of {conf.name} after {args.warmup} warm-up"},
             "e2e": {"value": v, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def relaunch(n):
+    """`--gpus N` outside torch.distributed.run: re-launch this command as N ranks, one per GPU."""
+    import socket
+    import torch
+    if args_impl_is_gpu() and torch.cuda.device_count() < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {torch.cuda.device_count()} "
+              f"(the one-GPU slab path is tools/slab_projection.py)", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def args_impl_is_gpu():
+    return "reference" not in sys.argv[1:]
 
 
 def main():
@@ -183,6 +217,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--tree", action="store_true", help="headline = dimension-tree Multi-TTM")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -41,7 +41,10 @@ enum {
   CPQR_ECUDA = 3,      /* CUDA runtime error (message in cpqr_last_error) */
   CPQR_ENCCL = 4,      /* NCCL error or NCCL unavailable with world > 1 */
   CPQR_ESTATE = 5,     /* call out of order (no tensor / no factors yet) */
-  CPQR_EDIVERGED = 6   /* non-finite factor produced; state left at the last finite mode */
+  CPQR_EDIVERGED = 6   /* a non-finite lambda appeared during the sweeps: the factors are then
+                          non-finite (the remaining modes of the call ran on them); restore a
+                          finite state with cpqr_set_factors / cpqr_init_factors, which clear
+                          the condition */
 };
 
 /* Variant of the per-mode LS solve (substitution or SVD; Alg. 1: normal eqs). */
@@ -59,7 +62,8 @@ typedef enum {
   CPQR_MEM_DEVICE_BORROW = 2  /* device memory; used in place, caller keeps it alive */
 } cpqr_mem;
 
-/* Non-fatal condition flags (cpqr_get_flags), OR-ed over all sweeps run so far. */
+/* Non-fatal condition flags (cpqr_get_flags), OR-ed over all sweeps run since the last
+ * cpqr_set_factors / cpqr_init_factors / cpqr_set_tensor (each of which clears them). */
 enum {
   CPQR_FLAG_ILLCOND_R0 = 1u,      /* QR variant: min|R0_jj| <= R^(N-1)*eps*max|R0_jj| (reading 17) */
   CPQR_FLAG_NE_CHOL_FALLBACK = 2u,/* NE: Cholesky met a non-positive pivot; LU used (reading 18) */
@@ -68,6 +72,16 @@ enum {
                                      normal equations lose > 8 digits; a robust driver switches to
                                      QR / QR-SVD */
 };
+
+/* How the ranks of the slab data parallelism (cpqr_options.world > 1) exchange W_n. */
+typedef enum {
+  CPQR_COMM_NCCL = 0,  /* one process (context) per GPU; ncclAllReduce / ncclAllGather over NVLink */
+  CPQR_COMM_LOCAL = 1  /* virtual ranks: ONE context on one device runs all `world` slabs in rank
+                          order (each with its own plans, TMA maps and slab of Q_N) and combines
+                          them with a fixed-order sum kernel (modes n < N) or one device copy per
+                          rank (mode N); `rank` is ignored.  The multi-GPU code path on one GPU, for
+                          parity tests and per-rank timing projections. */
+} cpqr_comm;
 
 typedef struct cpqr_options {
   uint32_t struct_size;   /* = sizeof(cpqr_options); ABI versioning */
@@ -84,17 +98,23 @@ typedef struct cpqr_options {
                              T_R = X x_{k<h} Q_k^T, h = ceil(N/2), so a sweep streams X twice
                              instead of N times; Y_(n) equals the per-mode Multi-TTM up to
                              rounding.  0 (default) = one pass over X per mode (Alg. 2 line 8). */
+  int32_t comm;           /* cpqr_comm (world > 1): CPQR_COMM_NCCL (default) or CPQR_COMM_LOCAL */
 } cpqr_options;
 
 /* Fills *opt with defaults: svd_tau = -1, FAST fit, device 0, own stream, world 1,
- * use_graph 1, profile 0, mttm_tree 0. */
+ * use_graph 1, profile 0, mttm_tree 0, comm NCCL. */
 void cpqr_default_options(cpqr_options* opt);
 
 typedef struct cpqr_ctx cpqr_ctx;
 
 /* Create a solver for an N-way tensor of global dims[0..N-1] and CP rank R.
- * Preconditions: 2 <= N <= 8; 1 <= R <= 32; dims[k] >= R for all k (tall factors, PAPER.md:33;
- * reading 27); with world = p > 1, the last mode is split into slabs (cpqr_set_tensor).
+ * Preconditions: 2 <= N <= 8; 1 <= R <= 32; R <= dims[k] < 2^31 for all k (tall factors,
+ * PAPER.md:33; reading 27); 1 <= world <= 16 and world divides dims[N-1]: with world = p > 1 the
+ * last mode is split into p equal slabs (cpqr_set_tensor), every variant (NE, QR, SVD) and both
+ * Multi-TTM schedules run slab-parallel, the factors are replicated (identical on every rank).
+ * Factor heights: any I_n (CholeskyQR2 for every height; its Householder fallback is the
+ * register / shared-memory TSQR up to ~3200 rows at R = 32 and a one-CTA global-memory
+ * Householder beyond, slow but exact).
  * Errors: EINVAL, ENOMEM, ECUDA, ENCCL. */
 cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
                         const cpqr_options* opt, cpqr_ctx** out);
@@ -102,8 +122,11 @@ cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
 /* Set the local tensor slab X(:, ..., :, slab_begin:slab_end) (0-based, end exclusive, on the
  * last mode), column-major I_1 x ... x I_{N-1} x (slab_end - slab_begin) = a contiguous block
  * of the global column-major tensor at element offset slab_begin * prod_{k<N} I_k.
- * world = 1 requires [0, I_N).  Computes ||X||^2 (all-reduced across ranks).
- * Errors: EINVAL (slab range / NULL), ENOMEM, ECUDA, ENCCL. */
+ * world = 1 requires [0, I_N); with NCCL ranks, this rank's slab [r I_N/p, (r+1) I_N/p).  With
+ * CPQR_COMM_LOCAL either the whole tensor [0, I_N) (split into the p slabs) or one virtual
+ * rank's slab (the sweep needs every slab set).  Computes ||X||^2 (summed over the ranks) and
+ * clears the condition flags.
+ * Errors: EINVAL (slab range / NULL / mem kind), ENOMEM, ECUDA, ENCCL. */
 cpqr_status cpqr_set_tensor(cpqr_ctx* ctx, const double* x, int64_t slab_begin,
                             int64_t slab_end, int mem);
 
@@ -186,6 +209,14 @@ cpqr_status cpqr_launches_per_sweep(cpqr_ctx* ctx, int64_t* n);
  *   W_out : I_n x R column-major (global rows). */
 cpqr_status cpqr_debug_mode(cpqr_ctx* ctx, int n, const double* const* Q_override,
                             double* Y_out, double* Q0_out, double* R0_out, double* W_out);
+
+/* The Multi-TTM plan of mode n (0-based) on slab `slab` (0 unless CPQR_COMM_LOCAL), for the
+ * plan tables of DESIGN.md §8 and the contraction-order tests: writes
+ * min(cap, #steps) rows of 6 int64 to info -- kernel kind (0/4 strided, 1/5 fibre, 2/6/8 fused
+ * slice, 3/7 partial-sum fix-up, 100 NE Khatri-Rao diagonal), bitmask of the contracted global
+ * modes, input elements, output elements, flops, 1 if the step reads X -- and #steps to *nsteps.
+ * Errors: EINVAL, ESTATE (no dense tensor set). */
+cpqr_status cpqr_debug_plan(cpqr_ctx* ctx, int n, int slab, int64_t* info, int cap, int* nsteps);
 
 /* Stand-alone kernels exposed for parity tests (host in/out, column-major):
  * thin Householder QR of an m x R matrix (m >= R): Q (m x R), Rf (R x R), diag(Rf) >= 0. */

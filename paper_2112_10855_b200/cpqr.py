@@ -24,13 +24,14 @@ NE, QR, SVD = 0, 1, 2
 VARIANTS = {"NE": NE, "QR": QR, "SVD": SVD}
 FIT_FAST, FIT_DIRECT = 0, 1
 MEM_HOST, MEM_DEVICE_COPY, MEM_DEVICE_BORROW = 0, 1, 2
+COMM_NCCL, COMM_LOCAL = 0, 1
 FLAG_ILLCOND_R0, FLAG_NE_CHOL_FALLBACK, FLAG_SVD_TRUNCATED, FLAG_NE_ILLCOND = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE", 6: "EDIVERGED"}
 
 EXPORTS = [
     "cpqr_default_options", "cpqr_create", "cpqr_set_tensor", "cpqr_set_factors", "cpqr_init_factors",
     "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile", "cpqr_get_timings",
-    "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_qr", "cpqr_debug_svd_solve",
+    "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_plan", "cpqr_debug_qr", "cpqr_debug_svd_solve",
     "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
 ]
 
@@ -39,7 +40,7 @@ class Options(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("svd_tau", C.c_double), ("fit_mode", C.c_int32),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_id", C.c_uint8 * 128), ("use_graph", C.c_int32), ("profile", C.c_int32),
-                ("mttm_tree", C.c_int32)]
+                ("mttm_tree", C.c_int32), ("comm", C.c_int32)]
 
 
 class Profile(C.Structure):
@@ -68,6 +69,7 @@ _sig = {
     "cpqr_debug_mode": (C.c_int32, [_P, C.c_int, C.POINTER(_DP), _DP, _DP, _DP, _DP]),
     "cpqr_debug_qr": (C.c_int32, [_P, _DP, C.c_int64, _DP, _DP]),
     "cpqr_debug_svd_solve": (C.c_int32, [_P, _DP, _DP, C.c_int64, C.c_double, _DP, C.POINTER(C.c_int)]),
+    "cpqr_debug_plan": (C.c_int32, [_P, C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int)]),
     "cpqr_destroy": (C.c_int32, [_P]),
     "cpqr_status_string": (C.c_char_p, [C.c_int32]),
     "cpqr_last_error": (C.c_char_p, [_P]),
@@ -135,7 +137,11 @@ class CPQR:
     """One CP-ALS(-QR) solver over a (slab of a) dense fp64 tensor on one GPU."""
 
     def __init__(self, dims, R, variant="QR", svd_tau=-1.0, fit_mode="fast", device=0, stream=None,
-                 rank=0, world=1, nccl_id=None, use_graph=True, profile=False, tree=False):
+                 rank=0, world=1, nccl_id=None, use_graph=True, profile=False, tree=False, comm="nccl"):
+        """world > 1 with comm="nccl": this process is rank `rank` of `world` (one GPU each, slab
+        of the last mode, NCCL id from nccl_unique_id() on rank 0).  comm="local": ONE context on
+        this device runs all `world` slabs as virtual ranks (cpqr.h CPQR_COMM_LOCAL); set_tensor
+        then takes the whole tensor."""
         self.dims = tuple(int(d) for d in dims)
         self.N, self.R = len(self.dims), int(R)
         self.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
@@ -151,9 +157,10 @@ class CPQR:
         opt.use_graph = 1 if use_graph else 0
         opt.profile = 1 if profile else 0
         opt.mttm_tree = 1 if tree else 0  # dimension-tree Multi-TTM (QR/SVD, N >= 3)
-        self.rank, self.world = int(rank), int(world)
+        opt.comm = {"nccl": COMM_NCCL, "local": COMM_LOCAL}[comm]
+        self.rank, self.world, self.comm = int(rank), int(world), comm
         per = self.dims[-1] // self.world
-        self.slab = (per * self.rank, per * (self.rank + 1))
+        self.slab = (0, self.dims[-1]) if comm == "local" else (per * self.rank, per * (self.rank + 1))
         d = (C.c_int64 * self.N)(*self.dims)
         h = _P()
         st = _lib.cpqr_create(self.N, d, self.R, self.variant, C.byref(opt), C.byref(h))
@@ -179,9 +186,11 @@ class CPQR:
             pass
 
     # ---------------------------------------------------------------------- API
-    def set_tensor(self, X, copy=False):
-        """X: numpy array (host) or torch tensor (host or CUDA), C-contiguous (I_N_local..I_1)."""
-        b, e = self.slab
+    def set_tensor(self, X, copy=False, slab=None):
+        """X: numpy array (host) or torch tensor (host or CUDA), C-contiguous (I_N_local..I_1).
+        slab=(b, e): the range of the last mode X holds (default: this rank's slab; comm="local":
+        the whole tensor, or one virtual rank's slab)."""
+        b, e = slab if slab is not None else self.slab
         try:
             import torch
             is_torch = isinstance(X, torch.Tensor)
@@ -287,6 +296,23 @@ class CPQR:
         self._check(_lib.cpqr_debug_mode(self._h, int(n), qp, Y.ctypes.data_as(_DP), Q0.ctypes.data_as(_DP),
                                          R0.ctypes.data_as(_DP), W.ctypes.data_as(_DP)))
         return dict(Y=Y, Q0=Q0, R0=R0, W=W)
+
+    PLAN_KINDS = {0: "strided", 1: "fiber", 2: "slice", 3: "slice-reduce", 4: "strided-tma", 5: "fiber-tma",
+                  6: "slice-tma", 7: "slice-fixup", 8: "slice-small-tma", 100: "ne-diag"}
+
+    def debug_plan(self, n, slab=0):
+        """The Multi-TTM plan of mode n on one slab (cpqr_debug_plan): a list of dicts with the
+        kernel kind, the contracted modes, input / output elements and flops of every step."""
+        cap = 64
+        buf = (C.c_int64 * (6 * cap))()
+        cnt = C.c_int()
+        self._check(_lib.cpqr_debug_plan(self._h, int(n), int(slab), buf, cap, C.byref(cnt)))
+        out = []
+        for i in range(cnt.value):
+            kind, mask, ni, no, fl, xp = (int(v) for v in buf[6 * i:6 * i + 6])
+            out.append(dict(kind=self.PLAN_KINDS.get(kind, kind), modes=[k for k in range(self.N) if mask >> k & 1],
+                            in_elems=ni, out_elems=no, flops=fl, x_pass=bool(xp)))
+        return out
 
     def debug_qr(self, A):
         A = np.asfortranarray(A, dtype=np.float64)

@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kMaxN = 8;
 constexpr int kMaxR = 32;
+constexpr int kMaxWorld = kMaxRanks;      // ranks (NCCL) or virtual ranks (CPQR_COMM_LOCAL)
 constexpr size_t kQSmemMax = 96 * 1024;   // Q panel budget per CTA (2 CTAs / SM)
 constexpr int64_t kQ0MaxSlices = 64;      // k-step slices of k_q0_apply_tc (partials buffer)
 
@@ -50,6 +51,7 @@ struct TtmStep {
   int64_t ldq2;
   int gps, nseg;
   int cw = 8;  // slice TMA: consumer warps per CTA (4: two CTAs per SM)
+  unsigned modes = 0;  // contracted modes (bit k = mode k of the global tensor)
 };
 
 struct DiagStep {
@@ -60,6 +62,7 @@ struct DiagStep {
   int k, rm;
   const double* Ak;
   int64_t lda;
+  int mode;  // global mode contracted
 };
 
 struct Plan {
@@ -75,21 +78,38 @@ struct Plan {
   size_t tree_elems = 0;  // dimension tree: size of the half intermediate this plan writes
 };
 
+// One rank's slab of the tensor (slab data parallelism over the last mode): the
+// global range [b, e) of mode N, the local dims, the tensor pointer, the per-mode plans (their TMA
+// maps encode this slab's X and the matching rows of Q_N), the dimension-tree buffer and the
+// partial W_n (modes n < N) or local rows of W_N.  A context holds one slab (single GPU, or one
+// NCCL rank) or, with CPQR_COMM_LOCAL, all p slabs of p virtual ranks run in rank order.
+struct Slab {
+  int64_t b = 0, e = 0;
+  int64_t ldims[kMaxN] = {0};
+  int64_t numel = 0;
+  const double* X = nullptr;
+  double* Xown = nullptr;
+  size_t Xown_elems = 0;
+  bool have = false;
+  Plan plans[kMaxN];
+  double* dTree = nullptr;
+  size_t tree_alloc = 0;
+  double* dWloc = nullptr;
+};
+
 }  // namespace
 
 struct cpqr_ctx {
   int N = 0, R = 0, variant = 1;
   int64_t dims[kMaxN] = {0};
-  int64_t ldims[kMaxN] = {0};
-  int64_t slab_b = 0, slab_e = 0, numel = 0;
+  int nslab = 1;            // slabs this context runs: 1, or world with CPQR_COMM_LOCAL
+  bool local = false;       // CPQR_COMM_LOCAL: p virtual ranks on one device, combined in rank order
+  Slab slabs[kMaxWorld];
   cpqr_options opt;
   int sms = 148;
   cudaStream_t st = nullptr;
   cudaStream_t user = nullptr;
   ncclComm_t comm = nullptr;
-  const double* X = nullptr;
-  double* Xown = nullptr;
-  size_t Xown_elems = 0;
   bool have_tensor = false, have_factors = false;
   double *dA[kMaxN] = {0}, *dQ[kMaxN] = {0}, *dRk[kMaxN] = {0}, *dG[kMaxN] = {0};
   double *dQt[kMaxN] = {0}, *dAt[kMaxN] = {0};  // transposed, zero-padded (I_k x RQ) TMA panels
@@ -110,8 +130,6 @@ struct cpqr_ctx {
   double *dVn = nullptr, *dVq1 = nullptr, *dVgp = nullptr, *dVr1 = nullptr, *dVr2 = nullptr;
   bool tree = false;       // dimension-tree Multi-TTM (opt.mttm_tree, QR/SVD, N >= 3)
   int tree_h = 0;
-  double* dTree = nullptr;
-  size_t tree_alloc = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t evf = nullptr, evj = nullptr;
   double *dRstack = nullptr, *dV = nullptr, *dtauv = nullptr, *dQtop = nullptr, *dinner = nullptr;
@@ -120,8 +138,9 @@ struct cpqr_ctx {
   int factor_qr_mode = 0;  // 0 auto (CholeskyQR2, Householder fallback), 1 Householder only
   int nparts = 0;
   int stream_sms = 148;  // CTAs of the stream-X kernels (one SM left to the concurrent V_n QR)
-  double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWloc = nullptr,
-         *dWp = nullptr, *dAhat = nullptr;
+  double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWp = nullptr,
+         *dAhat = nullptr;
+  double* dnX2p = nullptr;   // per-slab partial ||X||^2 (CPQR_COMM_LOCAL), summed in rank order
   unsigned* dq0cnt = nullptr;  // per-row-block arrival counters of k_q0_apply_tc (self re-arming)
   double* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
@@ -130,15 +149,20 @@ struct cpqr_ctx {
   int* dperm = nullptr;
   double* dKrWork = nullptr;
   double *dnX2 = nullptr, *dfit = nullptr, *dfits = nullptr, *dred = nullptr;
+  size_t dred_elems = 0;
   int fits_cap = 0;
   unsigned* dflags = nullptr;
   double* hpin = nullptr;  // pinned: [0] fit, [1] flags
-  Plan plans[kMaxN];
   bool plans_valid = false;
   cudaGraphExec_t gexec = nullptr;
   bool graph_valid = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t evp[16] = {};
+  // profiling (opt.profile): events recorded at phase boundaries; the time since the previous
+  // mark is attributed to the mark's phase (cpqr_get_profile ms[0..5])
+  std::vector<cudaEvent_t> evp;
+  std::vector<int> evphase;
+  std::vector<int64_t> evlaunch;
+  int nmarks = 0;
   cpqr_profile prof;
   int64_t launch_count = 0;
   int64_t launches_per_sweep = -1;
@@ -402,6 +426,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   };
   auto emit_ttm = [&](int k) {
     TtmStep s{};
+    s.modes = 1u << k;
     s.in = src;
     s.out = out_override ? out_override : bufs[nb];
     s.Q = in.Q[k];
@@ -442,6 +467,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   // fused contraction of modes 0 and 1 of src (fused slice kernels, Alg. 2 line 8)
   auto emit_slice = [&]() {
       TtmStep s{};
+      s.modes = 3u;
       s.kind = 2;
       s.in = src;
       s.I1 = (int)cur[0];
@@ -539,8 +565,12 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       advance(out_override ? out_override : bufs[nb]);
   };
   if (in.ne) {
-    // MTTKRP M_n = X_(n) Z_n: one dense TTM with A_k, then Khatri-Rao-diagonal contractions.
-    const int rmode = (n >= 1) ? 0 : N - 1;
+    // MTTKRP M_n = X_(n) Z_n: one dense TTM with A_k over the largest local dimension (
+    // ties: mode 1 for n >= 1, else the last mode -- with slabs the last mode is the smallest), then
+    // Khatri-Rao-diagonal contractions.
+    int rmode = (n >= 1) ? 0 : N - 1;
+    for (int k = N - 1; k >= 0; --k)
+      if (k != n && cur[k] > cur[rmode]) rmode = k;
     emit_ttm(rmode);
     int nd = N;
     int64_t dd[kMaxN];
@@ -562,6 +592,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       ds.rm = rpos;
       ds.Ak = in.Q[k];
       ds.lda = in.ldq[k];
+      ds.mode = k;
       p.diags.push_back(ds);
       for (int d = pos; d < nd - 1; ++d) { dd[d] = dd[d + 1]; orig[d] = orig[d + 1]; }
       --nd;
@@ -571,7 +602,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     p.Y = src;
     p.nd = nd;
     for (int d = 0; d < nd; ++d) p.ydims[d] = dd[d];
-    p.m_rowmajor = (n >= 1) ? 1 : 0;  // (R, I_n) column-major == row-major I_n x R
+    p.m_rowmajor = (rmode < n) ? 1 : 0;  // (R, I_n) column-major == row-major I_n x R
     return;
   }
   if (in.tree && N >= 3) {
@@ -584,7 +615,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     if (in.tree_fresh) {
       std::vector<int> ord;
       if (left) {
-        for (int k = N - 1; k >= h; --k) ord.push_back(k);  // last mode first: strided, B = 1
+        // the right half's modes by decreasing LOCAL dimension, ties last mode first
+        // (strided, B = 1): with slabs the slab mode is the smallest and goes last
+        for (int k = N - 1; k >= h; --k) ord.push_back(k);
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cur[a] > cur[b]; });
         for (size_t q = 0; q < ord.size(); ++q) {
           if (q + 1 == ord.size()) out_override = in.tbuf;
           emit_ttm(ord[q]);
@@ -619,8 +653,14 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     emit_slice();
     for (int k = 2; k < N; ++k) if (k != n) todo.push_back(k);
   } else if (N >= 3) {
-    emit_ttm(N - 1);
-    for (int k = 0; k < N - 1; ++k) if (k != n) todo.push_back(k);
+    // n < 2: the stream pass contracts the largest LOCAL dimension first; ties go to
+    // the last mode (strided kernel, B = 1, the largest contiguous GEMM).  With p > 1 slabs the last
+    // mode is the smallest local one and is contracted last, so every intermediate scales as 1/p.
+    int f = N - 1;
+    for (int k = N - 2; k >= 0; --k)
+      if (k != n && cur[k] > cur[f]) f = k;
+    emit_ttm(f);
+    for (int k = 0; k < N; ++k) if (k != n && k != f) todo.push_back(k);
   } else {
     todo.push_back(1 - n);
   }
@@ -775,11 +815,11 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
   return CPQR_OK;
 }
 
-void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = nullptr,
+void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* const* Qover = nullptr,
                   const double* const* Qtover = nullptr) {
   const bool ne = c->variant == CPQR_NE;
-  in.X = c->X;
-  in.ld = c->ldims;
+  in.X = sl.X;
+  in.ld = sl.ldims;
   in.N = c->N;
   in.R = c->R;
   in.n = n;
@@ -790,7 +830,7 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
   in.tree = c->tree && !ne;
   in.h = c->tree_h;
   in.tree_fresh = (n == 0 || n == c->tree_h);
-  in.tbuf = c->dTree;
+  in.tbuf = sl.dTree;
   in.RQ = c->RQ;
   for (int k = 0; k < c->N; ++k) {
     const double* base = ne ? c->dA[k] : c->dQ[k];
@@ -798,31 +838,36 @@ void fill_plan_in(cpqr_ctx* c, PlanIn& in, int n, const double* const* Qover = n
     if (Qover && Qover[k]) base = Qover[k];
     if (Qtover && Qtover[k]) bt = Qtover[k];
     const bool last = (k == c->N - 1);
-    in.Q[k] = last ? base + c->slab_b : base;
-    in.Qt[k] = last ? bt + c->slab_b * c->RQ : bt;
+    in.Q[k] = last ? base + sl.b : base;
+    in.Qt[k] = last ? bt + sl.b * c->RQ : bt;
     in.ldq[k] = c->dims[k];
   }
 }
 
 cpqr_status build_plans(cpqr_ctx* c) {
   size_t mb = 0, mp = 0, mt = 0;
-  for (int n = 0; n < c->N; ++n) {
-    PlanIn in{};
-    fill_plan_in(c, in, n);
-    in.tma = false;  // sizing pass (no maps)
-    Plan tmp;
-    double* nob[2] = {nullptr, nullptr};
-    plan_mode(in, tmp, nob, nullptr);
-    mb = std::max(mb, tmp.max_buf);
-    mp = std::max(mp, tmp.part);
-    mt = std::max(mt, tmp.tree_elems);
-    // TMA slice partials: L * nslots * R^2 with nslots <= ceil(nfb*G/U)+1 <= 2 + nfb
-    if (c->N >= 3 && n >= 2) {
-      const int64_t L = prod(c->ldims, 2, c->N);
-      const int nfb = (int)((c->ldims[1] + 127) / 128);
-      mp = std::max(mp, (size_t)L * (size_t)(nfb + 2) * c->R * c->R);
+  for (int q = 0; q < c->nslab; ++q) {
+    const Slab& sl = c->slabs[q];
+    for (int n = 0; n < c->N; ++n) {
+      PlanIn in{};
+      fill_plan_in(c, sl, in, n);
+      in.tma = false;  // sizing pass (no maps)
+      Plan tmp;
+      double* nob[2] = {nullptr, nullptr};
+      plan_mode(in, tmp, nob, nullptr);
+      mb = std::max(mb, tmp.max_buf);
+      mp = std::max(mp, tmp.part);
+      mt = std::max(mt, tmp.tree_elems);
+      // TMA slice partials: L * nslots * R^2 with nslots <= ceil(nfb*G/U)+1 <= 2 + nfb
+      if (c->N >= 3 && n >= 2) {
+        const int64_t L = prod(sl.ldims, 2, c->N);
+        const int nfb = (int)((sl.ldims[1] + 127) / 128);
+        mp = std::max(mp, (size_t)L * (size_t)(nfb + 2) * c->R * c->R);
+      }
     }
   }
+  // the ping-pong intermediates and slice partials are shared by the slabs (run in turn on one
+  // stream); each slab keeps its own dimension-tree buffer (it lives across modes)
   if (mb > c->buf_elems) {
     for (int i = 0; i < 2; ++i) { if (c->buf[i]) cudaFree(c->buf[i]); c->buf[i] = nullptr; }
     for (int i = 0; i < 2; ++i)
@@ -830,12 +875,15 @@ cpqr_status build_plans(cpqr_ctx* c) {
         return fail(c, CPQR_ENOMEM, "intermediate buffers (%zu doubles)", mb);
     c->buf_elems = mb;
   }
-  if (mt > c->tree_alloc) {
-    if (c->dTree) cudaFree(c->dTree);
-    c->dTree = nullptr;
-    if (dmalloc(&c->dTree, mt * sizeof(double)) != cudaSuccess)
-      return fail(c, CPQR_ENOMEM, "dimension-tree buffer (%zu doubles)", mt);
-    c->tree_alloc = mt;
+  for (int q = 0; q < c->nslab; ++q) {
+    Slab& sl = c->slabs[q];
+    if (mt > sl.tree_alloc) {
+      if (sl.dTree) cudaFree(sl.dTree);
+      sl.dTree = nullptr;
+      if (dmalloc(&sl.dTree, mt * sizeof(double)) != cudaSuccess)
+        return fail(c, CPQR_ENOMEM, "dimension-tree buffer (%zu doubles)", mt);
+      sl.tree_alloc = mt;
+    }
   }
   if (mp > c->part_elems) {
     if (c->dPart) cudaFree(c->dPart);
@@ -844,18 +892,34 @@ cpqr_status build_plans(cpqr_ctx* c) {
       return fail(c, CPQR_ENOMEM, "slice partials (%zu doubles)", mp);
     c->part_elems = mp;
   }
-  for (int n = 0; n < c->N; ++n) {
-    PlanIn in{};
-    fill_plan_in(c, in, n);
-    plan_mode(in, c->plans[n], c->buf, c->dPart);
+  for (int q = 0; q < c->nslab; ++q) {
+    Slab& sl = c->slabs[q];
+    for (int n = 0; n < c->N; ++n) {
+      PlanIn in{};
+      fill_plan_in(c, sl, in, n);
+      plan_mode(in, sl.plans[n], c->buf, c->dPart);
+    }
   }
   c->plans_valid = true;
   return CPQR_OK;
 }
 
 // ----------------------------------------------------------------------------- helpers
-void prof_mark(cpqr_ctx* c, int idx) {
-  if (c->opt.profile) cudaEventRecord(c->evp[idx], c->st);
+// phase marks (opt.profile only; never inside graph capture): the device time since the previous
+// mark is attributed to `phase` (cpqr_profile.ms index); phase -1 starts a new interval
+void prof_mark(cpqr_ctx* c, int phase) {
+  if (!c->opt.profile) return;
+  if (c->nmarks == (int)c->evp.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    c->evp.push_back(e);
+    c->evphase.push_back(-1);
+    c->evlaunch.push_back(0);
+  }
+  cudaEventRecord(c->evp[c->nmarks], c->st);
+  c->evphase[c->nmarks] = phase;
+  c->evlaunch[c->nmarks] = c->launch_count;
+  ++c->nmarks;
 }
 
 int rb_for(int R) { return R <= 8 ? 8 : (R <= 16 ? 16 : 32); }
@@ -890,12 +954,6 @@ cpqr_status launch_solve(cpqr_ctx* c, const double* W, int In, bool fit, int* nt
   return CPQR_OK;
 }
 
-cpqr_status launch_normalize(cpqr_ctx* c, int In, double* A) {
-  k_normalize<<<1, 1024, 0, c->st>>>(c->dAhat, c->dred, c->nparts, rb_for(c->R), In, c->R, A, c->dlam, c->dinner,
-                                     c->dflags);
-  CKL();
-  return CPQR_OK;
-}
 
 // TSQR launcher.  solve = false: thin QR of the m x R column-major A -> Q, Qt, Rn.
 // solve = true: the fused per-mode tail -- Ahat from W (and R0 / M), lambda, A_n = Ahat/lambda into
@@ -948,85 +1006,56 @@ cpqr_status launch_cq_compact(cpqr_ctx* c, const CqArgs& q, int RB, int tb, cuda
   return CPQR_OK;
 }
 
+// Multi-kernel CholeskyQR2 of the m x R column-major q.A (row blocks of 256 rows) on stream st.
+cpqr_status launch_cq_multi(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
+  const int RB = rb_for(c->R);
+  const int tb = 32 * ((q.mb + 31) / 32);
+  const size_t psm = (size_t)(q.mb | 1) * c->R * 8;
+  cq_multi_attrs();
+#define CQM(RBV)                                                   \
+  {                                                                \
+    k_cq_gram1<RBV><<<q.nb, tb, psm, st>>>(q); CKL();              \
+    k_cq_chol1<<<1, 256, 0, st>>>(q); CKL();                       \
+    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 1); CKL();           \
+    k_cq_chol2<<<1, 256, 0, st>>>(q, nullptr); CKL();              \
+    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 2); CKL();           \
+  }
+  switch (RB) { case 8: CQM(8) break; case 16: CQM(16) break; default: CQM(32) break; }
+#undef CQM
+  return CPQR_OK;
+}
+
 cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const double* W, double* Q,
                         double* Qt, double* Rn, double* Aout, bool do_fit) {
   const int R = c->R, RB = rb_for(R);
-  int nleaf = std::max(1, std::min(8, (m + 127) / 128));
-  int mb = (m + nleaf - 1) / nleaf;
-  while (nleaf > 1 && m - (nleaf - 1) * mb < R) { --nleaf; mb = (m + nleaf - 1) / nleaf; }
-  const size_t leaf_smem = (size_t)mb * R * 8, qf_smem = 2 * leaf_smem,
-               root_smem = (size_t)std::max(nleaf, 2) * R * R * 8;
-  if (qf_smem > 200 * 1024) {  // very tall factors: unfused kernels, global-memory Householder
-    if (do_fit) return fail(c, CPQR_EINVAL, "factor too tall for the fused tail with fast fit");
-    if (solve) {
-      TRY(launch_solve(c, W, m, false, nullptr));
-      TRY(launch_normalize(c, m, Aout));
-      A = Aout;
-    }
-    k_factor_qr<<<1, 1024, 0, c->st>>>(A, m, R, Q, Rn);
-    CKL();
-    k_transpose_pad<<<64, 256, 0, c->st>>>(Q, m, m, R, c->RQ, Qt);
-    CKL();
-    return CPQR_OK;
-  }
-  // fast path: CholeskyQR2 (cholqr.cuh); the Householder kernels below then run gated
+  if (solve && c->variant == CPQR_SVD && !c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
+  auto cq_args = [&](int nb) {
+    CqArgs q{};
+    q.A = A; q.m = m; q.R = R; q.nb = nb; q.mb = (m + nb - 1) / nb; q.solve = solve ? 1 : 0; q.W = W;
+    q.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0; q.R0 = c->dR0; q.variant = c->variant;
+    q.Ahat = c->dAhat; q.Q1 = c->dQ1; q.Gp = c->dGp; q.innerp = c->dinnerp; q.R1 = c->dR1; q.R2 = c->dR2;
+    q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
+    q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
+    return q;
+  };
+  // fast path: CholeskyQR2 (cholqr.cuh), any m; the Householder fallback below then runs gated
+  // (only when the device-side kappa / orthogonality guard rejected the CholeskyQR2 result)
   bool gated = false;
+  int cq_nb = 0;
   const int nbq = (m + 255) / 256;
   if (c->factor_qr_mode == 0 && nbq <= 8 && !getenv("CPQR_CQ_MULTI")) {  // single cluster launch
-    CqArgs q{};
-    const int mbq = (m + nbq - 1) / nbq;
-    q.A = A; q.m = m; q.R = R; q.nb = nbq; q.mb = mbq; q.solve = solve ? 1 : 0; q.W = W;
-    q.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0; q.R0 = c->dR0; q.variant = c->variant;
-    q.Ahat = c->dAhat; q.Q1 = c->dQ1; q.Gp = c->dGp; q.innerp = c->dinnerp; q.R1 = c->dR1; q.R2 = c->dR2;
-    q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
-    q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
-    if (solve && c->variant == CPQR_SVD) {
-      if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
-    }
+    const CqArgs q = cq_args(nbq);
     // >= 8 warps even for short factors: the 2-D Cholesky maps its columns to 8 warps (the rolled
     // fallback for fewer warps cost ~680 vs ~440 cycles per column); spare threads own no row
-    TRY(launch_cq_compact(c, q, RB, std::max(256, 32 * ((mbq + 31) / 32)), c->st));
+    TRY(launch_cq_compact(c, q, RB, std::max(256, 32 * ((q.mb + 31) / 32)), c->st));
     gated = true;
-  } else if (c->factor_qr_mode == 0) {
-    CqArgs q{};
-    const int nb = (m + 255) / 256, mbq = (m + nb - 1) / nb;
-    q.A = A; q.m = m; q.R = R; q.nb = nb; q.mb = mbq; q.solve = solve ? 1 : 0; q.W = W;
-    q.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0; q.R0 = c->dR0; q.variant = c->variant;
-    q.Ahat = c->dAhat; q.Q1 = c->dQ1; q.Gp = c->dGp; q.innerp = c->dinnerp; q.R1 = c->dR1; q.R2 = c->dR2;
-    q.Q = Q; q.Qt = Qt; q.RQ = c->RQ; q.Rn = Rn; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
-    q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
-    if (solve && c->variant == CPQR_SVD) {
-      if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
-    }
-    const int tb = 32 * ((mbq + 31) / 32);
-    const size_t psm = (size_t)(mbq | 1) * R * 8;
-    cq_multi_attrs();
-    switch (RB) {
-      case 8:
-        k_cq_gram1<8><<<nb, tb, psm, c->st>>>(q); CKL();
-        k_cq_chol1<<<1, 256, 0, c->st>>>(q); CKL();
-        k_cq_apply<8><<<nb, tb, psm, c->st>>>(q, 1); CKL();
-        k_cq_chol2<<<1, 256, 0, c->st>>>(q, nullptr); CKL();
-        k_cq_apply<8><<<nb, tb, psm, c->st>>>(q, 2); CKL();
-        break;
-      case 16:
-        k_cq_gram1<16><<<nb, tb, psm, c->st>>>(q); CKL();
-        k_cq_chol1<<<1, 256, 0, c->st>>>(q); CKL();
-        k_cq_apply<16><<<nb, tb, psm, c->st>>>(q, 1); CKL();
-        k_cq_chol2<<<1, 256, 0, c->st>>>(q, nullptr); CKL();
-        k_cq_apply<16><<<nb, tb, psm, c->st>>>(q, 2); CKL();
-        break;
-      default:
-        k_cq_gram1<32><<<nb, tb, psm, c->st>>>(q); CKL();
-        k_cq_chol1<<<1, 256, 0, c->st>>>(q); CKL();
-        k_cq_apply<32><<<nb, tb, psm, c->st>>>(q, 1); CKL();
-        k_cq_chol2<<<1, 256, 0, c->st>>>(q, nullptr); CKL();
-        k_cq_apply<32><<<nb, tb, psm, c->st>>>(q, 2); CKL();
-        break;
-    }
+    cq_nb = nbq;
+  } else if (c->factor_qr_mode == 0) {  // multi-kernel CholeskyQR2, row blocks of <= 256 rows
+    TRY(launch_cq_multi(c, cq_args(nbq), c->st));
     gated = true;
+    cq_nb = nbq;
   }
-  // register-resident Householder TSQR (one thread per row) whenever leaves and root fit in 256 rows
+  // Householder fallback 1: register-resident TSQR (one thread per row), leaves and root <= 256 rows
   {
     int nl = std::max(1, (m + 255) / 256);
     int mbr = (m + nl - 1) / nl;
@@ -1042,9 +1071,6 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
       q.Ahat = c->dAhat; q.part = c->dred; q.Aout = Aout; q.lam = c->dlam; q.flags = c->dflags;
       q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
       q.gated = gated ? 1 : 0;
-      if (solve && c->variant == CPQR_SVD && !gated) {
-        if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
-      }
       const int tl = 32 * ((mbr + 31) / 32), tr = 32 * ((nl * R + 31) / 32);
       static const bool rq_split = getenv("CPQR_RQ_SPLIT") && atoi(getenv("CPQR_RQ_SPLIT")) == 1;
       if (!rq_split) {  // one cluster launch of the three phases (k_rq_fused)
@@ -1069,84 +1095,89 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
         if (e != cudaSuccess) return fail(c, CPQR_ECUDA, "k_rq_fused launch: %s", cudaGetErrorString(e));
         CKL();
       } else {
-      switch (RB) {
-        case 8:
-          k_rq_leaf<8><<<nl, tl, 0, c->st>>>(q); CKL();
-          k_rq_root<8><<<1, tr, 0, c->st>>>(q); CKL();
-          k_rq_qform<8><<<nl, tl, 0, c->st>>>(q); CKL();
-          break;
-        case 16:
-          k_rq_leaf<16><<<nl, tl, 0, c->st>>>(q); CKL();
-          k_rq_root<16><<<1, tr, 0, c->st>>>(q); CKL();
-          k_rq_qform<16><<<nl, tl, 0, c->st>>>(q); CKL();
-          break;
-        default:
-          k_rq_leaf<32><<<nl, tl, 0, c->st>>>(q); CKL();
-          k_rq_root<32><<<1, tr, 0, c->st>>>(q); CKL();
-          k_rq_qform<32><<<nl, tl, 0, c->st>>>(q); CKL();
-          break;
-      }
+        switch (RB) {
+          case 8:
+            k_rq_leaf<8><<<nl, tl, 0, c->st>>>(q); CKL();
+            k_rq_root<8><<<1, tr, 0, c->st>>>(q); CKL();
+            k_rq_qform<8><<<nl, tl, 0, c->st>>>(q); CKL();
+            break;
+          case 16:
+            k_rq_leaf<16><<<nl, tl, 0, c->st>>>(q); CKL();
+            k_rq_root<16><<<1, tr, 0, c->st>>>(q); CKL();
+            k_rq_qform<16><<<nl, tl, 0, c->st>>>(q); CKL();
+            break;
+          default:
+            k_rq_leaf<32><<<nl, tl, 0, c->st>>>(q); CKL();
+            k_rq_root<32><<<1, tr, 0, c->st>>>(q); CKL();
+            k_rq_qform<32><<<nl, tl, 0, c->st>>>(q); CKL();
+            break;
+        }
       }
       return CPQR_OK;
     }
   }
-  TsqrArgs a{};
-  a.A = A; a.m = m; a.R = R; a.nleaf = nleaf; a.mb = mb;
-  a.Rstack = c->dRstack; a.V = c->dV; a.tauv = c->dtauv; a.Qtop = c->dQtop;
-  a.Q = Q; a.Qt = Qt; a.RQ = c->RQ; a.Rn = Rn;
-  a.solve = solve ? 1 : 0;
-  a.W = W;
-  a.R0 = c->dR0;
-  a.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0;
-  a.variant = c->variant;
-  a.Ahat = c->dAhat; a.part = c->dred; a.Aout = Aout; a.lam = c->dlam; a.flags = c->dflags;
-  a.do_fit = do_fit ? 1 : 0; a.nX2 = c->dnX2; a.fit = c->dfit;
-  if (solve && c->variant == CPQR_SVD) {
-    if (!c->pinv_ready) TRY(launch_pinv(c, c->st, nullptr));
+  // Householder fallback 2: shared-memory TSQR, <= 8 leaves of mb rows (2 mb R doubles per leaf)
+  int nleaf = std::max(1, std::min(8, (m + 127) / 128));
+  int mb = (m + nleaf - 1) / nleaf;
+  while (nleaf > 1 && m - (nleaf - 1) * mb < R) { --nleaf; mb = (m + nleaf - 1) / nleaf; }
+  const size_t leaf_smem = (size_t)mb * R * 8, qf_smem = 2 * leaf_smem,
+               root_smem = (size_t)std::max(nleaf, 2) * R * R * 8;
+  if (qf_smem <= 200 * 1024) {
+    TsqrArgs a{};
+    a.A = A; a.m = m; a.R = R; a.nleaf = nleaf; a.mb = mb;
+    a.Rstack = c->dRstack; a.V = c->dV; a.tauv = c->dtauv; a.Qtop = c->dQtop;
+    a.Q = Q; a.Qt = Qt; a.RQ = c->RQ; a.Rn = Rn;
+    a.solve = solve ? 1 : 0;
+    a.W = W;
+    a.R0 = c->dR0;
+    a.Rm = (c->variant == CPQR_SVD) ? c->dMpinv : c->dR0;
+    a.variant = c->variant;
+    a.Ahat = c->dAhat; a.part = c->dred; a.Aout = Aout; a.lam = c->dlam; a.flags = c->dflags;
+    a.do_fit = do_fit ? 1 : 0; a.nX2 = c->dnX2; a.fit = c->dfit;
+    a.gated = gated ? 1 : 0;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_tsqr_leaf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_tsqr_leaf<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_tsqr_leaf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_tsqr_root, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_tsqr_qform, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+      attr = true;
+    }
+    switch (RB) {
+      case 8: k_tsqr_leaf<8><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
+      case 16: k_tsqr_leaf<16><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
+      default: k_tsqr_leaf<32><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
+    }
+    CKL();
+    k_tsqr_root<<<1, 512, root_smem, c->st>>>(a);
+    CKL();
+    k_tsqr_qform<<<nleaf, 512, qf_smem, c->st>>>(a);
+    CKL();
+    return CPQR_OK;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_tsqr_leaf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tsqr_leaf<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tsqr_leaf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tsqr_root, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tsqr_qform, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    attr = true;
+  // Householder fallback 3 (very tall factors, e.g. I_n > 3200 at R = 32): one CTA over global
+  // memory.  Behind CholeskyQR2 it starts from the Ahat and <W, Ahat R0^T> partials k_cq_gram1
+  // already wrote; with Householder forced, k_solve_rows forms them first.
+  TallArgs t{};
+  t.A = A; t.Ahat = c->dAhat; t.m = m; t.R = R; t.RQ = c->RQ; t.solve = solve ? 1 : 0;
+  t.Q = Q; t.Qt = Qt; t.Rn = Rn; t.Aout = Aout; t.lam = c->dlam; t.flags = c->dflags;
+  t.gate_bit = gated ? FLAG_USE_HOUSEHOLDER : 0u;
+  t.do_fit = do_fit ? 1 : 0;
+  t.R0 = c->dR0; t.nX2 = c->dnX2; t.fit = c->dfit;
+  if (gated) {
+    t.innerp = c->dinnerp; t.ninner = cq_nb; t.istride = 1;
+  } else {
+    if (solve) TRY(launch_solve(c, W, m, do_fit, nullptr));
+    t.innerp = c->dred + RB; t.ninner = solve ? c->nparts : 0; t.istride = RB + 1;
   }
-  switch (RB) {
-    case 8: k_tsqr_leaf<8><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
-    case 16: k_tsqr_leaf<16><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
-    default: k_tsqr_leaf<32><<<nleaf, 256, leaf_smem, c->st>>>(a); break;
-  }
-  CKL();
-  k_tsqr_root<<<1, 512, root_smem, c->st>>>(a);
-  CKL();
-  k_tsqr_qform<<<nleaf, 512, qf_smem, c->st>>>(a);
+  k_tall_fallback<<<1, 1024, 0, c->st>>>(t);
   CKL();
   return CPQR_OK;
 }
 
 cpqr_status launch_factor_qr(cpqr_ctx* c, const double* A, int m, double* Q, double* Qt, double* Rn, bool do_fit) {
   return launch_tsqr(c, m, A, false, nullptr, Q, Qt, Rn, nullptr, do_fit);
-}
-
-// Multi-kernel CholeskyQR2 of the m x R column-major q.A (row blocks of 256 rows) on stream st.
-cpqr_status launch_cq_multi(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
-  const int RB = rb_for(c->R);
-  const int tb = 32 * ((q.mb + 31) / 32);
-  const size_t psm = (size_t)(q.mb | 1) * c->R * 8;
-  cq_multi_attrs();
-#define CQM(RBV)                                                   \
-  {                                                                \
-    k_cq_gram1<RBV><<<q.nb, tb, psm, st>>>(q); CKL();              \
-    k_cq_chol1<<<1, 256, 0, st>>>(q); CKL();                       \
-    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 1); CKL();           \
-    k_cq_chol2<<<1, 256, 0, st>>>(q, nullptr); CKL();              \
-    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 2); CKL();           \
-  }
-  switch (RB) { case 8: CQM(8) break; case 16: CQM(16) break; default: CQM(32) break; }
-#undef CQM
-  return CPQR_OK;
 }
 
 // Alg. 2 lines 6-7: V_n and its QR -> Q0, R0.  Default: k_kr_qr2, one CTA, Householder on the
@@ -1212,18 +1243,40 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
   return CPQR_OK;
 }
 
-// combine the per-rank W (or M) of mode n: sum (n < N-1) or gather rows (n == N-1)
-cpqr_status combine_w(cpqr_ctx* c, int n, double* Wloc, double* Wfull) {
+// where slab q's partial W_n (or its rows of W_N) is written: straight into W for one GPU
+double* wloc(cpqr_ctx* c, int q) { return c->opt.world > 1 ? c->slabs[q].dWloc : c->dW; }
+
+// Combine the slabs' results of mode n into the full row-major W_n (or NE's M_n) in c->dW
+// (DESIGN.md §8): the sum over ranks for n < N-1 (W_p = Y_p Q0 is linear in the slab, so Q0 is
+// applied before the reduction), the ranks' rows in rank order for n == N-1.  Across processes:
+// ncclAllReduce / ncclAllGather.  Virtual ranks (CPQR_COMM_LOCAL): a fixed-order sum kernel over
+// the p partials, or one device copy per rank.  src[q]: slab q's local result.
+cpqr_status combine_w(cpqr_ctx* c, int n, const double* const* src) {
   const int64_t R = c->R;
   if (c->opt.world <= 1) {
-    if (Wloc != Wfull)
-      CK(cudaMemcpyAsync(Wfull, Wloc, sizeof(double) * c->dims[n] * R, cudaMemcpyDeviceToDevice, c->st));
+    if (src[0] != c->dW)
+      CK(cudaMemcpyAsync(c->dW, src[0], sizeof(double) * c->dims[n] * R, cudaMemcpyDeviceToDevice, c->st));
+    return CPQR_OK;
+  }
+  if (!c->local) {
+    if (n < c->N - 1) {
+      CN(ncclAllReduce(src[0], c->dW, (size_t)(c->dims[n] * R), ncclDouble, ncclSum, c->comm, c->st));
+    } else {
+      CN(ncclAllGather(src[0], c->dW, (size_t)(c->slabs[0].ldims[n] * R), ncclDouble, c->comm, c->st));
+    }
     return CPQR_OK;
   }
   if (n < c->N - 1) {
-    CN(ncclAllReduce(Wloc, Wfull, (size_t)(c->dims[n] * R), ncclDouble, ncclSum, c->comm, c->st));
+    RankPtrs rp{};
+    for (int q = 0; q < c->nslab; ++q) rp.p[q] = src[q];
+    const int64_t cnt = c->dims[n] * R;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, (int64_t)c->sms * 4));
+    k_sum_ranks<<<grid, 256, 0, c->st>>>(rp, c->nslab, cnt, c->dW);
+    CKL();
   } else {
-    CN(ncclAllGather(Wloc, Wfull, (size_t)(c->ldims[n] * R), ncclDouble, c->comm, c->st));
+    for (int q = 0; q < c->nslab; ++q)
+      CK(cudaMemcpyAsync(c->dW + c->slabs[q].b * R, src[q], sizeof(double) * c->slabs[q].ldims[n] * R,
+                         cudaMemcpyDeviceToDevice, c->st));
   }
   return CPQR_OK;
 }
@@ -1248,14 +1301,12 @@ cpqr_status kt_cross(cpqr_ctx* c, const int* modes, int K, const double* const* 
 }
 
 cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
-  const Plan& p = c->plans[n];
   const int N = c->N;
-  const bool last = (n == N - 1);
   const int In = (int)c->dims[n];
+  prof_mark(c, -1);
   if (c->variant == CPQR_NE) {
-    prof_mark(c, 0);
-    double* Mloc;
-    int m_rowmajor = p.m_rowmajor;
+    const double* Mfull = nullptr;
+    int m_rowmajor = c->slabs[0].plans[n].m_rowmajor;
     if (c->kt) {  // Kruskal input: M_n = B_n diag(lam_x) (*)_{k != n} B_k^T A_k
       int modes[kMaxN], K = 0;
       for (int k = 0; k < N; ++k) if (k != n) modes[K++] = k;
@@ -1266,19 +1317,31 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
       const int grid = (int)std::min<int64_t>(((int64_t)In * c->R + 255) / 256, (int64_t)c->sms * 8);
       k_kt_mttkrp<<<grid, 256, 0, c->st>>>(c->dKtB[n], In, c->ktS, c->dKtLam, c->dKtC, K, c->R, c->dW);
       CKL();
-      Mloc = c->dW;
-      m_rowmajor = 1;
-    } else {
-      TRY(run_plan(c, p));
-      Mloc = const_cast<double*>(p.Y);
-    }
-    prof_mark(c, 2);
-    // M for the tail must be row-major complete; combine per-rank results
-    const double* Mfull = Mloc;
-    if (c->opt.world > 1) {
-      if (!p.m_rowmajor) return fail(c, CPQR_EINVAL, "NE multi-GPU needs row-major M");
-      TRY(combine_w(c, n, Mloc, c->dW));
       Mfull = c->dW;
+      m_rowmajor = 1;
+      prof_mark(c, 0);
+    } else {
+      // MTTKRP of each slab (the partial M_n, or M_N's local rows); the virtual ranks copy theirs
+      // out of the shared intermediate buffers before the next slab runs
+      const double* src[kMaxWorld];
+      for (int q = 0; q < c->nslab; ++q) {
+        const Plan& p = c->slabs[q].plans[n];
+        TRY(run_plan(c, p));
+        src[q] = p.Y;
+        if (c->local) {
+          const int64_t rows = (n == N - 1) ? c->slabs[q].ldims[n] : c->dims[n];
+          CK(cudaMemcpyAsync(c->slabs[q].dWloc, p.Y, sizeof(double) * rows * c->R, cudaMemcpyDeviceToDevice, c->st));
+          src[q] = c->slabs[q].dWloc;
+        }
+        prof_mark(c, 0);
+      }
+      Mfull = src[0];
+      if (c->opt.world > 1) {
+        // the rows of M_N are gathered: its layout must be row-major (rmode < n, plan_mode)
+        if (n == N - 1 && !m_rowmajor) return fail(c, CPQR_EINVAL, "NE: column-major M_N cannot be gathered");
+        TRY(combine_w(c, n, src));
+        Mfull = c->dW;
+      }
     }
     TailNeArgs a{};
     a.M = Mfull;
@@ -1323,7 +1386,6 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   // there the V_n QR runs inline, but the one-CTA SVD of R0 (QR-SVD) still forks to the side
   // stream (the stream grids leave it an SM) and is joined only before the solve
   const bool pinv_fork = !fork && c->variant == CPQR_SVD && !c->opt.profile && !no_fork;
-  prof_mark(c, 0);
   if (fork) {
     CK(cudaEventRecord(c->evf, c->st));
     CK(cudaStreamWaitEvent(c->side, c->evf, 0));
@@ -1345,32 +1407,17 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     TRY(st);
   }
   if (fork || pinv_fork) CK(cudaEventRecord(c->evj, c->side));
-  prof_mark(c, 1);
-  // line 8: Multi-TTM (first step = the stream-X pass; with the dimension tree only the first mode
-  // of each half has one).  Kruskal input: C_k = Q_k^T B_k, then W_n below
+  prof_mark(c, 3);
   if (c->kt) {
+    // Kruskal input: C_k = Q_k^T B_k, then W_n = B_n diag(lam_x) [((.)_k C_k)^T Q0]
     int modes[kMaxN], K = 0;
     for (int k = 0; k < N; ++k) if (k != n) modes[K++] = k;
     const double* Qc[kMaxN];
     const double* Bc[kMaxN];
     for (int k = 0; k < N; ++k) { Qc[k] = c->dQ[k]; Bc[k] = c->dKtB[k]; }
     TRY(kt_cross(c, modes, K, Qc, c->R, Bc, c->ktS, c->dKtC));
-    prof_mark(c, 2);
-    prof_mark(c, 3);
-  } else {
-    const size_t nx = (!p.steps.empty() && p.steps[0].in == c->X) ? 1 : 0;
-    Plan first;
-    first.steps.assign(p.steps.begin(), p.steps.begin() + nx);
-    TRY(run_plan(c, first));
-    prof_mark(c, 2);
-    Plan rest;
-    rest.steps.assign(p.steps.begin() + nx, p.steps.end());
-    TRY(run_plan(c, rest));
-    prof_mark(c, 3);
-  }
-  if (fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-  // line 9: W_n = Y_(n) Q0 (local rows); combine across ranks
-  if (c->kt) {  // W_n = B_n diag(lam_x) [((.)_k C_k)^T Q0]
+    prof_mark(c, 0);
+    if (fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
     int64_t J = 1;
     for (int k = 0; k < N - 1; ++k) J *= c->R;
     switch (rb_for(c->R)) {
@@ -1382,41 +1429,73 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     const int grid = (int)std::min<int64_t>(((int64_t)In * c->R + 255) / 256, (int64_t)c->sms * 8);
     k_kt_w<<<grid, 256, 0, c->st>>>(c->dKtB[n], In, c->ktS, c->dKtLam, c->dKtM, c->R, c->dW);
     CKL();
+    prof_mark(c, 4);
   } else {
-    double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
-    TRY(launch_q0_apply(c, p, Wloc));
-    TRY(combine_w(c, n, Wloc, c->dW));
+    // line 8, per slab: the Multi-TTM (first step = the stream-X pass; with the dimension tree only
+    // the first mode of each half has one), then line 9: W_p = Y_(n) Q0 of the slab (local rows)
+    const double* src[kMaxWorld];
+    for (int q = 0; q < c->nslab; ++q) {
+      const Slab& sl = c->slabs[q];
+      const Plan& p = sl.plans[n];
+      const size_t nx = (!p.steps.empty() && p.steps[0].in == sl.X) ? 1 : 0;
+      Plan first;
+      first.steps.assign(p.steps.begin(), p.steps.begin() + nx);
+      TRY(run_plan(c, first));
+      prof_mark(c, 0);
+      Plan rest;
+      rest.steps.assign(p.steps.begin() + nx, p.steps.end());
+      TRY(run_plan(c, rest));
+      prof_mark(c, 1);
+      if (fork && q == 0) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
+      TRY(launch_q0_apply(c, p, wloc(c, q)));
+      src[q] = wloc(c, q);
+      prof_mark(c, 4);
+    }
+    TRY(combine_w(c, n, src));
   }
-  prof_mark(c, 4);
   if (pinv_fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-  // lines 10-12: solve (substitution / SVD), lambda, normalise, factor QR (+ fast fit after mode N)
+  prof_mark(c, 5);
+  // lines 10-12: solve (substitution / SVD), lambda, normalise, factor QR (+ fast fit after mode N),
+  // one fused launch (k_cq_compact): timed as the factor-QR phase
   const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
   const cpqr_status tst = launch_tsqr(c, In, nullptr, true, c->dW, c->dQ[n], c->dQt[n], c->dRk[n], c->dA[n], fit);
   c->pinv_ready = false;
   TRY(tst);
-  prof_mark(c, 5);
-  (void)last;
+  prof_mark(c, 2);
   return CPQR_OK;
 }
 
+// DIRECT fit: ||X - [[lambda; A]]||^2 over each slab (fixed-order partials), summed
+// over the ranks, then fit = 1 - ||X - Xh|| / ||X||.
 cpqr_status direct_fit(cpqr_ctx* c) {
-  ResidArgs a{};
-  a.X = c->X;
-  a.n = c->numel;
-  a.N = c->N;
-  for (int k = 0; k < c->N; ++k) { a.dims[k] = c->ldims[k]; a.A[k] = c->dA[k]; a.lda[k] = c->dims[k]; }
-  a.off_last = c->slab_b;
-  a.lam = c->dlam;
-  a.R = c->R;
-  a.part = c->dred;
-  const int grid = c->sms * 4;
-  k_resid_partial<<<grid, 256, 0, c->st>>>(a);
+  prof_mark(c, -1);
+  double* res = c->dred + 4096;
+  for (int q = 0; q < c->nslab; ++q) {
+    const Slab& sl = c->slabs[q];
+    ResidArgs a{};
+    a.X = sl.X;
+    a.n = sl.numel;
+    a.N = c->N;
+    for (int k = 0; k < c->N; ++k) { a.dims[k] = sl.ldims[k]; a.A[k] = c->dA[k]; a.lda[k] = c->dims[k]; }
+    a.off_last = sl.b;
+    a.lam = c->dlam;
+    a.R = c->R;
+    a.part = c->dred;
+    const int grid = c->sms * 4;
+    k_resid_partial<<<grid, 256, 0, c->st>>>(a);
+    CKL();
+    k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, c->nslab > 1 ? res + 8 + q : res);
+    CKL();
+  }
+  if (c->nslab > 1) {  // virtual ranks: rank-order sum of the slab residuals
+    k_sum_final<<<1, 256, 0, c->st>>>(res + 8, c->nslab, res);
+    CKL();
+  } else if (c->opt.world > 1) {
+    CN(ncclAllReduce(res, res, 1, ncclDouble, ncclSum, c->comm, c->st));
+  }
+  k_fit_from_resid<<<1, 32, 0, c->st>>>(res, c->dnX2, c->dfit);
   CKL();
-  k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, c->dred + 4096);
-  CKL();
-  if (c->opt.world > 1) CN(ncclAllReduce(c->dred + 4096, c->dred + 4096, 1, ncclDouble, ncclSum, c->comm, c->st));
-  k_fit_from_resid<<<1, 32, 0, c->st>>>(c->dred + 4096, c->dnX2, c->dfit);
-  CKL();
+  prof_mark(c, 5);
   return CPQR_OK;
 }
 
@@ -1426,19 +1505,18 @@ cpqr_status one_sweep(cpqr_ctx* c) {
   return CPQR_OK;
 }
 
+// fold the recorded phase marks into c->prof (after they completed)
 void prof_accumulate(cpqr_ctx* c) {
-  // events: 0 start, 1 after K2, 2 after stream pass, 3 after rest TTM, 4 after Q0 apply, 5 end
-  float ms;
-  if (c->variant == CPQR_NE) {
-    if (cudaEventElapsedTime(&ms, c->evp[0], c->evp[2]) == cudaSuccess) c->prof.ms[0] += ms;
-    if (cudaEventElapsedTime(&ms, c->evp[2], c->evp[5]) == cudaSuccess) c->prof.ms[5] += ms;
-    return;
+  if (c->nmarks > 0) cudaEventSynchronize(c->evp[c->nmarks - 1]);
+  for (int i = 1; i < c->nmarks; ++i) {
+    const int ph = c->evphase[i];
+    float ms;
+    if (ph >= 0 && cudaEventElapsedTime(&ms, c->evp[i - 1], c->evp[i]) == cudaSuccess) {
+      c->prof.ms[ph] += ms;
+      c->prof.launches[ph] += c->evlaunch[i] - c->evlaunch[i - 1];
+    }
   }
-  if (cudaEventElapsedTime(&ms, c->evp[0], c->evp[1]) == cudaSuccess) c->prof.ms[3] += ms;
-  if (cudaEventElapsedTime(&ms, c->evp[1], c->evp[2]) == cudaSuccess) c->prof.ms[0] += ms;
-  if (cudaEventElapsedTime(&ms, c->evp[2], c->evp[3]) == cudaSuccess) c->prof.ms[1] += ms;
-  if (cudaEventElapsedTime(&ms, c->evp[3], c->evp[4]) == cudaSuccess) c->prof.ms[4] += ms;
-  if (cudaEventElapsedTime(&ms, c->evp[4], c->evp[5]) == cudaSuccess) c->prof.ms[5] += ms;
+  c->nmarks = 0;
 }
 
 cpqr_status ensure_fits(cpqr_ctx* c, int n) {
@@ -1544,7 +1622,11 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
     std::memcpy(&c->opt, opt, opt->struct_size);
     c->opt.struct_size = sizeof(cpqr_options);
   }
-  if (c->opt.world < 1 || c->opt.rank < 0 || c->opt.rank >= c->opt.world) { delete c; return CPQR_EINVAL; }
+  if (c->opt.world < 1 || c->opt.world > kMaxWorld || c->opt.rank < 0 || c->opt.rank >= c->opt.world) {
+    delete c;
+    return CPQR_EINVAL;
+  }
+  if (c->opt.comm != CPQR_COMM_NCCL && c->opt.comm != CPQR_COMM_LOCAL) { delete c; return CPQR_EINVAL; }
   if (c->opt.world > 1 && (dims[N - 1] % c->opt.world) != 0) { delete c; return CPQR_EINVAL; }
   c->variant = variant;
   cpqr_status st = create_impl(c, N, dims, R);
@@ -1568,12 +1650,20 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     const char* f = getenv("CPQR_SLICE");  // "1" / "0" force the fused slice kernel on / off
     c->fuse_slice = f ? (f[0] == '1') : (R < 24);
   }
-  for (int k = 0; k < N; ++k) c->dims[k] = c->ldims[k] = dims[k];
+  for (int k = 0; k < N; ++k) c->dims[k] = dims[k];
+  // slabs of the last mode: this rank's, or all p of the virtual ranks
+  c->local = c->opt.comm == CPQR_COMM_LOCAL && c->opt.world > 1;
+  c->nslab = c->local ? c->opt.world : 1;
   const int64_t per = dims[N - 1] / c->opt.world;
-  c->slab_b = per * c->opt.rank;
-  c->slab_e = c->slab_b + per;
-  c->ldims[N - 1] = per;
-  c->numel = prod(c->ldims, 0, N);
+  for (int q = 0; q < c->nslab; ++q) {
+    Slab& sl = c->slabs[q];
+    const int r = c->local ? q : c->opt.rank;
+    for (int k = 0; k < N; ++k) sl.ldims[k] = dims[k];
+    sl.b = per * r;
+    sl.e = sl.b + per;
+    sl.ldims[N - 1] = per;
+    sl.numel = prod(sl.ldims, 0, N);
+  }
   std::memset(&c->prof, 0, sizeof c->prof);
   if (cudaSetDevice(c->opt.device) != cudaSuccess) return fail(c, CPQR_ECUDA, "cudaSetDevice(%d)", c->opt.device);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->opt.device);
@@ -1585,7 +1675,6 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(cudaEventCreateWithFlags(&c->evj, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev0, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev1, cudaEventDisableTiming));
-  for (int i = 0; i < 16; ++i) CK(cudaEventCreate(&c->evp[i]));
   int64_t imax = 0;
   for (int k = 0; k < N; ++k) {
     imax = std::max(imax, dims[k]);
@@ -1604,7 +1693,9 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(dmalloc(&c->dQ0, sizeof(double) * J * R));
   CK(dmalloc(&c->dR0, sizeof(double) * R * R));
   CK(dmalloc(&c->dW, sizeof(double) * imax * R));
-  CK(dmalloc(&c->dWloc, sizeof(double) * imax * R));
+  if (c->opt.world > 1)
+    for (int q = 0; q < c->nslab; ++q) CK(dmalloc(&c->slabs[q].dWloc, sizeof(double) * imax * R));
+  CK(dmalloc(&c->dnX2p, sizeof(double) * 64));
   CK(dmalloc(&c->dAhat, sizeof(double) * imax * R));
   CK(dmalloc(&c->dRstack, sizeof(double) * 8 * R * R));
   CK(dmalloc(&c->dQtop, sizeof(double) * 8 * R * R));
@@ -1627,7 +1718,12 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(cudaMemset(c->dq0cnt, 0, sizeof(unsigned) * ((imax + 7) / 8 + 1)));
   CK(dmalloc(&c->dnX2, sizeof(double) * 4));
   CK(dmalloc(&c->dfit, sizeof(double) * 4));
-  CK(dmalloc(&c->dred, sizeof(double) * 8192));
+  {  // reduction scratch: k_solve_rows writes ceil(I_n / BT) x (RB + 1) partials (any I_n <= imax);
+     // k_sumsq / k_resid use the first sms * 4 slots and dred[4096] (never concurrently)
+    const int RB = rb_for(R), BT = RB > 16 ? 64 : 128;
+    c->dred_elems = std::max<size_t>(8192, (size_t)((imax + BT - 1) / BT) * (RB + 1) + 64);
+    CK(dmalloc(&c->dred, sizeof(double) * c->dred_elems));
+  }
   CK(dmalloc(&c->dflags, sizeof(unsigned) * 4));
   CK(cudaMemset(c->dflags, 0, sizeof(unsigned) * 4));
   CK(cudaMallocHost(&c->hpin, sizeof(double) * 64));
@@ -1683,7 +1779,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       CK(dmalloc(&c->dVr2, sizeof(double) * R * R));
     }
   }
-  if (c->opt.world > 1) {
+  if (c->opt.world > 1 && !c->local) {
     ncclUniqueId id;
     std::memcpy(&id, c->opt.nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&c->comm, c->opt.world, id, c->opt.rank);
@@ -1705,8 +1801,8 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->evf) cudaEventDestroy(c->evf);
   if (c->evj) cudaEventDestroy(c->evj);
-  double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dWloc, c->dWp, c->dAhat, c->buf[0], c->buf[1],
-                  c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred, c->Xown,
+  double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dWp, c->dAhat, c->buf[0], c->buf[1],
+                  c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred,
                   c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2};
   for (double* p : ps) if (p) cudaFree(p);
   if (c->dperm) cudaFree(c->dperm);
@@ -1716,48 +1812,85 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->dKtLam) cudaFree(c->dKtLam);
   if (c->dKtM) cudaFree(c->dKtM);
   if (c->dKtC) cudaFree(c->dKtC);
-  if (c->dTree) cudaFree(c->dTree);
+  for (int q = 0; q < kMaxWorld; ++q) {
+    Slab& sl = c->slabs[q];
+    if (sl.Xown) cudaFree(sl.Xown);
+    if (sl.dTree) cudaFree(sl.dTree);
+    if (sl.dWloc) cudaFree(sl.dWloc);
+  }
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  for (int i = 0; i < 16; ++i) if (c->evp[i]) cudaEventDestroy(c->evp[i]);
+  for (cudaEvent_t e : c->evp) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
   return CPQR_OK;
 }
 
-CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, int64_t e, int mem) {
-  if (!c || !x) return c ? fail(c, CPQR_EINVAL, "null tensor") : CPQR_EINVAL;
-  if (b != c->slab_b || e != c->slab_e)
-    return fail(c, CPQR_EINVAL, "slab [%lld,%lld) != expected [%lld,%lld) for rank %d/%d", (long long)b,
-                (long long)e, (long long)c->slab_b, (long long)c->slab_e, c->opt.rank, c->opt.world);
-  TRY(begin_call(c));
-  const size_t bytes = sizeof(double) * c->numel;
+// one slab's tensor: borrowed in place, or copied into a slab-owned buffer; its partial ||X||^2
+static cpqr_status set_slab(cpqr_ctx* c, Slab& sl, const double* x, int mem, double* nx2_out) {
+  const size_t bytes = sizeof(double) * sl.numel;
   if (mem == CPQR_MEM_DEVICE_BORROW) {
-    if (c->Xown) { cudaFree(c->Xown); c->Xown = nullptr; c->Xown_elems = 0; }
-    c->X = x;
-  } else if (mem == CPQR_MEM_HOST || mem == CPQR_MEM_DEVICE_COPY) {
-    if (c->Xown_elems < (size_t)c->numel) {
-      if (c->Xown) cudaFree(c->Xown);
-      c->Xown = nullptr;
-      if (dmalloc(&c->Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
-      c->Xown_elems = c->numel;
-    }
-    CK(cudaMemcpyAsync(c->Xown, x, bytes, mem == CPQR_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->st));
-    c->X = c->Xown;
+    if (sl.Xown) { cudaFree(sl.Xown); sl.Xown = nullptr; sl.Xown_elems = 0; }
+    sl.X = x;
   } else {
-    return fail(c, CPQR_EINVAL, "bad mem kind %d", mem);
+    if (sl.Xown_elems < (size_t)sl.numel) {
+      if (sl.Xown) cudaFree(sl.Xown);
+      sl.Xown = nullptr;
+      if (dmalloc(&sl.Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
+      sl.Xown_elems = sl.numel;
+    }
+    CK(cudaMemcpyAsync(sl.Xown, x, bytes, mem == CPQR_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->st));
+    sl.X = sl.Xown;
   }
   const int grid = c->sms * 4;
-  k_sumsq_partial<<<grid, 256, 0, c->st>>>(c->X, c->numel, c->dred);
+  k_sumsq_partial<<<grid, 256, 0, c->st>>>(sl.X, sl.numel, c->dred);
   CKL();
-  k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, c->dnX2);
+  k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, nx2_out);
   CKL();
-  if (c->opt.world > 1) CN(ncclAllReduce(c->dnX2, c->dnX2, 1, ncclDouble, ncclSum, c->comm, c->st));
-  c->have_tensor = true;
+  sl.have = true;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, int64_t e, int mem) {
+  if (!c || !x) return c ? fail(c, CPQR_EINVAL, "null tensor") : CPQR_EINVAL;
+  if (mem != CPQR_MEM_HOST && mem != CPQR_MEM_DEVICE_COPY && mem != CPQR_MEM_DEVICE_BORROW)
+    return fail(c, CPQR_EINVAL, "bad mem kind %d", mem);
+  // which slabs [b, e) covers: this rank's, or (virtual ranks) one rank's or all of them
+  int q0 = -1, q1 = -1;
+  if (c->local && b == 0 && e == c->dims[c->N - 1]) {
+    q0 = 0;
+    q1 = c->nslab;
+  } else {
+    for (int q = 0; q < c->nslab; ++q)
+      if (b == c->slabs[q].b && e == c->slabs[q].e) { q0 = q; q1 = q + 1; }
+  }
+  if (q0 < 0)
+    return fail(c, CPQR_EINVAL, "slab [%lld,%lld) is not %s (rank %d/%d%s)", (long long)b, (long long)e,
+                c->local ? "[0, I_N) or one virtual rank's slab" : "this rank's slab", c->opt.rank, c->opt.world,
+                c->local ? ", virtual ranks" : "");
+  TRY(begin_call(c));
+  CK(cudaMemsetAsync(c->dflags, 0, sizeof(unsigned) * 4, c->st));
+  c->flags = 0;
+  const int64_t slice = prod(c->dims, 0, c->N - 1);  // elements per index of the last mode
+  for (int q = q0; q < q1; ++q) {
+    const double* xs = x + (c->slabs[q].b - b) * slice;
+    TRY(set_slab(c, c->slabs[q], xs, mem, c->nslab > 1 ? c->dnX2p + q : c->dnX2));
+  }
+  bool all = true;
+  for (int q = 0; q < c->nslab; ++q) all = all && c->slabs[q].have;
   c->kt = false;
   c->graph_valid = false;
-  TRY(build_plans(c));
+  c->have_tensor = all;
+  if (all) {
+    if (c->nslab > 1) {  // virtual ranks: ||X||^2 = rank-order sum of the slab partials
+      k_sum_final<<<1, 256, 0, c->st>>>(c->dnX2p, c->nslab, c->dnX2);
+      CKL();
+    } else if (c->opt.world > 1) {
+      CN(ncclAllReduce(c->dnX2, c->dnX2, 1, ncclDouble, ncclSum, c->comm, c->st));
+    }
+    TRY(build_plans(c));
+  }
   return end_call(c);
 }
 
@@ -1823,6 +1956,10 @@ CPQR_API cpqr_status cpqr_set_ktensor(cpqr_ctx* c, int S, const double* lam, con
 
 static cpqr_status upload_factors(cpqr_ctx* c, const double* const* A, const double* lam) {
   const int R = c->R;
+  // a new run: clear the sticky device flags (FLAG_NONFINITE of a diverged run included) and the
+  // host-side OR of the condition flags
+  CK(cudaMemsetAsync(c->dflags, 0, sizeof(unsigned) * 4, c->st));
+  c->flags = 0;
   for (int k = 0; k < c->N; ++k) {
     if (!A[k]) {
       if (c->variant == CPQR_NE && k != 0) return fail(c, CPQR_EINVAL, "NE needs A[%d]", k);
@@ -1898,12 +2035,10 @@ CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
       for (int n = 0; n < c->N; ++n) {
         TRY(mode_update(c, n, n == c->N - 1));
         if (sync_modes) CK(cudaDeviceSynchronize());
-        if (c->opt.profile) {
-          CK(cudaEventSynchronize(c->evp[5]));
-          prof_accumulate(c);
-        }
+        if (c->opt.profile) prof_accumulate(c);
       }
       if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
+      if (c->opt.profile) prof_accumulate(c);
       c->launches_per_sweep = c->launch_count - before;
     }
     CK(cudaMemcpyAsync(c->dfits + s, c->dfit, sizeof(double), cudaMemcpyDeviceToDevice, c->st));
@@ -1953,18 +2088,21 @@ CPQR_API cpqr_status cpqr_get_profile(cpqr_ctx* c, cpqr_profile* p, int reset) {
   // algorithmic bytes / flops of the stream-X passes of one sweep:
   // bytes = passes * 8 * numel (X read once per pass: N passes, or 2 with the dimension tree);
   // flops = the first TTM of each pass (+ the fused second contraction of the slice kernels)
-  double fl = 0.0;
-  int passes = 0;
-  for (int n = 0; n < c->N; ++n) {
-    const Plan& pl = c->plans[n];
-    if (pl.steps.empty() || pl.steps[0].in != c->X) continue;  // passes over X only
-    const TtmStep& s = pl.steps[0];
-    const double R = c->R;
-    ++passes;
-    if (s.kind == 2 || s.kind == 6 || s.kind == 8) fl += 2.0 * c->numel * R + 2.0 * (c->numel / (double)s.I1) * R * R;
-    else fl += 2.0 * c->numel * R;
+  // (summed over the slabs this context runs)
+  double fl = 0.0, by = 0.0;
+  for (int q = 0; q < c->nslab && !c->kt && c->plans_valid; ++q) {
+    const Slab& sl = c->slabs[q];
+    for (int n = 0; n < c->N; ++n) {
+      const Plan& pl = sl.plans[n];
+      if (pl.steps.empty() || pl.steps[0].in != sl.X) continue;  // passes over X only
+      const TtmStep& s = pl.steps[0];
+      const double R = c->R, nel = (double)sl.numel;
+      by += 8.0 * nel;
+      if (s.kind == 2 || s.kind == 6 || s.kind == 8) fl += 2.0 * nel * R + 2.0 * (nel / (double)s.I1) * R * R;
+      else fl += 2.0 * nel * R;
+    }
   }
-  p->bytes0 = (double)passes * 8.0 * c->numel;
+  p->bytes0 = by;
   p->flops0 = fl;
   p->launches_total = c->launch_count;
   if (reset) std::memset(&c->prof, 0, sizeof c->prof);
@@ -1983,6 +2121,26 @@ CPQR_API cpqr_status cpqr_launches_per_sweep(cpqr_ctx* c, int64_t* n) {
   return CPQR_OK;
 }
 
+// device scratch freed on every exit path of the debug entry points
+struct DevScratch {
+  std::vector<void*> ptrs;
+  template <typename T>
+  cudaError_t alloc(T** p, size_t bytes) {
+    cudaError_t e = dmalloc(p, bytes);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+  ~DevScratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+static int64_t max_dim(const cpqr_ctx* c) {
+  int64_t m = 0;
+  for (int k = 0; k < c->N; ++k) m = std::max(m, c->dims[k]);
+  return m;
+}
+
 CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo, double* Y_out,
                                      double* Q0_out, double* R0_out, double* W_out) {
   if (!c) return CPQR_EINVAL;
@@ -1992,136 +2150,181 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   if (c->kt) return fail(c, CPQR_EINVAL, "debug_mode needs a dense tensor (Kruskal input forms no Y)");
   TRY(begin_call(c));
   const int R = c->R, N = c->N;
+  DevScratch sc;
   std::vector<double*> tmpQ(N, nullptr), tmpQt(N, nullptr);
   for (int k = 0; k < N; ++k) {
     if (Qo && k != n && Qo[k]) {
-      CK(dmalloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
-      CK(dmalloc(&tmpQt[k], sizeof(double) * c->dims[k] * c->RQ));
+      CK(sc.alloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
+      CK(sc.alloc(&tmpQt[k], sizeof(double) * c->dims[k] * c->RQ));
       CK(cudaMemcpyAsync(tmpQ[k], Qo[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
       k_transpose_pad<<<64, 256, 0, c->st>>>(tmpQ[k], c->dims[k], (int)c->dims[k], R, c->RQ, tmpQt[k]);
       CKL();
     }
   }
-  PlanIn in{};
-  fill_plan_in(c, in, n, tmpQ.data(), tmpQt.data());
-  in.tree_fresh = true;  // the tree buffer holds no valid half intermediate outside a sweep
-  Plan p;
-  plan_mode(in, p, c->buf, c->dPart);
   CK(cudaEventRecord(c->evf, c->st));
   CK(cudaStreamWaitEvent(c->side, c->evf, 0));
   c->vn_mode_cq = c->vn_cq_always;
-  cpqr_status st = launch_kr_qr(c, n);
-  if (st == CPQR_OK) st = run_plan(c, p);
-  if (st == CPQR_OK) {
-    CK(cudaEventRecord(c->evj, c->side));
-    CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-  }
-  double* Wloc = (c->opt.world > 1) ? c->dWloc : c->dW;
-  if (st == CPQR_OK) st = launch_q0_apply(c, p, Wloc);
-  if (st == CPQR_OK) st = combine_w(c, n, Wloc, c->dW);
-  const int64_t ylocal = (int64_t)p.Aa * p.In * p.Bb;
+  TRY(launch_kr_qr(c, n));
+  CK(cudaEventRecord(c->evj, c->side));
+  // per slab: Multi-TTM (fresh from X, the tree buffer holds no valid half intermediate outside a
+  // sweep), Q0 apply; the debug Y is summed over the ranks (n < N-1) or gathered (n == N-1)
   double* yfull = nullptr;
-  int64_t ytot = ylocal;
-  if (st == CPQR_OK && Y_out) {
-    if (c->opt.world > 1) {
-      ytot = (n == N - 1) ? ylocal * c->opt.world : ylocal;
-      if (dmalloc(&yfull, sizeof(double) * ytot) != cudaSuccess) st = fail(c, CPQR_ENOMEM, "debug Y");
-      if (st == CPQR_OK) {
-        ncclResult_t r = (n == N - 1)
-                             ? ncclAllGather(p.Y, yfull, (size_t)ylocal, ncclDouble, c->comm, c->st)
-                             : ncclAllReduce(p.Y, yfull, (size_t)ylocal, ncclDouble, ncclSum, c->comm, c->st);
-        if (r != ncclSuccess) st = fail(c, CPQR_ENCCL, "debug Y collective");
+  int64_t ylocal = 0, ytot = 0;
+  const double* src[kMaxWorld];
+  for (int q = 0; q < c->nslab; ++q) {
+    PlanIn in{};
+    fill_plan_in(c, c->slabs[q], in, n, tmpQ.data(), tmpQt.data());
+    in.tree_fresh = true;
+    Plan p;
+    plan_mode(in, p, c->buf, c->dPart);
+    TRY(run_plan(c, p));
+    if (q == 0) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
+    TRY(launch_q0_apply(c, p, wloc(c, q)));
+    src[q] = wloc(c, q);
+    ylocal = (int64_t)p.Aa * p.In * p.Bb;
+    if (Y_out) {
+      ytot = (c->opt.world > 1 && n == N - 1) ? ylocal * c->opt.world : ylocal;
+      if (!yfull) CK(sc.alloc(&yfull, sizeof(double) * ytot));
+      if (!c->local) {
+        CK(cudaMemcpyAsync(yfull, p.Y, sizeof(double) * ylocal, cudaMemcpyDeviceToDevice, c->st));
+      } else if (n == N - 1) {
+        CK(cudaMemcpyAsync(yfull + q * ylocal, p.Y, sizeof(double) * ylocal, cudaMemcpyDeviceToDevice, c->st));
+      } else if (q == 0) {
+        CK(cudaMemcpyAsync(yfull, p.Y, sizeof(double) * ylocal, cudaMemcpyDeviceToDevice, c->st));
+      } else {
+        RankPtrs rp{};
+        rp.p[0] = yfull;
+        rp.p[1] = p.Y;
+        k_sum_ranks<<<(int)std::min<int64_t>((ylocal + 255) / 256, (int64_t)c->sms * 4), 256, 0, c->st>>>(rp, 2, ylocal, yfull);
+        CKL();
       }
     }
   }
-  if (st == CPQR_OK) {
-    std::vector<double> w((size_t)c->dims[n] * R);
-    cudaMemcpyAsync(w.data(), c->dW, sizeof(double) * w.size(), cudaMemcpyDeviceToHost, c->st);
-    if (Y_out) cudaMemcpyAsync(Y_out, yfull ? yfull : p.Y, sizeof(double) * ytot, cudaMemcpyDeviceToHost, c->st);
-    int64_t J = 1;
-    for (int k = 0; k < N - 1; ++k) J *= R;
-    if (Q0_out) cudaMemcpyAsync(Q0_out, c->dQ0, sizeof(double) * J * R, cudaMemcpyDeviceToHost, c->st);
-    if (R0_out) cudaMemcpyAsync(R0_out, c->dR0, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st);
-    cudaError_t e = cudaStreamSynchronize(c->st);
-    if (e != cudaSuccess) st = fail(c, CPQR_ECUDA, "debug sync: %s", cudaGetErrorString(e));
-    if (W_out && st == CPQR_OK)
-      for (int64_t i = 0; i < c->dims[n]; ++i)
-        for (int r = 0; r < R; ++r) W_out[i + c->dims[n] * r] = w[i * R + r];
+  TRY(combine_w(c, n, src));
+  if (Y_out && c->opt.world > 1 && !c->local) {
+    double* ycoll = nullptr;
+    CK(sc.alloc(&ycoll, sizeof(double) * ytot));
+    if (n == N - 1) CN(ncclAllGather(yfull, ycoll, (size_t)ylocal, ncclDouble, c->comm, c->st));
+    else CN(ncclAllReduce(yfull, ycoll, (size_t)ylocal, ncclDouble, ncclSum, c->comm, c->st));
+    yfull = ycoll;
   }
-  cudaStreamSynchronize(c->st);
-  if (yfull) cudaFree(yfull);
-  for (double* q : tmpQ) if (q) cudaFree(q);
-  for (double* q : tmpQt) if (q) cudaFree(q);
-  if (st != CPQR_OK) return st;
+  std::vector<double> w((size_t)c->dims[n] * R);
+  CK(cudaMemcpyAsync(w.data(), c->dW, sizeof(double) * w.size(), cudaMemcpyDeviceToHost, c->st));
+  if (Y_out) CK(cudaMemcpyAsync(Y_out, yfull, sizeof(double) * ytot, cudaMemcpyDeviceToHost, c->st));
+  int64_t J = 1;
+  for (int k = 0; k < N - 1; ++k) J *= R;
+  if (Q0_out) CK(cudaMemcpyAsync(Q0_out, c->dQ0, sizeof(double) * J * R, cudaMemcpyDeviceToHost, c->st));
+  if (R0_out) CK(cudaMemcpyAsync(R0_out, c->dR0, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (W_out)
+    for (int64_t i = 0; i < c->dims[n]; ++i)
+      for (int r = 0; r < R; ++r) W_out[i + c->dims[n] * r] = w[i * R + r];
   return end_call(c);
 }
 
+CPQR_API cpqr_status cpqr_debug_plan(cpqr_ctx* c, int n, int slab, int64_t* info, int cap, int* nsteps) {
+  if (!c || !info || !nsteps || cap < 0) return CPQR_EINVAL;
+  if (n < 0 || n >= c->N || slab < 0 || slab >= c->nslab) return fail(c, CPQR_EINVAL, "mode %d / slab %d", n, slab);
+  if (!c->plans_valid || c->kt) return fail(c, CPQR_ESTATE, "no dense tensor set");
+  const Slab& sl = c->slabs[slab];
+  const Plan& p = sl.plans[n];
+  const int64_t R = c->R;
+  int cnt = 0;
+  auto put = [&](int64_t kind, int64_t modes, int64_t in, int64_t out, int64_t flops, int64_t xp) {
+    if (cnt < cap) {
+      int64_t* r = info + 6 * cnt;
+      r[0] = kind; r[1] = modes; r[2] = in; r[3] = out; r[4] = flops; r[5] = xp;
+    }
+    ++cnt;
+  };
+  for (const TtmStep& s : p.steps) {
+    const int64_t xp = (s.in == sl.X) ? 1 : 0;
+    switch (s.kind) {
+      case 0: case 4: put(s.kind, s.modes, s.A * s.I * s.B, s.A * R * s.B, 2 * s.A * s.I * s.B * R, xp); break;
+      case 1: case 5: put(s.kind, s.modes, (int64_t)s.I * s.F, R * s.F, 2 * (int64_t)s.I * s.F * R, xp); break;
+      case 2: case 6: case 8:
+        put(s.kind, s.modes, (int64_t)s.I1 * s.I2 * s.L, R * R * s.L,
+            2 * (int64_t)s.I1 * s.I2 * s.L * R + 2 * R * (int64_t)s.I2 * s.L * R, xp);
+        break;
+      default: put(s.kind, 0, 0, 0, 0, 0); break;  // partial-sum fix-ups
+    }
+  }
+  for (const DiagStep& d : p.diags) {
+    int64_t tot = 1;
+    for (int i = 0; i < d.nd; ++i) tot *= d.dims[i];
+    put(100, 1 << d.mode, tot, tot / d.dims[d.k], 2 * tot, 0);
+  }
+  *nsteps = cnt;
+  return CPQR_OK;
+}
+
 CPQR_API cpqr_status cpqr_debug_qr(cpqr_ctx* c, const double* A, int64_t m, double* Q, double* Rf) {
-  if (!c || !A || m < c->R) return CPQR_EINVAL;
+  if (!c || !A) return CPQR_EINVAL;
+  if (m < c->R || m > max_dim(c))
+    return fail(c, CPQR_EINVAL, "debug_qr: m = %lld outside [R, max(dims)] (context workspaces)", (long long)m);
   TRY(begin_call(c));
   const int R = c->R;
-  double *dA = nullptr, *dQ = nullptr, *dR = nullptr;
-  CK(dmalloc(&dA, sizeof(double) * m * R));
-  CK(dmalloc(&dQ, sizeof(double) * m * R));
-  CK(dmalloc(&dR, sizeof(double) * R * R));
+  DevScratch sc;
+  double *dA = nullptr, *dQ = nullptr, *dR = nullptr, *dQt = nullptr;
+  CK(sc.alloc(&dA, sizeof(double) * m * R));
+  CK(sc.alloc(&dQ, sizeof(double) * m * R));
+  CK(sc.alloc(&dR, sizeof(double) * R * R));
+  CK(sc.alloc(&dQt, sizeof(double) * m * c->RQ));
   CK(cudaMemcpyAsync(dA, A, sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
-  double* dQt = nullptr;
-  CK(dmalloc(&dQt, sizeof(double) * m * c->RQ));
   TRY(launch_factor_qr(c, dA, (int)m, dQ, dQt, dR, false));
-  CK(cudaStreamSynchronize(c->st));
-  cudaFree(dQt);
   if (Q) CK(cudaMemcpyAsync(Q, dQ, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
   if (Rf) CK(cudaMemcpyAsync(Rf, dR, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  cudaFree(dA); cudaFree(dQ); cudaFree(dR);
   return end_call(c);
 }
 
 CPQR_API cpqr_status cpqr_debug_svd_solve(cpqr_ctx* c, const double* R0, const double* W, int64_t m,
                                           double tau, double* Ahat, int* ntrunc) {
-  if (!c || !R0 || !W || !Ahat || m < 1) return CPQR_EINVAL;
+  if (!c || !R0 || !W || !Ahat) return CPQR_EINVAL;
+  if (m < 1 || m > max_dim(c))
+    return fail(c, CPQR_EINVAL, "debug_svd_solve: m = %lld outside [1, max(dims)]", (long long)m);
   TRY(begin_call(c));
   const int R = c->R;
-  double *dW, *dR0, *dAw, *dA, *dRn, *dlam, *dAh;
-  unsigned* dfl;
-  CK(dmalloc(&dW, sizeof(double) * m * R));
-  CK(dmalloc(&dR0, sizeof(double) * R * R));
-  CK(dmalloc(&dAw, sizeof(double) * m * R));
-  CK(dmalloc(&dA, sizeof(double) * m * R));
-  CK(dmalloc(&dAh, sizeof(double) * m * R));
-  CK(dmalloc(&dRn, sizeof(double) * R * R));
-  CK(dmalloc(&dlam, sizeof(double) * R));
-  CK(dmalloc(&dfl, sizeof(unsigned)));
-  CK(cudaMemsetAsync(dfl, 0, sizeof(unsigned), c->st));
+  DevScratch sc;
+  double *dW = nullptr, *dR0keep = nullptr;
+  unsigned* dflkeep = nullptr;
+  int* dnt = nullptr;
+  CK(sc.alloc(&dW, sizeof(double) * m * R));
+  CK(sc.alloc(&dR0keep, sizeof(double) * R * R));
+  CK(sc.alloc(&dflkeep, sizeof(unsigned) * 4));
+  CK(sc.alloc(&dnt, sizeof(int)));
+  CK(cudaMemsetAsync(dnt, 0, sizeof(int), c->st));
+  // the solve runs on the context's R0 / flag slots: save them and restore them afterwards, so a
+  // debug call leaves the solver state untouched
+  CK(cudaMemcpyAsync(dR0keep, c->dR0, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(dflkeep, c->dflags, sizeof(unsigned) * 4, cudaMemcpyDeviceToDevice, c->st));
   std::vector<double> wr((size_t)m * R);
   for (int64_t i = 0; i < m; ++i)
     for (int r = 0; r < R; ++r) wr[i * R + r] = W[i + m * r];
   CK(cudaMemcpyAsync(dW, wr.data(), sizeof(double) * m * R, cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemcpyAsync(dR0, R0, sizeof(double) * R * R, cudaMemcpyHostToDevice, c->st));
-  int* dnt = nullptr;
-  CK(dmalloc(&dnt, sizeof(int)));
-  CK(cudaMemsetAsync(dnt, 0, sizeof(int), c->st));
-  CK(cudaMemcpyAsync(c->dR0, dR0, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(c->dR0, R0, sizeof(double) * R * R, cudaMemcpyHostToDevice, c->st));
+  cpqr_status st;
   {
     const double keep = c->opt.svd_tau;
     const int kv = c->variant;
+    const bool kr = c->pinv_ready;
     c->opt.svd_tau = tau;
     c->variant = CPQR_SVD;
-    cpqr_status st = launch_solve(c, dW, (int)m, false, dnt);
+    st = launch_solve(c, dW, (int)m, false, dnt);
     c->opt.svd_tau = keep;
     c->variant = kv;
-    TRY(st);
+    c->pinv_ready = kr;
   }
-  dAh = c->dAhat;
-  unsigned fl = 0;
-  CK(cudaMemcpyAsync(Ahat, dAh, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(&fl, dfl, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+  if (st == CPQR_OK) {
+    CK(cudaMemcpyAsync(Ahat, c->dAhat, sizeof(double) * m * R, cudaMemcpyDeviceToHost, c->st));
+    int nt = 0;
+    CK(cudaMemcpyAsync(&nt, dnt, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (ntrunc) *ntrunc = nt;
+  }
+  cudaMemcpyAsync(c->dR0, dR0keep, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->st);
+  cudaMemcpyAsync(c->dflags, dflkeep, sizeof(unsigned) * 4, cudaMemcpyDeviceToDevice, c->st);
   CK(cudaStreamSynchronize(c->st));
-  int nt = 0;
-  CK(cudaMemcpy(&nt, dnt, sizeof(int), cudaMemcpyDeviceToHost));
-  cudaFree(dnt);
-  if (ntrunc) *ntrunc = nt;
-  (void)fl;
-  cudaFree(dW); cudaFree(dR0); cudaFree(dAw); cudaFree(dA); cudaFree(dRn); cudaFree(dlam); cudaFree(dfl);
+  TRY(st);
   return end_call(c);
 }

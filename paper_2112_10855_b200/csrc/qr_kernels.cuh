@@ -16,9 +16,10 @@
 //                          CholeskyQR2 path, and the one-CTA staircase Householder QR of V_n
 //                          (K2, line 7), gated by FLAG_VN_HOUSEHOLDER behind the CholeskyQR2 path.
 //   k_svd_pinv             M = U S^+ V^T of R0 by one-sided Jacobi (QR-SVD).
-//   k_solve_rows / k_normalize  Alg. 2 lines 10-11 for factors too tall for the fused tail:
-//                          Ahat R0^T = W (row-parallel back substitution) or Ahat = W M, lambda,
-//                          normalise, and <W, Ahat R0^T> for the fast fit.
+//   k_solve_rows           Alg. 2 line 10 for factors too tall for the shared-memory tails (Householder
+//                          forced): Ahat R0^T = W (row-parallel back substitution) or Ahat = W M,
+//                          with the column sums of squares and <W, Ahat R0^T> per
+//                          CTA; k_tall_fallback (small_kernels.cuh) then normalises and factors.
 #pragma once
 #include <cstdio>
 #include "small_kernels.cuh"
@@ -196,10 +197,19 @@ struct TsqrArgs {
   int do_fit;
   const double* nX2;
   double* fit;
+  int gated;  // 1: run only when the CholeskyQR2 path asked for the Householder fallback (0x200)
 };
+
+__device__ __forceinline__ bool tsqr_skip(const TsqrArgs& a) {
+  __shared__ unsigned fl;
+  if (threadIdx.x == 0) fl = a.gated ? *a.flags : 0x200u;
+  __syncthreads();
+  return (fl & 0x200u) == 0;
+}
 
 template <int RB>
 __global__ void __launch_bounds__(256) k_tsqr_leaf(TsqrArgs a) {
+  if (tsqr_skip(a)) return;
   extern __shared__ double sm[];
   __shared__ double tau[64], beta[64], w[64], red[8][RB + 1], np[64];
   __shared__ double Ms[RB * RB], R0s[RB * RB];
@@ -287,6 +297,7 @@ __global__ void __launch_bounds__(256) k_tsqr_leaf(TsqrArgs a) {
 }
 
 __global__ void __launch_bounds__(512) k_tsqr_root(TsqrArgs a) {
+  if (tsqr_skip(a)) return;
   extern __shared__ double sm[];
   __shared__ double tau[64], beta[64], w[64], red[32], lam[64], np[64];
   const int R = a.R, rows = a.nleaf * R;
@@ -348,6 +359,7 @@ __global__ void __launch_bounds__(512) k_tsqr_root(TsqrArgs a) {
 }
 
 __global__ void __launch_bounds__(512) k_tsqr_qform(TsqrArgs a) {
+  if (tsqr_skip(a)) return;
   extern __shared__ double sm[];
   __shared__ double w[64], tv[64];
   const int b = blockIdx.x, R = a.R, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5,
@@ -579,32 +591,6 @@ __global__ void __launch_bounds__(BT) k_solve_rows(const double* __restrict__ W,
     if (c < R || c == RB)
       for (int q = 0; q < BT / 32; ++q) v += red[q][c];
     part[(int64_t)blockIdx.x * (RB + 1) + c] = v;
-  }
-}
-
-// lambda, non-finite check, normalisation, <W, Ahat R0^T> (fixed-order over CTA partials).
-__global__ void __launch_bounds__(1024) k_normalize(const double* __restrict__ Ahat, const double* __restrict__ part,
-                                                    int nparts, int RB, int In, int R, double* __restrict__ A,
-                                                    double* __restrict__ lam_out, double* __restrict__ inner,
-                                                    unsigned* flags) {
-  __shared__ double lam[64];
-  if (threadIdx.x <= R) {
-    const int c = (threadIdx.x == R) ? RB : threadIdx.x;
-    double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * (RB + 1) + c];
-    if (threadIdx.x < R) {
-      lam[c] = sqrt(s);
-      lam_out[c] = lam[c];
-      if (!isfinite(lam[c])) atomicOr(flags, FLAG_NONFINITE);
-    } else {
-      *inner = s;
-    }
-  }
-  __syncthreads();
-  for (int c = 0; c < R; ++c) {
-    const double l = lam[c];
-    for (int i = threadIdx.x; i < In; i += blockDim.x)
-      A[i + (int64_t)In * c] = (l > 0.0) ? Ahat[i + (int64_t)In * c] / l : (i == 0 ? 1.0 : 0.0);
   }
 }
 

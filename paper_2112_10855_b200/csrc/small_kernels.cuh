@@ -2,8 +2,9 @@
 // O(I_n R + R^N) data; the passes over the tensor X are in tma_kernels.cuh / ttm_kernels.cuh
 // (and k_sumsq, once per set_tensor).
 //
-//   k_factor_qr / hh_qr_block  thin Householder QR of I_n x R for very tall factors (Alg. 2 line
-//                   3/12); the usual factor QR is cholqr.cuh
+//   k_tall_fallback / hh_qr_block  one-CTA global-memory Householder QR of I_n x R for factors
+//                   too tall for the shared-memory TSQR fallback (Alg. 2 lines 3/12,
+//                   PAPER.md:351,360); the usual factor QR is CholeskyQR2 (cholqr.cuh)
 //   k_q0_apply_tc   W_n = Y_(n) Q0 on DMMA (Alg. 2 line 9)
 //   jacobi_pinv     one-sided Jacobi SVD of R0 -> M = U S^+ V^T
 //   k_sumsq         ||X||^2 (fixed-order two-level reduction)
@@ -40,6 +41,20 @@ __global__ void k_sumsq_partial(const double* __restrict__ X, int64_t n, double*
   s = block_sum(s, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
+// Sum of the virtual ranks' partial results in rank order (CPQR_COMM_LOCAL's all-reduce):
+// out[e] = (((p0[e] + p1[e]) + p2[e]) + ...); out may alias p[0].
+constexpr int kMaxRanks = 16;
+struct RankPtrs {
+  const double* p[kMaxRanks];
+};
+__global__ void k_sum_ranks(RankPtrs a, int nr, int64_t n, double* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = a.p[0][e];
+    for (int q = 1; q < nr; ++q) s += a.p[q][e];
+    out[e] = s;
+  }
+}
+
 __global__ void k_sum_final(const double* __restrict__ part, int np, double* __restrict__ out) {
   __shared__ double red[32];
   double s = 0.0;
@@ -148,13 +163,84 @@ __device__ void hh_qr_block(double* Aw, int64_t lda, int m, int R, double* Rf, d
   __syncthreads();
 }
 
-// K1 standalone: Q (m x R, lda m) from A (copied into Q first), Rf (R x R).
-__global__ void __launch_bounds__(1024) k_factor_qr(const double* __restrict__ A, int m, int R, double* __restrict__ Q,
-                            double* __restrict__ Rf) {
-  __shared__ double tau[64], beta[64], w[64], red[32];
-  for (int64_t e = threadIdx.x; e < (int64_t)m * R; e += blockDim.x) Q[e] = A[e];
+// Householder fallback for factors too tall for the shared-memory TSQR (Alg. 2 lines 10-12,
+// PAPER.md:358-360), one CTA over global memory.  Runs only if gate_bit is set in *flags (the
+// CholeskyQR2 path rejected the panel) or gate_bit == 0 (Householder forced).  solve = 1: Ahat
+// (m x R column-major) is already formed (by k_cq_gram1 or k_solve_rows); lambda_c = ||Ahat(:,c)||,
+// A_n = Ahat / lambda (zero column -> e_1, reading 10), then Q_n R_n = A_n.  solve = 0: Q R = A.
+// Then the TMA panel Qt and, with do_fit, the fast fit from R0, R_n, lambda and
+// the <W, Ahat R0^T> partials innerp[b * istride] (b < ninner).
+struct TallArgs {
+  const double* A;     // solve = 0: input panel
+  const double* Ahat;  // solve = 1
+  int m, R, RQ, solve;
+  double *Q, *Qt, *Rn, *Aout, *lam;
+  unsigned* flags;
+  unsigned gate_bit;
+  int do_fit;
+  const double* innerp;
+  int ninner, istride;
+  const double* R0;
+  const double* nX2;
+  double* fit;
+};
+__global__ void __launch_bounds__(1024) k_tall_fallback(TallArgs a) {
+  __shared__ double tau[64], beta[64], w[64], red[32], lam[64];
+  __shared__ unsigned fl;
+  if (threadIdx.x == 0) fl = *a.flags;
   __syncthreads();
-  hh_qr_block(Q, m, m, R, Rf, tau, beta, w, red);
+  if (a.gate_bit && !(fl & a.gate_bit)) return;
+  const int m = a.m, R = a.R, tid = threadIdx.x, nt = blockDim.x;
+  if (a.solve) {
+    for (int c = 0; c < R; ++c) {
+      double s = 0.0;
+      for (int i = tid; i < m; i += nt) s = fma(a.Ahat[i + (int64_t)m * c], a.Ahat[i + (int64_t)m * c], s);
+      s = block_sum(s, red);
+      if (tid == 0) {
+        lam[c] = sqrt(s);
+        a.lam[c] = lam[c];
+        if (!isfinite(lam[c])) atomicOr(a.flags, FLAG_NONFINITE);
+      }
+      __syncthreads();
+    }
+    for (int c = 0; c < R; ++c) {
+      const double l = lam[c];
+      for (int i = tid; i < m; i += nt) {
+        const int64_t e = i + (int64_t)m * c;
+        const double v = (l > 0.0) ? a.Ahat[e] / l : (i == 0 ? 1.0 : 0.0);
+        a.Aout[e] = v;
+        a.Q[e] = v;
+      }
+    }
+  } else {
+    for (int64_t e = tid; e < (int64_t)m * R; e += nt) a.Q[e] = a.A[e];
+  }
+  __syncthreads();
+  hh_qr_block(a.Q, m, m, R, a.Rn, tau, beta, w, red);
+  __syncthreads();
+  for (int64_t e = tid; e < (int64_t)m * a.RQ; e += nt) {
+    const int i = (int)(e / a.RQ), r = (int)(e - (int64_t)i * a.RQ);
+    a.Qt[e] = (r < R) ? a.Q[i + (int64_t)m * r] : 0.0;
+  }
+  if (a.do_fit) {  // ||Xh||^2 = <R0^T R0, diag(lam) R_n^T R_n diag(lam)>
+    double q = 0.0;
+    for (int e = tid; e < R * R; e += nt) {
+      const int x = e % R, y = e / R;
+      double g0 = 0.0, g1 = 0.0;
+      for (int k = 0; k <= min(x, y); ++k) {
+        g0 = fma(a.R0[k + R * x], a.R0[k + R * y], g0);
+        g1 = fma(a.Rn[k + R * x], a.Rn[k + R * y], g1);
+      }
+      q = fma(g0, lam[x] * lam[y] * g1, q);
+    }
+    const double nxh2 = block_sum(q, red);
+    if (tid == 0) {
+      double inner = 0.0;
+      for (int b = 0; b < a.ninner; ++b) inner += a.innerp[(int64_t)b * a.istride];
+      const double nx2 = *a.nX2;
+      *a.fit = 1.0 - sqrt(fmax(0.0, nx2 - 2.0 * inner + nxh2)) / sqrt(nx2);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ K2: structured QR of V_n

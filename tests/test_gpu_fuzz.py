@@ -84,8 +84,10 @@ def test_fuzz_kruskal_parity(cp, dims, R, S, variant, seed):
     oracle's Kruskal drivers.  S < R is excluded: after one sweep the factors have rank <= S, R0 is
     singular and both sides' results depend on rounding (QR) or on truncation decisions at
     tau = R eps (SVD), so the two implementations legitimately differ there (a first draw with
-    S in {1, 2}, R >= 5 showed it); the rank-deficient regime is pinned by the exact-duplicate SVD
-    tests instead."""
+    S in {1, 2}, R >= 5 showed it); the rank-deficient regime is covered instead by
+    test_kruskal_rank_below_model_is_flagged below (the flags) and, for a truncating QR-SVD sweep
+    whose result is unique (min-norm, exact duplicate columns), by the GPU parity test
+    tests/test_gpu_parity.py::test_svd_truncation_exact_duplicate."""
     g = np.random.default_rng(seed)
     lam_x = g.standard_normal(S)
     B = [g.standard_normal((I, S)) for I in dims]
@@ -123,7 +125,7 @@ def test_kruskal_rank_below_model_is_flagged(cp, variant):
     s.set_factors(A0)
     try:
         f = s.sweep(3)
-    except cp.CpqrError as e:  # EDIVERGED: non-finite factor, state left at the last finite mode
+    except cp.CpqrError as e:  # EDIVERGED: a non-finite lambda appeared (cpqr.h)
         assert variant == "QR" and e.status == 6, e
         f = None
     fl = s.flags

@@ -668,3 +668,141 @@ def test_slice_kernel_split_slices(cp, dims, R):
     for k in range(N):
         assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
     s.close()
+
+
+@pytest.mark.parametrize("dims,R", [((30, 40, 50), 5), ((12, 10, 9, 11), 4), ((9, 8, 7, 6, 8), 4)])
+def test_svd_truncation_exact_duplicate(cp, dims, R):
+    """A truncating QR-SVD sweep on the GPU (SURVEY.md 8(c) 'Solve (SVD) (ii)').
+    Columns 1 and 2 of every initial factor but the first (unused, Alg. 2 line 2) are equal, so
+    Z_1 and R0 have rank R-1: the SVD with tau = 1e-12 drops one singular value and the LS
+    solution is the unique minimum-norm one, which keeps the two columns equal.  Both sides must
+    set SVD_TRUNCATED and agree (factors <= 1e-9 after one sweep, fits within 1e-8 on every
+    sweep); the QR variant flags R0 as numerically singular (ILLCOND_R0) or diverges."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=31 + len(dims), eta=0.01)
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    dup = [a.copy() for a in init]
+    for k in range(1, N):
+        dup[k][:, 1] = dup[k][:, 0]
+    s = cp.CPQR(dims, R, "SVD", svd_tau=1e-12)
+    s.set_tensor(Xc)
+    s.set_factors(dup)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_qr(X, dup, 1, variant="SVD", tau=1e-12)
+    assert ref1["flags"] & O.FLAG_SVD_TRUNCATED
+    assert s.flags & cp.FLAG_SVD_TRUNCATED
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+        assert rel(A[k][:, 1], A[k][:, 0]) <= 1e-10, (k, rel(A[k][:, 1], A[k][:, 0]))
+    assert rel(lam, ref1["lam"]) <= 1e-9
+    f = np.concatenate([f1, s.sweep(2)])
+    ref = O.cp_als_qr(X, dup, 3, variant="SVD", tau=1e-12)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (f, ref["fits"])
+    lam, A = s.get_factors()
+    for k in range(N):
+        assert rel(A[k][:, 1], A[k][:, 0]) <= 1e-10
+    s.close()
+    q = cp.CPQR(dims, R, "QR")
+    q.set_tensor(Xc)
+    q.set_factors(dup)
+    try:
+        q.sweep(1)
+        assert q.flags & cp.FLAG_ILLCOND_R0, q.flags
+    except cp.CpqrError as e:
+        assert e.status == 6 and q.flags & cp.FLAG_ILLCOND_R0, e
+    q.close()
+
+
+def test_edivergred_cleared_by_set_factors(cp):
+    """After EDIVERGED (X = 0 makes R0 singular) a new tensor and cpqr_set_factors restore a finite
+    state: the sticky non-finite condition and the flags are cleared (cpqr.h)."""
+    dims, R = (6, 5, 4), 2
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=5)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(np.zeros_like(Xc))
+    s.set_factors(init)
+    with pytest.raises(cp.CpqrError):
+        s.sweep(1)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    assert s.flags == 0
+    f = s.sweep(2)
+    ref = O.cp_als_qr(O.as_tensor(Xc), init, 2)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+
+
+@pytest.mark.parametrize("variant", ["QR", "SVD"])
+@pytest.mark.parametrize("dims,R,illcond", [((20000, 33, 40), 32, False), ((40, 33, 20000), 32, False),
+                                            ((13000, 9, 10), 8, False), ((40, 33, 20000), 32, True)])
+def test_tall_factor_mode(cp, dims, R, variant, illcond):
+    """One factor far taller than the shared-memory tails (I_n > 3200 at R = 32 took an
+    unfused path that returned EINVAL with the fast fit and overran a partials buffer): the
+    multi-kernel CholeskyQR2 handles it in the first mode and in the last (with the fused fast
+    fit); when its kappa guard rejects the panel (the tall initial factor with a column scaled by
+    1e-9, kappa ~ 1e9) the gated one-CTA Householder fallback factors it."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=11 + R, eta=0.01)
+    A0 = [a.copy() for a in init]
+    if illcond:
+        A0[2][:, 3] *= 1e-9
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(A0)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    X = O.as_tensor(Xc)
+    ref1 = O.cp_als_qr(X, A0, 1, variant=variant)
+    for k in range(3):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(1)])
+    ref = O.cp_als_qr(X, A0, 2, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+
+
+def test_tall_factor_forced_householder(cp, monkeypatch):
+    """The very-tall Householder path with CholeskyQR2 disabled (CPQR_FACTOR_QR=householder):
+    k_solve_rows forms Ahat and its partials (buffer sized for any I_n), k_tall_fallback the rest."""
+    monkeypatch.setenv("CPQR_FACTOR_QR", "householder")
+    dims, R = (9000, 20, 64), 32
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=3, eta=0.01)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f = s.sweep(2)
+    lam, A = s.get_factors()
+    X = O.as_tensor(Xc)
+    ref = O.cp_als_qr(X, init, 2)
+    for k in range(3):
+        assert rel(A[k], ref["factors"][k]) <= 1e-9, (k, rel(A[k], ref["factors"][k]))
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+
+
+def test_debug_calls_leave_state_and_bound_m(cp):
+    """cpqr_debug_svd_solve restores R0 and the flags; m > max(dims) is rejected."""
+    dims, R = (12, 10, 9), 4
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=8)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f_a = s.sweep(1)
+    g = np.random.default_rng(1)
+    R0 = np.triu(g.standard_normal((R, R)))
+    R0[3, 3] = 0.0
+    W = g.standard_normal((12, R))
+    out, nt = s.debug_svd_solve(R0, W, 1e-12)
+    assert nt == 1 and s.flags == 0
+    with pytest.raises(cp.CpqrError):
+        s.debug_svd_solve(R0, g.standard_normal((13, R)), 1e-12)
+    with pytest.raises(cp.CpqrError):
+        s.debug_qr(g.standard_normal((13, R)))
+    f_b = s.sweep(1)
+    s.close()
+    t = cp.CPQR(dims, R, "QR")
+    t.set_tensor(Xc)
+    t.set_factors(init)
+    f_c = t.sweep(2)
+    t.close()
+    assert np.array_equal(np.concatenate([f_a, f_b]), f_c)
