@@ -29,7 +29,7 @@ __all__ = [
     "EPS", "FLAG_ILLCOND_R0", "FLAG_NE_CHOL_FALLBACK", "FLAG_SVD_TRUNCATED",
     "as_tensor", "kron", "khatri_rao", "hadamard", "matricize", "tensorize", "ttm",
     "multi_ttm", "ttm_order", "qr_pos", "kr_of_triangular", "structured_qr", "apply_q0",
-    "solve_qr", "solve_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
+    "solve_qr", "solve_svd", "pinv_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
     "fit_direct", "mode_update_qr", "mode_update_ne", "cp_als_qr", "cp_als_ne",
     "qr_cost", "ttm_cost", "mttkrp", "ktensor_norm2", "w_ktensor", "mttkrp_ktensor",
     "sine_of_sums_ktensor", "score",
@@ -176,6 +176,20 @@ def solve_svd(R0: np.ndarray, W: np.ndarray, tau: float = -1.0):
     return Ahat, int(R - keep.sum())
 
 
+def pinv_svd(S: np.ndarray, tau: float = -1.0):
+    """Moore-Penrose pseudo-inverse by the SVD, as MATLAB's pinv: S = U diag(s)
+    V^T, S^+ = V diag(1/s_i) U^T over the kept s_i > tau * s_max (reading 32: tau < 0 -> R*eps, the
+    max(size(S)) * eps(norm(S)) default up to the ulp rounding of eps(norm)).  Returns
+    (S^+, n_truncated)."""
+    R = S.shape[0]
+    if tau < 0:
+        tau = R * EPS
+    U, s, Vt = np.linalg.svd(S)
+    keep = s > tau * s[0]
+    P = (Vt[keep, :].T / s[keep][None, :]) @ U[:, keep].T
+    return P, int(R - keep.sum())
+
+
 def normalize(Ahat: np.ndarray):
     """Normalize columns (Alg. 2 line 11): lam_r = ||Ahat(:,r)||_2, A = Ahat/lam.
     A zero column gives lam_r = 0 and column e_1 (reading 10)."""
@@ -267,11 +281,13 @@ def mode_update_qr(X, Qs, Rs, n, variant="QR", tau=-1.0, order=None, kt=None):
                 A=A, lam=lam, Q=Qn, R=Rn, ntrunc=ntrunc, flags=flags)
 
 
-def mode_update_ne(X, factors, grams, n, kt=None):
+def mode_update_ne(X, factors, grams, n, kt=None, solve="chol", tau=-1.0):
     """One CP-ALS mode update, Alg. 1 lines 6-11: S_n = Hadamard of the other
     Grams; M_n = X_(n) Z_n (MTTKRP); solve Ahat S_n = M_n by Cholesky, falling back
-    to LU with partial pivoting on a non-positive pivot (reading 18); normalize; G_n = A_n^T A_n.
-    kt = (lam_x, B): Kruskal input (MTTKRP by mttkrp_ktensor)."""
+    to LU with partial pivoting on a non-positive pivot (reading 18) -- or, solve="pinv"
+    (CP-ALS-PINV, PAPER.md:264-266), Ahat = M_n S_n^+ with the SVD pseudo-inverse (pinv_svd);
+    normalize; G_n = A_n^T A_n.  kt = (lam_x, B): Kruskal input (MTTKRP by mttkrp_ktensor,
+    PAPER.md:446-450)."""
     N = len(factors)
     S = np.ones_like(grams[0])
     for k in range(N - 1, -1, -1):                                # line 6
@@ -279,13 +295,19 @@ def mode_update_ne(X, factors, grams, n, kt=None):
             S = hadamard(S, grams[k])
     M = mttkrp(X, factors, n) if kt is None else mttkrp_ktensor(kt[0], kt[1], factors, n)  # lines 7-8
     flags = 0
-    try:                                                          # line 9
-        L = np.linalg.cholesky(S)
-        T = scipy.linalg.solve_triangular(L, M.T, lower=True)
-        Ahat = scipy.linalg.solve_triangular(L.T, T, lower=False).T
-    except np.linalg.LinAlgError:
-        Ahat = scipy.linalg.solve(S, M.T, assume_a="gen").T
-        flags |= FLAG_NE_CHOL_FALLBACK
+    if solve == "pinv":                                           # line 9, CP-ALS-PINV
+        P, ntrunc = pinv_svd(S, tau)
+        Ahat = M @ P
+        if ntrunc:
+            flags |= FLAG_SVD_TRUNCATED
+    else:
+        try:                                                      # line 9
+            L = np.linalg.cholesky(S)
+            T = scipy.linalg.solve_triangular(L, M.T, lower=True)
+            Ahat = scipy.linalg.solve_triangular(L.T, T, lower=False).T
+        except np.linalg.LinAlgError:
+            Ahat = scipy.linalg.solve(S, M.T, assume_a="gen").T
+            flags |= FLAG_NE_CHOL_FALLBACK
     A, lam = normalize(Ahat)                                      # line 10
     G = A.T @ A                                                   # line 11
     return dict(S=S, M=M, Ahat=Ahat, A=A, lam=lam, G=G, flags=flags)
@@ -401,9 +423,10 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
                 nX2=nX2)
 
 
-def cp_als_ne(X, A0, sweeps, fit_mode="fast", kt=None):
-    """CP-ALS with normal equations, Alg. 1, exactly `sweeps` sweeps.
-    Fit: PAPER.md:417-425 (fast) or direct.  kt = (lam_x, B): Kruskal input instead of X."""
+def cp_als_ne(X, A0, sweeps, fit_mode="fast", kt=None, solve="chol", tau=-1.0):
+    """CP-ALS with normal equations, Alg. 1, exactly `sweeps` sweeps; solve="pinv"
+    is CP-ALS-PINV (PAPER.md:264-266).  Fit: PAPER.md:417-425 (fast) or direct.  kt = (lam_x, B):
+    Kruskal input instead of X."""
     N = X.ndim if kt is None else len(kt[1])
     nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K"))) if kt is None else ktensor_norm2(*kt)
     factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
@@ -413,7 +436,7 @@ def cp_als_ne(X, A0, sweeps, fit_mode="fast", kt=None):
     for s in range(sweeps):
         last = None
         for n in range(N):
-            u = mode_update_ne(X, factors, grams, n, kt)
+            u = mode_update_ne(X, factors, grams, n, kt, solve, tau)
             factors[n], lam, grams[n] = u["A"], u["lam"], u["G"]
             flags |= u["flags"]
             last = u

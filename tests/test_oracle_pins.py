@@ -346,6 +346,67 @@ def test_svd_exact_duplicate_min_norm_and_qr_illcond_flag():
     assert qr["flags"] & O.FLAG_ILLCOND_R0
 
 
+# ------------------------------------------------------------- CP-ALS-PINV
+def test_pinv_svd_penrose_conditions_and_known_spectrum():
+    # the four Moore-Penrose conditions (the definition of S^+) on a singular symmetric S and a
+    # singular non-symmetric matrix, and the exact inverse when S is nonsingular
+    B = rng.standard_normal((6, 4))
+    for S in (B @ B.T, rng.standard_normal((6, 3)) @ rng.standard_normal((3, 6))):
+        P, nt = O.pinv_svd(S)
+        assert nt == 6 - np.linalg.matrix_rank(S)
+        sc = np.linalg.norm(S)
+        assert np.linalg.norm(S @ P @ S - S) <= 1e-12 * sc
+        assert np.linalg.norm(P @ S @ P - P) <= 1e-12 * np.linalg.norm(P)
+        assert np.linalg.norm((S @ P).T - S @ P) <= 1e-12
+        assert np.linalg.norm((P @ S).T - P @ S) <= 1e-12
+    G = rng.standard_normal((5, 5))
+    S = G @ G.T + 5 * np.eye(5)
+    P, nt = O.pinv_svd(S)
+    assert nt == 0 and np.linalg.norm(S @ P - np.eye(5)) <= 1e-13
+    # known spectrum: Q diag(1, 1e-3, 1e-17) Q^T -> the third value is dropped (<= 3 eps), the
+    # second kept, P = Q diag(1, 1e3, 0) Q^T
+    Q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    S = Q @ np.diag([1.0, 1e-3, 1e-17]) @ Q.T
+    P, nt = O.pinv_svd(S)
+    assert nt == 1
+    assert rel(P, Q @ np.diag([1.0, 1e3, 0.0]) @ Q.T) <= 1e-10
+
+
+def test_cp_als_pinv_equals_cholesky_on_well_conditioned():
+    conf, Xc, truth, init = synth.small_problem((9, 8, 7), 3, seed=21, eta=0.05)
+    X = O.as_tensor(Xc)
+    a = O.cp_als_ne(X, init, 3)
+    b = O.cp_als_ne(X, init, 3, solve="pinv")
+    assert b["flags"] == 0
+    for k in range(3):
+        assert rel(b["factors"][k], a["factors"][k]) <= 1e-10
+    assert np.max(np.abs(np.array(a["fits"]) - np.array(b["fits"]))) <= 1e-12
+
+
+def test_cp_als_pinv_exact_duplicate_is_the_min_norm_solution():
+    # Exact duplicate columns (1, 2) of A_2, A_3: S_1 = Z_1^T Z_1 is singular.  The pseudo-inverse
+    # solve gives the minimum-norm LS solution of min ||X_(1) - Ahat Z_1^T||, the same one the
+    # QR-SVD route computes through the SVD of R0 -- an independent path --
+    # and it keeps the two columns equal.
+    conf, Xc, truth, init = synth.small_problem((10, 9, 8), 3, seed=33, eta=0.05)
+    X = O.as_tensor(Xc)
+    dup = [a.copy() for a in init]
+    for k in (1, 2):
+        dup[k][:, 1] = dup[k][:, 0]
+    grams = [A.T @ A for A in dup]
+    u = O.mode_update_ne(X, dup, grams, 0, solve="pinv")
+    assert u["flags"] & O.FLAG_SVD_TRUNCATED
+    Qs, Rs = [None] * 3, [None] * 3
+    for k in (1, 2):
+        Qs[k], Rs[k] = O.qr_pos(dup[k])
+    v = O.mode_update_qr(X, Qs, Rs, 0, variant="SVD", tau=1e-12)
+    assert rel(u["Ahat"], v["Ahat"]) <= 1e-9
+    assert rel(u["Ahat"][:, 1], u["Ahat"][:, 0]) <= 1e-12
+    Z = O.khatri_rao([dup[2], dup[1]])
+    ref = np.linalg.lstsq(Z, O.matricize(X, 0).T, rcond=None)[0].T  # LAPACK min-norm LS
+    assert rel(u["Ahat"], ref) <= 1e-9
+
+
 # ---------------------------------------------------------------- generators / costs
 def test_generators_closed_forms():
     c2 = synth.CONFIGS[2]
