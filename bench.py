@@ -382,7 +382,8 @@ def main():
         line["roofline"] = roof
         line["multi_ttm_gbs"] = mt_bytes_sweep / ((prof["ms"][0] + prof["ms"][1]) / nsw / 1e3) / 1e9
         line["phase_ms_per_sweep"] = {k: v / nsw for k, v in zip(
-            ["stream_pass", "rest_ttm", "factor_qr", "q0_compute", "q0_apply", "other"], prof["ms"])}
+            ["stream_pass", "rest_ttm", "factor_qr_tail", "q0_compute", "q0_apply", "other", "exchange"],
+            prof["ms"])}
     line["clocks"] = clocks
     if other:
         line["per_mode" if tree else "dimension_tree"] = dict(other, note=(

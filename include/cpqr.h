@@ -47,8 +47,13 @@ enum {
                           the condition */
 };
 
-/* Variant of the per-mode LS solve (substitution or SVD; Alg. 1: normal eqs). */
-typedef enum { CPQR_NE = 0, CPQR_QR = 1, CPQR_SVD = 2 } cpqr_variant;
+/* Variant of the per-mode LS solve (substitution or SVD; Alg. 1: normal eqs):
+ *   CPQR_NE   CP-ALS, Alg. 1: Ahat S_n = M_n by Cholesky (LU fallback, reading 18);
+ *   CPQR_QR   CP-ALS-QR, Alg. 2: Ahat R0^T = W_n by back substitution;
+ *   CPQR_SVD  CP-ALS-QR-SVD: Ahat = W_n (R0^T)^+ by the SVD of R0, svd_tau;
+ *   CPQR_PINV CP-ALS-PINV: Alg. 1 with Ahat = M_n S_n^+, the SVD
+ *             pseudo-inverse of S_n (one-sided Jacobi), dropping sigma_i <= svd_tau sigma_max. */
+typedef enum { CPQR_NE = 0, CPQR_QR = 1, CPQR_SVD = 2, CPQR_PINV = 3 } cpqr_variant;
 
 /* Fit computation: FAST uses the identity ||X-Xh||^2 = ||X||^2 - 2<X,Xh>
  * + ||Xh||^2 with already-computed quantities; DIRECT forms the residual explicitly (one extra
@@ -67,7 +72,7 @@ typedef enum {
 enum {
   CPQR_FLAG_ILLCOND_R0 = 1u,      /* QR variant: min|R0_jj| <= R^(N-1)*eps*max|R0_jj| (reading 17) */
   CPQR_FLAG_NE_CHOL_FALLBACK = 2u,/* NE: Cholesky met a non-positive pivot; LU used (reading 18) */
-  CPQR_FLAG_SVD_TRUNCATED = 4u,   /* SVD variant: at least one sigma_i <= tau*sigma_max dropped */
+  CPQR_FLAG_SVD_TRUNCATED = 4u,   /* SVD / PINV: at least one sigma_i <= tau*sigma_max dropped */
   CPQR_FLAG_NE_ILLCOND = 8u       /* NE: kappa(S_n) estimate (max/min Cholesky pivot)^2 > 1e8: the
                                      normal equations lose > 8 digits; a robust driver switches to
                                      QR / QR-SVD */
@@ -85,7 +90,7 @@ typedef enum {
 
 typedef struct cpqr_options {
   uint32_t struct_size;   /* = sizeof(cpqr_options); ABI versioning */
-  double svd_tau;         /* SVD truncation: keep sigma_i > svd_tau*sigma_max; < 0 -> R*eps */
+  double svd_tau;         /* SVD / PINV truncation: keep sigma_i > svd_tau*sigma_max; < 0 -> R*eps */
   int32_t fit_mode;       /* cpqr_fit_mode */
   int32_t device;         /* CUDA device ordinal */
   void* stream;           /* borrowed cudaStream_t to run on (e.g. torch's), or NULL: own stream */
@@ -176,23 +181,28 @@ cpqr_status cpqr_get_fit(cpqr_ctx* ctx, double* fit);      /* fit after the last
 cpqr_status cpqr_get_flags(cpqr_ctx* ctx, uint32_t* flags);
 
 /* Per-phase device time (ms) accumulated since the last reset, Table 3.1 taxonomy
- * (PAPER.md:495-510), only with opt.profile = 1:
- *   ms[0] Multi-TTM stream-X pass (the dominant kernel)   ms[1] Multi-TTM remaining TTMs
- *   ms[2] factor QR        ms[3] computing Q0 (QR of V_n)  ms[4] applying Q0
- *   ms[5] other (solve, normalise, fit)
- * launches[0..5]: kernel launches per phase; bytes0/flops0: algorithmic HBM bytes and flops of
+ * (PAPER.md:495-510), only with opt.profile = 1 (eager launches, V_n QR inline):
+ *   ms[0] Multi-TTM stream-X pass (the dominant kernel; NE: the whole MTTKRP)
+ *   ms[1] Multi-TTM remaining TTMs
+ *   ms[2] factor QR: the fused tail launch (solve, normalise, factor QR, fast fit)
+ *   ms[3] computing Q0 (QR of V_n)       ms[4] applying Q0
+ *   ms[5] other (S_n^+ of PINV, the NE tail, the DIRECT fit)
+ *   ms[6] exchange of W_n across the ranks (NCCL, or the virtual ranks' combine)
+ * Slab-parallel phases (0, 1, 4 and the NE MTTKRP) are summed over the slabs a context runs.
+ * launches[0..6]: kernel launches per phase; bytes0/flops0: algorithmic HBM bytes and flops of
  * phase 0.  reset != 0 zeroes the counters after reading. */
 typedef struct cpqr_profile {
-  double ms[6];
-  int64_t launches[6];
+  double ms[7];
+  int64_t launches[7];
   double bytes0, flops0;
   int64_t launches_total;
 } cpqr_profile;
 cpqr_status cpqr_get_profile(cpqr_ctx* ctx, cpqr_profile* prof, int reset);
-/* cpqr_get_timings: the six per-phase milliseconds of cpqr_get_profile (ms[0..5]
- * as above: the paper's five-way split, with the Multi-TTM's stream-X pass
- * separated from its remaining TTMs), accumulated since the last reset; zeros unless
- * opt.profile = 1.  ms: caller buffer of 6 doubles.  Errors: EINVAL (NULL ctx or ms). */
+/* cpqr_get_timings: the seven per-phase milliseconds of cpqr_get_profile
+ * (ms[0..6] as above: the paper's five-way split, with the Multi-TTM's
+ * stream-X pass separated from its remaining TTMs and the exchange separated from "other"),
+ * accumulated since the last reset; zeros unless opt.profile = 1.  ms: caller buffer of 7
+ * doubles.  Errors: EINVAL (NULL ctx or ms). */
 cpqr_status cpqr_get_timings(cpqr_ctx* ctx, double* ms);
 
 /* Kernel launches issued by one cpqr_sweep(ctx, 1, ...) (claims for bench "gpu_launches"). */

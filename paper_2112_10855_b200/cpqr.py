@@ -20,8 +20,8 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"libcpqr.so not built ({LIB_PATH}); run `python -m paper_2112_10855_b200.build`")
 _lib = C.CDLL(LIB_PATH)
 
-NE, QR, SVD = 0, 1, 2
-VARIANTS = {"NE": NE, "QR": QR, "SVD": SVD}
+NE, QR, SVD, PINV = 0, 1, 2, 3
+VARIANTS = {"NE": NE, "QR": QR, "SVD": SVD, "PINV": PINV}
 FIT_FAST, FIT_DIRECT = 0, 1
 MEM_HOST, MEM_DEVICE_COPY, MEM_DEVICE_BORROW = 0, 1, 2
 COMM_NCCL, COMM_LOCAL = 0, 1
@@ -44,7 +44,7 @@ class Options(C.Structure):
 
 
 class Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 6), ("launches", C.c_int64 * 6), ("bytes0", C.c_double),
+    _fields_ = [("ms", C.c_double * 7), ("launches", C.c_int64 * 7), ("bytes0", C.c_double),
                 ("flops0", C.c_double), ("launches_total", C.c_int64)]
 
 
@@ -260,8 +260,9 @@ class CPQR:
 
     def timings(self):
         """cpqr_get_timings: per-phase ms since the last profile reset (needs profile=True):
-        stream-X pass, remaining TTMs, factor QR, Q0 compute, Q0 apply, other."""
-        ms = (C.c_double * 6)()
+        stream-X pass, remaining TTMs, factor QR (fused tail), Q0 compute, Q0 apply, other,
+        exchange."""
+        ms = (C.c_double * 7)()
         self._check(_lib.cpqr_get_timings(self._h, ms))
         return list(ms)
 

@@ -158,7 +158,7 @@ struct cpqr_ctx {
   bool graph_valid = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // profiling (opt.profile): events recorded at phase boundaries; the time since the previous
-  // mark is attributed to the mark's phase (cpqr_get_profile ms[0..5])
+  // mark is attributed to the mark's phase (cpqr_get_profile ms[0..6])
   std::vector<cudaEvent_t> evp;
   std::vector<int> evphase;
   std::vector<int64_t> evlaunch;
@@ -221,6 +221,8 @@ int64_t prod(const int64_t* d, int a, int b) {  // prod d[a..b)
 }
 
 int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+bool ne_family(int v) { return v == CPQR_NE || v == CPQR_PINV; }  // Alg. 1 (normal equations)
 
 int choose_kc(int I, int ld) {
   const size_t row = (size_t)ld * sizeof(double);
@@ -817,7 +819,7 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
 
 void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* const* Qover = nullptr,
                   const double* const* Qtover = nullptr) {
-  const bool ne = c->variant == CPQR_NE;
+  const bool ne = ne_family(c->variant);
   in.X = sl.X;
   in.ld = sl.ldims;
   in.N = c->N;
@@ -1304,9 +1306,29 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   const int N = c->N;
   const int In = (int)c->dims[n];
   prof_mark(c, -1);
-  if (c->variant == CPQR_NE) {
+  if (ne_family(c->variant)) {
     const double* Mfull = nullptr;
     int m_rowmajor = c->slabs[0].plans[n].m_rowmajor;
+    // CP-ALS-PINV: S_n^+ from the Grams (k_ne_pinv) on the side stream beside the MTTKRP
+    const bool pinv = c->variant == CPQR_PINV;
+    static const bool no_fork_ne = getenv("CPQR_NO_FORK") != nullptr;
+    const bool pfork = pinv && !c->opt.profile && !no_fork_ne;
+    if (pinv) {
+      if (pfork) {
+        CK(cudaEventRecord(c->evf, c->st));
+        CK(cudaStreamWaitEvent(c->side, c->evf, 0));
+      }
+      NePinvArgs q{};
+      for (int k = 0; k < N; ++k) q.G[k] = c->dG[k];
+      q.N = N; q.n = n; q.R = c->R;
+      q.tau = (c->opt.svd_tau < 0) ? c->R * 2.220446049250313e-16 : c->opt.svd_tau;
+      q.Mout = c->dMpinv; q.flags = c->dflags;
+      const size_t smem = (size_t)(2 * c->R * c->R + 2 * c->R * (c->R + 1)) * sizeof(double);
+      k_ne_pinv<<<1, 512, smem, pfork ? c->side : c->st>>>(q);
+      CKL();
+      if (pfork) CK(cudaEventRecord(c->evj, c->side));
+      prof_mark(c, 5);
+    }
     if (c->kt) {  // Kruskal input: M_n = B_n diag(lam_x) (*)_{k != n} B_k^T A_k
       int modes[kMaxN], K = 0;
       for (int k = 0; k < N; ++k) if (k != n) modes[K++] = k;
@@ -1341,9 +1363,12 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
         if (n == N - 1 && !m_rowmajor) return fail(c, CPQR_EINVAL, "NE: column-major M_N cannot be gathered");
         TRY(combine_w(c, n, src));
         Mfull = c->dW;
+        prof_mark(c, 6);
       }
     }
+    if (pfork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
     TailNeArgs a{};
+    a.Spinv = pinv ? c->dMpinv : nullptr;
     a.M = Mfull;
     a.m_rowmajor = m_rowmajor;
     for (int k = 0; k < N; ++k) a.G[k] = c->dG[k];
@@ -1380,7 +1405,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   static const bool no_fork = getenv("CPQR_NO_FORK") != nullptr;  // debugging: V_n QR inline
   // dimension-tree modes without an X pass have no long kernel to hide K2 behind, and a side-stream
   // multi-CTA QR would find no free SMs: there the CholeskyQR2 V_n QR runs inline (vn_inline)
-  const bool tree_nofresh = c->tree && !(n == 0 || n == c->tree_h) && c->variant != CPQR_NE && !c->kt;
+  const bool tree_nofresh = c->tree && !(n == 0 || n == c->tree_h) && !ne_family(c->variant) && !c->kt;
   c->vn_mode_cq = c->vn_cq_always || (c->vn_cq_tree && tree_nofresh);
   const bool fork = !c->opt.profile && !no_fork && !(c->vn_mode_cq && tree_nofresh);
   // there the V_n QR runs inline, but the one-CTA SVD of R0 (QR-SVD) still forks to the side
@@ -1452,6 +1477,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
       prof_mark(c, 4);
     }
     TRY(combine_w(c, n, src));
+    prof_mark(c, 6);
   }
   if (pinv_fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
   prof_mark(c, 5);
@@ -1487,12 +1513,14 @@ cpqr_status direct_fit(cpqr_ctx* c) {
     k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, c->nslab > 1 ? res + 8 + q : res);
     CKL();
   }
+  prof_mark(c, 5);
   if (c->nslab > 1) {  // virtual ranks: rank-order sum of the slab residuals
     k_sum_final<<<1, 256, 0, c->st>>>(res + 8, c->nslab, res);
     CKL();
   } else if (c->opt.world > 1) {
     CN(ncclAllReduce(res, res, 1, ncclDouble, ncclSum, c->comm, c->st));
   }
+  prof_mark(c, 6);
   k_fit_from_resid<<<1, 32, 0, c->st>>>(res, c->dnX2, c->dfit);
   CKL();
   prof_mark(c, 5);
@@ -1612,7 +1640,7 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
   if (!out || !dims) return CPQR_EINVAL;
   *out = nullptr;
   if (N < 2 || N > kMaxN || R < 1 || R > kMaxR) return CPQR_EINVAL;
-  if (variant < CPQR_NE || variant > CPQR_SVD) return CPQR_EINVAL;
+  if (variant < CPQR_NE || variant > CPQR_PINV) return CPQR_EINVAL;
   for (int k = 0; k < N; ++k)
     if (dims[k] < R || dims[k] > (1ll << 31) - 1) return CPQR_EINVAL;
   cpqr_ctx* c = new cpqr_ctx();
@@ -1644,7 +1672,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->R = R;
   c->RQ = 16 * ((R + 15) / 16);
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
-  c->tree = c->opt.mttm_tree != 0 && N >= 3 && c->variant != CPQR_NE;
+  c->tree = c->opt.mttm_tree != 0 && N >= 3 && !ne_family(c->variant);
   c->tree_h = (N + 1) / 2;
   {
     const char* f = getenv("CPQR_SLICE");  // "1" / "0" force the fused slice kernel on / off
@@ -1667,6 +1695,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   std::memset(&c->prof, 0, sizeof c->prof);
   if (cudaSetDevice(c->opt.device) != cudaSuccess) return fail(c, CPQR_ECUDA, "cudaSetDevice(%d)", c->opt.device);
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->opt.device);
+  // one SM left to the side-stream kernel beside the stream pass (V_n QR, or S_n^+ for PINV)
   c->stream_sms = (c->variant == CPQR_NE || getenv("CPQR_ALL_SMS")) ? c->sms : std::max(1, c->sms - 1);
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->user = (cudaStream_t)c->opt.stream;
@@ -1962,12 +1991,12 @@ static cpqr_status upload_factors(cpqr_ctx* c, const double* const* A, const dou
   c->flags = 0;
   for (int k = 0; k < c->N; ++k) {
     if (!A[k]) {
-      if (c->variant == CPQR_NE && k != 0) return fail(c, CPQR_EINVAL, "NE needs A[%d]", k);
+      if (ne_family(c->variant) && k != 0) return fail(c, CPQR_EINVAL, "NE needs A[%d]", k);
       if (k != 0) return fail(c, CPQR_EINVAL, "A[%d] is NULL", k);
       continue;
     }
     CK(cudaMemcpyAsync(c->dA[k], A[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
-    if (c->variant == CPQR_NE) {
+    if (ne_family(c->variant)) {
       k_gram<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dG[k]);
       CKL();
       k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[k], c->dims[k], (int)c->dims[k], R, c->RQ, c->dAt[k]);
@@ -2111,7 +2140,7 @@ CPQR_API cpqr_status cpqr_get_profile(cpqr_ctx* c, cpqr_profile* p, int reset) {
 
 CPQR_API cpqr_status cpqr_get_timings(cpqr_ctx* c, double* ms) {
   if (!c || !ms) return CPQR_EINVAL;
-  for (int i = 0; i < 6; ++i) ms[i] = c->prof.ms[i];
+  for (int i = 0; i < 7; ++i) ms[i] = c->prof.ms[i];
   return CPQR_OK;
 }
 
@@ -2146,7 +2175,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   if (!c) return CPQR_EINVAL;
   if (n < 0 || n >= c->N) return fail(c, CPQR_EINVAL, "mode %d", n);
   if (!c->have_tensor || !c->have_factors) return fail(c, CPQR_ESTATE, "tensor/factors not set");
-  if (c->variant == CPQR_NE) return fail(c, CPQR_EINVAL, "debug_mode is for the QR/SVD variants");
+  if (ne_family(c->variant)) return fail(c, CPQR_EINVAL, "debug_mode is for the QR/SVD variants");
   if (c->kt) return fail(c, CPQR_EINVAL, "debug_mode needs a dense tensor (Kruskal input forms no Y)");
   TRY(begin_call(c));
   const int R = c->R, N = c->N;

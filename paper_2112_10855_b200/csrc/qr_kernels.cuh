@@ -16,6 +16,7 @@
 //                          CholeskyQR2 path, and the one-CTA staircase Householder QR of V_n
 //                          (K2, line 7), gated by FLAG_VN_HOUSEHOLDER behind the CholeskyQR2 path.
 //   k_svd_pinv             M = U S^+ V^T of R0 by one-sided Jacobi (QR-SVD).
+//   k_ne_pinv              S_n^+ of the Hadamard product of Grams, same Jacobi (CP-ALS-PINV).
 //   k_solve_rows           Alg. 2 line 10 for factors too tall for the shared-memory tails (Householder
 //                          forced): Ahat R0^T = W (row-parallel back substitution) or Ahat = W M,
 //                          with the column sums of squares and <W, Ahat R0^T> per
@@ -516,6 +517,37 @@ __global__ void __launch_bounds__(512) k_svd_pinv(const double* __restrict__ R0,
     if (ntr > 0) atomicOr(flags, FLAG_SVD_TRUNCATED);
     if (ntrunc) *ntrunc = ntr;
   }
+}
+
+// k_ne_pinv: CP-ALS-PINV: S_n = Hadamard of the other Grams (Alg. 1 line 6),
+// then its Moore-Penrose pseudo-inverse by the same one-sided Jacobi SVD: for S = U Sigma V^T the
+// routine returns U Sigma^+ V^T = (S^+)^T = S^+ (S symmetric), dropping sigma_i <= tau sigma_max
+// (reading 32).  Depends on the Grams only, so it runs on the side stream beside the MTTKRP.
+struct NePinvArgs {
+  const double* G[8];
+  int N, n, R;
+  double tau;
+  double* Mout;
+  unsigned* flags;
+};
+__global__ void __launch_bounds__(512) k_ne_pinv(NePinvArgs a) {
+  extern __shared__ double sm[];
+  __shared__ int sflag;
+  const int R = a.R;
+  double* Ss = sm;
+  double* Ms = Ss + R * R;
+  double* Bs = Ms + R * R;
+  double* Vs = Bs + R * (R + 1);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    double v = 1.0;
+    for (int k = a.N - 1; k >= 0; --k)
+      if (k != a.n) v *= a.G[k][e];
+    Ss[e] = v;
+  }
+  __syncthreads();
+  const int ntr = jacobi_pinv(Ss, R, a.tau, Bs, Vs, Ms, &sflag);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) a.Mout[e] = Ms[e];
+  if (threadIdx.x == 0 && ntr > 0) atomicOr(a.flags, FLAG_SVD_TRUNCATED);
 }
 
 // k_solve_rows<RB>: one thread per row i: Ahat(i,:) from W(i,:) by back substitution with R0

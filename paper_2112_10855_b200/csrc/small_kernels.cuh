@@ -501,6 +501,7 @@ struct TailNeArgs {
   double* fit;
   double* Ahat;           // scratch In x R column-major
   int force_lu;           // testing: take the LU path even when S is positive definite
+  const double* Spinv;    // CP-ALS-PINV: S_n^+ (R x R, k_ne_pinv): Ahat = M S_n^+ instead of the solve
 };
 // One CTA of kNeThreads threads; RB = 8/16/32 >= R.  Rows of M are solved kNeThreads at a time on
 // a shared-memory row panel with the blocked register solves of cholqr.cuh:
@@ -531,9 +532,14 @@ __global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
     L[e] = v;
   }
   if (tid == 0) use_lu = a.force_lu;
+  if (a.Spinv)  // PINV: the pseudo-inverse in U (zero padded), no factorisation
+    for (int e = tid; e < RB * RB; e += nt) {
+      const int r = e % RB, c = e / RB;
+      U[e] = (r < R && c < R) ? a.Spinv[r + R * c] : 0.0;
+    }
   __syncthreads();
   // Cholesky S = L L^T (lower, column-major in L), by warp 0
-  if (wid == 0 && !use_lu) {
+  if (wid == 0 && !use_lu && !a.Spinv) {
     for (int j = 0; j < R; ++j) {
       double d = L[j + RB * j];
       for (int k = 0; k < j; ++k) d -= L[j + RB * k] * L[j + RB * k];
@@ -555,7 +561,8 @@ __global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
     }
   }
   __syncthreads();
-  if (use_lu) {
+  if (a.Spinv) {
+  } else if (use_lu) {
     if (tid == 0) {
       atomicOr(a.flags, FLAG_NE_CHOL_FALLBACK);
       for (int e = 0; e < RB * RB; ++e) L[e] = S[e];
@@ -586,7 +593,18 @@ __global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
 #pragma unroll 4
     for (int c = 0; c < RB; ++c)
       row[kNeLd * c] = (own && c < R) ? (a.m_rowmajor ? a.M[(int64_t)i * R + c] : a.M[i + (int64_t)In * c]) : 0.0;
-    if (!use_lu) {
+    if (a.Spinv) {  // x = m S^+ 
+      double m[RB];
+#pragma unroll
+      for (int c = 0; c < RB; ++c) m[c] = row[kNeLd * c];
+#pragma unroll 4
+      for (int c = 0; c < RB; ++c) {
+        double x = 0.0;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) x = fma(m[r], U[r + RB * c], x);
+        row[kNeLd * c] = x;
+      }
+    } else if (!use_lu) {
       cq_row_trsv<RB, false>(row, kNeLd, U, invd);  // y U = m
       cq_row_trsv<RB, true>(row, kNeLd, U, invd);   // x U^T = y
     } else {

@@ -64,6 +64,40 @@ def test_fuzz_sweep_parity(cp, dims, R, variant, tree, seed):
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (f, ref["fits"])
 
 
+def pinv_cases(n=12, seed=26426):
+    g = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        N = int(g.integers(3, 6))
+        R = int(g.integers(1, 21))
+        cap = {3: 64, 4: 40, 5: 20}[N]
+        if R > cap:
+            continue
+        dims = tuple(int(g.integers(R, cap + 1)) for _ in range(N))
+        if np.prod(dims) <= 400_000:
+            out.append((dims, R, int(g.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("dims,R,seed", pinv_cases())
+def test_fuzz_pinv_parity(cp, dims, R, seed):
+    """CP-ALS-PINV on random shapes against the oracle's pinv_svd driver."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=seed % 100000, eta=0.05)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "PINV")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    f = np.concatenate([f1, s.sweep(1)])
+    s.close()
+    ref1, ref = O.cp_als_ne(X, init, 1, solve="pinv"), O.cp_als_ne(X, init, 2, solve="pinv")
+    for k in range(len(dims)):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    assert rel(lam, ref1["lam"]) <= 1e-9
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (f, ref["fits"])
+
+
 def kt_cases(n=18, seed=31337):
     g = np.random.default_rng(seed)
     out = []

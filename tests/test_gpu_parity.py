@@ -734,18 +734,14 @@ def test_edivergred_cleared_by_set_factors(cp):
 
 
 @pytest.mark.parametrize("variant", ["QR", "SVD"])
-@pytest.mark.parametrize("dims,R,illcond", [((20000, 33, 40), 32, False), ((40, 33, 20000), 32, False),
-                                            ((13000, 9, 10), 8, False), ((40, 33, 20000), 32, True)])
-def test_tall_factor_mode(cp, dims, R, variant, illcond):
+@pytest.mark.parametrize("dims,R", [((20000, 33, 40), 32), ((40, 33, 20000), 32), ((13000, 9, 10), 8)])
+def test_tall_factor_mode(cp, dims, R, variant):
     """One factor far taller than the shared-memory tails (I_n > 3200 at R = 32 took an
     unfused path that returned EINVAL with the fast fit and overran a partials buffer): the
     multi-kernel CholeskyQR2 handles it in the first mode and in the last (with the fused fast
-    fit); when its kappa guard rejects the panel (the tall initial factor with a column scaled by
-    1e-9, kappa ~ 1e9) the gated one-CTA Householder fallback factors it."""
+    fit)."""
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=11 + R, eta=0.01)
     A0 = [a.copy() for a in init]
-    if illcond:
-        A0[2][:, 3] *= 1e-9
     s = cp.CPQR(dims, R, variant)
     s.set_tensor(Xc)
     s.set_factors(A0)
@@ -761,11 +757,29 @@ def test_tall_factor_mode(cp, dims, R, variant, illcond):
     s.close()
 
 
+@pytest.mark.parametrize("m,R", [(20000, 32), (13000, 8)])
+def test_tall_factor_qr_fallback(cp, m, R):
+    """A tall panel with kappa ~ 1e10: the multi-kernel CholeskyQR2 rejects it and the gated
+    one-CTA global-memory Householder (k_tall_fallback) factors it (Q orthonormal, QR = A, R as
+    LAPACK's up to the column scaling's conditioning)."""
+    rng = np.random.default_rng(m)
+    U, _ = np.linalg.qr(rng.standard_normal((m, R)))
+    Vt, _ = np.linalg.qr(rng.standard_normal((R, R)))
+    A = U @ np.diag(np.logspace(0, -10, R)) @ Vt
+    s = cp.CPQR((m, m), R, "QR")
+    Q, Rf = s.debug_qr(A)
+    assert np.linalg.norm(Q.T @ Q - np.eye(R)) <= 1e-13
+    assert rel(Q @ Rf, A) <= 1e-14 and np.all(np.diag(Rf) >= 0)
+    Qo, Ro = O.qr_pos(A)
+    assert rel(Rf, Ro) <= 1e-12
+    s.close()
+
+
 def test_tall_factor_forced_householder(cp, monkeypatch):
     """The very-tall Householder path with CholeskyQR2 disabled (CPQR_FACTOR_QR=householder):
     k_solve_rows forms Ahat and its partials (buffer sized for any I_n), k_tall_fallback the rest."""
     monkeypatch.setenv("CPQR_FACTOR_QR", "householder")
-    dims, R = (9000, 20, 64), 32
+    dims, R = (9000, 33, 64), 32
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=3, eta=0.01)
     s = cp.CPQR(dims, R, "QR")
     s.set_tensor(Xc)
@@ -806,3 +820,30 @@ def test_debug_calls_leave_state_and_bound_m(cp):
     f_c = t.sweep(2)
     t.close()
     assert np.array_equal(np.concatenate([f_a, f_b]), f_c)
+
+
+@pytest.mark.parametrize("dims,R", [((30, 40, 50), 5), ((12, 10, 9, 11), 4)])
+def test_pinv_exact_duplicate(cp, dims, R):
+    """CP-ALS-PINV on an exactly singular S_n (columns 1 and 2 of the initial
+    factors equal): the pseudo-inverse drops one singular value (SVD_TRUNCATED on both sides),
+    gives the minimum-norm solution (the two columns stay equal) and matches the oracle."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=61 + len(dims), eta=0.01)
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    dup = [a.copy() for a in init]
+    for k in range(N):
+        dup[k][:, 1] = dup[k][:, 0]
+    s = cp.CPQR(dims, R, "PINV", svd_tau=1e-12)
+    s.set_tensor(Xc)
+    s.set_factors(dup)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    ref1 = O.cp_als_ne(X, dup, 1, solve="pinv", tau=1e-12)
+    assert ref1["flags"] & O.FLAG_SVD_TRUNCATED and s.flags & cp.FLAG_SVD_TRUNCATED
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+        assert rel(A[k][:, 1], A[k][:, 0]) <= 1e-10
+    f = np.concatenate([f1, s.sweep(2)])
+    ref = O.cp_als_ne(X, dup, 3, solve="pinv", tau=1e-12)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()

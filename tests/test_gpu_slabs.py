@@ -45,6 +45,7 @@ CASES = [
     ((24, 20, 18, 16), 8, "QR", False),
     ((24, 20, 18, 16), 8, "SVD", True),       # dimension tree
     ((16, 14, 12, 16), 6, "NE", False),
+    ((16, 14, 12, 16), 6, "PINV", False),
     # C4-like 5-way
     ((9, 8, 7, 6, 8), 4, "SVD", False),
     ((9, 8, 7, 6, 8), 4, "QR", True),
@@ -60,7 +61,9 @@ def test_virtual_ranks_match_oracle(cp, dims, R, variant, tree, world):
     s = cp.CPQR(dims, R, variant, tree=tree, world=world, comm="local")
     s.set_tensor(Xc)
     s.set_factors(init)
-    if variant != "NE":
+    ne = variant in ("NE", "PINV")
+    solve = "pinv" if variant == "PINV" else "chol"
+    if not ne:
         Qs, Rs = [None] * N, [None] * N
         for k in range(N):
             Qs[k], Rs[k] = O.qr_pos(init[k])
@@ -73,8 +76,8 @@ def test_virtual_ranks_match_oracle(cp, dims, R, variant, tree, world):
             assert rel(out["W"], O.apply_q0(Yo, n, Q0o)) <= 1e-11
         ref = O.cp_als_qr(X, init, 3, variant=variant)
     else:
-        ref = O.cp_als_ne(X, init, 3)
-    ref1 = O.cp_als_ne(X, init, 1) if variant == "NE" else O.cp_als_qr(X, init, 1, variant=variant)
+        ref = O.cp_als_ne(X, init, 3, solve=solve)
+    ref1 = O.cp_als_ne(X, init, 1, solve=solve) if ne else O.cp_als_qr(X, init, 1, variant=variant)
     f1 = s.sweep(1)
     lam, A = s.get_factors()
     for k in range(N):

@@ -9,9 +9,9 @@ The projected time of one rank on its own GPU is
 
     T_rank(p) = (stream + rest + q0_apply) / p + tail + other + max(0, vn_qr - stream / p) + comm(p)
 
-(the V_n QR hides behind the stream pass on the side stream, as on one GPU; comm(p) is NOT
-measured here -- no multi-GPU box -- and is reported separately as an assumed per-mode NCCL
-latency).  Also printed: the measured sweep time of the LOCAL context (all slabs in sequence, CUDA
+(the V_n QR hides behind the stream pass on the side stream, as on one GPU; the virtual ranks'
+combine kernel is excluded; comm(p) is NOT measured here -- no multi-GPU box -- and is an
+assumed per-mode NCCL latency).  Also printed: the measured sweep time of the LOCAL context (all slabs in sequence, CUDA
 graph), which is p times the slab work plus the tails.  A projection, not a measurement.
 
   python tools/slab_projection.py [--configs 3 4 5] [--ps 1 2 4 8] [--comm-us 15]
@@ -55,7 +55,7 @@ def main():
             pr = s.profile(reset=True)
             s.close()
             ms = [v / args.sweeps for v in pr["ms"]]
-            stream, rest, fqr, vn, q0a, other = ms
+            stream, rest, fqr, vn, q0a, other, exch = ms
             slab = (stream + rest + q0a) / p
             t_rank = slab + fqr + other + max(0.0, vn - stream / p) + conf.N * args.comm_us / 1e3 * (p > 1)
             # the LOCAL context's own sweep time (graph, all p slabs in sequence)
@@ -75,7 +75,7 @@ def main():
                 base = t_rank
             row = dict(config=conf.name, variant=variant, tree=args.tree, p=p,
                        per_sweep_ms=dict(stream_pass=stream, rest_ttm=rest, q0_apply=q0a, vn_qr=vn,
-                                         factor_qr_tail=fqr, other=other),
+                                         factor_qr_tail=fqr, other=other, local_combine=exch),
                        slab_work_per_rank_ms=slab, projected_rank_ms=t_rank,
                        projected_sweeps_s=1e3 / t_rank, projected_aggregate_speedup=base / t_rank,
                        projected_efficiency=base / t_rank / p, local_context_sweep_ms=t_local,
