@@ -393,10 +393,12 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
     """CP-ALS-QR / CP-ALS-QR-SVD, Alg. 2, exactly `sweeps` sweeps (no early
     stop; reading 12).  X: Fortran (I_1..I_N) array.  A0: initial factors (A0[0] unused,
     PAPER.md:350).  fit after mode N of every sweep (reading 13): fast or
-    direct.  kt = (lam_x, B): Kruskal input instead of X (X = None; fast fit only,
-    PAPER.md:440-456).  Returns dict(lam, factors, fits, flags, debug)."""
+    direct (PAPER.md:411).  kt = (lam_x, B): Kruskal input instead of X (X = None, PAPER.md:440-456;
+    the direct fit then forms X = full_tensor(lam_x, B)).  Returns dict(lam, factors,
+    fits, flags, debug)."""
     N = X.ndim if kt is None else len(kt[1])
     nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K"))) if kt is None else ktensor_norm2(*kt)
+    Xd = X if (kt is None or fit_mode == "fast") else full_tensor(*kt)
     factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
     Qs, Rs = [None] * N, [None] * N
     for k in range(1, N):                                         # line 3 (PAPER.md:351)
@@ -418,7 +420,7 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
         if fit_mode == "fast":
             fits.append(fit_fast_qr(nX2, last["W"], last["Ahat"], last["R0"], Rs[N - 1], lam))
         else:
-            fits.append(fit_direct(X, lam, factors))
+            fits.append(fit_direct(Xd, lam, factors))
     return dict(lam=lam, factors=factors, fits=fits, flags=flags, debug=debug, Qs=Qs, Rs=Rs,
                 nX2=nX2)
 
@@ -426,9 +428,10 @@ def cp_als_qr(X, A0, sweeps, variant="QR", tau=-1.0, fit_mode="fast", debug_swee
 def cp_als_ne(X, A0, sweeps, fit_mode="fast", kt=None, solve="chol", tau=-1.0):
     """CP-ALS with normal equations, Alg. 1, exactly `sweeps` sweeps; solve="pinv"
     is CP-ALS-PINV (PAPER.md:264-266).  Fit: PAPER.md:417-425 (fast) or direct.  kt = (lam_x, B):
-    Kruskal input instead of X."""
+    Kruskal input instead of X (a direct fit forms X = full_tensor(lam_x, B))."""
     N = X.ndim if kt is None else len(kt[1])
     nX2 = float(np.dot(X.ravel(order="K"), X.ravel(order="K"))) if kt is None else ktensor_norm2(*kt)
+    Xd = X if (kt is None or fit_mode == "fast") else full_tensor(*kt)
     factors = [np.array(A, dtype=np.float64, order="F") for A in A0]
     grams = [A.T @ A for A in factors]                            # line 3 (PAPER.md:248)
     lam = np.ones(factors[0].shape[1])
@@ -443,7 +446,7 @@ def cp_als_ne(X, A0, sweeps, fit_mode="fast", kt=None, solve="chol", tau=-1.0):
         if fit_mode == "fast":
             fits.append(fit_fast_ne(nX2, last["M"], last["Ahat"], last["S"], grams[N - 1], lam))
         else:
-            fits.append(fit_direct(X, lam, factors))
+            fits.append(fit_direct(Xd, lam, factors))
     return dict(lam=lam, factors=factors, fits=fits, flags=flags, nX2=nX2)
 
 

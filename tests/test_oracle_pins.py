@@ -464,6 +464,27 @@ def test_sine_of_sums_ktensor_closed_form(N, n):
     assert np.max(np.abs(X - np.sin(sum(grid)))) <= 1e-13
 
 
+def test_ktensor_direct_fit_resolves_below_the_fast_fit_floor():
+    """on the 4-way sine of sums (exact rank N = 4 representation exists,
+    PAPER.md:599-602) CP-ALS-QR converges to machine precision; the DIRECT relative error of the
+    Kruskal driver equals the residual against the closed form sin(x_1 + .. + x_4) (an
+    independent formation of X) and falls below 1e-13, where the fast formula's
+    ||X||^2 - 2<X,Xh> + ||Xh||^2 cancellation (relative error ~ sqrt(eps) ~ 1e-8) cannot see it."""
+    N, n = 4, 16
+    lam_x, B = O.sine_of_sums_ktensor(N, n)
+    g = np.random.default_rng(7)
+    A0 = [g.standard_normal((n, N)) for _ in range(N)]
+    out = O.cp_als_qr(None, A0, 30, fit_mode="direct", kt=(lam_x, B))
+    x = 2 * np.pi * np.arange(n) / n
+    Xc = np.sin(sum(np.meshgrid(*([x] * N), indexing="ij")))
+    Xh = O.full_tensor(out["lam"], out["factors"])
+    rel_closed = np.linalg.norm((Xc - Xh).ravel()) / np.linalg.norm(Xc.ravel())
+    assert abs((1 - out["fits"][-1]) - rel_closed) <= 1e-14
+    assert 1 - out["fits"][-1] <= 1e-13
+    fast = O.cp_als_qr(None, A0, 30, kt=(lam_x, B))
+    assert np.max(np.abs(np.array(fast["fits"][:5]) - np.array(out["fits"][:5]))) <= 1e-7  # same iterates
+
+
 @pytest.mark.parametrize("dims,S,R", [((7, 6, 5), 3, 2), ((5, 4, 6, 3), 4, 3)])
 def test_ktensor_formulas_match_the_formed_tensor(dims, S, R):
     """||X||^2, W_n = Y_(n) Q0 and M_n = X_(n) Z_n computed from the factors
