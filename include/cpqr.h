@@ -153,8 +153,11 @@ cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const double* X, 
  * ones).  Each mode then computes W_n = B_n diag(lambda) [((.)_{k != n} Q_k^T B_k)^T Q0]
  * (QR / SVD) or the MTTKRP B_n diag(lambda) (*)_{k != n} B_k^T A_k (NE) in O(R^N S + I_n R S),
  * and ||X||^2 = lambda^T ((*)_k B_k^T B_k) lambda.  Replaces a dense tensor set before (and
- * cpqr_set_tensor replaces this).  The arrays are copied before return.  Single GPU (world = 1),
- * FAST fit only; cpqr_debug_mode is unavailable.  Errors: EINVAL, ENOMEM, ECUDA. */
+ * cpqr_set_tensor replaces this).  The arrays are copied before return.  Single GPU (world = 1);
+ * cpqr_debug_mode is unavailable.  The DIRECT fit (opt.fit_mode) evaluates
+ * ||X - Xh|| entry by entry from the factors of both Kruskal tensors, never forming either
+ * (O(prod I_k (S + R)) flops; S + R <= 512), so relative errors below the fast fit's sqrt(eps)
+ * floor are resolved.  Errors: EINVAL, ENOMEM, ECUDA. */
 cpqr_status cpqr_set_ktensor(cpqr_ctx* ctx, int S, const double* lambda, const double* const* B);
 
 /* Set the factors: A[k] is a host pointer to the column-major I_k x R matrix A_k (k = 0..N-1;

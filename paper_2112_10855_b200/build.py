@@ -28,8 +28,11 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force=False, verbose=True):
-    if not force and up_to_date():
+def build(force=False, verbose=True, out=None):
+    """out: another path for an instrumented build (e.g. CPQR_DEBUG_TIMING=1 ... --out libcpqr_dbg.so,
+    loaded with CPQR_LIB=...); the default in-tree libcpqr.so is the product library."""
+    LIB = out or globals()["LIB"]
+    if not force and out is None and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
     # link against libnccl.so.2 by soname (the pip package ships no unversioned symlink)
@@ -50,4 +53,6 @@ def build(force=False, verbose=True):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="ptxas" if "--ptxas" in sys.argv else True)
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    build(force="--force" in sys.argv, verbose="ptxas" if "--ptxas" in sys.argv else True,
+          out=os.path.join(HERE, o) if o and not os.path.isabs(o) else o)

@@ -52,6 +52,7 @@ struct TtmStep {
   int gps, nseg;
   int cw = 8;  // slice TMA: consumer warps per CTA (4: two CTAs per SM)
   unsigned modes = 0;  // contracted modes (bit k = mode k of the global tensor)
+  int skm = -1;        // strided TMA: stream-K split -1 auto (ragged waves), 0 off, 1 always
 };
 
 struct DiagStep {
@@ -141,6 +142,8 @@ struct cpqr_ctx {
   double *dlam = nullptr, *dQ0 = nullptr, *dR0 = nullptr, *dW = nullptr, *dWp = nullptr,
          *dAhat = nullptr;
   double* dnX2p = nullptr;   // per-slab partial ||X||^2 (CPQR_COMM_LOCAL), summed in rank order
+  double* dSk = nullptr;     // stream-K partial slots: 2 per CTA x (256-row unit x R)
+  int streamk = -1;          // CPQR_STREAMK: -1 auto, 0 off, 1 always (strided stream kernel)
   unsigned* dq0cnt = nullptr;  // per-row-block arrival counters of k_q0_apply_tc (self re-arming)
   double* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
@@ -331,6 +334,8 @@ struct PlanIn {
   int h = 0;                // tree split: halves [0, h) and [h, N)
   bool tree_fresh = false;  // this mode computes its half's intermediate from X
   double* tbuf = nullptr;   // the tree buffer
+  double* sk = nullptr;     // stream-K partial slots of the strided stream kernel
+  int skm = -1;             // stream-K mode (CPQR_STREAMK)
 };
 
 // cudaMalloc; with CPQR_POISON=1 (debugging) the block is filled with 0xFF bytes (NaN as fp64), so
@@ -457,6 +462,8 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         const uint32_t box[3] = {16, 16, 1};
         if (make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, k, s.I)) {
           s.kind = 4;
+          s.P = in.sk;
+          s.skm = in.skm;
           s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0, "CPQR_ST_STRIDED", (s.I + kBK - 1) / kBK <= 3 ? 3 : 4);
         }
       }
@@ -684,7 +691,7 @@ void set_smem(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
+int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns #launches
   const int NT = (R + 7) / 8, NQB = (NT + 1) / 2;
   if (s.kind == 4) {
     // CW consumer warps per CTA over 32 CW-row units.  CW = 4 runs two CTAs per SM, each with its
@@ -697,14 +704,19 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
     const size_t smem = 3072 + (size_t)S * stage;
     const int64_t units = ((s.A + 32 * cw - 1) / (32 * cw)) * s.B;
     const int grid = (int)std::min<int64_t>(units, (int64_t)sms * (cw == 4 ? 2 : 1));
+    // stream-K split (k_strided_tma) when the round-robin waves are ragged by > 2 %: e.g. C5 at 8
+    // slabs, 500 units on 147 CTAs.  CPQR_STREAMK=0/1 forces it off / on.
+    const double waves = (double)units / grid;
+    const bool sk = s.P && grid > 1 && units > grid && (s.skm == 1 || (s.skm != 0 && std::ceil(waves) / waves > 1.02));
+    double* P = sk ? s.P : nullptr;
 #define STR(NTV, NPV)                                                                                  \
   {                                                                                                     \
     if (cw == 4) {                                                                                      \
       set_smem(k_strided_tma<NTV, NPV, 4>, smem);                                                       \
-      k_strided_tma<NTV, NPV, 4><<<grid, (4 + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S); \
+      k_strided_tma<NTV, NPV, 4><<<grid, (4 + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
     } else {                                                                                            \
       set_smem(k_strided_tma<NTV, NPV>, smem);                                                          \
-      k_strided_tma<NTV, NPV><<<grid, (kCW + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S); \
+      k_strided_tma<NTV, NPV><<<grid, (kCW + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
     }                                                                                                   \
   }
     // producer warps issuing the 16 X boxes of a stage in parallel: a single issuing thread bounds
@@ -719,6 +731,12 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
       switch (NT) { case 1: STR(1, 1) break; case 2: STR(2, 1) break; case 3: STR(3, 1) break; default: STR(4, 1) break; }
     }
 #undef STR
+    if (sk) {
+      k_strided_fixup<<<dim3(grid - 1, (32 * cw * R + 255) / 256), 256, 0, st>>>(P, s.A, R, s.B, (s.I + kBK - 1) / kBK,
+                                                                                 32 * cw, grid, s.out);
+      return 2;
+    }
+    return 1;
   } else if (s.kind == 5) {
     // 8 warps of 2 fibre tiles; CPQR_FIB_CW=4 runs 4 warps of 4 tiles, two CTAs per SM (parity-
     // tested, but measured slower: C2 NE 2698 -> 2660 sweeps/s, neutral on C2 / C5 intermediates)
@@ -780,6 +798,7 @@ void launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {
     const int grid = (int)std::min<int64_t>(s.L, (int64_t)sms * 4);
     k_slice_fixup<<<grid, 256, 0, st>>>(s.P, s.nslots, s.L, s.nfb, s.G, R * R, s.out);
   }
+  return 1;
 }
 
 cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
@@ -794,7 +813,7 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
         k_reduce_slices<<<grid, 256, 0, c->st>>>(s.in, s.nseg, s.L, c->R * c->R, s.out);
         break;
       }
-      default: launch_tma(s, c->R, c->st, c->stream_sms); break;
+      default: c->launch_count += launch_tma(s, c->R, c->st, c->stream_sms) - 1; break;
     }
     CKL();
   }
@@ -833,6 +852,8 @@ void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* 
   in.h = c->tree_h;
   in.tree_fresh = (n == 0 || n == c->tree_h);
   in.tbuf = sl.dTree;
+  in.sk = c->dSk;
+  in.skm = c->streamk;
   in.RQ = c->RQ;
   for (int k = 0; k < c->N; ++k) {
     const double* base = ne ? c->dA[k] : c->dQ[k];
@@ -1496,6 +1517,20 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
 cpqr_status direct_fit(cpqr_ctx* c) {
   prof_mark(c, -1);
   double* res = c->dred + 4096;
+  if (c->kt) {  // Kruskal input: the residual entry by entry from the factors (k_kt_resid)
+    KtResidArgs a{};
+    for (int k = 0; k < c->N; ++k) { a.B[k] = c->dKtB[k]; a.A[k] = c->dA[k]; a.I[k] = c->dims[k]; }
+    a.N = c->N; a.S = c->ktS; a.R = c->R; a.lamx = c->dKtLam; a.lam = c->dlam; a.part = c->dred;
+    const int grid = c->sms * 4;
+    k_kt_resid<<<grid, 256, 0, c->st>>>(a);
+    CKL();
+    k_sum_final<<<1, 256, 0, c->st>>>(c->dred, grid, res);
+    CKL();
+    k_fit_from_resid<<<1, 32, 0, c->st>>>(res, c->dnX2, c->dfit);
+    CKL();
+    prof_mark(c, 5);
+    return CPQR_OK;
+  }
   for (int q = 0; q < c->nslab; ++q) {
     const Slab& sl = c->slabs[q];
     ResidArgs a{};
@@ -1672,6 +1707,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->R = R;
   c->RQ = 16 * ((R + 15) / 16);
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
+  c->streamk = getenv("CPQR_STREAMK") ? atoi(getenv("CPQR_STREAMK")) : -1;
   c->tree = c->opt.mttm_tree != 0 && N >= 3 && !ne_family(c->variant);
   c->tree_h = (N + 1) / 2;
   {
@@ -1725,6 +1761,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   if (c->opt.world > 1)
     for (int q = 0; q < c->nslab; ++q) CK(dmalloc(&c->slabs[q].dWloc, sizeof(double) * imax * R));
   CK(dmalloc(&c->dnX2p, sizeof(double) * 64));
+  CK(dmalloc(&c->dSk, sizeof(double) * 2 * (2 * c->sms) * 256 * R));
   CK(dmalloc(&c->dAhat, sizeof(double) * imax * R));
   CK(dmalloc(&c->dRstack, sizeof(double) * 8 * R * R));
   CK(dmalloc(&c->dQtop, sizeof(double) * 8 * R * R));
@@ -1830,7 +1867,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->evf) cudaEventDestroy(c->evf);
   if (c->evj) cudaEventDestroy(c->evj);
-  double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dWp, c->dAhat, c->buf[0], c->buf[1],
+  double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dSk, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred,
                   c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2};
   for (double* p : ps) if (p) cudaFree(p);
@@ -1946,7 +1983,8 @@ CPQR_API cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const do
 CPQR_API cpqr_status cpqr_set_ktensor(cpqr_ctx* c, int S, const double* lam, const double* const* B) {
   if (!c || !B || S < 1) return c ? fail(c, CPQR_EINVAL, "Kruskal input: S >= 1 and B required") : CPQR_EINVAL;
   if (c->opt.world > 1) return fail(c, CPQR_EINVAL, "Kruskal input is single-GPU (the factors are replicated)");
-  if (c->opt.fit_mode != CPQR_FIT_FAST) return fail(c, CPQR_EINVAL, "Kruskal input supports the FAST fit only");
+  if (c->opt.fit_mode == CPQR_FIT_DIRECT && S + c->R > kKtResidMaxSR)
+    return fail(c, CPQR_EINVAL, "Kruskal DIRECT fit: S + R = %d > %d", S + c->R, kKtResidMaxSR);
   for (int k = 0; k < c->N; ++k)
     if (!B[k]) return fail(c, CPQR_EINVAL, "B[%d] is NULL", k);
   TRY(begin_call(c));

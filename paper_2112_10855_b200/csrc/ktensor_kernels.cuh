@@ -101,6 +101,57 @@ __global__ void k_kt_mttkrp(const double* __restrict__ Bn, int64_t In, int S, co
   }
 }
 
+// DIRECT residual of a Kruskal input: ||X - Xh||^2 with X = [[lam_x; B]] (rank S)
+// and the model Xh = [[lam; A]] (rank R) evaluated entry by entry, never stored: the difference is
+// the rank-(S + R) Kruskal tensor [[ (lam_x, -lam); (B_k | A_k) ]], so for one index tuple
+// j = (i_2, .., i_N) of modes 2..N a warp forms p(s) = c_s prod_{k >= 2} C_k(i_k, s) in shared memory
+// and then d(i_1) = sum_s C_1(i_1, s) p(s) for every i_1 (lanes), accumulating d^2.  Each entry's
+// difference is formed before squaring, so the relative error resolves down to ~eps (the fast fit
+// ||X||^2 - 2 <X, Xh> + ||Xh||^2 cancels to ~sqrt(eps)).  Fixed-order partials.
+struct KtResidArgs {
+  const double* B[kKtMaxModes];  // I_k x S
+  const double* A[kKtMaxModes];  // I_k x R (normalised factors)
+  int64_t I[kKtMaxModes];
+  int N, S, R;
+  const double* lamx;            // S
+  const double* lam;             // R
+  double* part;                  // gridDim.x partial sums
+};
+constexpr int kKtResidMaxSR = 512;
+__global__ void __launch_bounds__(256) k_kt_resid(KtResidArgs a) {
+  __shared__ double pw[8][kKtResidMaxSR];
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int SR = a.S + a.R;
+  int64_t J = 1;
+  for (int k = 1; k < a.N; ++k) J *= a.I[k];
+  double acc = 0.0;
+  for (int64_t j = (int64_t)blockIdx.x * 8 + wid; j < J; j += (int64_t)gridDim.x * 8) {
+    for (int s = lane; s < SR; s += 32) {
+      const bool isx = s < a.S;
+      const int q = isx ? s : s - a.S;
+      double v = isx ? a.lamx[q] : -a.lam[q];
+      int64_t x = j;
+      for (int k = 1; k < a.N; ++k) {
+        const int64_t ik = x % a.I[k];
+        x /= a.I[k];
+        v *= isx ? a.B[k][ik + a.I[k] * q] : a.A[k][ik + a.I[k] * q];
+      }
+      pw[wid][s] = v;
+    }
+    __syncwarp();
+    for (int64_t i1 = lane; i1 < a.I[0]; i1 += 32) {
+      double d = 0.0;
+      for (int s = 0; s < a.S; ++s) d = fma(a.B[0][i1 + a.I[0] * s], pw[wid][s], d);
+      for (int r = 0; r < a.R; ++r) d = fma(a.A[0][i1 + a.I[0] * r], pw[wid][a.S + r], d);
+      acc = fma(d, d, acc);
+    }
+    __syncwarp();
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) a.part[blockIdx.x] = acc;
+}
+
 // ||X||^2 = sum_{s,t} lam(s) lam(t) prod_k G_k(s, t), G_k = B_k^T B_k (N blocks of S x S).
 __global__ void __launch_bounds__(256) k_kt_norm2(const double* __restrict__ G, int N, int S,
                                                   const double* __restrict__ lam, double* __restrict__ out) {

@@ -157,10 +157,23 @@ __device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& fu
 // warps); Q map 2D {RQ, I} over the transposed padded panel Qt[i*RQ + r], box {16, 16} (NT/2
 // boxes).  Consumer warp w owns rows 32w..32w+31: M-tiles mt = 2p + s hold rows 16(2w+p) + 2g + s
 // (one 16-byte load feeds two tiles).  CW = 4 runs two CTAs per SM (see launch_tma).
+//
+// Work decomposition.  P == nullptr: unit u goes to CTA u mod G (persistent round robin).  With
+// few units per CTA that leaves a ragged last wave (C5 at 8 slabs: 500 units on 147 CTAs = 3.4
+// waves, 15 % idle), so P != nullptr selects a stream-K split: the W = units x KS k-steps are cut
+// into G equal contiguous ranges, one per CTA.  A unit covered by one CTA is stored to T; a unit
+// cut by a range boundary leaves each CTA's partial sum in a slot P[(2 c + h) * 32 CW * R] (h = 0:
+// the CTA's first unit, 1: its last), and k_strided_fixup adds the slots in CTA order (fixed order:
+// bitwise reproducible).
+struct SkRange {  // the k-step range [it0, it1) of CTA c under the stream-K split
+  int64_t it0, it1;
+  __device__ __forceinline__ SkRange(int64_t W, int c, int G) : it0(W * c / G), it1(W * (c + 1) / G) {}
+};
+
 template <int NT, int NP = 1, int CW = kCW>
 __global__ void __launch_bounds__((CW + NP) * 32, CW == 4 ? 2 : 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
-              int I, int64_t B, int R, double* __restrict__ T, int S) {
+              int I, int64_t B, int R, double* __restrict__ T, int S, double* __restrict__ P) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (NT + 1) / 2;
   constexpr uint32_t XBYTES = 2 * CW * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
@@ -176,6 +189,22 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   const int64_t nA = (A + 32 * CW - 1) / (32 * CW);
   const int64_t units = nA * B;
   const int KS = (I + kBK - 1) / kBK;
+  const SkRange rg(units * KS, blockIdx.x, gridDim.x);
+  // the unit segments [ks0, ks1) of this CTA, in order: round robin (P == nullptr) or stream-K
+  auto segments = [&](auto&& body) {
+    if (P == nullptr) {
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) body(u, 0, KS);
+    } else {
+      for (int64_t it = rg.it0; it < rg.it1;) {
+        const int64_t u = it / KS;
+        const int ks0 = (int)(it - u * KS);
+        const int64_t rem = rg.it1 - it;
+        const int ks1 = (rem < (int64_t)(KS - ks0)) ? ks0 + (int)rem : KS;
+        body(u, ks0, ks1);
+        it += ks1 - ks0;
+      }
+    }
+  };
   if (warp >= CW) {  // ---------------------------------------------------------- producer(s)
     // NP producer warps split the 16 X boxes of a stage (the per-box TMA issue cost bounds the
     // HBM-bound passes); producer 0 also loads Q and does the arrive.expect_tx for the whole stage
@@ -186,10 +215,10 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
       if (pw == 0) prefetch_tmap(&tmQ);
       const uint64_t pol = policy_evict_first();
       RingPos rp;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      segments([&](int64_t u, int ks0, int ks1) {
         const int b = (int)(u / nA);
         const int a0 = (int)((u - (int64_t)b * nA) * 32 * CW);
-        for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+        for (int ks = ks0; ks < ks1; ++ks, rp.next(S)) {
           const int s = rp.s;
           mbar_wait(&empty[s], rp.ph ^ 1);
           if (pw == 0) mbar_expect_tx(&full[s], STAGE);
@@ -201,14 +230,15 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
 #pragma unroll
             for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
         }
-      }
+      });
     }
     return;
   }
   // --------------------------------------------------------------------------------- consumers
   const int g = lane >> 2, t = lane & 3;
+  const int64_t first_u = rg.it0 / KS;
   RingPos rp;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  segments([&](int64_t u, int ks0, int ks1) {
     const int64_t b = u / nA;
     const int64_t a0 = (u - b * nA) * 32 * CW;
     double acc[4][NT][2];
@@ -216,7 +246,7 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     for (int m = 0; m < 4; ++m)
 #pragma unroll
       for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-    for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+    for (int ks = ks0; ks < ks1; ++ks, rp.next(S)) {
       const int s = rp.s;
       mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE, qs = xs + XBYTES;
@@ -243,19 +273,59 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    double* __restrict__ Tb = T + A * (int64_t)R * b;
+    if (ks0 == 0 && ks1 == KS) {  // the whole unit: straight to T
+      double* __restrict__ Tb = T + A * (int64_t)R * b;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int64_t row = a0 + 32 * warp + 16 * (m >> 1) + 2 * g + (m & 1);
-      if (row >= A) continue;
+      for (int m = 0; m < 4; ++m) {
+        const int64_t row = a0 + 32 * warp + 16 * (m >> 1) + 2 * g + (m & 1);
+        if (row >= A) continue;
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        const int r0 = 8 * n + 2 * t;
-        if (r0 < R) Tb[row + A * r0] = acc[m][n][0];
-        if (r0 + 1 < R) Tb[row + A * (r0 + 1)] = acc[m][n][1];
+        for (int n = 0; n < NT; ++n) {
+          const int r0 = 8 * n + 2 * t;
+          if (r0 < R) Tb[row + A * r0] = acc[m][n][0];
+          if (r0 + 1 < R) Tb[row + A * (r0 + 1)] = acc[m][n][1];
+        }
+      }
+    } else {  // a stream-K partial: this CTA's slot (first or last unit of its range)
+      double* __restrict__ Pb = P + ((int64_t)2 * blockIdx.x + (u == first_u ? 0 : 1)) * (32 * CW) * R;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int row = 32 * warp + 16 * (m >> 1) + 2 * g + (m & 1);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int r0 = 8 * n + 2 * t;
+          if (r0 < R) Pb[row + 32 * CW * r0] = acc[m][n][0];
+          if (r0 + 1 < R) Pb[row + 32 * CW * (r0 + 1)] = acc[m][n][1];
+        }
       }
     }
-  }
+  });
+}
+
+// Stream-K fix-up of k_strided_tma: blockIdx.x = range boundary c - 1 (c = 1..G-1), blockIdx.y = a
+// 256-entry chunk of the UR x R unit tile.  A boundary that cuts a unit and is the first boundary
+// inside it sums the segments of CTAs c0 = c-1 .. c1 in that order into T (one entry per thread:
+// every load in flight at once -- a loop over the tile per CTA was latency-bound at 35 us).
+__global__ void __launch_bounds__(256) k_strided_fixup(const double* __restrict__ P, int64_t A, int R, int64_t B,
+                                                       int KS, int UR, int G, double* __restrict__ T) {
+  const int c = 1 + blockIdx.x;
+  const int64_t nA = (A + UR - 1) / UR;
+  const int64_t W = nA * B * KS;
+  const int64_t it = W * c / G;
+  const int64_t u = it / KS;
+  if (it == u * KS) return;                           // boundary on a unit edge: nothing cut
+  const int64_t itp = W * (c - 1) / G;
+  if (itp > u * KS) return;                           // not the first boundary inside u
+  const int e = blockIdx.y * blockDim.x + threadIdx.x;
+  if (e >= UR * R) return;
+  const int row = e % UR, r = e / UR;
+  const int64_t b = u / nA, a0 = (u - b * nA) * UR;
+  if (a0 + row >= A) return;
+  const int c0 = c - 1;
+  const int h0 = (itp / KS == u) ? 0 : 1;              // u is c0's first unit, or its last
+  double v = P[((int64_t)2 * c0 + h0) * UR * R + e];
+  for (int cc = c; cc < G && W * cc / G < (u + 1) * KS; ++cc) v += P[((int64_t)2 * cc) * UR * R + e];
+  T[a0 + row + A * ((int64_t)r + (int64_t)R * b)] = v;
 }
 
 // ======================================================== fibre kernels (mode 1 / fused slice)
