@@ -504,11 +504,12 @@ __global__ void __launch_bounds__(512) k_cq_compact(CqArgs a) {
   double* Y = X + ld * RB;     // panel of W / Q1 rows
   const int i = r0 + tid;
   const bool own = tid < rows;
-  if (tid == 0 && b == 0) atomicAnd(a.flags, ~cq_hh_bit(a));
   #pragma unroll 1
   for (int e = tid; e < 2 * ld * RB; e += blockDim.x) X[e] = 0.0;
   #pragma unroll 1
   for (int e = tid; e < 2 * RB * RB; e += blockDim.x) Ms[e] = 0.0;  // Ms, R0s
+  pdl_wait();                // W, R0 / M of the predecessors are complete from here on
+  if (tid == 0 && b == 0) atomicAnd(a.flags, ~cq_hh_bit(a));
   __syncthreads();
   CQ_T(13);
   // all global inputs in flight at once (cp.async), one wait

@@ -15,6 +15,14 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "d"(a), "d"(b));
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with the programmatic-serialization
+// attribute may start while its predecessor on the stream drains; pdl_wait() (griddepcontrol.wait)
+// blocks until the predecessor grid has completed and its memory is visible, so every kernel of the
+// per-mode chain calls it after its prologue (shared-memory / barrier set-up, tensor-map prefetch)
+// and before its first global access.  Without the attribute it returns at once.  (The launches use
+// the attribute only with CPQR_PDL=1: measured slower, see cpqr.cu.)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -144,6 +144,10 @@ struct cpqr_ctx {
   double* dnX2p = nullptr;   // per-slab partial ||X||^2 (CPQR_COMM_LOCAL), summed in rank order
   double* dSk = nullptr;     // stream-K partial slots: 2 per CTA x (256-row unit x R)
   int streamk = -1;          // CPQR_STREAMK: -1 auto, 0 off, 1 always (strided stream kernel)
+  // programmatic dependent launch along the per-mode chain (CPQR_PDL=1).  Off by default: measured
+  // slower in every config (interleaved A/B, 30 sweeps x 2: C2 -3 %, C3 -1 %, C5 -1 %; with early
+  // launch_dependents triggers in the persistent stream kernels C2 -7 %, C3 tree -9 %)
+  bool pdl = false;
   unsigned* dq0cnt = nullptr;  // per-row-block arrival counters of k_q0_apply_tc (self re-arming)
   double* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
@@ -691,7 +695,37 @@ void set_smem(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns #launches
+// Launch with the optional programmatic-dependent-launch attribute (the kernel may begin while its
+// stream predecessor drains; it calls pdl_wait() before touching global memory, common.cuh) and an
+// optional cluster shape.  Captured into the sweep's CUDA graph as programmatic edges.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                      int cluster, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  // returns #launches
   const int NT = (R + 7) / 8, NQB = (NT + 1) / 2;
   if (s.kind == 4) {
     // CW consumer warps per CTA over 32 CW-row units.  CW = 4 runs two CTAs per SM, each with its
@@ -713,10 +747,10 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns 
   {                                                                                                     \
     if (cw == 4) {                                                                                      \
       set_smem(k_strided_tma<NTV, NPV, 4>, smem);                                                       \
-      k_strided_tma<NTV, NPV, 4><<<grid, (4 + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
+      launch_ex(k_strided_tma<NTV, NPV, 4>, grid, (4 + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
     } else {                                                                                            \
       set_smem(k_strided_tma<NTV, NPV>, smem);                                                          \
-      k_strided_tma<NTV, NPV><<<grid, (kCW + NPV) * 32, smem, st>>>(s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
+      launch_ex(k_strided_tma<NTV, NPV>, grid, (kCW + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
     }                                                                                                   \
   }
     // producer warps issuing the 16 X boxes of a stage in parallel: a single issuing thread bounds
@@ -732,8 +766,8 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns 
     }
 #undef STR
     if (sk) {
-      k_strided_fixup<<<dim3(grid - 1, (32 * cw * R + 255) / 256), 256, 0, st>>>(P, s.A, R, s.B, (s.I + kBK - 1) / kBK,
-                                                                                 32 * cw, grid, s.out);
+      launch_ex(k_strided_fixup, grid - 1, 1024, 0, st, pdl, 1, (const double*)P, s.A, R, s.B, (s.I + kBK - 1) / kBK,
+                32 * cw, grid, s.out);
       return 2;
     }
     return 1;
@@ -751,10 +785,10 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns 
   {                                                                                                \
     if (cw == 4) {                                                                                 \
       set_smem(k_fiber_tma<MTV, 4>, smem);                                                         \
-      k_fiber_tma<MTV, 4><<<grid, 5 * 32, smem, st>>>(s.mx, s.mq, s.I, s.F, R, s.out, S);          \
+      launch_ex(k_fiber_tma<MTV, 4>, grid, 5 * 32, smem, st, pdl, 1, s.mx, s.mq, s.I, s.F, R, s.out, S); \
     } else {                                                                                       \
       set_smem(k_fiber_tma<MTV>, smem);                                                            \
-      k_fiber_tma<MTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I, s.F, R, s.out, S);        \
+      launch_ex(k_fiber_tma<MTV>, grid, kTmaThreads, smem, st, pdl, 1, s.mx, s.mq, s.I, s.F, R, s.out, S); \
     }                                                                                              \
   }
     switch (NT) { case 1: FIB(1) break; case 2: FIB(2) break; case 3: FIB(3) break; default: FIB(4) break; }
@@ -765,14 +799,14 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns 
 #define SLC(MTV, NFV)                                                                                      \
   {                                                                                                        \
     set_smem(k_slice_tma<MTV, NFV>, smem);                                                                 \
-    k_slice_tma<MTV, NFV><<<(int)s.G, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, \
-                                                               s.out, s.P, s.nslots, s.S);                 \
+    launch_ex(k_slice_tma<MTV, NFV>, (int)s.G, kTmaThreads, smem, st, pdl, 1, s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, \
+              s.ldq2, R, s.out, s.P, s.nslots, s.S);                                                       \
   }
 #define SLC4(MTV)                                                                                          \
   {                                                                                                        \
     set_smem(k_slice_tma<MTV, 4, 4>, smem);                                                                \
-    k_slice_tma<MTV, 4, 4><<<(int)s.G, 5 * 32, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R,    \
-                                                          s.out, s.P, s.nslots, s.S);                      \
+    launch_ex(k_slice_tma<MTV, 4, 4>, (int)s.G, 5 * 32, smem, st, pdl, 1, s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, \
+              s.ldq2, R, s.out, s.P, s.nslots, s.S);                                                       \
   }
     if (s.cw == 4) {
       switch (NT) { case 1: SLC4(1) break; case 2: SLC4(2) break; case 3: SLC4(3) break; default: SLC4(4) break; }
@@ -790,13 +824,14 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms) {  // returns 
 #define SSM(MTV)                                                                                             \
   {                                                                                                          \
     set_smem(k_slice_small_tma<MTV>, smem);                                                                  \
-    k_slice_small_tma<MTV><<<grid, kTmaThreads, smem, st>>>(s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, R, s.out, s.S); \
+    launch_ex(k_slice_small_tma<MTV>, grid, kTmaThreads, smem, st, pdl, 1, s.mx, s.mq, s.I1, s.I2, s.L, s.Q2, s.ldq2, \
+              R, s.out, s.S);                                                                                  \
   }
     switch (NT) { case 1: SSM(1) break; case 2: SSM(2) break; case 3: SSM(3) break; default: SSM(4) break; }
 #undef SSM
   } else if (s.kind == 7) {
     const int grid = (int)std::min<int64_t>(s.L, (int64_t)sms * 4);
-    k_slice_fixup<<<grid, 256, 0, st>>>(s.P, s.nslots, s.L, s.nfb, s.G, R * R, s.out);
+    launch_ex(k_slice_fixup, grid, 256, 0, st, pdl, 1, (const double*)s.P, s.nslots, s.L, s.nfb, s.G, R * R, s.out);
   }
   return 1;
 }
@@ -813,7 +848,7 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
         k_reduce_slices<<<grid, 256, 0, c->st>>>(s.in, s.nseg, s.L, c->R * c->R, s.out);
         break;
       }
-      default: c->launch_count += launch_tma(s, c->R, c->st, c->stream_sms) - 1; break;
+      default: c->launch_count += launch_tma(s, c->R, c->st, c->stream_sms, c->pdl) - 1; break;
     }
     CKL();
   }
@@ -1002,13 +1037,15 @@ cpqr_status launch_cq_compact(cpqr_ctx* c, const CqArgs& q, int RB, int tb, cuda
   cfg.blockDim = dim3(tb);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = q.nb;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (c->pdl && st == c->st) ? 2 : 1;
   cudaError_t e = cudaSuccess;
 #ifdef CPQR_DEBUG_TIMING
   const int reps = getenv("CPQR_CQ_TWICE") ? 2 : 1;  // warm-vs-cold instruction-fetch experiment
@@ -1102,13 +1139,15 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
         cfg.blockDim = dim3(std::max(tl, tr));
         cfg.dynamicSmemBytes = 0;
         cfg.stream = c->st;
-        cudaLaunchAttribute at[1];
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = nl;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = c->pdl ? 2 : 1;
         cudaError_t e;
         switch (RB) {
           case 8: e = cudaLaunchKernelEx(&cfg, k_rq_fused<8>, q); break;
@@ -1259,7 +1298,8 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
   KS = (KT + kpc - 1) / kpc;
   dim3 grid(iblocks, (unsigned)KS);
   const int NT = (c->R + 7) / 8;
-#define Q0A(NTV) k_q0_apply_tc<NTV><<<grid, 256, 0, c->st>>>(p.Y, p.Aa, In, p.Bb, c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout)
+#define Q0A(NTV) launch_ex(k_q0_apply_tc<NTV>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb, (const double*)c->dQ0, c->R, \
+                           kpc, (int)KS, c->dWp, c->dq0cnt, Wout)
   switch (NT) { case 1: Q0A(1); break; case 2: Q0A(2); break; case 3: Q0A(3); break; default: Q0A(4); break; }
 #undef Q0A
   CKL();
@@ -1294,7 +1334,7 @@ cpqr_status combine_w(cpqr_ctx* c, int n, const double* const* src) {
     for (int q = 0; q < c->nslab; ++q) rp.p[q] = src[q];
     const int64_t cnt = c->dims[n] * R;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, (int64_t)c->sms * 4));
-    k_sum_ranks<<<grid, 256, 0, c->st>>>(rp, c->nslab, cnt, c->dW);
+    launch_ex(k_sum_ranks, grid, 256, 0, c->st, c->pdl, 1, rp, c->nslab, cnt, c->dW);
     CKL();
   } else {
     for (int q = 0; q < c->nslab; ++q)
@@ -1708,6 +1748,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->RQ = 16 * ((R + 15) / 16);
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
   c->streamk = getenv("CPQR_STREAMK") ? atoi(getenv("CPQR_STREAMK")) : -1;
+  c->pdl = getenv("CPQR_PDL") && atoi(getenv("CPQR_PDL")) == 1;
   c->tree = c->opt.mttm_tree != 0 && N >= 3 && !ne_family(c->variant);
   c->tree_h = (N + 1) / 2;
   {

@@ -218,6 +218,7 @@ struct RqArgs {
 
 __device__ __forceinline__ bool rq_skip(const RqArgs& a) {
   __shared__ unsigned fl;
+  pdl_wait();  // the CholeskyQR2 launch before it has set (or not) the fallback flag
   if (threadIdx.x == 0) fl = a.gated ? *a.flags : 0x200u;
   __syncthreads();
   return (fl & 0x200u) == 0;

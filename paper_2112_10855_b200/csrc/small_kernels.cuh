@@ -48,6 +48,7 @@ struct RankPtrs {
   const double* p[kMaxRanks];
 };
 __global__ void k_sum_ranks(RankPtrs a, int nr, int64_t n, double* out) {
+  pdl_wait();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     double s = a.p[0][e];
     for (int q = 1; q < nr; ++q) s += a.p[q][e];
@@ -276,6 +277,7 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
               int kpc, int KS, double* __restrict__ Wp, unsigned* __restrict__ counters, double* __restrict__ W) {
   __shared__ double red[8][64 * NT];
   __shared__ int last;
+  pdl_wait();
   const int64_t J = Aa * Bb, KT = (J + 3) / 4;
   const int ib = blockIdx.x, ks = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;

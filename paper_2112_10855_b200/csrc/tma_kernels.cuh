@@ -186,6 +186,8 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     fence_barrier_init();
   }
   __syncthreads();
+  if (threadIdx.x == 0) prefetch_tmap(&tmX);
+  pdl_wait();                // the predecessor (previous mode's tail: Q panels) has completed
   const int64_t nA = (A + 32 * CW - 1) / (32 * CW);
   const int64_t units = nA * B;
   const int KS = (I + kBK - 1) / kBK;
@@ -302,12 +304,14 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   });
 }
 
-// Stream-K fix-up of k_strided_tma: blockIdx.x = range boundary c - 1 (c = 1..G-1), blockIdx.y = a
-// 256-entry chunk of the UR x R unit tile.  A boundary that cuts a unit and is the first boundary
-// inside it sums the segments of CTAs c0 = c-1 .. c1 in that order into T (one entry per thread:
-// every load in flight at once -- a loop over the tile per CTA was latency-bound at 35 us).
-__global__ void __launch_bounds__(256) k_strided_fixup(const double* __restrict__ P, int64_t A, int R, int64_t B,
-                                                       int KS, int UR, int G, double* __restrict__ T) {
+// Stream-K fix-up of k_strided_tma: one CTA of 1024 threads per range boundary c = 1..G-1.  A
+// boundary that cuts a unit and is the first boundary inside it sums the segments of CTAs
+// c0 = c-1 .. c1 in that order into T.  Each thread issues the loads of its (up to) 8 entries
+// before any add: one CTA per boundary with every load in flight (a CTA per 256 entries was bound
+// by CTA launch rate at ~20 us, a looped CTA by load latency at ~35 us).
+__global__ void __launch_bounds__(1024) k_strided_fixup(const double* __restrict__ P, int64_t A, int R, int64_t B,
+                                                        int KS, int UR, int G, double* __restrict__ T) {
+  pdl_wait();
   const int c = 1 + blockIdx.x;
   const int64_t nA = (A + UR - 1) / UR;
   const int64_t W = nA * B * KS;
@@ -316,16 +320,35 @@ __global__ void __launch_bounds__(256) k_strided_fixup(const double* __restrict_
   if (it == u * KS) return;                           // boundary on a unit edge: nothing cut
   const int64_t itp = W * (c - 1) / G;
   if (itp > u * KS) return;                           // not the first boundary inside u
-  const int e = blockIdx.y * blockDim.x + threadIdx.x;
-  if (e >= UR * R) return;
-  const int row = e % UR, r = e / UR;
-  const int64_t b = u / nA, a0 = (u - b * nA) * UR;
-  if (a0 + row >= A) return;
+  int c1 = c;                                         // last CTA with a segment in u
+  while (c1 + 1 < G && W * (c1 + 1) / G < (u + 1) * KS) ++c1;
   const int c0 = c - 1;
   const int h0 = (itp / KS == u) ? 0 : 1;              // u is c0's first unit, or its last
-  double v = P[((int64_t)2 * c0 + h0) * UR * R + e];
-  for (int cc = c; cc < G && W * cc / G < (u + 1) * KS; ++cc) v += P[((int64_t)2 * cc) * UR * R + e];
-  T[a0 + row + A * ((int64_t)r + (int64_t)R * b)] = v;
+  const int64_t b = u / nA, a0 = (u - b * nA) * UR;
+  const int n = UR * R;
+  constexpr int kPer = 8;
+  double v[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    v[q] = (e < n) ? P[((int64_t)2 * c0 + h0) * n + e] : 0.0;
+  }
+  for (int cc = c; cc <= c1; ++cc) {
+    double w[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = threadIdx.x + q * blockDim.x;
+      w[q] = (e < n) ? P[((int64_t)2 * cc) * n + e] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) v[q] += w[q];
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = threadIdx.x + q * blockDim.x;
+    const int row = e % UR, r = e / UR;
+    if (e < n && a0 + row < A) T[a0 + row + A * ((int64_t)r + (int64_t)R * b)] = v[q];
+  }
 }
 
 // ======================================================== fibre kernels (mode 1 / fused slice)
@@ -378,6 +401,7 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();
   const int64_t units = (F + 127) / 128;
   const int KS = (I + kBK - 1) / kBK;
   if (warp == CW) {
@@ -461,6 +485,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();
   const int nfb = (I2 + BN - 1) / BN;
   const int64_t U = L * nfb;
   const int64_t G = gridDim.x;
@@ -623,6 +648,7 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();
   const int nf2 = I2 / 8;
   const int64_t units = (L + 7) / 8;
   const int KS = (I1 + kBK - 1) / kBK;
@@ -726,6 +752,7 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 // Sum the partial slots of the slices split across CTA ranges (fixed order).
 __global__ void k_slice_fixup(const double* __restrict__ P, int nslots, int64_t L, int nfb, int64_t G, int RR,
                               double* __restrict__ Y) {
+  pdl_wait();
   const int64_t U = L * nfb;
   for (int64_t l = blockIdx.x; l < L; l += gridDim.x) {
     const int64_t c0 = ((l * nfb + 1) * G - 1) / U;

@@ -650,7 +650,7 @@ def test_batched_stopping_rule_and_paper_shape(cp):
 
 def test_profile_and_timings(cp):
     """opt.profile = 1 (the paper's per-phase time breakdown): eager sweeps with
-    events around each phase.  cpqr_get_timings returns the same six per-phase ms as
+    events around each phase.  cpqr_get_timings returns the same seven per-phase ms as
     cpqr_get_profile; the stream-X pass is timed, the algorithmic bytes equal N passes over X, and
     the fits equal those of the graph path bitwise (profiling changes launch order only)."""
     dims, R = (40, 36, 30), 6
@@ -664,10 +664,13 @@ def test_profile_and_timings(cp):
         if prof:
             t = s.timings()
             p = s.profile(reset=True)
-            assert len(t) == 6 and t == p["ms"]
+            assert len(t) == 7 and t == p["ms"]
             assert t[0] > 0.0 and all(v >= 0.0 for v in t)
+            assert t[2] > 0.0  # the fused factor-QR tail is timed (it was never written in round 1)
             assert p["bytes0"] == len(dims) * 8.0 * np.prod(dims)
-            assert s.timings() == [0.0] * 6  # reset by profile(reset=True)
+            # launches per phase add up to the launches of the profiled sweeps
+            assert sum(p["launches"]) > 0 and p["launches"][2] >= 3
+            assert s.timings() == [0.0] * 7  # reset by profile(reset=True)
         s.close()
     assert np.array_equal(fits[0], fits[1])
 
