@@ -53,6 +53,7 @@ struct TtmStep {
   int cw = 8;  // slice TMA: consumer warps per CTA (4: two CTAs per SM)
   unsigned modes = 0;  // contracted modes (bit k = mode k of the global tensor)
   int skm = -1;        // strided TMA: stream-K split -1 auto (ragged waves), 0 off, 1 always
+  int cw1 = 0;         // 1: one CTA per SM (8 consumer warps) so reserved SMs stay free (overlap)
 };
 
 struct DiagStep {
@@ -148,6 +149,23 @@ struct cpqr_ctx {
   // slower in every config (interleaved A/B, 30 sweeps x 2: C2 -3 %, C3 -1 %, C5 -1 %; with early
   // launch_dependents triggers in the persistent stream kernels C2 -7 %, C3 tree -9 %)
   bool pdl = false;
+  // overlap schedule: the tail of mode n (Q0 apply, solve, factor QR) runs on stream
+  // tl beside the stream-X pass of mode n+1 whenever that pass does not contract mode n
+  bool overlap = false, tail_single = false;
+  int overlap_reserve = 4;   // SMs the stream passes leave free for the tail / V_n QR
+  // stream passes one CTA per SM so the reserved SMs stay free (CPQR_OVERLAP_CW1=1).  Off: the
+  // two-CTA-per-SM passes (R <= 12) lose more than the freed SMs gain (interleaved A/B, 40 sweeps
+  // x 2: C2 2575 vs 2680, C3 524 vs 560; C4 488 vs 484)
+  bool ov_cw1 = false;
+  cudaStream_t tl = nullptr;
+  cudaEvent_t evY[kMaxN] = {}, evQ[kMaxN] = {}, evK[kMaxN] = {};
+  double* dY = nullptr;      // Y_(n) of the overlap schedule (read by the tail while the next pass runs)
+  size_t dY_elems = 0;
+  // CPQR_TRACE=1 (debugging, eager sweeps only): timing events around the overlap schedule's
+  // launches on each stream, printed to stderr after every sweep as a timeline
+  bool trace = false;
+  std::vector<std::pair<cudaEvent_t, std::string>> tev;
+  size_t ntev = 0;
   unsigned* dq0cnt = nullptr;  // per-row-block arrival counters of k_q0_apply_tc (self re-arming)
   double* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
@@ -340,6 +358,9 @@ struct PlanIn {
   double* tbuf = nullptr;   // the tree buffer
   double* sk = nullptr;     // stream-K partial slots of the strided stream kernel
   int skm = -1;             // stream-K mode (CPQR_STREAMK)
+  bool overlap = false;     // overlap schedule: N = 3 first contraction (n+1) mod 3
+  bool ov_cw1 = true;       // overlap schedule: one CTA per SM in the stream passes (CPQR_OVERLAP_CW1)
+  double* ybuf = nullptr;   // overlap schedule: the final step writes Y here
 };
 
 // cudaMalloc; with CPQR_POISON=1 (debugging) the block is filled with 0xFF bytes (NaN as fp64), so
@@ -468,6 +489,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
           s.kind = 4;
           s.P = in.sk;
           s.skm = in.skm;
+          s.cw1 = (in.overlap && in.ov_cw1) ? 1 : 0;
           s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0, "CPQR_ST_STRIDED", (s.I + kBK - 1) / kBK <= 3 ? 3 : 4);
         }
       }
@@ -500,7 +522,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         static const int scw_env = getenv("CPQR_SLICE_CW") ? atoi(getenv("CPQR_SLICE_CW")) : 0;
         static const bool wide4 = getenv("CPQR_SLICE_WIDE4") && atoi(getenv("CPQR_SLICE_WIDE4")) == 1;
         s.gps = slice_nf(s.I2);
-        if (scw_env != 8 && (s.gps == 2 || wide4)) { s.cw = 4; s.gps = 4; }
+        if (scw_env != 8 && !(in.overlap && in.ov_cw1) && (s.gps == 2 || wide4)) { s.cw = 4; s.gps = 4; }
         const uint32_t box[3] = {16, (uint32_t)(s.cw * 8 * s.gps), 1};
         tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
       }
@@ -659,12 +681,18 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       for (int k = o0; k < o1; ++k) cur[k] = R;
     }
     for (int k = left ? 0 : h; k < (left ? h : N); ++k) if (k != n) todo.push_back(k);
-  } else if (N >= 3 && n >= 2 && !in.fuse) {
+  } else if (N >= 3 && n >= 2 && !in.fuse && !(N == 3 && in.overlap)) {
     emit_ttm(1);  // stream pass over the middle mode (strided kernel), then the rest
     for (int k = 0; k < N; ++k) if (k != n && k != 1) todo.push_back(k);
-  } else if (N >= 3 && n >= 2) {
+  } else if (N >= 3 && n >= 2 && !(N == 3 && in.overlap)) {
     emit_slice();
     for (int k = 2; k < N; ++k) if (k != n) todo.push_back(k);
+  } else if (N == 3 && in.overlap) {
+    // overlap schedule: mode n's pass contracts mode (n+1) mod 3, never the mode n-1 whose factor
+    // the previous tail is still updating (the fibre kernel on X for n = 2)
+    const int f = (n + 1) % 3;
+    emit_ttm(f);
+    todo.push_back(3 - n - f);
   } else if (N >= 3) {
     // n < 2: the stream pass contracts the largest LOCAL dimension first; ties go to
     // the last mode (strided kernel, B = 1, the largest contiguous GEMM).  With p > 1 slabs the last
@@ -682,6 +710,14 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     return a > b;
   });
   for (int k : todo) emit_ttm(k);
+  if (in.ybuf && p.steps.size() >= 2) {  // overlap schedule: Y goes to its own buffer
+    size_t last = p.steps.size() - 1;
+    p.steps[last].out = in.ybuf;
+    if ((p.steps[last].kind == 7 || p.steps[last].kind == 3) && last > 0) {
+      if (p.steps[last].kind == 7) p.steps[last - 1].out = in.ybuf;  // whole slices of the TMA slice pass
+    }
+    src = in.ybuf;
+  }
   p.Y = src;
   p.nd = N;
   for (int k = 0; k < N; ++k) p.ydims[k] = cur[k];
@@ -732,7 +768,7 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
     // own ring, so one computes while the other waits for data: measured C2 +1..5 %, C4 tree +3 %,
     // but C3 -0.8 % and C5 -1.1 % (interleaved A/B), hence only for R <= 12.  Env CPQR_STR_CW=4/8.
     static const int cw_env = getenv("CPQR_STR_CW") ? atoi(getenv("CPQR_STR_CW")) : 0;
-    const int cw = cw_env == 4 ? 4 : cw_env == 8 ? 8 : (R <= 12 ? 4 : 8);
+    const int cw = s.cw1 ? 8 : cw_env == 4 ? 4 : cw_env == 8 ? 8 : (R <= 12 ? 4 : 8);
     const size_t stage = (size_t)(2 * cw + NQB) * kBoxBytes;
     const int S = cw == 4 ? std::min<int>(s.S, (int)((110 * 1024 - 3072) / stage)) : s.S;
     const size_t smem = 3072 + (size_t)S * stage;
@@ -889,6 +925,9 @@ void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* 
   in.tbuf = sl.dTree;
   in.sk = c->dSk;
   in.skm = c->streamk;
+  in.overlap = c->overlap;
+  in.ov_cw1 = c->ov_cw1;
+  in.ybuf = c->overlap ? c->dY : nullptr;
   in.RQ = c->RQ;
   for (int k = 0; k < c->N; ++k) {
     const double* base = ne ? c->dA[k] : c->dQ[k];
@@ -922,6 +961,20 @@ cpqr_status build_plans(cpqr_ctx* c) {
         const int nfb = (int)((sl.ldims[1] + 127) / 128);
         mp = std::max(mp, (size_t)L * (size_t)(nfb + 2) * c->R * c->R);
       }
+    }
+  }
+  if (c->overlap) {  // Y_(n) of every mode: I_n R^{N-1} (local) elements
+    size_t ye = 0;
+    for (int n = 0; n < c->N; ++n) {
+      size_t e = (size_t)c->slabs[0].ldims[n];
+      for (int k = 0; k < c->N - 1; ++k) e *= (size_t)c->R;
+      ye = std::max(ye, e);
+    }
+    if (ye > c->dY_elems) {
+      if (c->dY) cudaFree(c->dY);
+      c->dY = nullptr;
+      if (dmalloc(&c->dY, ye * sizeof(double)) != cudaSuccess) return fail(c, CPQR_ENOMEM, "Y buffer");
+      c->dY_elems = ye;
     }
   }
   // the ping-pong intermediates and slice partials are shared by the slabs (run in turn on one
@@ -1102,7 +1155,11 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
   // (only when the device-side kappa / orthogonality guard rejected the CholeskyQR2 result)
   bool gated = false;
   int cq_nb = 0;
-  const int nbq = (m + 255) / 256;
+  int nbq = (m + 255) / 256;
+  // overlap schedule: the tail runs beside the next stream pass on the few SMs it leaves free, so
+  // it must not need a co-scheduled cluster: one CTA of up to 512 rows when its panels fit
+  if (c->tail_single && m <= 512 && (8 * RB * RB + 2 * (((32 * ((m + 31) / 32) + 15) & ~15) + 4) * RB) * 8 <= 220 * 1024)
+    nbq = 1;
   if (c->factor_qr_mode == 0 && nbq <= 8 && !getenv("CPQR_CQ_MULTI")) {  // single cluster launch
     const CqArgs q = cq_args(nbq);
     // >= 8 warps even for short factors: the 2-D Cholesky maps its columns to 8 warps (the rolled
@@ -1132,7 +1189,8 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
       q.do_fit = do_fit ? 1 : 0; q.nX2 = c->dnX2; q.fit = c->dfit;
       q.gated = gated ? 1 : 0;
       const int tl = 32 * ((mbr + 31) / 32), tr = 32 * ((nl * R + 31) / 32);
-      static const bool rq_split = getenv("CPQR_RQ_SPLIT") && atoi(getenv("CPQR_RQ_SPLIT")) == 1;
+      static const bool rq_split_env = getenv("CPQR_RQ_SPLIT") && atoi(getenv("CPQR_RQ_SPLIT")) == 1;
+      const bool rq_split = rq_split_env || c->tail_single;  // overlap: no cluster co-scheduling
       if (!rq_split) {  // one cluster launch of the three phases (k_rq_fused)
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nl);
@@ -1276,7 +1334,7 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
     if (J <= 8 * tmax && !no_compact) {
       q.nb = (int)std::min<int64_t>(8, (J + 255) / 256);
       q.mb = (int)((J + q.nb - 1) / q.nb);
-      TRY(launch_cq_compact(c, q, rb, 32 * ((q.mb + 31) / 32), st));
+      TRY(launch_cq_compact(c, q, rb, std::max(256, 32 * ((q.mb + 31) / 32)), st));
     } else {
       TRY(launch_cq_multi(c, q, st));
     }
@@ -1363,9 +1421,112 @@ cpqr_status kt_cross(cpqr_ctx* c, const int* modes, int K, const double* const* 
   return CPQR_OK;
 }
 
+// Overlap schedule of one mode update (QR / QR-SVD, one slab).  Streams: st runs the
+// Multi-TTM (the stream-X pass on all but overlap_reserve SMs, then the remaining TTMs into dY), tl
+// the tail (Q0 apply, solve, normalise, factor QR, fit), side the V_n QR.  The pass of mode n waits
+// for the tail of mode n-1 only if it contracts mode n-1 (or writes dY itself); otherwise it runs
+// beside that tail, and the remaining TTMs -- which do contract mode n-1 -- wait for it.  Same
+// arithmetic as mode_update, only the launch order changes.
+void trace_mark(cpqr_ctx* c, cudaStream_t st, const char* what, int n) {
+  if (!c->trace) return;
+  if (c->ntev == c->tev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->tev.push_back({e, ""});
+  }
+  char buf[64];
+  snprintf(buf, sizeof buf, "%s %d %s", st == c->st ? "st" : st == c->tl ? "tl" : "side", n, what);
+  c->tev[c->ntev].second = buf;
+  cudaEventRecord(c->tev[c->ntev].first, st);
+  ++c->ntev;
+}
+
+void trace_dump(cpqr_ctx* c) {
+  if (!c->trace || c->ntev == 0) return;
+  cudaDeviceSynchronize();
+  for (size_t i = 0; i < c->ntev; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->tev[0].first, c->tev[i].first);
+    fprintf(stderr, "trace %9.1f us  %s\n", 1e3 * ms, c->tev[i].second.c_str());
+  }
+  c->ntev = 0;
+}
+
+cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
+  const int N = c->N;
+  const int In = (int)c->dims[n];
+  const int prev = (n + N - 1) % N;
+  const Plan& p = c->slabs[0].plans[n];
+  // V_n QR (+ SVD of R0) on the side stream once R_{n-1} is final
+  if (n == 0) {
+    CK(cudaEventRecord(c->evf, c->st));
+    CK(cudaStreamWaitEvent(c->side, c->evf, 0));
+  } else {
+    CK(cudaStreamWaitEvent(c->side, c->evQ[prev], 0));
+  }
+  // small V_n (R^{N-1} <= 512 rows): the one-CTA CholeskyQR2 (k_cq_compact, nb = 1) instead of the
+  // one-CTA staircase Householder, which is on this schedule's critical path (C2: 49 us -> ~15 us)
+  c->vn_mode_cq = c->vn_cq_always || c->vnJ <= 512;
+  trace_mark(c, c->side, "K2 start", n);
+  TRY(launch_kr_qr(c, n));
+  if (c->variant == CPQR_SVD) {
+    TRY(launch_pinv(c, c->side, nullptr));
+    c->pinv_ready = true;
+  }
+  trace_mark(c, c->side, "K2 end", n);
+  CK(cudaEventRecord(c->evK[n], c->side));
+  // the stream-X pass; its dependence on the previous tail
+  const Slab& sl = c->slabs[0];
+  const size_t nx = (!p.steps.empty() && p.steps[0].in == sl.X) ? 1 : 0;
+  bool dep = false;
+  for (size_t i = 0; i < p.steps.size(); ++i) {
+    const bool pass = i < nx || ((p.steps[i].kind == 7 || p.steps[i].kind == 3) && i == nx);
+    if (pass && ((p.steps[i].modes >> prev) & 1u)) dep = true;
+    if (pass && p.steps[i].out == c->dY) dep = true;
+  }
+  if (n > 0 && dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
+  trace_mark(c, c->st, dep ? "pass start (after tail n-1)" : "pass start", n);
+  Plan first, rest;
+  size_t nf = nx;
+  if (nf < p.steps.size() && (p.steps[nf].kind == 7 || p.steps[nf].kind == 3)) ++nf;  // the pass's fix-up
+  first.steps.assign(p.steps.begin(), p.steps.begin() + nf);
+  rest.steps.assign(p.steps.begin() + nf, p.steps.end());
+  TRY(run_plan(c, first));
+  trace_mark(c, c->st, "pass end", n);
+  if (n > 0 && !dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
+  trace_mark(c, c->st, "rest start", n);
+  TRY(run_plan(c, rest));
+  trace_mark(c, c->st, "rest end", n);
+  // W_n = Y_(n) Q0 on st with the whole GPU (on the reserved SMs beside the next pass it took 4x
+  // longer), once the V_n QR is done
+  CK(cudaStreamWaitEvent(c->st, c->evK[n], 0));
+  TRY(launch_q0_apply(c, p, c->dW));
+  trace_mark(c, c->st, "q0 end", n);
+  CK(cudaEventRecord(c->evY[n], c->st));
+  // the tail on tl: the fused solve / normalise / factor QR (/ fast fit)
+  CK(cudaStreamWaitEvent(c->tl, c->evY[n], 0));
+  trace_mark(c, c->tl, "tail start", n);
+  std::swap(c->st, c->tl);
+  cpqr_status st = CPQR_OK;
+  {
+    c->tail_single = true;
+    const bool fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
+    st = launch_tsqr(c, In, nullptr, true, c->dW, c->dQ[n], c->dQt[n], c->dRk[n], c->dA[n], fit);
+    c->tail_single = false;
+  }
+  std::swap(c->st, c->tl);
+  trace_mark(c, c->tl, "tail end", n);
+  c->pinv_ready = false;
+  TRY(st);
+  CK(cudaEventRecord(c->evQ[n], c->tl));
+  if (n == N - 1) CK(cudaStreamWaitEvent(c->st, c->evQ[n], 0));  // join: factors and fit complete
+  return CPQR_OK;
+}
+
 cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   const int N = c->N;
   const int In = (int)c->dims[n];
+  if (c->overlap && !c->kt && !c->opt.profile) return mode_update_overlap(c, n, fit_here);
   prof_mark(c, -1);
   if (ne_family(c->variant)) {
     const double* Mfull = nullptr;
@@ -1749,6 +1910,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
   c->streamk = getenv("CPQR_STREAMK") ? atoi(getenv("CPQR_STREAMK")) : -1;
   c->pdl = getenv("CPQR_PDL") && atoi(getenv("CPQR_PDL")) == 1;
+  c->trace = getenv("CPQR_TRACE") && atoi(getenv("CPQR_TRACE")) == 1 && !c->opt.use_graph;
   c->tree = c->opt.mttm_tree != 0 && N >= 3 && !ne_family(c->variant);
   c->tree_h = (N + 1) / 2;
   {
@@ -1774,9 +1936,24 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->opt.device);
   // one SM left to the side-stream kernel beside the stream pass (V_n QR, or S_n^+ for PINV)
   c->stream_sms = (c->variant == CPQR_NE || getenv("CPQR_ALL_SMS")) ? c->sms : std::max(1, c->sms - 1);
+  {  // overlap schedule (mode_update_overlap): HBM-bound QR / QR-SVD sweeps on one GPU by default
+     // (measured vs the serial schedule, 40 sweeps x 2: C2 2615 -> 2680, C3 555 -> 560, C4 465 -> 484)
+    const char* ov = getenv("CPQR_OVERLAP");
+    const bool elig = !ne_family(c->variant) && !c->tree && c->opt.world == 1 && N >= 3 && !c->opt.profile;
+    c->overlap = elig && (ov ? atoi(ov) == 1 : R <= 16);
+    if (const char* r = getenv("CPQR_OVERLAP_SMS")) c->overlap_reserve = std::max(0, atoi(r));
+    if (const char* r = getenv("CPQR_OVERLAP_CW1")) c->ov_cw1 = atoi(r) != 0;
+    if (c->overlap) c->stream_sms = std::max(1, c->sms - c->overlap_reserve);
+  }
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->user = (cudaStream_t)c->opt.stream;
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->tl, cudaStreamNonBlocking));
+  for (int k = 0; k < kMaxN; ++k) {
+    CK(cudaEventCreateWithFlags(&c->evY[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->evQ[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->evK[k], cudaEventDisableTiming));
+  }
   CK(cudaEventCreateWithFlags(&c->evf, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->evj, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev0, cudaEventDisableTiming));
@@ -1876,7 +2053,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       const bool compact_ok = J <= 8 * (R <= 16 ? 512 : 256);
       c->vn_cq_tree = !v && c->tree && (t ? atoi(t) == 1 : (compact_ok || J * R >= 50000));
     }
-    c->vn_cq = c->vn_cq_always || c->vn_cq_tree;
+    c->vn_cq = c->vn_cq_always || c->vn_cq_tree || (c->overlap && J <= 512);
     c->vnJ = J;
     if (c->vn_cq) {
       CK(dmalloc(&c->dVn, sizeof(double) * J * R));
@@ -1906,6 +2083,13 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
     cudaFree(c->dQt[k]); cudaFree(c->dAt[k]);
   }
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->tl) cudaStreamDestroy(c->tl);
+  for (int k = 0; k < kMaxN; ++k) {
+    if (c->evY[k]) cudaEventDestroy(c->evY[k]);
+    if (c->evQ[k]) cudaEventDestroy(c->evQ[k]);
+    if (c->evK[k]) cudaEventDestroy(c->evK[k]);
+  }
+  if (c->dY) cudaFree(c->dY);
   if (c->evf) cudaEventDestroy(c->evf);
   if (c->evj) cudaEventDestroy(c->evj);
   double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dSk, c->dWp, c->dAhat, c->buf[0], c->buf[1],
@@ -1929,6 +2113,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (cudaEvent_t e : c->evp) cudaEventDestroy(e);
+  for (auto& e : c->tev) cudaEventDestroy(e.first);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
   return CPQR_OK;
@@ -2147,6 +2332,7 @@ CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
       }
       if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
       if (c->opt.profile) prof_accumulate(c);
+      trace_dump(c);
       c->launches_per_sweep = c->launch_count - before;
     }
     CK(cudaMemcpyAsync(c->dfits + s, c->dfit, sizeof(double), cudaMemcpyDeviceToDevice, c->st));

@@ -648,13 +648,14 @@ def test_batched_stopping_rule_and_paper_shape(cp):
         assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
 
 
-def test_profile_and_timings(cp):
+def test_profile_and_timings(cp, monkeypatch):
     """opt.profile = 1 (the paper's per-phase time breakdown): eager sweeps with
     events around each phase.  cpqr_get_timings returns the same seven per-phase ms as
     cpqr_get_profile; the stream-X pass is timed, the algorithmic bytes equal N passes over X, and
     the fits equal those of the graph path bitwise (profiling changes launch order only)."""
     dims, R = (40, 36, 30), 6
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=13, eta=0.05)
+    monkeypatch.setenv("CPQR_OVERLAP", "0")  # profiling runs the serial schedule (same plans)
     fits = []
     for prof in (True, False):
         s = cp.CPQR(dims, R, "QR", profile=prof, use_graph=not prof)
@@ -669,7 +670,7 @@ def test_profile_and_timings(cp):
             assert t[2] > 0.0  # the fused factor-QR tail is timed (it was never written in round 1)
             assert p["bytes0"] == len(dims) * 8.0 * np.prod(dims)
             # launches per phase add up to the launches of the profiled sweeps
-            assert sum(p["launches"]) > 0 and p["launches"][2] >= 3
+            assert sum(p["launches"]) > 0 and p["launches"][2] >= 1
             assert s.timings() == [0.0] * 7  # reset by profile(reset=True)
         s.close()
     assert np.array_equal(fits[0], fits[1])
@@ -907,3 +908,36 @@ def test_streamk_strided_split(cp, dims, R, world, mode, monkeypatch):
     for k in range(N):
         assert rel(A[k], ref["factors"][k]) <= 1e-9
     s.close()
+
+
+@pytest.mark.parametrize("mode", ["1", "0"])
+@pytest.mark.parametrize("dims,R,variant", [((70, 66, 34), 10, "QR"), ((37, 29, 43), 7, "SVD"), ((300, 260, 64), 32, "QR"),
+                                            ((24, 20, 18, 22), 8, "QR"), ((9, 8, 7, 6, 8), 4, "SVD"),
+                                            ((520, 40, 30), 6, "QR")])
+def test_overlap_schedule(cp, dims, R, variant, mode, monkeypatch):
+    """The overlap schedule (CPQR_OVERLAP=1: the tail of mode n on a second stream beside the
+    stream-X pass of mode n+1 when that pass does not contract mode n; N = 3 passes contract mode
+    (n+1) mod 3; the tail as one CTA for I_n <= 512) and the serial schedule (0) both match the
+    oracle -- factors <= 1e-9 after one sweep, fits <= 1e-8 -- and are run-to-run bitwise
+    reproducible (graph replays)."""
+    monkeypatch.setenv("CPQR_OVERLAP", mode)
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=500 + R + len(dims))
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    runs = []
+    for _ in range(2):
+        s = cp.CPQR(dims, R, variant)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        f1 = s.sweep(1)
+        lam, A = s.get_factors()
+        f = np.concatenate([f1, s.sweep(3)])
+        runs.append((f, A))
+        s.close()
+    ref1 = O.cp_als_qr(X, init, 1, variant=variant)
+    ref = O.cp_als_qr(X, init, 4, variant=variant)
+    f, A = runs[0]
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    assert np.array_equal(runs[0][0], runs[1][0])
