@@ -19,6 +19,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -149,6 +150,7 @@ struct cpqr_ctx {
   // slower in every config (interleaved A/B, 30 sweeps x 2: C2 -3 %, C3 -1 %, C5 -1 %; with early
   // launch_dependents triggers in the persistent stream kernels C2 -7 %, C3 tree -9 %)
   bool pdl = false;
+  bool q0_stair = false;     // staircase Q0 apply (CPQR_Q0_STAIR=1, k_q0_apply_tc<NT, true>)
   // overlap schedule: the tail of mode n (Q0 apply, solve, factor QR) runs on stream
   // tl beside the stream-X pass of mode n+1 whenever that pass does not contract mode n
   bool overlap = false, tail_single = false;
@@ -363,17 +365,89 @@ struct PlanIn {
   double* ybuf = nullptr;   // overlap schedule: the final step writes Y here
 };
 
-// cudaMalloc; with CPQR_POISON=1 (debugging) the block is filled with 0xFF bytes (NaN as fp64), so
-// a kernel reading device memory before it was written shows up as NaN in the parity tests.
+// Device allocations.  Debugging switches (compute-sanitizer is unavailable on this pool):
+//  * CPQR_POISON=1 fills every block with 0xFF bytes (NaN as fp64): a kernel reading memory before
+//    it was written shows up as NaN in the parity tests (initcheck's job);
+//  * CPQR_CANARY=1 surrounds every block with 4 KB guard bands of a byte pattern, and every
+//    cpqr_sweep / cpqr_destroy verifies all of them: a kernel writing out of bounds (before or past
+//    its buffer) fails the call with ECUDA and names the allocation (memcheck's job for writes).
+constexpr size_t kGuard = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+struct Guarded {
+  char* base;
+  size_t bytes;
+};
+std::vector<Guarded>& guard_registry() {
+  static std::vector<Guarded> g;
+  return g;
+}
+std::mutex& guard_mutex() {
+  static std::mutex m;
+  return m;
+}
+bool canary_on() {
+  static const bool on = getenv("CPQR_CANARY") && atoi(getenv("CPQR_CANARY")) == 1;
+  return on;
+}
+
 template <typename T>
 cudaError_t dmalloc(T** p, size_t bytes) {
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  cudaError_t e;
+  if (canary_on()) {
+    char* base = nullptr;
+    e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuard);
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(base, kGuardByte, bytes + 2 * kGuard);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(guard_mutex());
+    guard_registry().push_back({base, bytes});
+    *p = reinterpret_cast<T*>(base + kGuard);
+  } else {
+    e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  }
   static const bool poison = getenv("CPQR_POISON") != nullptr;
   if (e == cudaSuccess && poison) {
     e = cudaMemset(*p, 0xff, bytes);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
   }
   return e;
+}
+
+// cudaFree for blocks from dmalloc (the guarded base under CPQR_CANARY)
+void dfree(void* p) {
+  if (!p) return;
+  if (canary_on()) {
+    std::lock_guard<std::mutex> lk(guard_mutex());
+    auto& g = guard_registry();
+    for (size_t i = 0; i < g.size(); ++i)
+      if (g[i].base + kGuard == p) {
+        cudaFree(g[i].base);
+        g.erase(g.begin() + i);
+        return;
+      }
+  }
+  cudaFree(p);
+}
+
+// CPQR_CANARY: the number of guard bytes changed in all live blocks (0 = clean); *which = the first
+// offending block's size for the error message
+size_t canary_violations(size_t* which) {
+  if (!canary_on()) return 0;
+  cudaDeviceSynchronize();
+  size_t bad = 0;
+  std::vector<unsigned char> h(kGuard);
+  std::lock_guard<std::mutex> lk(guard_mutex());
+  for (const Guarded& g : guard_registry()) {
+    for (int side = 0; side < 2; ++side) {
+      const char* src = side ? g.base + kGuard + g.bytes : g.base;
+      if (cudaMemcpy(h.data(), src, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return (size_t)-1;
+      size_t nb = 0;
+      for (unsigned char b : h) nb += (b != kGuardByte);
+      if (nb && !bad && which) *which = g.bytes;
+      bad += nb;
+    }
+  }
+  return bad;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -971,7 +1045,7 @@ cpqr_status build_plans(cpqr_ctx* c) {
       ye = std::max(ye, e);
     }
     if (ye > c->dY_elems) {
-      if (c->dY) cudaFree(c->dY);
+      if (c->dY) dfree(c->dY);
       c->dY = nullptr;
       if (dmalloc(&c->dY, ye * sizeof(double)) != cudaSuccess) return fail(c, CPQR_ENOMEM, "Y buffer");
       c->dY_elems = ye;
@@ -980,7 +1054,7 @@ cpqr_status build_plans(cpqr_ctx* c) {
   // the ping-pong intermediates and slice partials are shared by the slabs (run in turn on one
   // stream); each slab keeps its own dimension-tree buffer (it lives across modes)
   if (mb > c->buf_elems) {
-    for (int i = 0; i < 2; ++i) { if (c->buf[i]) cudaFree(c->buf[i]); c->buf[i] = nullptr; }
+    for (int i = 0; i < 2; ++i) { if (c->buf[i]) dfree(c->buf[i]); c->buf[i] = nullptr; }
     for (int i = 0; i < 2; ++i)
       if (dmalloc(&c->buf[i], mb * sizeof(double)) != cudaSuccess)
         return fail(c, CPQR_ENOMEM, "intermediate buffers (%zu doubles)", mb);
@@ -989,7 +1063,7 @@ cpqr_status build_plans(cpqr_ctx* c) {
   for (int q = 0; q < c->nslab; ++q) {
     Slab& sl = c->slabs[q];
     if (mt > sl.tree_alloc) {
-      if (sl.dTree) cudaFree(sl.dTree);
+      if (sl.dTree) dfree(sl.dTree);
       sl.dTree = nullptr;
       if (dmalloc(&sl.dTree, mt * sizeof(double)) != cudaSuccess)
         return fail(c, CPQR_ENOMEM, "dimension-tree buffer (%zu doubles)", mt);
@@ -997,7 +1071,7 @@ cpqr_status build_plans(cpqr_ctx* c) {
     }
   }
   if (mp > c->part_elems) {
-    if (c->dPart) cudaFree(c->dPart);
+    if (c->dPart) dfree(c->dPart);
     c->dPart = nullptr;
     if (dmalloc(&c->dPart, mp * sizeof(double)) != cudaSuccess)
       return fail(c, CPQR_ENOMEM, "slice partials (%zu doubles)", mp);
@@ -1356,8 +1430,12 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
   KS = (KT + kpc - 1) / kpc;
   dim3 grid(iblocks, (unsigned)KS);
   const int NT = (c->R + 7) / 8;
-#define Q0A(NTV) launch_ex(k_q0_apply_tc<NTV>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb, (const double*)c->dQ0, c->R, \
-                           kpc, (int)KS, c->dWp, c->dq0cnt, Wout)
+#define Q0A(NTV)                                                                                                 \
+  (c->q0_stair ? launch_ex(k_q0_apply_tc<NTV, true>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb,           \
+                           (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)c->dperm,  \
+                           c->N - 1)                                                                                 \
+               : launch_ex(k_q0_apply_tc<NTV, false>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb,          \
+                           (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)nullptr, 0))
   switch (NT) { case 1: Q0A(1); break; case 2: Q0A(2); break; case 3: Q0A(3); break; default: Q0A(4); break; }
 #undef Q0A
   CKL();
@@ -1785,7 +1863,7 @@ void prof_accumulate(cpqr_ctx* c) {
 
 cpqr_status ensure_fits(cpqr_ctx* c, int n) {
   if (n <= c->fits_cap) return CPQR_OK;
-  if (c->dfits) cudaFree(c->dfits);
+  if (c->dfits) dfree(c->dfits);
   c->dfits = nullptr;
   if (dmalloc(&c->dfits, sizeof(double) * n) != cudaSuccess) return fail(c, CPQR_ENOMEM, "fits");
   c->fits_cap = n;
@@ -1910,6 +1988,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->use_tma = getenv("CPQR_NO_TMA") == nullptr;
   c->streamk = getenv("CPQR_STREAMK") ? atoi(getenv("CPQR_STREAMK")) : -1;
   c->pdl = getenv("CPQR_PDL") && atoi(getenv("CPQR_PDL")) == 1;
+  c->q0_stair = getenv("CPQR_Q0_STAIR") && atoi(getenv("CPQR_Q0_STAIR")) == 1;
   c->trace = getenv("CPQR_TRACE") && atoi(getenv("CPQR_TRACE")) == 1 && !c->opt.use_graph;
   c->tree = c->opt.mttm_tree != 0 && N >= 3 && !ne_family(c->variant);
   c->tree_h = (N + 1) / 2;
@@ -2076,11 +2155,16 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (!c) return CPQR_OK;
   cudaSetDevice(c->opt.device);
   if (c->st) cudaStreamSynchronize(c->st);
+  {
+    size_t which = 0;
+    if (const size_t bad = canary_violations(&which))
+      fprintf(stderr, "cpqr_destroy: CPQR_CANARY: %zu guard bytes overwritten (first: block of %zu bytes)\n", bad, which);
+  }
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->comm) ncclCommDestroy(c->comm);
   for (int k = 0; k < kMaxN; ++k) {
-    cudaFree(c->dA[k]); cudaFree(c->dQ[k]); cudaFree(c->dRk[k]); cudaFree(c->dG[k]);
-    cudaFree(c->dQt[k]); cudaFree(c->dAt[k]);
+    dfree(c->dA[k]); dfree(c->dQ[k]); dfree(c->dRk[k]); dfree(c->dG[k]);
+    dfree(c->dQt[k]); dfree(c->dAt[k]);
   }
   if (c->side) cudaStreamDestroy(c->side);
   if (c->tl) cudaStreamDestroy(c->tl);
@@ -2089,25 +2173,25 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
     if (c->evQ[k]) cudaEventDestroy(c->evQ[k]);
     if (c->evK[k]) cudaEventDestroy(c->evK[k]);
   }
-  if (c->dY) cudaFree(c->dY);
+  if (c->dY) dfree(c->dY);
   if (c->evf) cudaEventDestroy(c->evf);
   if (c->evj) cudaEventDestroy(c->evj);
   double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dSk, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred,
                   c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2};
-  for (double* p : ps) if (p) cudaFree(p);
-  if (c->dperm) cudaFree(c->dperm);
-  if (c->dflags) cudaFree(c->dflags);
-  if (c->dq0cnt) cudaFree(c->dq0cnt);
-  for (int k = 0; k < kMaxN; ++k) if (c->dKtB[k]) cudaFree(c->dKtB[k]);
-  if (c->dKtLam) cudaFree(c->dKtLam);
-  if (c->dKtM) cudaFree(c->dKtM);
-  if (c->dKtC) cudaFree(c->dKtC);
+  for (double* p : ps) if (p) dfree(p);
+  if (c->dperm) dfree(c->dperm);
+  if (c->dflags) dfree(c->dflags);
+  if (c->dq0cnt) dfree(c->dq0cnt);
+  for (int k = 0; k < kMaxN; ++k) if (c->dKtB[k]) dfree(c->dKtB[k]);
+  if (c->dKtLam) dfree(c->dKtLam);
+  if (c->dKtM) dfree(c->dKtM);
+  if (c->dKtC) dfree(c->dKtC);
   for (int q = 0; q < kMaxWorld; ++q) {
     Slab& sl = c->slabs[q];
-    if (sl.Xown) cudaFree(sl.Xown);
-    if (sl.dTree) cudaFree(sl.dTree);
-    if (sl.dWloc) cudaFree(sl.dWloc);
+    if (sl.Xown) dfree(sl.Xown);
+    if (sl.dTree) dfree(sl.dTree);
+    if (sl.dWloc) dfree(sl.dWloc);
   }
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -2123,11 +2207,11 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
 static cpqr_status set_slab(cpqr_ctx* c, Slab& sl, const double* x, int mem, double* nx2_out) {
   const size_t bytes = sizeof(double) * sl.numel;
   if (mem == CPQR_MEM_DEVICE_BORROW) {
-    if (sl.Xown) { cudaFree(sl.Xown); sl.Xown = nullptr; sl.Xown_elems = 0; }
+    if (sl.Xown) { dfree(sl.Xown); sl.Xown = nullptr; sl.Xown_elems = 0; }
     sl.X = x;
   } else {
     if (sl.Xown_elems < (size_t)sl.numel) {
-      if (sl.Xown) cudaFree(sl.Xown);
+      if (sl.Xown) dfree(sl.Xown);
       sl.Xown = nullptr;
       if (dmalloc(&sl.Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
       sl.Xown_elems = sl.numel;
@@ -2216,10 +2300,10 @@ CPQR_API cpqr_status cpqr_set_ktensor(cpqr_ctx* c, int S, const double* lam, con
   TRY(begin_call(c));
   const int N = c->N, R = c->R;
   if (S != c->ktS) {
-    for (int k = 0; k < N; ++k) { if (c->dKtB[k]) cudaFree(c->dKtB[k]); c->dKtB[k] = nullptr; }
-    if (c->dKtLam) cudaFree(c->dKtLam);
-    if (c->dKtM) cudaFree(c->dKtM);
-    if (c->dKtC) cudaFree(c->dKtC);
+    for (int k = 0; k < N; ++k) { if (c->dKtB[k]) dfree(c->dKtB[k]); c->dKtB[k] = nullptr; }
+    if (c->dKtLam) dfree(c->dKtLam);
+    if (c->dKtM) dfree(c->dKtM);
+    if (c->dKtC) dfree(c->dKtC);
     c->dKtLam = c->dKtM = c->dKtC = nullptr;
     for (int k = 0; k < N; ++k) CK(dmalloc(&c->dKtB[k], sizeof(double) * c->dims[k] * S));
     CK(dmalloc(&c->dKtLam, sizeof(double) * S));
@@ -2348,6 +2432,9 @@ CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
     c->last_fit = hf[nsweeps - 1];
     if (fits) std::memcpy(fits, hf.data(), sizeof(double) * nsweeps);
     if (fl & FLAG_NONFINITE) return fail(c, CPQR_EDIVERGED, "non-finite factor");
+    size_t which = 0;
+    if (const size_t bad = canary_violations(&which))
+      return fail(c, CPQR_ECUDA, "CPQR_CANARY: %zu guard bytes overwritten (first: block of %zu bytes)", bad, which);
     return CPQR_OK;
   }
   return end_call(c);
@@ -2425,7 +2512,7 @@ struct DevScratch {
     return e;
   }
   ~DevScratch() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) dfree(p);
   }
 };
 

@@ -271,10 +271,18 @@ struct KrQrArgs {
 // Q0 (4 columns j per k-step); its 8 warps interleave those k-steps.  Warp partials are summed in
 // warp order; with KS > 1 slices, the last CTA of a row block to finish (threadfence + counter)
 // sums the slice partials in slice order.  One launch, bitwise reproducible.
-template <int NT>
+//
+// STAIR: Q0 has V_n's staircase support -- column c is
+// nonzero only on the rows of level max_m j_m <= c, (c + 1)^{N-1} of them -- so the k loop runs over
+// the rows in level order (perm, the packed-staircase order of K2) and N-tile n (columns 8n..8n+7)
+// stops after its (8n + 8)^{N-1} rows: ~1/N of the dense apply's flops and Q0 reads.  The skipped
+// products are exact zeros (both V_n QR paths preserve the support), so W is the same up to the
+// summation order.
+template <int NT, bool STAIR = false>
 __global__ void __launch_bounds__(256)
 k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, const double* __restrict__ Q0, int R,
-              int kpc, int KS, double* __restrict__ Wp, unsigned* __restrict__ counters, double* __restrict__ W) {
+              int kpc, int KS, double* __restrict__ Wp, unsigned* __restrict__ counters, double* __restrict__ W,
+              const int* __restrict__ perm = nullptr, int N1 = 0) {
   __shared__ double red[8][64 * NT];
   __shared__ int last;
   pdl_wait();
@@ -283,12 +291,22 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int i = ib * 8 + g;
   double acc[NT][2];
+  int64_t lim[NT];  // STAIR: rows (in level order) of N-tile n's staircase
 #pragma unroll
-  for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
-  const int64_t kb = (int64_t)ks * kpc, ke = min(KT, kb + kpc);
+  for (int n = 0; n < NT; ++n) {
+    acc[n][0] = acc[n][1] = 0.0;
+    lim[n] = J;
+    if (STAIR) {
+      int64_t v = 1;
+      for (int m = 0; m < N1; ++m) v *= (int64_t)min(8 * n + 8, R);
+      lim[n] = min(J, v);
+    }
+  }
+  const int64_t kb = (int64_t)ks * kpc, ke = min(STAIR ? (lim[NT - 1] + 3) / 4 : KT, kb + kpc);
 #pragma unroll 4
   for (int64_t kk = kb + warp; kk < ke; kk += 8) {
-    const int64_t j = 4 * kk + t;
+    const int64_t pos = 4 * kk + t;
+    const int64_t j = STAIR ? (pos < J ? (int64_t)__ldg(perm + pos) : J) : pos;
     double av = 0.0;
     if (i < In && j < J) {
       const int64_t bq = j / Aa, aa = j - bq * Aa;
@@ -296,6 +314,7 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
+      if (STAIR && 4 * kk >= lim[n]) continue;  // warp-uniform: the whole k-step is past the staircase
       const int c = 8 * n + g;
       const double bv = (j < J && c < R) ? __ldg(Q0 + j + J * c) : 0.0;
       dmma(acc[n][0], acc[n][1], av, bv);
