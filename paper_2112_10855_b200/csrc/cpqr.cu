@@ -181,8 +181,15 @@ struct cpqr_ctx {
   unsigned* dflags = nullptr;
   double* hpin = nullptr;  // pinned: [0] fit, [1] flags
   bool plans_valid = false;
-  cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t gexec = nullptr;   // one sweep
+  cudaGraphExec_t gexecG = nullptr;  // gsw sweeps in one graph (the tails overlap across sweeps)
+  // sweeps per multi-sweep graph (CPQR_GRAPH_SWEEPS).  Default 1: measured slower with more
+  // (interleaved, 40 sweeps x 2: C2 2537 / 2450 / 2285 sweeps/s at 1 / 2 / 4, C4 480 / 466 / 454)
+  int gsw = 1;
+  int64_t launches_G = 0;
   bool graph_valid = false;
+  unsigned* dfitc = nullptr;         // device counter: next slot of dfits (k_store_fit)
+  bool ov_first = true, ov_join = true;  // overlap schedule: first / last sweep of a capture
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // profiling (opt.profile): events recorded at phase boundaries; the time since the previous
   // mark is attributed to the mark's phase (cpqr_get_profile ms[0..6])
@@ -1535,8 +1542,10 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
   const int In = (int)c->dims[n];
   const int prev = (n + N - 1) % N;
   const Plan& p = c->slabs[0].plans[n];
-  // V_n QR (+ SVD of R0) on the side stream once R_{n-1} is final
-  if (n == 0) {
+  // V_n QR (+ SVD of R0) on the side stream once R_{n-1} is final.  The first mode of the first
+  // sweep of a capture has no tail before it in the graph (the previous launch completed).
+  const bool inflight = !(n == 0 && c->ov_first);  // a tail of mode prev is in this capture
+  if (!inflight) {
     CK(cudaEventRecord(c->evf, c->st));
     CK(cudaStreamWaitEvent(c->side, c->evf, 0));
   } else {
@@ -1562,7 +1571,7 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
     if (pass && ((p.steps[i].modes >> prev) & 1u)) dep = true;
     if (pass && p.steps[i].out == c->dY) dep = true;
   }
-  if (n > 0 && dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
+  if (inflight && dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
   trace_mark(c, c->st, dep ? "pass start (after tail n-1)" : "pass start", n);
   Plan first, rest;
   size_t nf = nx;
@@ -1571,7 +1580,7 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
   rest.steps.assign(p.steps.begin() + nf, p.steps.end());
   TRY(run_plan(c, first));
   trace_mark(c, c->st, "pass end", n);
-  if (n > 0 && !dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
+  if (inflight && !dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
   trace_mark(c, c->st, "rest start", n);
   TRY(run_plan(c, rest));
   trace_mark(c, c->st, "rest end", n);
@@ -1596,8 +1605,14 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
   trace_mark(c, c->tl, "tail end", n);
   c->pinv_ready = false;
   TRY(st);
+  if (n == N - 1 && c->opt.fit_mode == CPQR_FIT_FAST) {  // the sweep's fit (computed by this tail)
+    k_store_fit<<<1, 32, 0, c->tl>>>(c->dfit, c->dfits, c->dfitc, c->fits_cap);
+    CKL();
+  }
   CK(cudaEventRecord(c->evQ[n], c->tl));
-  if (n == N - 1) CK(cudaStreamWaitEvent(c->st, c->evQ[n], 0));  // join: factors and fit complete
+  // join at the end of the capture (or every sweep with the DIRECT fit, which reads all factors)
+  if (n == N - 1 && (c->ov_join || c->opt.fit_mode == CPQR_FIT_DIRECT))
+    CK(cudaStreamWaitEvent(c->st, c->evQ[n], 0));
   return CPQR_OK;
 }
 
@@ -1841,12 +1856,6 @@ cpqr_status direct_fit(cpqr_ctx* c) {
   return CPQR_OK;
 }
 
-cpqr_status one_sweep(cpqr_ctx* c) {
-  for (int n = 0; n < c->N; ++n) TRY(mode_update(c, n, n == c->N - 1));
-  if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
-  return CPQR_OK;
-}
-
 // fold the recorded phase marks into c->prof (after they completed)
 void prof_accumulate(cpqr_ctx* c) {
   if (c->nmarks > 0) cudaEventSynchronize(c->evp[c->nmarks - 1]);
@@ -1861,12 +1870,57 @@ void prof_accumulate(cpqr_ctx* c) {
   c->nmarks = 0;
 }
 
+// One sweep of mode updates, then the fit into the next dfits slot (k_store_fit; in the overlap
+// schedule with the fast fit the last tail stores it on its own stream).
+cpqr_status one_sweep(cpqr_ctx* c) {
+  const bool ov = c->overlap && !c->kt && !c->opt.profile;
+  for (int n = 0; n < c->N; ++n) {
+    TRY(mode_update(c, n, n == c->N - 1));
+    if (c->opt.profile) prof_accumulate(c);
+  }
+  if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
+  if (!ov || c->opt.fit_mode == CPQR_FIT_DIRECT) {
+    k_store_fit<<<1, 32, 0, c->st>>>(c->dfit, c->dfits, c->dfitc, c->fits_cap);
+    CKL();
+  }
+  if (c->opt.profile) prof_accumulate(c);
+  return CPQR_OK;
+}
+
+// capture `ns` sweeps into a graph; the overlap schedule's tails cross the sweep boundaries inside
+cpqr_status capture_sweeps(cpqr_ctx* c, int ns, cudaGraphExec_t* out, int64_t* launches) {
+  const int64_t before = c->launch_count;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  cpqr_status st = CPQR_OK;
+  for (int s = 0; s < ns && st == CPQR_OK; ++s) {
+    c->ov_first = (s == 0);
+    c->ov_join = (s == ns - 1);
+    st = one_sweep(c);
+  }
+  c->ov_first = c->ov_join = true;
+  cudaError_t ce = cudaStreamEndCapture(c->st, &g);
+  if (st != CPQR_OK) {
+    if (ce == cudaSuccess) cudaGraphDestroy(g);
+    return st;
+  }
+  CK(ce);
+  if (*out) cudaGraphExecDestroy(*out);
+  *out = nullptr;
+  CK(cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  *launches = c->launch_count - before;
+  return CPQR_OK;
+}
+
+
 cpqr_status ensure_fits(cpqr_ctx* c, int n) {
   if (n <= c->fits_cap) return CPQR_OK;
   if (c->dfits) dfree(c->dfits);
   c->dfits = nullptr;
   if (dmalloc(&c->dfits, sizeof(double) * n) != cudaSuccess) return fail(c, CPQR_ENOMEM, "fits");
   c->fits_cap = n;
+  c->graph_valid = false;  // the captured k_store_fit launches hold the old buffer and capacity
   return CPQR_OK;
 }
 
@@ -1989,6 +2043,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   c->streamk = getenv("CPQR_STREAMK") ? atoi(getenv("CPQR_STREAMK")) : -1;
   c->pdl = getenv("CPQR_PDL") && atoi(getenv("CPQR_PDL")) == 1;
   c->q0_stair = getenv("CPQR_Q0_STAIR") && atoi(getenv("CPQR_Q0_STAIR")) == 1;
+  c->gsw = getenv("CPQR_GRAPH_SWEEPS") ? std::max(1, atoi(getenv("CPQR_GRAPH_SWEEPS"))) : 1;
   c->trace = getenv("CPQR_TRACE") && atoi(getenv("CPQR_TRACE")) == 1 && !c->opt.use_graph;
   c->tree = c->opt.mttm_tree != 0 && N >= 3 && !ne_family(c->variant);
   c->tree_h = (N + 1) / 2;
@@ -2058,6 +2113,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   if (c->opt.world > 1)
     for (int q = 0; q < c->nslab; ++q) CK(dmalloc(&c->slabs[q].dWloc, sizeof(double) * imax * R));
   CK(dmalloc(&c->dnX2p, sizeof(double) * 64));
+  CK(dmalloc(&c->dfitc, sizeof(unsigned) * 4));
   CK(dmalloc(&c->dSk, sizeof(double) * 2 * (2 * c->sms) * 256 * R));
   CK(dmalloc(&c->dAhat, sizeof(double) * imax * R));
   CK(dmalloc(&c->dRstack, sizeof(double) * 8 * R * R));
@@ -2161,6 +2217,8 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
       fprintf(stderr, "cpqr_destroy: CPQR_CANARY: %zu guard bytes overwritten (first: block of %zu bytes)\n", bad, which);
   }
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->gexecG) cudaGraphExecDestroy(c->gexecG);
+  if (c->dfitc) dfree(c->dfitc);
   if (c->comm) ncclCommDestroy(c->comm);
   for (int k = 0; k < kMaxN; ++k) {
     dfree(c->dA[k]); dfree(c->dQ[k]); dfree(c->dRk[k]); dfree(c->dG[k]);
@@ -2387,39 +2445,41 @@ CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
   TRY(begin_call(c));
   TRY(ensure_fits(c, std::max(1, nsweeps)));
   const bool graph = c->opt.use_graph && !c->opt.profile;
-  for (int s = 0; s < nsweeps; ++s) {
+  CK(cudaMemsetAsync(c->dfitc, 0, sizeof(unsigned), c->st));
+  for (int s = 0; s < nsweeps;) {
     if (graph) {
       if (!c->graph_valid) {
-        const int64_t before = c->launch_count;
-        cudaGraph_t g;
-        CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-        cpqr_status st = one_sweep(c);
-        cudaError_t ce = cudaStreamEndCapture(c->st, &g);
-        if (st != CPQR_OK) { if (ce == cudaSuccess) cudaGraphDestroy(g); return st; }
-        CK(ce);
-        if (c->gexec) cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
-        CK(cudaGraphInstantiate(&c->gexec, g, 0));
-        cudaGraphDestroy(g);
+        TRY(capture_sweeps(c, 1, &c->gexec, &c->launches_per_sweep));
+        if (c->gsw > 1) TRY(capture_sweeps(c, c->gsw, &c->gexecG, &c->launches_G));
         c->graph_valid = true;
-        c->launches_per_sweep = c->launch_count - before;
       }
-      CK(cudaGraphLaunch(c->gexec, c->st));
-      c->launch_count += c->launches_per_sweep;
+      if (c->gsw > 1 && nsweeps - s >= c->gsw) {
+        CK(cudaGraphLaunch(c->gexecG, c->st));
+        c->launch_count += c->launches_G;
+        s += c->gsw;
+      } else {
+        CK(cudaGraphLaunch(c->gexec, c->st));
+        c->launch_count += c->launches_per_sweep;
+        ++s;
+      }
     } else {
       const int64_t before = c->launch_count;
       static const bool sync_modes = getenv("CPQR_SYNC_MODES") != nullptr;  // debugging
-      for (int n = 0; n < c->N; ++n) {
-        TRY(mode_update(c, n, n == c->N - 1));
-        if (sync_modes) CK(cudaDeviceSynchronize());
-        if (c->opt.profile) prof_accumulate(c);
+      if (sync_modes) {
+        for (int n = 0; n < c->N; ++n) {
+          TRY(mode_update(c, n, n == c->N - 1));
+          CK(cudaDeviceSynchronize());
+        }
+        if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
+        k_store_fit<<<1, 32, 0, c->st>>>(c->dfit, c->dfits, c->dfitc, c->fits_cap);
+        CKL();
+      } else {
+        TRY(one_sweep(c));
       }
-      if (c->opt.fit_mode == CPQR_FIT_DIRECT) TRY(direct_fit(c));
-      if (c->opt.profile) prof_accumulate(c);
       trace_dump(c);
       c->launches_per_sweep = c->launch_count - before;
+      ++s;
     }
-    CK(cudaMemcpyAsync(c->dfits + s, c->dfit, sizeof(double), cudaMemcpyDeviceToDevice, c->st));
   }
   if (nsweeps > 0) {
     std::vector<double> hf(nsweeps);

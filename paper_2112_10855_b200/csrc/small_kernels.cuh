@@ -56,6 +56,16 @@ __global__ void k_sum_ranks(RankPtrs a, int nr, int64_t n, double* out) {
   }
 }
 
+// The sweep's fit into the next slot of the per-call fits array (a device counter, reset by each
+// cpqr_sweep), so one captured graph can hold several sweeps.
+__global__ void k_store_fit(const double* __restrict__ fit, double* __restrict__ fits, unsigned* counter, int cap) {
+  if (threadIdx.x == 0) {
+    const unsigned i = *counter;
+    if ((int)i < cap) fits[i] = *fit;
+    *counter = i + 1;
+  }
+}
+
 __global__ void k_sum_final(const double* __restrict__ part, int np, double* __restrict__ out) {
   __shared__ double red[32];
   double s = 0.0;

@@ -976,3 +976,29 @@ def test_staircase_q0_apply(cp, dims, R, monkeypatch):
     f_dn = d.sweep(2)
     d.close()
     assert np.max(np.abs(f_st - f_dn)) <= 1e-10
+
+
+@pytest.mark.parametrize("overlap", ["1", "0"])
+@pytest.mark.parametrize("dims,R,variant,fit_mode", [((70, 66, 34), 10, "QR", "fast"), ((24, 20, 18, 22), 8, "SVD", "fast"),
+                                                     ((30, 38, 48), 5, "QR", "direct")])
+def test_multi_sweep_graph(cp, dims, R, variant, fit_mode, overlap, monkeypatch):
+    """CPQR_GRAPH_SWEEPS=3: several sweeps captured in one CUDA graph (the overlap schedule's tails
+    cross the sweep boundaries inside it; each sweep's fit goes to its slot through a device
+    counter).  Bitwise the same fits and factors as one graph per sweep, for call lengths that mix
+    3-sweep and 1-sweep graphs and grow the fits buffer (re-capture)."""
+    monkeypatch.setenv("CPQR_OVERLAP", overlap)
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=600 + R)
+    out = {}
+    for gs in ("1", "3"):
+        monkeypatch.setenv("CPQR_GRAPH_SWEEPS", gs)
+        s = cp.CPQR(dims, R, variant, fit_mode=fit_mode)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        f = np.concatenate([s.sweep(2), s.sweep(7), s.sweep(4)])
+        lam, A = s.get_factors()
+        out[gs] = (f, A)
+        s.close()
+    assert np.array_equal(out["1"][0], out["3"][0])
+    assert all(np.array_equal(a, b) for a, b in zip(out["1"][1], out["3"][1]))
+    ref = O.cp_als_qr(O.as_tensor(Xc), init, 13, variant=variant, fit_mode=fit_mode)
+    assert np.max(np.abs(out["3"][0] - np.array(ref["fits"]))) <= 1e-8
