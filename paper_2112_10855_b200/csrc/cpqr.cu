@@ -10,6 +10,7 @@
 #include "ttm_kernels.cuh"
 #include "ktensor_kernels.cuh"
 #include "batched_kernels.cuh"
+#include "small_ttm.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -36,7 +37,8 @@ constexpr size_t kQSmemMax = 96 * 1024;   // Q panel budget per CTA (2 CTAs / SM
 constexpr int64_t kQ0MaxSlices = 64;      // k-step slices of k_q0_apply_tc (partials buffer)
 
 struct TtmStep {
-  int kind;  // 0 strided, 1 fiber, 2 slice, 3 slice-reduce, 4 strided TMA, 5 fiber TMA, 6 slice TMA, 7 slice fix-up
+  int kind;  // 0 strided, 1 fiber, 2 slice, 3 slice-reduce, 4 strided TMA, 5 fiber TMA, 6 slice TMA, 7 slice fix-up,
+            // 8 small slice TMA, 9 small (L2-resident) TTM
   alignas(64) CUtensorMap mx;
   alignas(64) CUtensorMap mq;
   int S = 0, nslots = 1, nfb = 1;
@@ -55,6 +57,10 @@ struct TtmStep {
   unsigned modes = 0;  // contracted modes (bit k = mode k of the global tensor)
   int skm = -1;        // strided TMA: stream-K split -1 auto (ragged waves), 0 off, 1 always
   int cw1 = 0;         // 1: one CTA per SM (8 consumer warps) so reserved SMs stay free (overlap)
+  unsigned* cnt = nullptr;  // strided TMA stream-K: per-CTA arrival counters of the fused fix-up
+  int wk = 1, kc = 1;       // k_ttm_small (kind 9): contraction split over WK warps x KC CTAs
+  const double* Qt = nullptr;  // k_ttm_small: the transposed zero-padded panel (I x rq row-major)
+  int rq = 0;
 };
 
 struct DiagStep {
@@ -145,6 +151,7 @@ struct cpqr_ctx {
          *dAhat = nullptr;
   double* dnX2p = nullptr;   // per-slab partial ||X||^2 (CPQR_COMM_LOCAL), summed in rank order
   double* dSk = nullptr;     // stream-K partial slots: 2 per CTA x (256-row unit x R)
+  unsigned* dSkCnt = nullptr;  // stream-K fused fix-up: arrival counter per CTA (self re-arming)
   int streamk = -1;          // CPQR_STREAMK: -1 auto, 0 off, 1 always (strided stream kernel)
   // programmatic dependent launch along the per-mode chain (CPQR_PDL=1).  Off by default: measured
   // slower in every config (interleaved A/B, 30 sweeps x 2: C2 -3 %, C3 -1 %, C5 -1 %; with early
@@ -366,6 +373,7 @@ struct PlanIn {
   bool tree_fresh = false;  // this mode computes its half's intermediate from X
   double* tbuf = nullptr;   // the tree buffer
   double* sk = nullptr;     // stream-K partial slots of the strided stream kernel
+  unsigned* skcnt = nullptr;  // their arrival counters (zeroed, self re-arming)
   int skm = -1;             // stream-K mode (CPQR_STREAMK)
   bool overlap = false;     // overlap schedule: N = 3 first contraction (n+1) mod 3
   bool ov_cw1 = true;       // overlap schedule: one CTA per SM in the stream passes (CPQR_OVERLAP_CW1)
@@ -514,6 +522,23 @@ int stages_for(size_t stage, size_t extra, const char* kind_env, int cap = 8) {
 // N-tiles of 8 fibres per consumer warp in the fused slice kernel (box height kCW * 8 * NF)
 static int slice_nf(int I2) { return I2 >= 256 ? 4 : 2; }
 
+// k_ttm_small (small_ttm.cuh) for a TTM on an intermediate of A I B <= kSmallTtmMax elements (the
+// stream pass's output: L2 resident): WK warps x KC CTAs split the contraction so that ~2 CTAs x
+// 8 warps per SM have work.  False when the CTA's Q rows exceed the shared-memory budget or the
+// row blocks exceed the arrival counters (then the TMA / register-staged kernels run).
+constexpr int64_t kSmallTtmMax = 8ll << 20;
+bool small_split(int64_t A, int I, int64_t B, int R, int sms, int& WK, int& KC, size_t& smem) {
+  const int64_t M = A * B, rt = (M + 15) / 16;
+  int64_t KT = ((int64_t)sms * 16 + rt - 1) / rt;
+  KT = std::max<int64_t>(1, std::min<int64_t>(KT, std::max(1, I / 16)));
+  WK = KT >= 8 ? 8 : KT >= 4 ? 4 : KT >= 2 ? 2 : 1;
+  KC = (int)((KT + WK - 1) / WK);
+  const int NT = (R + 7) / 8;
+  smem = (size_t)WK * 16 * (8 / WK) * (8 * NT + 1) * sizeof(double);  // the warp partials
+  const int64_t rcs = (M + 16 * (8 / WK) - 1) / (16 * (8 / WK));
+  return KC == 1 || rcs <= 2 * sms;
+}
+
 void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
   p.steps.clear();
   p.diags.clear();
@@ -569,10 +594,38 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         if (make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, k, s.I)) {
           s.kind = 4;
           s.P = in.sk;
+          s.cnt = in.skcnt;
           s.skm = in.skm;
           s.cw1 = (in.overlap && in.ov_cw1) ? 1 : 0;
           s.S = stages_for(16 * kBoxBytes + NQB * kBoxBytes, 0, "CPQR_ST_STRIDED", (s.I + kBK - 1) / kBK <= 3 ? 3 : 4);
         }
+      }
+    }
+    // an intermediate (not X) small enough to sit in L2: the latency-bound small-TTM kernel
+    const bool small_off = getenv("CPQR_TTM_SMALL") && atoi(getenv("CPQR_TTM_SMALL")) == 0;  // per plan build (tests)
+    {
+      const int64_t A = prod(cur, 0, k), B = prod(cur, k + 1, N);
+      const int I = (int)cur[k];
+      int wk, kc;
+      size_t smem;
+      // where the TMA kernels are starved: units of 32 CW rows (CW = 4 for R <= 12, else 8) or of
+      // 128 fibres fewer than half the SMs, or rows of A < 32 filling few of a unit's rows (C2's
+      // intermediates); on C3 / C4's the TMA kernels measured faster (A/B)
+      const int64_t ur = (k == 0) ? 128 : (R <= 12 ? 128 : 256);
+      const int64_t tunits = (k == 0) ? (B + ur - 1) / ur : ((A + ur - 1) / ur) * B;
+      const bool starved = tunits < in.sms / 2 || (k != 0 && A < 32);
+      const bool force = getenv("CPQR_TTM_SMALL") && atoi(getenv("CPQR_TTM_SMALL")) == 2;  // tests
+      if (!small_off && (starved || force) && src != in.X && A * I * B <= kSmallTtmMax && in.Qt[k] &&
+          small_split(A, I, B, R, in.sms, wk, kc, smem)) {
+        s.kind = 9;
+        s.A = A; s.I = I; s.B = B;
+        s.Qt = in.Qt[k];
+        s.rq = in.RQ;
+        s.wk = wk; s.kc = kc;
+        s.P = part;
+        s.cnt = in.skcnt;
+        s.S = (int)smem;
+        if (kc > 1) p.part = std::max(p.part, (size_t)((A * B + 16 * (8 / wk) - 1) / (16 * (8 / wk))) * kc * 16 * (8 / wk) * R);
       }
     }
     cur[k] = R;
@@ -860,14 +913,18 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
     const double waves = (double)units / grid;
     const bool sk = s.P && grid > 1 && units > grid && (s.skm == 1 || (s.skm != 0 && std::ceil(waves) / waves > 1.02));
     double* P = sk ? s.P : nullptr;
+    // the fix-up is fused into the kernel (last-arriving CTA per cut unit); CPQR_SK_FIXUP=1 keeps the
+    // separate k_strided_fixup launch (same sums, same order)
+    static const bool sep_fixup = getenv("CPQR_SK_FIXUP") && atoi(getenv("CPQR_SK_FIXUP")) == 1;
+    unsigned* skc = (sk && !sep_fixup) ? s.cnt : nullptr;
 #define STR(NTV, NPV)                                                                                  \
   {                                                                                                     \
     if (cw == 4) {                                                                                      \
       set_smem(k_strided_tma<NTV, NPV, 4>, smem);                                                       \
-      launch_ex(k_strided_tma<NTV, NPV, 4>, grid, (4 + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
+      launch_ex(k_strided_tma<NTV, NPV, 4>, grid, (4 + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P, skc); \
     } else {                                                                                            \
       set_smem(k_strided_tma<NTV, NPV>, smem);                                                          \
-      launch_ex(k_strided_tma<NTV, NPV>, grid, (kCW + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P); \
+      launch_ex(k_strided_tma<NTV, NPV>, grid, (kCW + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P, skc); \
     }                                                                                                   \
   }
     // producer warps issuing the 16 X boxes of a stage in parallel: a single issuing thread bounds
@@ -882,7 +939,7 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
       switch (NT) { case 1: STR(1, 1) break; case 2: STR(2, 1) break; case 3: STR(3, 1) break; default: STR(4, 1) break; }
     }
 #undef STR
-    if (sk) {
+    if (sk && !skc) {
       launch_ex(k_strided_fixup, grid - 1, 1024, 0, st, pdl, 1, (const double*)P, s.A, R, s.B, (s.I + kBK - 1) / kBK,
                 32 * cw, grid, s.out);
       return 2;
@@ -965,6 +1022,21 @@ cpqr_status run_plan(cpqr_ctx* c, const Plan& p) {
         k_reduce_slices<<<grid, 256, 0, c->st>>>(s.in, s.nseg, s.L, c->R * c->R, s.out);
         break;
       }
+      case 9: {
+        const int64_t rcs = (s.A * s.B + 16 * (8 / s.wk) - 1) / (16 * (8 / s.wk));
+        const dim3 grid((unsigned)(rcs * s.kc));
+        switch ((c->R + 7) / 8) {
+#define SML(NTV)                                                                                              \
+  case NTV:                                                                                                   \
+    set_smem(k_ttm_small<NTV>, s.S);                                                                          \
+    launch_ex(k_ttm_small<NTV>, grid, 256, s.S, c->st, c->pdl, 1, s.in, s.A, s.I, s.B, s.Qt, s.rq, c->R, s.out, \
+              s.wk, s.kc, s.P, s.cnt);                                                                        \
+    break;
+          SML(1) SML(2) SML(3) SML(4)
+#undef SML
+        }
+        break;
+      }
       default: c->launch_count += launch_tma(s, c->R, c->st, c->stream_sms, c->pdl) - 1; break;
     }
     CKL();
@@ -1005,6 +1077,7 @@ void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* 
   in.tree_fresh = (n == 0 || n == c->tree_h);
   in.tbuf = sl.dTree;
   in.sk = c->dSk;
+  in.skcnt = c->dSkCnt;
   in.skm = c->streamk;
   in.overlap = c->overlap;
   in.ov_cw1 = c->ov_cw1;
@@ -1272,7 +1345,16 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
       const int tl = 32 * ((mbr + 31) / 32), tr = 32 * ((nl * R + 31) / 32);
       static const bool rq_split_env = getenv("CPQR_RQ_SPLIT") && atoi(getenv("CPQR_RQ_SPLIT")) == 1;
       const bool rq_split = rq_split_env || c->tail_single;  // overlap: no cluster co-scheduling
-      if (!rq_split) {  // one cluster launch of the three phases (k_rq_fused)
+      static const bool rq_serial_off = getenv("CPQR_RQ_SERIAL") && atoi(getenv("CPQR_RQ_SERIAL")) == 0;
+      if (c->tail_single && !rq_split_env && !rq_serial_off) {  // one CTA, the phases in turn (k_rq_serial)
+        const int tb = std::max(tl, tr);
+        switch (RB) {
+          case 8: k_rq_serial<8><<<1, tb, 0, c->st>>>(q); break;
+          case 16: k_rq_serial<16><<<1, tb, 0, c->st>>>(q); break;
+          default: k_rq_serial<32><<<1, tb, 0, c->st>>>(q); break;
+        }
+        CKL();
+      } else if (!rq_split) {  // one cluster launch of the three phases (k_rq_fused)
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nl);
         cfg.blockDim = dim3(std::max(tl, tr));
@@ -2115,6 +2197,8 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(dmalloc(&c->dnX2p, sizeof(double) * 64));
   CK(dmalloc(&c->dfitc, sizeof(unsigned) * 4));
   CK(dmalloc(&c->dSk, sizeof(double) * 2 * (2 * c->sms) * 256 * R));
+  CK(dmalloc(&c->dSkCnt, sizeof(unsigned) * (2 * c->sms + 1)));
+  CK(cudaMemset(c->dSkCnt, 0, sizeof(unsigned) * (2 * c->sms + 1)));
   CK(dmalloc(&c->dAhat, sizeof(double) * imax * R));
   CK(dmalloc(&c->dRstack, sizeof(double) * 8 * R * R));
   CK(dmalloc(&c->dQtop, sizeof(double) * 8 * R * R));
@@ -2241,6 +2325,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->dperm) dfree(c->dperm);
   if (c->dflags) dfree(c->dflags);
   if (c->dq0cnt) dfree(c->dq0cnt);
+  if (c->dSkCnt) dfree(c->dSkCnt);
   for (int k = 0; k < kMaxN; ++k) if (c->dKtB[k]) dfree(c->dKtB[k]);
   if (c->dKtLam) dfree(c->dKtLam);
   if (c->dKtM) dfree(c->dKtM);
@@ -2681,7 +2766,7 @@ CPQR_API cpqr_status cpqr_debug_plan(cpqr_ctx* c, int n, int slab, int64_t* info
   for (const TtmStep& s : p.steps) {
     const int64_t xp = (s.in == sl.X) ? 1 : 0;
     switch (s.kind) {
-      case 0: case 4: put(s.kind, s.modes, s.A * s.I * s.B, s.A * R * s.B, 2 * s.A * s.I * s.B * R, xp); break;
+      case 0: case 4: case 9: put(s.kind, s.modes, s.A * s.I * s.B, s.A * R * s.B, 2 * s.A * s.I * s.B * R, xp); break;
       case 1: case 5: put(s.kind, s.modes, (int64_t)s.I * s.F, R * s.F, 2 * (int64_t)s.I * s.F * R, xp); break;
       case 2: case 6: case 8:
         put(s.kind, s.modes, (int64_t)s.I1 * s.I2 * s.L, R * R * s.L,

@@ -423,6 +423,24 @@ __global__ void __launch_bounds__(256) k_rq_qform(RqArgs a) {
   rq_qform_body<RB>(a, blockIdx.x);
 }
 
+// All three phases in one launch of ONE CTA (the leaves and the Q formations in turn): the overlap
+// schedule's tail runs beside the next stream pass, where a co-scheduled cluster is not available
+// and three gated launches cost ~8 us of the per-mode chain (C2) even when the fallback is not taken.
+template <int RB>
+__global__ void __launch_bounds__(256) k_rq_serial(RqArgs a) {
+  if (rq_skip(a)) return;
+  for (int b = 0; b < a.nleaf; ++b) {
+    rq_leaf_body<RB>(a, b);
+    __syncthreads();  // block-scope ordering of the leaf's global writes (Rstack, V, tau, partials)
+  }
+  rq_root_body<RB>(a);
+  __syncthreads();
+  for (int b = 0; b < a.nleaf; ++b) {
+    rq_qform_body<RB>(a, b);
+    __syncthreads();
+  }
+}
+
 // All three phases in one launch: a cluster of nleaf (<= 8) CTAs.  The cluster barrier orders the
 // leaves' global writes (Rstack, V, tau, partials) before the root reads them, and the root's
 // (Q_top, lambda) before the Q formation.  Gated like the three kernels: every CTA reads the same

@@ -163,18 +163,27 @@ __device__ __forceinline__ uint8_t* tma_carve(uint8_t* raw, int S, uint64_t*& fu
 // waves, 15 % idle), so P != nullptr selects a stream-K split: the W = units x KS k-steps are cut
 // into G equal contiguous ranges, one per CTA.  A unit covered by one CTA is stored to T; a unit
 // cut by a range boundary leaves each CTA's partial sum in a slot P[(2 c + h) * 32 CW * R] (h = 0:
-// the CTA's first unit, 1: its last), and k_strided_fixup adds the slots in CTA order (fixed order:
-// bitwise reproducible).
+// the CTA's first unit, 1: its last).  The last of the unit's CTAs to arrive (arrival counter
+// cnt[c0], c0 = the unit's first CTA; self re-arming) adds the slots in CTA order c0..c1 and stores
+// T: fixed order, so bitwise reproducible, and no fix-up launch (k_strided_fixup, kept for
+// CPQR_SK_FIXUP=1, computes the same sums in the same order).
 struct SkRange {  // the k-step range [it0, it1) of CTA c under the stream-K split
   int64_t it0, it1;
   __device__ __forceinline__ SkRange(int64_t W, int c, int G) : it0(W * c / G), it1(W * (c + 1) / G) {}
 };
+// the CTA whose stream-K range [W c / G, W (c+1) / G) holds k-step it: the largest c with
+// floor(W c / G) <= it, i.e. c = ceil((it + 1) G / W) - 1
+__device__ __forceinline__ int sk_cta_of(int64_t it, int64_t W, int G) {
+  return (int)(((it + 1) * G + W - 1) / W) - 1;
+}
 
 template <int NT, int NP = 1, int CW = kCW>
 __global__ void __launch_bounds__((CW + NP) * 32, CW == 4 ? 2 : 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
-              int I, int64_t B, int R, double* __restrict__ T, int S, double* __restrict__ P) {
+              int I, int64_t B, int R, double* __restrict__ T, int S, double* __restrict__ P,
+              unsigned* __restrict__ cnt) {
   extern __shared__ uint8_t smraw[];
+  __shared__ int sk_last;
   constexpr int NQB = (NT + 1) / 2;
   constexpr uint32_t XBYTES = 2 * CW * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
@@ -299,6 +308,26 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
           if (r0 < R) Pb[row + 32 * CW * r0] = acc[m][n][0];
           if (r0 + 1 < R) Pb[row + 32 * CW * (r0 + 1)] = acc[m][n][1];
         }
+      }
+      if (cnt == nullptr) return;  // CPQR_SK_FIXUP=1: k_strided_fixup sums the slots
+      // fused fix-up: the unit's CTAs c0..c1 each leave one slot; the last to arrive sums them
+      const int64_t W = units * KS;
+      const int c0 = sk_cta_of(u * KS, W, gridDim.x), c1 = sk_cta_of((u + 1) * KS - 1, W, gridDim.x);
+      __threadfence();
+      consumers_sync_n<CW * 32>();
+      if (threadIdx.x == 0) sk_last = (atomicAdd(&cnt[c0], 1u) == (unsigned)(c1 - c0)) ? 1 : 0;
+      consumers_sync_n<CW * 32>();
+      if (sk_last) {
+        __threadfence();
+        const int h0 = ((W * c0 / gridDim.x) / KS == u) ? 0 : 1;  // u is c0's first unit, or its last
+        constexpr int UR = 32 * CW;
+        for (int e = threadIdx.x; e < UR * R; e += CW * 32) {
+          const int row = e % UR, r = e / UR;
+          double v = __ldcg(P + ((int64_t)2 * c0 + h0) * UR * R + e);
+          for (int cc = c0 + 1; cc <= c1; ++cc) v += __ldcg(P + ((int64_t)2 * cc) * UR * R + e);
+          if (a0 + row < A) T[a0 + row + A * ((int64_t)r + (int64_t)R * b)] = v;
+        }
+        if (threadIdx.x == 0) cnt[c0] = 0u;  // re-armed for the next launch (graph replay)
       }
     }
   });

@@ -1002,3 +1002,63 @@ def test_multi_sweep_graph(cp, dims, R, variant, fit_mode, overlap, monkeypatch)
     assert all(np.array_equal(a, b) for a, b in zip(out["1"][1], out["3"][1]))
     ref = O.cp_als_qr(O.as_tensor(Xc), init, 13, variant=variant, fit_mode=fit_mode)
     assert np.max(np.abs(out["3"][0] - np.array(ref["fits"]))) <= 1e-8
+
+
+@pytest.mark.parametrize("small", ["2", "1", "0"])
+@pytest.mark.parametrize("dims,R", [((400, 40, 30), 10), ((12, 300, 250), 10), ((30, 40, 50), 5),
+                                    ((37, 29, 43), 7), ((24, 20, 18, 22), 16), ((9, 8, 7, 6, 8), 4),
+                                    ((70, 66, 34), 32), ((8, 500, 64), 3), ((33, 41, 27, 30), 24)])
+def test_small_ttm_kernel(cp, dims, R, small, monkeypatch):
+    """The remaining TTMs on L2-resident intermediates (k_ttm_small, plan kind 9: 16-row DMMA tiles,
+    the contraction split over warps and CTAs, warp partials summed in warp order and CTA partials by
+    the last-arriving CTA in CTA order) against the oracle's Multi-TTM: Y of every
+    mode <= 1e-11 (Frobenius) and max|dY| <= 1e-11 max|Y| (element-wise), with the kernel forced on
+    every intermediate (CPQR_TTM_SMALL=2), on where the TMA kernels are starved (1, default) and off
+    (0: the TMA / register-staged kernels).  Shapes cover A = 1 (fibre
+    contraction), A < 8 (rows spanning several b), ragged 16-row tiles, R = 3..32 (NT = 1..4), and
+    the cross-CTA split (KC > 1: few rows, long contraction, e.g. 120 rows x I = 250)."""
+    monkeypatch.setenv("CPQR_TTM_SMALL", small)
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=700 + R + len(dims))
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    N = len(dims)
+    Qs = [O.qr_pos(init[k])[0] for k in range(N)]
+    used = 0
+    for n in range(N):
+        used += sum(st["kind"] == "small-ttm" for st in s.debug_plan(n))
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+        assert np.max(np.abs(out["Y"] - Yo)) <= 1e-11 * np.max(np.abs(Yo)), n
+    if small == "2":
+        assert used > 0
+    if small == "0":
+        assert used == 0
+    f = s.sweep(2)
+    s.close()
+    ref = O.cp_als_qr(X, init, 2)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+
+
+@pytest.mark.parametrize("dims,R", [((70, 66, 34), 10), ((520, 40, 30), 6), ((24, 20, 18, 22), 8)])
+def test_overlap_schedule_householder_tail(cp, dims, R, monkeypatch):
+    """The overlap schedule with the Householder factor QR forced (CPQR_FACTOR_QR=householder): its
+    tail runs the whole TSQR (leaves, root, Q formation) in ONE CTA (k_rq_serial) beside the next
+    stream pass; factors <= 1e-9 after one sweep and fits <= 1e-8 against the oracle."""
+    monkeypatch.setenv("CPQR_OVERLAP", "1")
+    monkeypatch.setenv("CPQR_FACTOR_QR", "householder")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=900 + R)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    f = np.concatenate([f1, s.sweep(2)])
+    s.close()
+    ref1, ref = O.cp_als_qr(X, init, 1), O.cp_als_qr(X, init, 3)
+    for k in range(len(dims)):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, k
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8

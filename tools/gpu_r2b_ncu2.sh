@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -rf -x -k "small_ttm or householder_tail" 2>&1 | tail -4 > gpurun_out/n2_tests.log
+for c in 2 3 4; do
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/n2_launch_c$c.csv \
+    python tools/prof_case.py --config $c --sweeps 1 --graph 0 --profile 0 > gpurun_out/n2_ncu_c$c.log 2>&1
+done
