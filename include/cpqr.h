@@ -148,6 +148,16 @@ cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const double* X, 
                             int max_iters, double tol, double* A, double* lam, double* fits,
                             int* iters, void* stream);
 
+/* cpqr_batched_qr for any of the four solvers of the paper's accuracy study:
+ * variant = CPQR_NE (Alg. 1, Cholesky solve with an LU fallback), CPQR_QR, CPQR_SVD (QR-SVD,
+ * sigma_i kept iff sigma_i > tau sigma_max of R0) or CPQR_PINV (Alg. 1 with
+ * pinv(S_n), same tau rule); tau < 0 means R * eps.  NE / PINV use A0 of modes
+ * 2 and 3 (Alg. 1 line 3; A0[mode 1] unused, as for QR).  Same shapes, layouts, outputs and errors
+ * as cpqr_batched_qr (which is this call with CPQR_QR). */
+cpqr_status cpqr_batched(int P, const int64_t* dims, int R, int variant, double tau, const double* X,
+                         const double* A0, int max_iters, double tol, double* A, double* lam,
+                         double* fits, int* iters, void* stream);
+
 /* Kruskal-tensor input: X = [[lambda; B_1..B_N]] of rank S is never formed.
  * B[k] is a host pointer to the column-major I_k x S matrix B_k, lambda a host S-vector (NULL:
  * ones).  Each mode then computes W_n = B_n diag(lambda) [((.)_{k != n} Q_k^T B_k)^T Q0]

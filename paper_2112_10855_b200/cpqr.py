@@ -30,7 +30,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE"
 
 EXPORTS = [
     "cpqr_default_options", "cpqr_create", "cpqr_set_tensor", "cpqr_set_factors", "cpqr_init_factors",
-    "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile", "cpqr_get_timings",
+    "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_batched", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile", "cpqr_get_timings",
     "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_plan", "cpqr_debug_qr", "cpqr_debug_svd_solve",
     "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
 ]
@@ -57,6 +57,8 @@ _sig = {
     "cpqr_set_ktensor": (C.c_int32, [_P, C.c_int, _DP, C.POINTER(_DP)]),
     "cpqr_batched_qr": (C.c_int32, [C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                     C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cpqr_batched": (C.c_int32, [C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                                 C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cpqr_set_factors": (C.c_int32, [_P, C.POINTER(_DP), _DP]),
     "cpqr_init_factors": (C.c_int32, [_P, C.c_uint64]),
     "cpqr_sweep": (C.c_int32, [_P, C.c_int, _DP]),
@@ -104,8 +106,9 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(_DP)
 
 
-def batched_qr(X, A0, R, max_iters=500, tol=1e-15, stream=None):
-    """Batched CP-ALS-QR, one CTA per problem (cpqr_batched_qr).  X: CUDA float64 tensor
+def batched_qr(X, A0, R, max_iters=500, tol=1e-15, stream=None, variant="QR", tau=-1.0):
+    """Batched CP-ALS, one CTA per problem (cpqr_batched; variant "QR" is cpqr_batched_qr, also
+    "NE", "SVD", "PINV" with the truncation tau for SVD / PINV).  X: CUDA float64 tensor
     (P, I_3, I_2, I_1) C-contiguous (= P column-major tensors); A0: list of three CUDA float64
     tensors (P, R, I_k) C-contiguous (= column-major I_k x R per problem).  Returns (A, lam, fits,
     iters) as CUDA tensors: A a list of (P, R, I_k), lam (P, R), fits (P, max_iters), iters (P,)."""
@@ -120,12 +123,13 @@ def batched_qr(X, A0, R, max_iters=500, tol=1e-15, stream=None):
     iters = torch.empty((P,), dtype=torch.int32, device=dev)
     if stream is None:  # run in order with the torch work that produced X / A0 and reads the outputs
         stream = torch.cuda.current_stream(dev).cuda_stream
-    st = _lib.cpqr_batched_qr(P, dims, int(R), C.c_void_p(X.data_ptr()), C.c_void_p(A0cat.data_ptr()),
-                              int(max_iters), float(tol), C.c_void_p(Aout.data_ptr()), C.c_void_p(lam.data_ptr()),
-                              C.c_void_p(fits.data_ptr()), C.c_void_p(iters.data_ptr()),
-                              C.c_void_p(int(stream)) if stream else None)
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    st = _lib.cpqr_batched(P, dims, int(R), v, float(tau), C.c_void_p(X.data_ptr()), C.c_void_p(A0cat.data_ptr()),
+                           int(max_iters), float(tol), C.c_void_p(Aout.data_ptr()), C.c_void_p(lam.data_ptr()),
+                           C.c_void_p(fits.data_ptr()), C.c_void_p(iters.data_ptr()),
+                           C.c_void_p(int(stream)) if stream else None)
     if st:
-        raise CpqrError(st, "cpqr_batched_qr failed")
+        raise CpqrError(st, "cpqr_batched failed")
     out, o = [], 0
     for I in (I1, I2, I3):
         out.append(Aout[:, o:o + I * R].reshape(P, R, I))

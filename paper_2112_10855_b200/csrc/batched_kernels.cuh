@@ -1,6 +1,9 @@
-// Batched CP-ALS-QR for many small 3-way problems ("one CTA per problem"):
-// one CTA runs a whole solve -- Alg. 2 sweep after sweep with the stopping rule
-// of PAPER.md:532 (change in relative error below tol) -- with no host round trip.  Shapes:
+// Batched CP-ALS for many small 3-way problems ("one CTA per problem"):
+// one CTA runs a whole solve -- Alg. 2 (variants QR and QR-SVD)
+// or Alg. 1 (NE with the Cholesky solve, LU fallback, and CP-ALS-PINV,
+// PAPER.md:264-266) -- sweep after sweep with the stopping rule of PAPER.md:532 (change in relative
+// error below tol) and no host round trip: the four solvers of the collinear-factor study
+// (Table 4.1) on the same batch.  Shapes:
 // N = 3, I_k <= 64, R <= 8, I_1 I_2 R <= 16384 and I_2 I_3 R <= 16384 (e.g. the paper's 50^3,
 // rank-5 collinearity study).
 //
@@ -9,11 +12,17 @@
 //   with the Q_1 just updated; Q_3 is unchanged in between), U = X x_1 Q_1^T (R x I_2 x I_3)
 //   serves mode 3 (Y = U x_2 Q_2^T).
 // Each mode then: V_n = R_b (.) R_a (Kolda-Bader rows j = j_a + R j_b, a < b the other modes),
-// Householder QR of V_n (one warp), W = Y_(n) Q0, back substitution Ahat R0^T = W, lambda and
-// normalisation (zero column -> e_1), Householder QR of A_n (one warp), and after mode 3 the fast
-// fit.  QRs carry the sign fix diag(R) >= 0.  All reductions fixed-order.
+// Householder QR of V_n (one warp), W = Y_(n) Q0, back substitution Ahat R0^T = W (QR) or Ahat =
+// W U S^+ V^T from the one-sided Jacobi SVD of R0 (QR-SVD), lambda and normalisation (zero column
+// -> e_1), Householder QR of A_n (one warp), and after mode 3 the fast fit.
+// NE / PINV hold A_k and G_k = A_k^T A_k instead of Q_k, R_k: the same TTM chain with A_k gives
+// Y = X x_{k != n} A_k^T, whose Khatri-Rao diagonal Y(i, c + R c) is the MTTKRP M_n;
+// S_n = G_a (*) G_b; Ahat S_n = M_n by Cholesky (LU with partial pivoting on a non-positive pivot,
+// reading 18) or Ahat = M_n S_n^+ (PINV); normalise; G_n = A_n^T A_n; fit by PAPER.md:417-425.
+// QRs carry the sign fix diag(R) >= 0.  All reductions fixed-order.
 #pragma once
 #include "common.cuh"
+#include "small_kernels.cuh"  // jacobi_pinv
 
 namespace cpqr {
 
@@ -30,7 +39,48 @@ struct BatchedArgs {
   double* lam;          // out: P x R
   double* fits;         // out: P x max_iters (NaN after the last sweep run)
   int* iters;           // out: P (sweeps run)
+  int variant;          // 0 NE, 1 QR, 2 QR-SVD, 3 PINV (cpqr_variant)
+  double tau;           // SVD / PINV truncation (relative to sigma_max; < 0: R eps)
 };
+
+// Ahat S = M for the R x R symmetric S (R <= 8) by one thread: Cholesky, or LU with partial
+// pivoting when a pivot is not positive (the oracle's LAPACK gesv fallback).  Returns the factors
+// in F (ld 8) and the row permutation piv (identity for Cholesky); *chol = 1 for Cholesky.
+__device__ void bat_ne_factor(const double* S, int R, double* F, int* piv, int* chol) {
+  bool ok = true;
+  for (int e = 0; e < 64; ++e) F[e] = (e % 8 < R && e / 8 < R) ? S[(e % 8) + 8 * (e / 8)] : 0.0;
+  for (int j = 0; j < R && ok; ++j) {  // lower Cholesky in place: F = L
+    double d = F[j + 8 * j];
+    for (int k = 0; k < j; ++k) d -= F[j + 8 * k] * F[j + 8 * k];
+    if (!(d > 0.0)) { ok = false; break; }
+    const double l = sqrt(d);
+    F[j + 8 * j] = l;
+    for (int i = j + 1; i < R; ++i) {
+      double v = F[i + 8 * j];
+      for (int k = 0; k < j; ++k) v -= F[i + 8 * k] * F[j + 8 * k];
+      F[i + 8 * j] = v / l;
+    }
+  }
+  for (int i = 0; i < R; ++i) piv[i] = i;
+  *chol = ok ? 1 : 0;
+  if (ok) return;
+  for (int e = 0; e < 64; ++e) F[e] = (e % 8 < R && e / 8 < R) ? S[(e % 8) + 8 * (e / 8)] : 0.0;
+  for (int j = 0; j < R; ++j) {  // PA = LU (unit L below, U on and above the diagonal)
+    int p = j;
+    for (int i = j + 1; i < R; ++i)
+      if (fabs(F[i + 8 * j]) > fabs(F[p + 8 * j])) p = i;
+    if (p != j) {
+      for (int c = 0; c < R; ++c) { const double t = F[j + 8 * c]; F[j + 8 * c] = F[p + 8 * c]; F[p + 8 * c] = t; }
+      const int t = piv[j]; piv[j] = piv[p]; piv[p] = t;
+    }
+    const double d = F[j + 8 * j];
+    for (int i = j + 1; i < R; ++i) {
+      const double l = (d != 0.0) ? F[i + 8 * j] / d : 0.0;
+      F[i + 8 * j] = l;
+      for (int c = j + 1; c < R; ++c) F[i + 8 * c] -= l * F[j + 8 * c];
+    }
+  }
+}
 
 // Thin Householder QR of the m x R panel M (smem, ld 64, m <= 64, R <= 8) by one warp, in place:
 // on exit M = Q (sign-fixed) and Rf (R x R, ld 8) = R with diag >= 0.  tau: R doubles of scratch.
@@ -112,9 +162,17 @@ __global__ void __launch_bounds__(256, 1) k_batched_cpqr(BatchedArgs a) {
   double* V = Rk + 3 * 64;               // V_n / Q0 panel (64 x 8, ld 64)
   double* R0 = V + 64 * 8;               // 8 x 8
   double* Wm = R0 + 64;                  // W / Ahat / A_n panel (64 x 8, ld 64)
-  double* Wsave = Wm + 64 * 8;           // W of mode 3 (fit)
+  double* Wsave = Wm + 64 * 8;           // W (QR / SVD) or M (NE / PINV) of mode 3 (fit)
+  double* Ss = Wsave + 64 * 8;           // S_n (NE / PINV), 8 x 8
+  double* Fs = Ss + 64;                  // its Cholesky / LU factors, 8 x 8
+  double* Jb = Fs + 64;                  // jacobi_pinv scratch: B, V (R x (R+1) each), M (R x R), input
+  double* Jv = Jb + 72;
+  double* Jm = Jv + 72;
+  double* Jin = Jm + 64;
   __shared__ double tau[kBatMaxR], lam[kBatMaxR], red[8], nX2s, fitprev, inner3;
-  __shared__ int stop;
+  __shared__ int stop, piv[kBatMaxR], cholok, jflag;
+  const bool ne = (a.variant == 0 || a.variant == 3);
+  const double tauv = (a.tau < 0.0) ? R * 2.220446049250313e-16 : a.tau;
   const int Id[3] = {I0, I1, I2};
   int64_t aoff[3];
   aoff[0] = (int64_t)p * (I0 + I1 + I2) * R;
@@ -133,7 +191,17 @@ __global__ void __launch_bounds__(256, 1) k_batched_cpqr(BatchedArgs a) {
       Qk[k * 512 + e] = (i < Id[k] && c < R) ? a.A0[aoff[k] + i + (int64_t)Id[k] * c] : 0.0;
     }
     __syncthreads();
-    if (wid == 0) bat_hh_qr(Qk + k * 512, Id[k], R, Rk + k * 64, tau);
+    if (ne) {  // G_k = A_k^T A_k (Alg. 1 line 3)
+      for (int e = tid; e < 64; e += nt) {
+        const int r = e % 8, c = e / 8;
+        double g = 0.0;
+        if (r < R && c < R)
+          for (int i = 0; i < Id[k]; ++i) g = fma(Qk[k * 512 + i + 64 * r], Qk[k * 512 + i + 64 * c], g);
+        Rk[k * 64 + e] = g;
+      }
+    } else if (wid == 0) {
+      bat_hh_qr(Qk + k * 512, Id[k], R, Rk + k * 64, tau);
+    }
     __syncthreads();
   }
   int it = 0;
@@ -181,35 +249,108 @@ __global__ void __launch_bounds__(256, 1) k_batched_cpqr(BatchedArgs a) {
           Y[i2 + 64 * j] = s;
         }
       }
-      // ---- lines 6-7: V_n = R_b (.) R_a and its QR (concurrently with the Y step above finishing)
       const int ka = (n == 0) ? 1 : 0, kb = (n == 2) ? 1 : 2;
-      for (int e = tid; e < 64 * 8; e += nt) {
-        const int j = e % 64, c = e / 64;
-        double v = 0.0;
-        if (j < R * R && c < R) v = Rk[ka * 64 + (j % R) + 8 * c] * Rk[kb * 64 + (j / R) + 8 * c];
-        V[e] = v;
-      }
-      __syncthreads();
-      if (wid == 0) bat_hh_qr(V, R * R, R, R0, tau);
-      __syncthreads();
-      // ---- line 9: W = Y_(n) Q0;  line 10: Ahat R0^T = W (back substitution per row)
       const int In = Id[n];
-      for (int e = tid; e < In * R; e += nt) {
-        const int i = e % In, c = e / In;
-        double s = 0.0;
-        for (int j = 0; j < R * R; ++j) s = fma(Y[i + 64 * j], V[j + 64 * c], s);
-        Wm[i + 64 * c] = s;
-        if (n == 2) Wsave[i + 64 * c] = s;
-      }
-      __syncthreads();
-      if (tid < In) {
-        for (int j = R - 1; j >= 0; --j) {
-          double acc = Wm[tid + 64 * j];
-          for (int l = j + 1; l < R; ++l) acc -= Wm[tid + 64 * l] * R0[j + 8 * l];
-          Wm[tid + 64 * j] = acc / R0[j + 8 * j];
+      if (ne) {
+        // ---- Alg. 1 lines 6-9: S_n = G_a (*) G_b, M_n = diag part of Y, Ahat S_n = M_n
+        for (int e = tid; e < 64; e += nt) Ss[e] = Rk[ka * 64 + e] * Rk[kb * 64 + e];
+        __syncthreads();  // every Y column written
+        for (int e = tid; e < In * R; e += nt) {
+          const int i = e % In, c = e / In;
+          const double m = Y[i + 64 * (c + R * c)];
+          Wm[i + 64 * c] = m;
+          if (n == 2) Wsave[i + 64 * c] = m;
         }
+        __syncthreads();
+        if (a.variant == 3) {  // CP-ALS-PINV: Ahat = M S^+ (SVD pseudo-inverse)
+          for (int e = tid; e < R * R; e += nt) Jin[e] = Ss[(e % R) + 8 * (e / R)];
+          __syncthreads();
+          jacobi_pinv(Jin, R, tauv, Jb, Jv, Jm, &jflag);
+          if (tid < In) {
+            double mv[kBatMaxR];
+            for (int c = 0; c < R; ++c) mv[c] = Wm[tid + 64 * c];
+            for (int c = 0; c < R; ++c) {
+              double s = 0.0;
+              for (int r = 0; r < R; ++r) s = fma(mv[r], Jm[r + R * c], s);
+              Wm[tid + 64 * c] = s;
+            }
+          }
+        } else {
+          if (tid == 0) bat_ne_factor(Ss, R, Fs, piv, &cholok);
+          __syncthreads();
+          if (tid < In) {  // row i: S ahat = m (S symmetric)
+            double x[kBatMaxR];
+            if (cholok) {
+              for (int j = 0; j < R; ++j) {  // L y = m
+                double v = Wm[tid + 64 * j];
+                for (int k = 0; k < j; ++k) v -= Fs[j + 8 * k] * x[k];
+                x[j] = v / Fs[j + 8 * j];
+              }
+              for (int j = R - 1; j >= 0; --j) {  // L^T ahat = y
+                double v = x[j];
+                for (int k = j + 1; k < R; ++k) v -= Fs[k + 8 * j] * x[k];
+                x[j] = v / Fs[j + 8 * j];
+              }
+            } else {
+              double y[kBatMaxR];
+              for (int j = 0; j < R; ++j) {  // L y = P m
+                double v = Wm[tid + 64 * piv[j]];
+                for (int k = 0; k < j; ++k) v -= Fs[j + 8 * k] * y[k];
+                y[j] = v;
+              }
+              for (int j = R - 1; j >= 0; --j) {  // U ahat = y
+                double v = y[j];
+                for (int k = j + 1; k < R; ++k) v -= Fs[j + 8 * k] * x[k];
+                x[j] = v / Fs[j + 8 * j];
+              }
+            }
+            for (int c = 0; c < R; ++c) Wm[tid + 64 * c] = x[c];
+          }
+        }
+        __syncthreads();
+      } else {
+        // ---- lines 6-7: V_n = R_b (.) R_a and its QR
+        for (int e = tid; e < 64 * 8; e += nt) {
+          const int j = e % 64, c = e / 64;
+          double v = 0.0;
+          if (j < R * R && c < R) v = Rk[ka * 64 + (j % R) + 8 * c] * Rk[kb * 64 + (j / R) + 8 * c];
+          V[e] = v;
+        }
+        __syncthreads();
+        if (wid == 0) bat_hh_qr(V, R * R, R, R0, tau);
+        __syncthreads();
+        // ---- line 9: W = Y_(n) Q0;  line 10: Ahat R0^T = W (back substitution per row), or the
+        // QR-SVD solve Ahat = W U S^+ V^T
+        for (int e = tid; e < In * R; e += nt) {
+          const int i = e % In, c = e / In;
+          double s = 0.0;
+          for (int j = 0; j < R * R; ++j) s = fma(Y[i + 64 * j], V[j + 64 * c], s);
+          Wm[i + 64 * c] = s;
+          if (n == 2) Wsave[i + 64 * c] = s;
+        }
+        __syncthreads();
+        if (a.variant == 2) {
+          for (int e = tid; e < R * R; e += nt) Jin[e] = R0[(e % R) + 8 * (e / R)];
+          __syncthreads();
+          jacobi_pinv(Jin, R, tauv, Jb, Jv, Jm, &jflag);
+          if (tid < In) {
+            double wv[kBatMaxR];
+            for (int c = 0; c < R; ++c) wv[c] = Wm[tid + 64 * c];
+            for (int c = 0; c < R; ++c) {
+              double s = 0.0;
+              for (int r = 0; r < R; ++r) s = fma(wv[r], Jm[r + R * c], s);
+              Wm[tid + 64 * c] = s;
+            }
+          }
+        } else if (tid < In) {
+          for (int j = R - 1; j >= 0; --j) {
+            double acc = Wm[tid + 64 * j];
+            for (int l = j + 1; l < R; ++l) acc -= Wm[tid + 64 * l] * R0[j + 8 * l];
+            Wm[tid + 64 * j] = acc / R0[j + 8 * j];
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
       // ---- line 11: lambda, normalise (lambda = 0 -> e_1);  line 12: QR(A_n)
       if (wid < R) {
         double ss = 0.0;
@@ -218,12 +359,14 @@ __global__ void __launch_bounds__(256, 1) k_batched_cpqr(BatchedArgs a) {
         if (lane == 0) lam[wid] = sqrt(ss);
       }
       __syncthreads();
-      if (n == 2 && a.max_iters > 0) {  // keep Ahat_3 for the fit: <W_3, Ahat_3 R0^T>
+      if (n == 2 && a.max_iters > 0) {  // <X, Xh>: <W_3, Ahat_3 R0^T> (QR / SVD) or <M_3, Ahat_3> (NE)
         double s = 0.0;
         for (int e = tid; e < In * R; e += nt) {
           const int i = e % In, c = e / In;
           double t = 0.0;
-          for (int l = c; l < R; ++l) t = fma(Wm[i + 64 * l], R0[c + 8 * l], t);
+          if (ne) t = Wm[i + 64 * c];
+          else
+            for (int l = c; l < R; ++l) t = fma(Wm[i + 64 * l], R0[c + 8 * l], t);
           s = fma(Wsave[i + 64 * c], t, s);
         }
         s = block_sum(s, red);
@@ -240,14 +383,28 @@ __global__ void __launch_bounds__(256, 1) k_batched_cpqr(BatchedArgs a) {
         Qk[n * 512 + e] = v;
       }
       __syncthreads();
-      if (wid == 0) bat_hh_qr(Qk + n * 512, In, R, Rk + n * 64, tau);
+      if (ne) {  // G_n = A_n^T A_n (Alg. 1 line 11)
+        for (int e = tid; e < 64; e += nt) {
+          const int r = e % 8, c = e / 8;
+          double g = 0.0;
+          if (r < R && c < R)
+            for (int i = 0; i < In; ++i) g = fma(Qk[n * 512 + i + 64 * r], Qk[n * 512 + i + 64 * c], g);
+          Rk[n * 64 + e] = g;
+        }
+      } else if (wid == 0) {
+        bat_hh_qr(Qk + n * 512, In, R, Rk + n * 64, tau);
+      }
       __syncthreads();
     }
-    // ---- fast fit after mode 3
+    // ---- fast fit after mode 3 (NE: PAPER.md:417-425)
     if (tid == 0) {
-      double nxh2 = 0.0;  // <R0^T R0, diag(lam) R_3^T R_3 diag(lam)>
+      double nxh2 = 0.0;  // <R0^T R0, diag(lam) R_3^T R_3 diag(lam)>  or  <S_3, diag(lam) G_3 diag(lam)>
       for (int x = 0; x < R; ++x)
         for (int y = 0; y < R; ++y) {
+          if (ne) {
+            nxh2 = fma(Ss[x + 8 * y], lam[x] * lam[y] * Rk[2 * 64 + x + 8 * y], nxh2);
+            continue;
+          }
           double g0 = 0.0, g1 = 0.0;
           for (int k = 0; k <= min(x, y); ++k) {
             g0 = fma(R0[k + 8 * x], R0[k + 8 * y], g0);

@@ -2416,7 +2416,14 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
 CPQR_API cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const double* X, const double* A0,
                                      int max_iters, double tol, double* A, double* lam, double* fits,
                                      int* iters, void* stream) {
+  return cpqr_batched(P, dims, R, CPQR_QR, -1.0, X, A0, max_iters, tol, A, lam, fits, iters, stream);
+}
+
+CPQR_API cpqr_status cpqr_batched(int P, const int64_t* dims, int R, int variant, double tau, const double* X,
+                                  const double* A0, int max_iters, double tol, double* A, double* lam,
+                                  double* fits, int* iters, void* stream) {
   if (P < 0 || !dims || !X || !A0 || !A || !lam || !fits || !iters || max_iters < 1) return CPQR_EINVAL;
+  if (variant < CPQR_NE || variant > CPQR_PINV) return CPQR_EINVAL;
   if (R < 1 || R > kBatMaxR) return CPQR_EINVAL;
   for (int k = 0; k < 3; ++k)
     if (dims[k] < R || dims[k] > kBatMaxI) return CPQR_EINVAL;
@@ -2426,7 +2433,9 @@ CPQR_API cpqr_status cpqr_batched_qr(int P, const int64_t* dims, int R, const do
   a.X = X; a.A0 = A0; a.R = R; a.max_iters = max_iters; a.tol = tol;
   for (int k = 0; k < 3; ++k) a.I[k] = (int)dims[k];
   a.A = A; a.lam = lam; a.fits = fits; a.iters = iters;
-  const size_t smem = (size_t)(kBatTBuf + 64 * 64 + 3 * 64 * 8 + 3 * 64 + 64 * 8 + 64 + 2 * 64 * 8) * sizeof(double);
+  a.variant = variant; a.tau = tau;
+  const size_t smem = (size_t)(kBatTBuf + 64 * 64 + 3 * 64 * 8 + 3 * 64 + 64 * 8 + 64 + 2 * 64 * 8 +
+                               2 * 64 + 2 * 72 + 2 * 64) * sizeof(double);
   if (cudaFuncSetAttribute(k_batched_cpqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return CPQR_ECUDA;
   k_batched_cpqr<<<P, 256, smem, (cudaStream_t)stream>>>(a);

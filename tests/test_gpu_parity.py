@@ -1062,3 +1062,55 @@ def test_overlap_schedule_householder_tail(cp, dims, R, monkeypatch):
     for k in range(len(dims)):
         assert rel(A[k], ref1["factors"][k]) <= 1e-9, k
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+
+
+def _oracle_run(variant, X, A0, sweeps, tau=-1.0):
+    if variant in ("QR", "SVD"):
+        return O.cp_als_qr(X, A0, sweeps, variant=variant, tau=tau)
+    return O.cp_als_ne(X, A0, sweeps, solve="pinv" if variant == "PINV" else "chol", tau=tau)
+
+
+@pytest.mark.parametrize("variant", ["NE", "SVD", "PINV", "QR"])
+@pytest.mark.parametrize("dims,R,kw", [((20, 18, 16), 3, dict(eta=0.05)),
+                                       ((12, 14, 10), 5, dict(eta=1e-3, kind="congruence", c=0.99)),
+                                       ((50, 50, 50), 5, dict(eta=1e-4)), ((33, 30, 31), 5, dict(eta=1e-4))])
+def test_batched_all_variants(cp, dims, R, kw, variant):
+    """cpqr_batched: the four solvers of the accuracy study one CTA per problem --
+    CP-ALS (Alg. 1, Cholesky), CP-ALS-PINV (PAPER.md:264-266), CP-ALS-QR and QR-SVD (Alg. 2,
+    PAPER.md:335-339) -- against the oracle's drivers: factors and lambda <= 1e-9 after one sweep,
+    fits within 1e-8 for every sweep of a 6-sweep run (tol = 0), every problem of the batch."""
+    seeds = [301, 302, 303, 304]
+    Xs, A0s, X, A0 = _batched_inputs(dims, R, seeds, **kw)
+    for sweeps in (1, 6):
+        A, lam, fits, iters = cp.batched_qr(X, A0, R, max_iters=sweeps, tol=0.0, variant=variant)
+        A = [a.cpu().numpy() for a in A]
+        lam, fits, iters = lam.cpu().numpy(), fits.cpu().numpy(), iters.cpu().numpy()
+        assert np.all(iters == sweeps)
+        for p in range(len(seeds)):
+            ref = _oracle_run(variant, O.as_tensor(Xs[p]), A0s[p], sweeps)
+            assert np.max(np.abs(fits[p] - np.array(ref["fits"]))) <= 1e-8, (p, fits[p], ref["fits"])
+            if sweeps == 1:
+                for k in range(3):
+                    assert rel(A[k][p].T, ref["factors"][k]) <= 1e-9, (p, k, rel(A[k][p].T, ref["factors"][k]))
+                assert rel(lam[p], ref["lam"]) <= 1e-9
+
+
+@pytest.mark.parametrize("variant", ["SVD", "PINV"])
+def test_batched_truncation_exact_duplicate(cp, variant):
+    """Exact duplicate columns (A_k(:,2) = A_k(:,1) for the initial factors of modes 2, 3): R0 (QR-SVD)
+    and S_n (PINV) are singular, sigma's below tau sigma_max are dropped,
+    and the minimum-norm solution is unique: the batched solvers match the oracle's after one sweep
+    (factors <= 1e-9) and the duplicated columns of A_1 stay equal."""
+    import torch
+    dims, R = (16, 14, 12), 4
+    Xs, A0s, X, A0 = _batched_inputs(dims, R, [401, 402], eta=0.05)
+    for p in range(2):
+        for k in (1, 2):
+            A0s[p][k][:, 1] = A0s[p][k][:, 0]
+    A0 = [torch.from_numpy(np.stack([np.ascontiguousarray(a[k].T) for a in A0s])).cuda() for k in range(3)]
+    A, lam, fits, iters = cp.batched_qr(X, A0, R, max_iters=1, tol=0.0, variant=variant, tau=1e-12)
+    A = [a.cpu().numpy() for a in A]
+    for p in range(2):
+        ref = _oracle_run(variant, O.as_tensor(Xs[p]), A0s[p], 1, tau=1e-12)
+        assert rel(A[0][p].T, ref["factors"][0]) <= 1e-9, p
+        assert np.allclose(A[0][p][0], A[0][p][1], rtol=0, atol=1e-12)
