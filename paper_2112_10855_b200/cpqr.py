@@ -79,6 +79,8 @@ _sig = {
     "cpqr_version": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _sig.items():
+    if "CPQR_LIB" in os.environ and not hasattr(_lib, _name):
+        continue  # an alternate (older / instrumented A-B) build may lack newer entry points
     _f = getattr(_lib, _name)
     _f.restype = _res
     _f.argtypes = _args

@@ -37,6 +37,37 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef CPQR_RELEASE_MODE
+#define CPQR_RELEASE_MODE 1
+#endif
+// OR of the raw bits of a warp's accumulator array: a value that depends on every DMMA of the stage
+template <int M, int N>
+__device__ __forceinline__ unsigned long long acc_dep(const double (&acc)[M][N][2]) {
+  unsigned long long d = 0;
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int n = 0; n < N; ++n) d |= __double_as_longlong(acc[m][n][0]) | __double_as_longlong(acc[m][n][1]);
+  return d;
+}
+// Consumer release of a ring stage (write-after-read hazard with the producer's next TMA into it).
+// The stage was read with generic-proxy ld.shared; the refill is an async-proxy write.  Each thread
+// orders its reads before the release with fence.proxy.async, then the warp's lane 0 arrives with
+// release semantics.  dep: a value computed from the stage's data (the warp's accumulators), so the
+// arrive also waits on the loads' results (mode 2).
+__device__ __forceinline__ void consumer_release(uint64_t* bar, int lane, unsigned long long dep) {
+#if CPQR_RELEASE_MODE >= 1
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
+  __syncwarp();
+#if CPQR_RELEASE_MODE == 2
+  if (lane == 0 && dep != 0x7ff4dead0000beefull)
+#else
+  (void)dep;
+  if (lane == 0)
+#endif
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 #ifdef CPQR_DEBUG_HANG
 // debugging build (CPQR_DEBUG_HANG=1 python -m paper_2112_10855_b200.build): a wait that spins too
 // long reports block / thread / barrier / parity and traps instead of hanging the GPU
@@ -183,11 +214,12 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
               int I, int64_t B, int R, double* __restrict__ T, int S, double* __restrict__ P,
               unsigned* __restrict__ cnt) {
   extern __shared__ uint8_t smraw[];
-  __shared__ int sk_last;
   constexpr int NQB = (NT + 1) / 2;
   constexpr uint32_t XBYTES = 2 * CW * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
   uint8_t* st0 = tma_carve(smraw, S, full, empty);
+  // the fused fix-up's "last to arrive" flag: in the carved barrier block (no static shared memory)
+  volatile int& sk_last = *reinterpret_cast<volatile int*>(reinterpret_cast<uint8_t*>(full) + 1024);
   const uint32_t sbase = smem_u32(st0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -281,8 +313,7 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             dmma(acc[3][n][0], acc[3][n][1], xa[1].y, qb[n]);
           }
         }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      consumer_release(&empty[s], lane, acc_dep(acc));
     }
     if (ks0 == 0 && ks1 == KS) {  // the whole unit: straight to T
       double* __restrict__ Tb = T + A * (int64_t)R * b;
@@ -465,8 +496,7 @@ k_fiber_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
       mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE;
       fiber_stage<MT, NF>(xs, xs + XBYTES, warp, g, t, acc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      consumer_release(&empty[s], lane, acc_dep(acc));
     }
     const int64_t f0 = u * 128 + 8 * NF * warp;
 #pragma unroll
@@ -566,8 +596,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
       mbar_wait(&full[s], rp.ph);
       const uint32_t xs = sbase + s * STAGE;
       fiber_stage<MT, NF>(xs, xs + XBYTES, warp, g, t, acc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      consumer_release(&empty[s], lane, acc_dep(acc));
     }
     if constexpr (YREG) {
 #pragma unroll
@@ -733,8 +762,7 @@ k_slice_small_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant
               for (int m = 0; m < MT; ++m) dmma(acc[m][n][0], acc[m][n][1], qa[m], sk ? xb[n].y : xb[n].x);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      consumer_release(&empty[s], lane, acc_dep(acc));
     }
     const int64_t l = u * 8 + warp;
     double yacc[MT][MT][2];
