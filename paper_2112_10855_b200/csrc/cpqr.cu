@@ -1326,8 +1326,6 @@ cpqr_status launch_tsqr(cpqr_ctx* c, int m, const double* A, bool solve, const d
     gated = true;
     cq_nb = nbq;
   }
-  // (measurement only: CPQR_EXP_NO_HH=1 drops the gated fallback launch -- unsafe if it is needed)
-  if (gated && getenv("CPQR_EXP_NO_HH") && atoi(getenv("CPQR_EXP_NO_HH")) == 1) return CPQR_OK;
   // Householder fallback 1: register-resident TSQR (one thread per row), leaves and root <= 256 rows
   {
     int nl = std::max(1, (m + 255) / 256);

@@ -1114,3 +1114,26 @@ def test_batched_truncation_exact_duplicate(cp, variant):
         ref = _oracle_run(variant, O.as_tensor(Xs[p]), A0s[p], 1, tau=1e-12)
         assert rel(A[0][p].T, ref["factors"][0]) <= 1e-9, p
         assert np.allclose(A[0][p][0], A[0][p][1], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("n", [0, 1])
+def test_tma_ring_war_determinism_l2_resident(cp, n):
+    """The C3 shape (128^4, R = 16): the Multi-TTM's later strided steps stream an L2-resident
+    intermediate, so the TMA refill of a ring stage lands within a few hundred cycles of the
+    consumers' release.  Without fence.proxy.async between the consumers' ld.shared reads and the
+    release (generic vs async proxy, write-after-read), ~1-2 % of these Multi-TTMs had one 16-row
+    box wrong.  100 repeats of mode n's Multi-TTM must be bitwise identical."""
+    import torch
+    from paper_2112_10855_b200 import synth as S
+    conf = S.CONFIGS[3]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    X = torch.randn(int(np.prod(conf.dims)), dtype=torch.float64, device="cuda", generator=g)
+    s = cp.CPQR(conf.dims, conf.R, "QR")
+    s.set_tensor(X)
+    s.set_factors(S.init_factors(conf))
+    ref = s.debug_mode(n)["Y"]
+    bad = sum(not np.array_equal(s.debug_mode(n)["Y"], ref) for _ in range(100))
+    s.close()
+    del X
+    torch.cuda.empty_cache()
+    assert bad == 0, bad
