@@ -1137,3 +1137,32 @@ def test_tma_ring_war_determinism_l2_resident(cp, n):
     del X
     torch.cuda.empty_cache()
     assert bad == 0, bad
+
+
+@pytest.mark.parametrize("dims,R,tree", [((40, 36, 30), 6, False), ((24, 20, 18, 22), 8, False),
+                                         ((9, 8, 7, 6, 8), 4, False), ((24, 20, 18, 22), 8, True)])
+def test_cost_accounting_matches_oracle_ttm_cost(cp, dims, R, tree):
+    """SURVEY.md 8(c) cost accounting: the flops the library attributes to each Multi-TTM step
+    (cpqr_debug_plan) follow Eq. (TTMcost): for every mode, in the library's own
+    contraction order, the steps' flops sum to the oracle's ttm_cost(dims, n, R, order) (fused slice
+    steps count both contractions); and cpqr_get_profile's flops0 / bytes0 equal the stream-X
+    passes' first steps and N (or 2 with the dimension tree) reads of X."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=5)
+    s = cp.CPQR(dims, R, "QR", profile=True, use_graph=False, tree=tree)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    N = len(dims)
+    first, passes = 0.0, 0
+    for n in range(N):
+        pl = [st for st in s.debug_plan(n) if st["kind"] not in ("slice-reduce", "slice-fixup")]
+        order = [k for st in pl for k in st["modes"]]
+        if not tree:
+            assert sorted(order) == [k for k in range(N) if k != n]
+            assert sum(st["flops"] for st in pl) == O.ttm_cost(dims, n, R, order=order), (n, pl)
+        if pl and pl[0]["x_pass"]:
+            first += pl[0]["flops"]
+            passes += 1
+    p = s.profile()
+    s.close()
+    assert passes == (2 if tree else N)
+    assert p["flops0"] == first and p["bytes0"] == passes * 8.0 * np.prod(dims)
