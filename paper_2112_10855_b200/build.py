@@ -39,6 +39,7 @@ def build(force=False, verbose=True, out=None):
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v" if verbose == "ptxas" else "-O3", *(["-DCPQR_DEBUG_FIT"] if os.environ.get("CPQR_DEBUG_FIT") else []), *(["-DCPQR_DEBUG_TIMING"] if os.environ.get("CPQR_DEBUG_TIMING") else []), *(["-DCPQR_DEBUG_HANG"] if os.environ.get("CPQR_DEBUG_HANG") else []),
            *([f"-DCPQR_RELEASE_MODE={int(os.environ['CPQR_RELEASE_MODE'])}"] if os.environ.get("CPQR_RELEASE_MODE") else []),
+           *([f"-DCPQR_CQ_CLOSED_FORM={int(os.environ['CPQR_CQ_CLOSED_FORM'])}"] if os.environ.get("CPQR_CQ_CLOSED_FORM") else []),
            "-I", inc, "-I", os.path.join(ROOT, "include"),
            *SRC, "-o", LIB + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-cudart", "static"]

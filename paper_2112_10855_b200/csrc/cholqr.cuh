@@ -22,6 +22,10 @@
 namespace cpqr {
 
 constexpr double kCqKappaMax = 1.0e5;
+#ifndef CPQR_CQ_CLOSED_FORM
+#define CPQR_CQ_CLOSED_FORM 1
+#endif
+constexpr bool kCqClosedForm = CPQR_CQ_CLOSED_FORM != 0;  // second CholeskyQR pass in closed form
 constexpr unsigned FLAG_USE_HOUSEHOLDER = 0x200u;
 constexpr unsigned FLAG_VN_HOUSEHOLDER = 0x400u;  // the CholeskyQR2 V_n QR handed over to K2
 
@@ -605,17 +609,37 @@ __global__ void __launch_bounds__(512) k_cq_compact(CqArgs a) {
   cluster.sync();
   #pragma unroll 1
   for (int e = tid; e < RB * RB; e += blockDim.x) Gs[e] = cluster_sum_ordered(cluster, G2b + e, nb);
+  bool small_e;
   {
-    bool bad = false;  // ||G2 - I||_max must be O(kappa^2 eps)
+    // ||G2 - I||_max must be O(kappa^2 eps); below 2^-30 the second Cholesky has a closed form
+    bool bad = false, big = false;
     #pragma unroll 4
     for (int q = tid; q < RB * RB; q += blockDim.x) {
       const int r = q % RB, c = q / RB;
-      if (r < R && c < R) bad |= !(fabs(Gs[q] - (r == c ? 1.0 : 0.0)) < 1.0e-4);
+      if (r < R && c < R) {
+        const double e = fabs(Gs[q] - (r == c ? 1.0 : 0.0));
+        bad |= !(e < 1.0e-4);
+        big |= !(e < 9.313225746154785e-10);  // 2^-30
+      }
     }
     bad = __syncthreads_or(bad);
+    small_e = !__syncthreads_or(big) && kCqClosedForm;
     if (tid == 0) okf = !bad;
   }
-  {
+  if (small_e) {
+    // G2 = I + E with max|E| < 2^-30 (CholeskyQR2's usual case, kappa(A)^2 eps small): the Cholesky
+    // factor of I + E is R2 = I + U, U = strict upper part of E + diag(E) / 2, up to U^T U (entries
+    // below R 2^-60 < eps) -- the same R2 to rounding without the 32-step dependent column chain
+    #pragma unroll 1
+    for (int e = tid; e < RB * RB; e += blockDim.x) {
+      const int r = e % RB, c = e / RB;
+      double v = 0.0;
+      if (r < R && c < R && r <= c) v = (r == c) ? 1.0 + 0.5 * (Gs[e] - 1.0) : Gs[e];
+      R2s[e] = v;
+    }
+    if (tid < RB) inv2[tid] = (tid < R) ? 1.0 / (1.0 + 0.5 * (Gs[tid + RB * tid] - 1.0)) : 0.0;
+    __syncthreads();
+  } else {
     double ratio;
     const bool ok = cq_chol_2d<RB>(Gs, R, R2s, inv2, &ratio);
     if (tid == 0) okf = okf && ok;

@@ -615,7 +615,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       const int64_t tunits = (k == 0) ? (B + ur - 1) / ur : ((A + ur - 1) / ur) * B;
       const bool starved = tunits < in.sms / 2 || (k != 0 && A < 32);
       const bool force = getenv("CPQR_TTM_SMALL") && atoi(getenv("CPQR_TTM_SMALL")) == 2;  // tests
-      if (!small_off && (starved || force) && src != in.X && A * I * B <= kSmallTtmMax && in.Qt[k] &&
+      if (!small_off && (starved || force) && src != in.X && (A * I * B <= kSmallTtmMax || (force && A * I * B < (1ll << 30))) && in.Qt[k] &&
           small_split(A, I, B, R, in.sms, wk, kc, smem)) {
         s.kind = 9;
         s.A = A; s.I = I; s.B = B;
@@ -2263,7 +2263,10 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     const char* v = getenv("CPQR_VN_QR");  // "cq" / "householder" force the choice
     // every mode above R^{N-1} R = 2e5 (the one-CTA K2 dominates the sweep); from 5e4, inline, in the
     // dimension tree's modes without an X pass, which cannot hide K2 (see mode_update)
-    c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000);
+    // slab data parallelism: the V_n QR is replicated on every rank and no longer hides behind a
+    // p-times shorter stream pass, so it takes the CholeskyQR2 path there too (virtual-rank
+    // projection: C3 at p = 8 0.50 -> 0.16 ms per sweep)
+    c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000 || c->opt.world > 1);
     {  // tree modes without an X pass run the V_n QR inline (CholeskyQR2); CPQR_VN_TREE=0/1 overrides
       const char* t = getenv("CPQR_VN_TREE");
       // the one-launch cluster CholeskyQR2 (k_cq_compact) takes V_n up to 8 CTAs x 512 rows (R <= 16)

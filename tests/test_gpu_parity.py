@@ -428,7 +428,12 @@ def test_edge_shapes(cp, dims, R, variant):
         assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
     f = np.concatenate([f1, s.sweep(2)])
     ref = O.cp_als_qr(X, init, 3, variant=variant)
-    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    # an exact fit (N = 2, square factor) puts ||X||^2 - 2<X,Xh> + ||Xh||^2 at the rounding level,
+    # where the fast fit only resolves sqrt(eps) ~ 1.5e-8: there both sides must sit
+    # at fit 1 within that floor (sqrt(8 eps) = 4.2e-8); elsewhere within 1e-8
+    rf = np.array(ref["fits"])
+    tol = np.where(rf > 1 - 1e-7, 4.3e-8, 1e-8)
+    assert np.all(np.abs(f - rf) <= tol), (f, rf)
     s.close()
 
 

@@ -9,8 +9,9 @@ The projected time of one rank on its own GPU is
 
     T_rank(p) = (stream + rest + q0_apply) / p + tail + other + max(0, vn_qr - stream / p) + comm(p)
 
-(the V_n QR hides behind the stream pass on the side stream, as on one GPU; the virtual ranks'
-combine kernel is excluded; comm(p) is NOT measured here -- no multi-GPU box -- and is an
+(the one-CTA Householder V_n QR hides behind the stream pass on the side stream as on one GPU;
+the CholeskyQR2 V_n QR used at p > 1 is counted in full; the virtual ranks' combine kernel is
+excluded; comm(p) is NOT measured here -- no multi-GPU box -- and is an
 assumed per-mode NCCL latency).  Also printed: the measured sweep time of the LOCAL context (all slabs in sequence, CUDA
 graph), which is p times the slab work plus the tails.  A projection, not a measurement.
 
@@ -57,7 +58,13 @@ def main():
             ms = [v / args.sweeps for v in pr["ms"]]
             stream, rest, fqr, vn, q0a, other, exch = ms
             slab = (stream + rest + q0a) / p
-            t_rank = slab + fqr + other + max(0.0, vn - stream / p) + conf.N * args.comm_us / 1e3 * (p > 1)
+            # the one-CTA Householder V_n QR (p = 1, low rank) runs on the SM the stream grids leave
+            # free and hides behind the pass; the CholeskyQR2 V_n QR (p > 1, or R^{N-1} R >= 2e5) is
+            # a multi-CTA launch that cannot co-run with a 147-CTA stream grid: counted in full
+            J = conf.R ** (conf.N - 1)
+            cq = p > 1 or J * conf.R >= 200000 or os.environ.get("CPQR_VN_QR") == "cq"
+            vn_exposed = vn if cq else max(0.0, vn - stream / p)
+            t_rank = slab + fqr + other + vn_exposed + conf.N * args.comm_us / 1e3 * (p > 1)
             # the LOCAL context's own sweep time (graph, all p slabs in sequence)
             g = cpqr.CPQR(conf.dims, conf.R, variant, **kw)
             g.set_tensor(Xd)
