@@ -2263,10 +2263,10 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     const char* v = getenv("CPQR_VN_QR");  // "cq" / "householder" force the choice
     // every mode above R^{N-1} R = 2e5 (the one-CTA K2 dominates the sweep); from 5e4, inline, in the
     // dimension tree's modes without an X pass, which cannot hide K2 (see mode_update)
-    // slab data parallelism: the V_n QR is replicated on every rank and no longer hides behind a
-    // p-times shorter stream pass, so it takes the CholeskyQR2 path there too (virtual-rank
-    // projection: C3 at p = 8 0.50 -> 0.16 ms per sweep)
-    c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000 || c->opt.world > 1);
+    // (at world > 1 the V_n QR is replicated and must hide behind a p-times shorter pass: the
+    // one-CTA K2 still does on C5 at p = 8, while C3 gains from CPQR_VN_QR=cq -- the multi-CTA
+    // CholeskyQR2 cannot co-run with the stream grid and is exposed)
+    c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000);
     {  // tree modes without an X pass run the V_n QR inline (CholeskyQR2); CPQR_VN_TREE=0/1 overrides
       const char* t = getenv("CPQR_VN_TREE");
       // the one-launch cluster CholeskyQR2 (k_cq_compact) takes V_n up to 8 CTAs x 512 rows (R <= 16)

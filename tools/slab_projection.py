@@ -9,8 +9,9 @@ The projected time of one rank on its own GPU is
 
     T_rank(p) = (stream + rest + q0_apply) / p + tail + other + max(0, vn_qr - stream / p) + comm(p)
 
-(the one-CTA Householder V_n QR hides behind the stream pass on the side stream as on one GPU;
-the CholeskyQR2 V_n QR used at p > 1 is counted in full; the virtual ranks' combine kernel is
+(the one-CTA Householder V_n QR hides behind the stream pass on the side stream as on one GPU,
+as far as the pass is long enough; the multi-CTA CholeskyQR2 V_n QR (high rank, or CPQR_VN_QR=cq)
+cannot co-run with the stream grid and is counted in full; the virtual ranks' combine kernel is
 excluded; comm(p) is NOT measured here -- no multi-GPU box -- and is an
 assumed per-mode NCCL latency).  Also printed: the measured sweep time of the LOCAL context (all slabs in sequence, CUDA
 graph), which is p times the slab work plus the tails.  A projection, not a measurement.
@@ -62,7 +63,7 @@ def main():
             # free and hides behind the pass; the CholeskyQR2 V_n QR (p > 1, or R^{N-1} R >= 2e5) is
             # a multi-CTA launch that cannot co-run with a 147-CTA stream grid: counted in full
             J = conf.R ** (conf.N - 1)
-            cq = p > 1 or J * conf.R >= 200000 or os.environ.get("CPQR_VN_QR") == "cq"
+            cq = J * conf.R >= 200000 or os.environ.get("CPQR_VN_QR") == "cq"
             vn_exposed = vn if cq else max(0.0, vn - stream / p)
             t_rank = slab + fqr + other + vn_exposed + conf.N * args.comm_us / 1e3 * (p > 1)
             # the LOCAL context's own sweep time (graph, all p slabs in sequence)
