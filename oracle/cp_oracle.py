@@ -32,7 +32,7 @@ __all__ = [
     "solve_qr", "solve_svd", "pinv_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
     "fit_direct", "mode_update_qr", "mode_update_ne", "cp_als_qr", "cp_als_ne",
     "qr_cost", "ttm_cost", "mttkrp", "ktensor_norm2", "w_ktensor", "mttkrp_ktensor",
-    "sine_of_sums_ktensor", "score",
+    "sine_of_sums_ktensor", "sine_of_sums_rank_n_ktensor", "score",
 ]
 
 
@@ -355,6 +355,24 @@ def sine_of_sums_ktensor(N: int, n: int):
     terms = [t for t in range(1 << N) if bin(t).count("1") % 2 == 1]
     lam = np.array([(-1.0) ** ((bin(t).count("1") - 1) // 2) for t in terms])
     B = [np.stack([np.sin(x) if (t >> j) & 1 else np.cos(x) for t in terms], axis=1) for j in range(N)]
+    return lam, B
+
+
+def sine_of_sums_rank_n_ktensor(N: int, n: int, alpha=None):
+    """The rank-N representation of sin(x_1 + .. + x_N) (Eq. (sinsum_rkd)):
+    sum_j sin(x_j) prod_{k != j} sin(x_k + alpha_k - alpha_j) / sin(alpha_k - alpha_j), on the grid
+    x = 2 pi i / n, with alpha_j = (j - 1) pi / N by default (the paper leaves alpha open; any
+    values with sin(alpha_k - alpha_j) != 0 are exact; reading 33).  Used for the 10-way case
+    "in rank-10 representation" (PAPER.md:638-641)."""
+    x = 2.0 * np.pi * np.arange(n) / n
+    a = np.pi * np.arange(N) / N if alpha is None else np.asarray(alpha, dtype=np.float64)
+    lam = np.ones(N)
+    B = []
+    for k in range(N):
+        cols = []
+        for j in range(N):
+            cols.append(np.sin(x) if k == j else np.sin(x + a[k] - a[j]) / np.sin(a[k] - a[j]))
+        B.append(np.stack(cols, axis=1))
     return lam, B
 
 

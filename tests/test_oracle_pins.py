@@ -544,3 +544,54 @@ def test_score_limits_and_invariances():
     Fo = [np.vstack([np.zeros((4, R)), np.ones((2, R))]), E[1], E[2]]  # mode-1 columns orthogonal to E's
     assert O.score(np.ones(R), E, np.ones(R), Fo) <= 1e-14
     assert abs(O.score(np.ones(R), E, 2.0 * np.ones(R), E) - 0.5) <= 1e-14
+
+
+# ---------------------------------------------------- short modes (I_k < R)
+def test_short_modes_mode_update_is_the_least_squares_minimizer():
+    """I_k < R (the 10-way sine of sums has I_k = 8 < R = 10): qr_pos returns the economy QR
+    (Q_k I_k x I_k, R_k I_k x R, trapezoidal), V_n has prod_{k != n} I_k rows, and the QR mode
+    update still equals LAPACK least squares min ||X_(n) - Ahat Z_n^T|| whenever Z_n has full
+    column rank."""
+    dims, R = (2, 3, 7, 6), 4
+    X = rand_tensor(dims)
+    A, Qs, Rs = _setup_factors(dims, R)
+    assert Rs[0].shape == (2, 4) and Qs[1].shape == (3, 3)
+    for n in range(4):
+        u = O.mode_update_qr(X, Qs, Rs, n)
+        Z = O.khatri_rao([A[k] for k in range(3, -1, -1) if k != n])
+        assert np.linalg.matrix_rank(Z) == R
+        ref = np.linalg.lstsq(Z, O.matricize(X, n).T, rcond=None)[0].T
+        assert rel(u["Ahat"], ref) <= 1e-12, n
+
+
+def test_short_modes_zero_padding_is_exact():
+    """The library stores a short mode's factor with max(I_k, R) rows, the extra rows zero, and
+    pads the Kruskal input's B_k the same way: CP-ALS-QR on the padded problem follows the
+    unpadded one exactly up to rounding (the padded rows of X are zero, so every Ahat keeps them
+    zero; their rows of R_k are zero, so V_n's extra rows are zero).  Pinned here on the oracle."""
+    rng2 = np.random.default_rng(8)
+    dims, R, S = (3, 5, 4, 6), 5, 3
+    lam = rng2.standard_normal(S)
+    B = [rng2.standard_normal((d, S)) for d in dims]
+    A0 = [rng2.standard_normal((d, R)) for d in dims]
+    pad = lambda M, d: np.vstack([M, np.zeros((d - M.shape[0], M.shape[1]))])
+    pd = [max(d, R) for d in dims]
+    a = O.cp_als_qr(None, A0, 3, kt=(lam, B))
+    b = O.cp_als_qr(None, [pad(M, d) for M, d in zip(A0, pd)], 3, kt=(lam, [pad(M, d) for M, d in zip(B, pd)]))
+    assert np.max(np.abs(np.array(a["fits"]) - np.array(b["fits"]))) <= 1e-12
+    for k in range(4):
+        assert rel(b["factors"][k][:dims[k]], a["factors"][k]) <= 1e-11, k
+        assert np.all(b["factors"][k][dims[k]:] == 0.0)
+
+
+@pytest.mark.parametrize("N,n", [(3, 7), (5, 6), (10, 3)])
+def test_sine_of_sums_rank_n_representation_closed_form(N, n):
+    """Eq. (sinsum_rkd): the rank-N Kruskal tensor equals sin(x_1 + .. + x_N)
+    entry by entry on the grid x = 2 pi i / n (and so equals the rank-2^{N-1} representation)."""
+    lam, B = O.sine_of_sums_rank_n_ktensor(N, n)
+    assert len(lam) == N and all(b.shape == (n, N) for b in B)
+    X = O.full_tensor(lam, B)
+    x = 2.0 * np.pi * np.arange(n) / n
+    idx = np.indices((n,) * N)
+    ref = np.sin(sum(x[idx[k]] for k in range(N)))
+    assert np.max(np.abs(X - ref)) <= 1e-11
