@@ -113,8 +113,14 @@ void cpqr_default_options(cpqr_options* opt);
 typedef struct cpqr_ctx cpqr_ctx;
 
 /* Create a solver for an N-way tensor of global dims[0..N-1] and CP rank R.
- * Preconditions: 2 <= N <= 8; 1 <= R <= 32; R <= dims[k] < 2^31 for all k (tall factors,
- * PAPER.md:33; reading 27); 1 <= world <= 16 and world divides dims[N-1]: with world = p > 1 the
+ * Preconditions: 2 <= N <= 10; 1 <= R <= 32; 1 <= dims[k] < 2^31.  A dense tensor needs tall
+ * factors, R <= dims[k] for all k (reading 27).  "Short modes" dims[k] < R (the
+ * 10-way sine of sums: I_k = 8 < R = 10) are accepted for Kruskal input only
+ * (cpqr_set_ktensor; cpqr_set_tensor then returns EINVAL), world = 1: the factors are stored
+ * zero-padded to R rows, V_n keeps its prod_{k != n} min(I_k, R) nonzero rows and is factored by the
+ * shifted CholeskyQR3; the factor arrays the caller passes and receives stay dims[k] x R.  V_n and
+ * its QR buffers must fit: 3 x 8 x R x max_n prod_{k != n} min(dims[k], R) bytes <= 120 GB (ENOMEM).
+ * 1 <= world <= 16 and world divides dims[N-1]: with world = p > 1 the
  * last mode is split into p equal slabs (cpqr_set_tensor), every variant (NE, QR, SVD) and both
  * Multi-TTM schedules run slab-parallel, the factors are replicated (identical on every rank).
  * Factor heights: any I_n (CholeskyQR2 for every height; its Householder fallback is the

@@ -54,6 +54,7 @@ struct CqArgs {
   const double* nX2;
   double* fit;
   unsigned hh_bit;  // flag bit of the Householder-fallback decision (0: FLAG_USE_HOUSEHOLDER)
+  double shift_c;   // > 0: shifted CholeskyQR pass (k_cq_chol1 factors G + shift_c tr(G) I, no guard)
 };
 __device__ __forceinline__ unsigned cq_hh_bit(const CqArgs& a) { return a.hh_bit ? a.hh_bit : FLAG_USE_HOUSEHOLDER; }
 
@@ -160,6 +161,14 @@ __device__ void cq_chol(const CqArgs& a, double* Gs, double* Ls, bool pass1, boo
     Gs[e] = s;
   }
   __syncthreads();
+  const bool shifted = pass1 && a.shift_c > 0.0;
+  if (shifted && tid == 0) {  // shifted CholeskyQR (Fukaya et al.): G + s I, s = c ||A||_F^2 >= c ||A||_2^2
+    double tr = 0.0;
+    for (int j = 0; j < R; ++j) tr += Gs[j + R * j];
+    const double sh = a.shift_c * tr;
+    for (int j = 0; j < R; ++j) Gs[j + R * j] += sh;
+  }
+  __syncthreads();
   if (tid < 32) {  // warp 0: left-looking Cholesky, lane i owns row i of L (R <= 32)
     bool ok = true;
     double dmax = 0.0, dmin = 1e308;
@@ -180,13 +189,25 @@ __device__ void cq_chol(const CqArgs& a, double* Gs, double* Ls, bool pass1, boo
       else if (lane > j && lane < R) Ls[j + R * lane] = (ljj > 0.0) ? s / ljj : 0.0;  // R1(j, lane)
       __syncwarp();
     }
-    if (lane == 0) *ok_out = ok && (dmin > 0.0) && (dmax / dmin < (pass1 ? kCqKappaMax : 1.0e3));
+    if (lane == 0) *ok_out = ok && (dmin > 0.0) && (shifted || dmax / dmin < (pass1 ? kCqKappaMax : 1.0e3));
   }
   for (int e = tid; e < R * R; e += blockDim.x) {
     const int r = e % R, c = e / R;
     if (r > c) Ls[e] = 0.0;
   }
   __syncthreads();
+}
+
+// First level of the Gram-partial sum for very tall panels (nb > 1024 row blocks, e.g. the
+// 10-way sine of sums' 134M-row V_n): CTA g adds blocks [g per, (g+1) per) in order; the Cholesky
+// kernels then add the <= 1024 group sums in order (fixed two-level order, deterministic).
+__global__ void k_reduce_gp(const double* __restrict__ in, int nb, int RR, int per, double* __restrict__ out) {
+  const int g = blockIdx.x, b0 = g * per, b1 = min(nb, b0 + per);
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+    double s = 0.0;
+    for (int b = b0; b < b1; ++b) s += in[(int64_t)b * RR + e];
+    out[(int64_t)g * RR + e] = s;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_cq_chol1(CqArgs a) {

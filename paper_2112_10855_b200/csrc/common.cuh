@@ -5,6 +5,9 @@
 
 #define CPQR_WARP 32
 
+// Tensor order limit of the library (N <= kMaxModes): the 10-way sine of sums.
+constexpr int kMaxModes = 10;
+
 // FP64 tensor-core MMA, D(8x8) += A(8x4) * B(4x8) (SASS DMMA.8x8x4).  tcgen05 has no f64 kind
 // on sm_100a (SURVEY.md §7 hard part 1), so the warp-level mma.sync is the FP64 tensor path.
 // Fragment ownership, lane = 4*g + t (g = lane>>2, t = lane&3):

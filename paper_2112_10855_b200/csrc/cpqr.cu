@@ -30,7 +30,7 @@ using namespace cpqr;
 
 namespace {
 
-constexpr int kMaxN = 8;
+constexpr int kMaxN = kMaxModes;
 constexpr int kMaxR = 32;
 constexpr int kMaxWorld = kMaxRanks;      // ranks (NCCL) or virtual ranks (CPQR_COMM_LOCAL)
 constexpr size_t kQSmemMax = 96 * 1024;   // Q panel budget per CTA (2 CTAs / SM)
@@ -127,11 +127,23 @@ struct cpqr_ctx {
   bool fuse_slice = true;  // see plan_mode
   bool pinv_ready = false; // M = pinv(R0) already launched for this mode (side stream, after K2)
   bool kt = false;         // Kruskal-tensor input (cpqr_set_ktensor): X never formed
+  // short modes (I_k < R, the 10-way sine of sums): the factors are stored with
+  // D_k = max(I_k, R) rows (zero rows below I_k) and dims[] holds D_k; tdims[] the true I_k.  The
+  // zero rows change nothing in CP-ALS (their rows of X are zero), their QR rows of R_k are exact
+  // zeros, and V_n keeps only its prod_{k != n} min(I_k, R) nonzero rows (mixed radix vq).
+  bool short_modes = false;
+  int64_t tdims[kMaxModes] = {0};
+  int vq[kMaxModes] = {0};  // min(I_k, R): the V_n / Q0 row radix of mode k
+  double* dVrs = nullptr;   // short modes: the shifted CholeskyQR factor R_s of V_n
+  double* dGp2 = nullptr;   // first-level sums of the Gram partials (multi-kernel CholeskyQR, nb > 1024)
+  double* dVrp = nullptr;   // short modes: R' of the CholeskyQR2 of V_n R_s^{-1}
   int ktS = 0;
   double* dKtLam = nullptr;
   double* dKtB[kMaxN] = {nullptr};
   double* dKtC = nullptr;  // cross products C_k (N blocks of up to max(R,S)^2)
   double* dKtM = nullptr;  // S x R
+  double* dKtP = nullptr;  // k_kt_m chunk partials (large V_n)
+  size_t ktP_elems = 0;
   size_t ktC_elems = 0;
   bool vn_cq = false;      // CholeskyQR2 V_n buffers allocated (some mode may use that path)
   bool vn_cq_always = false, vn_cq_tree = false, vn_mode_cq = false;  // per-mode choice (launch_kr_qr)
@@ -1274,6 +1286,18 @@ cpqr_status launch_cq_compact(cpqr_ctx* c, const CqArgs& q, int RB, int tb, cuda
 }
 
 // Multi-kernel CholeskyQR2 of the m x R column-major q.A (row blocks of 256 rows) on stream st.
+// The Cholesky kernels' view of the nb Gram partials: beyond 1024 row blocks a first level sums
+// groups of 512 blocks (k_reduce_gp) into c->dGp2, so the one-CTA Cholesky adds <= 1024 partials
+CqArgs cq_reduced(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
+  if (q.nb <= 1024) return q;
+  CqArgs r = q;
+  const int per = 512, ng = (q.nb + per - 1) / per;
+  k_reduce_gp<<<ng, 128, 0, st>>>(q.Gp, q.nb, q.R * q.R, per, c->dGp2);
+  r.Gp = c->dGp2;
+  r.nb = ng;
+  return r;
+}
+
 cpqr_status launch_cq_multi(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
   const int RB = rb_for(c->R);
   const int tb = 32 * ((q.mb + 31) / 32);
@@ -1282,9 +1306,9 @@ cpqr_status launch_cq_multi(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
 #define CQM(RBV)                                                   \
   {                                                                \
     k_cq_gram1<RBV><<<q.nb, tb, psm, st>>>(q); CKL();              \
-    k_cq_chol1<<<1, 256, 0, st>>>(q); CKL();                       \
+    k_cq_chol1<<<1, 256, 0, st>>>(cq_reduced(c, q, st)); CKL();    \
     k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 1); CKL();           \
-    k_cq_chol2<<<1, 256, 0, st>>>(q, nullptr); CKL();              \
+    k_cq_chol2<<<1, 256, 0, st>>>(cq_reduced(c, q, st), nullptr); CKL(); \
     k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 2); CKL();           \
   }
   switch (RB) { case 8: CQM(8) break; case 16: CQM(16) break; default: CQM(32) break; }
@@ -1481,6 +1505,42 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   a.use_smem = c->kr_smem > 0;
   a.flags = c->dflags;
   cudaStream_t st = c->side ? c->side : c->st;
+  if (c->short_modes) {
+    // short modes (I_k < R): V_n keeps its prod_{k != n} min(I_k, R) nonzero rows (mixed radix); no
+    // staircase K2 for them, so the QR is the shifted CholeskyQR3 (Fukaya et al.), stable up to
+    // kappa(V_n) ~ 1/eps: a shifted pass G + s I (s = 11 (J R + R (R+1)) eps ||V||_F^2) gives
+    // V = Q_s R_s with kappa(Q_s) ~ sqrt(kappa), then CholeskyQR2 of Q_s: Q0 and R0 = R' R_s.
+    int64_t J = 1;
+    for (int k = 0, m = 0; k < c->N; ++k)
+      if (k != n) { a.rad[m++] = c->vq[k]; J *= c->vq[k]; }
+    const int grid = (int)std::min<int64_t>((J * c->R + 255) / 256, (int64_t)c->sms * 8);
+    k_form_v<<<grid, 256, 0, st>>>(a, J, c->dVn);
+    CKL();
+    CqArgs q{};
+    q.A = c->dVn; q.m = (int)J; q.R = c->R; q.nb = (int)((J + 255) / 256); q.mb = (int)((J + q.nb - 1) / q.nb);
+    q.solve = 0; q.Q1 = c->dVq1; q.Gp = c->dVgp; q.innerp = c->dinnerp; q.R1 = c->dVr1; q.R2 = c->dVr2;
+    q.Q = c->dQ0; q.Qt = nullptr; q.RQ = c->RQ; q.Rn = c->dVrp; q.flags = c->dflags; q.do_fit = 0;
+    q.nX2 = c->dnX2; q.fit = c->dfit; q.hh_bit = FLAG_VN_HOUSEHOLDER;
+    q.shift_c = 11.0 * ((double)J * c->R + (double)c->R * (c->R + 1)) * 2.220446049250313e-16;
+    const int RB = rb_for(c->R), tb = 32 * ((q.mb + 31) / 32);
+    const size_t psm = (size_t)(q.mb | 1) * c->R * 8;
+    cq_multi_attrs();
+#define SHP(RBV)                                                        \
+  {                                                                     \
+    k_cq_gram1<RBV><<<q.nb, tb, psm, st>>>(q); CKL();                   \
+    k_cq_chol1<<<1, 256, 0, st>>>(cq_reduced(c, q, st)); CKL();         \
+    k_cq_apply<RBV><<<q.nb, tb, psm, st>>>(q, 1); CKL();                \
+  }
+    switch (RB) { case 8: SHP(8) break; case 16: SHP(16) break; default: SHP(32) break; }
+#undef SHP
+    CK(cudaMemcpyAsync(c->dVrs, c->dVr1, sizeof(double) * c->R * c->R, cudaMemcpyDeviceToDevice, st));
+    CqArgs q2 = q;  // CholeskyQR2 of Q_s (in dVq1); V's buffer is free scratch now
+    q2.A = c->dVq1; q2.Q1 = c->dVn; q2.shift_c = 0.0;
+    TRY(launch_cq_multi(c, q2, st));
+    k_tri_mul<<<1, 256, 0, st>>>(c->dVrp, c->dVrs, c->R, c->dR0);  // R0 = R' R_s
+    CKL();
+    return CPQR_OK;
+  }
   if (c->vn_mode_cq) {
     const int64_t J = c->vnJ;
     const int grid = (int)std::min<int64_t>((J * c->R + 255) / 256, (int64_t)c->sms * 8);
@@ -1617,6 +1677,12 @@ void trace_dump(cpqr_ctx* c) {
     fprintf(stderr, "trace %9.1f us  %s\n", 1e3 * ms, c->tev[i].second.c_str());
   }
   c->ntev = 0;
+}
+
+// k_kt_m: V_n beyond 64K rows splits its rows over chunks so ~4 CTAs per SM work
+int kt_m_chunks(const cpqr_ctx* c, int64_t J, int S) {
+  const int tiles = (S + (c->R <= 16 ? 4 : 2) - 1) / (c->R <= 16 ? 4 : 2);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)c->sms * 4 + tiles - 1) / tiles, J / 65536));
 }
 
 cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
@@ -1840,14 +1906,27 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     TRY(kt_cross(c, modes, K, Qc, c->R, Bc, c->ktS, c->dKtC));
     prof_mark(c, 0);
     if (fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-    int64_t J = 1;
-    for (int k = 0; k < N - 1; ++k) J *= c->R;
+    KtMArgs ma{};
+    ma.C = c->dKtC; ma.N1 = N - 1; ma.R = c->R; ma.S = c->ktS; ma.Q0 = c->dQ0; ma.M = c->dKtM;
+    ma.J = 1;
+    for (int k = 0, m = 0; k < N; ++k)
+      if (k != n) { ma.rad[m] = c->vq[k]; ma.J *= c->vq[k]; ++m; }
+    // V_n beyond 64K rows: split the rows over chunks so ~4 CTAs per SM work (partials in c->dPart...)
+    ma.nc = kt_m_chunks(c, ma.J, ma.S);
+    ma.P = c->dKtP;  // sized by cpqr_set_ktensor (kt_m_chunks)
+    if (ma.nc > 1 && (size_t)ma.S * ma.nc * c->R > c->ktP_elems) return fail(c, CPQR_ECUDA, "k_kt_m partials undersized");
+    const int kst = c->R <= 16 ? 4 : 2;  // kt_m_st (terms per CTA)
+    const dim3 kg((unsigned)((ma.S + kst - 1) / kst), (unsigned)ma.nc);
     switch (rb_for(c->R)) {
-      case 8: k_kt_m<8><<<c->ktS, 256, 0, c->st>>>(c->dKtC, N - 1, c->R, c->ktS, J, c->dQ0, c->dKtM); break;
-      case 16: k_kt_m<16><<<c->ktS, 256, 0, c->st>>>(c->dKtC, N - 1, c->R, c->ktS, J, c->dQ0, c->dKtM); break;
-      default: k_kt_m<32><<<c->ktS, 256, 0, c->st>>>(c->dKtC, N - 1, c->R, c->ktS, J, c->dQ0, c->dKtM); break;
+      case 8: k_kt_m<8><<<kg, 256, 0, c->st>>>(ma); break;
+      case 16: k_kt_m<16><<<kg, 256, 0, c->st>>>(ma); break;
+      default: k_kt_m<32><<<kg, 256, 0, c->st>>>(ma); break;
     }
     CKL();
+    if (ma.nc > 1) {
+      k_kt_m_reduce<<<(ma.S * c->R + 255) / 256, 256, 0, c->st>>>(c->dKtP, ma.S, c->R, ma.nc, c->dKtM);
+      CKL();
+    }
     const int grid = (int)std::min<int64_t>(((int64_t)In * c->R + 255) / 256, (int64_t)c->sms * 8);
     k_kt_w<<<grid, 256, 0, c->st>>>(c->dKtB[n], In, c->ktS, c->dKtLam, c->dKtM, c->R, c->dW);
     CKL();
@@ -1895,7 +1974,7 @@ cpqr_status direct_fit(cpqr_ctx* c) {
   double* res = c->dred + 4096;
   if (c->kt) {  // Kruskal input: the residual entry by entry from the factors (k_kt_resid)
     KtResidArgs a{};
-    for (int k = 0; k < c->N; ++k) { a.B[k] = c->dKtB[k]; a.A[k] = c->dA[k]; a.I[k] = c->dims[k]; }
+    for (int k = 0; k < c->N; ++k) { a.B[k] = c->dKtB[k]; a.A[k] = c->dA[k]; a.I[k] = c->tdims[k]; a.ld[k] = c->dims[k]; }
     a.N = c->N; a.S = c->ktS; a.R = c->R; a.lamx = c->dKtLam; a.lam = c->dlam; a.part = c->dred;
     const int grid = c->sms * 4;
     k_kt_resid<<<grid, 256, 0, c->st>>>(a);
@@ -2092,8 +2171,15 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
   if (N < 2 || N > kMaxN || R < 1 || R > kMaxR) return CPQR_EINVAL;
   if (variant < CPQR_NE || variant > CPQR_PINV) return CPQR_EINVAL;
   for (int k = 0; k < N; ++k)
-    if (dims[k] < R || dims[k] > (1ll << 31) - 1) return CPQR_EINVAL;
+    if (dims[k] < 1 || dims[k] > (1ll << 31) - 1) return CPQR_EINVAL;
   cpqr_ctx* c = new cpqr_ctx();
+  int64_t pdims[kMaxModes];  // short modes (I_k < R) are stored padded to R rows
+  for (int k = 0; k < N; ++k) {
+    c->tdims[k] = dims[k];
+    c->vq[k] = (int)std::min<int64_t>(dims[k], R);
+    pdims[k] = std::max<int64_t>(dims[k], R);
+    c->short_modes = c->short_modes || dims[k] < R;
+  }
   cpqr_default_options(&c->opt);
   if (opt) {
     if (opt->struct_size < sizeof(uint32_t) || opt->struct_size > sizeof(cpqr_options)) { delete c; return CPQR_EINVAL; }
@@ -2107,7 +2193,8 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
   if (c->opt.comm != CPQR_COMM_NCCL && c->opt.comm != CPQR_COMM_LOCAL) { delete c; return CPQR_EINVAL; }
   if (c->opt.world > 1 && (dims[N - 1] % c->opt.world) != 0) { delete c; return CPQR_EINVAL; }
   c->variant = variant;
-  cpqr_status st = create_impl(c, N, dims, R);
+  if (c->short_modes && c->opt.world > 1) { delete c; return CPQR_EINVAL; }  // Kruskal input only
+  cpqr_status st = create_impl(c, N, pdims, R);
   if (st != CPQR_OK) {
     fprintf(stderr, "cpqr_create: %s: %s\n", cpqr_status_string(st), c->err.c_str());
     cpqr_destroy(c);
@@ -2188,6 +2275,15 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   }
   int64_t J = 1;
   for (int k = 0; k < N - 1; ++k) J *= R;
+  if (c->short_modes) {  // V_n rows: prod_{k != n} min(I_k, R), the largest over the modes
+    J = 0;
+    for (int n = 0; n < N; ++n) {
+      int64_t j = 1;
+      for (int k = 0; k < N; ++k) if (k != n) j *= c->vq[k];
+      J = std::max(J, j);
+    }
+  }
+  if ((double)J * R * 8.0 * 3.0 > 120e9) return fail(c, CPQR_ENOMEM, "V_n of %lld x %d rows: Q0 and the V_n QR buffers exceed 120 GB", (long long)J, R);
   CK(dmalloc(&c->dlam, sizeof(double) * R));
   CK(dmalloc(&c->dQ0, sizeof(double) * J * R));
   CK(dmalloc(&c->dR0, sizeof(double) * R * R));
@@ -2230,8 +2326,9 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(dmalloc(&c->dflags, sizeof(unsigned) * 4));
   CK(cudaMemset(c->dflags, 0, sizeof(unsigned) * 4));
   CK(cudaMallocHost(&c->hpin, sizeof(double) * 64));
-  // staircase row order for K2: sort KB rows of R^{N-1} by (level, index)
-  {
+  // staircase row order for K2: sort KB rows of R^{N-1} by (level, index).  Short modes (mixed-radix
+  // V_n) and V_n beyond 2^28 rows use the CholeskyQR path only: no K2.
+  if (!c->short_modes && J <= (1ll << 28)) {
     std::vector<int> perm(J);
     std::vector<int> lvl(J);
     for (int64_t j = 0; j < J; ++j) {
@@ -2266,7 +2363,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     // (at world > 1 the V_n QR is replicated and must hide behind a p-times shorter pass: the
     // one-CTA K2 still does on C5 at p = 8, while C3 gains from CPQR_VN_QR=cq -- the multi-CTA
     // CholeskyQR2 cannot co-run with the stream grid and is exposed)
-    c->vn_cq_always = v ? std::string(v) == "cq" : (J * R >= 200000);
+    c->vn_cq_always = c->short_modes || !c->dperm || (v ? std::string(v) == "cq" : (J * R >= 200000));
     {  // tree modes without an X pass run the V_n QR inline (CholeskyQR2); CPQR_VN_TREE=0/1 overrides
       const char* t = getenv("CPQR_VN_TREE");
       // the one-launch cluster CholeskyQR2 (k_cq_compact) takes V_n up to 8 CTAs x 512 rows (R <= 16)
@@ -2283,7 +2380,15 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       CK(dmalloc(&c->dVgp, sizeof(double) * ((J + 255) / 256 + 1) * R * R));
       CK(dmalloc(&c->dVr1, sizeof(double) * R * R));
       CK(dmalloc(&c->dVr2, sizeof(double) * R * R));
+      if (c->short_modes) {
+        CK(dmalloc(&c->dVrs, sizeof(double) * R * R));
+        CK(dmalloc(&c->dVrp, sizeof(double) * R * R));
+      }
     }
+  }
+  {  // first-level Gram sums of the multi-kernel CholeskyQR beyond 1024 row blocks (cq_reduced)
+    const int64_t nbmax = std::max<int64_t>((imax + 255) / 256, c->vn_cq ? (J + 255) / 256 : 0);
+    if (nbmax > 1024) CK(dmalloc(&c->dGp2, sizeof(double) * ((nbmax + 511) / 512 + 1) * R * R));
   }
   if (c->opt.world > 1 && !c->local) {
     ncclUniqueId id;
@@ -2323,11 +2428,12 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->evj) cudaEventDestroy(c->evj);
   double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dSk, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred,
-                  c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2};
+                  c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2, c->dVrs, c->dVrp, c->dGp2};
   for (double* p : ps) if (p) dfree(p);
   if (c->dperm) dfree(c->dperm);
   if (c->dflags) dfree(c->dflags);
   if (c->dq0cnt) dfree(c->dq0cnt);
+  if (c->dKtP) dfree(c->dKtP);
   if (c->dSkCnt) dfree(c->dSkCnt);
   for (int k = 0; k < kMaxN; ++k) if (c->dKtB[k]) dfree(c->dKtB[k]);
   if (c->dKtLam) dfree(c->dKtLam);
@@ -2378,6 +2484,8 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
   if (!c || !x) return c ? fail(c, CPQR_EINVAL, "null tensor") : CPQR_EINVAL;
   if (mem != CPQR_MEM_HOST && mem != CPQR_MEM_DEVICE_COPY && mem != CPQR_MEM_DEVICE_BORROW)
     return fail(c, CPQR_EINVAL, "bad mem kind %d", mem);
+  if (c->short_modes)
+    return fail(c, CPQR_EINVAL, "a dense tensor needs I_k >= R in every mode (short modes: Kruskal input only)");
   // which slabs [b, e) covers: this rank's, or (virtual ranks) one rank's or all of them
   int q0 = -1, q1 = -1;
   if (c->local && b == 0 && e == c->dims[c->N - 1]) {
@@ -2468,8 +2576,26 @@ CPQR_API cpqr_status cpqr_set_ktensor(cpqr_ctx* c, int S, const double* lam, con
     CK(dmalloc(&c->dKtC, sizeof(double) * c->ktC_elems));
     c->ktS = S;
   }
-  for (int k = 0; k < N; ++k)
-    CK(cudaMemcpyAsync(c->dKtB[k], B[k], sizeof(double) * c->dims[k] * S, cudaMemcpyHostToDevice, c->st));
+  {  // k_kt_m chunk partials of the largest V_n (never allocated inside a graph capture)
+    size_t need = 0;
+    for (int n = 0; n < N; ++n) {
+      int64_t J = 1;
+      for (int k = 0; k < N; ++k) if (k != n) J *= c->vq[k];
+      const int nc = kt_m_chunks(c, J, S);
+      if (nc > 1) need = std::max(need, (size_t)S * nc * R);
+    }
+    if (need > c->ktP_elems) {
+      if (c->dKtP) dfree(c->dKtP);
+      c->dKtP = nullptr;
+      CK(dmalloc(&c->dKtP, sizeof(double) * need));
+      c->ktP_elems = need;
+    }
+  }
+  for (int k = 0; k < N; ++k) {  // (short modes: I_k rows of the max(I_k, R)-row zero-padded array)
+    if (c->tdims[k] != c->dims[k]) CK(cudaMemsetAsync(c->dKtB[k], 0, sizeof(double) * c->dims[k] * S, c->st));
+    CK(cudaMemcpy2DAsync(c->dKtB[k], sizeof(double) * c->dims[k], B[k], sizeof(double) * c->tdims[k],
+                         sizeof(double) * c->tdims[k], S, cudaMemcpyHostToDevice, c->st));
+  }
   std::vector<double> ones(S, 1.0);
   CK(cudaMemcpyAsync(c->dKtLam, lam ? lam : ones.data(), sizeof(double) * S, cudaMemcpyHostToDevice, c->st));
   int modes[kMaxN];
@@ -2498,7 +2624,13 @@ static cpqr_status upload_factors(cpqr_ctx* c, const double* const* A, const dou
       if (k != 0) return fail(c, CPQR_EINVAL, "A[%d] is NULL", k);
       continue;
     }
-    CK(cudaMemcpyAsync(c->dA[k], A[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
+    if (c->tdims[k] == c->dims[k]) {
+      CK(cudaMemcpyAsync(c->dA[k], A[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
+    } else {  // a short mode: I_k rows into the zero-padded max(I_k, R)-row array
+      CK(cudaMemsetAsync(c->dA[k], 0, sizeof(double) * c->dims[k] * R, c->st));
+      CK(cudaMemcpy2DAsync(c->dA[k], sizeof(double) * c->dims[k], A[k], sizeof(double) * c->tdims[k],
+                           sizeof(double) * c->tdims[k], R, cudaMemcpyHostToDevice, c->st));
+    }
     if (ne_family(c->variant)) {
       k_gram<<<1, 1024, 0, c->st>>>(c->dA[k], (int)c->dims[k], R, c->dG[k]);
       CKL();
@@ -2529,7 +2661,7 @@ CPQR_API cpqr_status cpqr_init_factors(cpqr_ctx* c, uint64_t seed) {
   std::vector<const double*> p(c->N);
   uint64_t ctr = 0;
   for (int k = 0; k < c->N; ++k) {
-    h[k].resize(c->dims[k] * c->R);
+    h[k].resize(c->tdims[k] * c->R);
     for (auto& v : h[k]) v = normal_at(seed, ctr++);
     p[k] = h[k].data();
   }
@@ -2603,7 +2735,9 @@ CPQR_API cpqr_status cpqr_get_factors(cpqr_ctx* c, double* const* A_out, double*
   TRY(begin_call(c));
   if (A_out)
     for (int k = 0; k < c->N; ++k)
-      if (A_out[k]) CK(cudaMemcpyAsync(A_out[k], c->dA[k], sizeof(double) * c->dims[k] * c->R, cudaMemcpyDeviceToHost, c->st));
+      if (A_out[k])
+        CK(cudaMemcpy2DAsync(A_out[k], sizeof(double) * c->tdims[k], c->dA[k], sizeof(double) * c->dims[k],
+                             sizeof(double) * c->tdims[k], c->R, cudaMemcpyDeviceToHost, c->st));
   if (lam) CK(cudaMemcpyAsync(lam, c->dlam, sizeof(double) * c->R, cudaMemcpyDeviceToHost, c->st));
   return end_call(c);
 }

@@ -11,7 +11,7 @@
 
 namespace cpqr {
 
-constexpr int kKtMaxModes = 8;
+constexpr int kKtMaxModes = kMaxModes;
 
 struct KtCrossArgs {
   const double* P[kKtMaxModes];  // I_k x np, column-major
@@ -38,38 +38,88 @@ __global__ void __launch_bounds__(256) k_kt_cross(KtCrossArgs a) {
   if (lane == 0) a.out[k * per + e] = s;
 }
 
-// M(s, r) = sum_j Q0(j, r) prod_m C_m(j_m, s), j = sum_m j_m R^m (C_m: R x S block m of C).
-// One CTA per term s; threads stride over the J = R^{N1} rows; per-warp then per-CTA sums in order.
+// M(s, r) = sum_j Q0(j, r) prod_m C_m(j_m, s), j = sum_m j_m prod_{m' < m} rad_m' (C_m: R x S block
+// m of C; rad_m = R, or min(I_k, R) for a short mode, whose C_m rows beyond it are zero).  CTA (s,
+// ch) covers rows [ch J / NC, (ch+1) J / NC); threads stride over them; per-warp then per-CTA sums in
+// order.  NC = 1 writes M directly; NC > 1 (V_n of 10^5+ rows, e.g. the 10-way sine of sums' 8^9)
+// writes slot P[(s NC + ch) R + r], summed in chunk order by k_kt_m_reduce.
+struct KtMArgs {
+  const double* C;
+  int N1, R, S, nc;
+  int64_t J;
+  int rad[kMaxModes];
+  const double* Q0;
+  double* M;
+  double* P;
+};
 template <int RB>
-__global__ void __launch_bounds__(256) k_kt_m(const double* __restrict__ C, int N1, int R, int S, int64_t J,
-                                              const double* __restrict__ Q0, double* __restrict__ M) {
-  __shared__ double red[8][RB];
-  const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  double acc[RB];
+__host__ __device__ constexpr int kt_m_st() { return RB <= 16 ? 4 : 2; }  // terms s per CTA (register budget)
+template <int RB>
+__global__ void __launch_bounds__(256) k_kt_m(KtMArgs a) {
+  // CTA (s-tile, chunk): ST terms s share each pass over Q0's rows (Q0 is read S / ST times, not S);
+  // rows go by groups of r0 = rad_0 (the fastest factor's digit), whose slow-factor product is
+  // formed once per group and term
+  constexpr int ST = kt_m_st<RB>();
+  __shared__ double red[8][ST][RB];
+  const int s0 = blockIdx.x * ST, ch = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  const int R = a.R, S = a.S, r0 = a.rad[0];
+  const int64_t JG = a.J / r0;
+  const int64_t g0 = JG * ch / a.nc, g1 = JG * (ch + 1) / a.nc;
+  double acc[ST][RB];
 #pragma unroll
-  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
-  for (int64_t j = tid; j < J; j += blockDim.x) {
-    int64_t x = j;
-    double p = 1.0;
-    for (int m = 0; m < N1; ++m) {
-      const int jm = (int)(x % R);
-      x /= R;
-      p *= C[(int64_t)m * R * S + jm + (int64_t)R * s];
+  for (int u = 0; u < ST; ++u)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[u][r] = 0.0;
+  for (int64_t grp = g0 + tid; grp < g1; grp += blockDim.x) {
+    double hi[ST];
+#pragma unroll
+    for (int u = 0; u < ST; ++u) hi[u] = 1.0;
+    int64_t x = grp;
+    for (int m = 1; m < a.N1; ++m) {
+      const int rm = a.rad[m];
+      const int jm = (int)(x % rm);
+      x /= rm;
+#pragma unroll
+      for (int u = 0; u < ST; ++u)
+        if (s0 + u < S) hi[u] *= a.C[(int64_t)m * R * S + jm + (int64_t)R * (s0 + u)];
     }
+    const int64_t j0 = grp * r0;
+    for (int i0 = 0; i0 < r0; ++i0) {
+      double q[RB];
 #pragma unroll
-    for (int r = 0; r < RB; ++r)
-      if (r < R) acc[r] = fma(p, Q0[j + J * r], acc[r]);
+      for (int r = 0; r < RB; ++r) q[r] = (r < R) ? a.Q0[j0 + i0 + a.J * r] : 0.0;
+#pragma unroll
+      for (int u = 0; u < ST; ++u) {
+        const double p = (s0 + u < S) ? a.C[i0 + (int64_t)R * (s0 + u)] * hi[u] : 0.0;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[u][r] = fma(p, q[r], acc[u][r]);
+      }
+    }
   }
 #pragma unroll
-  for (int r = 0; r < RB; ++r) {
-    const double v = warp_sum(acc[r]);
-    if (lane == 0) red[wid][r] = v;
-  }
+  for (int u = 0; u < ST; ++u)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const double v = warp_sum(acc[u][r]);
+      if (lane == 0) red[wid][u][r] = v;
+    }
   __syncthreads();
-  if (tid < R) {
+  for (int e = tid; e < ST * R; e += blockDim.x) {
+    const int u = e / R, r = e - u * R, s = s0 + u;
+    if (s >= S) continue;
     double t = 0.0;
-    for (int w = 0; w < nw; ++w) t += red[w][tid];
-    M[s + (int64_t)S * tid] = t;
+    for (int w = 0; w < nw; ++w) t += red[w][u][r];
+    if (a.nc == 1) a.M[s + (int64_t)S * r] = t;
+    else a.P[((int64_t)s * a.nc + ch) * R + r] = t;
+  }
+}
+__global__ void k_kt_m_reduce(const double* __restrict__ P, int S, int R, int nc, double* __restrict__ M) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < S * R; e += gridDim.x * blockDim.x) {
+    const int s = e / R, r = e - s * R;
+    double t = 0.0;
+    for (int ch = 0; ch < nc; ++ch) t += P[((int64_t)s * nc + ch) * R + r];
+    M[s + (int64_t)S * r] = t;
   }
 }
 
@@ -109,9 +159,10 @@ __global__ void k_kt_mttkrp(const double* __restrict__ Bn, int64_t In, int S, co
 // difference is formed before squaring, so the relative error resolves down to ~eps (the fast fit
 // ||X||^2 - 2 <X, Xh> + ||Xh||^2 cancels to ~sqrt(eps)).  Fixed-order partials.
 struct KtResidArgs {
-  const double* B[kKtMaxModes];  // I_k x S
-  const double* A[kKtMaxModes];  // I_k x R (normalised factors)
-  int64_t I[kKtMaxModes];
+  const double* B[kKtMaxModes];  // I_k x S (leading dimension ld[k])
+  const double* A[kKtMaxModes];  // I_k x R (normalised factors, leading dimension ld[k])
+  int64_t I[kKtMaxModes];        // extents (the true I_k)
+  int64_t ld[kKtMaxModes];       // row counts of the stored arrays (max(I_k, R) for short modes)
   int N, S, R;
   const double* lamx;            // S
   const double* lam;             // R
@@ -135,15 +186,15 @@ __global__ void __launch_bounds__(256) k_kt_resid(KtResidArgs a) {
       for (int k = 1; k < a.N; ++k) {
         const int64_t ik = x % a.I[k];
         x /= a.I[k];
-        v *= isx ? a.B[k][ik + a.I[k] * q] : a.A[k][ik + a.I[k] * q];
+        v *= isx ? a.B[k][ik + a.ld[k] * q] : a.A[k][ik + a.ld[k] * q];
       }
       pw[wid][s] = v;
     }
     __syncwarp();
     for (int64_t i1 = lane; i1 < a.I[0]; i1 += 32) {
       double d = 0.0;
-      for (int s = 0; s < a.S; ++s) d = fma(a.B[0][i1 + a.I[0] * s], pw[wid][s], d);
-      for (int r = 0; r < a.R; ++r) d = fma(a.A[0][i1 + a.I[0] * r], pw[wid][a.S + r], d);
+      for (int s = 0; s < a.S; ++s) d = fma(a.B[0][i1 + a.ld[0] * s], pw[wid][s], d);
+      for (int r = 0; r < a.R; ++r) d = fma(a.A[0][i1 + a.ld[0] * r], pw[wid][a.S + r], d);
       acc = fma(d, d, acc);
     }
     __syncwarp();

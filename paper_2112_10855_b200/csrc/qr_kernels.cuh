@@ -418,17 +418,24 @@ __global__ void __launch_bounds__(512) k_tsqr_qform(TsqrArgs a) {
 // line 6) formed densely: V(j, c) = prod_m R_{k_m}(j_m, c), j = sum_m j_m R^m (the
 // Kolda-Bader row order of K2's Q0).  Used by the multi-CTA CholeskyQR2 V_n QR (high rank).
 __global__ void k_form_v(KrQrArgs a, int64_t J, double* __restrict__ V) {
+  // one thread per (column c, group of r0 rows sharing digits 1..N1-1): the product over the slow
+  // factors once per group, then the r0 rows of the fastest factor (r0 = its radix)
   const int R = a.R;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < J * R; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e / J);
-    int64_t j = e - (int64_t)c * J;
-    double v = 1.0;
-    for (int m = 0; m < a.N1; ++m) {
-      const int im = (int)(j % R);
-      j /= R;
-      v *= (im <= c) ? a.Rk[m][im + R * c] : 0.0;
+  const int r0 = a.rad[0] ? a.rad[0] : R;  // mixed radix: short modes keep their min(I_k, R) rows
+  const int64_t JG = J / r0;                // groups per column
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < JG * R; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / JG);
+    const int64_t grp = e - (int64_t)c * JG;
+    int64_t j = grp;
+    double hi = 1.0;
+    for (int m = 1; m < a.N1; ++m) {
+      const int rm = a.rad[m] ? a.rad[m] : R;
+      const int im = (int)(j % rm);
+      j /= rm;
+      hi *= (im <= c) ? a.Rk[m][im + R * c] : 0.0;
     }
-    V[e] = v;
+    double* out = V + (int64_t)c * J + grp * r0;
+    for (int i0 = 0; i0 < r0; ++i0) out[i0] = (i0 <= c) ? a.Rk[0][i0 + R * c] * hi : 0.0;
   }
 }
 
@@ -524,7 +531,7 @@ __global__ void __launch_bounds__(512) k_svd_pinv(const double* __restrict__ R0,
 // routine returns U Sigma^+ V^T = (S^+)^T = S^+ (S symmetric), dropping sigma_i <= tau sigma_max
 // (reading 32).  Depends on the Grams only, so it runs on the side stream beside the MTTKRP.
 struct NePinvArgs {
-  const double* G[8];
+  const double* G[kMaxModes];
   int N, n, R;
   double tau;
   double* Mout;

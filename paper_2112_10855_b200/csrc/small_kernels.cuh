@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(1024) k_tall_fallback(TallArgs a) {
 // packed at offset off_c.  Householder needs no fill-in and Q0 has the same
 // support.  One CTA; `work` is shared memory when the packed matrix fits, else global scratch.
 struct KrQrArgs {
-  const double* Rk[8];  // retained triangular factors, R x R column-major, ascending mode
+  const double* Rk[kMaxModes];  // retained triangular factors, R x R column-major, ascending mode
   int N1;               // N - 1
   int R;
   const int* perm;      // sorted position -> KB row (R^{N1})
@@ -272,6 +272,7 @@ struct KrQrArgs {
   int use_smem;
   unsigned* flags;
   unsigned gate_bit;    // != 0: run only if this flag bit is set (fallback of the CholeskyQR2 V_n QR)
+  int rad[kMaxModes];   // k_form_v: row radix of factor m (min(I_k, R) for short modes; 0 = R)
 };
 
 // ------------------------------------------------------------------------- K4: Q0 apply
@@ -448,7 +449,7 @@ __device__ int jacobi_pinv(const double* R0, int R, double tau, double* Bs, doub
 struct DiagArgs {
   const double* T;
   int nd;
-  int64_t dims[8];
+  int64_t dims[kMaxModes];
   int k, rm;
   const double* Ak;
   int64_t lda;
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(256) k_diag_contract(DiagArgs a) {
 struct TailNeArgs {
   const double* M;        // In x R, layout given by m_rowmajor
   int m_rowmajor;
-  const double* G[8];     // Grams (R x R), index k; G[n] ignored
+  const double* G[kMaxModes];  // Grams (R x R), index k; G[n] ignored
   int N, n, In, R;
   double* A;              // out: normalised factor (column-major)
   double* Gn;             // out: new Gram of mode n
@@ -705,6 +706,17 @@ __global__ void __launch_bounds__(kNeThreads) k_tail_ne(TailNeArgs a) {
 }
 
 // Gram G = A^T A (warp per entry) for set_factors in the NE variant.
+// C = A B for upper-triangular R x R A, B (column-major; one CTA): the shifted CholeskyQR3's
+// R0 = R' R_s (short modes, launch_kr_qr).
+__global__ void k_tri_mul(const double* __restrict__ A, const double* __restrict__ B, int R, double* __restrict__ C) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int r = e % R, c = e / R;
+    double s = 0.0;
+    for (int k = r; k <= c; ++k) s = fma(A[r + R * k], B[k + R * c], s);
+    C[e] = (r <= c) ? s : 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_gram(const double* __restrict__ A, int In, int R, double* __restrict__ G) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int e = wid; e < R * R; e += nw) {
@@ -722,10 +734,10 @@ struct ResidArgs {
   const double* X;
   int64_t n;           // local numel
   int N;
-  int64_t dims[8];     // local dims
+  int64_t dims[kMaxModes];     // local dims
   int64_t off_last;    // global offset of the slab on the last mode
-  const double* A[8];  // global factors (column-major, lda = global I_k)
-  int64_t lda[8];
+  const double* A[kMaxModes];  // global factors (column-major, lda = global I_k)
+  int64_t lda[kMaxModes];
   const double* lam;
   int R;
   double* part;
@@ -734,7 +746,7 @@ __global__ void k_resid_partial(ResidArgs a) {
   __shared__ double red[32];
   double s = 0.0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < a.n; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t idx[8];
+    int64_t idx[kMaxModes];
     int64_t rem = e;
     for (int k = 0; k < a.N; ++k) { idx[k] = rem % a.dims[k]; rem /= a.dims[k]; }
     idx[a.N - 1] += a.off_last;

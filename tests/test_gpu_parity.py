@@ -141,8 +141,14 @@ def test_direct_fit_and_torch_borrow(cp):
 
 
 def test_errors_are_reported(cp):
+    # wide factors (I_k < R, reading 27) are accepted for Kruskal input only (short modes, the
+    # 10-way sine of sums): a dense tensor is rejected
+    w = cp.CPQR((4, 4, 4), 8, "QR")
     with pytest.raises(cp.CpqrError):
-        cp.CPQR((4, 4, 4), 8, "QR")          # wide factors (reading 27)
+        w.set_tensor(np.zeros((4, 4, 4)))
+    w.close()
+    with pytest.raises(cp.CpqrError):
+        cp.CPQR((4,) * 11, 2, "QR")           # N > 10
     s = cp.CPQR((10, 10, 10), 2, "QR")
     with pytest.raises(cp.CpqrError) as e:
         s.sweep(1)                           # no tensor yet
@@ -1171,3 +1177,57 @@ def test_cost_accounting_matches_oracle_ttm_cost(cp, dims, R, tree):
     s.close()
     assert passes == (2 if tree else N)
     assert p["flops0"] == first and p["bytes0"] == passes * 8.0 * np.prod(dims)
+
+
+def _kt_oracle(variant, lam, B, A0, sweeps, fit_mode="fast"):
+    if variant in ("QR", "SVD"):
+        return O.cp_als_qr(None, A0, sweeps, variant=variant, kt=(lam, B), fit_mode=fit_mode)
+    return O.cp_als_ne(None, A0, sweeps, solve="pinv" if variant == "PINV" else "chol", kt=(lam, B),
+                       fit_mode=fit_mode)
+
+
+@pytest.mark.parametrize("variant", ["QR", "SVD", "NE", "PINV"])
+@pytest.mark.parametrize("dims,R,S", [((3, 5, 4, 6), 5, 6), ((3,) * 10, 4, 5), ((4,) * 10, 5, 3)])
+def test_short_modes_kruskal(cp, dims, R, S, variant):
+    """Short modes I_k < R with Kruskal input (the 10-way sine of sums has I_k = 8 < R = 10,
+    PAPER.md:630-645), N up to 10: the library stores such factors zero-padded to R rows (pinned on
+    the oracle: test_short_modes_zero_padding_is_exact), keeps V_n's prod min(I_k, R) nonzero rows
+    and factors it by the shifted CholeskyQR3; against the oracle's economy-QR run: factors <= 1e-9
+    after one sweep, fits within 1e-8 over three.  (4,)*10 has a 262144-row V_n (chunked M)."""
+    g = np.random.default_rng(len(dims) * 100 + R)
+    lam = g.standard_normal(S)
+    B = [g.standard_normal((d, S)) for d in dims]
+    A0 = [g.standard_normal((d, R)) for d in dims]
+    s = cp.CPQR(dims, R, variant)
+    s.set_ktensor(lam, B)
+    s.set_factors(A0)
+    f1 = s.sweep(1)
+    lam1, A = s.get_factors()
+    f = np.concatenate([f1, s.sweep(2)])
+    s.close()
+    ref1, ref = _kt_oracle(variant, lam, B, A0, 1), _kt_oracle(variant, lam, B, A0, 3)
+    for k in range(len(dims)):
+        assert A[k].shape == (dims[k], R)
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    assert rel(lam1, ref1["lam"]) <= 1e-9
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (f, ref["fits"])
+
+
+def test_short_modes_direct_fit_and_errors(cp):
+    """Short modes: the DIRECT relative error iterates the true I_k (not the padded
+    rows) and matches the oracle; a dense tensor is rejected (EINVAL: short modes need Kruskal
+    input)."""
+    dims, R, S = (3, 6, 4, 5), 5, 4
+    g = np.random.default_rng(77)
+    lam = g.standard_normal(S)
+    B = [g.standard_normal((d, S)) for d in dims]
+    A0 = [g.standard_normal((d, R)) for d in dims]
+    s = cp.CPQR(dims, R, "QR", fit_mode="direct")
+    with pytest.raises(cp.CpqrError):
+        s.set_tensor(np.zeros(dims[::-1]))
+    s.set_ktensor(lam, B)
+    s.set_factors(A0)
+    f = s.sweep(3)
+    s.close()
+    ref = _kt_oracle("QR", lam, B, A0, 3, fit_mode="direct")
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-10, (f, ref["fits"])
