@@ -1915,8 +1915,10 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     ma.nc = kt_m_chunks(c, ma.J, ma.S);
     ma.P = c->dKtP;  // sized by cpqr_set_ktensor (kt_m_chunks)
     if (ma.nc > 1 && (size_t)ma.S * ma.nc * c->R > c->ktP_elems) return fail(c, CPQR_ECUDA, "k_kt_m partials undersized");
-    const int kst = c->R <= 16 ? 4 : 2;  // kt_m_st (terms per CTA)
-    const dim3 kg((unsigned)((ma.S + kst - 1) / kst), (unsigned)ma.nc);
+    // terms per CTA: kt_m_st when V_n is chunked (Q0 re-read S / st times), else one term per CTA
+    // (a small V_n: more CTAs beat fewer passes)
+    ma.st = ma.nc > 1 ? (c->R <= 16 ? 4 : 2) : 1;
+    const dim3 kg((unsigned)((ma.S + ma.st - 1) / ma.st), (unsigned)ma.nc);
     switch (rb_for(c->R)) {
       case 8: k_kt_m<8><<<kg, 256, 0, c->st>>>(ma); break;
       case 16: k_kt_m<16><<<kg, 256, 0, c->st>>>(ma); break;

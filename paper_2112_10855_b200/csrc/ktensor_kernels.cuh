@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) k_kt_cross(KtCrossArgs a) {
 struct KtMArgs {
   const double* C;
   int N1, R, S, nc;
+  int st;  // terms per CTA (<= kt_m_st): kt_m_st for a chunked (large) V_n, 1 for a small one
   int64_t J;
   int rad[kMaxModes];
   const double* Q0;
@@ -61,7 +62,8 @@ __global__ void __launch_bounds__(256) k_kt_m(KtMArgs a) {
   // formed once per group and term
   constexpr int ST = kt_m_st<RB>();
   __shared__ double red[8][ST][RB];
-  const int s0 = blockIdx.x * ST, ch = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int s0 = blockIdx.x * a.st, ch = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int send = min(a.S, s0 + a.st);
   const int nw = blockDim.x >> 5;
   const int R = a.R, S = a.S, r0 = a.rad[0];
   const int64_t JG = a.J / r0;
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(256) k_kt_m(KtMArgs a) {
       x /= rm;
 #pragma unroll
       for (int u = 0; u < ST; ++u)
-        if (s0 + u < S) hi[u] *= a.C[(int64_t)m * R * S + jm + (int64_t)R * (s0 + u)];
+        if (s0 + u < send) hi[u] *= a.C[(int64_t)m * R * S + jm + (int64_t)R * (s0 + u)];
     }
     const int64_t j0 = grp * r0;
     for (int i0 = 0; i0 < r0; ++i0) {
@@ -91,7 +93,8 @@ __global__ void __launch_bounds__(256) k_kt_m(KtMArgs a) {
       for (int r = 0; r < RB; ++r) q[r] = (r < R) ? a.Q0[j0 + i0 + a.J * r] : 0.0;
 #pragma unroll
       for (int u = 0; u < ST; ++u) {
-        const double p = (s0 + u < S) ? a.C[i0 + (int64_t)R * (s0 + u)] * hi[u] : 0.0;
+        if (s0 + u >= send) continue;
+        const double p = a.C[i0 + (int64_t)R * (s0 + u)] * hi[u];
 #pragma unroll
         for (int r = 0; r < RB; ++r) acc[u][r] = fma(p, q[r], acc[u][r]);
       }
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(256) k_kt_m(KtMArgs a) {
   __syncthreads();
   for (int e = tid; e < ST * R; e += blockDim.x) {
     const int u = e / R, r = e - u * R, s = s0 + u;
-    if (s >= S) continue;
+    if (s >= send) continue;
     double t = 0.0;
     for (int w = 0; w < nw; ++w) t += red[w][u][r];
     if (a.nc == 1) a.M[s + (int64_t)S * r] = t;
