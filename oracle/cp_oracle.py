@@ -28,7 +28,8 @@ FLAG_SVD_TRUNCATED = 4
 __all__ = [
     "EPS", "FLAG_ILLCOND_R0", "FLAG_NE_CHOL_FALLBACK", "FLAG_SVD_TRUNCATED",
     "as_tensor", "kron", "khatri_rao", "hadamard", "matricize", "tensorize", "ttm",
-    "multi_ttm", "ttm_order", "qr_pos", "kr_of_triangular", "structured_qr", "apply_q0",
+    "multi_ttm", "ttm_order", "qr_pos", "kr_of_triangular", "structured_qr", "kr_group_qr",
+    "vn_tree_groups", "tree_qr", "apply_q0",
     "solve_qr", "solve_svd", "pinv_svd", "normalize", "full_tensor", "fit_fast_qr", "fit_fast_ne",
     "fit_direct", "mode_update_qr", "mode_update_ne", "cp_als_qr", "cp_als_ne",
     "qr_cost", "ttm_cost", "mttkrp", "ktensor_norm2", "w_ktensor", "mttkrp_ktensor",
@@ -143,6 +144,50 @@ def kr_of_triangular(Rs, n: int) -> np.ndarray:
 def structured_qr(Rs, n: int):
     """Q0, R0 = QR(V_n), dense (Alg. 2 line 7; PAPER.md:314 treats V_n dense)."""
     return qr_pos(kr_of_triangular(Rs, n))
+
+
+def kr_group_qr(Rg):
+    """QR of the Khatri-Rao product of a group of triangular factors, Rg = [R_a, R_b, ...] in the
+    product's order (R_a slowest), by a chain of pairwise QRs (the tree across the Khatri-Rao
+    factors of PAPER.md:479).  With (A C) (.) (B D) = (A (x) B)(C (.) D) (Eq. (2.1),
+    PAPER.md:97-100): start from P = I, S = (the fastest factor); for each next-slower
+    factor R_k, QR(R_k (.) S) = Q S' gives R_k (.) (P S) = (I (x) P) Q S', so P <- (I (x) P) Q,
+    S <- S'.  Returns (P, S): the group's product = P S, P orthonormal, S upper triangular with
+    diag >= 0.  A one-factor group returns (I, R_k) (R_k is already triangular).  A short mode
+    (I_k < R) contributes its min(I_k, R) x R trapezoidal R_k (economy QR, reading 34)."""
+    P, S = np.eye(Rg[-1].shape[0]), Rg[-1]
+    for Rk in reversed(Rg[:-1]):
+        Qm, S = qr_pos(khatri_rao([Rk, S]))
+        P = kron(np.eye(Rk.shape[0]), P) @ Qm
+    return P, S
+
+
+def vn_tree_groups(N: int, n: int):
+    """The two factor groups of V_n in the tree QR (reading 36): the modes are split at
+    h = ceil(N/2) as in the dimension tree; the retained modes of the half that
+    does not hold n form a group shared by every mode of the other half (their R_k do not change
+    between those modes in a sweep), the rest of n's own half the other group.  Both in decreasing
+    mode order (the Khatri-Rao order of V_n).  Returns (hi, lo): V_n = [(.) hi] (.) [(.) lo]."""
+    h = (N + 1) // 2
+    hi = [k for k in range(N - 1, h - 1, -1) if k != n]
+    lo = [k for k in range(h - 1, -1, -1) if k != n]
+    return hi, lo
+
+
+def tree_qr(Rs, n: int):
+    """Q0, R0 = QR(V_n) by a tree across the Khatri-Rao factors (SURVEY.md 8(f)
+    NEXT-2): each group of vn_tree_groups is reduced by kr_group_qr to (P_g, S_g), then the root
+    QR(S_hi (.) S_lo) = Q_r R0 and Q0 = (P_hi (x) P_lo) Q_r, since
+    V_n = (P_hi S_hi) (.) (P_lo S_lo) = (P_hi (x) P_lo)(S_hi (.) S_lo) (Eq. (2.1)).  Equal to the
+    dense QR of V_n (structured_qr) up to rounding: the thin QR with diag(R0) > 0 is unique."""
+    hi, lo = vn_tree_groups(len(Rs), n)
+    if not hi or not lo:                      # N = 2: one retained factor
+        g = hi or lo
+        return kr_group_qr([Rs[k] for k in g])
+    P_hi, S_hi = kr_group_qr([Rs[k] for k in hi])
+    P_lo, S_lo = kr_group_qr([Rs[k] for k in lo])
+    Q_r, R0 = qr_pos(khatri_rao([S_hi, S_lo]))
+    return kron(P_hi, P_lo) @ Q_r, R0
 
 
 def apply_q0(Y: np.ndarray, n: int, Q0: np.ndarray) -> np.ndarray:

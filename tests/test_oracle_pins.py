@@ -171,6 +171,66 @@ def test_structured_qr_eq_Z_qr(dims):
         assert rel(R0, Rz) <= 1e-12
 
 
+def test_vn_tree_groups_partition_and_sharing():
+    # reading 36: hi and lo partition the retained modes {k != n}, each in decreasing (Khatri-Rao)
+    # order, hi above lo; the group of the other half is the same for every mode of a half
+    for N in range(2, 11):
+        h = (N + 1) // 2
+        for n in range(N):
+            hi, lo = O.vn_tree_groups(N, n)
+            assert sorted(hi + lo) == [k for k in range(N) if k != n]
+            assert hi + lo == sorted(hi + lo, reverse=True)
+            if n < h:
+                assert hi == list(range(N - 1, h - 1, -1))            # shared by modes 0..h-1
+            else:
+                assert lo == list(range(h - 1, -1, -1))               # shared by modes h..N-1
+
+
+@pytest.mark.parametrize("N,R", [(3, 3), (4, 3), (4, 5), (5, 3), (6, 2)])
+def test_kr_group_qr_bruteforce_product(N, R):
+    # P S = Khatri-Rao of the group, formed here entry by entry from PAPER.md:95's column rule
+    # V(j, c) = prod_m R_m(j_m, c) (last factor fastest); P orthonormal, S upper triangular, diag >= 0
+    _, _, Rs = _setup_factors((7,) * N, R)
+    P, S = O.kr_group_qr(Rs)
+    V = np.zeros((R ** N, R))
+    for idx in itertools.product(range(R), repeat=N):       # idx[0] slowest
+        j = 0
+        for i in idx:
+            j = j * R + i
+        for c in range(R):
+            V[j, c] = np.prod([Rs[m][idx[m], c] for m in range(N)])
+    assert rel(P @ S, V) <= 1e-13
+    assert np.linalg.norm(P.T @ P - np.eye(R)) <= 1e-13
+    assert np.allclose(np.tril(S, -1), 0) and np.all(np.diag(S) >= 0)
+    P1, S1 = O.kr_group_qr(Rs[:1])                          # one factor: (I, R_k)
+    assert np.array_equal(P1, np.eye(R)) and np.array_equal(S1, Rs[0])
+
+
+@pytest.mark.parametrize("dims,R", [((6, 5), 3), ((6, 5, 4), 3), ((5, 4, 3, 4), 4), ((3, 4, 3, 3, 4), 3),
+                                    ((4, 4, 4, 4, 4, 4), 2), ((9, 9, 9, 9), 8)])
+def test_tree_qr_equals_lapack_qr_of_vn(dims, R):
+    # the tree QR across the Khatri-Rao factors reaches the thin QR of V_n, unique
+    # under diag(R0) > 0 (reading 6): equal to LAPACK's QR of the explicitly formed V_n up to rounding
+    N = len(dims)
+    _, _, Rs = _setup_factors(dims, R)
+    for n in range(N):
+        V = O.kr_of_triangular(Rs, n)
+        Q0, R0 = O.tree_qr(Rs, n)
+        Qd, Rd = np.linalg.qr(V, mode="reduced")
+        s = np.sign(np.diag(Rd))
+        Qd, Rd = Qd * s[None, :], Rd * s[:, None]
+        assert rel(R0, Rd) <= 1e-12 and rel(Q0, Qd) <= 1e-11
+        assert rel(Q0 @ R0, V) <= 1e-13
+        assert np.linalg.norm(Q0.T @ Q0 - np.eye(R)) <= 1e-13
+        # Q0 keeps V_n's staircase support: zero where the row level > column
+        rad = [Rs[k].shape[0] for k in range(N) if k != n]      # fastest factor first
+        for j in range(V.shape[0]):
+            lvl, t = 0, j
+            for r in rad:
+                lvl, t = max(lvl, t % r), t // r
+            assert np.all(np.abs(Q0[j, :lvl]) <= 1e-13)
+
+
 def test_structured_qr_identity_gives_selection_and_staircase_support():
     R, N = 3, 4
     Q0, R0 = O.structured_qr([np.eye(R)] * N, 0)
