@@ -11,6 +11,7 @@
 #include "ktensor_kernels.cuh"
 #include "batched_kernels.cuh"
 #include "small_ttm.cuh"
+#include "vn_tree.cuh"
 
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -148,6 +149,11 @@ struct cpqr_ctx {
   bool vn_cq = false;      // CholeskyQR2 V_n buffers allocated (some mode may use that path)
   bool vn_cq_always = false, vn_cq_tree = false, vn_mode_cq = false;  // per-mode choice (launch_kr_qr)
   int64_t vnJ = 0;         // R^{N-1}
+  // tree QR of V_n across the Khatri-Rao factors (NEXT-2; vn_tree.cuh)
+  bool vn_krtree = false;
+  bool kr_standalone = false;  // a debug call: factor the shared group afresh
+  double *dTrP[2] = {nullptr, nullptr}, *dTrS[2] = {nullptr, nullptr}, *dTrPa = nullptr, *dTrPb = nullptr,
+         *dTrT = nullptr, *dTrQ = nullptr;
   double *dVn = nullptr, *dVq1 = nullptr, *dVgp = nullptr, *dVr1 = nullptr, *dVr2 = nullptr;
   bool tree = false;       // dimension-tree Multi-TTM (opt.mttm_tree, QR/SVD, N >= 3)
   int tree_h = 0;
@@ -1505,6 +1511,23 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   a.use_smem = c->kr_smem > 0;
   a.flags = c->dflags;
   cudaStream_t st = c->side ? c->side : c->st;
+  if (c->vn_krtree) {
+    // tree QR across the Khatri-Rao factors (one CTA): the group of the other half is factored at
+    // the first mode of each half (n == 0, n == h) and reused by the rest of that half
+    VnTreeArgs t{};
+    for (int k = 0; k < c->N; ++k) t.Rk[k] = c->dRk[k];
+    t.N = c->N; t.n = n; t.R = c->R; t.h = c->tree_h;
+    t.fresh = (c->kr_standalone || n == 0 || n == c->tree_h) ? 1 : 0;
+    for (int i = 0; i < 2; ++i) { t.Psh[i] = c->dTrP[i]; t.Ssh[i] = c->dTrS[i]; }
+    t.Pa = c->dTrPa; t.Pb = c->dTrPb; t.T = c->dTrT; t.Qg = c->dTrQ;
+    t.Q0 = c->dQ0; t.R0 = c->dR0; t.flags = c->dflags;
+    const size_t sm = vn_tree_smem(c->R);
+    if (c->R <= 8) k_vn_tree<8><<<1, 256, sm, st>>>(t);
+    else if (c->R <= 16) k_vn_tree<16><<<1, 512, sm, st>>>(t);
+    else k_vn_tree<32><<<1, 256, sm, st>>>(t);
+    CKL();
+    return CPQR_OK;
+  }
   if (c->short_modes) {
     // short modes (I_k < R): V_n keeps its prod_{k != n} min(I_k, R) nonzero rows (mixed radix); no
     // staircase K2 for them, so the QR is the shifted CholeskyQR3 (Fukaya et al.), stable up to
@@ -2374,6 +2397,26 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
       const bool compact_ok = J <= 8 * (R <= 16 ? 512 : 256);
       c->vn_cq_tree = !v && c->tree && (t ? atoi(t) == 1 : (compact_ok || J * R >= 50000));
     }
+    // tree QR of V_n (vn_tree.cuh): CPQR_VN_QR=tree; N >= 3, not with short modes
+    c->vn_krtree = !c->short_modes && N >= 3 && v && std::string(v) == "tree";
+    if (c->vn_krtree) {
+      c->vn_cq_always = c->vn_cq_tree = false;
+      const int h = c->tree_h;
+      int64_t Jh = 1, Jl = 1;
+      for (int i = 0; i < N - h; ++i) Jh *= R;
+      for (int i = 0; i < h; ++i) Jl *= R;
+      CK(dmalloc(&c->dTrP[0], sizeof(double) * Jh * R));
+      CK(dmalloc(&c->dTrP[1], sizeof(double) * Jl * R));
+      CK(dmalloc(&c->dTrS[0], sizeof(double) * R * R));
+      CK(dmalloc(&c->dTrS[1], sizeof(double) * R * R));
+      CK(dmalloc(&c->dTrPa, sizeof(double) * std::max(Jh, Jl) * R));
+      CK(dmalloc(&c->dTrPb, sizeof(double) * std::max(Jh, Jl) * R));
+      CK(dmalloc(&c->dTrT, sizeof(double) * J * R));
+      if (R > 16) CK(dmalloc(&c->dTrQ, sizeof(double) * R * R * R));
+      CK(cudaFuncSetAttribute(k_vn_tree<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vn_tree_smem(R)));
+      CK(cudaFuncSetAttribute(k_vn_tree<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vn_tree_smem(R)));
+      CK(cudaFuncSetAttribute(k_vn_tree<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vn_tree_smem(R)));
+    }
     c->vn_cq = c->vn_cq_always || c->vn_cq_tree || (c->overlap && J <= 512);
     c->vnJ = J;
     if (c->vn_cq) {
@@ -2430,7 +2473,8 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->evj) cudaEventDestroy(c->evj);
   double* ps[] = {c->dQ1, c->dGp, c->dinnerp, c->dR1, c->dR2, c->dMpinv, c->dRstack, c->dQtop, c->dV, c->dtauv, c->dinner, c->dlam, c->dQ0, c->dR0, c->dW, c->dnX2p, c->dSk, c->dWp, c->dAhat, c->buf[0], c->buf[1],
                   c->dPart, c->dKrWork, c->dnX2, c->dfit, c->dfits, c->dred,
-                  c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2, c->dVrs, c->dVrp, c->dGp2};
+                  c->dVn, c->dVq1, c->dVgp, c->dVr1, c->dVr2, c->dVrs, c->dVrp, c->dGp2,
+                  c->dTrP[0], c->dTrP[1], c->dTrS[0], c->dTrS[1], c->dTrPa, c->dTrPb, c->dTrT, c->dTrQ};
   for (double* p : ps) if (p) dfree(p);
   if (c->dperm) dfree(c->dperm);
   if (c->dflags) dfree(c->dflags);
@@ -2838,7 +2882,10 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   CK(cudaEventRecord(c->evf, c->st));
   CK(cudaStreamWaitEvent(c->side, c->evf, 0));
   c->vn_mode_cq = c->vn_cq_always;
-  TRY(launch_kr_qr(c, n));
+  c->kr_standalone = true;
+  const cpqr_status kst = launch_kr_qr(c, n);
+  c->kr_standalone = false;
+  TRY(kst);
   CK(cudaEventRecord(c->evj, c->side));
   // per slab: Multi-TTM (fresh from X, the tree buffer holds no valid half intermediate outside a
   // sweep), Q0 apply; the debug Y is summed over the ranks (n < N-1) or gathered (n == N-1)

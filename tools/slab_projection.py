@@ -63,7 +63,8 @@ def main():
             # free and hides behind the pass; the CholeskyQR2 V_n QR (p > 1, or R^{N-1} R >= 2e5) is
             # a multi-CTA launch that cannot co-run with a 147-CTA stream grid: counted in full
             J = conf.R ** (conf.N - 1)
-            cq = J * conf.R >= 200000 or os.environ.get("CPQR_VN_QR") == "cq"
+            vq = os.environ.get("CPQR_VN_QR")  # "tree": one CTA like K2 (hides behind the pass)
+            cq = vq == "cq" or (vq != "tree" and J * conf.R >= 200000)
             vn_exposed = vn if cq else max(0.0, vn - stream / p)
             t_rank = slab + fqr + other + vn_exposed + conf.N * args.comm_us / 1e3 * (p > 1)
             # the LOCAL context's own sweep time (graph, all p slabs in sequence)
