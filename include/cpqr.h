@@ -39,7 +39,7 @@ enum {
   CPQR_EINVAL = 1,     /* bad argument (N, dims, R, variant, NULL pointer, slab range, ...) */
   CPQR_ENOMEM = 2,     /* device allocation failed */
   CPQR_ECUDA = 3,      /* CUDA runtime error (message in cpqr_last_error) */
-  CPQR_ENCCL = 4,      /* NCCL error or NCCL unavailable with world > 1 */
+  CPQR_ENCCL = 4,      /* NCCL error, or a rank missing from a peer exchange (timeout) */
   CPQR_ESTATE = 5,     /* call out of order (no tensor / no factors yet) */
   CPQR_EDIVERGED = 6   /* a non-finite lambda appeared during the sweeps: the factors are then
                           non-finite (the remaining modes of the call ran on them); restore a
@@ -81,11 +81,24 @@ enum {
 /* How the ranks of the slab data parallelism (cpqr_options.world > 1) exchange W_n. */
 typedef enum {
   CPQR_COMM_NCCL = 0,  /* one process (context) per GPU; ncclAllReduce / ncclAllGather over NVLink */
-  CPQR_COMM_LOCAL = 1  /* virtual ranks: ONE context on one device runs all `world` slabs in rank
+  CPQR_COMM_LOCAL = 1, /* virtual ranks: ONE context on one device runs all `world` slabs in rank
                           order (each with its own plans, TMA maps and slab of Q_N) and combines
                           them with a fixed-order sum kernel (modes n < N) or one device copy per
                           rank (mode N); `rank` is ignored.  The multi-GPU code path on one GPU, for
                           parity tests and per-rank timing projections. */
+  CPQR_COMM_PEER = 2,  /* one process (context) per GPU, no collective library on the data path: the
+                          Q0 apply's final sum (Alg. 2 line 9; NE: a copy kernel) stores this rank's
+                          W_n partial straight into a slot of EVERY rank's receive window over
+                          NVLink peer memory and raises a flag; each rank then sums the p slots in
+                          rank order (modes n < N) or places the ranks' rows (mode N), so the
+                          factors stay bitwise identical on all ranks (SURVEY.md 8(f) NEXT-2,
+                          DESIGN.md §8).  ||X||^2 and the DIRECT residual take the same path.  The
+                          windows are exchanged with cpqr_peer_handle / cpqr_peer_connect before
+                          cpqr_set_tensor; nccl_id is optional (only cpqr_debug_mode's Y uses it). */
+  CPQR_COMM_LOCAL_PEER = 3 /* CPQR_COMM_LOCAL with the exchange of CPQR_COMM_PEER: p receive windows
+                          in the one context, every virtual rank pushes into all of them (the same
+                          kernels on one GPU, none waiting on another); cpqr_debug_peer checks that
+                          all windows received identical bytes. */
 } cpqr_comm;
 
 typedef struct cpqr_options {
@@ -103,7 +116,9 @@ typedef struct cpqr_options {
                              T_R = X x_{k<h} Q_k^T, h = ceil(N/2), so a sweep streams X twice
                              instead of N times; Y_(n) equals the per-mode Multi-TTM up to
                              rounding.  0 (default) = one pass over X per mode (Alg. 2 line 8). */
-  int32_t comm;           /* cpqr_comm (world > 1): CPQR_COMM_NCCL (default) or CPQR_COMM_LOCAL */
+  int32_t comm;           /* cpqr_comm: how world > 1 ranks exchange W_n (default CPQR_COMM_NCCL).  With
+                             world = 1, CPQR_COMM_NCCL plus a non-zero nccl_id, or CPQR_COMM_PEER, run
+                             the same in-graph exchange on one rank (a hardware check of the path). */
 } cpqr_options;
 
 /* Fills *opt with defaults: svd_tau = -1, FAST fit, device 0, own stream, world 1,
@@ -206,7 +221,7 @@ cpqr_status cpqr_get_flags(cpqr_ctx* ctx, uint32_t* flags);
  *   ms[2] factor QR: the fused tail launch (solve, normalise, factor QR, fast fit)
  *   ms[3] computing Q0 (QR of V_n)       ms[4] applying Q0
  *   ms[5] other (S_n^+ of PINV, the NE tail, the DIRECT fit)
- *   ms[6] exchange of W_n across the ranks (NCCL, or the virtual ranks' combine)
+ *   ms[6] exchange of W_n across the ranks (NCCL, the virtual ranks' combine, or the peer combine)
  * Slab-parallel phases (0, 1, 4 and the NE MTTKRP) are summed over the slabs a context runs.
  * launches[0..6]: kernel launches per phase; bytes0/flops0: algorithmic HBM bytes and flops of
  * phase 0.  reset != 0 zeroes the counters after reading. */
@@ -262,6 +277,29 @@ const char* cpqr_last_error(const cpqr_ctx* ctx);
 /* NCCL bootstrap: rank 0 calls this, broadcasts the 128 bytes (e.g. over torch.distributed),
  * every rank passes them in cpqr_options.nccl_id.  Returns ENCCL if NCCL is unavailable. */
 cpqr_status cpqr_nccl_unique_id(uint8_t id[128]);
+
+/* CPQR_COMM_PEER bootstrap (one process per GPU; P2P access between the devices required):
+ * cpqr_peer_handle writes the 64-byte CUDA IPC handle of this rank's receive window; the caller
+ * all-gathers the handles in rank order (e.g. torch.distributed.all_gather) and passes the
+ * world x 64 bytes to cpqr_peer_connect on every rank, which maps the peers' windows
+ * (cudaIpcOpenMemHandle).  Both before cpqr_set_tensor.  world = 1 needs neither.
+ * Errors: EINVAL (other comm modes, NULL), ESTATE (connected twice), ECUDA (IPC / no P2P). */
+cpqr_status cpqr_peer_handle(cpqr_ctx* ctx, uint8_t handle[64]);
+cpqr_status cpqr_peer_connect(cpqr_ctx* ctx, const uint8_t* handles);
+
+/* State of the peer windows (CPQR_COMM_PEER / CPQR_COMM_LOCAL_PEER), for tests: info[0] =
+ * exchanges completed by this rank (its epoch), info[1] = virtual ranks' windows whose received
+ * bytes, flags or epoch differ from window 0 (LOCAL_PEER; else 0), info[2] = bytes per window,
+ * info[3] = the smallest arrival flag of this rank's window. */
+cpqr_status cpqr_debug_peer(cpqr_ctx* ctx, int64_t info[4]);
+/* Plumbing check of the IPC windows between processes WITHOUT kernels that wait on each other:
+ * cpqr_debug_peer_put pushes n host doubles as one exchange into every rank's window (the
+ * k_peer_push kernel; it never waits); after a host-side barrier, cpqr_debug_peer_get runs the
+ * combine of that exchange -- the rank-order sum (gather = 0, n doubles) or the ranks' blocks in
+ * rank order (gather = 1, world x n doubles) -- into a host buffer.  Every rank must put before
+ * any rank gets (else the combine waits up to CPQR_PEER_TIMEOUT_MS, default 20000, then ENCCL). */
+cpqr_status cpqr_debug_peer_put(cpqr_ctx* ctx, const double* src, int64_t n);
+cpqr_status cpqr_debug_peer_get(cpqr_ctx* ctx, double* out, int64_t n, int gather);
 
 /* Library version string ("cpqr <semver> sm_100a"). */
 const char* cpqr_version(void);

@@ -24,7 +24,7 @@ NE, QR, SVD, PINV = 0, 1, 2, 3
 VARIANTS = {"NE": NE, "QR": QR, "SVD": SVD, "PINV": PINV}
 FIT_FAST, FIT_DIRECT = 0, 1
 MEM_HOST, MEM_DEVICE_COPY, MEM_DEVICE_BORROW = 0, 1, 2
-COMM_NCCL, COMM_LOCAL = 0, 1
+COMM_NCCL, COMM_LOCAL, COMM_PEER, COMM_LOCAL_PEER = 0, 1, 2, 3
 FLAG_ILLCOND_R0, FLAG_NE_CHOL_FALLBACK, FLAG_SVD_TRUNCATED, FLAG_NE_ILLCOND = 1, 2, 4, 8
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ESTATE", 6: "EDIVERGED"}
 
@@ -33,6 +33,7 @@ EXPORTS = [
     "cpqr_set_ktensor", "cpqr_batched_qr", "cpqr_batched", "cpqr_sweep", "cpqr_get_factors", "cpqr_get_fit", "cpqr_get_flags", "cpqr_get_profile", "cpqr_get_timings",
     "cpqr_launches_per_sweep", "cpqr_debug_mode", "cpqr_debug_plan", "cpqr_debug_qr", "cpqr_debug_svd_solve",
     "cpqr_destroy", "cpqr_status_string", "cpqr_last_error", "cpqr_nccl_unique_id", "cpqr_version",
+    "cpqr_peer_handle", "cpqr_peer_connect", "cpqr_debug_peer", "cpqr_debug_peer_put", "cpqr_debug_peer_get",
 ]
 
 
@@ -77,6 +78,11 @@ _sig = {
     "cpqr_last_error": (C.c_char_p, [_P]),
     "cpqr_nccl_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),
     "cpqr_version": (C.c_char_p, []),
+    "cpqr_peer_handle": (C.c_int32, [_P, C.POINTER(C.c_uint8)]),
+    "cpqr_peer_connect": (C.c_int32, [_P, C.POINTER(C.c_uint8)]),
+    "cpqr_debug_peer": (C.c_int32, [_P, C.POINTER(C.c_int64)]),
+    "cpqr_debug_peer_put": (C.c_int32, [_P, _DP, C.c_int64]),
+    "cpqr_debug_peer_get": (C.c_int32, [_P, _DP, C.c_int64, C.c_int]),
 }
 for _name, (_res, _args) in _sig.items():
     if "CPQR_LIB" in os.environ and not hasattr(_lib, _name):
@@ -147,7 +153,9 @@ class CPQR:
         """world > 1 with comm="nccl": this process is rank `rank` of `world` (one GPU each, slab
         of the last mode, NCCL id from nccl_unique_id() on rank 0).  comm="local": ONE context on
         this device runs all `world` slabs as virtual ranks (cpqr.h CPQR_COMM_LOCAL); set_tensor
-        then takes the whole tensor."""
+        then takes the whole tensor.  comm="peer": one process per GPU with the fused push-reduce over
+        peer windows (CPQR_COMM_PEER; call peer_connect() with the all-gathered peer_handle()s, or
+        connect_peers_torch(), before set_tensor); comm="local_peer": its virtual-rank form."""
         self.dims = tuple(int(d) for d in dims)
         self.N, self.R = len(self.dims), int(R)
         self.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
@@ -163,10 +171,11 @@ class CPQR:
         opt.use_graph = 1 if use_graph else 0
         opt.profile = 1 if profile else 0
         opt.mttm_tree = 1 if tree else 0  # dimension-tree Multi-TTM (QR/SVD, N >= 3)
-        opt.comm = {"nccl": COMM_NCCL, "local": COMM_LOCAL}[comm]
+        opt.comm = {"nccl": COMM_NCCL, "local": COMM_LOCAL, "peer": COMM_PEER, "local_peer": COMM_LOCAL_PEER}[comm]
         self.rank, self.world, self.comm = int(rank), int(world), comm
         per = self.dims[-1] // self.world
-        self.slab = (0, self.dims[-1]) if comm == "local" else (per * self.rank, per * (self.rank + 1))
+        virt = comm in ("local", "local_peer")
+        self.slab = (0, self.dims[-1]) if virt else (per * self.rank, per * (self.rank + 1))
         d = (C.c_int64 * self.N)(*self.dims)
         h = _P()
         st = _lib.cpqr_create(self.N, d, self.R, self.variant, C.byref(opt), C.byref(h))
@@ -257,6 +266,43 @@ class CPQR:
         f = C.c_uint32()
         self._check(_lib.cpqr_get_flags(self._h, C.byref(f)))
         return f.value
+
+    # -------------------------------------------------------- peer windows (CPQR_COMM_PEER)
+    def peer_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        self._check(_lib.cpqr_peer_handle(self._h, buf))
+        return bytes(buf)
+
+    def peer_connect(self, handles):
+        """handles: the ranks' peer_handle() bytes in rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        assert len(blob) == 64 * self.world
+        self._check(_lib.cpqr_peer_connect(self._h, (C.c_uint8 * len(blob)).from_buffer_copy(blob)))
+
+    def connect_peers_torch(self, group=None):
+        """All-gather the window handles over a torch.distributed process group and connect."""
+        import torch
+        import torch.distributed as dist
+        mine = torch.frombuffer(bytearray(self.peer_handle()), dtype=torch.uint8).clone()
+        if dist.get_backend(group) == "nccl":
+            mine = mine.cuda()
+        outs = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(outs, mine, group=group)
+        self.peer_connect([bytes(o.cpu().numpy().tobytes()) for o in outs])
+
+    def debug_peer(self):
+        info = (C.c_int64 * 4)()
+        self._check(_lib.cpqr_debug_peer(self._h, info))
+        return dict(epoch=info[0], windows_differing=info[1], window_bytes=info[2], min_flag=info[3])
+
+    def debug_peer_put(self, src):
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        self._check(_lib.cpqr_debug_peer_put(self._h, _dptr(src), src.size))
+
+    def debug_peer_get(self, n, gather=False):
+        out = np.zeros(n * (self.world if gather else 1))
+        self._check(_lib.cpqr_debug_peer_get(self._h, _dptr(out), int(n), 1 if gather else 0))
+        return out
 
     def profile(self, reset=True):
         p = Profile()

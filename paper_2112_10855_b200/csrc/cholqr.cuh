@@ -28,6 +28,7 @@ constexpr double kCqKappaMax = 1.0e5;
 constexpr bool kCqClosedForm = CPQR_CQ_CLOSED_FORM != 0;  // second CholeskyQR pass in closed form
 constexpr unsigned FLAG_USE_HOUSEHOLDER = 0x200u;
 constexpr unsigned FLAG_VN_HOUSEHOLDER = 0x400u;  // the CholeskyQR2 V_n QR handed over to K2
+constexpr unsigned FLAG_PEER_TIMEOUT = 0x800u;    // k_peer_combine gave up waiting for a rank
 
 struct CqArgs {
   const double* A;   // solve = 0: m x R column-major input

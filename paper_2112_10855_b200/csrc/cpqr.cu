@@ -120,6 +120,18 @@ struct cpqr_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t user = nullptr;
   ncclComm_t comm = nullptr;
+  // exchange of the slabs' results: NCCL collectives, the virtual ranks' sum kernel,
+  // or the peer push-reduce (CPQR_COMM_PEER / CPQR_COMM_LOCAL_PEER; small_kernels.cuh): receive
+  // windows win_base[r] -- this rank's own (cudaMalloc) and its peers' (CUDA IPC), or all p of the
+  // virtual ranks -- laid out [2 parities][p slots][slot_elems] doubles, kMaxRanks flags, epoch
+  bool exchange = false;      // world > 1, or a one-rank NCCL / PEER exchange (hardware check of the path)
+  bool peer = false, peers_connected = false;
+  void* win_base[kMaxWorld] = {nullptr};
+  bool win_mapped[kMaxWorld] = {false};
+  int64_t slot_elems = 0;
+  size_t win_data_bytes = 0, win_bytes = 0;
+  unsigned* dpushcnt = nullptr;
+  unsigned long long peer_timeout_ns = 20000000000ull;
   bool have_tensor = false, have_factors = false;
   double *dA[kMaxN] = {0}, *dQ[kMaxN] = {0}, *dRk[kMaxN] = {0}, *dG[kMaxN] = {0};
   double *dQt[kMaxN] = {0}, *dAt[kMaxN] = {0};  // transposed, zero-padded (I_k x RQ) TMA panels
@@ -1591,7 +1603,8 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
   return CPQR_OK;
 }
 
-cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
+// pp: the peer push of this slab's W (np = 0: none), fused into the apply's final sum
+cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const PeerPush& pp = PeerPush{}) {
   const int64_t J = p.Aa * p.Bb, KT = (J + 3) / 4;
   const int In = (int)p.In;
   const int iblocks = (In + 7) / 8;
@@ -1605,29 +1618,84 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout) {
 #define Q0A(NTV)                                                                                                 \
   (c->q0_stair ? launch_ex(k_q0_apply_tc<NTV, true>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb,           \
                            (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)c->dperm,  \
-                           c->N - 1)                                                                                 \
+                           c->N - 1, pp)                                                                             \
                : launch_ex(k_q0_apply_tc<NTV, false>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb,          \
-                           (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)nullptr, 0))
+                           (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)nullptr, 0, pp))
   switch (NT) { case 1: Q0A(1); break; case 2: Q0A(2); break; case 3: Q0A(3); break; default: Q0A(4); break; }
 #undef Q0A
   CKL();
   return CPQR_OK;
 }
 
-// where slab q's partial W_n (or its rows of W_N) is written: straight into W for one GPU
-double* wloc(cpqr_ctx* c, int q) { return c->opt.world > 1 ? c->slabs[q].dWloc : c->dW; }
+// where slab q's partial W_n (or its rows of W_N) is written: straight into W without an exchange
+double* wloc(cpqr_ctx* c, int q) { return c->exchange ? c->slabs[q].dWloc : c->dW; }
+
+// ---- peer push-reduce (small_kernels.cuh): window accessors and the two halves of an exchange
+double* win_data(const cpqr_ctx* c, int r) { return static_cast<double*>(c->win_base[r]); }
+unsigned long long* win_flags(const cpqr_ctx* c, int r) {
+  return reinterpret_cast<unsigned long long*>(static_cast<char*>(c->win_base[r]) + c->win_data_bytes);
+}
+unsigned long long* win_epoch(const cpqr_ctx* c, int r) { return win_flags(c, r) + kMaxRanks; }
+// this context's own window: virtual rank 0's, or this rank's
+int own_win(const cpqr_ctx* c) { return c->local ? 0 : c->opt.rank; }
+
+// the push of slab q: source rank s = q (virtual ranks) or this rank; np = 0 without peer exchange
+PeerPush make_push(const cpqr_ctx* c, int q) {
+  PeerPush pp{};
+  if (!c->peer) return pp;
+  const int s = c->local ? q : c->opt.rank;
+  pp.np = c->opt.world;
+  for (int r = 0; r < pp.np; ++r) {
+    pp.dst[r] = win_data(c, r) + (int64_t)s * c->slot_elems;
+    pp.flag[r] = win_flags(c, r) + s;
+  }
+  pp.epoch = win_epoch(c, s);
+  pp.gcount = c->dpushcnt;
+  pp.parity_stride = (int64_t)pp.np * c->slot_elems;
+  return pp;
+}
+
+// this rank's combine of the exchange its own push just started
+cpqr_status peer_combine(cpqr_ctx* c, int64_t cnt, int gather, double* out) {
+  if (cnt > c->slot_elems) return fail(c, CPQR_EINVAL, "peer exchange of %lld elements exceeds the window slot", (long long)cnt);
+  const int o = own_win(c);
+  const int64_t tot = gather ? cnt * c->opt.world : cnt;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)c->sms * 4));
+  launch_ex(k_peer_combine, grid, 256, 0, c->st, c->pdl, 1, (const double*)win_data(c, o),
+            (const unsigned long long*)win_flags(c, o), (const unsigned long long*)win_epoch(c, o), c->opt.world,
+            c->slot_elems, cnt, gather, out, c->dflags, (unsigned)FLAG_PEER_TIMEOUT, c->peer_timeout_ns);
+  CKL();
+  return CPQR_OK;
+}
+
+// stand-alone push of every slab's n doubles, then the combine (sum in rank order, or gather)
+cpqr_status peer_exchange(cpqr_ctx* c, const double* const* src, int64_t n, int gather, double* out) {
+  if (n > c->slot_elems) return fail(c, CPQR_EINVAL, "peer exchange of %lld elements exceeds the window slot", (long long)n);
+  for (int q = 0; q < c->nslab; ++q) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sms));
+    launch_ex(k_peer_push, grid, 256, 0, c->st, c->pdl, 1, src[q], n, make_push(c, q));
+    CKL();
+  }
+  return peer_combine(c, n, gather, out);
+}
 
 // Combine the slabs' results of mode n into the full row-major W_n (or NE's M_n) in c->dW
 // (DESIGN.md §8): the sum over ranks for n < N-1 (W_p = Y_p Q0 is linear in the slab, so Q0 is
 // applied before the reduction), the ranks' rows in rank order for n == N-1.  Across processes:
-// ncclAllReduce / ncclAllGather.  Virtual ranks (CPQR_COMM_LOCAL): a fixed-order sum kernel over
-// the p partials, or one device copy per rank.  src[q]: slab q's local result.
-cpqr_status combine_w(cpqr_ctx* c, int n, const double* const* src) {
+// ncclAllReduce / ncclAllGather, or the peer push-reduce.  Virtual ranks (CPQR_COMM_LOCAL): a
+// fixed-order sum kernel over the p partials, or one device copy per rank.  src[q]: slab q's local
+// result; pushed: the producing kernel already pushed it into the peer windows (the Q0 apply).
+cpqr_status combine_w(cpqr_ctx* c, int n, const double* const* src, bool pushed = false) {
   const int64_t R = c->R;
-  if (c->opt.world <= 1) {
+  if (!c->exchange) {
     if (src[0] != c->dW)
       CK(cudaMemcpyAsync(c->dW, src[0], sizeof(double) * c->dims[n] * R, cudaMemcpyDeviceToDevice, c->st));
     return CPQR_OK;
+  }
+  if (c->peer) {
+    const int gather = (n == c->N - 1) ? 1 : 0;
+    const int64_t cnt = (gather ? c->slabs[0].ldims[n] : c->dims[n]) * R;
+    return pushed ? peer_combine(c, cnt, gather, c->dW) : peer_exchange(c, src, cnt, gather, c->dW);
   }
   if (!c->local) {
     if (n < c->N - 1) {
@@ -1844,7 +1912,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
         prof_mark(c, 0);
       }
       Mfull = src[0];
-      if (c->opt.world > 1) {
+      if (c->exchange) {
         // the rows of M_N are gathered: its layout must be row-major (rmode < n, plan_mode)
         if (n == N - 1 && !m_rowmajor) return fail(c, CPQR_EINVAL, "NE: column-major M_N cannot be gathered");
         TRY(combine_w(c, n, src));
@@ -1973,11 +2041,11 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
       TRY(run_plan(c, rest));
       prof_mark(c, 1);
       if (fork && q == 0) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-      TRY(launch_q0_apply(c, p, wloc(c, q)));
+      TRY(launch_q0_apply(c, p, wloc(c, q), make_push(c, q)));
       src[q] = wloc(c, q);
       prof_mark(c, 4);
     }
-    TRY(combine_w(c, n, src));
+    TRY(combine_w(c, n, src, c->peer));
     prof_mark(c, 6);
   }
   if (pinv_fork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
@@ -2029,10 +2097,14 @@ cpqr_status direct_fit(cpqr_ctx* c) {
     CKL();
   }
   prof_mark(c, 5);
-  if (c->nslab > 1) {  // virtual ranks: rank-order sum of the slab residuals
+  if (c->peer) {  // rank-order sum of the slab residuals through the peer windows
+    const double* src[kMaxWorld];
+    for (int q = 0; q < c->nslab; ++q) src[q] = c->nslab > 1 ? res + 8 + q : res;
+    TRY(peer_exchange(c, src, 1, 0, res));
+  } else if (c->nslab > 1) {  // virtual ranks: rank-order sum of the slab residuals
     k_sum_final<<<1, 256, 0, c->st>>>(res + 8, c->nslab, res);
     CKL();
-  } else if (c->opt.world > 1) {
+  } else if (c->comm) {
     CN(ncclAllReduce(res, res, 1, ncclDouble, ncclSum, c->comm, c->st));
   }
   prof_mark(c, 6);
@@ -2187,6 +2259,98 @@ CPQR_API cpqr_status cpqr_nccl_unique_id(uint8_t id[128]) {
   return CPQR_OK;
 }
 
+static int64_t max_dim(const cpqr_ctx* c);
+// ---- peer push-reduce: window exchange between processes (CUDA IPC) and its debug hooks
+CPQR_API cpqr_status cpqr_peer_handle(cpqr_ctx* c, uint8_t handle[64]) {
+  if (!c || !handle) return CPQR_EINVAL;
+  if (!c->peer || c->local) return fail(c, CPQR_EINVAL, "cpqr_peer_handle needs comm = CPQR_COMM_PEER");
+  CK(cudaSetDevice(c->opt.device));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  CK(cudaIpcGetMemHandle(&h, c->win_base[c->opt.rank]));
+  std::memcpy(handle, &h, 64);
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_peer_connect(cpqr_ctx* c, const uint8_t* handles) {
+  if (!c || !handles) return CPQR_EINVAL;
+  if (!c->peer || c->local) return fail(c, CPQR_EINVAL, "cpqr_peer_connect needs comm = CPQR_COMM_PEER");
+  if (c->peers_connected) return c->opt.world == 1 ? CPQR_OK : fail(c, CPQR_ESTATE, "peers already connected");
+  CK(cudaSetDevice(c->opt.device));
+  for (int r = 0; r < c->opt.world; ++r) {
+    if (r == c->opt.rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * (size_t)r, 64);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->win_base[r] = p;
+    c->win_mapped[r] = true;
+  }
+  c->peers_connected = true;
+  return CPQR_OK;
+}
+
+CPQR_API cpqr_status cpqr_debug_peer(cpqr_ctx* c, int64_t info[4]) {
+  if (!c || !info) return CPQR_EINVAL;
+  if (!c->peer) return fail(c, CPQR_EINVAL, "no peer windows (comm)");
+  TRY(begin_call(c));
+  CK(cudaStreamSynchronize(c->st));
+  const int o = own_win(c);
+  std::vector<unsigned char> w0(c->win_bytes), wr(c->win_bytes);
+  CK(cudaMemcpy(w0.data(), c->win_base[o], c->win_bytes, cudaMemcpyDeviceToHost));
+  unsigned long long ep = 0, fmin = ~0ull;
+  std::memcpy(&ep, w0.data() + c->win_data_bytes + sizeof(unsigned long long) * kMaxRanks, sizeof ep);
+  for (int q = 0; q < c->opt.world; ++q) {
+    unsigned long long f;
+    std::memcpy(&f, w0.data() + c->win_data_bytes + sizeof(unsigned long long) * q, sizeof f);
+    fmin = std::min(fmin, f);
+  }
+  int64_t differ = 0;
+  if (c->local)  // every virtual rank received the same slots and flags (the epoch word aside)
+    for (int r = 1; r < c->opt.world; ++r) {
+      CK(cudaMemcpy(wr.data(), c->win_base[r], c->win_bytes, cudaMemcpyDeviceToHost));
+      const size_t cmp = c->win_data_bytes + sizeof(unsigned long long) * kMaxRanks;
+      if (std::memcmp(w0.data(), wr.data(), cmp) != 0) ++differ;
+      unsigned long long er;
+      std::memcpy(&er, wr.data() + cmp, sizeof er);
+      if (er != ep) ++differ;
+    }
+  info[0] = (int64_t)ep;
+  info[1] = differ;
+  info[2] = (int64_t)c->win_bytes;
+  info[3] = (int64_t)fmin;
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_debug_peer_put(cpqr_ctx* c, const double* src, int64_t n) {
+  if (!c || !src || n < 1) return CPQR_EINVAL;
+  if (!c->peer || c->local) return fail(c, CPQR_EINVAL, "cpqr_debug_peer_put needs comm = CPQR_COMM_PEER");
+  if (!c->peers_connected) return fail(c, CPQR_ESTATE, "cpqr_peer_connect first");
+  if (n > c->slot_elems) return fail(c, CPQR_EINVAL, "n exceeds the window slot (%lld)", (long long)c->slot_elems);
+  TRY(begin_call(c));
+  CK(cudaMemcpyAsync(c->slabs[0].dWloc, src, sizeof(double) * n, cudaMemcpyHostToDevice, c->st));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sms));
+  launch_ex(k_peer_push, grid, 256, 0, c->st, false, 1, (const double*)c->slabs[0].dWloc, n, make_push(c, 0));
+  CKL();
+  return end_call(c);
+}
+
+CPQR_API cpqr_status cpqr_debug_peer_get(cpqr_ctx* c, double* out, int64_t n, int gather) {
+  if (!c || !out || n < 1) return CPQR_EINVAL;
+  if (!c->peer || c->local) return fail(c, CPQR_EINVAL, "cpqr_debug_peer_get needs comm = CPQR_COMM_PEER");
+  if (!c->peers_connected) return fail(c, CPQR_ESTATE, "cpqr_peer_connect first");
+  const int64_t tot = gather ? n * c->opt.world : n;
+  if (n > c->slot_elems || tot > max_dim(c) * c->R) return fail(c, CPQR_EINVAL, "n too large");
+  TRY(begin_call(c));
+  TRY(peer_combine(c, n, gather ? 1 : 0, c->dW));
+  unsigned fl = 0;
+  CK(cudaMemcpyAsync(out, c->dW, sizeof(double) * tot, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&fl, c->dflags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+  TRY(end_call(c));
+  if (fl & FLAG_PEER_TIMEOUT) return fail(c, CPQR_ENCCL, "peer exchange: a rank did not arrive in time");
+  return CPQR_OK;
+}
+
 static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R);
 
 CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
@@ -2215,7 +2379,7 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
     delete c;
     return CPQR_EINVAL;
   }
-  if (c->opt.comm != CPQR_COMM_NCCL && c->opt.comm != CPQR_COMM_LOCAL) { delete c; return CPQR_EINVAL; }
+  if (c->opt.comm < CPQR_COMM_NCCL || c->opt.comm > CPQR_COMM_LOCAL_PEER) { delete c; return CPQR_EINVAL; }
   if (c->opt.world > 1 && (dims[N - 1] % c->opt.world) != 0) { delete c; return CPQR_EINVAL; }
   c->variant = variant;
   if (c->short_modes && c->opt.world > 1) { delete c; return CPQR_EINVAL; }  // Kruskal input only
@@ -2247,8 +2411,16 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   }
   for (int k = 0; k < N; ++k) c->dims[k] = dims[k];
   // slabs of the last mode: this rank's, or all p of the virtual ranks
-  c->local = c->opt.comm == CPQR_COMM_LOCAL && c->opt.world > 1;
+  c->local = (c->opt.comm == CPQR_COMM_LOCAL || c->opt.comm == CPQR_COMM_LOCAL_PEER) && c->opt.world > 1;
   c->nslab = c->local ? c->opt.world : 1;
+  c->peer = c->opt.comm == CPQR_COMM_PEER || (c->opt.comm == CPQR_COMM_LOCAL_PEER && c->opt.world > 1);
+  // a one-rank communicator (world = 1, comm = NCCL, an id given) runs the in-graph collectives on
+  // one GPU; so does a one-rank peer window (comm = PEER): hardware checks of the exchange paths
+  bool have_id = false;
+  for (int i = 0; i < 128; ++i) have_id = have_id || c->opt.nccl_id[i] != 0;
+  const bool nccl1 = c->opt.world == 1 && c->opt.comm == CPQR_COMM_NCCL && have_id;
+  c->exchange = c->opt.world > 1 || c->peer || nccl1;
+  if (const char* t = getenv("CPQR_PEER_TIMEOUT_MS")) c->peer_timeout_ns = 1000000ull * (unsigned long long)std::max(1, atoi(t));
   const int64_t per = dims[N - 1] / c->opt.world;
   for (int q = 0; q < c->nslab; ++q) {
     Slab& sl = c->slabs[q];
@@ -2267,7 +2439,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   {  // overlap schedule (mode_update_overlap): HBM-bound QR / QR-SVD sweeps on one GPU by default
      // (measured vs the serial schedule, 40 sweeps x 2: C2 2615 -> 2680, C3 555 -> 560, C4 465 -> 484)
     const char* ov = getenv("CPQR_OVERLAP");
-    const bool elig = !ne_family(c->variant) && !c->tree && c->opt.world == 1 && N >= 3 && !c->opt.profile;
+    const bool elig = !ne_family(c->variant) && !c->tree && !c->exchange && N >= 3 && !c->opt.profile;
     c->overlap = elig && (ov ? atoi(ov) == 1 : R <= 16);
     if (const char* r = getenv("CPQR_OVERLAP_SMS")) c->overlap_reserve = std::max(0, atoi(r));
     if (const char* r = getenv("CPQR_OVERLAP_CW1")) c->ov_cw1 = atoi(r) != 0;
@@ -2313,8 +2485,23 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   CK(dmalloc(&c->dQ0, sizeof(double) * J * R));
   CK(dmalloc(&c->dR0, sizeof(double) * R * R));
   CK(dmalloc(&c->dW, sizeof(double) * imax * R));
-  if (c->opt.world > 1)
+  if (c->exchange)
     for (int q = 0; q < c->nslab; ++q) CK(dmalloc(&c->slabs[q].dWloc, sizeof(double) * imax * R));
+  if (c->peer) {
+    // receive windows (plain cudaMalloc: exported through CUDA IPC): this rank's, or all virtual ranks'
+    const int np = c->opt.world;
+    c->slot_elems = std::max<int64_t>(imax * R, 64);
+    c->win_data_bytes = ((size_t)2 * np * c->slot_elems * sizeof(double) + 127) / 128 * 128;
+    c->win_bytes = c->win_data_bytes + sizeof(unsigned long long) * (kMaxRanks + 16);
+    for (int r = 0; r < np; ++r) {
+      if (!c->local && r != c->opt.rank) continue;
+      CK(cudaMalloc(&c->win_base[r], c->win_bytes));
+      CK(cudaMemset(c->win_base[r], 0, c->win_bytes));
+    }
+    CK(dmalloc(&c->dpushcnt, sizeof(unsigned) * 4));
+    CK(cudaMemset(c->dpushcnt, 0, sizeof(unsigned) * 4));
+    c->peers_connected = c->local || np == 1;
+  }
   CK(dmalloc(&c->dnX2p, sizeof(double) * 64));
   CK(dmalloc(&c->dfitc, sizeof(unsigned) * 4));
   CK(dmalloc(&c->dSk, sizeof(double) * 2 * (2 * c->sms) * 256 * R));
@@ -2435,7 +2622,8 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     const int64_t nbmax = std::max<int64_t>((imax + 255) / 256, c->vn_cq ? (J + 255) / 256 : 0);
     if (nbmax > 1024) CK(dmalloc(&c->dGp2, sizeof(double) * ((nbmax + 511) / 512 + 1) * R * R));
   }
-  if (c->opt.world > 1 && !c->local) {
+  // PEER ranks need no communicator; with an id they get one (cpqr_debug_mode's Y collectives)
+  if ((c->opt.world > 1 && !c->local && (!c->peer || have_id)) || nccl1) {
     ncclUniqueId id;
     std::memcpy(&id, c->opt.nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&c->comm, c->opt.world, id, c->opt.rank);
@@ -2457,6 +2645,12 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->gexecG) cudaGraphExecDestroy(c->gexecG);
   if (c->dfitc) dfree(c->dfitc);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (int r = 0; r < kMaxWorld; ++r) {
+    if (!c->win_base[r]) continue;
+    if (c->win_mapped[r]) cudaIpcCloseMemHandle(c->win_base[r]);
+    else cudaFree(c->win_base[r]);
+  }
+  dfree(c->dpushcnt);
   for (int k = 0; k < kMaxN; ++k) {
     dfree(c->dA[k]); dfree(c->dQ[k]); dfree(c->dRk[k]); dfree(c->dG[k]);
     dfree(c->dQt[k]); dfree(c->dAt[k]);
@@ -2559,10 +2753,15 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
   c->graph_valid = false;
   c->have_tensor = all;
   if (all) {
-    if (c->nslab > 1) {  // virtual ranks: ||X||^2 = rank-order sum of the slab partials
+    if (c->peer) {  // ||X||^2 = rank-order sum of the slab partials through the peer windows
+      if (!c->peers_connected) return fail(c, CPQR_ESTATE, "CPQR_COMM_PEER: cpqr_peer_connect first");
+      const double* src[kMaxWorld];
+      for (int q = 0; q < c->nslab; ++q) src[q] = c->nslab > 1 ? c->dnX2p + q : c->dnX2;
+      TRY(peer_exchange(c, src, 1, 0, c->dnX2));
+    } else if (c->nslab > 1) {  // virtual ranks: ||X||^2 = rank-order sum of the slab partials
       k_sum_final<<<1, 256, 0, c->st>>>(c->dnX2p, c->nslab, c->dnX2);
       CKL();
-    } else if (c->opt.world > 1) {
+    } else if (c->comm) {
       CN(ncclAllReduce(c->dnX2, c->dnX2, 1, ncclDouble, ncclSum, c->comm, c->st));
     }
     TRY(build_plans(c));
@@ -2766,6 +2965,9 @@ CPQR_API cpqr_status cpqr_sweep(cpqr_ctx* c, int nsweeps, double* fits) {
     c->flags |= fl;
     c->last_fit = hf[nsweeps - 1];
     if (fits) std::memcpy(fits, hf.data(), sizeof(double) * nsweeps);
+    if (fl & FLAG_PEER_TIMEOUT)
+      return fail(c, CPQR_ENCCL, "peer exchange: a rank did not arrive within %llu ms (CPQR_PEER_TIMEOUT_MS)",
+                  (unsigned long long)(c->peer_timeout_ns / 1000000ull));
     if (fl & FLAG_NONFINITE) return fail(c, CPQR_EDIVERGED, "non-finite factor");
     size_t which = 0;
     if (const size_t bad = canary_violations(&which))
@@ -2900,7 +3102,7 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
     plan_mode(in, p, c->buf, c->dPart);
     TRY(run_plan(c, p));
     if (q == 0) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-    TRY(launch_q0_apply(c, p, wloc(c, q)));
+    TRY(launch_q0_apply(c, p, wloc(c, q), make_push(c, q)));
     src[q] = wloc(c, q);
     ylocal = (int64_t)p.Aa * p.In * p.Bb;
     if (Y_out) {
@@ -2921,8 +3123,10 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
       }
     }
   }
-  TRY(combine_w(c, n, src));
-  if (Y_out && c->opt.world > 1 && !c->local) {
+  TRY(combine_w(c, n, src, c->peer));
+  if (Y_out && c->opt.world > 1 && !c->local && !c->comm)
+    return fail(c, CPQR_EINVAL, "debug_mode: Y across CPQR_COMM_PEER ranks needs an NCCL id (pass Y_out = NULL)");
+  if (Y_out && c->comm) {
     double* ycoll = nullptr;
     CK(sc.alloc(&ycoll, sizeof(double) * ytot));
     if (n == N - 1) CN(ncclAllGather(yfull, ycoll, (size_t)ylocal, ncclDouble, c->comm, c->st));

@@ -56,6 +56,111 @@ __global__ void k_sum_ranks(RankPtrs a, int nr, int64_t n, double* out) {
   }
 }
 
+// ------------------------------------------------------------- peer push-reduce of W_n
+// The exchange of the slab data parallelism without a collective library (SURVEY.md 8(f) NEXT-2,
+// DESIGN.md §8): every rank owns a RECEIVE WINDOW -- [2 parities][p slots][slot_elems] doubles, p
+// arrival flags and an exchange counter (epoch) -- that its peers map (CUDA IPC over NVLink, or the
+// same device for virtual ranks).  Exchange number e + 1 of source rank s:
+//   push    the producing kernel (the Q0 apply's final sum, or k_peer_push) stores its result into
+//           slot s, parity e & 1, of EVERY rank's window with plain stores; each CTA that finishes
+//           rows fences at system scope and arrives on a grid counter; the last one to arrive
+//           fences again, raises flag[s] = e + 1 on every rank (st.release.sys) and advances the
+//           local epoch;
+//   combine k_peer_combine on every rank waits until its p flags reach e + 1 (ld.acquire.sys),
+//           then sums the p slots in rank order (n < N) or places them by rank (mode N), so the
+//           result is bitwise identical on all ranks.
+// No reset and no second barrier: the flags only grow, and a rank can start exchange e + 3 (same
+// parity as e + 1) only after its own combine of e + 2, i.e. after every peer pushed e + 2, which
+// each peer does after ITS combine of e + 1 (stream order) -- so slot parity e & 1 is free again.
+struct PeerPush {
+  double* dst[kMaxRanks];               // rank r's slot for this source rank (parity 0)
+  unsigned long long* flag[kMaxRanks];  // rank r's arrival flag for this source rank
+  unsigned long long* epoch;            // this source rank's exchange counter (its own window)
+  unsigned* gcount;                     // arrivals of the pushing grid's finishing CTAs (self re-arming)
+  int64_t parity_stride;                // elements between the two parities of a slot
+  int np;                               // ranks (0: no push)
+};
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Called by all threads of a CTA once its peer stores are issued; `finishers` CTAs of the grid
+// call it exactly once each.  e: the epoch the CTA read before storing.
+__device__ __forceinline__ void peer_push_done(const PeerPush& pp, unsigned long long e, unsigned finishers) {
+  __shared__ int s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(pp.gcount, 1u) == finishers - 1u);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence_system();
+  if ((int)threadIdx.x < pp.np) st_release_sys(pp.flag[threadIdx.x], e + 1ull);
+  if (threadIdx.x == 0) {
+    *pp.gcount = 0u;
+    *pp.epoch = e + 1ull;
+  }
+}
+// Stand-alone push of n doubles (the NE MTTKRP partial, scalars such as ||X||^2 and the DIRECT
+// residual); the QR path pushes from the Q0 apply itself.
+__global__ void __launch_bounds__(256) k_peer_push(const double* __restrict__ src, int64_t n, PeerPush pp) {
+  pdl_wait();
+  const unsigned long long e = ld_relaxed_sys(pp.epoch);
+  const int64_t off = (e & 1ull) ? pp.parity_stride : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = src[i];
+    for (int r = 0; r < pp.np; ++r) pp.dst[r][off + i] = v;
+  }
+  peer_push_done(pp, e, gridDim.x);
+}
+// This rank's side of the exchange.  win: its window's data; cnt: elements per source rank;
+// gather = 0: out[i] = ((s_0[i] + s_1[i]) + ...); gather = 1: out[q cnt + i] = s_q[i].  A peer that
+// does not arrive within timeout_ns raises err_bit in *flags (the host reports ENCCL) and the
+// kernel gives up waiting.
+__global__ void __launch_bounds__(256)
+k_peer_combine(const double* __restrict__ win, const unsigned long long* __restrict__ wflag,
+               const unsigned long long* __restrict__ epoch, int np, int64_t slot_elems, int64_t cnt, int gather,
+               double* __restrict__ out, unsigned* __restrict__ flags, unsigned err_bit,
+               unsigned long long timeout_ns) {
+  pdl_wait();
+  const unsigned long long e = ld_relaxed_sys(epoch);  // advanced by this rank's own push
+  if ((int)threadIdx.x < np) {
+    unsigned long long t0 = 0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
+    while (ld_acquire_sys(wflag + threadIdx.x) < e) {
+      asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
+      if (now - t0 > timeout_ns) {
+        atomicOr(flags, err_bit);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  const double* base = win + (((e - 1ull) & 1ull) ? (int64_t)np * slot_elems : 0);
+  if (!gather) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+      double s = __ldcg(base + i);
+      for (int q = 1; q < np; ++q) s += __ldcg(base + q * slot_elems + i);
+      out[i] = s;
+    }
+  } else {
+    const int64_t tot = cnt * np;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t q = i / cnt;
+      out[i] = __ldcg(base + q * slot_elems + (i - q * cnt));
+    }
+  }
+}
+
 // The sweep's fit into the next slot of the per-call fits array (a device counter, reset by each
 // cpqr_sweep), so one captured graph can hold several sweeps.
 __global__ void k_store_fit(const double* __restrict__ fit, double* __restrict__ fits, unsigned* counter, int cap) {
@@ -293,10 +398,13 @@ template <int NT, bool STAIR = false>
 __global__ void __launch_bounds__(256)
 k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, const double* __restrict__ Q0, int R,
               int kpc, int KS, double* __restrict__ Wp, unsigned* __restrict__ counters, double* __restrict__ W,
-              const int* __restrict__ perm = nullptr, int N1 = 0) {
+              const int* __restrict__ perm, int N1, const __grid_constant__ PeerPush pp) {
   __shared__ double red[8][64 * NT];
   __shared__ int last;
   pdl_wait();
+  // peer push-reduce: the rows this CTA finishes also go to slot (rank, parity) of every window
+  const unsigned long long pe = pp.np ? ld_relaxed_sys(pp.epoch) : 0ull;
+  const int64_t poff = (pe & 1ull) ? pp.parity_stride : 0;
   const int64_t J = Aa * Bb, KT = (J + 3) / 4;
   const int ib = blockIdx.x, ks = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -343,11 +451,18 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
 #pragma unroll
     for (int w = 0; w < 8; ++w) s += red[w][e];
     if (ii < In && c < R) {
-      if (KS == 1) W[(int64_t)ii * R + c] = s;
-      else Wp[((int64_t)ks * In + ii) * R + c] = s;
+      if (KS == 1) {
+        W[(int64_t)ii * R + c] = s;
+        for (int r = 0; r < pp.np; ++r) pp.dst[r][poff + (int64_t)ii * R + c] = s;
+      } else {
+        Wp[((int64_t)ks * In + ii) * R + c] = s;
+      }
     }
   }
-  if (KS == 1) return;
+  if (KS == 1) {
+    if (pp.np) peer_push_done(pp, pe, gridDim.x);
+    return;
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = (atomicAdd(&counters[ib], 1u) == (unsigned)(KS - 1));
@@ -360,9 +475,11 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
       double s = 0.0;
       for (int k = 0; k < KS; ++k) s += __ldcg(Wp + ((int64_t)k * In + ii) * R + c);
       W[(int64_t)ii * R + c] = s;
+      for (int r = 0; r < pp.np; ++r) pp.dst[r][poff + (int64_t)ii * R + c] = s;
     }
   }
   if (threadIdx.x == 0) counters[ib] = 0u;  // re-armed for the next launch (graph replay)
+  if (pp.np) peer_push_done(pp, pe, gridDim.x);  // one finisher per row block
 }
 
 // ------------------------------------------------------------- one-sided Jacobi SVD of R0
