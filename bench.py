@@ -16,7 +16,8 @@ SURVEY.md §8(f) NEXT-1; two passes over X per sweep, identical mode updates up 
 the same way on the same resident tensor.  --tree swaps the two.
 
 Multi-GPU: one process per GPU under torch.distributed.run (`--gpus N` without WORLD_SIZE in
-the environment re-launches itself that way); the NCCL id is broadcast over a gloo group; timing =
+the environment re-launches itself that way); the NCCL id (or, with --comm peer, the CUDA IPC
+handles of the peer windows) travels over a gloo group; timing =
 CUDA events on the stream the library runs on, max over ranks.  The same slab path on one GPU
 (virtual ranks, parity tests and per-rank projections): tests/test_gpu_slabs.py,
 tools/slab_projection.py.
@@ -216,7 +217,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--tree", action="store_true", help="headline = dimension-tree Multi-TTM")
+    ap.add_argument("--comm", default="auto", choices=["auto", "nccl", "peer"],
+                    help="exchange of W_n across ranks: NCCL collectives or the fused peer push-reduce "
+                         "(CPQR_COMM_PEER); auto = NCCL at world > 1, none at world 1 (nccl / peer at world 1 "
+                         "run the in-graph exchange on one rank)")
     args = ap.parse_args()
+    # NCCL's version banner (NCCL_DEBUG=VERSION) goes to stdout by default: keep stdout to the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(args.gpus)
     if args.impl == "reference":
@@ -230,15 +237,27 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("gloo")
 
+    comm = args.comm if args.comm != "auto" else "nccl"
+
     def new_nccl_id():
         """A fresh ncclUniqueId for every context (one NCCL communicator each), broadcast from
         rank 0 over the gloo group; all ranks create contexts in the same order."""
-        if world == 1:
+        if comm != "nccl" or (world == 1 and args.comm == "auto"):
             return None
+        if world == 1:
+            return cpqr.nccl_unique_id()
         import torch.distributed as dist
         obj = [cpqr.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return obj[0]
+
+    def new_ctx(**kw):
+        """One context of this rank; CPQR_COMM_PEER ranks exchange their window handles (gloo)."""
+        s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
+                      rank=rank, world=world, nccl_id=new_nccl_id(), comm=comm, **kw)
+        if comm == "peer" and world > 1:
+            s.connect_peers_torch()
+        return s
     conf = synth.CONFIGS[args.config]
     variant = args.variant or conf.variants[0]
     conf, Xc, slab, truth, init, _ = load_input(conf, rank, world)
@@ -256,8 +275,7 @@ def main():
     def timed_arm(use_tree, sample_clocks):
         """W warm-up sweeps (CUDA-graph capture), then exactly K sweeps between CUDA events on
         the library's stream, barrier + synchronize on both sides, max over ranks."""
-        s = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                      rank=rank, world=world, nccl_id=new_nccl_id(), tree=use_tree)
+        s = new_ctx(tree=use_tree)
         s.set_tensor(Xd)                     # device-resident input (borrowed)
         s.set_factors(init)
         s.sweep(args.warmup)
@@ -290,8 +308,7 @@ def main():
                  "gpu_launches": int(l2)}
 
     # phase profile (separate short run; events around each phase on the library stream)
-    sp = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                   rank=rank, world=world, nccl_id=new_nccl_id(), profile=True, use_graph=False, tree=tree)
+    sp = new_ctx(profile=True, use_graph=False, tree=tree)
     prof = None
     if sp is not None:
         sp.set_tensor(Xd)
@@ -309,8 +326,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         Xh = torch.from_numpy(np.ascontiguousarray(slab)).pin_memory()
-        se = cpqr.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, device=local, stream=stream.cuda_stream,
-                       rank=rank, world=world, nccl_id=new_nccl_id(), tree=tree)
+        se = new_ctx(tree=tree)
         se.set_tensor(Xh)
         se.set_factors(init)
         se.sweep(1)
@@ -352,6 +368,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (synth.py seeded recipe of BASELINE.json config; no dataset)",
         "config": bench_config(conf, variant, world, tree),
+        "exchange": comm if (world > 1 or args.comm != "auto") else "none (one GPU)",
         "gpu_launches": int(launches),
     }
     if prof:

@@ -1652,6 +1652,8 @@ PeerPush make_push(const cpqr_ctx* c, int q) {
   pp.epoch = win_epoch(c, s);
   pp.gcount = c->dpushcnt;
   pp.parity_stride = (int64_t)pp.np * c->slot_elems;
+  static const bool sysf = getenv("CPQR_PEER_FENCE") && std::strcmp(getenv("CPQR_PEER_FENCE"), "sys") == 0;
+  pp.sysfence = sysf ? 1 : 0;
   return pp;
 }
 

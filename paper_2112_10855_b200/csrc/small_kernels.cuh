@@ -64,7 +64,7 @@ __global__ void k_sum_ranks(RankPtrs a, int nr, int64_t n, double* out) {
 //   push    the producing kernel (the Q0 apply's final sum, or k_peer_push) stores its result into
 //           slot s, parity e & 1, of EVERY rank's window with plain stores; each CTA that finishes
 //           rows fences at system scope and arrives on a grid counter; the last one to arrive
-//           fences again, raises flag[s] = e + 1 on every rank (st.release.sys) and advances the
+//           fences again, raises flag[s] = e + 1 on every rank and advances the
 //           local epoch;
 //   combine k_peer_combine on every rank waits until its p flags reach e + 1 (ld.acquire.sys),
 //           then sums the p slots in rank order (n < N) or places them by rank (mode N), so the
@@ -79,10 +79,8 @@ struct PeerPush {
   unsigned* gcount;                     // arrivals of the pushing grid's finishing CTAs (self re-arming)
   int64_t parity_stride;                // elements between the two parities of a slot
   int np;                               // ranks (0: no push)
+  int sysfence;                         // 1: every finishing CTA fences at system scope (see peer_push_done)
 };
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
@@ -94,20 +92,24 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
   return v;
 }
 // Called by all threads of a CTA once its peer stores are issued; `finishers` CTAs of the grid
-// call it exactly once each.  e: the epoch the CTA read before storing.
+// call it exactly once each.  e: the epoch the CTA read before storing.  One thread per CTA fences:
+// the barrier orders the CTA's stores before thread 0's fence, which is cumulative, so the arrival
+// cannot overtake them; the last CTA to arrive observes every arrival (device-scope atomics on the
+// local counter), fences at SYSTEM scope -- cumulative again over everything that happened before
+// it, the other CTAs' peer stores included (PTX memory model: causality order is transitive over
+// morally strong synchronisation) -- and only then raises the flags.  sysfence = 1 makes every
+// arrival fence at system scope too (CPQR_PEER_FENCE=sys; ~4 us more per exchange on one GPU).
 __device__ __forceinline__ void peer_push_done(const PeerPush& pp, unsigned long long e, unsigned finishers) {
-  __shared__ int s_last;
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(pp.gcount, 1u) == finishers - 1u);
-  __syncthreads();
-  if (!s_last) return;
+  if (threadIdx.x != 0) return;
+  if (pp.sysfence) __threadfence_system();
+  else __threadfence();
+  if (atomicAdd(pp.gcount, 1u) != finishers - 1u) return;
   __threadfence_system();
-  if ((int)threadIdx.x < pp.np) st_release_sys(pp.flag[threadIdx.x], e + 1ull);
-  if (threadIdx.x == 0) {
-    *pp.gcount = 0u;
-    *pp.epoch = e + 1ull;
-  }
+  for (int r = 0; r < pp.np; ++r)
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;\n" ::"l"(pp.flag[r]), "l"(e + 1ull) : "memory");
+  *pp.gcount = 0u;
+  *pp.epoch = e + 1ull;
 }
 // Stand-alone push of n doubles (the NE MTTKRP partial, scalars such as ||X||^2 and the DIRECT
 // residual); the QR path pushes from the Q0 apply itself.

@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--comm-us", type=float, default=15.0, help="assumed NCCL latency per mode (not measured)")
     ap.add_argument("--sweeps", type=int, default=3)
     ap.add_argument("--tree", action="store_true")
+    ap.add_argument("--comm", default="local", choices=["local", "local_peer"],
+                    help="virtual ranks' exchange: the sum kernel, or the fused peer push-reduce (push fused "
+                         "into the Q0 apply + combine kernel; its cost then shows in q0_apply and local_combine)")
     args = ap.parse_args()
     rows = []
     for cfg in args.configs:
@@ -47,7 +50,7 @@ def main():
         del Xc
         base = None
         for p in args.ps:
-            kw = dict(svd_tau=conf.svd_tau, tree=args.tree, world=p, comm="local")
+            kw = dict(svd_tau=conf.svd_tau, tree=args.tree, world=p, comm=args.comm if p > 1 else "local")
             s = cpqr.CPQR(conf.dims, conf.R, variant, profile=True, use_graph=False, **kw)
             s.set_tensor(Xd)
             s.set_factors(init)
@@ -82,7 +85,7 @@ def main():
             g.close()
             if base is None:
                 base = t_rank
-            row = dict(config=conf.name, variant=variant, tree=args.tree, p=p,
+            row = dict(config=conf.name, variant=variant, tree=args.tree, p=p, comm=args.comm,
                        per_sweep_ms=dict(stream_pass=stream, rest_ttm=rest, q0_apply=q0a, vn_qr=vn,
                                          factor_qr_tail=fqr, other=other, local_combine=exch),
                        slab_work_per_rank_ms=slab, projected_rank_ms=t_rank,
