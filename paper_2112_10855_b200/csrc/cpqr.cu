@@ -2328,7 +2328,7 @@ CPQR_API cpqr_status cpqr_debug_peer_put(cpqr_ctx* c, const double* src, int64_t
   if (!c || !src || n < 1) return CPQR_EINVAL;
   if (!c->peer || c->local) return fail(c, CPQR_EINVAL, "cpqr_debug_peer_put needs comm = CPQR_COMM_PEER");
   if (!c->peers_connected) return fail(c, CPQR_ESTATE, "cpqr_peer_connect first");
-  if (n > c->slot_elems) return fail(c, CPQR_EINVAL, "n exceeds the window slot (%lld)", (long long)c->slot_elems);
+  if (n > max_dim(c) * c->R) return fail(c, CPQR_EINVAL, "n exceeds max(I_k) R = %lld", (long long)(max_dim(c) * c->R));
   TRY(begin_call(c));
   CK(cudaMemcpyAsync(c->slabs[0].dWloc, src, sizeof(double) * n, cudaMemcpyHostToDevice, c->st));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sms));
@@ -2767,6 +2767,17 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
       CN(ncclAllReduce(c->dnX2, c->dnX2, 1, ncclDouble, ncclSum, c->comm, c->st));
     }
     TRY(build_plans(c));
+  }
+  if (c->peer && all) {  // a rank missing from the ||X||^2 exchange
+    unsigned fl = 0;
+    CK(cudaMemcpyAsync(&fl, c->dflags, sizeof(unsigned), cudaMemcpyDeviceToHost, c->st));
+    TRY(end_call(c));
+    if (fl & FLAG_PEER_TIMEOUT) {
+      c->have_tensor = false;
+      return fail(c, CPQR_ENCCL, "peer exchange of ||X||^2: a rank did not arrive within %llu ms",
+                  (unsigned long long)(c->peer_timeout_ns / 1000000ull));
+    }
+    return CPQR_OK;
   }
   return end_call(c);
 }

@@ -40,7 +40,9 @@ CASES = [(1, "QR", False, 1), (2, "QR", False, 1), (2, "NE", False, 1), (3, "QR"
          (5, "QR", False, 2), (5, "QR", False, 8), (3, "QR", False, 8), (3, "SVD", True, 4),
          (4, "SVD", False, 8), (2, "NE", False, 8),
          # CP-ALS-PINV on the ill-conditioned C2
-         (2, "PINV", False, 1), (2, "PINV", False, 4)]
+         (2, "PINV", False, 1), (2, "PINV", False, 4),
+         # the same slabs with the peer push-reduce exchange (CPQR_COMM_LOCAL_PEER, tests/test_gpu_peer.py)
+         (5, "QR", False, -8), (3, "QR", False, -8), (4, "SVD", False, -4), (2, "NE", False, -8)]
 
 
 def maxrel(a, b):
@@ -53,8 +55,10 @@ def test_fullsize_parity(cp, cfg, variant, tree, world):
     conf, Xc, truth, init = synth.make_problem(cfg)
     X = O.as_tensor(Xc)
     fit_mode = "direct" if cfg == 4 else "fast"
+    comm = "local_peer" if world < 0 else "local"  # world < 0: the peer push-reduce exchange
+    world = abs(world)
     s = cp.CPQR(conf.dims, conf.R, variant, svd_tau=conf.svd_tau, fit_mode=fit_mode, tree=tree,
-                world=world, comm="local")
+                world=world, comm=comm)
     Xd = torch.from_numpy(np.ascontiguousarray(Xc)).cuda()
     s.set_tensor(Xd)
     s.set_factors(init)
@@ -91,6 +95,8 @@ def test_fullsize_parity(cp, cfg, variant, tree, world):
         last = O.fit_direct(X, ref["lam"], ref["factors"])
     assert abs(fits[-1] - last) <= 1e-8, (cfg, fits[-1], last)
     assert np.max(np.abs(fits - np.array(ref["fits"]))) <= 1e-8
+    if comm == "local_peer":
+        assert s.debug_peer()["windows_differing"] == 0
     s.close()
     del Xd
     torch.cuda.empty_cache()
