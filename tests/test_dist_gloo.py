@@ -150,3 +150,27 @@ def test_dimension_tree_slab_decomposition_world2(dims, R):
     results = mgr.dict()
     mp.spawn(_tree_worker, args=(world, port, dims, R, results), nprocs=world, join=True)
     assert results.get(0) and results.get(1), dict(results)
+
+
+def test_bench_reference_arm_under_torchrun_world2():
+    """bench.py's launch contract on CPU: under torch.distributed.run with 2 ranks the reference arm
+    (the oracle) runs on rank 0 alone and prints exactly ONE JSON line; the other rank exits 0."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", f"--master-port={port}", os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+           "--config", "1", "--steps", "2", "--warmup", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 2 and d["unit"] == "sweeps/s"
+    assert d["config"]["workload"].startswith("C1") and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
