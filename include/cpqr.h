@@ -152,6 +152,12 @@ cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
  * CPQR_COMM_LOCAL either the whole tensor [0, I_N) (split into the p slabs) or one virtual
  * rank's slab (the sweep needs every slab set).  Computes ||X||^2 (summed over the ranks) and
  * clears the condition flags.
+ * Odd I_1: TMA needs 16-byte global strides, so the library stores mode 1 padded to I_1 + 1 with a
+ * zero row (in X and in A_1; exact: the pad row of every W_1, Ahat_1 and Q_1 stays zero).  The
+ * tensor is then COPIED into a context-owned padded buffer whatever `mem` says (a borrowed tensor
+ * too; host input is staged once on the device), costing prod(I_k) (1 + 1/I_1) extra doubles; all
+ * arrays the caller passes or receives keep I_1 rows.  CPQR_PAD_ODD=0 (environment, at create)
+ * keeps the unpadded layout and the slower register-staged stream kernels.
  * Errors: EINVAL (slab range / NULL / mem kind), ENOMEM, ECUDA, ENCCL. */
 cpqr_status cpqr_set_tensor(cpqr_ctx* ctx, const double* x, int64_t slab_begin,
                             int64_t slab_end, int mem);

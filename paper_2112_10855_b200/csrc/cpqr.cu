@@ -145,6 +145,11 @@ struct cpqr_ctx {
   // zero rows change nothing in CP-ALS (their rows of X are zero), their QR rows of R_k are exact
   // zeros, and V_n keeps only its prod_{k != n} min(I_k, R) nonzero rows (mixed radix vq).
   bool short_modes = false;
+  // odd I_1: mode 1 is stored padded to the next even size (a zero row in X and in A_1, the same
+  // exact-zero argument as above), because TMA needs 16-byte global strides: with an odd I_1 every
+  // A = prod_{j<k} I_j is odd and all stream passes would fall back to the register-staged kernels
+  // (the paper's 75^5 shape: 5x slower).  CPQR_PAD_ODD=0 keeps the unpadded layout.
+  bool pad1 = false;
   int64_t tdims[kMaxModes] = {0};
   int vq[kMaxModes] = {0};  // min(I_k, R): the V_n / Q0 row radix of mode k
   double* dVrs = nullptr;   // short modes: the shifted CholeskyQR factor R_s of V_n
@@ -2385,6 +2390,13 @@ CPQR_API cpqr_status cpqr_create(int N, const int64_t* dims, int R, int variant,
   if (c->opt.world > 1 && (dims[N - 1] % c->opt.world) != 0) { delete c; return CPQR_EINVAL; }
   c->variant = variant;
   if (c->short_modes && c->opt.world > 1) { delete c; return CPQR_EINVAL; }  // Kruskal input only
+  {
+    const char* po = getenv("CPQR_PAD_ODD");
+    if (!c->short_modes && (pdims[0] & 1) && !(po && atoi(po) == 0)) {
+      pdims[0] += 1;
+      c->pad1 = true;
+    }
+  }
   cpqr_status st = create_impl(c, N, pdims, R);
   if (st != CPQR_OK) {
     fprintf(stderr, "cpqr_create: %s: %s\n", cpqr_status_string(st), c->err.c_str());
@@ -2700,7 +2712,33 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
 // one slab's tensor: borrowed in place, or copied into a slab-owned buffer; its partial ||X||^2
 static cpqr_status set_slab(cpqr_ctx* c, Slab& sl, const double* x, int mem, double* nx2_out) {
   const size_t bytes = sizeof(double) * sl.numel;
-  if (mem == CPQR_MEM_DEVICE_BORROW) {
+  if (c->pad1) {
+    // odd I_1: every kind of input is copied into the slab-owned buffer with mode 1 padded to even
+    // (the pad row stays zero: written once here, never touched by the row copies)
+    const int64_t I = c->tdims[0], D = c->dims[0], rows = sl.numel / D;
+    if (sl.Xown_elems < (size_t)sl.numel) {
+      if (sl.Xown) dfree(sl.Xown);
+      sl.Xown = nullptr;
+      if (dmalloc(&sl.Xown, bytes) != cudaSuccess) return fail(c, CPQR_ENOMEM, "tensor (%zu bytes)", bytes);
+      sl.Xown_elems = sl.numel;
+    }
+    CK(cudaMemsetAsync(sl.Xown, 0, bytes, c->st));
+    const double* src = x;
+    double* stage = nullptr;
+    if (mem == CPQR_MEM_HOST) {  // one contiguous H2D copy, then the padding on the device
+      if (dmalloc(&stage, sizeof(double) * I * rows) != cudaSuccess)
+        return fail(c, CPQR_ENOMEM, "tensor staging (%zu bytes)", sizeof(double) * (size_t)(I * rows));
+      CK(cudaMemcpyAsync(stage, x, sizeof(double) * I * rows, cudaMemcpyHostToDevice, c->st));
+      src = stage;
+    }
+    k_pad_rows<<<c->sms * 8, 256, 0, c->st>>>(src, I, D, rows, sl.Xown);
+    CKL();
+    if (stage) {
+      CK(cudaStreamSynchronize(c->st));
+      dfree(stage);
+    }
+    sl.X = sl.Xown;
+  } else if (mem == CPQR_MEM_DEVICE_BORROW) {
     if (sl.Xown) { dfree(sl.Xown); sl.Xown = nullptr; sl.Xown_elems = 0; }
     sl.X = x;
   } else {
@@ -2744,7 +2782,7 @@ CPQR_API cpqr_status cpqr_set_tensor(cpqr_ctx* c, const double* x, int64_t b, in
   TRY(begin_call(c));
   CK(cudaMemsetAsync(c->dflags, 0, sizeof(unsigned) * 4, c->st));
   c->flags = 0;
-  const int64_t slice = prod(c->dims, 0, c->N - 1);  // elements per index of the last mode
+  const int64_t slice = prod(c->tdims, 0, c->N - 1);  // elements per index of the last mode (caller's layout)
   for (int q = q0; q < q1; ++q) {
     const double* xs = x + (c->slabs[q].b - b) * slice;
     TRY(set_slab(c, c->slabs[q], xs, mem, c->nslab > 1 ? c->dnX2p + q : c->dnX2));
@@ -3089,7 +3127,9 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
     if (Qo && k != n && Qo[k]) {
       CK(sc.alloc(&tmpQ[k], sizeof(double) * c->dims[k] * R));
       CK(sc.alloc(&tmpQt[k], sizeof(double) * c->dims[k] * c->RQ));
-      CK(cudaMemcpyAsync(tmpQ[k], Qo[k], sizeof(double) * c->dims[k] * R, cudaMemcpyHostToDevice, c->st));
+      if (c->tdims[k] != c->dims[k]) CK(cudaMemsetAsync(tmpQ[k], 0, sizeof(double) * c->dims[k] * R, c->st));
+      CK(cudaMemcpy2DAsync(tmpQ[k], sizeof(double) * c->dims[k], Qo[k], sizeof(double) * c->tdims[k],
+                           sizeof(double) * c->tdims[k], R, cudaMemcpyHostToDevice, c->st));
       k_transpose_pad<<<64, 256, 0, c->st>>>(tmpQ[k], c->dims[k], (int)c->dims[k], R, c->RQ, tmpQt[k]);
       CKL();
     }
@@ -3148,15 +3188,20 @@ CPQR_API cpqr_status cpqr_debug_mode(cpqr_ctx* c, int n, const double* const* Qo
   }
   std::vector<double> w((size_t)c->dims[n] * R);
   CK(cudaMemcpyAsync(w.data(), c->dW, sizeof(double) * w.size(), cudaMemcpyDeviceToHost, c->st));
-  if (Y_out) CK(cudaMemcpyAsync(Y_out, yfull, sizeof(double) * ytot, cudaMemcpyDeviceToHost, c->st));
+  if (Y_out && n == 0 && c->tdims[0] != c->dims[0]) {  // mode 1 stored padded: drop the pad row of every fibre
+    CK(cudaMemcpy2DAsync(Y_out, sizeof(double) * c->tdims[0], yfull, sizeof(double) * c->dims[0],
+                         sizeof(double) * c->tdims[0], (size_t)(ytot / c->dims[0]), cudaMemcpyDeviceToHost, c->st));
+  } else if (Y_out) {
+    CK(cudaMemcpyAsync(Y_out, yfull, sizeof(double) * ytot, cudaMemcpyDeviceToHost, c->st));
+  }
   int64_t J = 1;
   for (int k = 0; k < N - 1; ++k) J *= R;
   if (Q0_out) CK(cudaMemcpyAsync(Q0_out, c->dQ0, sizeof(double) * J * R, cudaMemcpyDeviceToHost, c->st));
   if (R0_out) CK(cudaMemcpyAsync(R0_out, c->dR0, sizeof(double) * R * R, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if (W_out)
-    for (int64_t i = 0; i < c->dims[n]; ++i)
-      for (int r = 0; r < R; ++r) W_out[i + c->dims[n] * r] = w[i * R + r];
+    for (int64_t i = 0; i < c->tdims[n]; ++i)
+      for (int r = 0; r < R; ++r) W_out[i + c->tdims[n] * r] = w[i * R + r];
   return end_call(c);
 }
 

@@ -41,6 +41,14 @@ __global__ void k_sumsq_partial(const double* __restrict__ X, int64_t n, double*
   s = block_sum(s, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
+// dst (D x rows, column-major) <- src (I x rows), I < D; the pad rows of dst are left untouched
+__global__ void k_pad_rows(const double* __restrict__ src, int64_t I, int64_t D, int64_t rows, double* __restrict__ dst) {
+  const int64_t n = I * rows;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / I, i = e - r * I;
+    dst[r * D + i] = __ldcs(src + e);
+  }
+}
 // Sum of the virtual ranks' partial results in rank order (CPQR_COMM_LOCAL's all-reduce):
 // out[e] = (((p0[e] + p1[e]) + p2[e]) + ...); out may alias p[0].
 constexpr int kMaxRanks = 16;

@@ -1157,8 +1157,11 @@ def test_cost_accounting_matches_oracle_ttm_cost(cp, dims, R, tree):
     (cpqr_debug_plan) follow Eq. (TTMcost): for every mode, in the library's own
     contraction order, the steps' flops sum to the oracle's ttm_cost(dims, n, R, order) (fused slice
     steps count both contractions); and cpqr_get_profile's flops0 / bytes0 equal the stream-X
-    passes' first steps and N (or 2 with the dimension tree) reads of X."""
+    passes' first steps and N (or 2 with the dimension tree) reads of X.  The library stores an
+    odd I_1 padded to I_1 + 1 (a zero row, cpqr.h cpqr_set_tensor: TMA needs 16-byte strides) and
+    counts the work it executes, so the paper's formula is evaluated on the stored dims."""
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=5)
+    stored = (dims[0] + (dims[0] & 1),) + tuple(dims[1:])
     s = cp.CPQR(dims, R, "QR", profile=True, use_graph=False, tree=tree)
     s.set_tensor(Xc)
     s.set_factors(init)
@@ -1169,14 +1172,14 @@ def test_cost_accounting_matches_oracle_ttm_cost(cp, dims, R, tree):
         order = [k for st in pl for k in st["modes"]]
         if not tree:
             assert sorted(order) == [k for k in range(N) if k != n]
-            assert sum(st["flops"] for st in pl) == O.ttm_cost(dims, n, R, order=order), (n, pl)
+            assert sum(st["flops"] for st in pl) == O.ttm_cost(stored, n, R, order=order), (n, pl)
         if pl and pl[0]["x_pass"]:
             first += pl[0]["flops"]
             passes += 1
     p = s.profile()
     s.close()
     assert passes == (2 if tree else N)
-    assert p["flops0"] == first and p["bytes0"] == passes * 8.0 * np.prod(dims)
+    assert p["flops0"] == first and p["bytes0"] == passes * 8.0 * np.prod(stored)
 
 
 def _kt_oracle(variant, lam, B, A0, sweeps, fit_mode="fast"):
@@ -1231,3 +1234,65 @@ def test_short_modes_direct_fit_and_errors(cp):
     s.close()
     ref = _kt_oracle("QR", lam, B, A0, 3, fit_mode="direct")
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-10, (f, ref["fits"])
+
+
+@pytest.mark.parametrize("variant,tree,mem", [("QR", False, "host"), ("SVD", True, "borrow"), ("NE", False, "copy"),
+                                              ("PINV", False, "host"), ("QR", False, "borrow")])
+@pytest.mark.parametrize("dims,R", [((35, 34, 33), 6), ((75, 40, 33), 32), ((15, 14, 13, 12), 5), ((9, 7, 5, 6, 8), 4)])
+def test_odd_first_mode_is_padded_for_tma(cp, dims, R, variant, tree, mem):
+    """Odd I_1 (the paper's 75^5 shape): mode 1 is stored padded to even so the TMA
+    stream kernels run (cpqr.h cpqr_set_tensor); host, copied and borrowed tensors all take the
+    padded copy.  The plans must use the TMA kernels on X, Y / W / factors / fits match the oracle
+    on the true dims, and CPQR_PAD_ODD=0 (the unpadded fallback kernels) gives the same results."""
+    import os
+    import torch
+    if R > min(dims):
+        pytest.skip("tall factors only")
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=900 + R + len(dims))
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    ne = variant in ("NE", "PINV")
+
+    def make():
+        s = cp.CPQR(dims, R, variant, tree=tree)
+        if mem == "host":
+            s.set_tensor(Xc)
+        else:
+            s.set_tensor(torch.from_numpy(np.ascontiguousarray(Xc)).cuda(), copy=(mem == "copy"))
+        s.set_factors(init)
+        return s
+    s = make()
+    kinds = [st["kind"] for n in range(N) for st in s.debug_plan(n) if st["x_pass"]]
+    assert kinds and all("tma" in k for k in kinds), kinds
+    if not ne:
+        Qs, Rs = zip(*[O.qr_pos(a) for a in init])
+        for n in range(N):
+            out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+            Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+            assert out["Y"].shape == Yo.shape and rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+            Q0o, R0o = O.structured_qr(list(Rs), n)
+            assert rel(out["W"], O.apply_q0(Yo, n, Q0o)) <= 1e-11
+    ref1 = O.cp_als_ne(X, init, 1, solve="pinv" if variant == "PINV" else "chol") if ne else \
+        O.cp_als_qr(X, init, 1, variant=variant)
+    ref = O.cp_als_ne(X, init, 3, solve="pinv" if variant == "PINV" else "chol") if ne else \
+        O.cp_als_qr(X, init, 3, variant=variant)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    assert [a.shape for a in A] == [(d, R) for d in dims]
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(2)])
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    lam3, A3 = s.get_factors()
+    s.close()
+    os.environ["CPQR_PAD_ODD"] = "0"
+    try:
+        u = make()
+    finally:
+        del os.environ["CPQR_PAD_ODD"]
+    fu = u.sweep(3)
+    lamu, Au = u.get_factors()
+    u.close()
+    assert np.max(np.abs(fu - f)) <= 1e-9
+    for k in range(N):
+        assert rel(Au[k], A3[k]) <= 1e-8
