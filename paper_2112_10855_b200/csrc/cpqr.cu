@@ -402,6 +402,7 @@ struct PlanIn {
   bool ne;
   bool tma;
   bool fuse;  // fused two-mode slice kernel allowed for n >= 3
+  int pad0 = 0;  // 1: mode 1 is stored padded by one row (odd I_1): orders compare the true dimension
   int sms;
   bool tree = false;        // dimension-tree Multi-TTM (QR/SVD variants)
   int h = 0;                // tree split: halves [0, h) and [h, N)
@@ -549,9 +550,10 @@ int stages_for(size_t stage, size_t extra, const char* kind_env, int cap = 8) {
 
 // Multi-TTM Y = X x_{k != n} Q_k^T (Alg. 2 line 8).  Stream-X pass: modes 1 and 2 together
 // (fused slice kernel) when n >= 3 and the pass is HBM-bound (R < 24: R/4 flop per byte is below
-// the FP64-DMMA : HBM balance of ~5.7); when it is FP64-bound (R >= 24) mode 2 alone (strided
-// kernel over the middle mode, no second contraction on the critical DMMA loop); for n < 3 the
-// last mode (strided kernel, the largest contiguous GEMM).  The remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
+// the FP64-DMMA : HBM balance of ~5.7); when it is FP64-bound (R >= 24) one mode alone, no second
+// contraction on the critical DMMA loop: for N = 3 the middle mode (strided kernel), for N >= 4 the
+// largest dimension, ties to the highest mode (the strided kernel's slices then have the most
+// rows); for n < 3 the last mode (strided kernel, the largest contiguous GEMM).  The remaining TTMs run on the (R/I)-smaller intermediate in decreasing-dimension order
 // (ties by decreasing mode, reading 5).  TMA kernels whenever the layout allows
 // (even leading dimension, 16-B aligned base), else the register-staged kernels.
 // N-tiles of 8 fibres per consumer warp in the fused slice kernel (box height kCW * 8 * NF)
@@ -592,6 +594,9 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     const uint32_t box[2] = {16, 16};
     return in.Qt[k] && make_tmap(&s.mq, in.Qt[k], 2, d, st, box);
   };
+  // dimension of mode k for the contraction orders: the pad row of an odd I_1 is not
+  // a reason to contract mode 1 first
+  auto dim_of = [&](int k) { return (k == 0 && cur[0] == in.ld[0]) ? cur[0] - in.pad0 : cur[k]; };
   double* out_override = nullptr;  // tree plans: the last step of a half pass writes the tree buffer
   auto advance = [&](double* out) {  // the next step reads `out`
     src = out;
@@ -822,7 +827,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         // the right half's modes by decreasing LOCAL dimension, ties last mode first
         // (strided, B = 1): with slabs the slab mode is the smallest and goes last
         for (int k = N - 1; k >= h; --k) ord.push_back(k);
-        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cur[a] > cur[b]; });
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return dim_of(a) > dim_of(b); });
         for (size_t q = 0; q < ord.size(); ++q) {
           if (q + 1 == ord.size()) out_override = in.tbuf;
           emit_ttm(ord[q]);
@@ -835,9 +840,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
           emit_ttm(k);
         }
       } else {
-        if (h >= 2) ord.push_back(1);  // middle mode (strided), then mode 0 (fibres), then the rest
-        ord.push_back(0);
-        for (int k = 2; k < h; ++k) ord.push_back(k);
+        // the left half's modes by decreasing dimension, ties highest mode first (the strided kernel
+        // with the most rows A per slice; mode 0, the fibre kernel, last): h = 2 gives (1, 0)
+        for (int k = h - 1; k >= 0; --k) ord.push_back(k);
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return dim_of(a) > dim_of(b); });
         for (size_t q = 0; q < ord.size(); ++q) {
           if (q + 1 == ord.size()) out_override = in.tbuf;
           emit_ttm(ord[q]);
@@ -850,10 +856,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
       for (int k = o0; k < o1; ++k) cur[k] = R;
     }
     for (int k = left ? 0 : h; k < (left ? h : N); ++k) if (k != n) todo.push_back(k);
-  } else if (N >= 3 && n >= 2 && !in.fuse && !(N == 3 && in.overlap)) {
-    emit_ttm(1);  // stream pass over the middle mode (strided kernel), then the rest
-    for (int k = 0; k < N; ++k) if (k != n && k != 1) todo.push_back(k);
-  } else if (N >= 3 && n >= 2 && !(N == 3 && in.overlap)) {
+  } else if (N == 3 && n == 2 && !in.fuse && !in.overlap) {
+    emit_ttm(1);  // stream pass over the middle mode (strided kernel), then mode 0 on the intermediate
+    todo.push_back(0);
+  } else if (N >= 3 && n >= 2 && in.fuse && !(N == 3 && in.overlap)) {
     emit_slice();
     for (int k = 2; k < N; ++k) if (k != n) todo.push_back(k);
   } else if (N == 3 && in.overlap) {
@@ -866,16 +872,18 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     // n < 2: the stream pass contracts the largest LOCAL dimension first; ties go to
     // the last mode (strided kernel, B = 1, the largest contiguous GEMM).  With p > 1 slabs the last
     // mode is the smallest local one and is contracted last, so every intermediate scales as 1/p.
-    int f = N - 1;
-    for (int k = N - 2; k >= 0; --k)
-      if (k != n && cur[k] > cur[f]) f = k;
+    // (Also n >= 2 without the fused slice pass, N >= 4: contracting mode 1 first there gave the
+    // strided kernel slices of only A = I_1 rows -- 75^5 R = 32: 16.4 ms per pass against 5.7.)
+    int f = (n == N - 1) ? N - 2 : N - 1;
+    for (int k = f - 1; k >= 0; --k)
+      if (k != n && dim_of(k) > dim_of(f)) f = k;
     emit_ttm(f);
     for (int k = 0; k < N; ++k) if (k != n && k != f) todo.push_back(k);
   } else {
     todo.push_back(1 - n);
   }
   std::sort(todo.begin(), todo.end(), [&](int a, int b) {
-    if (cur[a] != cur[b]) return cur[a] > cur[b];
+    if (dim_of(a) != dim_of(b)) return dim_of(a) > dim_of(b);
     return a > b;
   });
   for (int k : todo) emit_ttm(k);
@@ -941,12 +949,28 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
     const size_t stage = (size_t)(2 * cw + NQB) * kBoxBytes;
     const int S = cw == 4 ? std::min<int>(s.S, (int)((110 * 1024 - 3072) / stage)) : s.S;
     const size_t smem = 3072 + (size_t)S * stage;
-    const int64_t units = ((s.A + 32 * cw - 1) / (32 * cw)) * s.B;
+    // rows of a slice per unit: 32 wa, with wb = cw / wa consecutive slices per unit (k_strided_tma).
+    // wa = cw unless a shorter unit fills its M-tiles at least 10 % better (short slices: A = R or a
+    // small I_1 after the leading modes are contracted; 75^5 R = 32: A = 32 ran at 1/8 of the tiles)
+    static const int wa_env = getenv("CPQR_STR_WA") ? atoi(getenv("CPQR_STR_WA")) : 0;
+    auto fill = [&](int wa) {
+      const int wb = cw / wa;
+      const double fa = (double)s.A / (32.0 * wa * (double)((s.A + 32 * wa - 1) / (32 * wa)));
+      const double fb = (double)s.B / ((double)wb * (double)((s.B + wb - 1) / wb));
+      return fa * fb;
+    };
+    int wa = cw;
+    for (int w = cw / 2; w >= 1; w /= 2)
+      if (fill(w) > 1.10 * fill(wa)) wa = w;
+    if (wa_env >= 1 && wa_env <= cw && (cw % wa_env) == 0) wa = wa_env;
+    const int wbs = cw / wa;
+    const int64_t units = ((s.A + 32 * wa - 1) / (32 * wa)) * ((s.B + wbs - 1) / wbs);
     const int grid = (int)std::min<int64_t>(units, (int64_t)sms * (cw == 4 ? 2 : 1));
     // stream-K split (k_strided_tma) when the round-robin waves are ragged by > 2 %: e.g. C5 at 8
     // slabs, 500 units on 147 CTAs.  CPQR_STREAMK=0/1 forces it off / on.
     const double waves = (double)units / grid;
-    const bool sk = s.P && grid > 1 && units > grid && (s.skm == 1 || (s.skm != 0 && std::ceil(waves) / waves > 1.02));
+    const bool sk = wa == cw && s.P && grid > 1 && units > grid &&
+                    (s.skm == 1 || (s.skm != 0 && std::ceil(waves) / waves > 1.02));
     double* P = sk ? s.P : nullptr;
     // the fix-up is fused into the kernel (last-arriving CTA per cut unit); CPQR_SK_FIXUP=1 keeps the
     // separate k_strided_fixup launch (same sums, same order)
@@ -956,10 +980,10 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
   {                                                                                                     \
     if (cw == 4) {                                                                                      \
       set_smem(k_strided_tma<NTV, NPV, 4>, smem);                                                       \
-      launch_ex(k_strided_tma<NTV, NPV, 4>, grid, (4 + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P, skc); \
+      launch_ex(k_strided_tma<NTV, NPV, 4>, grid, (4 + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P, skc, wa); \
     } else {                                                                                            \
       set_smem(k_strided_tma<NTV, NPV>, smem);                                                          \
-      launch_ex(k_strided_tma<NTV, NPV>, grid, (kCW + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P, skc); \
+      launch_ex(k_strided_tma<NTV, NPV>, grid, (kCW + NPV) * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, s.B, R, s.out, S, P, skc, wa); \
     }                                                                                                   \
   }
     // producer warps issuing the 16 X boxes of a stage in parallel: a single issuing thread bounds
@@ -1106,6 +1130,7 @@ void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* 
   in.ne = ne;
   in.tma = c->use_tma;
   in.fuse = c->fuse_slice;
+  in.pad0 = c->pad1 ? 1 : 0;
   in.sms = c->stream_sms;
   in.tree = c->tree && !ne;
   in.h = c->tree_h;

@@ -208,11 +208,17 @@ __device__ __forceinline__ int sk_cta_of(int64_t it, int64_t W, int G) {
   return (int)(((it + 1) * G + W - 1) / W) - 1;
 }
 
+//
+// Short slices (wa < CW).  A unit is 32 wa rows of wb = CW / wa consecutive slices b: warp w owns
+// rows 32 (w mod wa) .. +31 of slice b0 + w / wa.  With A < 32 CW rows per slice (intermediates
+// whose leading modes are already contracted, A = R; the paper's 75^5 shape, A = 76) a unit of one
+// slice would leave most of its M-tiles empty; the host picks the wa in {1, 2, 4, 8} that fills
+// them best (launch_tma).  wa = CW is the layout above; the stream-K split needs it.
 template <int NT, int NP = 1, int CW = kCW>
 __global__ void __launch_bounds__((CW + NP) * 32, CW == 4 ? 2 : 1)
 k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A,
               int I, int64_t B, int R, double* __restrict__ T, int S, double* __restrict__ P,
-              unsigned* __restrict__ cnt) {
+              unsigned* __restrict__ cnt, int wa) {
   extern __shared__ uint8_t smraw[];
   constexpr int NQB = (NT + 1) / 2;
   constexpr uint32_t XBYTES = 2 * CW * kBoxBytes, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
@@ -229,8 +235,9 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   __syncthreads();
   if (threadIdx.x == 0) prefetch_tmap(&tmX);
   pdl_wait();                // the predecessor (previous mode's tail: Q panels) has completed
-  const int64_t nA = (A + 32 * CW - 1) / (32 * CW);
-  const int64_t units = nA * B;
+  const int wb = CW / wa;
+  const int64_t nA = (A + 32 * wa - 1) / (32 * wa);
+  const int64_t units = nA * ((B + wb - 1) / wb);
   const int KS = (I + kBK - 1) / kBK;
   const SkRange rg(units * KS, blockIdx.x, gridDim.x);
   // the unit segments [ks0, ks1) of this CTA, in order: round robin (P == nullptr) or stream-K
@@ -259,16 +266,27 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
       const uint64_t pol = policy_evict_first();
       RingPos rp;
       segments([&](int64_t u, int ks0, int ks1) {
-        const int b = (int)(u / nA);
-        const int a0 = (int)((u - (int64_t)b * nA) * 32 * CW);
+        const int64_t bq = u / nA;
+        const int a0 = (int)((u - bq * nA) * 32 * wa);
+        const int64_t b0 = bq * wb;
+        // box q belongs to warp q / 2: rows a0 + 32 (w mod wa) + 16 (q & 1) of slice b0 + w / wa; a
+        // warp beyond the unit's wb slices (CW not a multiple of wa) gets slice B: zero fill, no read
+        int qa[2 * CW / NP], qb[2 * CW / NP];
+#pragma unroll
+        for (int j = 0; j < 2 * CW / NP; ++j) {
+          const int q = pw * (2 * CW / NP) + j, w = q >> 1;
+          qa[j] = a0 + 32 * (w % wa) + 16 * (q & 1);
+          const int64_t bb = b0 + w / wa;
+          qb[j] = (w / wa < wb && bb < B) ? (int)bb : (int)B;
+        }
         for (int ks = ks0; ks < ks1; ++ks, rp.next(S)) {
           const int s = rp.s;
           mbar_wait(&empty[s], rp.ph ^ 1);
           if (pw == 0) mbar_expect_tx(&full[s], STAGE);
           uint8_t* dst = st0 + (size_t)s * STAGE;
-#pragma unroll 4
-          for (int q = pw * (2 * CW / NP); q < (pw + 1) * (2 * CW / NP); ++q)
-            tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
+#pragma unroll
+          for (int j = 0; j < 2 * CW / NP; ++j)
+            tma_load_3d_ef(dst + (pw * (2 * CW / NP) + j) * kBoxBytes, &tmX, qa[j], ks * kBK, qb[j], &full[s], pol);
           if (pw == 0)
 #pragma unroll
             for (int q = 0; q < NQB; ++q) tma_load_2d(dst + XBYTES + q * kBoxBytes, &tmQ, 16 * q, ks * kBK, &full[s]);
@@ -281,9 +299,11 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   const int g = lane >> 2, t = lane & 3;
   const int64_t first_u = rg.it0 / KS;
   RingPos rp;
+  const int wai = warp % wa, wbi = warp / wa;
   segments([&](int64_t u, int ks0, int ks1) {
-    const int64_t b = u / nA;
-    const int64_t a0 = (u - b * nA) * 32 * CW;
+    const int64_t bq = u / nA;
+    const int64_t a0 = (u - bq * nA) * 32 * wa;
+    const int64_t b = bq * wb + wbi;  // this warp's slice (beyond B or the unit's wb slices: idle)
     double acc[4][NT][2];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
@@ -316,16 +336,22 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
       consumer_release(&empty[s], lane, acc_dep(acc));
     }
     if (ks0 == 0 && ks1 == KS) {  // the whole unit: straight to T
+      // M-tiles 2p and 2p + 1 hold the adjacent rows 2g and 2g + 1 of the same columns: one 16-byte
+      // store per column (A is even -- the TMA map requires it -- so the pair is aligned and inside
+      // A together), and the 8 lanes g of a column write 128 contiguous bytes
       double* __restrict__ Tb = T + A * (int64_t)R * b;
+      const bool live = wbi < wb && b < B;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int64_t row = a0 + 32 * warp + 16 * (m >> 1) + 2 * g + (m & 1);
-        if (row >= A) continue;
+      for (int p = 0; p < 2; ++p) {
+        const int64_t row = a0 + 32 * wai + 16 * p + 2 * g;
+        if (row >= A || !live) continue;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const int r0 = 8 * n + 2 * t;
-          if (r0 < R) Tb[row + A * r0] = acc[m][n][0];
-          if (r0 + 1 < R) Tb[row + A * (r0 + 1)] = acc[m][n][1];
+          if (r0 < R)
+            *reinterpret_cast<double2*>(Tb + row + A * r0) = make_double2(acc[2 * p][n][0], acc[2 * p + 1][n][0]);
+          if (r0 + 1 < R)
+            *reinterpret_cast<double2*>(Tb + row + A * (r0 + 1)) = make_double2(acc[2 * p][n][1], acc[2 * p + 1][n][1]);
         }
       }
     } else {  // a stream-K partial: this CTA's slot (first or last unit of its range)
