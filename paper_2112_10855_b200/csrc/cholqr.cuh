@@ -92,8 +92,18 @@ __global__ void __launch_bounds__(256) k_cq_gram1(CqArgs a) {
   if (b == 0 && tid == 0) atomicAnd(a.flags, ~cq_hh_bit(a));  // per-mode decision
   const int r0 = b * a.mb, rows = min(a.m, r0 + a.mb) - r0, ld = rows | 1;
   if (!a.solve) {
-    for (int c = 0; c < R; ++c)
-      for (int i = tid; i < rows; i += blockDim.x) P[i + ld * c] = a.A[r0 + i + (int64_t)a.m * c];
+    // blockDim >= rows: one row per thread, eight columns' loads in flight
+    if (tid < rows) {
+      int c = 0;
+      for (; c + 8 <= R; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = a.A[r0 + tid + (int64_t)a.m * (c + q)];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) P[tid + ld * (c + q)] = v[q];
+      }
+      for (; c < R; ++c) P[tid + ld * c] = a.A[r0 + tid + (int64_t)a.m * c];
+    }
   } else {
     for (int e = tid; e < RB * RB; e += blockDim.x) {
       const int r = e % RB, c = e / RB;
@@ -201,12 +211,21 @@ __device__ void cq_chol(const CqArgs& a, double* Gs, double* Ls, bool pass1, boo
 
 // First level of the Gram-partial sum for very tall panels (nb > 1024 row blocks, e.g. the
 // 10-way sine of sums' 134M-row V_n): CTA g adds blocks [g per, (g+1) per) in order; the Cholesky
-// kernels then add the <= 1024 group sums in order (fixed two-level order, deterministic).
+// kernels then add the <= 1024 group sums in order (fixed two-level order, deterministic).  Eight
+// loads in flight per thread (the adds stay in block order): with one it ran at 50 GB/s.
 __global__ void k_reduce_gp(const double* __restrict__ in, int nb, int RR, int per, double* __restrict__ out) {
   const int g = blockIdx.x, b0 = g * per, b1 = min(nb, b0 + per);
   for (int e = threadIdx.x; e < RR; e += blockDim.x) {
     double s = 0.0;
-    for (int b = b0; b < b1; ++b) s += in[(int64_t)b * RR + e];
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(in + (int64_t)(b + q) * RR + e);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; b < b1; ++b) s += __ldcg(in + (int64_t)b * RR + e);
     out[(int64_t)g * RR + e] = s;
   }
 }

@@ -1339,7 +1339,9 @@ cpqr_status launch_cq_compact(cpqr_ctx* c, const CqArgs& q, int RB, int tb, cuda
 CqArgs cq_reduced(cpqr_ctx* c, const CqArgs& q, cudaStream_t st) {
   if (q.nb <= 1024) return q;
   CqArgs r = q;
-  const int per = 512, ng = (q.nb + per - 1) / per;
+  // groups of >= 32 blocks, at most 1024 of them (c->dGp2): 4096 blocks -> 128 CTAs (8 CTAs of 512
+  // blocks each took 0.65 ms of the 1M-row V_n QR, twice per mode)
+  const int per = std::max(32, (q.nb + 1023) / 1024), ng = (q.nb + per - 1) / per;
   k_reduce_gp<<<ng, 128, 0, st>>>(q.Gp, q.nb, q.R * q.R, per, c->dGp2);
   r.Gp = c->dGp2;
   r.nb = ng;
@@ -1637,6 +1639,25 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
 cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const PeerPush& pp = PeerPush{}) {
   const int64_t J = p.Aa * p.Bb, KT = (J + 3) / 4;
   const int In = (int)p.In;
+  // a large V_n: 4 M-tiles per CTA so that Q0 is read once per 32 rows of Y_(n) (k_q0_apply_big)
+  const char* big_s = getenv("CPQR_Q0_BIG");  // 0 / 1: never / always (tests); read per launch
+  const int big_env = big_s ? atoi(big_s) : -1;
+  if (!c->q0_stair && In > 8 && (big_env == 1 || (big_env != 0 && J >= 32768))) {
+    constexpr int MTL = 4;
+    const int groups = (In + 8 * MTL - 1) / (8 * MTL);
+    int64_t KS = std::max<int64_t>(1, std::min<int64_t>((2 * c->sms + groups - 1) / groups, (KT + 7) / 8));
+    KS = std::min<int64_t>(KS, kQ0MaxSlices);
+    const int kpc = (int)((KT + KS - 1) / KS);
+    KS = (KT + kpc - 1) / kpc;
+    dim3 grid(groups, (unsigned)KS);
+#define Q0B(NTV)                                                                                          \
+  launch_ex(k_q0_apply_big<NTV, MTL>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb, (const double*)c->dQ0, \
+            c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, pp)
+    switch ((c->R + 7) / 8) { case 1: Q0B(1); break; case 2: Q0B(2); break; case 3: Q0B(3); break; default: Q0B(4); break; }
+#undef Q0B
+    CKL();
+    return CPQR_OK;
+  }
   const int iblocks = (In + 7) / 8;
   // slices of Q0's k-steps so that ~2 CTAs per SM run, each with >= 1 k-step per warp
   int64_t KS = std::max<int64_t>(1, std::min<int64_t>((2 * c->sms + iblocks - 1) / iblocks, (KT + 7) / 8));
@@ -2659,7 +2680,7 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
   }
   {  // first-level Gram sums of the multi-kernel CholeskyQR beyond 1024 row blocks (cq_reduced)
     const int64_t nbmax = std::max<int64_t>((imax + 255) / 256, c->vn_cq ? (J + 255) / 256 : 0);
-    if (nbmax > 1024) CK(dmalloc(&c->dGp2, sizeof(double) * ((nbmax + 511) / 512 + 1) * R * R));
+    if (nbmax > 1024) CK(dmalloc(&c->dGp2, sizeof(double) * 1025 * R * R));
   }
   // PEER ranks need no communicator; with an id they get one (cpqr_debug_mode's Y collectives)
   if ((c->opt.world > 1 && !c->local && (!c->peer || have_id)) || nccl1) {

@@ -492,6 +492,97 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
   if (pp.np) peer_push_done(pp, pe, gridDim.x);  // one finisher per row block
 }
 
+// Large V_n (the 5-way high-rank regime: 75^5 at R = 32 has a 1M x 32 Q0 of 268 MB
+// beside a 629 MB Y_(n)): the dense apply with MTL 8-row M-tiles per CTA, so each Q0 fragment feeds
+// MTL DMMAs and Q0 is read ceil(In / (8 MTL)) times instead of ceil(In / 8).  Same k-slices, warp
+// and slice sums in the same fixed orders as k_q0_apply_tc; counters / Wp indexed by row group.
+template <int NT, int MTL>
+__global__ void __launch_bounds__(256)
+k_q0_apply_big(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, const double* __restrict__ Q0, int R,
+               int kpc, int KS, double* __restrict__ Wp, unsigned* __restrict__ counters, double* __restrict__ W,
+               const __grid_constant__ PeerPush pp) {
+  __shared__ double red[8][64 * NT];
+  __shared__ int last;
+  pdl_wait();
+  const unsigned long long pe = pp.np ? ld_relaxed_sys(pp.epoch) : 0ull;
+  const int64_t poff = (pe & 1ull) ? pp.parity_stride : 0;
+  const int64_t J = Aa * Bb, KT = (J + 3) / 4;
+  const int ib = blockIdx.x, ks = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double acc[MTL][NT][2];
+#pragma unroll
+  for (int m = 0; m < MTL; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  const int64_t kb = (int64_t)ks * kpc, ke = min(KT, kb + kpc);
+#pragma unroll 2
+  for (int64_t kk = kb + warp; kk < ke; kk += 8) {
+    const int64_t j = 4 * kk + t;
+    const bool jin = j < J;
+    const int64_t bq = jin ? j / Aa : 0, aa = jin ? j - bq * Aa : 0;
+    double bv[NT], av[MTL];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int c = 8 * n + g;
+      bv[n] = (jin && c < R) ? __ldg(Q0 + j + J * c) : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < MTL; ++m) {
+      const int i = (ib * MTL + m) * 8 + g;
+      av[m] = (jin && i < In) ? __ldg(Y + aa + Aa * (i + (int64_t)In * bq)) : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < MTL; ++m)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dmma(acc[m][n][0], acc[m][n][1], av[m], bv[n]);
+  }
+#pragma unroll
+  for (int m = 0; m < MTL; ++m) {
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      red[warp][g * 8 * NT + 8 * n + 2 * t] = acc[m][n][0];
+      red[warp][g * 8 * NT + 8 * n + 2 * t + 1] = acc[m][n][1];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * NT; e += blockDim.x) {
+      const int r = e / (8 * NT), c = e % (8 * NT), ii = (ib * MTL + m) * 8 + r;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w][e];
+      if (ii < In && c < R) {
+        if (KS == 1) {
+          W[(int64_t)ii * R + c] = s;
+          for (int q = 0; q < pp.np; ++q) pp.dst[q][poff + (int64_t)ii * R + c] = s;
+        } else {
+          Wp[((int64_t)ks * In + ii) * R + c] = s;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (KS == 1) {
+    if (pp.np) peer_push_done(pp, pe, gridDim.x);
+    return;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&counters[ib], 1u) == (unsigned)(KS - 1));
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < MTL * 8 * R; e += blockDim.x) {
+    const int ii = ib * MTL * 8 + e / R, c = e % R;
+    if (ii < In) {
+      double s = 0.0;
+      for (int k = 0; k < KS; ++k) s += __ldcg(Wp + ((int64_t)k * In + ii) * R + c);
+      W[(int64_t)ii * R + c] = s;
+      for (int q = 0; q < pp.np; ++q) pp.dst[q][poff + (int64_t)ii * R + c] = s;
+    }
+  }
+  if (threadIdx.x == 0) counters[ib] = 0u;  // re-armed for the next launch (graph replay)
+  if (pp.np) peer_push_done(pp, pe, gridDim.x);
+}
+
 // ------------------------------------------------------------- one-sided Jacobi SVD of R0
 // B = R0 V with orthogonal columns (cyclic round-robin pairs, one warp per pair); returns
 // M = U S^+ V^T = sum_{kept j} b_j v_j^T / sigma_j^2 in Ms (R x R, column-major) and the number

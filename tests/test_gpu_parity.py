@@ -1296,3 +1296,49 @@ def test_odd_first_mode_is_padded_for_tma(cp, dims, R, variant, tree, mem):
     assert np.max(np.abs(fu - f)) <= 1e-9
     for k in range(N):
         assert rel(Au[k], A3[k]) <= 1e-8
+
+
+@pytest.mark.parametrize("dims,R,variant,world", [((30, 38, 48), 5, "QR", 1), ((70, 66, 32), 32, "QR", 1),
+                                                  ((33, 20, 18, 16), 8, "SVD", 1), ((9, 8, 7, 6, 8), 4, "QR", 1),
+                                                  ((70, 66, 32), 32, "QR", 4), ((24, 20, 18, 16), 8, "QR", 8)])
+def test_q0_apply_big_kernel(cp, dims, R, variant, world):
+    """k_q0_apply_big (4 M-tiles per CTA, chosen for V_n of >= 32768 rows) forced on small shapes:
+    W of every mode against the oracle's apply_q0 (<= 1e-11, element-wise too), sweeps against the
+    oracle, and -- with virtual ranks -- the fused peer push bitwise equal to the sum-kernel exchange."""
+    import os
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=1300 + R + len(dims))
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    os.environ["CPQR_Q0_BIG"] = "1"
+    try:
+        comm = "local_peer" if world > 1 else "local"
+        s = cp.CPQR(dims, R, variant, world=world, comm=comm)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        Qs, Rs = zip(*[O.qr_pos(a) for a in init])
+        for n in range(N):
+            out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+            Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+            Q0o, R0o = O.structured_qr(list(Rs), n)
+            Wo = O.apply_q0(Yo, n, Q0o)
+            assert rel(out["W"], Wo) <= 1e-11, (n, rel(out["W"], Wo))
+            assert np.max(np.abs(out["W"] - Wo)) <= 1e-11 * np.max(np.abs(Wo))
+        f = s.sweep(3)
+        lam, A = s.get_factors()
+        if world > 1:
+            assert s.debug_peer()["windows_differing"] == 0
+        s.close()
+        if world > 1:
+            t = cp.CPQR(dims, R, variant, world=world, comm="local")
+            t.set_tensor(Xc)
+            t.set_factors(init)
+            t.sweep(3)
+            lt, At = t.get_factors()
+            t.close()
+            assert all(np.array_equal(x, y) for x, y in zip(A, At))
+    finally:
+        del os.environ["CPQR_Q0_BIG"]
+    ref = O.cp_als_qr(X, init, 3, variant=variant)
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    for k in range(N):
+        assert rel(A[k], ref["factors"][k]) <= 1e-8
