@@ -263,7 +263,8 @@ cpqr_status cpqr_debug_mode(cpqr_ctx* ctx, int n, const double* const* Q_overrid
 /* The Multi-TTM plan of mode n (0-based) on slab `slab` (0 unless CPQR_COMM_LOCAL), for the
  * plan tables of DESIGN.md §8 and the contraction-order tests: writes
  * min(cap, #steps) rows of 6 int64 to info -- kernel kind (0/4 strided, 1/5 fibre, 2/6/8 fused
- * slice, 3/7 partial-sum fix-up, 100 NE Khatri-Rao diagonal), bitmask of the contracted global
+ * slice, 3/7 partial-sum fix-up, 9 small TTM, 10 fused last-two-modes strided pass, 100 NE Khatri-Rao
+ * diagonal), bitmask of the contracted global
  * modes, input elements, output elements, flops, 1 if the step reads X -- and #steps to *nsteps.
  * Errors: EINVAL, ESTATE (no dense tensor set). */
 cpqr_status cpqr_debug_plan(cpqr_ctx* ctx, int n, int slab, int64_t* info, int cap, int* nsteps);

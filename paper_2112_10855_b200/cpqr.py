@@ -351,7 +351,8 @@ class CPQR:
         return dict(Y=Y, Q0=Q0, R0=R0, W=W)
 
     PLAN_KINDS = {0: "strided", 1: "fiber", 2: "slice", 3: "slice-reduce", 4: "strided-tma", 5: "fiber-tma",
-                  6: "slice-tma", 7: "slice-fixup", 8: "slice-small-tma", 9: "small-ttm", 100: "ne-diag"}
+                  6: "slice-tma", 7: "slice-fixup", 8: "slice-small-tma", 9: "small-ttm", 10: "strided2-tma",
+                  100: "ne-diag"}
 
     def debug_plan(self, n, slab=0):
         """The Multi-TTM plan of mode n on one slab (cpqr_debug_plan): a list of dicts with the

@@ -673,6 +673,36 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     p.steps.push_back(s);
     advance(s.out);
   };
+  // fused contraction of the two slowest modes f2 = f - 1 and f = N - 1 of src in one pass
+  // (k_strided2_tma, R <= 8): false if the layout does not allow it (the caller then emits two TTMs)
+  auto emit_ttm2 = [&](int f2, int f) {
+    const bool off = getenv("CPQR_STR_FUSE2") && atoi(getenv("CPQR_STR_FUSE2")) == 0;  // per plan build (tests)
+    if (off || !in.tma || R > 8 || f != N - 1 || f2 != f - 1 || f2 < 1 || !in.Qt[f] || !bufs[0]) return false;
+    TtmStep s{};
+    s.modes = (1u << f2) | (1u << f);
+    s.in = src;
+    s.out = out_override ? out_override : bufs[nb];
+    s.A = prod(cur, 0, f2);
+    s.I = (int)cur[f2];
+    s.B = cur[f];
+    if (s.A % 2 != 0 || s.A < 128 || s.A >= (1ll << 31) || s.B >= (1ll << 31)) return false;
+    const uint64_t d[3] = {(uint64_t)s.A, (uint64_t)s.I, (uint64_t)s.B};
+    const uint64_t st[2] = {(uint64_t)s.A * 8, (uint64_t)s.A * s.I * 8};
+    const uint32_t box[3] = {16, 16, 1};
+    if (!make_tmap(&s.mx, src, 3, d, st, box) || !qmap(s, f2, s.I)) return false;
+    s.kind = 10;
+    s.Q = in.Q[f2];
+    s.ldq = in.ldq[f2];
+    s.Qt = in.Qt[f];
+    s.rq = in.RQ;
+    s.S = stages_for(9 * kBoxBytes, 0, "CPQR_ST_STRIDED2", 8);
+    cur[f2] = R;
+    cur[f] = R;
+    p.max_buf = std::max(p.max_buf, (size_t)prod(cur, 0, N));
+    p.steps.push_back(s);
+    advance(s.out);
+    return true;
+  };
   // fused contraction of modes 0 and 1 of src (fused slice kernels, Alg. 2 line 8)
   auto emit_slice = [&]() {
       TtmStep s{};
@@ -877,8 +907,19 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     int f = (n == N - 1) ? N - 2 : N - 1;
     for (int k = f - 1; k >= 0; --k)
       if (k != n && dim_of(k) > dim_of(f)) f = k;
-    emit_ttm(f);
-    for (int k = 0; k < N; ++k) if (k != n && k != f) todo.push_back(k);
+    // HBM-bound low rank, N >= 4: when the next mode in the order is f - 1, both go in one pass
+    // (the R / I-sized intermediate of the first contraction stays on chip)
+    int f2 = -1;
+    if (N >= 4 && in.fuse && R <= 8 && f == N - 1 && f - 1 != n && f - 1 >= 1) {
+      f2 = f - 1;
+      for (int k = 0; k < N; ++k)
+        if (k != n && k != f && k != f2 && dim_of(k) > dim_of(f2)) f2 = -1;
+    }
+    if (f2 < 0 || !emit_ttm2(f2, f)) {
+      f2 = -1;
+      emit_ttm(f);
+    }
+    for (int k = 0; k < N; ++k) if (k != n && k != f && k != f2) todo.push_back(k);
   } else {
     todo.push_back(1 - n);
   }
@@ -1062,6 +1103,12 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
   }
     switch (NT) { case 1: SSM(1) break; case 2: SSM(2) break; case 3: SSM(3) break; default: SSM(4) break; }
 #undef SSM
+  } else if (s.kind == 10) {
+    const size_t smem = 3072 + (size_t)s.S * 9 * kBoxBytes;
+    const int64_t units = (s.A + 127) / 128;
+    const int grid = (int)std::min<int64_t>(units, sms);
+    set_smem(k_strided2_tma<2>, smem);
+    launch_ex(k_strided2_tma<2>, grid, 10 * 32, smem, st, pdl, 1, s.mx, s.mq, s.A, s.I, (int)s.B, R, s.Qt, s.rq, s.out, s.S);
   } else if (s.kind == 7) {
     const int grid = (int)std::min<int64_t>(s.L, (int64_t)sms * 4);
     launch_ex(k_slice_fixup, grid, 256, 0, st, pdl, 1, (const double*)s.P, s.nslots, s.L, s.nfb, s.G, R * R, s.out);
@@ -3116,6 +3163,7 @@ CPQR_API cpqr_status cpqr_get_profile(cpqr_ctx* c, cpqr_profile* p, int reset) {
       const double R = c->R, nel = (double)sl.numel;
       by += 8.0 * nel;
       if (s.kind == 2 || s.kind == 6 || s.kind == 8) fl += 2.0 * nel * R + 2.0 * (nel / (double)s.I1) * R * R;
+      else if (s.kind == 10) fl += 2.0 * nel * R + 2.0 * (nel / (double)s.I) * R * R;
       else fl += 2.0 * nel * R;
     }
   }
@@ -3270,6 +3318,9 @@ CPQR_API cpqr_status cpqr_debug_plan(cpqr_ctx* c, int n, int slab, int64_t* info
     const int64_t xp = (s.in == sl.X) ? 1 : 0;
     switch (s.kind) {
       case 0: case 4: case 9: put(s.kind, s.modes, s.A * s.I * s.B, s.A * R * s.B, 2 * s.A * s.I * s.B * R, xp); break;
+      case 10:  // both contractions of the fused pass: over I (all B slices), then over B
+        put(s.kind, s.modes, s.A * s.I * s.B, s.A * R * R, 2 * s.A * s.I * s.B * R + 2 * s.A * R * s.B * R, xp);
+        break;
       case 1: case 5: put(s.kind, s.modes, (int64_t)s.I * s.F, R * s.F, 2 * (int64_t)s.I * s.F * R, xp); break;
       case 2: case 6: case 8:
         put(s.kind, s.modes, (int64_t)s.I1 * s.I2 * s.L, R * R * s.L,

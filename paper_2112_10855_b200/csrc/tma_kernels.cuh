@@ -390,6 +390,123 @@ k_strided_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
   });
 }
 
+// ============================================ strided, the last two modes in one pass (R <= 8)
+// T(a, r, q) = sum_b Q2(b, q) sum_i X(a, i, b) Q(i, r): the two slowest modes of an (A, I, B) view
+// contracted in ONE pass over X, so the (R / I)-sized intermediate T1(a, r, b) of the first
+// contraction never goes to HBM (C4 48^5 R = 8, modes 1-2: 340 MB written and read back per mode).
+// A unit is 128 rows of a (8 consumer warps x one 16-row box) over ALL b: per slice b the warp
+// contracts i on DMMA (acc1, rows 2g / 2g + 1 of its box), then folds the slice into the unit's
+// output acc2(a, r, q) += acc1(a, r) Q2(b, q) with R plain FMAs per element (R / I of the DMMA work;
+// Q2's row b comes from the transposed panel through L1, uniform across the warp).  acc2 is 2 x 2 x R
+// doubles per thread, which bounds R at 8 (one N-tile).  X is read once, T written once.
+template <int NP = 2>
+__global__ void __launch_bounds__((8 + NP) * 32, 1)
+k_strided2_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ, int64_t A, int I,
+               int B, int R, const double* __restrict__ Q2t, int rq, double* __restrict__ T, int S) {
+  extern __shared__ uint8_t smraw[];
+  constexpr int CW = 8;
+  constexpr uint32_t XBYTES = CW * kBoxBytes, STAGE = XBYTES + kBoxBytes;
+  uint64_t *full, *empty;
+  uint8_t* st0 = tma_carve(smraw, S, full, empty);
+  const uint32_t sbase = smem_u32(st0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CW); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) prefetch_tmap(&tmX);
+  pdl_wait();
+  const int64_t units = (A + 16 * CW - 1) / (16 * CW);
+  const int KS = (I + kBK - 1) / kBK;
+  if (warp >= CW) {  // ---------------------------------------------------------- producer(s)
+    const int pw = warp - CW;
+    if (lane == 0) {
+      prefetch_tmap(&tmX);
+      if (pw == 0) prefetch_tmap(&tmQ);
+      const uint64_t pol = policy_evict_first();
+      RingPos rp;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int a0 = (int)(u * 16 * CW);
+        for (int b = 0; b < B; ++b)
+          for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+            const int s = rp.s;
+            mbar_wait(&empty[s], rp.ph ^ 1);
+            if (pw == 0) mbar_expect_tx(&full[s], STAGE);
+            uint8_t* dst = st0 + (size_t)s * STAGE;
+#pragma unroll
+            for (int q = pw * (CW / NP); q < (pw + 1) * (CW / NP); ++q)
+              tma_load_3d_ef(dst + q * kBoxBytes, &tmX, a0 + 16 * q, ks * kBK, b, &full[s], pol);
+            if (pw == 0) tma_load_2d(dst + XBYTES, &tmQ, 0, ks * kBK, &full[s]);
+          }
+      }
+    }
+    return;
+  }
+  // --------------------------------------------------------------------------------- consumers
+  const int g = lane >> 2, t = lane & 3;
+  RingPos rp;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t a0 = u * 16 * CW;
+    double acc2[2][2][8];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc2[m][j][q] = 0.0;
+    for (int b = 0; b < B; ++b) {
+      double acc[2][1][2];
+      acc[0][0][0] = acc[0][0][1] = acc[1][0][0] = acc[1][0][1] = 0.0;
+      for (int ks = 0; ks < KS; ++ks, rp.next(S)) {
+        const int s = rp.s;
+        mbar_wait(&full[s], rp.ph);
+        const uint32_t xs = sbase + s * STAGE, qs = xs + XBYTES;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int sk = 0; sk < 2; ++sk) {
+            const int k = 8 * h + 2 * t + sk;  // row (k index) inside the stage
+            const double2 xa = lds128(xs + warp * kBoxBytes + swz(k, g));
+            const double qb = lds64(qs + swz(k, g >> 1) + 8 * (g & 1));
+            dmma(acc[0][0][0], acc[0][0][1], xa.x, qb);
+            dmma(acc[1][0][0], acc[1][0][1], xa.y, qb);
+          }
+        consumer_release(&empty[s], lane, acc_dep(acc));
+      }
+      // fold slice b: acc2(a, r, q) += acc1(a, r) Q2(b, q)
+      const double2* q2 = reinterpret_cast<const double2*>(Q2t + (int64_t)b * rq);
+      double qv[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 v = __ldg(q2 + q);
+        qv[2 * q] = v.x;
+        qv[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc2[m][j][q] = fma(acc[m][0][j], qv[q], acc2[m][j][q]);
+    }
+    // rows 2g and 2g + 1 of the warp's box are adjacent: one 16-byte store per (r, q) column
+    const int64_t row = a0 + 16 * warp + 2 * g;
+    if (row < A) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = 2 * t + j;
+        if (r >= R) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < R)
+            *reinterpret_cast<double2*>(T + row + A * ((int64_t)r + (int64_t)R * q)) =
+                make_double2(acc2[0][j][q], acc2[1][j][q]);
+      }
+    }
+  }
+}
+
 // Stream-K fix-up of k_strided_tma: one CTA of 1024 threads per range boundary c = 1..G-1.  A
 // boundary that cuts a unit and is the first boundary inside it sums the segments of CTAs
 // c0 = c-1 .. c1 in that order into T.  Each thread issues the loads of its (up to) 8 entries

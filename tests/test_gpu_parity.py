@@ -1342,3 +1342,55 @@ def test_q0_apply_big_kernel(cp, dims, R, variant, world):
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
     for k in range(N):
         assert rel(A[k], ref["factors"][k]) <= 1e-8
+
+
+@pytest.mark.parametrize("variant", ["QR", "SVD"])
+@pytest.mark.parametrize("dims,R", [((20, 20, 20, 20), 8), ((14, 13, 13, 13), 5), ((22, 9, 9, 9, 9), 4),
+                                    ((16, 12, 12, 12, 12), 8), ((130, 6, 7, 7), 3)])
+def test_fused_last_two_modes_pass(cp, dims, R, variant):
+    """k_strided2_tma (N >= 4, R <= 8): modes 1 and 2 contract the two slowest modes in ONE pass over
+    X when they are next in the decreasing-dimension order.  The plan must show the
+    fused step, its flops must be Eq. (TTMcost) for that order, Y / W of every mode, factors and
+    fits must match the oracle, and CPQR_STR_FUSE2=0 (two separate TTMs) must agree."""
+    import os
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=1500 + R + len(dims))
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    s = cp.CPQR(dims, R, variant)
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    stored = (dims[0] + (dims[0] & 1),) + tuple(dims[1:])
+    fused = 0
+    for n in range(N):
+        pl = [st for st in s.debug_plan(n) if st["kind"] not in ("slice-reduce", "slice-fixup")]
+        order = [k for st in pl for k in st["modes"]]
+        assert sum(st["flops"] for st in pl) == O.ttm_cost(stored, n, R, order=order), (n, pl)
+        fused += sum(1 for st in pl if st["kind"] == "strided2-tma")
+    assert fused >= 1, fused  # mode 1, and mode 2 when mode 1 is not the largest
+    Qs, Rs = zip(*[O.qr_pos(a) for a in init])
+    for n in range(N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+        assert np.max(np.abs(out["Y"] - Yo)) <= 1e-11 * np.max(np.abs(Yo)), n
+    ref1 = O.cp_als_qr(X, init, 1, variant=variant)
+    ref = O.cp_als_qr(X, init, 3, variant=variant)
+    f1 = s.sweep(1)
+    lam, A = s.get_factors()
+    for k in range(N):
+        assert rel(A[k], ref1["factors"][k]) <= 1e-9, (k, rel(A[k], ref1["factors"][k]))
+    f = np.concatenate([f1, s.sweep(2)])
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+    s.close()
+    os.environ["CPQR_STR_FUSE2"] = "0"
+    try:
+        u = cp.CPQR(dims, R, variant)
+    finally:
+        pass
+    u.set_tensor(Xc)
+    u.set_factors(init)
+    assert not any(st["kind"] == "strided2-tma" for n in range(N) for st in u.debug_plan(n))
+    fu = u.sweep(3)
+    u.close()
+    del os.environ["CPQR_STR_FUSE2"]
+    assert np.max(np.abs(fu - f)) <= 1e-10
