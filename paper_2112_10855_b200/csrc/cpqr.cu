@@ -858,7 +858,15 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         // (strided, B = 1): with slabs the slab mode is the smallest and goes last
         for (int k = N - 1; k >= h; --k) ord.push_back(k);
         std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return dim_of(a) > dim_of(b); });
-        for (size_t q = 0; q < ord.size(); ++q) {
+        size_t q0 = 0;
+        if (ord.size() >= 2 && ord[0] == N - 1 && ord[1] == N - 2 && in.fuse && R <= 8) {
+          // the two slowest modes in one pass (k_strided2_tma), straight into the tree buffer if
+          // they are the whole right half
+          if (ord.size() == 2) out_override = in.tbuf;
+          if (emit_ttm2(N - 2, N - 1)) q0 = 2;
+          else out_override = nullptr;
+        }
+        for (size_t q = q0; q < ord.size(); ++q) {
           if (q + 1 == ord.size()) out_override = in.tbuf;
           emit_ttm(ord[q]);
         }
