@@ -386,7 +386,7 @@ def main():
         else:
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                     "peak_source": hbm_src}
-        roof["kernel"] = ("Multi-TTM stream-X pass (k_strided_tma / k_slice_tma / k_slice_small_tma), "
+        roof["kernel"] = ("Multi-TTM stream-X pass (k_strided_tma / k_strided2_tma / k_slice_tma / k_slice_small_tma), "
                           "avg over %d passes" % n_launch0)
         roof["traffic"] = None
         tfile = os.path.join(ROOT, "profiles", "traffic.json")
