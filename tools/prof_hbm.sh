@@ -1,7 +1,7 @@
 # ncu --set full of the HBM-bound configs' stream-X kernels (C2 strided, C3 strided + fused slice,
-# C4 strided + small slice), one launch each; summaries -> profiles/ncu_hbm_stream_r01.json
+# C4 fused last-two-modes strided + small slice), one launch each; summaries -> profiles/ncu_hbm_stream_r01.json
 mkdir -p gpurun_out
-for cfg in "2 k_strided_tma 0" "3 k_strided_tma 0" "3 k_slice_tma 0" "4 k_strided_tma 0" "4 k_slice_small_tma 0"; do
+for cfg in "2 k_strided_tma 0" "3 k_strided_tma 0" "3 k_slice_tma 0" "4 k_strided2_tma 0" "4 k_slice_small_tma 0"; do
   set -- $cfg
   timeout 300 python tools/prof_case.py --config $1 --sweeps 1 --graph 0 --profile 0 > /dev/null 2>&1 && timeout 600 \
     ncu -f --set full --import-source on --clock-control none -k regex:"$2" -s $3 -c 1 \
