@@ -726,7 +726,11 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         static const int scw_env = getenv("CPQR_SLICE_CW") ? atoi(getenv("CPQR_SLICE_CW")) : 0;
         static const bool wide4 = getenv("CPQR_SLICE_WIDE4") && atoi(getenv("CPQR_SLICE_WIDE4")) == 1;
         s.gps = slice_nf(s.I2);
-        if (scw_env != 8 && !(in.overlap && in.ov_cw1) && (s.gps == 2 || wide4)) { s.cw = 4; s.gps = 4; }
+        // 256-fibre boxes waste their second block when I_2 is just above 256 (300^4: 300 of 512
+        // fibre slots, and the pass turns DMMA-bound): 128-fibre boxes when they fill >= 10 % better
+        auto fillf = [&](int bn) { return (double)s.I2 / ((double)bn * (double)((s.I2 + bn - 1) / bn)); };
+        const bool narrow = s.gps == 4 && fillf(128) > 1.10 * fillf(256);
+        if (scw_env != 8 && !(in.overlap && in.ov_cw1) && (s.gps == 2 || wide4 || narrow)) { s.cw = 4; s.gps = 4; }
         const uint32_t box[3] = {16, (uint32_t)(s.cw * 8 * s.gps), 1};
         tma = make_tmap(&s.mx, src, 3, d, st, box) && qmap(s, 0, s.I1);
       }

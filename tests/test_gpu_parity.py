@@ -1394,3 +1394,27 @@ def test_fused_last_two_modes_pass(cp, dims, R, variant):
     u.close()
     del os.environ["CPQR_STR_FUSE2"]
     assert np.max(np.abs(fu - f)) <= 1e-10
+
+
+@pytest.mark.parametrize("dims,R", [((18, 300, 7, 6), 6), ((16, 270, 18, 17), 16), ((16, 520, 12, 11), 10)])
+def test_slice_pass_box_width_by_fill(cp, dims, R):
+    """The fused slice pass takes 128-fibre boxes instead of 256-fibre ones when I_2 sits just above
+    a multiple of 256 (the paper's 300^4: 300 of 512 fibre slots): Y of the modes that use it
+    (n >= 3) against the oracle, element-wise, and the sweeps."""
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=1700 + R + len(dims))
+    X = O.as_tensor(Xc)
+    N = len(dims)
+    s = cp.CPQR(dims, R, "QR")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    assert any("slice" in st["kind"] for n in range(2, N) for st in s.debug_plan(n))
+    Qs, Rs = zip(*[O.qr_pos(a) for a in init])
+    for n in range(2, N):
+        out = s.debug_mode(n, Q_override=[Qs[k] if k != n else None for k in range(N)])
+        Yo = O.multi_ttm(X, {k: Qs[k].T for k in range(N) if k != n})
+        assert rel(out["Y"], Yo) <= 1e-11, (n, rel(out["Y"], Yo))
+        assert np.max(np.abs(out["Y"] - Yo)) <= 1e-11 * np.max(np.abs(Yo)), n
+    ref = O.cp_als_qr(X, init, 3)
+    f = s.sweep(3)
+    s.close()
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
