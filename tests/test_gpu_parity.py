@@ -1418,3 +1418,22 @@ def test_slice_pass_box_width_by_fill(cp, dims, R):
     f = s.sweep(3)
     s.close()
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_odd_first_mode_direct_fit_and_slabs(cp, world):
+    """Odd I_1 (stored padded) with the DIRECT fit (the residual pass reads the padded X and A_1) and
+    with virtual ranks: fits of every sweep against the oracle's direct fit."""
+    dims, R = (21, 18, 16), 4
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=91, eta=0.0)
+    X = O.as_tensor(Xc)
+    s = cp.CPQR(dims, R, "QR", fit_mode="direct", world=world, comm="local")
+    s.set_tensor(Xc)
+    s.set_factors(init)
+    f = s.sweep(4)
+    lam, A = s.get_factors()
+    s.close()
+    ref = O.cp_als_qr(X, init, 4, fit_mode="direct")
+    assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (f, ref["fits"])
+    for k in range(3):
+        assert A[k].shape == (dims[k], R) and rel(A[k], ref["factors"][k]) <= 1e-7
