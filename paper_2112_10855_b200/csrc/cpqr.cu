@@ -86,6 +86,13 @@ struct Plan {
   size_t max_buf = 0;
   size_t part = 0;
   size_t tree_elems = 0;  // dimension tree: size of the half intermediate this plan writes
+  // Z fusion (k_zform, small_kernels.cuh): the last step (a TTM over mode zk) is skipped and the Q0
+  // apply reads its input T = zT, viewed (zAa, In, zBb), against Z = (Q_zk (x) I) Q0
+  bool zf = false;
+  int zk = -1;
+  const double* zT = nullptr;
+  int64_t zAa = 1, zBb = 1;
+  int64_t zcur[kMaxN];    // T's dims
 };
 
 // One rank's slab of the tensor (slab data parallelism over the last mode): the
@@ -211,6 +218,8 @@ struct cpqr_ctx {
   std::vector<std::pair<cudaEvent_t, std::string>> tev;
   size_t ntev = 0;
   unsigned* dq0cnt = nullptr;  // per-row-block arrival counters of k_q0_apply_tc (self re-arming)
+  double* dZ = nullptr;        // Z fusion: Z = (Q_k (x) I) Q0 of the current mode (k_zform)
+  size_t dZ_elems = 0;
   double* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
   double* dPart = nullptr;
@@ -403,6 +412,7 @@ struct PlanIn {
   bool tma;
   bool fuse;  // fused two-mode slice kernel allowed for n >= 3
   int pad0 = 0;  // 1: mode 1 is stored padded by one row (odd I_1): orders compare the true dimension
+  bool zf_ok = false;  // Z fusion allowed (one slab, no exchange, QR / SVD, dense apply)
   int sms;
   bool tree = false;        // dimension-tree Multi-TTM (QR/SVD variants)
   int h = 0;                // tree split: halves [0, h) and [h, N)
@@ -939,7 +949,28 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     if (dim_of(a) != dim_of(b)) return dim_of(a) > dim_of(b);
     return a > b;
   });
-  for (int k : todo) emit_ttm(k);
+  p.zf = false;
+  for (size_t q = 0; q < todo.size(); ++q) {
+    if (q + 1 == todo.size() && in.zf_ok && src != in.X && !p.steps.empty()) {
+      // Z fusion: skip this last TTM and let the apply kernel take its flops.  Opt-in (CPQR_ZFUSE=1;
+      // =2: only where T has <= CPQR_ZFUSE_MAX elements, default 2M): measured C2 per mode +1 to
+      // +4 % (2590-2640 -> 2670-2710 sweeps/s) but C2 tree -3.5 %, C3 -1.5 %, C4 -1 % -- the
+      // latency-bound apply kernel over J_T = I_k R^{N-2} rows costs what the launch it saves does
+      const char* ze = getenv("CPQR_ZFUSE");
+      const int zmode = ze ? atoi(ze) : 0;
+      static const int64_t zmax = getenv("CPQR_ZFUSE_MAX") ? atoll(getenv("CPQR_ZFUSE_MAX")) : (2ll << 20);
+      const int64_t tel = prod(cur, 0, N);
+      if (zmode == 1 || (zmode == 2 && tel <= zmax)) {
+        p.zf = true;
+        p.zk = todo[q];
+        p.zT = src;
+        for (int k = 0; k < N; ++k) p.zcur[k] = cur[k];
+        p.zAa = prod(cur, 0, n);
+        p.zBb = prod(cur, n + 1, N);
+      }
+    }
+    emit_ttm(todo[q]);
+  }
   if (in.ybuf && p.steps.size() >= 2) {  // overlap schedule: Y goes to its own buffer
     size_t last = p.steps.size() - 1;
     p.steps[last].out = in.ybuf;
@@ -1190,6 +1221,7 @@ void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* 
   in.tma = c->use_tma;
   in.fuse = c->fuse_slice;
   in.pad0 = c->pad1 ? 1 : 0;
+  in.zf_ok = c->nslab == 1 && !c->exchange && !ne && !c->q0_stair;
   in.sms = c->stream_sms;
   in.tree = c->tree && !ne;
   in.h = c->tree_h;
@@ -1282,6 +1314,20 @@ cpqr_status build_plans(cpqr_ctx* c) {
       PlanIn in{};
       fill_plan_in(c, sl, in, n);
       plan_mode(in, sl.plans[n], c->buf, c->dPart);
+    }
+  }
+  {  // Z fusion buffer: the largest J_T x R over the modes that use it
+    size_t ze = 0;
+    for (int q = 0; q < c->nslab; ++q)
+      for (int n = 0; n < c->N; ++n) {
+        const Plan& p = c->slabs[q].plans[n];
+        if (p.zf) ze = std::max(ze, (size_t)(p.zAa * p.zBb) * (size_t)c->R);
+      }
+    if (ze > c->dZ_elems) {
+      if (c->dZ) dfree(c->dZ);
+      c->dZ = nullptr;
+      if (dmalloc(&c->dZ, ze * sizeof(double)) != cudaSuccess) return fail(c, CPQR_ENOMEM, "Z buffer");
+      c->dZ_elems = ze;
     }
   }
   c->plans_valid = true;
@@ -1695,7 +1741,10 @@ cpqr_status launch_kr_qr(cpqr_ctx* c, int n) {
 }
 
 // pp: the peer push of this slab's W (np = 0: none), fused into the apply's final sum
-cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const PeerPush& pp = PeerPush{}) {
+// Qm: the J x R matrix applied (default Q0; Z of the Z fusion, with p describing T instead of Y)
+cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const PeerPush& pp = PeerPush{},
+                            const double* Qm = nullptr) {
+  if (!Qm) Qm = c->dQ0;
   const int64_t J = p.Aa * p.Bb, KT = (J + 3) / 4;
   const int In = (int)p.In;
   // a large V_n: 4 M-tiles per CTA so that Q0 is read once per 32 rows of Y_(n) (k_q0_apply_big)
@@ -1710,7 +1759,7 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const Peer
     KS = (KT + kpc - 1) / kpc;
     dim3 grid(groups, (unsigned)KS);
 #define Q0B(NTV)                                                                                          \
-  launch_ex(k_q0_apply_big<NTV, MTL>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb, (const double*)c->dQ0, \
+  launch_ex(k_q0_apply_big<NTV, MTL>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb, Qm, \
             c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, pp)
     switch ((c->R + 7) / 8) { case 1: Q0B(1); break; case 2: Q0B(2); break; case 3: Q0B(3); break; default: Q0B(4); break; }
 #undef Q0B
@@ -1727,14 +1776,50 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const Peer
   const int NT = (c->R + 7) / 8;
 #define Q0A(NTV)                                                                                                 \
   (c->q0_stair ? launch_ex(k_q0_apply_tc<NTV, true>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb,           \
-                           (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)c->dperm,  \
+                           Qm, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)c->dperm,                     \
                            c->N - 1, pp)                                                                             \
                : launch_ex(k_q0_apply_tc<NTV, false>, grid, 256, 0, c->st, c->pdl, 1, p.Y, p.Aa, In, p.Bb,          \
-                           (const double*)c->dQ0, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)nullptr, 0, pp))
+                           Qm, c->R, kpc, (int)KS, c->dWp, c->dq0cnt, Wout, (const int*)nullptr, 0, pp))
   switch (NT) { case 1: Q0A(1); break; case 2: Q0A(2); break; case 3: Q0A(3); break; default: Q0A(4); break; }
 #undef Q0A
   CKL();
   return CPQR_OK;
+}
+
+// Z fusion (k_zform): Z = (Q_zk (x) I) Q0 of mode n on stream st (behind the V_n QR), and the
+// pseudo-plan under which the apply kernel reads T instead of Y
+cpqr_status launch_zform(cpqr_ctx* c, int n, const Plan& p, cudaStream_t st) {
+  ZArgs a{};
+  a.Qk = c->dQ[p.zk];
+  a.ldq = c->dims[p.zk];
+  a.Q0 = c->dQ0;
+  a.Z = c->dZ;
+  a.R = c->R;
+  int64_t ystride = 1;
+  a.JT = 1;
+  for (int k = 0; k < c->N; ++k) {
+    if (k == n) continue;
+    if (k == p.zk) a.kpos = a.nm;
+    a.td[a.nm] = p.zcur[k];
+    a.ys[a.nm] = ystride;
+    ystride *= c->R;
+    a.JT *= p.zcur[k];
+    ++a.nm;
+  }
+  a.JY = ystride;
+  if ((size_t)(a.JT * c->R) > c->dZ_elems) return fail(c, CPQR_ECUDA, "Z buffer undersized");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((a.JT * c->R + 255) / 256, (int64_t)c->sms * 4));
+  k_zform<<<grid, 256, 0, st>>>(a);
+  CKL();
+  return CPQR_OK;
+}
+Plan zf_view(const Plan& p) {
+  Plan v;
+  v.Y = p.zT;
+  v.Aa = p.zAa;
+  v.In = p.In;
+  v.Bb = p.zBb;
+  return v;
 }
 
 // where slab q's partial W_n (or its rows of W_N) is written: straight into W without an exchange
@@ -1911,6 +1996,7 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
     TRY(launch_pinv(c, c->side, nullptr));
     c->pinv_ready = true;
   }
+  if (p.zf) TRY(launch_zform(c, n, p, c->side));
   trace_mark(c, c->side, "K2 end", n);
   CK(cudaEventRecord(c->evK[n], c->side));
   // the stream-X pass; its dependence on the previous tail
@@ -1928,7 +2014,7 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
   size_t nf = nx;
   if (nf < p.steps.size() && (p.steps[nf].kind == 7 || p.steps[nf].kind == 3)) ++nf;  // the pass's fix-up
   first.steps.assign(p.steps.begin(), p.steps.begin() + nf);
-  rest.steps.assign(p.steps.begin() + nf, p.steps.end());
+  rest.steps.assign(p.steps.begin() + nf, p.steps.end() - ((p.zf && nf < p.steps.size()) ? 1 : 0));
   TRY(run_plan(c, first));
   trace_mark(c, c->st, "pass end", n);
   if (inflight && !dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
@@ -1938,7 +2024,8 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
   // W_n = Y_(n) Q0 on st with the whole GPU (on the reserved SMs beside the next pass it took 4x
   // longer), once the V_n QR is done
   CK(cudaStreamWaitEvent(c->st, c->evK[n], 0));
-  TRY(launch_q0_apply(c, p, c->dW));
+  if (p.zf && nf < p.steps.size()) TRY(launch_q0_apply(c, zf_view(p), c->dW, PeerPush{}, c->dZ));
+  else TRY(launch_q0_apply(c, p, c->dW));
   trace_mark(c, c->st, "q0 end", n);
   CK(cudaEventRecord(c->evY[n], c->st));
   // the tail on tl: the fused solve / normalise / factor QR (/ fast fit)
@@ -2085,6 +2172,8 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
     cudaStream_t keep = c->side;
     if (!fork) c->side = nullptr;
     cpqr_status st = launch_kr_qr(c, n);
+    if (st == CPQR_OK && !c->kt && c->slabs[0].plans[n].zf)
+      st = launch_zform(c, n, c->slabs[0].plans[n], fork ? keep : c->st);
     if (st == CPQR_OK && pinv_fork) {
       CK(cudaEventRecord(c->evf, c->st));
       CK(cudaStreamWaitEvent(keep, c->evf, 0));
@@ -2149,11 +2238,12 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
       TRY(run_plan(c, first));
       prof_mark(c, 0);
       Plan rest;
-      rest.steps.assign(p.steps.begin() + nx, p.steps.end());
+      rest.steps.assign(p.steps.begin() + nx, p.steps.end() - (p.zf ? 1 : 0));  // Z fusion: no last TTM
       TRY(run_plan(c, rest));
       prof_mark(c, 1);
       if (fork && q == 0) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-      TRY(launch_q0_apply(c, p, wloc(c, q), make_push(c, q)));
+      if (p.zf) TRY(launch_q0_apply(c, zf_view(p), wloc(c, q), make_push(c, q), c->dZ));
+      else TRY(launch_q0_apply(c, p, wloc(c, q), make_push(c, q)));
       src[q] = wloc(c, q);
       prof_mark(c, 4);
     }
@@ -2794,6 +2884,7 @@ CPQR_API cpqr_status cpqr_destroy(cpqr_ctx* c) {
   if (c->dq0cnt) dfree(c->dq0cnt);
   if (c->dKtP) dfree(c->dKtP);
   if (c->dSkCnt) dfree(c->dSkCnt);
+  if (c->dZ) dfree(c->dZ);
   for (int k = 0; k < kMaxN; ++k) if (c->dKtB[k]) dfree(c->dKtB[k]);
   if (c->dKtLam) dfree(c->dKtLam);
   if (c->dKtM) dfree(c->dKtM);

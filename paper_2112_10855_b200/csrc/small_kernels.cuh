@@ -492,6 +492,45 @@ k_q0_apply_tc(const double* __restrict__ Y, int64_t Aa, int In, int64_t Bb, cons
   if (pp.np) peer_push_done(pp, pe, gridDim.x);  // one finisher per row block
 }
 
+// Z fusion: the last TTM of the Multi-TTM (over mode k) and the Q0 apply are one product
+//   W_n = Y_(n) Q0 = T_(n) [(Q_k (x) I) Q0] = T_(n) Z,   Z(j_T, c) = sum_r Q_k(i_k, r) Q0(j_Y(r), c)
+// where T is the intermediate BEFORE the last TTM (mode k still I_k long), j_T runs over T_(n)'s
+// columns and j_Y(r) is the same multi-index with i_k replaced by r.  Z (J_T x R, J_T = I_k R^{N-2})
+// is formed on the side stream right behind the V_n QR, beside the stream pass; the apply kernel
+// then reads T instead of Y.  One launch and one L2 round trip less on the per-mode chain; same
+// flops as the last TTM.  Used where T is small (launch-bound configs), see plan_mode.
+struct ZArgs {
+  const double* Qk;
+  int64_t ldq;
+  const double* Q0;
+  double* Z;
+  int nm;                   // modes != n
+  int kpos;                 // position of mode k among them
+  int64_t td[kMaxModes];    // T's dims over the modes != n, in mode order (R, or I_k at kpos)
+  int64_t ys[kMaxModes];    // Y_(n) column strides of those modes (powers of R)
+  int R;
+  int64_t JT, JY;
+};
+__global__ void __launch_bounds__(256) k_zform(ZArgs a) {
+  const int64_t tot = a.JT * a.R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e % a.JT;
+    const int c = (int)(e / a.JT);
+    int64_t rem = j, base = 0, ik = 0;
+    for (int m = 0; m < a.nm; ++m) {
+      const int64_t idx = rem % a.td[m];
+      rem /= a.td[m];
+      if (m == a.kpos) ik = idx;
+      else base += idx * a.ys[m];
+    }
+    const double* q0 = a.Q0 + base + a.JY * c;
+    const int64_t sk = a.ys[a.kpos];
+    double s = 0.0;
+    for (int r = 0; r < a.R; ++r) s = fma(__ldg(a.Qk + ik + a.ldq * r), __ldg(q0 + r * sk), s);
+    a.Z[e] = s;
+  }
+}
+
 // Large V_n (the 5-way high-rank regime: 75^5 at R = 32 has a 1M x 32 Q0 of 268 MB
 // beside a 629 MB Y_(n)): the dense apply with MTL 8-row M-tiles per CTA, so each Q0 fragment feeds
 // MTL DMMAs and Q0 is read ceil(In / (8 MTL)) times instead of ceil(In / 8).  Same k-slices, warp

@@ -1437,3 +1437,40 @@ def test_odd_first_mode_direct_fit_and_slabs(cp, world):
     assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (f, ref["fits"])
     for k in range(3):
         assert A[k].shape == (dims[k], R) and rel(A[k], ref["factors"][k]) <= 1e-7
+
+
+@pytest.mark.parametrize("dims,R,variant,tree", [((30, 38, 48), 5, "QR", False), ((33, 20, 18, 16), 8, "SVD", False),
+                                                 ((24, 20, 18, 16), 8, "QR", True), ((9, 8, 7, 6, 8), 4, "QR", False),
+                                                 ((70, 66, 32), 32, "QR", False)])
+def test_z_fusion(cp, dims, R, variant, tree):
+    """CPQR_ZFUSE=1: the last TTM and the Q0 apply as one product W = T_(n) [(Q_k (x) I) Q0] (Z formed
+    on the side stream by k_zform): factors after one sweep and fits of three against the oracle,
+    in the overlap and the serial schedule, and against the unfused sweep."""
+    import os
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=1900 + R + len(dims))
+    X = O.as_tensor(Xc)
+    ref1 = O.cp_als_qr(X, init, 1, variant=variant)
+    ref = O.cp_als_qr(X, init, 3, variant=variant)
+    base = cp.CPQR(dims, R, variant, tree=tree)
+    base.set_tensor(Xc)
+    base.set_factors(init)
+    fb = base.sweep(3)
+    base.close()
+    for overlap in ("1", "0"):
+        os.environ["CPQR_ZFUSE"] = "1"
+        os.environ["CPQR_OVERLAP"] = overlap
+        try:
+            s = cp.CPQR(dims, R, variant, tree=tree)
+            s.set_tensor(Xc)
+            s.set_factors(init)
+            f1 = s.sweep(1)
+            lam, A = s.get_factors()
+            f = np.concatenate([f1, s.sweep(2)])
+            s.close()
+        finally:
+            del os.environ["CPQR_ZFUSE"]
+            del os.environ["CPQR_OVERLAP"]
+        for k in range(len(dims)):
+            assert rel(A[k], ref1["factors"][k]) <= 1e-9, (overlap, k, rel(A[k], ref1["factors"][k]))
+        assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
+        assert np.max(np.abs(f - fb)) <= 1e-10
