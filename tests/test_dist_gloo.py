@@ -174,3 +174,57 @@ def test_bench_reference_arm_under_torchrun_world2():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["steps"] == 2 and d["unit"] == "sweeps/s"
     assert d["config"]["workload"].startswith("C1") and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["value"] > 0
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+def test_peer_window_protocol_model(p):
+    """Host-side model of the peer push-reduce protocol (small_kernels.cuh): p ranks,
+    each with a receive window of [2 parities][p slots] and p arrival flags, run exchanges
+    e = 1..E as push (store into slot `rank`, parity (e-1) & 1, of EVERY window -- one micro-step per
+    destination, in any order -- then, after all of them, raise flag[rank] = e on every window, again
+    one micro-step per destination) and combine (wait for all p flags >= e, then read the p slots of
+    that parity).  Under random interleavings of the ranks' micro-steps, every combine must read
+    exactly the values pushed for ITS exchange (no slot overwritten early, none stale) and no rank
+    may deadlock -- the claim behind "flags only grow, two parities, no reset, no second barrier"."""
+    import random
+    E = 7
+    for seed in range(200):
+        rng = random.Random(1000 * p + seed)
+        slot = [[[None] * p for _ in range(2)] for _ in range(p)]   # slot[dst][parity][src]
+        flag = [[0] * p for _ in range(p)]                          # flag[dst][src]
+        # per-rank program counter: (exchange e, phase, pending micro-steps)
+        state = [dict(e=1, phase="data", todo=list(range(p))) for _ in range(p)]
+        done = [False] * p
+        steps = 0
+        while not all(done):
+            steps += 1
+            assert steps < 100000, "no progress"
+            ready = []
+            for r in range(p):
+                if done[r]:
+                    continue
+                st = state[r]
+                if st["phase"] in ("data", "flag") or all(flag[r][q] >= st["e"] for q in range(p)):
+                    ready.append(r)
+            assert ready, ("deadlock", seed, [(s["e"], s["phase"]) for s in state])
+            r = rng.choice(ready)
+            st = state[r]
+            e = st["e"]
+            if st["phase"] == "data":
+                d = st["todo"].pop(rng.randrange(len(st["todo"])))
+                slot[d][(e - 1) & 1][r] = (r, e)
+                if not st["todo"]:
+                    st["phase"], st["todo"] = "flag", list(range(p))
+            elif st["phase"] == "flag":
+                d = st["todo"].pop(rng.randrange(len(st["todo"])))
+                assert flag[d][r] == e - 1   # flags only grow, one exchange at a time
+                flag[d][r] = e
+                if not st["todo"]:
+                    st["phase"] = "combine"
+            else:  # combine: all p flags have reached e
+                got = [slot[r][(e - 1) & 1][q] for q in range(p)]
+                assert got == [(q, e) for q in range(p)], (seed, r, e, got)
+                if e == E:
+                    done[r] = True
+                else:
+                    state[r] = dict(e=e + 1, phase="data", todo=list(range(p)))
