@@ -1770,6 +1770,8 @@ cpqr_status launch_q0_apply(cpqr_ctx* c, const Plan& p, double* Wout, const Peer
   // slices of Q0's k-steps so that ~2 CTAs per SM run, each with >= 1 k-step per warp
   int64_t KS = std::max<int64_t>(1, std::min<int64_t>((2 * c->sms + iblocks - 1) / iblocks, (KT + 7) / 8));
   KS = std::min<int64_t>(KS, kQ0MaxSlices);
+  static const int ks_env = getenv("CPQR_Q0_KS") ? atoi(getenv("CPQR_Q0_KS")) : 0;  // experiments
+  if (ks_env > 0) KS = std::min<int64_t>(ks_env, std::min<int64_t>(kQ0MaxSlices, KT));
   const int kpc = (int)((KT + KS - 1) / KS);
   KS = (KT + kpc - 1) / kpc;
   dim3 grid(iblocks, (unsigned)KS);
