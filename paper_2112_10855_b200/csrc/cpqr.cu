@@ -765,10 +765,10 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
         const int MT = NT;
         const int BN = s.cw * 8 * s.gps;
         if (s.cw == 4) {
-          const size_t stage = (size_t)BN * 128 + NQB * kBoxBytes, extra = (size_t)4 * R * R * 8;
+          const size_t stage = (size_t)BN * 128 + NQB * kBoxBytes, extra = (size_t)4 * slice_ldy(R) * R * 8;
           s.S = std::min<int>(stages_for(stage, extra, "CPQR_ST_SLICE", 4), (int)((110 * 1024 - 3072 - extra) / stage));
         } else {
-          s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * R * R * 8, "CPQR_ST_SLICE");
+          s.S = stages_for((size_t)BN * 128 + NQB * kBoxBytes, (size_t)kCW * slice_ldy(R) * R * 8, "CPQR_ST_SLICE");
         }
         s.nfb = (s.I2 + BN - 1) / BN;
         const int64_t U = s.L * s.nfb;
@@ -1112,7 +1112,7 @@ int launch_tma(const TtmStep& s, int R, cudaStream_t st, int sms, bool pdl) {  /
 #undef FIB
   } else if (s.kind == 6) {
     const int BN = s.cw * 8 * s.gps;
-    const size_t smem = 3072 + (size_t)s.S * ((size_t)BN * 128 + NQB * kBoxBytes) + (size_t)s.cw * R * R * 8;
+    const size_t smem = 3072 + (size_t)s.S * ((size_t)BN * 128 + NQB * kBoxBytes) + (size_t)s.cw * slice_ldy(R) * R * 8;
 #define SLC(MTV, NFV)                                                                                      \
   {                                                                                                        \
     set_smem(k_slice_tma<MTV, NFV>, smem);                                                                 \

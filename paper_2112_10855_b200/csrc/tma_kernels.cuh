@@ -560,6 +560,9 @@ __global__ void __launch_bounds__(1024) k_strided_fixup(const double* __restrict
 // fibres 16w..16w+15 of the block; N-tile n (0/1), lane g -> fibre 16w + 8n + fmap(g) with
 // fmap(g) = (g>>1) + 4(g&1) (makes the 16-byte X loads conflict free under the swizzle).
 __device__ __forceinline__ int fmap(int g) { return (g >> 1) + 4 * (g & 1); }
+// leading dimension of the fused slice kernel's per-warp Y in shared memory: the smallest ldy >= R
+// with ldy = 2 (mod 8) (k_slice_tma)
+__host__ __device__ inline int slice_ldy(int R) { return R + ((10 - R % 8) % 8); }
 
 // One stage of the first contraction: acc[m][n] += Q1^T(r1, i) X(i, fibre) over the 16 i, for the
 // warp's NF N-tiles of 8 fibres (fibre rows FW*warp + 8n + fmap(g) of the stage box).
@@ -677,11 +680,15 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   constexpr uint32_t XBYTES = BN * 128, QBYTES = NQB * kBoxBytes, STAGE = XBYTES + QBYTES;
   uint64_t *full, *empty;
   uint8_t* st0 = tma_carve(smraw, S, full, empty);
-  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // CW x R x R: per-warp Y
+  double* red = reinterpret_cast<double*>(st0 + (size_t)S * STAGE);  // CW x (ldy x R): per-warp Y
   const uint32_t sbase = smem_u32(st0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int RR = R * R;
-  for (int e = threadIdx.x; e < CW * RR; e += blockDim.x) red[e] = 0.0;
+  // leading dimension of the per-warp Y (r1 + ldy r2): ldy = 2 mod 8, so that the four lanes t of a
+  // half-warp (r2 = 8 m2 + 2 t + j, stride 2 ldy doubles) fall into different 4-double bank groups
+  // (ldy = R = 16 put them in the same banks: 18 % of C3's shared-memory wavefronts were conflicts)
+  const int ldy = slice_ldy(R), WY = ldy * R;
+  for (int e = threadIdx.x; e < CW * WY; e += blockDim.x) red[e] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CW); }
     fence_barrier_init();
@@ -715,7 +722,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     return;
   }
   const int g = lane >> 2, t = lane & 3;
-  double* yw = red + warp * RR;  // this warp's running Y (r1 + R r2)
+  double* yw = red + warp * WY;  // this warp's running Y (r1 + ldy r2)
   // NF == 2 (few stages per unit): Y stays in registers between flushes; NF == 4: in smem (yw),
   // which frees the registers the 4 N-tiles of the first contraction need
   constexpr bool YREG = NF <= 2;
@@ -770,7 +777,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int r2 = 8 * m2 + 2 * t + j;
-            yacc[m2][j] = (r1 < R && r2 < R) ? yw[r1 + R * r2] : 0.0;
+            yacc[m2][j] = (r1 < R && r2 < R) ? yw[r1 + ldy * r2] : 0.0;
           }
   #pragma unroll
         for (int n = 0; n < NF; ++n)
@@ -789,7 +796,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int r2 = 8 * m2 + 2 * t + j;
-            if (r1 < R && r2 < R) yw[r1 + R * r2] = yacc[m2][j];
+            if (r1 < R && r2 < R) yw[r1 + ldy * r2] = yacc[m2][j];
           }
       }
     }
@@ -803,7 +810,7 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               const int r1 = 8 * m + g, r2 = 8 * m2 + 2 * t + j;
-              if (r1 < R && r2 < R) yw[r1 + R * r2] = yreg[m][m2][j];
+              if (r1 < R && r2 < R) yw[r1 + ldy * r2] = yreg[m][m2][j];
               yreg[m][m2][j] = 0.0;
             }
       }
@@ -817,12 +824,13 @@ k_slice_tma(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
         dst = P + (l * nslots + (blockIdx.x - first_cta)) * RR;
       }
       for (int e = threadIdx.x; e < RR; e += CW * 32) {
+        const int r2 = e / R, o = (e - r2 * R) + ldy * r2;
         double v = 0.0;
-        for (int w = 0; w < CW; ++w) v += red[w * RR + e];
+        for (int w = 0; w < CW; ++w) v += red[w * WY + o];
         dst[e] = v;
       }
       consumers_sync_n<CW * 32>();
-      for (int e = threadIdx.x; e < CW * RR; e += CW * 32) red[e] = 0.0;
+      for (int e = threadIdx.x; e < CW * WY; e += CW * 32) red[e] = 0.0;
       consumers_sync_n<CW * 32>();
       run_start = u + 1;
     }
