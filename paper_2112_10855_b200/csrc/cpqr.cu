@@ -203,6 +203,9 @@ struct cpqr_ctx {
   // overlap schedule: the tail of mode n (Q0 apply, solve, factor QR) runs on stream
   // tl beside the stream-X pass of mode n+1 whenever that pass does not contract mode n
   bool overlap = false, tail_single = false;
+  // CP-ALS (NE), N = 3, one GPU: the one-CTA NE tail of mode n on stream tl beside the MTTKRP's first
+  // TTM of mode n+1, which contracts mode (n+2) mod 3 -- not the factor that tail is updating
+  bool overlap_ne = false;
   int overlap_reserve = 4;   // SMs the stream passes leave free for the tail / V_n QR
   // stream passes one CTA per SM so the reserved SMs stay free (CPQR_OVERLAP_CW1=1).  Off: the
   // two-CTA-per-SM passes (R <= 12) lose more than the freed SMs gain (interleaved A/B, 40 sweeps
@@ -413,6 +416,7 @@ struct PlanIn {
   bool fuse;  // fused two-mode slice kernel allowed for n >= 3
   int pad0 = 0;  // 1: mode 1 is stored padded by one row (odd I_1): orders compare the true dimension
   bool zf_ok = false;  // Z fusion allowed (one slab, no exchange, QR / SVD, dense apply)
+  bool ne_ov = false;  // NE overlap schedule: first TTM over mode (n+1) mod 3
   int sms;
   bool tree = false;        // dimension-tree Multi-TTM (QR/SVD variants)
   int h = 0;                // tree split: halves [0, h) and [h, N)
@@ -824,6 +828,7 @@ void plan_mode(const PlanIn& in, Plan& p, double* const bufs[2], double* part) {
     int rmode = (n >= 1) ? 0 : N - 1;
     for (int k = N - 1; k >= 0; --k)
       if (k != n && cur[k] > cur[rmode]) rmode = k;
+    if (in.ne_ov && N == 3) rmode = (n + 1) % 3;  // never mode n-1, whose factor the previous tail updates
     emit_ttm(rmode);
     int nd = N;
     int64_t dd[kMaxN];
@@ -1221,6 +1226,7 @@ void fill_plan_in(cpqr_ctx* c, const Slab& sl, PlanIn& in, int n, const double* 
   in.tma = c->use_tma;
   in.fuse = c->fuse_slice;
   in.pad0 = c->pad1 ? 1 : 0;
+  in.ne_ov = c->overlap_ne;
   in.zf_ok = c->nslab == 1 && !c->exchange && !ne && !c->q0_stair;
   in.sms = c->stream_sms;
   in.tree = c->tree && !ne;
@@ -2056,10 +2062,83 @@ cpqr_status mode_update_overlap(cpqr_ctx* c, int n, bool fit_here) {
   return CPQR_OK;
 }
 
+// The NE tail of mode n on c->st (Alg. 1 lines 7-10 + the fast fit):
+// Cholesky (LU fallback) or S_n^+ solve of Ahat S_n = M, lambda, normalise, Gram; then the TMA panel
+cpqr_status launch_tail_ne(cpqr_ctx* c, int n, const double* Mfull, int m_rowmajor, bool fit_here) {
+  const int N = c->N, In = (int)c->dims[n];
+  TailNeArgs a{};
+  a.Spinv = c->variant == CPQR_PINV ? c->dMpinv : nullptr;
+  a.M = Mfull;
+  a.m_rowmajor = m_rowmajor;
+  for (int k = 0; k < N; ++k) a.G[k] = c->dG[k];
+  a.N = N;
+  a.n = n;
+  a.In = In;
+  a.R = c->R;
+  a.A = c->dA[n];
+  a.Gn = c->dG[n];
+  a.lam = c->dlam;
+  a.flags = c->dflags;
+  a.do_fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
+  a.nX2 = c->dnX2;
+  a.fit = c->dfit;
+  a.Ahat = c->dAhat;
+  a.force_lu = getenv("CPQR_NE_FORCE_LU") ? 1 : 0;
+  const int RB = rb_for(c->R);
+  const size_t smem = (size_t)(3 * RB * RB + kNeLd * RB) * sizeof(double);
+  switch (RB) {
+    case 8: set_smem(k_tail_ne<8>, smem); k_tail_ne<8><<<1, kNeThreads, smem, c->st>>>(a); break;
+    case 16: set_smem(k_tail_ne<16>, smem); k_tail_ne<16><<<1, kNeThreads, smem, c->st>>>(a); break;
+    default: set_smem(k_tail_ne<32>, smem); k_tail_ne<32><<<1, kNeThreads, smem, c->st>>>(a); break;
+  }
+  CKL();
+  k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[n], c->dims[n], In, c->R, c->RQ, c->dAt[n]);
+  CKL();
+  return CPQR_OK;
+}
+
+// Overlap schedule of one CP-ALS (NE) mode update, N = 3, one slab.  st: the MTTKRP -- its first TTM
+// contracts mode (n+1) mod 3 with A_{n+1}, which the tail of mode n-1 (still running on tl) does not
+// write; the Khatri-Rao diagonal contraction with A_{n-1} waits for that tail.  tl: the one-CTA tail
+// (it also needs G_{n-1}).  M_n is copied out of the ping-pong buffers (the next pass writes them
+// while the tail reads M_n).  Same arithmetic as the serial schedule up to the contraction order.
+cpqr_status mode_update_ne_overlap(cpqr_ctx* c, int n, bool fit_here) {
+  const int N = c->N;
+  const int prev = (n + N - 1) % N;
+  const Plan& p = c->slabs[0].plans[n];
+  const bool inflight = !(n == 0 && c->ov_first);
+  Plan first, second;
+  first.steps = p.steps;
+  second.diags = p.diags;
+  bool dep = false;  // the dense TTM must not touch mode prev (plan_mode: ne_ov)
+  for (const TtmStep& s : p.steps) dep = dep || ((s.modes >> prev) & 1u);
+  if (inflight && dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
+  TRY(run_plan(c, first));
+  if (inflight && !dep) CK(cudaStreamWaitEvent(c->st, c->evQ[prev], 0));
+  TRY(run_plan(c, second));
+  const int64_t mel = c->dims[n] * c->R;
+  CK(cudaMemcpyAsync(c->dW, p.Y, sizeof(double) * mel, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaEventRecord(c->evY[n], c->st));
+  CK(cudaStreamWaitEvent(c->tl, c->evY[n], 0));
+  std::swap(c->st, c->tl);
+  cpqr_status st = launch_tail_ne(c, n, c->dW, p.m_rowmajor, fit_here);
+  if (st == CPQR_OK && n == N - 1 && c->opt.fit_mode == CPQR_FIT_FAST) {
+    k_store_fit<<<1, 32, 0, c->st>>>(c->dfit, c->dfits, c->dfitc, c->fits_cap);
+    if (cudaGetLastError() != cudaSuccess) st = CPQR_ECUDA;
+    else c->launch_count++;
+  }
+  std::swap(c->st, c->tl);
+  TRY(st);
+  CK(cudaEventRecord(c->evQ[n], c->tl));
+  if (n == N - 1 && (c->ov_join || c->opt.fit_mode == CPQR_FIT_DIRECT)) CK(cudaStreamWaitEvent(c->st, c->evQ[n], 0));
+  return CPQR_OK;
+}
+
 cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
   const int N = c->N;
   const int In = (int)c->dims[n];
   if (c->overlap && !c->kt && !c->opt.profile) return mode_update_overlap(c, n, fit_here);
+  if (c->overlap_ne && !c->kt && !c->opt.profile) return mode_update_ne_overlap(c, n, fit_here);
   prof_mark(c, -1);
   if (ne_family(c->variant)) {
     const double* Mfull = nullptr;
@@ -2122,36 +2201,7 @@ cpqr_status mode_update(cpqr_ctx* c, int n, bool fit_here) {
       }
     }
     if (pfork) CK(cudaStreamWaitEvent(c->st, c->evj, 0));
-    TailNeArgs a{};
-    a.Spinv = pinv ? c->dMpinv : nullptr;
-    a.M = Mfull;
-    a.m_rowmajor = m_rowmajor;
-    for (int k = 0; k < N; ++k) a.G[k] = c->dG[k];
-    a.N = N;
-    a.n = n;
-    a.In = In;
-    a.R = c->R;
-    a.A = c->dA[n];
-    a.Gn = c->dG[n];
-    a.lam = c->dlam;
-    a.flags = c->dflags;
-    a.do_fit = fit_here && c->opt.fit_mode == CPQR_FIT_FAST;
-    a.nX2 = c->dnX2;
-    a.fit = c->dfit;
-    a.Ahat = c->dAhat;
-    {
-      a.force_lu = getenv("CPQR_NE_FORCE_LU") ? 1 : 0;
-      const int RB = rb_for(c->R);
-      const size_t smem = (size_t)(3 * RB * RB + kNeLd * RB) * sizeof(double);
-      switch (RB) {
-        case 8: set_smem(k_tail_ne<8>, smem); k_tail_ne<8><<<1, kNeThreads, smem, c->st>>>(a); break;
-        case 16: set_smem(k_tail_ne<16>, smem); k_tail_ne<16><<<1, kNeThreads, smem, c->st>>>(a); break;
-        default: set_smem(k_tail_ne<32>, smem); k_tail_ne<32><<<1, kNeThreads, smem, c->st>>>(a); break;
-      }
-    }
-    CKL();
-    k_transpose_pad<<<64, 256, 0, c->st>>>(c->dA[n], c->dims[n], In, c->R, c->RQ, c->dAt[n]);
-    CKL();
+    TRY(launch_tail_ne(c, n, Mfull, m_rowmajor, fit_here));
     prof_mark(c, 5);
     return CPQR_OK;
   }
@@ -2335,7 +2385,7 @@ void prof_accumulate(cpqr_ctx* c) {
 // One sweep of mode updates, then the fit into the next dfits slot (k_store_fit; in the overlap
 // schedule with the fast fit the last tail stores it on its own stream).
 cpqr_status one_sweep(cpqr_ctx* c) {
-  const bool ov = c->overlap && !c->kt && !c->opt.profile;
+  const bool ov = (c->overlap || c->overlap_ne) && !c->kt && !c->opt.profile;
   for (int n = 0; n < c->N; ++n) {
     TRY(mode_update(c, n, n == c->N - 1));
     if (c->opt.profile) prof_accumulate(c);
@@ -2655,6 +2705,16 @@ static cpqr_status create_impl(cpqr_ctx* c, int N, const int64_t* dims, int R) {
     if (const char* r = getenv("CPQR_OVERLAP_SMS")) c->overlap_reserve = std::max(0, atoi(r));
     if (const char* r = getenv("CPQR_OVERLAP_CW1")) c->ov_cw1 = atoi(r) != 0;
     if (c->overlap) c->stream_sms = std::max(1, c->sms - c->overlap_reserve);
+    // NE overlap schedule (mode_update_ne_overlap): 3-way CP-ALS on one GPU; the stream grids leave
+    // one SM to the one-CTA tail.  Default where it measured faster: tensors up to 1.2 GB, whose
+    // 21-26 us tail is a large share of the pass (C2 400^3 R = 10: 2810 -> 3150 sweeps/s), and
+    // R >= 24 (700^3 R = 32: 2.66 -> 2.46 ms per iteration); at 700^3 R = 4..8 its contraction order
+    // (mode (n+1) mod 3 first instead of the last mode) costs 8 %.  CPQR_OVERLAP_NE=0/1 off / on
+    const char* ovn = getenv("CPQR_OVERLAP_NE");
+    const double xbytes = 8.0 * (double)prod(dims, 0, N);
+    const bool ne_elig = c->variant == CPQR_NE && N == 3 && !c->exchange && !c->opt.profile;
+    c->overlap_ne = ne_elig && (ovn ? atoi(ovn) == 1 : (xbytes <= 1.2e9 || R >= 24));
+    if (c->overlap_ne) c->stream_sms = std::max(1, c->sms - 1);
   }
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->user = (cudaStream_t)c->opt.stream;

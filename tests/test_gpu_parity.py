@@ -1474,3 +1474,37 @@ def test_z_fusion(cp, dims, R, variant, tree):
             assert rel(A[k], ref1["factors"][k]) <= 1e-9, (overlap, k, rel(A[k], ref1["factors"][k]))
         assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8
         assert np.max(np.abs(f - fb)) <= 1e-10
+
+
+@pytest.mark.parametrize("dims,R,fit_mode", [((30, 38, 48), 5, "fast"), ((41, 36, 24), 6, "direct"), ((70, 66, 32), 32, "fast")])
+def test_ne_overlap_schedule(cp, dims, R, fit_mode):
+    """CP-ALS (NE), N = 3: the overlap schedule (the one-CTA tail of mode n beside the first TTM of
+    mode n+1, which contracts mode (n+2) mod 3) against the oracle and against the serial schedule
+    (CPQR_OVERLAP_NE=0; the two contract in different orders, so they agree to rounding only), as a
+    CUDA graph and eagerly (bitwise equal)."""
+    import os
+    conf, Xc, truth, init = synth.small_problem(dims, R, seed=2100 + R)
+    X = O.as_tensor(Xc)
+    ref1 = O.cp_als_ne(X, init, 1)
+    ref = O.cp_als_ne(X, init, 4, fit_mode=fit_mode)
+    out = {}
+    for key, env, graph in [("ov", None, True), ("ov_eager", None, False), ("serial", "0", True)]:
+        if env is not None:
+            os.environ["CPQR_OVERLAP_NE"] = env
+        try:
+            s = cp.CPQR(dims, R, "NE", fit_mode=fit_mode, use_graph=graph)
+        finally:
+            os.environ.pop("CPQR_OVERLAP_NE", None)
+        s.set_tensor(Xc)
+        s.set_factors(init)
+        f1 = s.sweep(1)
+        lam1, A1 = s.get_factors()
+        f = np.concatenate([f1, s.sweep(3)])
+        out[key] = (f, A1, s.get_factors()[1])
+        s.close()
+        for k in range(3):
+            assert rel(A1[k], ref1["factors"][k]) <= 1e-9, (key, k, rel(A1[k], ref1["factors"][k]))
+        assert np.max(np.abs(f - np.array(ref["fits"]))) <= 1e-8, (key, f, ref["fits"])
+    assert np.array_equal(out["ov"][0], out["ov_eager"][0])
+    assert all(np.array_equal(x, y) for x, y in zip(out["ov"][2], out["ov_eager"][2]))
+    assert np.max(np.abs(out["ov"][0] - out["serial"][0])) <= 1e-10
