@@ -113,12 +113,14 @@ def test_one_rank_exchange_in_graph(cp, dims, R, variant, tree, comm):
     """world = 1 through the exchange path: the push to the rank's own window, or a one-rank NCCL
     communicator whose collectives are captured in the sweep graph -- bitwise the plain sweep."""
     conf, Xc, truth, init = synth.small_problem(dims, R, seed=611 + R)
-    # the plain context runs the serial schedule the exchange paths use (CPQR_OVERLAP is read at create)
+    # the plain context runs the serial schedules the exchange paths use (the switches are read at create)
     os.environ["CPQR_OVERLAP"] = "0"
+    os.environ["CPQR_OVERLAP_NE"] = "0"
     try:
         a = cp.CPQR(dims, R, variant, tree=tree)
     finally:
         del os.environ["CPQR_OVERLAP"]
+        del os.environ["CPQR_OVERLAP_NE"]
     kw = dict(nccl_id=cp.nccl_unique_id()) if comm == "nccl" else {}
     b = cp.CPQR(dims, R, variant, tree=tree, world=1, comm=comm, **kw)
     for s in (a, b):
